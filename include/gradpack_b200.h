@@ -1,0 +1,144 @@
+/*
+ * gradpack_b200.h — C-ABI of the B200-native DeepReduce sparse-gradient path.
+ *
+ * Drop-in boundary for the reference's C++ compressor API (gradpack,
+ * /root/reference/proj).  Every entry point below names the reference
+ * interface it replaces.  Plain pointers and sizes only: device pointers are
+ * prefixed d_, host pointers h_; `stream` is a cudaStream_t passed as void*.
+ *
+ * Asynchrony contract: functions that take a stream only ENQUEUE work and
+ * return GP_OK when the launch succeeded.  Errors that depend on device data
+ * (checksums, payload validation) are latched in a per-context device status
+ * word; gp_ctx_status() synchronises the stream and returns the first one, in
+ * the reference's check order (container.cpp:84-127, pipeline.cpp:223-306).
+ * Host-detectable misuse (bad config, capacity) is returned immediately.
+ */
+#ifndef GRADPACK_B200_H_
+#define GRADPACK_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes, 1:1 with the exception classes of errors.hpp:21-53. */
+enum gp_status {
+  GP_OK = 0,
+  GP_ERROR = 1,              /* gradpack::Error            errors.hpp:21 */
+  GP_DECODE = 2,             /* gradpack::DecodeError      errors.hpp:26 */
+  GP_TRUNCATED = 3,          /* gradpack::TruncatedError   errors.hpp:31 */
+  GP_CHECKSUM = 4,           /* gradpack::ChecksumError    errors.hpp:36 */
+  GP_UNKNOWN_METHOD = 5,     /* gradpack::UnknownMethodError errors.hpp:41 */
+  GP_CORRUPT_PAYLOAD = 6,    /* gradpack::CorruptPayloadError errors.hpp:46 */
+  GP_FIT = 7,                /* gradpack::FitError         errors.hpp:51 */
+  GP_CUDA = 8,               /* CUDA runtime failure (no reference equivalent) */
+  GP_UNSUPPORTED = 9,        /* method id registered in FORMAT.md but not on this device path */
+  GP_CAPACITY = 10           /* device workspace / output buffer too small */
+};
+
+/* Stable wire ids (container.hpp:23-43, FORMAT.md:46-89). */
+enum gp_index_method {
+  GP_INDEX_NONE = 0, GP_INDEX_BITMAP = 1, GP_INDEX_RLE = 2, GP_INDEX_HUFFMAN = 3,
+  GP_INDEX_BLOOM_P0 = 4, GP_INDEX_BLOOM_P1 = 5, GP_INDEX_BLOOM_P2 = 6,
+  GP_INDEX_BLOOM_PD = 7, GP_INDEX_BLOOM_NAIVE = 8
+};
+enum gp_value_method {
+  GP_VALUE_NONE = 0, GP_VALUE_FIT_POLY = 1, GP_VALUE_FIT_DEXP = 2, GP_VALUE_QUANT = 3,
+  GP_VALUE_DEFLATE_SLOT = 4, GP_VALUE_RAW_F64 = 5
+};
+
+/* POD mirror of gradpack::PipelineConfig (pipeline.hpp:28-39), same defaults. */
+typedef struct gp_pipeline_config {
+  uint8_t index_method;   /* gp_index_method, default NONE */
+  uint8_t value_method;   /* gp_value_method, default NONE */
+  uint8_t pd_variant;     /* 0 leftmost, 1 middle, 2 rightmost */
+  uint8_t slot_codec;     /* 0 store, 1 deflate (default 1) */
+  int32_t degree;         /* fit polynomial degree, default 5 */
+  int32_t max_segments;   /* fit cap, 0 = knot heuristic */
+  int32_t quant_bits;     /* default 7 */
+  uint32_t quant_bucket;  /* default 512 */
+  double fpr;             /* Bloom target FPR, default 0.01 */
+  uint64_t seed;          /* pipeline seed */
+} gp_pipeline_config;
+
+void gp_pipeline_config_default(gp_pipeline_config* cfg);
+
+/* ---------------------------------------------------------------- context */
+typedef struct gp_ctx gp_ctx;
+
+/* One context per (device, stream user).  The workspace is sized once for
+ * gradients of up to max_d elements; no allocation happens inside a step. */
+int gp_ctx_create(int device, uint64_t max_d, gp_ctx** out);
+void gp_ctx_destroy(gp_ctx* ctx);
+const char* gp_last_error(const gp_ctx* ctx);
+/* Synchronise `stream`, return and clear the first latched device status. */
+int gp_ctx_status(gp_ctx* ctx, void* stream);
+/* Number of kernel launches this context has enqueued since creation. */
+uint64_t gp_ctx_launch_count(const gp_ctx* ctx);
+
+/* Upper bound of pack(compress_gradient(...)) for a gradient of d elements with
+ * r kept (container.cpp:58-82 layout).  Host-only arithmetic. */
+uint64_t gp_max_container_bytes(uint64_t d, uint64_t r, const gp_pipeline_config* cfg);
+
+/* ---------------------------------------------------------------- encode */
+/* top_r (sparsify.cpp:32-46) + compress_gradient(sg, cfg, &dense)
+ * (pipeline.cpp:146-221) + pack (container.cpp:58-82), fused.
+ * d_grad: f32[d] on device.  Writes the container to d_out (capacity cap) and
+ * its byte length to the device word *d_len.  r == 0 is invalid (Error). */
+int gp_encode_topr(gp_ctx* ctx, const float* d_grad, uint64_t d, uint64_t r,
+                   const gp_pipeline_config* cfg, uint8_t* d_out, uint64_t cap,
+                   uint64_t* d_len, void* stream);
+
+/* compress_gradient(sg, cfg, &dense) + pack for a caller-chosen support:
+ * d_support: u32[r] strictly increasing (validated, gradient.cpp:19-30),
+ * values are gathered from d_dense (pipeline.cpp:38-54). */
+int gp_encode_support(gp_ctx* ctx, const float* d_dense, uint64_t d, const uint32_t* d_support,
+                      uint64_t r, const gp_pipeline_config* cfg, uint8_t* d_out, uint64_t cap,
+                      uint64_t* d_len, void* stream);
+
+/* ---------------------------------------------------------------- decode */
+/* unpack (container.cpp:84-127) + decompress_gradient (pipeline.cpp:223-306)
+ * + to_dense accumulate: d_dense[support[i]] += scale * value[i] (f32).
+ * This is the per-peer step of the harness mean (harness.cpp:274-284). */
+int gp_decode_accumulate(gp_ctx* ctx, const uint8_t* d_container, uint64_t len,
+                         float* d_dense, uint64_t d, float scale, void* stream);
+
+/* unpack + decompress_gradient to sparse form.  Writes up to cap entries of
+ * support (u32) and values (f64) and the count to the device word *d_count.
+ * *d_dim receives the container's d. */
+int gp_decode_sparse(gp_ctx* ctx, const uint8_t* d_container, uint64_t len,
+                     uint32_t* d_support, double* d_values, uint64_t cap,
+                     uint64_t* d_count, uint64_t* d_dim, void* stream);
+
+/* ---------------------------------------------------------------- components */
+/* top_r (sparsify.cpp:32-46): ascending support of the r largest |g|, ties to
+ * the lower index; values gathered alongside (gradient.cpp:44-54). */
+int gp_top_r(gp_ctx* ctx, const float* d_grad, uint64_t d, uint64_t r, uint32_t* d_support,
+             float* d_values, void* stream);
+
+/* crc32c (container.cpp:30-48) of n device bytes into the device word *d_crc. */
+int gp_crc32c(gp_ctx* ctx, const uint8_t* d_data, uint64_t n, uint32_t* d_crc, void* stream);
+
+/* positive_scan (bloom.cpp:123-128) of a serialized filter (bloom.cpp:84-94,
+ * FORMAT.md:58-75) over [0, d): ascending positives, count to *d_count. */
+int gp_bloom_positive_scan(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter_len,
+                           uint64_t d, uint32_t* d_positives, uint64_t cap, uint64_t* d_count,
+                           void* stream);
+
+/* p1_select / p2_select (bloom.cpp:140-154, :175-222) over the positives of a
+ * serialized filter, with the selection stream seeded as
+ * derive_selection_seed(seed_a, seed_b) (pipeline.cpp:23-25, :205, :286).
+ * index_method selects P1 (5) or P2 (6).  Output: r ascending keys. */
+int gp_bloom_select(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter_len, uint64_t d,
+                    uint64_t r, int index_method, uint32_t* d_selected, void* stream);
+
+/* bloom_params (bloom.cpp:22-31).  Host arithmetic, returns GP_ERROR on bad args. */
+int gp_bloom_params(double epsilon, uint64_t r, uint64_t* m, uint32_t* k);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif  /* GRADPACK_B200_H_ */
