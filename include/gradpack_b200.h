@@ -19,6 +19,12 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#if defined(__GNUC__)
+#define GP_API __attribute__((visibility("default")))
+#else
+#define GP_API
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -63,38 +69,38 @@ typedef struct gp_pipeline_config {
   uint64_t seed;          /* pipeline seed */
 } gp_pipeline_config;
 
-void gp_pipeline_config_default(gp_pipeline_config* cfg);
+GP_API void gp_pipeline_config_default(gp_pipeline_config* cfg);
 
 /* ---------------------------------------------------------------- context */
 typedef struct gp_ctx gp_ctx;
 
 /* One context per (device, stream user).  The workspace is sized once for
  * gradients of up to max_d elements; no allocation happens inside a step. */
-int gp_ctx_create(int device, uint64_t max_d, gp_ctx** out);
-void gp_ctx_destroy(gp_ctx* ctx);
-const char* gp_last_error(const gp_ctx* ctx);
+GP_API int gp_ctx_create(int device, uint64_t max_d, gp_ctx** out);
+GP_API void gp_ctx_destroy(gp_ctx* ctx);
+GP_API const char* gp_last_error(const gp_ctx* ctx);
 /* Synchronise `stream`, return and clear the first latched device status. */
-int gp_ctx_status(gp_ctx* ctx, void* stream);
+GP_API int gp_ctx_status(gp_ctx* ctx, void* stream);
 /* Number of kernel launches this context has enqueued since creation. */
-uint64_t gp_ctx_launch_count(const gp_ctx* ctx);
+GP_API uint64_t gp_ctx_launch_count(const gp_ctx* ctx);
 
 /* Upper bound of pack(compress_gradient(...)) for a gradient of d elements with
  * r kept (container.cpp:58-82 layout).  Host-only arithmetic. */
-uint64_t gp_max_container_bytes(uint64_t d, uint64_t r, const gp_pipeline_config* cfg);
+GP_API uint64_t gp_max_container_bytes(uint64_t d, uint64_t r, const gp_pipeline_config* cfg);
 
 /* ---------------------------------------------------------------- encode */
 /* top_r (sparsify.cpp:32-46) + compress_gradient(sg, cfg, &dense)
  * (pipeline.cpp:146-221) + pack (container.cpp:58-82), fused.
  * d_grad: f32[d] on device.  Writes the container to d_out (capacity cap) and
  * its byte length to the device word *d_len.  r == 0 is invalid (Error). */
-int gp_encode_topr(gp_ctx* ctx, const float* d_grad, uint64_t d, uint64_t r,
+GP_API int gp_encode_topr(gp_ctx* ctx, const float* d_grad, uint64_t d, uint64_t r,
                    const gp_pipeline_config* cfg, uint8_t* d_out, uint64_t cap,
                    uint64_t* d_len, void* stream);
 
 /* compress_gradient(sg, cfg, &dense) + pack for a caller-chosen support:
  * d_support: u32[r] strictly increasing (validated, gradient.cpp:19-30),
  * values are gathered from d_dense (pipeline.cpp:38-54). */
-int gp_encode_support(gp_ctx* ctx, const float* d_dense, uint64_t d, const uint32_t* d_support,
+GP_API int gp_encode_support(gp_ctx* ctx, const float* d_dense, uint64_t d, const uint32_t* d_support,
                       uint64_t r, const gp_pipeline_config* cfg, uint8_t* d_out, uint64_t cap,
                       uint64_t* d_len, void* stream);
 
@@ -102,28 +108,37 @@ int gp_encode_support(gp_ctx* ctx, const float* d_dense, uint64_t d, const uint3
 /* unpack (container.cpp:84-127) + decompress_gradient (pipeline.cpp:223-306)
  * + to_dense accumulate: d_dense[support[i]] += scale * value[i] (f32).
  * This is the per-peer step of the harness mean (harness.cpp:274-284). */
-int gp_decode_accumulate(gp_ctx* ctx, const uint8_t* d_container, uint64_t len,
+GP_API int gp_decode_accumulate(gp_ctx* ctx, const uint8_t* d_container, uint64_t len,
                          float* d_dense, uint64_t d, float scale, void* stream);
+
+/* As gp_decode_accumulate, but dispatches the device pipeline for the
+ * methods in `hint` without peeking the header on the host (no host sync).
+ * The device verifies the container's method ids against the hint after the
+ * CRC check; a mismatch latches GP_UNSUPPORTED and leaves d_dense untouched,
+ * and the caller may retry without a hint. */
+GP_API int gp_decode_accumulate_hint(gp_ctx* ctx, const uint8_t* d_container, uint64_t len,
+                              const gp_pipeline_config* hint, float* d_dense, uint64_t d,
+                              float scale, void* stream);
 
 /* unpack + decompress_gradient to sparse form.  Writes up to cap entries of
  * support (u32) and values (f64) and the count to the device word *d_count.
  * *d_dim receives the container's d. */
-int gp_decode_sparse(gp_ctx* ctx, const uint8_t* d_container, uint64_t len,
+GP_API int gp_decode_sparse(gp_ctx* ctx, const uint8_t* d_container, uint64_t len,
                      uint32_t* d_support, double* d_values, uint64_t cap,
                      uint64_t* d_count, uint64_t* d_dim, void* stream);
 
 /* ---------------------------------------------------------------- components */
 /* top_r (sparsify.cpp:32-46): ascending support of the r largest |g|, ties to
  * the lower index; values gathered alongside (gradient.cpp:44-54). */
-int gp_top_r(gp_ctx* ctx, const float* d_grad, uint64_t d, uint64_t r, uint32_t* d_support,
+GP_API int gp_top_r(gp_ctx* ctx, const float* d_grad, uint64_t d, uint64_t r, uint32_t* d_support,
              float* d_values, void* stream);
 
 /* crc32c (container.cpp:30-48) of n device bytes into the device word *d_crc. */
-int gp_crc32c(gp_ctx* ctx, const uint8_t* d_data, uint64_t n, uint32_t* d_crc, void* stream);
+GP_API int gp_crc32c(gp_ctx* ctx, const uint8_t* d_data, uint64_t n, uint32_t* d_crc, void* stream);
 
 /* positive_scan (bloom.cpp:123-128) of a serialized filter (bloom.cpp:84-94,
  * FORMAT.md:58-75) over [0, d): ascending positives, count to *d_count. */
-int gp_bloom_positive_scan(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter_len,
+GP_API int gp_bloom_positive_scan(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter_len,
                            uint64_t d, uint32_t* d_positives, uint64_t cap, uint64_t* d_count,
                            void* stream);
 
@@ -131,11 +146,11 @@ int gp_bloom_positive_scan(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter
  * serialized filter, with the selection stream seeded as
  * derive_selection_seed(seed_a, seed_b) (pipeline.cpp:23-25, :205, :286).
  * index_method selects P1 (5) or P2 (6).  Output: r ascending keys. */
-int gp_bloom_select(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter_len, uint64_t d,
+GP_API int gp_bloom_select(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter_len, uint64_t d,
                     uint64_t r, int index_method, uint32_t* d_selected, void* stream);
 
 /* bloom_params (bloom.cpp:22-31).  Host arithmetic, returns GP_ERROR on bad args. */
-int gp_bloom_params(double epsilon, uint64_t r, uint64_t* m, uint32_t* k);
+GP_API int gp_bloom_params(double epsilon, uint64_t r, uint64_t* m, uint32_t* k);
 
 #ifdef __cplusplus
 }  /* extern "C" */

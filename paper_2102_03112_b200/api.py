@@ -1,0 +1,262 @@
+"""Host-side mirror of gradpack's compressor API over the B200 C-ABI.
+
+Names, argument meaning and error behaviour follow the reference
+(/root/reference/proj/include/gradpack/*.hpp):
+
+  reference                                   here
+  ------------------------------------------  -----------------------------------------
+  IndexMethod / ValueMethod (container.hpp:23) IndexMethod / ValueMethod (same ids)
+  PipelineConfig (pipeline.hpp:28-39)          PipelineConfig (same fields, defaults)
+  top_r (sparsify.hpp:22)                      Codec.top_r
+  compress_gradient + pack (pipeline.hpp:53,   Codec.compress / Codec.compress_support
+    container.hpp:65)                            (device tensor in, packed bytes on device out)
+  unpack + decompress_gradient (:59, :66)      Codec.decompress
+  to_dense + harness mean (harness.cpp:274)    Codec.decode_accumulate
+  Error / DecodeError / ... (errors.hpp:21-53)  the same exception classes
+
+Device memory and streams come from torch; torch is plumbing here, every
+byte of the path is computed by libgradpack_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+
+import torch
+
+from ._lib import GpConfig, lib
+
+
+# ---------------------------------------------------------------- errors (errors.hpp:21-53)
+class Error(RuntimeError):
+    """gradpack::Error — base class of every error raised by this library."""
+
+
+class DecodeError(Error):
+    """A byte stream failed structural validation while decoding."""
+
+
+class TruncatedError(DecodeError):
+    """The stream ended before a complete structure could be read."""
+
+
+class ChecksumError(DecodeError):
+    """A stored checksum does not match the recomputed one."""
+
+
+class UnknownMethodError(DecodeError):
+    """A method or codec id is not in the registry."""
+
+
+class CorruptPayloadError(DecodeError):
+    """A payload parsed structurally but violates its own invariants."""
+
+
+class FitError(Error):
+    """An iterative fit failed to converge to a usable model."""
+
+
+class CudaError(Error):
+    """The CUDA runtime failed (no reference equivalent)."""
+
+
+class UnsupportedMethodError(Error):
+    """Method id registered in FORMAT.md but not implemented on the device path."""
+
+
+class CapacityError(Error):
+    """The context workspace or an output buffer is too small."""
+
+
+_STATUS = {1: Error, 2: DecodeError, 3: TruncatedError, 4: ChecksumError, 5: UnknownMethodError,
+           6: CorruptPayloadError, 7: FitError, 8: CudaError, 9: UnsupportedMethodError, 10: CapacityError}
+
+
+# ---------------------------------------------------------------- method ids (container.hpp:23-43)
+class IndexMethod(enum.IntEnum):
+    None_ = 0
+    Bitmap = 1
+    Rle = 2
+    Huffman = 3
+    BloomP0 = 4
+    BloomP1 = 5
+    BloomP2 = 6
+    BloomPd = 7
+    BloomNaive = 8
+
+
+class ValueMethod(enum.IntEnum):
+    None_ = 0
+    FitPoly = 1
+    FitDexp = 2
+    Quant = 3
+    DeflateSlot = 4
+    RawF64 = 5
+
+
+@dataclass
+class PipelineConfig:
+    """gradpack::PipelineConfig (pipeline.hpp:28-39) with the same defaults."""
+
+    index_method: IndexMethod = IndexMethod.None_
+    value_method: ValueMethod = ValueMethod.None_
+    fpr: float = 0.01
+    pd_variant: int = 0
+    degree: int = 5
+    max_segments: int = 0
+    quant_bits: int = 7
+    quant_bucket: int = 512
+    slot_codec: int = 1
+    seed: int = 0
+
+    def to_c(self) -> GpConfig:
+        return GpConfig(int(self.index_method), int(self.value_method), int(self.pd_variant),
+                        int(self.slot_codec), int(self.degree), int(self.max_segments),
+                        int(self.quant_bits), int(self.quant_bucket), float(self.fpr),
+                        int(self.seed) & 0xFFFFFFFFFFFFFFFF)
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+@dataclass
+class Codec:
+    """One device context (gp_ctx): a preallocated workspace for gradients of up
+    to ``max_d`` elements on ``device``.  All calls enqueue on the current torch
+    stream; ``status()`` synchronises and raises the first latched device error."""
+
+    max_d: int
+    device: int = 0
+    _ctx: C.c_void_p = field(default=None, repr=False)
+
+    def __post_init__(self):
+        if not torch.cuda.is_available():
+            raise CudaError("no CUDA device: the B200 path has no CPU fallback")
+        torch.cuda.set_device(self.device)
+        h = C.c_void_p()
+        rc = lib.gp_ctx_create(self.device, self.max_d, C.byref(h))
+        if rc != 0:
+            raise _STATUS.get(rc, Error)(f"gp_ctx_create failed with status {rc}")
+        self._ctx = h
+        # 8-byte device scratch for container lengths / counts
+        self._len = torch.zeros(4, dtype=torch.int64, device=f"cuda:{self.device}")
+
+    def close(self):
+        if self._ctx:
+            lib.gp_ctx_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -------------------------------------------------------------- status
+    def _raise(self, rc: int):
+        if rc != 0:
+            msg = lib.gp_last_error(self._ctx)
+            raise _STATUS.get(rc, Error)(msg.decode(errors="replace") if msg else f"status {rc}")
+
+    def status(self, stream=None):
+        """Synchronise and raise the first device-side error, if any."""
+        self._raise(lib.gp_ctx_status(self._ctx, _stream(stream)))
+
+    @property
+    def launches(self) -> int:
+        return int(lib.gp_ctx_launch_count(self._ctx))
+
+    # -------------------------------------------------------------- encode
+    @staticmethod
+    def max_container_bytes(d: int, r: int, cfg: PipelineConfig) -> int:
+        c = cfg.to_c()
+        return int(lib.gp_max_container_bytes(d, r, C.byref(c)))
+
+    def encode_into(self, grad: torch.Tensor, r: int, cfg: PipelineConfig, out: torch.Tensor,
+                    length: torch.Tensor, support: torch.Tensor | None = None, stream=None):
+        """Asynchronous top_r + compress_gradient + pack of ``grad`` (f32, device)
+        into ``out`` (u8, device); the byte length lands in ``length`` (int64, device).
+        With ``support`` given, that support replaces top_r (compress_gradient(sg, cfg, &dense))."""
+        assert grad.dtype == torch.float32 and grad.is_cuda and grad.is_contiguous()
+        assert out.dtype == torch.uint8 and out.is_cuda
+        c = cfg.to_c()
+        if support is None:
+            rc = lib.gp_encode_topr(self._ctx, _ptr(grad), grad.numel(), r, C.byref(c), _ptr(out),
+                                    out.numel(), _ptr(length), _stream(stream))
+        else:
+            assert support.dtype == torch.int32 and support.is_cuda
+            rc = lib.gp_encode_support(self._ctx, _ptr(grad), grad.numel(), _ptr(support),
+                                       support.numel(), C.byref(c), _ptr(out), out.numel(),
+                                       _ptr(length), _stream(stream))
+        self._raise(rc)
+
+    def compress(self, grad: torch.Tensor, r: int, cfg: PipelineConfig,
+                 support: torch.Tensor | None = None) -> torch.Tensor:
+        """top_r + compress_gradient + pack; returns the packed container (device u8)."""
+        d = grad.numel()
+        rr = r if support is None else support.numel()
+        out = torch.empty(self.max_container_bytes(d, rr, cfg), dtype=torch.uint8, device=grad.device)
+        self.encode_into(grad, r, cfg, out, self._len[0:1], support=support)
+        self.status()
+        return out[: int(self._len[0].item())]
+
+    # -------------------------------------------------------------- decode
+    def decode_accumulate(self, container: torch.Tensor, dense: torch.Tensor, scale: float = 1.0,
+                          length: int | None = None, hint: PipelineConfig | None = None, stream=None):
+        """Asynchronous unpack + decompress_gradient + dense[support] += scale * values."""
+        assert dense.dtype == torch.float32 and dense.is_cuda and dense.is_contiguous()
+        n = container.numel() if length is None else length
+        if hint is None:
+            rc = lib.gp_decode_accumulate(self._ctx, _ptr(container), n, _ptr(dense), dense.numel(),
+                                          float(scale), _stream(stream))
+        else:
+            c = hint.to_c()
+            rc = lib.gp_decode_accumulate_hint(self._ctx, _ptr(container), n, C.byref(c), _ptr(dense),
+                                               dense.numel(), float(scale), _stream(stream))
+        self._raise(rc)
+
+    def decompress(self, container: torch.Tensor, length: int | None = None):
+        """unpack + decompress_gradient → (d, support int32 tensor, values float64 tensor)."""
+        n = container.numel() if length is None else length
+        cap = self.max_d
+        dev = container.device
+        sup = torch.empty(cap, dtype=torch.int32, device=dev)
+        val = torch.empty(cap, dtype=torch.float64, device=dev)
+        meta = torch.zeros(2, dtype=torch.int64, device=dev)
+        rc = lib.gp_decode_sparse(self._ctx, _ptr(container), n, _ptr(sup), _ptr(val), cap,
+                                  C.c_void_p(meta.data_ptr()), C.c_void_p(meta.data_ptr() + 8), _stream())
+        self._raise(rc)
+        self.status()
+        cnt, d = (int(x) for x in meta.tolist())
+        return d, sup[:cnt], val[:cnt]
+
+    # -------------------------------------------------------------- components
+    def top_r(self, grad: torch.Tensor, r: int):
+        """top_r (sparsify.cpp:32-46) → (support int32, values f32), ascending support."""
+        sup = torch.empty(r, dtype=torch.int32, device=grad.device)
+        val = torch.empty(r, dtype=torch.float32, device=grad.device)
+        self._raise(lib.gp_top_r(self._ctx, _ptr(grad), grad.numel(), r, _ptr(sup), _ptr(val), _stream()))
+        self.status()
+        return sup, val
+
+    def crc32c(self, data: torch.Tensor) -> int:
+        out = torch.zeros(1, dtype=torch.int64, device=data.device)
+        self._raise(lib.gp_crc32c(self._ctx, _ptr(data), data.numel(), _ptr(out), _stream()))
+        self.status()
+        return int(out.item()) & 0xFFFFFFFF
+
+
+def bloom_params(epsilon: float, r: int) -> tuple[int, int]:
+    """bloom_params (bloom.cpp:22-31) → (m, k)."""
+    m, k = C.c_uint64(), C.c_uint32()
+    rc = lib.gp_bloom_params(float(epsilon), int(r), C.byref(m), C.byref(k))
+    if rc != 0:
+        raise Error("bloom_params: epsilon must be in (0, 1) and r >= 1")
+    return m.value, k.value

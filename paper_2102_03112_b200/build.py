@@ -1,0 +1,54 @@
+"""Builds the in-tree CUDA library libgradpack_b200.so for sm_100a.
+
+    python -m paper_2102_03112_b200.build        (or __graft_entry__.build())
+
+One nvcc invocation per translation unit, then a shared link.  The library
+exports only the C-ABI of include/gradpack_b200.h.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "libgradpack_b200.so")
+OBJ = os.path.join(HERE, "build_obj")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "--expt-relaxed-constexpr",
+         "-Xptxas", "-warn-spills"]
+SOURCES = ["capi.cu", "topr.cu", "container.cu", "indexcodec.cu", "values.cu"]
+
+
+def _run(cmd):
+    r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout)
+        raise RuntimeError(f"command failed: {' '.join(cmd)}")
+    return r.stdout
+
+
+def build(verbose: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    objs = []
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp"))]
+    deps.append(os.path.join(HERE, "..", "include", "gradpack_b200.h"))
+    newest_dep = max(os.path.getmtime(p) for p in deps)
+    for src in SOURCES:
+        path = os.path.join(CSRC, src)
+        obj = os.path.join(OBJ, src.replace(".cu", ".o"))
+        if (not os.path.exists(obj) or os.path.getmtime(obj) < os.path.getmtime(path)
+                or os.path.getmtime(obj) < newest_dep):
+            out = _run([NVCC, *ARCH, *FLAGS, "-c", path, "-o", obj])
+            if verbose and out.strip():
+                print(out)
+        objs.append(obj)
+    if not os.path.exists(OUT) or any(os.path.getmtime(o) > os.path.getmtime(OUT) for o in objs):
+        _run([NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-Xlinker", "--exclude-libs,ALL"])
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(verbose=True))

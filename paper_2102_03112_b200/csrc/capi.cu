@@ -1,0 +1,416 @@
+// capi.cu — the C-ABI (include/gradpack_b200.h): context, workspace, and the
+// host orchestration of encode (top_r → compress_gradient → pack) and decode
+// (unpack → decompress_gradient → to_dense accumulate).
+//
+// The host side only enqueues.  Method dispatch is decided on the host from
+// the config (encode) or from the container header (decode: either a caller
+// hint that the device verifies after the CRC, or a synchronous 75-byte
+// header peek when no hint is given).  No CPU fallback exists: if the CUDA
+// device or this library is unavailable, every entry point fails.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "gp_ctx.hpp"
+#include "gp_device.cuh"
+
+namespace gp {
+
+int set_error(gp_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->last_error = msg;
+  return code;
+}
+
+int check_launch(gp_ctx* ctx, const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(ctx, GP_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return GP_OK;
+}
+
+void reset_scan(gp_ctx* ctx, cudaStream_t s, uint64_t ntiles_bound) {
+  Workspace& w = ctx->ws;
+  const uint64_t n = ntiles_bound < w.tiles_cap ? ntiles_bound : w.tiles_cap;
+  cudaMemsetAsync(w.scan_base, 0, 128 + n * 8, s);
+}
+
+namespace {
+
+bool is_bloom(int m) { return m >= GP_INDEX_BLOOM_P0 && m <= GP_INDEX_BLOOM_NAIVE; }
+
+// Methods with a device implementation on this path (the rest of FORMAT.md's
+// registry returns GP_UNSUPPORTED).
+bool index_supported(int m) { return m == GP_INDEX_NONE || m == GP_INDEX_BITMAP; }
+bool value_supported(int m) { return m == GP_VALUE_NONE || m == GP_VALUE_RAW_F64; }
+
+struct PlanInit {
+  uint64_t d, r, il, n_values;
+  uint8_t index_method, value_method, pd_variant;
+};
+
+__global__ void init_plan(Plan* plan, PlanInit p) {
+  plan->d = p.d;
+  plan->r = p.r;
+  plan->index_method = p.index_method;
+  plan->value_method = p.value_method;
+  plan->pd_variant = p.pd_variant;
+  plan->flags = 0;
+  plan->il = p.il;
+  plan->vl = 0;
+  plan->rl = 0;
+  plan->n_values = p.n_values;
+  plan->n_sel = p.r;
+  plan->off_index = 49;
+  plan->off_value = 49 + p.il;
+  plan->off_reorder = 49 + p.il;
+}
+
+// compress_gradient's validate(sg) (gradient.cpp:19-30) + gather(dense, support)
+__global__ void take_support(const float* __restrict__ dense, const uint32_t* __restrict__ support, uint64_t r,
+                             uint64_t d, uint32_t* ws_support, float* ws_values, uint32_t* status) {
+  if (failed(status)) return;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < r;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t s = support[i];
+    if (static_cast<uint64_t>(s) >= d || (i > 0 && s <= support[i - 1])) {
+      latch(status, GP_ERROR);
+      return;
+    }
+    ws_support[i] = s;
+    ws_values[i] = dense[s];
+  }
+}
+
+uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------- workspace
+struct Carver {
+  uint8_t* base;
+  size_t off;
+  template <typename T>
+  T* take(uint64_t n) {
+    off = (off + 255) & ~static_cast<size_t>(255);
+    T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+void carve(Workspace& w, uint8_t* base, uint64_t D) {
+  Carver c{base, 0};
+  w.plan = c.take<Plan>(1);
+  w.status = c.take<uint32_t>(64);
+  w.tiles_cap = 4 * (D / 1024) + 4096;
+  w.scan_base = c.take<uint8_t>(128 + w.tiles_cap * 8);
+  w.ticket = reinterpret_cast<uint32_t*>(w.scan_base);
+  w.tiles = reinterpret_cast<uint64_t*>(w.scan_base ? w.scan_base + 128 : nullptr);
+  w.hist = c.take<uint32_t>(65536);
+  w.cand_idx = c.take<uint32_t>(D);
+  w.cand_val = c.take<float>(D);
+  w.support = c.take<uint32_t>(D);
+  w.values = c.take<float>(D);
+  w.m_cap = 48 * D + 4096;
+  w.filter = c.take<uint32_t>(w.m_cap / 32 + 1);
+  w.pos = c.take<uint32_t>(D);
+  w.sel = c.take<uint32_t>(D);
+  w.flags = c.take<uint8_t>(D);
+  w.u32a = c.take<uint32_t>(D);
+  w.u32b = c.take<uint32_t>(D);
+  w.u32c = c.take<uint32_t>(D);
+  w.u32d = c.take<uint32_t>(D);
+  w.f64a = c.take<double>(D);
+  w.f64b = c.take<double>(D);
+  w.partial = c.take<double>(4096 * 32);
+  w.crc_cap = (64 * D + (1 << 20)) / (256 * 1024) + 64;
+  w.crc_part = c.take<uint32_t>(w.crc_cap);
+  w.scratch = c.take<uint8_t>(2 * D);
+  w.bytes_total = c.off;
+}
+
+}  // namespace
+}  // namespace gp
+
+using namespace gp;
+
+extern "C" {
+
+void gp_pipeline_config_default(gp_pipeline_config* cfg) {
+  if (!cfg) return;
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->index_method = GP_INDEX_NONE;
+  cfg->value_method = GP_VALUE_NONE;
+  cfg->pd_variant = 0;
+  cfg->slot_codec = 1;
+  cfg->degree = 5;
+  cfg->max_segments = 0;
+  cfg->quant_bits = 7;
+  cfg->quant_bucket = 512;
+  cfg->fpr = 0.01;
+  cfg->seed = 0;
+}
+
+int gp_ctx_create(int device, uint64_t max_d, gp_ctx** out) {
+  if (!out) return GP_ERROR;
+  *out = nullptr;
+  if (max_d < 1 || max_d > 0xFFFFFFFFULL) return GP_ERROR;
+  auto* ctx = new (std::nothrow) gp_ctx();
+  if (!ctx) return GP_ERROR;
+  ctx->device = device;
+  ctx->max_d = max_d;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return GP_CUDA;
+  }
+  const uint64_t D = max_d < 4096 ? 4096 : max_d;
+  carve(ctx->ws, nullptr, D);
+  const size_t bytes = ctx->ws.bytes_total;
+  void* base = nullptr;
+  e = cudaMalloc(&base, bytes);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return GP_CUDA;
+  }
+  carve(ctx->ws, static_cast<uint8_t*>(base), D);
+  ctx->ws.base = base;
+  ctx->ws.bytes = bytes;
+  e = cudaMemset(ctx->ws.status, 0, 64 * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(ctx->ws.plan, 0, sizeof(Plan));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    cudaFree(base);
+    delete ctx;
+    return GP_CUDA;
+  }
+  *out = ctx;
+  return GP_OK;
+}
+
+void gp_ctx_destroy(gp_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->ws.base) cudaFree(ctx->ws.base);
+  delete ctx;
+}
+
+const char* gp_last_error(const gp_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "null context"; }
+
+uint64_t gp_ctx_launch_count(const gp_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int gp_ctx_status(gp_ctx* ctx, void* stream) {
+  if (!ctx) return GP_ERROR;
+  auto s = static_cast<cudaStream_t>(stream);
+  uint32_t st = 0;
+  cudaError_t e = cudaMemcpyAsync(&st, ctx->ws.status, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return set_error(ctx, GP_CUDA, std::string("status: ") + cudaGetErrorString(e));
+  if (st != 0) {
+    cudaMemsetAsync(ctx->ws.status, 0, sizeof(uint32_t), s);
+    cudaStreamSynchronize(s);
+    static const char* names[] = {"ok", "Error", "DecodeError", "TruncatedError", "ChecksumError",
+                                  "UnknownMethodError", "CorruptPayloadError", "FitError", "CUDA",
+                                  "unsupported method on the device path", "device capacity exceeded"};
+    return set_error(ctx, static_cast<int>(st),
+                     std::string("device: ") + (st < 11 ? names[st] : "unknown status"));
+  }
+  return GP_OK;
+}
+
+int gp_bloom_params(double epsilon, uint64_t r, uint64_t* m, uint32_t* k) {
+  // bloom.cpp:22-31; evaluated on the host exactly as the reference does
+  if (!(epsilon > 0.0 && epsilon < 1.0) || r < 1) return GP_ERROR;
+  const double ln2 = 0.693147180559945309417232121458176568;
+  const double lninv = std::log(1.0 / epsilon);
+  if (m) *m = static_cast<uint64_t>(std::ceil(static_cast<double>(r) * lninv / (ln2 * ln2)));
+  if (k) *k = static_cast<uint32_t>(std::ceil(lninv / ln2));
+  return GP_OK;
+}
+
+uint64_t gp_max_container_bytes(uint64_t d, uint64_t r, const gp_pipeline_config* cfg) {
+  if (!cfg) return 0;
+  uint64_t il = 0, n = r;
+  switch (cfg->index_method) {
+    case GP_INDEX_NONE: il = 4 * r; break;
+    case GP_INDEX_BITMAP: il = (d + 7) / 8; break;
+    case GP_INDEX_RLE: il = (d + 7) / 8 * 11 / 8 + 16; break;  // <= 1 + 8 * (runs * <=10 groups)
+    default: {
+      uint64_t m = 0;
+      uint32_t k = 0;
+      gp_bloom_params(cfg->fpr, r < 1 ? 1 : r, &m, &k);
+      il = 26 + (m + 7) / 8 + 1;
+      if (cfg->index_method == GP_INDEX_BLOOM_P0) n = d;
+    }
+  }
+  uint64_t vl = 0, rl = 0;
+  switch (cfg->value_method) {
+    case GP_VALUE_RAW_F64: vl = 8 * n; break;
+    case GP_VALUE_FIT_POLY:
+    case GP_VALUE_FIT_DEXP: {
+      const uint64_t segs = kMaxSeg;
+      vl = 1 + 2 + 4 * segs + 1 + 4 * segs * (static_cast<uint64_t>(cfg->degree) + 1) + 4;
+      uint64_t w = 0;
+      for (uint64_t x = d - 1; x; x >>= 1) ++w;
+      rl = (n * w + 7) / 8;
+      break;
+    }
+    default: vl = 4 * n; break;
+  }
+  return 49 + il + vl + rl + 4;
+}
+
+static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const uint32_t* d_support, uint64_t r,
+                         const gp_pipeline_config* cfg, uint8_t* d_out, uint64_t cap, uint64_t* d_len,
+                         void* stream) {
+  if (!ctx || !cfg || !d_dense || !d_out) return set_error(ctx, GP_ERROR, "encode: null argument");
+  auto s = static_cast<cudaStream_t>(stream);
+  if (d < 1) return set_error(ctx, GP_ERROR, "sparsifier: dim must be >= 1");
+  if (d > 0xFFFFFFFFULL) return set_error(ctx, GP_ERROR, "sparsifier: dim exceeds 32-bit index space");
+  if (r < 1 || r > d) return set_error(ctx, GP_ERROR, "sparsifier: r out of range [1, d]");
+  if (d > ctx->max_d) return set_error(ctx, GP_CAPACITY, "encode: d exceeds the context's max_d");
+  const int im = cfg->index_method, vm = cfg->value_method;
+  if (im > GP_INDEX_BLOOM_NAIVE || vm > GP_VALUE_RAW_F64)
+    return set_error(ctx, GP_ERROR, "container: unregistered method");
+  if (!index_supported(im) || !value_supported(vm))
+    return set_error(ctx, GP_UNSUPPORTED, "method not implemented on the device path");
+  const uint64_t bound = gp_max_container_bytes(d, r, cfg);
+  if (cap < bound) return set_error(ctx, GP_CAPACITY, "encode: output capacity below gp_max_container_bytes");
+
+  PlanInit pi{};
+  pi.d = d;
+  pi.r = r;
+  pi.index_method = static_cast<uint8_t>(im);
+  pi.value_method = static_cast<uint8_t>(vm);
+  pi.pd_variant = cfg->pd_variant;
+  pi.n_values = r;
+  pi.il = im == GP_INDEX_NONE ? 4 * r : im == GP_INDEX_BITMAP ? (d + 7) / 8 : 0;
+  GP_LAUNCH(ctx, init_plan, 1, 1, 0, s, ctx->ws.plan, pi);
+
+  if (d_support) {
+    GP_LAUNCH(ctx, take_support, grid_for(ctx, r, 256), 256, 0, s, d_dense, d_support, r, d, ctx->ws.support,
+              ctx->ws.values, ctx->ws.status);
+  } else {
+    launch_top_r(ctx, d_dense, d, r, s);
+  }
+  switch (im) {
+    case GP_INDEX_NONE: launch_index_none(ctx, d_out, r, s); break;
+    case GP_INDEX_BITMAP: launch_index_bitmap(ctx, d_out, d, r, s); break;
+    default: break;
+  }
+  switch (vm) {
+    case GP_VALUE_NONE:
+    case GP_VALUE_RAW_F64: launch_values_raw(ctx, d_out, vm == GP_VALUE_RAW_F64, r, s); break;
+    default: break;
+  }
+  launch_finish_container(ctx, d_out, cap, d_len, bound, s);
+  return check_launch(ctx, "encode");
+}
+
+int gp_encode_topr(gp_ctx* ctx, const float* d_grad, uint64_t d, uint64_t r, const gp_pipeline_config* cfg,
+                   uint8_t* d_out, uint64_t cap, uint64_t* d_len, void* stream) {
+  return encode_common(ctx, d_grad, d, nullptr, r, cfg, d_out, cap, d_len, stream);
+}
+
+int gp_encode_support(gp_ctx* ctx, const float* d_dense, uint64_t d, const uint32_t* d_support, uint64_t r,
+                      const gp_pipeline_config* cfg, uint8_t* d_out, uint64_t cap, uint64_t* d_len,
+                      void* stream) {
+  if (!d_support) return set_error(ctx, GP_ERROR, "encode_support: null support");
+  return encode_common(ctx, d_dense, d, d_support, r, cfg, d_out, cap, d_len, stream);
+}
+
+static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const gp_pipeline_config* hint,
+                         float* d_dense, uint64_t dense_d, float scale, uint32_t* d_support, double* d_values,
+                         uint64_t cap, uint64_t* d_count, uint64_t* d_dim, void* stream) {
+  if (!ctx || !d_in) return set_error(ctx, GP_ERROR, "decode: null argument");
+  auto s = static_cast<cudaStream_t>(stream);
+  gp_pipeline_config h{};
+  if (hint) {
+    h = *hint;
+  } else {
+    // synchronous header peek: method ids drive the host-side dispatch
+    uint8_t hdr[8] = {0};
+    const uint64_t n = len < 8 ? len : 8;
+    if (n) {
+      cudaError_t e = cudaMemcpyAsync(hdr, d_in, n, cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) return set_error(ctx, GP_CUDA, std::string("decode peek: ") + cudaGetErrorString(e));
+    }
+    h.index_method = hdr[6];
+    h.value_method = hdr[7];
+  }
+  // parse + CRC verdict always run first: the reference reports header and
+  // checksum errors before it looks at the method ids
+  launch_parse_container(ctx, d_in, len, hint ? &h : nullptr, s);
+  const int im = h.index_method, vm = h.value_method;
+  const bool known = im <= GP_INDEX_BLOOM_NAIVE && vm <= GP_VALUE_RAW_F64;
+  if (known && (!index_supported(im) || !value_supported(vm))) {
+    // surface header/CRC errors first, then report the unsupported method
+    const int st = gp_ctx_status(ctx, stream);
+    if (st != GP_OK) return st;
+    return set_error(ctx, GP_UNSUPPORTED, "method not implemented on the device path");
+  }
+  if (!known) return check_launch(ctx, "decode");  // verify_container latches UnknownMethod
+  const uint64_t bound = ctx->max_d;
+  switch (im) {
+    case GP_INDEX_NONE: launch_decode_index_none(ctx, d_in, bound, s); break;
+    case GP_INDEX_BITMAP: launch_decode_index_bitmap(ctx, d_in, bound, s); break;
+    default: break;
+  }
+  switch (vm) {
+    case GP_VALUE_NONE:
+    case GP_VALUE_RAW_F64: launch_values_raw_check(ctx, s); break;
+    default: break;
+  }
+  if (im == GP_INDEX_NONE) launch_validate_support(ctx, bound, s);
+  (void)dense_d;
+  launch_decode_scatter(ctx, d_in, bound, d_dense, scale, d_support, d_values, cap, d_count, d_dim, s);
+  return check_launch(ctx, "decode");
+}
+
+int gp_decode_accumulate(gp_ctx* ctx, const uint8_t* d_container, uint64_t len, float* d_dense, uint64_t d,
+                         float scale, void* stream) {
+  return decode_common(ctx, d_container, len, nullptr, d_dense, d, scale, nullptr, nullptr, 0, nullptr, nullptr,
+                       stream);
+}
+
+int gp_decode_accumulate_hint(gp_ctx* ctx, const uint8_t* d_container, uint64_t len, const gp_pipeline_config* hint,
+                              float* d_dense, uint64_t d, float scale, void* stream) {
+  return decode_common(ctx, d_container, len, hint, d_dense, d, scale, nullptr, nullptr, 0, nullptr, nullptr,
+                       stream);
+}
+
+int gp_decode_sparse(gp_ctx* ctx, const uint8_t* d_container, uint64_t len, uint32_t* d_support, double* d_values,
+                     uint64_t cap, uint64_t* d_count, uint64_t* d_dim, void* stream) {
+  if (!d_support || !d_values) return set_error(ctx, GP_ERROR, "decode_sparse: null output");
+  return decode_common(ctx, d_container, len, nullptr, nullptr, 0, 0.0f, d_support, d_values, cap, d_count, d_dim,
+                       stream);
+}
+
+int gp_top_r(gp_ctx* ctx, const float* d_grad, uint64_t d, uint64_t r, uint32_t* d_support, float* d_values,
+             void* stream) {
+  if (!ctx || !d_grad || !d_support) return set_error(ctx, GP_ERROR, "top_r: null argument");
+  if (d < 1) return set_error(ctx, GP_ERROR, "sparsifier: dim must be >= 1");
+  if (d > 0xFFFFFFFFULL) return set_error(ctx, GP_ERROR, "sparsifier: dim exceeds 32-bit index space");
+  if (r < 1 || r > d) return set_error(ctx, GP_ERROR, "sparsifier: r out of range [1, d]");
+  if (d > ctx->max_d) return set_error(ctx, GP_CAPACITY, "top_r: d exceeds the context's max_d");
+  auto s = static_cast<cudaStream_t>(stream);
+  launch_top_r(ctx, d_grad, d, r, s);
+  cudaMemcpyAsync(d_support, ctx->ws.support, r * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s);
+  if (d_values) cudaMemcpyAsync(d_values, ctx->ws.values, r * sizeof(float), cudaMemcpyDeviceToDevice, s);
+  return check_launch(ctx, "top_r");
+}
+
+int gp_crc32c(gp_ctx* ctx, const uint8_t* d_data, uint64_t n, uint32_t* d_crc, void* stream) {
+  if (!ctx || (!d_data && n) || !d_crc) return set_error(ctx, GP_ERROR, "crc32c: null argument");
+  launch_crc_host_range(ctx, d_data, n, d_crc, static_cast<cudaStream_t>(stream));
+  return check_launch(ctx, "crc32c");
+}
+
+int gp_bloom_positive_scan(gp_ctx* ctx, const uint8_t*, uint64_t, uint64_t, uint32_t*, uint64_t, uint64_t*, void*) {
+  return set_error(ctx, GP_UNSUPPORTED, "bloom positive scan not built yet");
+}
+
+int gp_bloom_select(gp_ctx* ctx, const uint8_t*, uint64_t, uint64_t, uint64_t, int, uint32_t*, void*) {
+  return set_error(ctx, GP_UNSUPPORTED, "bloom selection not built yet");
+}
+
+}  // extern "C"

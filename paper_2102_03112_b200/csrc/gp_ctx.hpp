@@ -1,0 +1,157 @@
+// gp_ctx.hpp — host-side context: device workspace, device plan, launch accounting.
+//
+// One gp_ctx per (device, stream user).  Everything a step needs is carved out
+// of one cudaMalloc made at gp_ctx_create, sized for gradients of up to max_d
+// elements, so no allocation (and no implicit synchronisation) happens inside
+// encode/decode.  Data-dependent sizes (|P|, payload lengths, segment counts)
+// never travel to the host: kernels read them from the device-resident Plan
+// and size their grid-stride loops from it.
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include <cuda_runtime.h>
+
+#include "../../include/gradpack_b200.h"
+
+namespace gp {
+
+// Device-resident step descriptor, rewritten by each encode/decode call.
+struct Plan {
+  // ---- shared
+  uint64_t d, r;
+  uint8_t index_method, value_method, flags, pd_variant;
+  uint32_t pad0;
+  uint64_t il, vl, rl;          // payload lengths (bytes)
+  uint64_t total_len;           // container length
+  uint64_t n_values;            // value count (|P| for bloom-p0, else r)
+  uint64_t n_sel;               // selected coordinates written to `sel`
+  // ---- top-r
+  uint32_t bin_star, full_bin;  // threshold bin of key >> kTopShift; bin fully kept?
+  uint32_t thresh, tie_cut;     // exact threshold key; last kept index among ties
+  uint64_t above, n_cand;       // keys in bins above bin_star; candidates emitted
+  // ---- bloom
+  uint64_t m, seed_a, seed_b, minv;
+  uint32_t k, pad1;
+  uint64_t n_pos;               // |P|
+  uint64_t n_pairs, n_sets, n_multi, n_single_sel;
+  // ---- rle
+  uint64_t n_runs, n_groups;
+  // ---- value codec
+  uint32_t sign_split, identity;
+  uint32_t nseg, degree;
+  uint32_t seg_end[64];         // fit bounds (<= 64 segments on this path)
+  float coeffs[64 * 8];
+  // ---- decode
+  uint64_t crc_stored;
+  uint32_t crc_calc, post_crc_error;
+  uint64_t off_index, off_value, off_reorder;
+};
+
+constexpr int kMaxSeg = 64;
+
+struct Workspace {
+  void* base = nullptr;
+  size_t bytes = 0;
+  size_t bytes_total = 0;
+  Plan* plan = nullptr;
+  uint32_t* status = nullptr;
+  uint8_t* scan_base = nullptr;   // [128 B tickets | tile descriptors], zeroed per scan
+  uint32_t* ticket = nullptr;     // 32 tickets (first 128 B of scan_base)
+  uint64_t* tiles = nullptr;      // scan tile descriptors
+  size_t tiles_cap = 0;
+  uint32_t* hist = nullptr;       // 65536 bins
+  uint32_t* cand_idx = nullptr;   // [D]
+  float* cand_val = nullptr;      // [D]
+  uint32_t* support = nullptr;    // [D]
+  float* values = nullptr;        // [D]
+  uint32_t* filter = nullptr;     // filter words, m_cap bits
+  uint64_t m_cap = 0;
+  uint32_t* pos = nullptr;        // P [D]
+  uint32_t* sel = nullptr;        // selection [D]
+  uint8_t* flags = nullptr;       // per-P flags [D]
+  uint32_t* bucket = nullptr;     // per-bit counters [m_cap + 1]
+  uint32_t* bucket_off = nullptr; // per-bit offsets [m_cap + 1]
+  uint32_t* pairs = nullptr;      // conflict pairs [pair_cap]
+  uint64_t pair_cap = 0;
+  uint32_t* set_bit = nullptr;    // multi-member sets (bit) [m_cap]
+  uint32_t* set_key = nullptr;    // sort keys [m_cap]
+  uint32_t* set_tmp = nullptr;    // [m_cap]
+  uint32_t* set_tmp2 = nullptr;   // [m_cap]
+  uint32_t* u32a = nullptr;       // generic [D]
+  uint32_t* u32b = nullptr;       // generic [D]
+  uint32_t* u32c = nullptr;       // generic [D]
+  uint32_t* u32d = nullptr;       // generic [D]
+  double* f64a = nullptr;         // [D]
+  double* f64b = nullptr;         // [D]
+  double* partial = nullptr;      // fit partial sums [4096 * 32]
+  uint32_t* crc_part = nullptr;   // chunk CRCs [crc_cap]
+  uint64_t crc_cap = 0;
+  uint8_t* scratch = nullptr;     // generic byte scratch [2 * D]
+};
+
+}  // namespace gp
+
+struct gp_ctx {
+  int device = 0;
+  int sm_count = 148;
+  uint64_t max_d = 0;
+  gp::Workspace ws;
+  std::string last_error;
+  uint64_t launches = 0;
+};
+
+namespace gp {
+
+// Every kernel launch goes through this macro so gp_ctx_launch_count() can
+// report how many native kernels a step enqueued.
+#define GP_LAUNCH(ctx, kernel, grid, block, smem, stream, ...)                         \
+  do {                                                                                \
+    kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                       \
+    ++(ctx)->launches;                                                                \
+  } while (0)
+
+// Grid for a grid-stride loop over n items: enough blocks to cover n, capped
+// at 8 resident blocks per SM.
+inline int grid_for(const gp_ctx* ctx, uint64_t n, int block) {
+  const uint64_t g = (n + block - 1) / block;
+  const uint64_t cap = static_cast<uint64_t>(ctx->sm_count) * 8;
+  return static_cast<int>(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+int set_error(gp_ctx* ctx, int code, const std::string& msg);
+int check_launch(gp_ctx* ctx, const char* what);
+
+// ---- host launchers, grouped by translation unit ----
+void reset_scan(gp_ctx* ctx, cudaStream_t s, uint64_t ntiles_bound);  // capi.cu
+
+// topr.cu: ws.support / ws.values <- top-r of grad
+void launch_top_r(gp_ctx* ctx, const float* grad, uint64_t d, uint64_t r, cudaStream_t s);
+
+// container.cu
+void launch_crc_range(gp_ctx* ctx, const uint8_t* base, const uint64_t* off_dev, uint64_t off_host,
+                      const uint64_t* la, const uint64_t* lb, const uint64_t* lc, uint64_t len_host,
+                      uint64_t len_bound, uint32_t* out, cudaStream_t s);
+void launch_crc_host_range(gp_ctx* ctx, const uint8_t* data, uint64_t n, uint32_t* out, cudaStream_t s);
+void launch_finish_container(gp_ctx* ctx, uint8_t* out, uint64_t cap, uint64_t* d_len, uint64_t len_bound,
+                             cudaStream_t s);
+void launch_parse_container(gp_ctx* ctx, const uint8_t* in, uint64_t len, const gp_pipeline_config* hint,
+                            cudaStream_t s);
+
+// indexcodec.cu
+void launch_index_none(gp_ctx* ctx, uint8_t* out, uint64_t r, cudaStream_t s);
+void launch_index_bitmap(gp_ctx* ctx, uint8_t* out, uint64_t d, uint64_t r, cudaStream_t s);
+void launch_decode_index_none(gp_ctx* ctx, const uint8_t* in, uint64_t r_bound, cudaStream_t s);
+void launch_validate_support(gp_ctx* ctx, uint64_t r_bound, cudaStream_t s);
+void launch_decode_index_bitmap(gp_ctx* ctx, const uint8_t* in, uint64_t d_bound, cudaStream_t s);
+
+// values.cu
+void launch_gather_values(gp_ctx* ctx, const float* dense, uint64_t n_bound, cudaStream_t s);
+void launch_values_raw(gp_ctx* ctx, uint8_t* out, bool f64, uint64_t n_bound, cudaStream_t s);
+void launch_values_raw_check(gp_ctx* ctx, cudaStream_t s);
+void launch_decode_scatter(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, float* dense, float scale,
+                           uint32_t* out_support, double* out_values, uint64_t cap, uint64_t* d_count,
+                           uint64_t* d_dim, cudaStream_t s);
+
+}  // namespace gp

@@ -1,0 +1,114 @@
+// values.cu — value payloads and the decode scatter.
+//   gather_values (pipeline.cpp:38-54): v[j] = dense[sel[j]] for Bloom selections
+//   id 0 raw f32 / id 5 raw f64 (pipeline.cpp:58-68, :97-112)
+//   K18 decode_accumulate: dense[support[i]] += scale * value[i] — the
+//   per-peer term of the harness mean (harness.cpp:274-284) fused with
+//   to_dense (gradient.cpp:38-42).  Supports are unique per container, so the
+//   scatter needs no atomics; peers are accumulated in rank order.
+#include "gp_ctx.hpp"
+#include "gp_device.cuh"
+
+namespace gp {
+
+namespace {
+
+__global__ void gather_values(const float* __restrict__ dense, const uint32_t* __restrict__ sel, const Plan* plan,
+                              float* __restrict__ values, const uint32_t* status) {
+  if (failed(status)) return;
+  const uint64_t n = plan->n_values;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    values[i] = dense[sel[i]];
+}
+
+__global__ void values_raw_encode(const float* __restrict__ values, Plan* plan, uint8_t* out, int f64,
+                                  const uint32_t* status) {
+  if (failed(status)) return;
+  const uint64_t n = plan->n_values;
+  uint8_t* p = out + 49 + plan->il;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    if (f64) {
+      const double v = static_cast<double>(values[i]);
+      st_u64_unaligned(p + 8 * i, static_cast<uint64_t>(__double_as_longlong(v)));
+    } else {
+      st_u32_unaligned(p + 4 * i, __float_as_uint(values[i]));
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    plan->vl = (f64 ? 8 : 4) * n;
+    plan->rl = 0;
+  }
+}
+
+// decode_values length checks for the raw kinds (pipeline.cpp:98-99, :107-108)
+__global__ void values_raw_check(Plan* plan, uint32_t* status) {
+  if (failed(status)) return;
+  const uint8_t vm = plan->value_method;
+  const uint64_t n = plan->n_values;
+  if (vm == GP_VALUE_NONE && plan->vl != 4 * n) latch(status, GP_CORRUPT_PAYLOAD);
+  if (vm == GP_VALUE_RAW_F64 && plan->vl != 8 * n) latch(status, GP_CORRUPT_PAYLOAD);
+  if (vm == GP_VALUE_QUANT || vm == GP_VALUE_DEFLATE_SLOT || vm == GP_VALUE_FIT_DEXP) latch(status, GP_UNSUPPORTED);
+}
+
+// value i of the decoded container: raw payload bytes or the fit evaluation
+__device__ __forceinline__ double value_at(const uint8_t* vp, uint8_t vm, const double* fitv, uint64_t i) {
+  if (vm == GP_VALUE_NONE) return static_cast<double>(__uint_as_float(ld_u32_unaligned(vp + 4 * i)));
+  if (vm == GP_VALUE_RAW_F64) return __longlong_as_double(static_cast<long long>(ld_u64_unaligned(vp + 8 * i)));
+  return fitv[i];
+}
+
+__global__ void decode_scatter(const uint8_t* __restrict__ in, const Plan* plan, const uint32_t* __restrict__ sel,
+                               const double* __restrict__ fitv, float* dense, float scale, uint32_t* out_support,
+                               double* out_values, uint64_t cap, uint64_t* d_count, uint64_t* d_dim,
+                               uint32_t* status) {
+  if (failed(status)) return;
+  const uint64_t n = plan->n_values;
+  if (out_support && n > cap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) latch(status, GP_CAPACITY);
+    return;
+  }
+  const uint8_t vm = plan->value_method;
+  const uint8_t* vp = in + plan->off_value;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t s = sel[i];
+    const double v = value_at(vp, vm, fitv, i);
+    if (dense) dense[s] = fmaf(scale, static_cast<float>(v), dense[s]);
+    if (out_support) {
+      out_support[i] = s;
+      out_values[i] = v;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (d_count) *d_count = n;
+    if (d_dim) *d_dim = plan->d;
+  }
+}
+
+}  // namespace
+
+void launch_gather_values(gp_ctx* ctx, const float* dense, uint64_t n_bound, cudaStream_t s) {
+  Workspace& w = ctx->ws;
+  GP_LAUNCH(ctx, gather_values, grid_for(ctx, n_bound, 256), 256, 0, s, dense, w.sel, w.plan, w.values, w.status);
+}
+
+void launch_values_raw(gp_ctx* ctx, uint8_t* out, bool f64, uint64_t n_bound, cudaStream_t s) {
+  Workspace& w = ctx->ws;
+  GP_LAUNCH(ctx, values_raw_encode, grid_for(ctx, n_bound, 256), 256, 0, s, w.values, w.plan, out, f64 ? 1 : 0,
+            w.status);
+}
+
+void launch_values_raw_check(gp_ctx* ctx, cudaStream_t s) {
+  GP_LAUNCH(ctx, values_raw_check, 1, 1, 0, s, ctx->ws.plan, ctx->ws.status);
+}
+
+void launch_decode_scatter(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, float* dense, float scale,
+                           uint32_t* out_support, double* out_values, uint64_t cap, uint64_t* d_count,
+                           uint64_t* d_dim, cudaStream_t s) {
+  Workspace& w = ctx->ws;
+  GP_LAUNCH(ctx, decode_scatter, grid_for(ctx, n_bound, 256), 256, 0, s, in, w.plan, w.sel, w.f64a, dense, scale,
+            out_support, out_values, cap, d_count, d_dim, w.status);
+}
+
+}  // namespace gp
