@@ -40,11 +40,16 @@ bool is_bloom(int m) { return m >= GP_INDEX_BLOOM_P0 && m <= GP_INDEX_BLOOM_NAIV
 
 // Methods with a device implementation on this path (the rest of FORMAT.md's
 // registry returns GP_UNSUPPORTED).
-bool index_supported(int m) { return m == GP_INDEX_NONE || m == GP_INDEX_BITMAP; }
+bool index_supported(int m) {
+  return m == GP_INDEX_NONE || m == GP_INDEX_BITMAP || m == GP_INDEX_BLOOM_P0 || m == GP_INDEX_BLOOM_P2 ||
+         m == GP_INDEX_BLOOM_PD || m == GP_INDEX_BLOOM_NAIVE;
+}
 bool value_supported(int m) { return m == GP_VALUE_NONE || m == GP_VALUE_RAW_F64; }
 
 struct PlanInit {
   uint64_t d, r, il, n_values;
+  uint64_t m, seed_a, seed_b, minv;
+  uint32_t k;
   uint8_t index_method, value_method, pd_variant;
 };
 
@@ -63,6 +68,11 @@ __global__ void init_plan(Plan* plan, PlanInit p) {
   plan->off_index = 49;
   plan->off_value = 49 + p.il;
   plan->off_reorder = 49 + p.il;
+  plan->m = p.m;
+  plan->k = p.k;
+  plan->seed_a = p.seed_a;
+  plan->seed_b = p.seed_b;
+  plan->minv = p.minv;
 }
 
 // compress_gradient's validate(sg) (gradient.cpp:19-30) + gather(dense, support)
@@ -114,6 +124,16 @@ void carve(Workspace& w, uint8_t* base, uint64_t D) {
   w.pos = c.take<uint32_t>(D);
   w.sel = c.take<uint32_t>(D);
   w.flags = c.take<uint8_t>(D);
+  w.selbits = c.take<uint32_t>(D / 32 + 1);
+  w.set_cap = 2 * D;
+  w.pair_cap = 4 * D;
+  w.p2_count = c.take<uint32_t>(w.set_cap + 1);
+  w.p2_off = c.take<uint32_t>(w.set_cap + 1);
+  w.p2_size = c.take<uint32_t>(w.set_cap);
+  w.p2_sets = c.take<uint32_t>(w.set_cap);
+  w.p2_table = c.take<uint32_t>(256 * (w.set_cap / 4096 + 1) + 256);
+  w.pairs = c.take<uint32_t>(w.pair_cap);
+  w.p2_members = c.take<uint32_t>(w.pair_cap);
   w.u32a = c.take<uint32_t>(D);
   w.u32b = c.take<uint32_t>(D);
   w.u32c = c.take<uint32_t>(D);
@@ -282,7 +302,23 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
   pi.value_method = static_cast<uint8_t>(vm);
   pi.pd_variant = cfg->pd_variant;
   pi.n_values = r;
-  pi.il = im == GP_INDEX_NONE ? 4 * r : im == GP_INDEX_BITMAP ? (d + 7) / 8 : 0;
+  if (is_bloom(im)) {
+    uint64_t m = 0;
+    uint32_t k = 0;
+    if (gp_bloom_params(cfg->fpr, r, &m, &k) != GP_OK)
+      return set_error(ctx, GP_ERROR, "bloom_params: epsilon must be in (0, 1)");
+    if (m >= (1ULL << 32) || m > ctx->ws.m_cap || k > 0xFFFF)
+      return set_error(ctx, GP_CAPACITY, "bloom filter exceeds the context's filter capacity");
+    if (im == GP_INDEX_BLOOM_PD && cfg->pd_variant > 2) return set_error(ctx, GP_ERROR, "pd_select: unknown variant");
+    pi.m = m;
+    pi.k = k;
+    pi.seed_a = gp::hash64(0xA, cfg->seed);  // derive_filter_seed_a, pipeline.cpp:21
+    pi.seed_b = gp::hash64(0xB, cfg->seed);  // derive_filter_seed_b, pipeline.cpp:22
+    pi.minv = ~0ULL / m;
+    pi.il = 26 + (m + 7) / 8 + (im == GP_INDEX_BLOOM_PD ? 1 : 0);
+  } else {
+    pi.il = im == GP_INDEX_NONE ? 4 * r : (d + 7) / 8;
+  }
   GP_LAUNCH(ctx, init_plan, 1, 1, 0, s, ctx->ws.plan, pi);
 
   if (d_support) {
@@ -294,11 +330,21 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
   switch (im) {
     case GP_INDEX_NONE: launch_index_none(ctx, d_out, r, s); break;
     case GP_INDEX_BITMAP: launch_index_bitmap(ctx, d_out, d, r, s); break;
-    default: break;
+    default: {
+      launch_bloom_build(ctx, d_out, pi.m, r, s);
+      if (im == GP_INDEX_BLOOM_NAIVE) break;  // values stay in support order (pipeline.cpp:196-199)
+      launch_bloom_scan(ctx, d, pi.m, false, s);
+      if (im == GP_INDEX_BLOOM_P2)
+        launch_select_p2(ctx, d, pi.m, pi.k, s);
+      else
+        launch_select_slice(ctx, d, s);
+      launch_gather_values(ctx, d_dense, d, s);
+    }
   }
+  const uint64_t n_bound = im == GP_INDEX_BLOOM_P0 ? d : r;
   switch (vm) {
     case GP_VALUE_NONE:
-    case GP_VALUE_RAW_F64: launch_values_raw(ctx, d_out, vm == GP_VALUE_RAW_F64, r, s); break;
+    case GP_VALUE_RAW_F64: launch_values_raw(ctx, d_out, vm == GP_VALUE_RAW_F64, n_bound, s); break;
     default: break;
   }
   launch_finish_container(ctx, d_out, cap, d_len, bound, s);
@@ -353,7 +399,14 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const g
   switch (im) {
     case GP_INDEX_NONE: launch_decode_index_none(ctx, d_in, bound, s); break;
     case GP_INDEX_BITMAP: launch_decode_index_bitmap(ctx, d_in, bound, s); break;
-    default: break;
+    default: {
+      launch_bloom_parse(ctx, d_in, ctx->ws.m_cap, s);
+      launch_bloom_scan(ctx, bound, 0, true, s);
+      if (im == GP_INDEX_BLOOM_P2)
+        launch_select_p2(ctx, bound, ctx->ws.set_cap, 64, s);
+      else
+        launch_select_slice(ctx, bound, s);
+    }
   }
   switch (vm) {
     case GP_VALUE_NONE:

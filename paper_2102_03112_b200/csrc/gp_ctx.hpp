@@ -71,6 +71,15 @@ struct Workspace {
   uint32_t* pos = nullptr;        // P [D]
   uint32_t* sel = nullptr;        // selection [D]
   uint8_t* flags = nullptr;       // per-P flags [D]
+  uint32_t* selbits = nullptr;    // selection bitset over P positions [D/32]
+  // conflict sets (p2.cu)
+  uint64_t set_cap = 0;           // max filter width m for P2
+  uint32_t* p2_count = nullptr;   // [set_cap + 1]
+  uint32_t* p2_off = nullptr;     // [set_cap + 1]
+  uint32_t* p2_size = nullptr;    // [set_cap]
+  uint32_t* p2_sets = nullptr;    // [set_cap]
+  uint32_t* p2_table = nullptr;   // [256 * set_cap / 4096 + 256]
+  uint32_t* p2_members = nullptr; // [pair_cap]
   uint32_t* bucket = nullptr;     // per-bit counters [m_cap + 1]
   uint32_t* bucket_off = nullptr; // per-bit offsets [m_cap + 1]
   uint32_t* pairs = nullptr;      // conflict pairs [pair_cap]
@@ -145,6 +154,13 @@ void launch_index_bitmap(gp_ctx* ctx, uint8_t* out, uint64_t d, uint64_t r, cuda
 void launch_decode_index_none(gp_ctx* ctx, const uint8_t* in, uint64_t r_bound, cudaStream_t s);
 void launch_validate_support(gp_ctx* ctx, uint64_t r_bound, cudaStream_t s);
 void launch_decode_index_bitmap(gp_ctx* ctx, const uint8_t* in, uint64_t d_bound, cudaStream_t s);
+
+// bloom.cu / p2.cu
+void launch_bloom_build(gp_ctx* ctx, uint8_t* out, uint64_t m, uint64_t r, cudaStream_t s);
+void launch_bloom_parse(gp_ctx* ctx, const uint8_t* in, uint64_t m_bound, cudaStream_t s);
+void launch_bloom_scan(gp_ctx* ctx, uint64_t d_bound, uint64_t m_host, bool decoding, cudaStream_t s);
+void launch_select_slice(gp_ctx* ctx, uint64_t n_bound, cudaStream_t s);
+void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t k_bound, cudaStream_t s);
 
 // values.cu
 void launch_gather_values(gp_ctx* ctx, const float* dense, uint64_t n_bound, cudaStream_t s);

@@ -1,0 +1,390 @@
+// p2.cu — K9/K10: conflict sets and the P2 greedy selection
+// (conflict_sets bloom.cpp:156-173, p2_select bloom.cpp:175-222), bit-exact.
+//
+// conflict_sets: every positive x (in P order) contributes its k probe
+// positions; a bit's set is the ascending, de-duplicated list of positives
+// probing it; sets are ordered by (size, bit).  Device form:
+//   pairs    : one thread per positive, k positions, per-bit counts (atomics)
+//   offsets  : exclusive scan of the counts over [0, m)
+//   scatter  : members into per-bit buckets (arbitrary order)
+//   dedupe   : per bucket, sort + unique (buckets hold ~1-20 entries);
+//              a bucket of one distinct member is a singleton
+//   order    : one stable counting-sort pass by size over the bit domain,
+//              which also compacts away empty bits → sets in (size, bit) order
+//
+// p2_select: pass 1 first visits every singleton (bit order) and selects its
+// member.  Singleton members are always true keys (a false positive's probes
+// all land on bits set by true keys, so they are shared), hence at most r
+// distinct, and selection is a set: stage A is one parallel flag write.  When
+// a crafted filter breaks that bound (decode only) the exact sequential engine
+// below replays pass 1 from the first singleton instead.
+// Stage B is inherently sequential (each visit depends on earlier selections
+// and consumes the CounterRng stream): one warp walks the non-singleton sets
+// in order, repeating passes until r are selected.  A set whose unselected
+// member count is 0 retires, 1 selects it, >= 2 draws below(cnt) from the
+// stream (rng.hpp:52-59, rejection exact) and selects that member.  Retired
+// sets need no flag: revisiting them changes nothing and draws nothing.
+#include "gp_ctx.hpp"
+#include "gp_device.cuh"
+
+namespace gp {
+
+namespace {
+
+constexpr int kTileBlock = 256;
+constexpr int kTileItems = 16;
+constexpr int kTile = kTileBlock * kTileItems;
+constexpr int kMaxSetSize = 255;  // counting-sort digit; larger sets → GP_CAPACITY
+
+__device__ __forceinline__ bool p2_active(const Plan* plan) {
+  return plan->index_method == GP_INDEX_BLOOM_P2;
+}
+
+__global__ void p2_pairs(const uint32_t* __restrict__ P, Plan* plan, uint32_t* __restrict__ pairs,
+                         uint32_t* __restrict__ count, uint64_t pair_cap, uint64_t set_cap, uint32_t* status) {
+  if (failed(status) || !p2_active(plan)) return;
+  const uint64_t n = plan->n_pos, m = plan->m;
+  const uint32_t k = plan->k;
+  if (n * k > pair_cap || m > set_cap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) latch(status, GP_CAPACITY);
+    return;
+  }
+  const FastMod fm{m, plan->minv};
+  const uint64_t sa = plan->seed_a + kGamma, sb = plan->seed_b + kGamma;
+  for (uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; p < n;
+       p += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t x = P[p];
+    const uint64_t a = mix64(x ^ sa), b = mix64(x ^ sb);
+    uint64_t h = a;
+    for (uint32_t j = 0; j < k; ++j, h += b) {
+      const uint32_t bit = static_cast<uint32_t>(fast_mod(mix64(h), fm));
+      pairs[p * k + j] = bit;
+      atomicAdd(&count[bit], 1u);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) plan->n_pairs = n * k;
+}
+
+// exclusive scan of count[0, m) into off[0, m]; tiles of 4096 bits
+__global__ void __launch_bounds__(kTileBlock) p2_offsets(const uint32_t* __restrict__ count, Plan* plan,
+                                                         uint32_t* __restrict__ off, uint64_t* tiles,
+                                                         uint32_t* ticket, const uint32_t* status) {
+  __shared__ uint64_t sh[36];
+  __shared__ uint32_t slot;
+  if (failed(status) || !p2_active(plan)) return;
+  const uint64_t m = plan->m;
+  const uint64_t ntiles = (m + kTile - 1) / kTile;
+  while (true) {
+    const uint32_t tile = claim_tile(ticket, &slot);
+    if (tile >= ntiles) break;
+    const uint64_t base = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(threadIdx.x) * kTileItems;
+    uint32_t c[kTileItems];
+    uint64_t sum = 0;
+#pragma unroll
+    for (int q = 0; q < kTileItems; ++q) {
+      c[q] = base + q < m ? count[base + q] : 0;
+      sum += c[q];
+    }
+    uint64_t tot;
+    uint64_t o = tile_exclusive_offset<kTileBlock>(sum, tile, tiles, sh, tot);
+#pragma unroll
+    for (int q = 0; q < kTileItems; ++q) {
+      if (base + q < m) off[base + q] = static_cast<uint32_t>(o);
+      o += c[q];
+    }
+    if (tile == ntiles - 1 && threadIdx.x == kTileBlock - 1) off[m] = static_cast<uint32_t>(o);
+  }
+}
+
+__global__ void p2_scatter(const uint32_t* __restrict__ pairs, const Plan* plan, const uint32_t* __restrict__ off,
+                           uint32_t* count, uint32_t* __restrict__ members, const uint32_t* status) {
+  if (failed(status) || !p2_active(plan)) return;
+  const uint64_t np = plan->n_pairs;
+  const uint32_t k = plan->k;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < np;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t bit = pairs[i];
+    const uint32_t slot = off[bit] + atomicSub(&count[bit], 1u) - 1u;  // count returns to 0
+    members[slot] = static_cast<uint32_t>(i / k);
+  }
+}
+
+// per bit: sort + unique the bucket; size[bit] = distinct members; stage A flags
+__global__ void p2_dedupe(const Plan* plan, const uint32_t* __restrict__ off, uint32_t* __restrict__ members,
+                          uint32_t* __restrict__ size, uint32_t* __restrict__ selbits, uint32_t* status) {
+  if (failed(status) || !p2_active(plan)) return;
+  const uint64_t m = plan->m;
+  for (uint64_t b = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; b < m;
+       b += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t lo = off[b], hi = off[b + 1];
+    const uint32_t n = hi - lo;
+    if (n == 0) {
+      size[b] = 0;
+      continue;
+    }
+    uint32_t* mem = members + lo;
+    // insertion sort (buckets are tiny: k probes of ~|P|k/m positives)
+    for (uint32_t i = 1; i < n; ++i) {
+      const uint32_t v = mem[i];
+      uint32_t j = i;
+      while (j > 0 && mem[j - 1] > v) {
+        mem[j] = mem[j - 1];
+        --j;
+      }
+      mem[j] = v;
+    }
+    uint32_t u = 1;
+    for (uint32_t i = 1; i < n; ++i)
+      if (mem[i] != mem[u - 1]) mem[u++] = mem[i];
+    size[b] = u;
+    if (u > kMaxSetSize) latch(status, GP_CAPACITY);
+    if (u == 1) atomicOr(&selbits[mem[0] >> 5], 1u << (mem[0] & 31));
+  }
+}
+
+// Stable counting sort of the non-empty bits by size (digit = size <= 255):
+// upsweep per-tile histograms into table[digit * ntiles + tile] ...
+__global__ void __launch_bounds__(kTileBlock) p2_size_hist(const Plan* plan, const uint32_t* __restrict__ size,
+                                                           uint32_t* __restrict__ table, const uint32_t* status) {
+  __shared__ uint32_t h[256];
+  if (failed(status) || !p2_active(plan)) return;
+  const uint64_t m = plan->m;
+  const uint64_t ntiles = (m + kTile - 1) / kTile;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t base = tile * kTile;
+    for (int q = threadIdx.x; q < kTile; q += kTileBlock) {
+      const uint64_t b = base + q;
+      if (b < m) {
+        const uint32_t s = size[b];
+        if (s) atomicAdd(&h[s], 1u);
+      }
+    }
+    __syncthreads();
+    table[threadIdx.x * ntiles + tile] = h[threadIdx.x];
+    __syncthreads();
+  }
+}
+
+// ... exclusive scan of the digit-major table (one block) ...
+__global__ void __launch_bounds__(1024) p2_table_scan(Plan* plan, uint32_t* table, const uint32_t* status) {
+  __shared__ uint64_t sh[40];
+  if (failed(status) || !p2_active(plan)) return;
+  const uint64_t m = plan->m;
+  const uint64_t ntiles = (m + kTile - 1) / kTile;
+  const uint64_t n = 256 * ntiles;
+  uint64_t carry = 0;
+  for (uint64_t base = 0; base < n; base += 1024) {
+    const uint64_t i = base + threadIdx.x;
+    const uint64_t v = i < n ? table[i] : 0;
+    uint64_t tot;
+    const uint64_t ex = block_exclusive_sum<uint64_t, 1024>(v, sh, tot);
+    if (i < n) table[i] = static_cast<uint32_t>(carry + ex);
+    carry += tot;
+  }
+  if (threadIdx.x == 0) plan->n_sets = carry;
+}
+
+// ... and the stable downsweep: sets[table[digit][tile] + rank] = bit.
+__global__ void __launch_bounds__(kTileBlock) p2_size_scatter(const Plan* plan, const uint32_t* __restrict__ size,
+                                                              const uint32_t* __restrict__ table,
+                                                              uint32_t* __restrict__ sets, const uint32_t* status) {
+  __shared__ uint32_t run[256];
+  __shared__ uint32_t wcnt[kTileBlock / 32][256];
+  if (failed(status) || !p2_active(plan)) return;
+  const uint64_t m = plan->m;
+  const uint64_t ntiles = (m + kTile - 1) / kTile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    run[threadIdx.x] = table[threadIdx.x * ntiles + tile];
+    __syncthreads();
+    const uint64_t base = tile * kTile;
+    for (int round = 0; round < kTileItems; ++round) {
+      const uint64_t b = base + static_cast<uint64_t>(round) * kTileBlock + threadIdx.x;
+      const uint32_t s = b < m ? size[b] : 0;
+      const uint32_t dig = s;  // 0 = empty bit, not emitted
+      const unsigned peers = __match_any_sync(kFull, dig);
+      const uint32_t lrank = __popc(peers & ((1u << lane) - 1));
+      for (int i = lane; i < 256; i += 32) wcnt[warp][i] = 0;
+      __syncwarp();
+      if ((peers & ((1u << lane) - 1)) == 0) wcnt[warp][dig] = __popc(peers);
+      __syncthreads();
+      uint32_t before = 0;
+      for (int w2 = 0; w2 < warp; ++w2) before += wcnt[w2][dig];
+      if (s) sets[run[dig] + before + lrank] = static_cast<uint32_t>(b);
+      __syncthreads();
+      // advance running offsets by this round's per-digit totals
+      {
+        uint32_t tot = 0;
+        for (int w2 = 0; w2 < kTileBlock / 32; ++w2) tot += wcnt[w2][threadIdx.x];
+        run[threadIdx.x] += tot;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// stage-A count (distinct singleton members) and the singleton/multi split
+__global__ void __launch_bounds__(1024) p2_stage_a(Plan* plan, const uint32_t* __restrict__ selbits,
+                                                   const uint32_t* __restrict__ table, const uint32_t* status) {
+  __shared__ uint64_t sh[40];
+  if (failed(status) || !p2_active(plan)) return;
+  const uint64_t nw = (plan->n_pos + 31) / 32;
+  uint64_t c = 0;
+  for (uint64_t i = threadIdx.x; i < nw; i += 1024) c += __popc(selbits[i]);
+  uint64_t tot;
+  block_exclusive_sum<uint64_t, 1024>(c, sh, tot);
+  if (threadIdx.x == 0) {
+    const uint64_t ntiles = (plan->m + kTile - 1) / kTile;
+    const uint64_t n1 = table[2 * ntiles] - table[1 * ntiles];  // sets of size 1
+    plan->n_single_sel = tot;
+    plan->n_multi = plan->n_sets - n1;
+    plan->n_cand = n1;  // first multi set index in the sorted list
+  }
+}
+
+// Stage B: one warp replays the sequential greedy loop.
+__device__ __forceinline__ bool bs_test(const uint32_t* bs, uint32_t p) { return (bs[p >> 5] >> (p & 31)) & 1u; }
+
+template <bool kSmem>
+__global__ void __launch_bounds__(32) p2_engine(Plan* plan, const uint32_t* __restrict__ sets,
+                                                const uint32_t* __restrict__ off, const uint32_t* __restrict__ size,
+                                                const uint32_t* __restrict__ members, uint32_t* selbits,
+                                                uint32_t* status) {
+  extern __shared__ uint32_t sbits[];
+  if (failed(status) || !p2_active(plan)) return;
+  const int lane = threadIdx.x;
+  const uint64_t n = plan->n_pos, r = plan->r;
+  const uint64_t nwords = (n + 31) / 32;
+  uint32_t* bits = kSmem ? sbits : selbits;
+  const bool fallback = plan->n_single_sel > r;
+  // selected bitset over P positions: the stage-A singletons (empty on fallback)
+  if (kSmem || fallback)
+    for (uint64_t w = lane; w < nwords; w += 32) bits[w] = fallback ? 0u : selbits[w];
+  __syncwarp();
+  uint64_t nsel = fallback ? 0 : plan->n_single_sel;
+  const uint64_t nsets = plan->n_sets;
+  const uint64_t start = fallback ? 0 : plan->n_cand;
+  const uint64_t seed = hash64(plan->seed_a, plan->seed_b);  // derive_selection_seed
+  uint64_t rpos = 0;                                          // CounterRng draws consumed
+  while (nsel < r && start < nsets) {
+    const uint64_t before = nsel;
+    for (uint64_t si = start; si < nsets && nsel < r; ++si) {
+      const uint32_t bit = sets[si];
+      const uint32_t lo = off[bit], sz = size[bit];
+      // count unselected members (ascending order = lane order within chunks)
+      uint32_t cnt = 0;
+      for (uint32_t c = 0; c < sz; c += 32) {
+        const bool in = c + lane < sz;
+        const uint32_t p = in ? members[lo + c + lane] : 0;
+        cnt += __popc(__ballot_sync(kFull, in && !bs_test(bits, p)));
+      }
+      if (cnt == 0) continue;
+      uint32_t target = 0;
+      if (cnt > 1) {
+        // CounterRng::below(cnt), exact rejection (rng.hpp:52-59)
+        const uint64_t bound = below_bound(cnt);
+        uint64_t v = rng_at(seed, rpos++);
+        while (v > bound) v = rng_at(seed, rpos++);
+        target = static_cast<uint32_t>(v % cnt);
+      }
+      // select the target-th unselected member
+      uint32_t seen = 0;
+      for (uint32_t c = 0; c < sz; c += 32) {
+        const bool in = c + lane < sz;
+        const uint32_t p = in ? members[lo + c + lane] : 0;
+        const bool un = in && !bs_test(bits, p);
+        const unsigned bal = __ballot_sync(kFull, un);
+        const uint32_t here = __popc(bal);
+        if (target < seen + here) {
+          const uint32_t want = target - seen;
+          if (un && __popc(bal & ((1u << lane) - 1)) == want) bits[p >> 5] |= 1u << (p & 31);
+          __syncwarp();
+          break;
+        }
+        seen += here;
+      }
+      ++nsel;
+    }
+    if (nsel == before) break;  // no progress possible (cannot happen with |P| >= r)
+  }
+  __syncwarp();
+  if (kSmem)
+    for (uint64_t w = lane; w < nwords; w += 32) selbits[w] = bits[w];
+  if (lane == 0) plan->n_sel = nsel;
+}
+
+// sel = ascending P[p] for flagged p (bloom.cpp:221 sort), count must be r
+__global__ void __launch_bounds__(kTileBlock) flags_compact(const uint32_t* __restrict__ P,
+                                                            const uint32_t* __restrict__ selbits, Plan* plan,
+                                                            int method, uint32_t* __restrict__ sel, uint64_t* tiles,
+                                                            uint32_t* ticket, uint32_t* status) {
+  __shared__ uint64_t sh[36];
+  __shared__ uint32_t slot;
+  if (failed(status) || plan->index_method != method) return;
+  const uint64_t n = plan->n_pos;
+  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  while (true) {
+    const uint32_t tile = claim_tile(ticket, &slot);
+    if (tile >= ntiles) break;
+    const uint64_t base = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(threadIdx.x) * kTileItems;
+    uint32_t mask = 0;
+#pragma unroll
+    for (int q = 0; q < kTileItems; ++q)
+      if (base + q < n && bs_test(selbits, static_cast<uint32_t>(base + q))) mask |= 1u << q;
+    uint64_t tot;
+    uint64_t o = tile_exclusive_offset<kTileBlock>(__popc(mask), tile, tiles, sh, tot);
+    while (mask) {
+      const int q = __ffs(mask) - 1;
+      if (o < plan->r) sel[o] = P[base + q];
+      ++o;
+      mask &= mask - 1;
+    }
+    if (tile == ntiles - 1 && threadIdx.x == kTileBlock - 1 && o != plan->r) latch(status, GP_ERROR);
+  }
+}
+
+}  // namespace
+
+void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t k_bound, cudaStream_t s) {
+  Workspace& w = ctx->ws;
+  const uint64_t m_cap = std::min<uint64_t>(m_bound, w.set_cap);
+  cudaMemsetAsync(w.p2_count, 0, (m_cap + 1) * sizeof(uint32_t), s);
+  cudaMemsetAsync(w.selbits, 0, ((n_bound + 31) / 32) * 4, s);
+  GP_LAUNCH(ctx, p2_pairs, grid_for(ctx, n_bound, 128), 128, 0, s, w.pos, w.plan, w.pairs, w.p2_count, w.pair_cap,
+            w.set_cap, w.status);
+  const uint64_t mtiles = (m_cap + kTile - 1) / kTile;
+  reset_scan(ctx, s, mtiles + 1);
+  GP_LAUNCH(ctx, p2_offsets, grid_for(ctx, mtiles * kTileBlock, kTileBlock), kTileBlock, 0, s, w.p2_count, w.plan,
+            w.p2_off, w.tiles, w.ticket, w.status);
+  const uint64_t pair_bound = std::min<uint64_t>(n_bound * k_bound, w.pair_cap);
+  GP_LAUNCH(ctx, p2_scatter, grid_for(ctx, pair_bound, 256), 256, 0, s, w.pairs, w.plan, w.p2_off, w.p2_count,
+            w.p2_members, w.status);
+  GP_LAUNCH(ctx, p2_dedupe, grid_for(ctx, m_cap, 128), 128, 0, s, w.plan, w.p2_off, w.p2_members, w.p2_size,
+            w.selbits, w.status);
+  const int tgrid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(mtiles, ctx->sm_count * 4ULL)));
+  GP_LAUNCH(ctx, p2_size_hist, tgrid, kTileBlock, 0, s, w.plan, w.p2_size, w.p2_table, w.status);
+  GP_LAUNCH(ctx, p2_table_scan, 1, 1024, 0, s, w.plan, w.p2_table, w.status);
+  GP_LAUNCH(ctx, p2_size_scatter, tgrid, kTileBlock, 0, s, w.plan, w.p2_size, w.p2_table, w.p2_sets, w.status);
+  GP_LAUNCH(ctx, p2_stage_a, 1, 1024, 0, s, w.plan, w.selbits, w.p2_table, w.status);
+  const uint64_t bs_bytes = ((n_bound + 31) / 32) * 4;
+  if (bs_bytes <= 200 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(p2_engine<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    GP_LAUNCH(ctx, p2_engine<true>, 1, 32, bs_bytes, s, w.plan, w.p2_sets, w.p2_off, w.p2_size, w.p2_members,
+              w.selbits, w.status);
+  } else {
+    GP_LAUNCH(ctx, p2_engine<false>, 1, 32, 0, s, w.plan, w.p2_sets, w.p2_off, w.p2_size, w.p2_members,
+              w.selbits, w.status);
+  }
+  const uint64_t ptiles = (n_bound + kTile - 1) / kTile;
+  reset_scan(ctx, s, ptiles + 1);
+  GP_LAUNCH(ctx, flags_compact, grid_for(ctx, ptiles * kTileBlock, kTileBlock), kTileBlock, 0, s, w.pos, w.selbits,
+            w.plan, static_cast<int>(GP_INDEX_BLOOM_P2), w.sel, w.tiles, w.ticket, w.status);
+}
+
+}  // namespace gp

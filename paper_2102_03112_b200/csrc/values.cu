@@ -63,7 +63,8 @@ __global__ void decode_scatter(const uint8_t* __restrict__ in, const Plan* plan,
                                double* out_values, uint64_t cap, uint64_t* d_count, uint64_t* d_dim,
                                uint32_t* status) {
   if (failed(status)) return;
-  const uint64_t n = plan->n_values;
+  const uint64_t n = plan->n_sel;       // coordinates written (|P| for naive)
+  const uint64_t nv = plan->n_values;   // values carried (naive: r, zero-filled past it)
   if (out_support && n > cap) {
     if (blockIdx.x == 0 && threadIdx.x == 0) latch(status, GP_CAPACITY);
     return;
@@ -73,7 +74,7 @@ __global__ void decode_scatter(const uint8_t* __restrict__ in, const Plan* plan,
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint32_t s = sel[i];
-    const double v = value_at(vp, vm, fitv, i);
+    const double v = i < nv ? value_at(vp, vm, fitv, i) : 0.0;
     if (dense) dense[s] = fmaf(scale, static_cast<float>(v), dense[s]);
     if (out_support) {
       out_support[i] = s;

@@ -136,3 +136,30 @@ def test_decode_error_classes_match_oracle(codec, oracle):
                 codec.status()
             assert type(ge.value).__name__ == oe.value.kind, (im, vm, len(bad), ge.value, oe.value)
             assert float(dense.abs().sum()) == 0.0  # a failed decode never touches the output
+
+
+BLOOM_CASES = [(P0, V_NONE), (P2, V_NONE), (PD, V_NONE), (NAIVE, V_NONE), (P2, V_F64)]
+
+
+@pytest.mark.parametrize("im,vm", BLOOM_CASES)
+@pytest.mark.parametrize("fpr", [0.1, 0.01, 0.001])
+def test_bloom_encode_bytes_bit_exact(codec, oracle, im, vm, fpr):
+    for d, r in [(1000, 10), (65536 + 3, 655), (269722, 2697), (1_000_000, 10_000)]:
+        g = synthetic_gradient(d, rank=d % 7)
+        for seed in (1, 12345):
+            cfg = _cfg(im, vm, fpr=fpr, seed=seed, pd_variant=seed % 3)
+            got = codec.compress(_dev(g), r, cfg).cpu().numpy().tobytes()
+            want = oracle.encode_dense(g, r, GpConfig.make(im, vm, fpr=fpr, seed=seed, pd_variant=seed % 3))
+            assert len(got) == len(want), (im, vm, fpr, d, r, seed)
+            assert got == want, (im, vm, fpr, d, r, seed)
+
+
+@pytest.mark.parametrize("im,vm", BLOOM_CASES)
+def test_bloom_decode_bit_exact(codec, oracle, im, vm):
+    for d, r, fpr in [(5000, 50, 0.3), (269722, 2697, 0.01), (1_000_000, 10_000, 0.001)]:
+        g = synthetic_gradient(d, rank=3)
+        c = oracle.encode_dense(g, r, GpConfig.make(im, vm, fpr=fpr, seed=d, pd_variant=2))
+        gd, sup, val = codec.decompress(_dev(np.frombuffer(c, np.uint8)))
+        od, osup, oval = oracle.decode(c)
+        assert gd == od and np.array_equal(sup.cpu().numpy().astype(np.uint32), osup)
+        assert np.array_equal(val.cpu().numpy(), oval)
