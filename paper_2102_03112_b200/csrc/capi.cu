@@ -44,7 +44,7 @@ bool index_supported(int m) {
   return m == GP_INDEX_NONE || m == GP_INDEX_BITMAP || m == GP_INDEX_BLOOM_P0 || m == GP_INDEX_BLOOM_P2 ||
          m == GP_INDEX_BLOOM_PD || m == GP_INDEX_BLOOM_NAIVE;
 }
-bool value_supported(int m) { return m == GP_VALUE_NONE || m == GP_VALUE_RAW_F64; }
+bool value_supported(int m) { return m == GP_VALUE_NONE || m == GP_VALUE_RAW_F64 || m == GP_VALUE_FIT_POLY; }
 
 struct PlanInit {
   uint64_t d, r, il, n_values;
@@ -140,7 +140,8 @@ void carve(Workspace& w, uint8_t* base, uint64_t D) {
   w.u32d = c.take<uint32_t>(D);
   w.f64a = c.take<double>(D);
   w.f64b = c.take<double>(D);
-  w.partial = c.take<double>(4096 * 32);
+  w.partial = c.take<double>((D / 2048 + 128) * 44);
+  w.sort_table = c.take<uint32_t>(256 * (D / 4096 + 2));
   w.crc_cap = (64 * D + (1 << 20)) / (256 * 1024) + 64;
   w.crc_part = c.take<uint32_t>(w.crc_cap);
   w.scratch = c.take<uint8_t>(2 * D);
@@ -292,6 +293,10 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
     return set_error(ctx, GP_ERROR, "container: unregistered method");
   if (!index_supported(im) || !value_supported(vm))
     return set_error(ctx, GP_UNSUPPORTED, "method not implemented on the device path");
+  if (vm == GP_VALUE_FIT_POLY) {
+    if (cfg->degree < 0 || cfg->degree > 60) return set_error(ctx, GP_ERROR, "value_compress: bad degree");
+    if (cfg->degree > 7) return set_error(ctx, GP_UNSUPPORTED, "fit degree > 7 is not on the device path");
+  }
   const uint64_t bound = gp_max_container_bytes(d, r, cfg);
   if (cap < bound) return set_error(ctx, GP_CAPACITY, "encode: output capacity below gp_max_container_bytes");
 
@@ -345,6 +350,7 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
   switch (vm) {
     case GP_VALUE_NONE:
     case GP_VALUE_RAW_F64: launch_values_raw(ctx, d_out, vm == GP_VALUE_RAW_F64, n_bound, s); break;
+    case GP_VALUE_FIT_POLY: launch_values_fit(ctx, d_out, cfg->degree, cfg->max_segments, n_bound, s); break;
     default: break;
   }
   launch_finish_container(ctx, d_out, cap, d_len, bound, s);
@@ -411,6 +417,7 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const g
   switch (vm) {
     case GP_VALUE_NONE:
     case GP_VALUE_RAW_F64: launch_values_raw_check(ctx, s); break;
+    case GP_VALUE_FIT_POLY: launch_decode_fit(ctx, d_in, bound, s); break;
     default: break;
   }
   if (im == GP_INDEX_NONE) launch_validate_support(ctx, bound, s);

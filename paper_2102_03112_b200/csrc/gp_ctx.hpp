@@ -94,7 +94,8 @@ struct Workspace {
   uint32_t* u32d = nullptr;       // generic [D]
   double* f64a = nullptr;         // [D]
   double* f64b = nullptr;         // [D]
-  double* partial = nullptr;      // fit partial sums [4096 * 32]
+  double* partial = nullptr;      // fit chunk partial sums [(D/2048 + 128) * 44]
+  uint32_t* sort_table = nullptr; // radix digit table [256 * (D/4096 + 2)]
   uint32_t* crc_part = nullptr;   // chunk CRCs [crc_cap]
   uint64_t crc_cap = 0;
   uint8_t* scratch = nullptr;     // generic byte scratch [2 * D]
@@ -166,6 +167,8 @@ void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t 
 void launch_gather_values(gp_ctx* ctx, const float* dense, uint64_t n_bound, cudaStream_t s);
 void launch_values_raw(gp_ctx* ctx, uint8_t* out, bool f64, uint64_t n_bound, cudaStream_t s);
 void launch_values_raw_check(gp_ctx* ctx, cudaStream_t s);
+void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, uint64_t n_bound, cudaStream_t s);
+void launch_decode_fit(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, cudaStream_t s);
 void launch_decode_scatter(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, float* dense, float scale,
                            uint32_t* out_support, double* out_values, uint64_t cap, uint64_t* d_count,
                            uint64_t* d_dim, cudaStream_t s);

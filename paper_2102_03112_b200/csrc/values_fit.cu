@@ -1,0 +1,600 @@
+// values_fit.cu — K11-K15: the piecewise-polynomial value codec
+// (value_compress / value_decompress, curvefit.cpp:26-174, :285-356, :388-542).
+//
+// Encode (values in ws.values, n = plan->n_values):
+//   fit_keys     : descending, stable sort keys (-0.0 canonicalised to +0.0, the
+//                  reference comparator treats them as equal) + sign split l
+//   radix sort   : 4 x 8-bit stable passes → map[sorted_pos] = original pos
+//   fit_prepare  : identity flag; folded sequence t (negatives reversed and
+//                  negated behind the sign split, curvefit.cpp:442-446)
+//   fit_segment  : greedy max-chord-deviation splitting per sign part, fp64
+//                  with no contraction and lowest-index ties (curvefit.cpp:50-99)
+//                  — bit-exact boundaries
+//   fit_accumulate / fit_solve : least squares of degree <= 7 per segment on
+//                  t in [-1, 1].  The reference solves the Vandermonde system
+//                  with Eigen's column-pivoted QR (curvefit.cpp:154); here the
+//                  normal equations are formed in the Legendre basis (Gram
+//                  matrix ~ diagonal, condition ~ 2*degree+1) with fixed-order
+//                  fp64 reductions, solved by Cholesky, mapped to t-monomials,
+//                  then expanded to x-monomials exactly as curvefit.cpp:157-172.
+//                  Coefficients agree with the reference within f32 rounding
+//                  (tolerance-checked).
+//   fit_emit / reorder_pack : serialize_fit + the bit-packed map
+// Decode: fit_parse (parse_fit + reorder checks), reorder_unpack (entries,
+// permutation check), fit_eval (fp64 Horner without FMA, sign unfold,
+// permutation scatter) — bit-exact for a given container.
+#include "gp_ctx.hpp"
+#include "gp_device.cuh"
+
+namespace gp {
+
+namespace {
+
+constexpr int kMaxDeg = 7;
+constexpr int kCps = kMaxDeg + 1;           // coefficient stride in Plan::coeffs
+constexpr int kChunk = 2048;                // points per accumulate block
+constexpr int kAcc = 36 + 8;                // Gram upper triangle (<= 36) + rhs (<= 8)
+
+__device__ __forceinline__ bool fit_active(const Plan* plan) {
+  return plan->value_method == GP_VALUE_FIT_POLY;
+}
+
+__global__ void fit_keys(const float* __restrict__ values, Plan* plan, uint32_t* __restrict__ keys,
+                         uint32_t* __restrict__ idx, const uint32_t* status) {
+  __shared__ uint32_t cnt;
+  if (failed(status) || !fit_active(plan)) return;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  const uint64_t n = plan->n_values;
+  uint32_t nonneg = 0;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const float v = values[i];
+    uint32_t b = __float_as_uint(v);
+    if (b == 0x80000000u) b = 0;  // -0.0 == +0.0 under operator>
+    const uint32_t asc = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+    keys[i] = ~asc;  // ascending key order == descending value order
+    idx[i] = static_cast<uint32_t>(i);
+    nonneg += v >= 0.0f ? 1u : 0u;
+  }
+  nonneg = warp_sum(nonneg);
+  if ((threadIdx.x & 31) == 0 && nonneg) atomicAdd(&cnt, nonneg);
+  __syncthreads();
+  if (threadIdx.x == 0 && cnt) atomicAdd(&plan->sign_split, cnt);
+}
+
+// t[s] and the identity flag; map = sorted idx
+__global__ void fit_prepare(const float* __restrict__ values, const uint32_t* __restrict__ map, Plan* plan,
+                            double* __restrict__ t, const uint32_t* status) {
+  if (failed(status) || !fit_active(plan)) return;
+  const uint64_t n = plan->n_values;
+  const uint64_t l = plan->sign_split;
+  bool ident = true;
+  for (uint64_t s = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; s < n;
+       s += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    if (map[s] != s) ident = false;
+    t[s] = s < l ? static_cast<double>(values[map[s]]) : -static_cast<double>(values[map[n - 1 - (s - l)]]);
+  }
+  if (__any_sync(kFull, !ident) && (threadIdx.x & 31) == 0) atomicAnd(&plan->identity, 0u);
+}
+
+// ---------------------------------------------------------------- segmentation
+struct Piece {
+  uint32_t begin, end, arg, live;
+  double dev;
+};
+
+// block-wide make_piece over t[base + begin, base + end) (curvefit.cpp:50-67)
+__device__ Piece make_piece(const double* __restrict__ t, uint32_t begin, uint32_t end, uint32_t mp,
+                            double* sdev, uint32_t* sarg) {
+  Piece p{begin, end, 0, 0, 0.0};
+  const uint32_t len = end - begin;
+  if (len < 3) return p;
+  const double y0 = t[begin];
+  const double slope = __ddiv_rn(__dsub_rn(t[end - 1], y0), static_cast<double>(len - 1));
+  double best = 0.0;
+  uint32_t arg = 0;
+  for (uint32_t i = begin + 1 + threadIdx.x; i + 1 < end; i += blockDim.x) {
+    const double pred = __dadd_rn(y0, __dmul_rn(slope, static_cast<double>(i - begin)));
+    const double e = __dsub_rn(t[i], pred);
+    const double d2 = __dmul_rn(e, e);
+    if (d2 > best) {  // strict: the first (lowest) index wins within a thread
+      best = d2;
+      arg = i;
+    }
+  }
+  // (max dev, min index among equals); threads with best == 0 never win ties
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(kFull, best, o);
+    const uint32_t oa = __shfl_xor_sync(kFull, arg, o);
+    if (ob > best || (ob == best && ob > 0.0 && oa < arg)) {
+      best = ob;
+      arg = oa;
+    }
+  }
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    sdev[warp] = best;
+    sarg[warp] = arg;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    uint32_t a = 0;
+    for (int w = 0; w < nw; ++w)
+      if (sdev[w] > b || (sdev[w] == b && b > 0.0 && sarg[w] < a)) {
+        b = sdev[w];
+        a = sarg[w];
+      }
+    sdev[32] = b;
+    sarg[32] = a;
+  }
+  __syncthreads();
+  p.dev = sdev[32];
+  p.arg = sarg[32];
+  __syncthreads();
+  p.live = (p.dev > 0.0 && p.arg - begin >= mp && end - p.arg >= mp) ? 1u : 0u;
+  return p;
+}
+
+// One block: both sign parts in order (the max_segments share of the last
+// part depends on the segments emitted for the first, curvefit.cpp:473-481).
+__global__ void __launch_bounds__(1024) fit_segment(Plan* plan, const double* __restrict__ t, int degree,
+                                                    int max_segments, uint32_t* status) {
+  __shared__ double sdev[33];
+  __shared__ uint32_t sarg[33];
+  __shared__ Piece pieces[kMaxSeg];
+  __shared__ int s_np, s_best, s_budget;
+  if (failed(status) || !fit_active(plan)) return;
+  const uint64_t n = plan->n_values;
+  const uint32_t l = plan->sign_split;
+  const uint32_t un = static_cast<uint32_t>(n);
+  uint32_t pb[2], pe[2];
+  int nparts = 0;
+  if (l > 0) {
+    pb[nparts] = 0;
+    pe[nparts++] = l;
+  }
+  if (l < un) {
+    pb[nparts] = l;
+    pe[nparts++] = un;
+  }
+  const uint32_t mp = static_cast<uint32_t>(degree + 1 > 1 ? degree + 1 : 1);
+  uint32_t nseg = 0;
+  for (int pi = 0; pi < nparts; ++pi) {
+    const uint32_t b = pb[pi], e = pe[pi], len = e - b;
+    if (threadIdx.x == 0) {
+      int budget;
+      if (max_segments > 0) {
+        const long long share = static_cast<long long>(max_segments) * static_cast<long long>(len) /
+                                static_cast<long long>(n);
+        budget = share > 1 ? static_cast<int>(share) : 1;
+        if (pi + 1 == nparts) budget = max_segments - static_cast<int>(nseg) > 1 ? max_segments - static_cast<int>(nseg) : 1;
+      } else if (len < 4) {
+        budget = 1;
+      } else {  // part_budget: knot_m + knot_count_linear (curvefit.cpp:101-110, :424-428)
+        const double km = fabs(__dsub_rn(__dsub_rn(t[b], t[b + 1]), __dsub_rn(t[e - 2], t[e - 1])));
+        const double p = ceil(2.0 * sqrt(km > 0.0 ? km : 0.0));
+        const int kc = static_cast<int>(p) > 1 ? static_cast<int>(p) : 1;
+        budget = kc + 1 < 0xffff ? kc + 1 : 0xffff;
+      }
+      s_budget = budget;
+    }
+    __syncthreads();
+    const int budget = s_budget;
+    // pieces are in part-local coordinates, stored shifted by b
+    Piece p0 = make_piece(t + b, 0, len, mp, sdev, sarg);
+    if (threadIdx.x == 0) {
+      pieces[0] = p0;
+      s_np = 1;
+    }
+    __syncthreads();
+    while (s_np < budget) {
+      if (threadIdx.x == 0) {
+        int best = -1;
+        for (int i = 0; i < s_np; ++i) {
+          if (!pieces[i].live) continue;
+          if (best < 0 || pieces[i].dev > pieces[best].dev ||
+              (pieces[i].dev == pieces[best].dev && pieces[i].begin < pieces[best].begin))
+            best = i;
+        }
+        s_best = best;
+      }
+      __syncthreads();
+      const int best = s_best;
+      if (best < 0) break;
+      if (s_np >= kMaxSeg || nseg + s_np >= kMaxSeg) {
+        if (threadIdx.x == 0) latch(status, GP_CAPACITY);
+        return;
+      }
+      const Piece pp = pieces[best];
+      const Piece left = make_piece(t + b, pp.begin, pp.arg, mp, sdev, sarg);
+      const Piece right = make_piece(t + b, pp.arg, pp.end, mp, sdev, sarg);
+      if (threadIdx.x == 0) {
+        pieces[best] = left;
+        pieces[s_np] = right;
+        s_np = s_np + 1;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      const int np = s_np;
+      // sort by begin (insertion) and append the bounds
+      for (int i = 1; i < np; ++i) {
+        const Piece v = pieces[i];
+        int j = i;
+        while (j > 0 && pieces[j - 1].begin > v.begin) {
+          pieces[j] = pieces[j - 1];
+          --j;
+        }
+        pieces[j] = v;
+      }
+      for (int i = 0; i < np; ++i) plan->seg_end[nseg + i] = b + pieces[i].end;
+    }
+    __syncthreads();
+    nseg += static_cast<uint32_t>(s_np);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    plan->nseg = nseg;
+    plan->degree = static_cast<uint32_t>(degree);
+  }
+}
+
+// ---------------------------------------------------------------- least squares
+__device__ __forceinline__ void seg_range(const Plan* plan, uint32_t s, uint32_t& b, uint32_t& e) {
+  b = s == 0 ? 0 : plan->seg_end[s - 1];
+  e = plan->seg_end[s];
+}
+
+// chunk c of the concatenated per-segment chunk lists → (segment, start)
+__device__ bool locate_chunk(const Plan* plan, uint64_t c, uint32_t& seg, uint32_t& start, uint32_t& stop) {
+  uint64_t acc = 0;
+  for (uint32_t s = 0; s < plan->nseg; ++s) {
+    uint32_t b, e;
+    seg_range(plan, s, b, e);
+    const uint64_t nc = (e - b + kChunk - 1) / kChunk;
+    if (c < acc + nc) {
+      seg = s;
+      start = b + static_cast<uint32_t>((c - acc) * kChunk);
+      stop = start + kChunk < e ? start + kChunk : e;
+      return true;
+    }
+    acc += nc;
+  }
+  return false;
+}
+
+__global__ void __launch_bounds__(256) fit_accumulate(const Plan* plan, const double* __restrict__ t,
+                                                      double* __restrict__ partial, const uint32_t* status) {
+  __shared__ double red[8][kAcc];
+  if (failed(status) || !fit_active(plan)) return;
+  uint32_t seg, start, stop;
+  if (!locate_chunk(plan, blockIdx.x, seg, start, stop)) return;
+  uint32_t b, e;
+  seg_range(plan, seg, b, e);
+  const uint32_t len = e - b;
+  const int deg = static_cast<int>(plan->degree);
+  const int eff = deg < static_cast<int>(len) - 1 ? deg : static_cast<int>(len) - 1;
+  double acc[kAcc];
+#pragma unroll
+  for (int j = 0; j < kAcc; ++j) acc[j] = 0.0;
+  if (len > 1) {
+    const double alpha = 2.0 / static_cast<double>(len - 1);
+    const double beta = -static_cast<double>(len + 1) / static_cast<double>(len - 1);
+    for (uint32_t i = start + threadIdx.x; i < stop; i += 256) {
+      const double x = alpha * static_cast<double>(i - b + 1) + beta;  // t in [-1, 1]
+      const double y = t[i];
+      double P[kCps];
+      P[0] = 1.0;
+      P[1] = x;
+#pragma unroll
+      for (int j = 1; j < kMaxDeg; ++j) P[j + 1] = ((2 * j + 1) * x * P[j] - j * P[j - 1]) / (j + 1);
+      int a = 0;
+#pragma unroll
+      for (int j = 0; j <= kMaxDeg; ++j)
+#pragma unroll
+        for (int q = j; q <= kMaxDeg; ++q, ++a)
+          if (q <= eff) acc[a] += P[j] * P[q];
+#pragma unroll
+      for (int j = 0; j <= kMaxDeg; ++j)
+        if (j <= eff) acc[36 + j] += P[j] * y;
+    }
+  }
+  // fixed-order reduction: warp tree, then warps in index order
+#pragma unroll
+  for (int j = 0; j < kAcc; ++j) {
+    double v = acc[j];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][j] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < kAcc) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v += red[w][threadIdx.x];
+    partial[static_cast<uint64_t>(blockIdx.x) * kAcc + threadIdx.x] = v;
+  }
+}
+
+// one block per segment; thread 0 solves (sizes are <= 8x8)
+__global__ void fit_solve(Plan* plan, const double* __restrict__ t, const double* __restrict__ partial,
+                          const uint32_t* status) {
+  if (failed(status) || !fit_active(plan)) return;
+  const uint32_t seg = blockIdx.x;
+  if (seg >= plan->nseg || threadIdx.x != 0) return;
+  uint32_t b, e;
+  seg_range(plan, seg, b, e);
+  const uint32_t len = e - b;
+  const int deg = static_cast<int>(plan->degree);
+  float* out = plan->coeffs + seg * kCps;
+  for (int j = 0; j <= deg; ++j) out[j] = 0.0f;
+  if (len == 1) {  // curvefit.cpp:134-138
+    out[0] = static_cast<float>(t[b]);
+    return;
+  }
+  const int eff = deg < static_cast<int>(len) - 1 ? deg : static_cast<int>(len) - 1;
+  const int m = eff + 1;
+  // chunk index range of this segment
+  uint64_t first = 0;
+  for (uint32_t s = 0; s < seg; ++s) {
+    uint32_t bb, ee;
+    seg_range(plan, s, bb, ee);
+    first += (ee - bb + kChunk - 1) / kChunk;
+  }
+  const uint64_t nc = (len + kChunk - 1) / kChunk;
+  double acc[kAcc];
+  for (int j = 0; j < kAcc; ++j) acc[j] = 0.0;
+  for (uint64_t c = 0; c < nc; ++c)
+    for (int j = 0; j < kAcc; ++j) acc[j] += partial[(first + c) * kAcc + j];
+  double G[kCps][kCps], rhs[kCps];
+  int a = 0;
+  for (int j = 0; j <= kMaxDeg; ++j)
+    for (int q = j; q <= kMaxDeg; ++q, ++a) {
+      if (j < m && q < m) G[j][q] = G[q][j] = acc[a];
+    }
+  for (int j = 0; j < m; ++j) rhs[j] = acc[36 + j];
+  // Cholesky G = L L^T (SPD: the Legendre columns are independent for len > eff)
+  double L[kCps][kCps] = {};
+  for (int j = 0; j < m; ++j) {
+    double s = G[j][j];
+    for (int q = 0; q < j; ++q) s -= L[j][q] * L[j][q];
+    L[j][j] = sqrt(s > 0.0 ? s : 0.0);
+    for (int i = j + 1; i < m; ++i) {
+      double v = G[i][j];
+      for (int q = 0; q < j; ++q) v -= L[i][q] * L[j][q];
+      L[i][j] = L[j][j] > 0.0 ? v / L[j][j] : 0.0;
+    }
+  }
+  double z[kCps], aL[kCps];
+  for (int i = 0; i < m; ++i) {
+    double v = rhs[i];
+    for (int q = 0; q < i; ++q) v -= L[i][q] * z[q];
+    z[i] = L[i][i] > 0.0 ? v / L[i][i] : 0.0;
+  }
+  for (int i = m - 1; i >= 0; --i) {
+    double v = z[i];
+    for (int q = i + 1; q < m; ++q) v -= L[q][i] * aL[q];
+    aL[i] = L[i][i] > 0.0 ? v / L[i][i] : 0.0;
+  }
+  // Legendre → t-monomials: P_{j+1} = ((2j+1) t P_j - j P_{j-1}) / (j+1)
+  double Lc[kCps][kCps] = {};
+  Lc[0][0] = 1.0;
+  if (m > 1) Lc[1][1] = 1.0;
+  for (int j = 1; j + 1 < m; ++j)
+    for (int p = 0; p <= j + 1; ++p)
+      Lc[j + 1][p] = ((2 * j + 1) * (p > 0 ? Lc[j][p - 1] : 0.0) - j * Lc[j - 1][p]) / (j + 1);
+  double ct[kCps];
+  for (int p = 0; p < m; ++p) {
+    double v = 0.0;
+    for (int j = p; j < m; ++j) v += aL[j] * Lc[j][p];
+    ct[p] = v;
+  }
+  // t-monomials → x-monomials, curvefit.cpp:157-172
+  const double alpha = 2.0 / static_cast<double>(len - 1);
+  const double beta = -static_cast<double>(len + 1) / static_cast<double>(len - 1);
+  double binom[kCps][kCps];
+  for (int j = 0; j < m; ++j) {
+    for (int k = 0; k <= j; ++k) binom[j][k] = 1.0;
+    for (int k = 1; k < j; ++k) binom[j][k] = binom[j - 1][k - 1] + binom[j - 1][k];
+  }
+  for (int k = 0; k < m; ++k) {
+    double c = 0.0;
+    const double ak = pow(alpha, static_cast<double>(k));
+    for (int j = k; j < m; ++j) c += ct[j] * binom[j][k] * ak * pow(beta, static_cast<double>(j - k));
+    out[k] = static_cast<float>(c);
+  }
+}
+
+// serialize_fit (curvefit.cpp:285-298) + reorder payload size; vl, rl, flags
+__global__ void fit_emit(Plan* plan, uint8_t* out, const uint32_t* status) {
+  if (failed(status) || !fit_active(plan) || threadIdx.x != 0) return;
+  const uint32_t S = plan->nseg, deg = plan->degree;
+  uint8_t* p = out + 49 + plan->il;
+  p[0] = 0;  // kind: piecewise polynomial
+  p[1] = static_cast<uint8_t>(S);
+  p[2] = static_cast<uint8_t>(S >> 8);
+  uint8_t* q = p + 3;
+  for (uint32_t s = 0; s < S; ++s, q += 4) st_u32_unaligned(q, plan->seg_end[s]);
+  *q++ = static_cast<uint8_t>(deg);
+  for (uint32_t s = 0; s < S; ++s)
+    for (uint32_t j = 0; j <= deg; ++j, q += 4) st_u32_unaligned(q, __float_as_uint(plan->coeffs[s * kCps + j]));
+  st_u32_unaligned(q, plan->sign_split);
+  plan->vl = 1 + 2 + 4ull * S + 1 + 4ull * S * (deg + 1) + 4;
+  uint32_t w = 0;
+  for (uint64_t x = plan->d - 1; x; x >>= 1) ++w;
+  plan->rl = plan->identity ? 0 : (plan->n_values * w + 7) / 8;
+}
+
+// reorder_encode (curvefit.cpp:332-340): entries of w bits, LSB-first
+__global__ void reorder_pack(const uint32_t* __restrict__ map, Plan* plan, uint8_t* out, const uint32_t* status) {
+  if (failed(status) || !fit_active(plan) || plan->identity) return;
+  const uint64_t rl = plan->rl, n = plan->n_values;
+  uint32_t w = 0;
+  for (uint64_t x = plan->d - 1; x; x >>= 1) ++w;
+  if (w == 0) return;
+  uint8_t* p = out + 49 + plan->il + plan->vl;
+  for (uint64_t byte = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; byte < rl;
+       byte += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint32_t v = 0;
+    uint64_t bit = 8 * byte;
+    int filled = 0;
+    while (filled < 8) {
+      const uint64_t e = bit / w;
+      if (e >= n) break;
+      const uint32_t off = static_cast<uint32_t>(bit - e * w);
+      const int take = static_cast<int>(w - off) < 8 - filled ? static_cast<int>(w - off) : 8 - filled;
+      v |= ((map[e] >> off) & ((1u << take) - 1u)) << filled;
+      filled += take;
+      bit += take;
+    }
+    p[byte] = static_cast<uint8_t>(v);
+  }
+}
+
+// ---------------------------------------------------------------- decode
+// parse_fit (curvefit.cpp:300-325), pipeline.cpp:117-118 trailing bytes, and
+// the reorder_decode length/slack rules (curvefit.cpp:342-356).
+__global__ void fit_parse(const uint8_t* __restrict__ in, Plan* plan, uint32_t* status) {
+  if (failed(status) || !fit_active(plan)) return;
+  const uint8_t* p = in + plan->off_value;
+  const uint64_t vl = plan->vl, count = plan->n_values;
+  if (vl < 1) return latch(status, GP_TRUNCATED);
+  if (p[0] > 1) return latch(status, GP_UNKNOWN_METHOD);
+  const uint8_t kind = p[0];
+  if (vl < 3) return latch(status, GP_TRUNCATED);
+  const uint32_t S = p[1] | (p[2] << 8);
+  if (S < 1) return latch(status, GP_CORRUPT_PAYLOAD);
+  uint32_t prev = 0;
+  for (uint32_t i = 0; i < S; ++i) {
+    if (vl < 3 + 4ull * (i + 1)) return latch(status, GP_TRUNCATED);
+    const uint32_t e = ld_u32_unaligned(p + 3 + 4 * i);
+    if (e <= prev && !(i == 0 && e > 0)) return latch(status, GP_CORRUPT_PAYLOAD);
+    prev = e;
+    if (i < kMaxSeg) plan->seg_end[i] = e;
+  }
+  if (prev != count) return latch(status, GP_CORRUPT_PAYLOAD);
+  uint64_t at = 3 + 4ull * S;
+  if (vl < at + 1) return latch(status, GP_TRUNCATED);
+  const uint32_t deg = p[at++];
+  const uint64_t cps = kind == 1 ? 4 : deg + 1;
+  if (vl < at + 4 * S * cps) return latch(status, GP_TRUNCATED);
+  const uint64_t coeff_at = at;
+  at += 4 * S * cps;
+  if (vl < at + 4) return latch(status, GP_TRUNCATED);
+  const uint32_t l = ld_u32_unaligned(p + at);
+  at += 4;
+  if (l > count) return latch(status, GP_CORRUPT_PAYLOAD);
+  if (l > 0 && l < count) {
+    bool found = false;
+    for (uint32_t i = 0; i < S; ++i) found |= ld_u32_unaligned(p + 3 + 4 * i) == l;
+    if (!found) return latch(status, GP_CORRUPT_PAYLOAD);
+  }
+  if (at != vl) return latch(status, GP_CORRUPT_PAYLOAD);
+  // reorder_decode structure: count entries of w bits, < 8 slack bits, zero slack
+  if (plan->rl) {
+    uint32_t w = 0;
+    for (uint64_t x = plan->d - 1; x; x >>= 1) ++w;
+    const uint64_t need = count * w, have = 8 * plan->rl;
+    if (have < need) return latch(status, GP_TRUNCATED);
+    if (have - need >= 8) return latch(status, GP_CORRUPT_PAYLOAD);
+    if (have > need) {
+      const uint8_t last = in[plan->off_reorder + plan->rl - 1];
+      if (last >> (need % 8)) return latch(status, GP_CORRUPT_PAYLOAD);
+    }
+  }
+  if (kind == 1) return latch(status, GP_UNSUPPORTED);  // dexp evaluation is out of scope
+  if (S > kMaxSeg || deg > kMaxDeg) return latch(status, GP_CAPACITY);
+  plan->nseg = S;
+  plan->degree = deg;
+  plan->sign_split = l;
+  for (uint32_t s = 0; s < S; ++s)
+    for (uint32_t j = 0; j <= deg; ++j)
+      plan->coeffs[s * kCps + j] = __uint_as_float(ld_u32_unaligned(p + coeff_at + 4 * (s * cps + j)));
+}
+
+// reorder entries (entry >= d → corrupt) + permutation check (curvefit.cpp:531-538)
+__global__ void reorder_unpack(const uint8_t* __restrict__ in, Plan* plan, uint32_t* __restrict__ map,
+                               uint32_t* seen, uint32_t* status) {
+  if (failed(status) || !fit_active(plan) || plan->rl == 0) return;
+  const uint64_t n = plan->n_values, d = plan->d;
+  uint32_t w = 0;
+  for (uint64_t x = d - 1; x; x >>= 1) ++w;
+  const uint8_t* p = in + plan->off_reorder;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint64_t v = 0;
+    const uint64_t bit0 = i * w;
+    for (uint32_t j = 0; j < w; ++j) {
+      const uint64_t bit = bit0 + j;
+      v |= static_cast<uint64_t>((p[bit >> 3] >> (bit & 7)) & 1u) << j;
+    }
+    if (v >= d || v >= n) {
+      latch(status, GP_CORRUPT_PAYLOAD);
+      continue;
+    }
+    map[i] = static_cast<uint32_t>(v);
+    if (atomicOr(&seen[v >> 5], 1u << (v & 31)) & (1u << (v & 31))) latch(status, GP_CORRUPT_PAYLOAD);
+  }
+}
+
+// value_decompress evaluate + unfold + scatter (curvefit.cpp:517-541)
+__global__ void fit_eval(const Plan* plan, const uint32_t* __restrict__ map, double* __restrict__ out,
+                         const uint32_t* status) {
+  __shared__ uint32_t bounds[kMaxSeg];
+  __shared__ float coeffs[kMaxSeg * kCps];
+  if (failed(status) || !fit_active(plan)) return;
+  const uint32_t S = plan->nseg, cps = plan->degree + 1;
+  for (uint32_t i = threadIdx.x; i < S; i += blockDim.x) bounds[i] = plan->seg_end[i];
+  for (uint32_t i = threadIdx.x; i < S * kCps; i += blockDim.x) coeffs[i] = plan->coeffs[i];
+  __syncthreads();
+  const uint64_t n = plan->n_values;
+  const uint64_t l = plan->sign_split;
+  const bool reorder = plan->rl != 0;
+  for (uint64_t s = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; s < n;
+       s += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t j = s < l ? s : l + (n - 1 - s);  // position in the folded sequence
+    uint32_t seg = 0;
+    while (bounds[seg] <= j) ++seg;
+    const uint32_t begin = seg == 0 ? 0 : bounds[seg - 1];
+    const double x = static_cast<double>(j - begin + 1);
+    const float* c = coeffs + seg * kCps;
+    double acc = 0.0;
+    for (int q = static_cast<int>(cps) - 1; q >= 0; --q) acc = __dadd_rn(__dmul_rn(acc, x), static_cast<double>(c[q]));
+    const double v = s < l ? acc : -acc;
+    out[reorder ? map[s] : s] = v;
+  }
+}
+
+}  // namespace
+
+void launch_radix_sort(gp_ctx* ctx, uint32_t* keys, uint32_t* vals, uint32_t* ktmp, uint32_t* vtmp,
+                       const uint64_t* n_dev, uint64_t n_bound, int bits, cudaStream_t s);
+
+__global__ void fit_reset(Plan* plan) {
+  plan->sign_split = 0;
+  plan->identity = 1;
+}
+
+void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, uint64_t n_bound, cudaStream_t s) {
+  Workspace& w = ctx->ws;
+  GP_LAUNCH(ctx, fit_reset, 1, 1, 0, s, w.plan);
+  GP_LAUNCH(ctx, fit_keys, grid_for(ctx, n_bound, 256), 256, 0, s, w.values, w.plan, w.u32a, w.u32b, w.status);
+  launch_radix_sort(ctx, w.u32a, w.u32b, w.u32c, w.u32d, &w.plan->n_values, n_bound, 32, s);
+  GP_LAUNCH(ctx, fit_prepare, grid_for(ctx, n_bound, 256), 256, 0, s, w.values, w.u32b, w.plan, w.f64b, w.status);
+  GP_LAUNCH(ctx, fit_segment, 1, 1024, 0, s, w.plan, w.f64b, degree, max_segments, w.status);
+  const uint64_t chunks = n_bound / kChunk + kMaxSeg + 1;
+  GP_LAUNCH(ctx, fit_accumulate, static_cast<int>(chunks), 256, 0, s, w.plan, w.f64b, w.partial, w.status);
+  GP_LAUNCH(ctx, fit_solve, kMaxSeg, 32, 0, s, w.plan, w.f64b, w.partial, w.status);
+  GP_LAUNCH(ctx, fit_emit, 1, 32, 0, s, w.plan, out, w.status);
+  GP_LAUNCH(ctx, reorder_pack, grid_for(ctx, n_bound * 4, 256), 256, 0, s, w.u32b, w.plan, out, w.status);
+}
+
+void launch_decode_fit(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, cudaStream_t s) {
+  Workspace& w = ctx->ws;
+  GP_LAUNCH(ctx, fit_parse, 1, 1, 0, s, in, w.plan, w.status);
+  cudaMemsetAsync(w.u32c, 0, ((n_bound + 31) / 32) * 4, s);
+  GP_LAUNCH(ctx, reorder_unpack, grid_for(ctx, n_bound, 256), 256, 0, s, in, w.plan, w.u32b, w.u32c, w.status);
+  GP_LAUNCH(ctx, fit_eval, grid_for(ctx, n_bound, 256), 256, 0, s, w.plan, w.u32b, w.f64a, w.status);
+}
+
+}  // namespace gp
