@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""bench.py — DeepReduce sparse-gradient encode → allgather → decode on B200.
+
+Metric (BASELINE.json): dense-gradient GB/s through encode+allgather+decode
+(whole job: N * 4d bytes / step time), plus bits per nonzero (volume()).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl native|reference]
+
+One process per GPU (torchrun for N > 1, NCCL).  A step on every rank:
+top_r + compress_gradient + pack of its own d-element f32 gradient (pipeline
+seed per (rank, step), harness.cpp:201-203), sizes-first NCCL allgather of
+the containers, decode of all N containers into the dense mean.
+
+value : device time with inputs resident in HBM, CUDA events on the step's
+        stream, L2 flushed (256 MiB write) between steps outside the events,
+        max over ranks.
+e2e   : the same step through the public API with HOST buffers: pinned H2D
+        of the gradient and D2H of the dense mean inside the timed region.
+roofline : the dominant stage from a profiled pass of the same K steps.
+cpu_baseline : the reference implementation (oracle/_ref, the reference's
+        own sources) — or the C restatement when _ref is absent — timed on
+        this box's host cores on a bounded sample (rank 0, N = 1).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "dense-gradient GB/s through encode+allgather+decode; bits per nonzero"
+
+CONFIGS = {
+    "c4": dict(workload="ResNet-50-sized 25.6M-element gradient, top-r 1%, bloom-filter P2 (eps=1e-3) + "
+                        "polynomial curve-fit (degree 5), encode+allgather+decode",
+               d=25_557_032, ratio=0.01, index=6, value=1, fpr=0.001, degree=5, max_segments=0, sparse=False),
+    "c4s": dict(workload="C4 stress point: bloom-filter P2 at eps=1e-2 + polynomial curve-fit",
+                d=25_557_032, ratio=0.01, index=6, value=1, fpr=0.01, degree=5, max_segments=0, sparse=False),
+    "c1": dict(workload="synthetic 1M-element gradient, top-r 1%, bloom-filter P0 (eps=1e-2) + polynomial "
+                        "curve-fit, single-worker round trip",
+               d=1_000_000, ratio=0.01, index=4, value=1, fpr=0.01, degree=5, max_segments=0, sparse=False),
+    "c2": dict(workload="ResNet-20-sized 0.27M-element gradient, top-r 1%, bitmap indices + raw f32 values",
+               d=269_722, ratio=0.01, index=1, value=0, fpr=0.01, degree=5, max_segments=0, sparse=False),
+    "c3": dict(workload="NCF-style natural sparsity (40% zero 64-wide rows), 32M elements, bitmap indices + "
+                        "raw f32 values (support = nonzeros)",
+               d=31_832_577, ratio=None, index=1, value=0, fpr=0.01, degree=5, max_segments=0, sparse=True),
+}
+METHOD_NAMES = {0: "none", 1: "bitmap", 2: "rle", 4: "bloom-p0", 5: "bloom-p1", 6: "bloom-p2", 7: "bloom-pd",
+                8: "bloom-naive"}
+VALUE_NAMES = {0: "raw-f32", 1: "fit-poly", 5: "raw-f64"}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        return float(p.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------- reference arm
+def cpu_codec():
+    from oracle.bindings import oracle, reference
+    ref = reference()
+    return (ref, "reference") if ref is not None else (oracle(), "port")
+
+
+def cpu_step(lib, g, r, cfg_c, dense64):
+    """One reference step: top_r + compress + pack, then unpack + decompress + to_dense."""
+    c = lib.encode_dense(g, r, cfg_c)
+    dense64[:] = 0.0
+    lib.decode_accumulate(c, dense64, 1.0)
+    return len(c)
+
+
+def run_cpu_sample(cfg, threads: int, shrink: int, steps: int, seed_step: int = 0):
+    """Times `steps` rounds of `threads` concurrent reference steps on d/shrink-element
+    gradients.  Returns (GB/s, seconds per round, sample description, bits/nnz)."""
+    from oracle.bindings import GpConfig
+    from paper_2102_03112_b200 import synth
+    from paper_2102_03112_b200.dp import pipeline_seed, ratio_r
+    lib, kind = cpu_codec()
+    d = cfg["d"] // shrink
+    grads = [synth.gradient(d, rank=t) for t in range(threads)]
+    rs = [ratio_r(d, cfg["ratio"]) if cfg["ratio"] else int(np.count_nonzero(g)) for g in grads]
+    denses = [np.zeros(d, np.float64) for _ in range(threads)]
+    sizes = [0] * threads
+
+    def work(t, step):
+        cc = GpConfig.make(cfg["index"], cfg["value"], fpr=cfg["fpr"], degree=cfg["degree"],
+                           max_segments=cfg["max_segments"], seed=pipeline_seed(1, t, step))
+        sizes[t] = cpu_step(lib, grads[t], rs[t], cc, denses[t])
+
+    times = []
+    for step in range(steps):
+        ths = [threading.Thread(target=work, args=(t, seed_step + step)) for t in range(threads)]
+        t0 = time.perf_counter()
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+        times.append(time.perf_counter() - t0)
+    sec = float(np.median(times))
+    gbs = threads * 4.0 * d / sec / 1e9
+    bits = 8.0 * sizes[0] / rs[0]
+    desc = (f"{threads} thread(s) x one full encode+decode step of a {d}-element gradient "
+            f"(d/{shrink} of the workload, r={rs[0]}), median of {steps}")
+    return gbs, sec, desc, kind, bits
+
+
+def reference_main(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    shrink = args.ref_shrink
+    for _ in range(args.warmup):
+        run_cpu_sample(cfg, threads, shrink, 1)
+    gbs, sec, desc, kind, bits = run_cpu_sample(cfg, threads, shrink, args.steps)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 6), "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
+        "data": "synthetic", "bits_per_nonzero": round(bits, 4),
+        "config": {"workload": cfg["workload"], "d": cfg["d"], "sample": desc},
+        "cpu_baseline": {"value": round(gbs, 6), "unit": "GB/s", "cores": threads, "kind": kind, "sample": desc},
+        "e2e": {"value": round(gbs, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------- native arm
+def native_main(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2102_03112_b200 import Codec, PipelineConfig, synth
+    from paper_2102_03112_b200.dp import SparseAllgather, ratio_r
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    d = cfg["d"]
+    g_host = synth.natural_sparse_gradient(d, rank) if cfg["sparse"] else synth.gradient(d, rank)
+    r = int(np.count_nonzero(g_host)) if cfg["ratio"] is None else ratio_r(d, cfg["ratio"])
+    pinned = torch.from_numpy(g_host).pin_memory()
+    grad = pinned.to(dev)
+    codec = Codec(max_d=d, device=local)
+    pcfg = PipelineConfig(index_method=cfg["index"], value_method=cfg["value"], fpr=cfg["fpr"],
+                          degree=cfg["degree"], max_segments=cfg["max_segments"])
+    ex = SparseAllgather(codec, d, r, pcfg)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for w in range(args.warmup):
+        ex.step(grad, step=w)
+    codec.status()
+
+    # ---- timed region: device time with inputs resident in HBM
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = codec.launches
+    barrier()
+    with ClockSampler(local) as clk:
+        wall0 = time.perf_counter()
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            evs[i][0].record(stream)
+            ex.step(grad, step=args.warmup + i)
+            evs[i][1].record(stream)
+        barrier()
+        wall = time.perf_counter() - wall0
+    codec.status()
+    launches = (codec.launches - launches0) // max(1, args.steps)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    t_ms = float(sum(step_ms)) / args.steps
+    if world > 1:
+        t = torch.tensor([t_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ms = float(t.item())
+    clocks = clk.summary()
+    length = int(ex.length.item())
+
+    # ---- profiled pass (same steps): per-stage CUDA events on the launch stream
+    codec.profile(True)
+    stage = {}
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        ex.step(grad, step=args.warmup + i)
+        for k, (ms, n) in codec.stage_times().items():
+            a = stage.setdefault(k, [0.0, 0])
+            a[0] += ms
+            a[1] += n
+    codec.profile(False)
+    prof_total = sum(v[0] for v in stage.values()) / args.steps
+
+    # ---- e2e: host gradient in, host dense mean out, through the public API
+    out_host = torch.empty(d, dtype=torch.float32).pin_memory()
+    e2e_ms = []
+    barrier()
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        gdev = pinned.to(dev, non_blocking=True)
+        dense = ex.step(gdev, step=args.warmup + i)
+        out_host.copy_(dense, non_blocking=True)
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_t = float(np.mean(e2e_ms))
+    if world > 1:
+        t = torch.tensor([e2e_t], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_t = float(t.item())
+
+    hbm, peak_kind = peaks()
+    value = world * 4.0 * d / (t_ms * 1e-3) / 1e9
+    e2e_value = world * 4.0 * d / (e2e_t * 1e-3) / 1e9
+
+    # roofline of the dominant stage: algorithmic HBM bytes per launch / its event time
+    per_launch = {k: (v[0] / v[1], v[1] / args.steps) for k, v in stage.items()}
+    algo_bytes = {
+        "topr": 4.0 * d,                      # the gradient must be read once
+        "bloom_scan": 4.0 * d * 0 + 4.0 * (2 * r),  # writes |P| keys (compute-bound)
+        "dec_bloom_scan": 4.0 * (2 * r),
+        "dec_scatter": 8.0 * r,
+        "pack_crc": float(length),
+        "dec_parse_crc": float(length),
+    }
+    dom = max(stage.items(), key=lambda kv: kv[1][0])[0] if stage else None
+    roof = None
+    if dom is not None:
+        ms_launch, _ = per_launch[dom]
+        ab = algo_bytes.get(dom)
+        achieved = (ab / (ms_launch * 1e-3) / 1e9) if ab else None
+        roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 3) if achieved else None,
+                "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 5) if achieved else None,
+                "traffic": None, "ms_per_launch": round(ms_launch, 5), "peak_kind": peak_kind}
+    step_hbm_bytes = 8.0 * d + 2.0 * world * length
+    step_roof = {"hbm_bytes": step_hbm_bytes, "t_roof_ms": step_hbm_bytes / (hbm * 1e9) * 1e3,
+                 "frac": round(step_hbm_bytes / (hbm * 1e9) / (t_ms * 1e-3), 5)}
+
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(t_ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 values, u32 keys, f64 fit", "data": "synthetic",
+        "bits_per_nonzero": round(8.0 * length / r, 4),
+        "config": {"workload": cfg["workload"], "d": d, "r": r, "index_method": METHOD_NAMES[cfg["index"]],
+                   "value_method": VALUE_NAMES[cfg["value"]], "fpr": cfg["fpr"], "degree": cfg["degree"],
+                   "container_bytes": length, "parallelism": f"dp{world}",
+                   "l2": "flushed between steps (256 MiB write outside the timed events)"},
+        "e2e": {"value": round(e2e_value, 4), "unit": "GB/s", "h2d_bytes_per_step": 4 * d,
+                "d2h_bytes_per_step": 4 * d, "ms_per_step": round(e2e_t, 4)},
+        "roofline": roof, "step_roofline": step_roof,
+        "stages_ms_per_step": {k: round(v[0] / args.steps, 5) for k, v in sorted(stage.items())},
+        "profiled_ms_per_step": round(prof_total, 4),
+        "gpu_launches": int(launches), "clocks": clocks, "wall_s_timed": round(wall, 4),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        gbs, sec, desc, kind, _ = run_cpu_sample(cfg, 1, 1, 1)
+        line["cpu_baseline"] = {"value": round(gbs, 6), "unit": "GB/s", "cores": 1, "kind": kind, "sample": desc,
+                                "seconds": round(sec, 3)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--ref-shrink", type=int, default=8, help="reference arm: d/shrink-element sample per thread")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return reference_main(args, cfg)
+    return native_main(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -84,6 +84,14 @@ GP_API int gp_ctx_status(gp_ctx* ctx, void* stream);
 /* Number of kernel launches this context has enqueued since creation. */
 GP_API uint64_t gp_ctx_launch_count(const gp_ctx* ctx);
 
+/* Stage profiling: with on != 0 every pipeline stage enqueued by this
+ * context is bracketed by CUDA events on its stream.  gp_ctx_stage_times
+ * synchronises, ADDS the elapsed ms and counts per stage into the caller's
+ * arrays (index = stage id, see gp_stage_name) and resets the record. */
+GP_API int gp_ctx_profile(gp_ctx* ctx, int on);
+GP_API int gp_ctx_stage_times(gp_ctx* ctx, double* ms, uint64_t* counts, int n_stages);
+GP_API const char* gp_stage_name(int stage);
+
 /* Upper bound of pack(compress_gradient(...)) for a gradient of d elements with
  * r kept (container.cpp:58-82 layout).  Host-only arithmetic. */
 GP_API uint64_t gp_max_container_bytes(uint64_t d, uint64_t r, const gp_pipeline_config* cfg);
@@ -119,6 +127,13 @@ GP_API int gp_decode_accumulate(gp_ctx* ctx, const uint8_t* d_container, uint64_
 GP_API int gp_decode_accumulate_hint(gp_ctx* ctx, const uint8_t* d_container, uint64_t len,
                               const gp_pipeline_config* hint, float* d_dense, uint64_t d,
                               float scale, void* stream);
+
+/* As gp_decode_accumulate_hint, with the container length read on the device
+ * from *d_len (e.g. the length word gp_encode_topr wrote); `cap` is the
+ * buffer capacity.  Fully asynchronous: no host round trip at all. */
+GP_API int gp_decode_accumulate_dlen(gp_ctx* ctx, const uint8_t* d_container, uint64_t cap,
+                                     const uint64_t* d_len, const gp_pipeline_config* hint,
+                                     float* d_dense, uint64_t d, float scale, void* stream);
 
 /* unpack + decompress_gradient to sparse form.  Writes up to cap entries of
  * support (u32) and values (f64) and the count to the device word *d_count.

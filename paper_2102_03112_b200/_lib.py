@@ -43,12 +43,16 @@ _SIGS = {
     "gp_last_error": ([_vp], C.c_char_p),
     "gp_ctx_status": ([_vp, _vp], C.c_int),
     "gp_ctx_launch_count": ([_vp], _u64),
+    "gp_ctx_profile": ([_vp, C.c_int], C.c_int),
+    "gp_ctx_stage_times": ([_vp, _P(C.c_double), _P(_u64), C.c_int], C.c_int),
+    "gp_stage_name": ([C.c_int], C.c_char_p),
     "gp_max_container_bytes": ([_u64, _u64, _P(GpConfig)], _u64),
     "gp_encode_topr": ([_vp, _vp, _u64, _u64, _P(GpConfig), _vp, _u64, _vp, _vp], C.c_int),
     "gp_encode_support": ([_vp, _vp, _u64, _vp, _u64, _P(GpConfig), _vp, _u64, _vp, _vp], C.c_int),
     "gp_decode_accumulate": ([_vp, _vp, _u64, _vp, _u64, C.c_float, _vp], C.c_int),
     "gp_decode_accumulate_hint": ([_vp, _vp, _u64, _P(GpConfig), _vp, _u64, C.c_float, _vp], C.c_int),
-    "gp_decode_sparse": ([_vp, _vp, _u64, _vp, _vp, _u64, _vp, _vp, _vp], C.c_int),
+    "gp_decode_accumulate_dlen": ([_vp, _vp, _u64, _vp, _P(GpConfig), _vp, _u64, C.c_float, _vp], C.c_int),
+    "gp_decode_sparse":([_vp, _vp, _u64, _vp, _vp, _u64, _vp, _vp, _vp], C.c_int),
     "gp_top_r": ([_vp, _vp, _u64, _u64, _vp, _vp, _vp], C.c_int),
     "gp_crc32c": ([_vp, _vp, _u64, _vp, _vp], C.c_int),
     "gp_bloom_positive_scan": ([_vp, _vp, _u64, _u64, _vp, _u64, _vp, _vp], C.c_int),

@@ -173,6 +173,23 @@ class Codec:
     def launches(self) -> int:
         return int(lib.gp_ctx_launch_count(self._ctx))
 
+    def profile(self, on: bool = True):
+        """Bracket every pipeline stage with CUDA events on its stream."""
+        self._raise(lib.gp_ctx_profile(self._ctx, 1 if on else 0))
+
+    def stage_times(self) -> dict:
+        """{stage: (total ms, launches)} recorded since the last call (synchronises)."""
+        n = 32
+        ms = (C.c_double * n)()
+        cnt = (C.c_uint64 * n)()
+        self._raise(lib.gp_ctx_stage_times(self._ctx, ms, cnt, n))
+        out = {}
+        for i in range(n):
+            name = lib.gp_stage_name(i)
+            if name and cnt[i]:
+                out[name.decode()] = (ms[i], int(cnt[i]))
+        return out
+
     # -------------------------------------------------------------- encode
     @staticmethod
     def max_container_bytes(d: int, r: int, cfg: PipelineConfig) -> int:
@@ -212,6 +229,14 @@ class Codec:
                           length: int | None = None, hint: PipelineConfig | None = None, stream=None):
         """Asynchronous unpack + decompress_gradient + dense[support] += scale * values."""
         assert dense.dtype == torch.float32 and dense.is_cuda and dense.is_contiguous()
+        if isinstance(length, torch.Tensor):  # device length word: fully asynchronous path
+            assert hint is not None, "a device-side length needs a dispatch hint"
+            c = hint.to_c()
+            rc = lib.gp_decode_accumulate_dlen(self._ctx, _ptr(container), container.numel(), _ptr(length),
+                                               C.byref(c), _ptr(dense), dense.numel(), float(scale),
+                                               _stream(stream))
+            self._raise(rc)
+            return
         n = container.numel() if length is None else length
         if hint is None:
             rc = lib.gp_decode_accumulate(self._ctx, _ptr(container), n, _ptr(dense), dense.numel(),

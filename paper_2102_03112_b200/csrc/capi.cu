@@ -28,6 +28,23 @@ int check_launch(gp_ctx* ctx, const char* what) {
   return GP_OK;
 }
 
+void stage_begin(gp_ctx* ctx, int stage, cudaStream_t s) {
+  Profiler& p = ctx->prof;
+  if (!p.on || p.next + 2 > p.pool.size()) return;
+  p.open_stage = stage;
+  p.open_event = p.next;
+  cudaEventRecord(p.pool[p.next++], s);
+}
+
+void stage_end(gp_ctx* ctx, cudaStream_t s) {
+  Profiler& p = ctx->prof;
+  if (!p.on || p.open_stage < 0) return;
+  cudaEventRecord(p.pool[p.next++], s);
+  p.stage.push_back(p.open_stage);
+  p.first.push_back(p.open_event);
+  p.open_stage = -1;
+}
+
 void reset_scan(gp_ctx* ctx, cudaStream_t s, uint64_t ntiles_bound) {
   Workspace& w = ctx->ws;
   const uint64_t n = ntiles_bound < w.tiles_cap ? ntiles_bound : w.tiles_cap;
@@ -210,6 +227,7 @@ int gp_ctx_create(int device, uint64_t max_d, gp_ctx** out) {
 
 void gp_ctx_destroy(gp_ctx* ctx) {
   if (!ctx) return;
+  for (auto& e : ctx->prof.pool) cudaEventDestroy(e);
   if (ctx->ws.base) cudaFree(ctx->ws.base);
   delete ctx;
 }
@@ -235,6 +253,48 @@ int gp_ctx_status(gp_ctx* ctx, void* stream) {
                      std::string("device: ") + (st < 11 ? names[st] : "unknown status"));
   }
   return GP_OK;
+}
+
+int gp_ctx_profile(gp_ctx* ctx, int on) {
+  if (!ctx) return GP_ERROR;
+  Profiler& p = ctx->prof;
+  if (on && p.pool.empty()) {
+    p.pool.resize(8192);
+    for (auto& e : p.pool)
+      if (cudaEventCreate(&e) != cudaSuccess) return set_error(ctx, GP_CUDA, "event pool");
+  }
+  p.on = on != 0;
+  p.next = 0;
+  p.stage.clear();
+  p.first.clear();
+  return GP_OK;
+}
+
+int gp_ctx_stage_times(gp_ctx* ctx, double* ms, uint64_t* counts, int n) {
+  if (!ctx) return GP_ERROR;
+  Profiler& p = ctx->prof;
+  if (!p.stage.empty()) {
+    if (cudaEventSynchronize(p.pool[p.next - 1]) != cudaSuccess) return set_error(ctx, GP_CUDA, "event sync");
+    for (size_t i = 0; i < p.stage.size(); ++i) {
+      float t = 0.0f;
+      cudaEventElapsedTime(&t, p.pool[p.first[i]], p.pool[p.first[i] + 1]);
+      if (p.stage[i] < n) {
+        if (ms) ms[p.stage[i]] += t;
+        if (counts) counts[p.stage[i]] += 1;
+      }
+    }
+  }
+  p.next = 0;
+  p.stage.clear();
+  p.first.clear();
+  return GP_OK;
+}
+
+const char* gp_stage_name(int stage) {
+  static const char* names[] = {"topr", "index", "bloom_build", "bloom_scan", "p2_sets", "p2_engine", "select",
+                                "gather", "values", "pack_crc", "dec_parse_crc", "dec_index", "dec_bloom_scan",
+                                "dec_p2_sets", "dec_p2_engine", "dec_select", "dec_values", "dec_scatter"};
+  return stage >= 0 && stage < ST_COUNT ? names[stage] : "";
 }
 
 int gp_bloom_params(double epsilon, uint64_t r, uint64_t* m, uint32_t* k) {
@@ -330,30 +390,32 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
     GP_LAUNCH(ctx, take_support, grid_for(ctx, r, 256), 256, 0, s, d_dense, d_support, r, d, ctx->ws.support,
               ctx->ws.values, ctx->ws.status);
   } else {
-    launch_top_r(ctx, d_dense, d, r, s);
+    GP_STAGE(ctx, ST_TOPR, s, launch_top_r(ctx, d_dense, d, r, s));
   }
   switch (im) {
     case GP_INDEX_NONE: launch_index_none(ctx, d_out, r, s); break;
     case GP_INDEX_BITMAP: launch_index_bitmap(ctx, d_out, d, r, s); break;
     default: {
-      launch_bloom_build(ctx, d_out, pi.m, r, s);
+      GP_STAGE(ctx, ST_BLOOM_BUILD, s, launch_bloom_build(ctx, d_out, pi.m, r, s));
       if (im == GP_INDEX_BLOOM_NAIVE) break;  // values stay in support order (pipeline.cpp:196-199)
-      launch_bloom_scan(ctx, d, pi.m, false, s);
+      GP_STAGE(ctx, ST_BLOOM_SCAN, s, launch_bloom_scan(ctx, d, pi.m, false, s));
       if (im == GP_INDEX_BLOOM_P2)
-        launch_select_p2(ctx, d, pi.m, pi.k, s);
+        launch_select_p2(ctx, d, pi.m, pi.k, false, s);
       else
-        launch_select_slice(ctx, d, s);
-      launch_gather_values(ctx, d_dense, d, s);
+        GP_STAGE(ctx, ST_SELECT, s, launch_select_slice(ctx, d, s));
+      GP_STAGE(ctx, ST_GATHER, s, launch_gather_values(ctx, d_dense, d, s));
     }
   }
   const uint64_t n_bound = im == GP_INDEX_BLOOM_P0 ? d : r;
   switch (vm) {
     case GP_VALUE_NONE:
     case GP_VALUE_RAW_F64: launch_values_raw(ctx, d_out, vm == GP_VALUE_RAW_F64, n_bound, s); break;
-    case GP_VALUE_FIT_POLY: launch_values_fit(ctx, d_out, cfg->degree, cfg->max_segments, n_bound, s); break;
+    case GP_VALUE_FIT_POLY:
+      GP_STAGE(ctx, ST_VALUES, s, launch_values_fit(ctx, d_out, cfg->degree, cfg->max_segments, n_bound, s));
+      break;
     default: break;
   }
-  launch_finish_container(ctx, d_out, cap, d_len, bound, s);
+  GP_STAGE(ctx, ST_PACK, s, launch_finish_container(ctx, d_out, cap, d_len, bound, s));
   return check_launch(ctx, "encode");
 }
 
@@ -369,7 +431,8 @@ int gp_encode_support(gp_ctx* ctx, const float* d_dense, uint64_t d, const uint3
   return encode_common(ctx, d_dense, d, d_support, r, cfg, d_out, cap, d_len, stream);
 }
 
-static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const gp_pipeline_config* hint,
+static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const uint64_t* d_len,
+                         const gp_pipeline_config* hint,
                          float* d_dense, uint64_t dense_d, float scale, uint32_t* d_support, double* d_values,
                          uint64_t cap, uint64_t* d_count, uint64_t* d_dim, void* stream) {
   if (!ctx || !d_in) return set_error(ctx, GP_ERROR, "decode: null argument");
@@ -391,7 +454,7 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const g
   }
   // parse + CRC verdict always run first: the reference reports header and
   // checksum errors before it looks at the method ids
-  launch_parse_container(ctx, d_in, len, hint ? &h : nullptr, s);
+  GP_STAGE(ctx, ST_DEC_PARSE, s, launch_parse_container(ctx, d_in, len, d_len, hint ? &h : nullptr, s));
   const int im = h.index_method, vm = h.value_method;
   const bool known = im <= GP_INDEX_BLOOM_NAIVE && vm <= GP_VALUE_RAW_F64;
   if (known && (!index_supported(im) || !value_supported(vm))) {
@@ -406,43 +469,51 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const g
     case GP_INDEX_NONE: launch_decode_index_none(ctx, d_in, bound, s); break;
     case GP_INDEX_BITMAP: launch_decode_index_bitmap(ctx, d_in, bound, s); break;
     default: {
-      launch_bloom_parse(ctx, d_in, ctx->ws.m_cap, s);
-      launch_bloom_scan(ctx, bound, 0, true, s);
+      GP_STAGE(ctx, ST_DEC_BLOOM_SCAN, s, launch_bloom_parse(ctx, d_in, ctx->ws.m_cap, s);
+                                           launch_bloom_scan(ctx, bound, 0, true, s));
       if (im == GP_INDEX_BLOOM_P2)
-        launch_select_p2(ctx, bound, ctx->ws.set_cap, 64, s);
+        launch_select_p2(ctx, bound, ctx->ws.set_cap, 64, true, s);
       else
-        launch_select_slice(ctx, bound, s);
+        GP_STAGE(ctx, ST_DEC_SELECT, s, launch_select_slice(ctx, bound, s));
     }
   }
   switch (vm) {
     case GP_VALUE_NONE:
     case GP_VALUE_RAW_F64: launch_values_raw_check(ctx, s); break;
-    case GP_VALUE_FIT_POLY: launch_decode_fit(ctx, d_in, bound, s); break;
+    case GP_VALUE_FIT_POLY: GP_STAGE(ctx, ST_DEC_VALUES, s, launch_decode_fit(ctx, d_in, bound, s)); break;
     default: break;
   }
   if (im == GP_INDEX_NONE) launch_validate_support(ctx, bound, s);
   (void)dense_d;
-  launch_decode_scatter(ctx, d_in, bound, d_dense, scale, d_support, d_values, cap, d_count, d_dim, s);
+  GP_STAGE(ctx, ST_DEC_SCATTER, s,
+           launch_decode_scatter(ctx, d_in, bound, d_dense, scale, d_support, d_values, cap, d_count, d_dim, s));
   return check_launch(ctx, "decode");
 }
 
 int gp_decode_accumulate(gp_ctx* ctx, const uint8_t* d_container, uint64_t len, float* d_dense, uint64_t d,
                          float scale, void* stream) {
-  return decode_common(ctx, d_container, len, nullptr, d_dense, d, scale, nullptr, nullptr, 0, nullptr, nullptr,
+  return decode_common(ctx, d_container, len, nullptr, nullptr, d_dense, d, scale, nullptr, nullptr, 0, nullptr,
+                       nullptr, stream);
+}
+
+int gp_decode_accumulate_dlen(gp_ctx* ctx, const uint8_t* d_container, uint64_t cap, const uint64_t* d_len,
+                              const gp_pipeline_config* hint, float* d_dense, uint64_t d, float scale, void* stream) {
+  if (!hint || !d_len) return set_error(ctx, GP_ERROR, "decode_accumulate_dlen: needs a hint and a length word");
+  return decode_common(ctx, d_container, cap, d_len, hint, d_dense, d, scale, nullptr, nullptr, 0, nullptr, nullptr,
                        stream);
 }
 
 int gp_decode_accumulate_hint(gp_ctx* ctx, const uint8_t* d_container, uint64_t len, const gp_pipeline_config* hint,
                               float* d_dense, uint64_t d, float scale, void* stream) {
-  return decode_common(ctx, d_container, len, hint, d_dense, d, scale, nullptr, nullptr, 0, nullptr, nullptr,
-                       stream);
+  return decode_common(ctx, d_container, len, nullptr, hint, d_dense, d, scale, nullptr, nullptr, 0, nullptr,
+                       nullptr, stream);
 }
 
 int gp_decode_sparse(gp_ctx* ctx, const uint8_t* d_container, uint64_t len, uint32_t* d_support, double* d_values,
                      uint64_t cap, uint64_t* d_count, uint64_t* d_dim, void* stream) {
   if (!d_support || !d_values) return set_error(ctx, GP_ERROR, "decode_sparse: null output");
-  return decode_common(ctx, d_container, len, nullptr, nullptr, 0, 0.0f, d_support, d_values, cap, d_count, d_dim,
-                       stream);
+  return decode_common(ctx, d_container, len, nullptr, nullptr, nullptr, 0, 0.0f, d_support, d_values, cap, d_count,
+                       d_dim, stream);
 }
 
 int gp_top_r(gp_ctx* ctx, const float* d_grad, uint64_t d, uint64_t r, uint32_t* d_support, float* d_values,

@@ -166,9 +166,12 @@ __global__ void finish_container(uint8_t* out, uint64_t cap, uint64_t* d_len, Pl
 }
 
 // unpack (container.cpp:84-127) up to, but not including, the CRC verdict.
-__global__ void parse_container(const uint8_t* __restrict__ in, uint64_t len, uint64_t max_d, Plan* plan,
-                                const gp_pipeline_config hint, int use_hint, uint32_t* status) {
+__global__ void parse_container(const uint8_t* __restrict__ in, uint64_t len_host, const uint64_t* len_dev,
+                                uint64_t max_d, Plan* plan, const gp_pipeline_config hint, int use_hint,
+                                uint32_t* status) {
   if (failed(status)) return;
+  const uint64_t len = len_dev ? *len_dev : len_host;
+  if (len_dev && len > len_host) return latch(status, GP_CAPACITY);  // len_host is the buffer capacity
   if (len < 4) return latch(status, GP_TRUNCATED);
   if (in[0] != 'D' || in[1] != 'R' || in[2] != 'C' || in[3] != '1') return latch(status, GP_CORRUPT_PAYLOAD);
   if (len < 6) return latch(status, GP_TRUNCATED);
@@ -237,12 +240,12 @@ void launch_finish_container(gp_ctx* ctx, uint8_t* out, uint64_t cap, uint64_t* 
   GP_LAUNCH(ctx, finish_container, 1, 32, 0, s, out, cap, d_len, w.plan, crc, w.status);
 }
 
-void launch_parse_container(gp_ctx* ctx, const uint8_t* in, uint64_t len, const gp_pipeline_config* hint,
-                            cudaStream_t s) {
+void launch_parse_container(gp_ctx* ctx, const uint8_t* in, uint64_t len, const uint64_t* len_dev,
+                            const gp_pipeline_config* hint, cudaStream_t s) {
   Workspace& w = ctx->ws;
   gp_pipeline_config h{};
   if (hint) h = *hint;
-  GP_LAUNCH(ctx, parse_container, 1, 1, 0, s, in, len, ctx->max_d, w.plan, h, hint ? 1 : 0, w.status);
+  GP_LAUNCH(ctx, parse_container, 1, 1, 0, s, in, len, len_dev, ctx->max_d, w.plan, h, hint ? 1 : 0, w.status);
   uint32_t* crc = reinterpret_cast<uint32_t*>(&w.plan->crc_calc);
   launch_crc_range(ctx, in, &w.plan->off_index, 0, &w.plan->il, &w.plan->vl, &w.plan->rl, 0, len, crc, s);
   GP_LAUNCH(ctx, verify_container, 1, 1, 0, s, w.plan, crc, w.status);

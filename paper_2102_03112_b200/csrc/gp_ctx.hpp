@@ -10,6 +10,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include <cuda_runtime.h>
 
@@ -103,6 +104,24 @@ struct Workspace {
 
 }  // namespace gp
 
+namespace gp {
+// Pipeline stages timed with CUDA events when profiling is on (gp_ctx_profile).
+enum Stage {
+  ST_TOPR, ST_INDEX, ST_BLOOM_BUILD, ST_BLOOM_SCAN, ST_P2_SETS, ST_P2_ENGINE, ST_SELECT, ST_GATHER, ST_VALUES,
+  ST_PACK, ST_DEC_PARSE, ST_DEC_INDEX, ST_DEC_BLOOM_SCAN, ST_DEC_P2_SETS, ST_DEC_P2_ENGINE, ST_DEC_SELECT,
+  ST_DEC_VALUES, ST_DEC_SCATTER, ST_COUNT
+};
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t next = 0;
+  std::vector<int> stage;   // per recorded pair
+  std::vector<size_t> first;
+  int open_stage = -1;
+  size_t open_event = 0;
+};
+}  // namespace gp
+
 struct gp_ctx {
   int device = 0;
   int sm_count = 148;
@@ -110,6 +129,7 @@ struct gp_ctx {
   gp::Workspace ws;
   std::string last_error;
   uint64_t launches = 0;
+  gp::Profiler prof;
 };
 
 namespace gp {
@@ -131,6 +151,15 @@ inline int grid_for(const gp_ctx* ctx, uint64_t n, int block) {
 }
 
 int set_error(gp_ctx* ctx, int code, const std::string& msg);
+void stage_begin(gp_ctx* ctx, int stage, cudaStream_t s);
+void stage_end(gp_ctx* ctx, cudaStream_t s);
+// Times `call` as `stage` when profiling is on (events on the launch stream).
+#define GP_STAGE(ctx, stage, s, call)         \
+  do {                                        \
+    ::gp::stage_begin((ctx), (stage), (s));   \
+    call;                                     \
+    ::gp::stage_end((ctx), (s));              \
+  } while (0)
 int check_launch(gp_ctx* ctx, const char* what);
 
 // ---- host launchers, grouped by translation unit ----
@@ -146,8 +175,8 @@ void launch_crc_range(gp_ctx* ctx, const uint8_t* base, const uint64_t* off_dev,
 void launch_crc_host_range(gp_ctx* ctx, const uint8_t* data, uint64_t n, uint32_t* out, cudaStream_t s);
 void launch_finish_container(gp_ctx* ctx, uint8_t* out, uint64_t cap, uint64_t* d_len, uint64_t len_bound,
                              cudaStream_t s);
-void launch_parse_container(gp_ctx* ctx, const uint8_t* in, uint64_t len, const gp_pipeline_config* hint,
-                            cudaStream_t s);
+void launch_parse_container(gp_ctx* ctx, const uint8_t* in, uint64_t len, const uint64_t* len_dev,
+                            const gp_pipeline_config* hint, cudaStream_t s);
 
 // indexcodec.cu
 void launch_index_none(gp_ctx* ctx, uint8_t* out, uint64_t r, cudaStream_t s);
@@ -161,7 +190,8 @@ void launch_bloom_build(gp_ctx* ctx, uint8_t* out, uint64_t m, uint64_t r, cudaS
 void launch_bloom_parse(gp_ctx* ctx, const uint8_t* in, uint64_t m_bound, cudaStream_t s);
 void launch_bloom_scan(gp_ctx* ctx, uint64_t d_bound, uint64_t m_host, bool decoding, cudaStream_t s);
 void launch_select_slice(gp_ctx* ctx, uint64_t n_bound, cudaStream_t s);
-void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t k_bound, cudaStream_t s);
+void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t k_bound, bool decoding,
+                      cudaStream_t s);
 
 // values.cu
 void launch_gather_values(gp_ctx* ctx, const float* dense, uint64_t n_bound, cudaStream_t s);

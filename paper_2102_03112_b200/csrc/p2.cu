@@ -347,8 +347,10 @@ __global__ void __launch_bounds__(kTileBlock) flags_compact(const uint32_t* __re
 
 }  // namespace
 
-void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t k_bound, cudaStream_t s) {
+void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t k_bound, bool decoding,
+                      cudaStream_t s) {
   Workspace& w = ctx->ws;
+  stage_begin(ctx, decoding ? ST_DEC_P2_SETS : ST_P2_SETS, s);
   const uint64_t m_cap = std::min<uint64_t>(m_bound, w.set_cap);
   cudaMemsetAsync(w.p2_count, 0, (m_cap + 1) * sizeof(uint32_t), s);
   cudaMemsetAsync(w.selbits, 0, ((n_bound + 31) / 32) * 4, s);
@@ -368,6 +370,8 @@ void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t 
   GP_LAUNCH(ctx, p2_table_scan, 1, 1024, 0, s, w.plan, w.p2_table, w.status);
   GP_LAUNCH(ctx, p2_size_scatter, tgrid, kTileBlock, 0, s, w.plan, w.p2_size, w.p2_table, w.p2_sets, w.status);
   GP_LAUNCH(ctx, p2_stage_a, 1, 1024, 0, s, w.plan, w.selbits, w.p2_table, w.status);
+  stage_end(ctx, s);
+  stage_begin(ctx, decoding ? ST_DEC_P2_ENGINE : ST_P2_ENGINE, s);
   const uint64_t bs_bytes = ((n_bound + 31) / 32) * 4;
   if (bs_bytes <= 200 * 1024) {
     static bool attr = false;
@@ -381,6 +385,7 @@ void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t 
     GP_LAUNCH(ctx, p2_engine<false>, 1, 32, 0, s, w.plan, w.p2_sets, w.p2_off, w.p2_size, w.p2_members,
               w.selbits, w.status);
   }
+  stage_end(ctx, s);
   const uint64_t ptiles = (n_bound + kTile - 1) / kTile;
   reset_scan(ctx, s, ptiles + 1);
   GP_LAUNCH(ctx, flags_compact, grid_for(ctx, ptiles * kTileBlock, kTileBlock), kTileBlock, 0, s, w.pos, w.selbits,
