@@ -108,8 +108,6 @@ __global__ void take_support(const float* __restrict__ dense, const uint32_t* __
   }
 }
 
-uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
-
 // ---------------------------------------------------------------- workspace
 struct Carver {
   uint8_t* base;
@@ -151,6 +149,7 @@ void carve(Workspace& w, uint8_t* base, uint64_t D) {
   w.p2_table = c.take<uint32_t>(256 * (w.set_cap / 4096 + 1) + 256);
   w.pairs = c.take<uint32_t>(w.pair_cap);
   w.p2_members = c.take<uint32_t>(w.pair_cap);
+  w.first_touch = c.take<uint32_t>(D);
   w.u32a = c.take<uint32_t>(D);
   w.u32b = c.take<uint32_t>(D);
   w.u32c = c.take<uint32_t>(D);
@@ -159,8 +158,10 @@ void carve(Workspace& w, uint8_t* base, uint64_t D) {
   w.f64b = c.take<double>(D);
   w.partial = c.take<double>((D / 2048 + 128) * 44);
   w.sort_table = c.take<uint32_t>(256 * (D / 4096 + 2));
-  w.crc_cap = (64 * D + (1 << 20)) / (256 * 1024) + 64;
-  w.crc_part = c.take<uint32_t>(w.crc_cap);
+  w.crc_cap = 2 * ((64 * D + (1 << 20)) / (64 * 256) + 64);
+  w.crc_part = c.take<uint32_t>(64);
+  w.crc_digits = c.take<uint32_t>(5 * 256);
+  w.crc_acc = c.take<uint32_t>(64);
   w.scratch = c.take<uint8_t>(2 * D);
   w.bytes_total = c.off;
 }

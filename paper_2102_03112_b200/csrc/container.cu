@@ -20,7 +20,6 @@ namespace gp {
 namespace {
 
 constexpr uint32_t kPoly = 0x82F63B78u;
-constexpr int kChunk = 1024;
 constexpr int kCrcBlock = 256;
 
 __device__ __forceinline__ uint32_t multmodp(uint32_t a, uint32_t b) {
@@ -37,101 +36,100 @@ __device__ __forceinline__ uint32_t multmodp(uint32_t a, uint32_t b) {
   return p;
 }
 
-// x^(8 n) mod P via square-and-multiply on x^(2^k)
-__device__ uint32_t x8nmodp(uint64_t n) {
-  uint32_t p = 1u << 31;      // x^0
-  uint32_t sq = 1u << 23;     // x^8
-  while (n) {
-    if (n & 1) p = multmodp(sq, p);
-    sq = multmodp(sq, sq);
-    n >>= 1;
-  }
-  return p;
+// CRC-32C is linear over GF(2): with R(M) the raw register (init 0, no
+// xorout) and S_L(c) = c * x^(8L) mod P,
+//   crc(M) = XOR_q S_{after(q)}(R(C_q)) ^ S_{|M|}(0xFFFFFFFF) ^ 0xFFFFFFFF
+// for any chunking M = C_0 ... C_{n-1}, after(q) = bytes following chunk q.
+// Every thread folds one aligned 64-byte chunk (slice-by-4 tables), shifts it
+// to the end of the range with x^(8L) = prod_i T_i[byte i of L] (byte-digit
+// operator tables, 5 x 256 words, built on the host), and the chunks
+// XOR-reduce — no combine tree, no sequential merge.
+__device__ __forceinline__ uint64_t range_len(const uint64_t* len_a, const uint64_t* len_b, const uint64_t* len_c,
+                                              uint64_t len_h) {
+  return len_a ? (*len_a + (len_b ? *len_b : 0) + (len_c ? *len_c : 0)) : len_h;
 }
 
-__device__ __forceinline__ uint32_t crc_combine(uint32_t a, uint32_t b, uint64_t len_b) {
-  return multmodp(x8nmodp(len_b), a) ^ b;
+__device__ __forceinline__ uint32_t shift_op(const uint32_t (*D)[256], uint64_t L) {
+  uint32_t op = 1u << 31;  // x^0
+  for (int i = 0; L; ++i, L >>= 8)
+    if (L & 0xFF) op = multmodp(D[i][L & 0xFF], op);
+  return op;
 }
 
-__device__ void load_table(uint32_t* t) {
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-    uint32_t c = static_cast<uint32_t>(i);
-    for (int j = 0; j < 8; ++j) c = (c >> 1) ^ ((c & 1u) ? kPoly : 0u);
-    t[i] = c;
-  }
-  __syncthreads();
-}
-
-// Per block: 256 chunks of 1 KiB.  Writes the block CRC to part[blockIdx].
-// The range is [base + off, base + off + len) with off/len from device words.
 __global__ void __launch_bounds__(kCrcBlock) crc_chunks(const uint8_t* __restrict__ base, const uint64_t* off_p,
                                                         uint64_t off_h, const uint64_t* len_a, const uint64_t* len_b,
-                                                        const uint64_t* len_c, uint64_t len_h, uint32_t* part,
-                                                        const uint32_t* status) {
-  __shared__ uint32_t table[256];
-  __shared__ uint32_t crc_s[kCrcBlock];
-  __shared__ uint64_t len_s[kCrcBlock];
+                                                        const uint64_t* len_c, uint64_t len_h,
+                                                        const uint32_t* __restrict__ digits, uint32_t* acc,
+                                                        uint32_t* done, uint32_t* out, const uint32_t* status) {
+  __shared__ uint32_t T[4][256];
+  __shared__ uint32_t D[5][256];
+  __shared__ uint32_t red[kCrcBlock / 32];
+  __shared__ bool last;
   if (failed(status)) return;
-  load_table(table);
+  for (int i = threadIdx.x; i < 256; i += kCrcBlock) {
+    uint32_t c = static_cast<uint32_t>(i);
+    for (int j = 0; j < 8; ++j) c = (c >> 1) ^ ((c & 1u) ? kPoly : 0u);
+    T[0][i] = c;
+  }
+  for (int i = threadIdx.x; i < 5 * 256; i += kCrcBlock) D[i / 256][i % 256] = digits[i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += kCrcBlock) {
+    uint32_t c = T[0][i];
+    for (int k = 1; k < 4; ++k) {
+      c = (c >> 8) ^ T[0][c & 0xFFu];
+      T[k][i] = c;
+    }
+  }
+  __syncthreads();
   const uint64_t off = off_p ? *off_p : off_h;
-  const uint64_t len = len_a ? (*len_a + (len_b ? *len_b : 0) + (len_c ? *len_c : 0)) : len_h;
-  const uint64_t nblocks = (len + static_cast<uint64_t>(kChunk) * kCrcBlock - 1) / (static_cast<uint64_t>(kChunk) * kCrcBlock);
-  const uint8_t* data = base + off;
-  for (uint64_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
-    const uint64_t start = (blk * kCrcBlock + threadIdx.x) * static_cast<uint64_t>(kChunk);
-    const uint64_t end = start + kChunk < len ? start + kChunk : len;
-    uint32_t c = 0xFFFFFFFFu;
-    for (uint64_t i = start; i < end; ++i) c = (c >> 8) ^ table[(c ^ data[i]) & 0xFFu];
-    crc_s[threadIdx.x] = start < end ? (c ^ 0xFFFFFFFFu) : 0u;
-    len_s[threadIdx.x] = start < end ? end - start : 0;
-    __syncthreads();
-    for (int stride = 1; stride < kCrcBlock; stride <<= 1) {
-      const int i = threadIdx.x;
-      if ((i % (2 * stride)) == 0 && i + stride < kCrcBlock) {
-        const uint64_t lb = len_s[i + stride];
-        if (lb) crc_s[i] = crc_combine(crc_s[i], crc_s[i + stride], lb);
-        len_s[i] += lb;
+  const uint64_t len = range_len(len_a, len_b, len_c, len_h);
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(base + off);
+  const uintptr_t a1 = a0 + len;
+  const uintptr_t c0 = a0 & ~static_cast<uintptr_t>(63);
+  const uint64_t nchunks = len ? (a1 - c0 + 63) / 64 : 0;
+  uint32_t x = 0;
+  for (uint64_t q = blockIdx.x * static_cast<uint64_t>(kCrcBlock) + threadIdx.x; q < nchunks;
+       q += static_cast<uint64_t>(gridDim.x) * kCrcBlock) {
+    const uintptr_t cs = c0 + 64 * q;
+    const uintptr_t lo = cs < a0 ? a0 : cs, hi = cs + 64 > a1 ? a1 : cs + 64;
+    uint32_t c = 0;  // raw register, init 0
+    if (lo == cs && hi == cs + 64) {
+      const uint4* p4 = reinterpret_cast<const uint4*>(cs);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint4 v = p4[k];
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          c ^= w[j];
+          c = T[3][c & 0xFFu] ^ T[2][(c >> 8) & 0xFFu] ^ T[1][(c >> 16) & 0xFFu] ^ T[0][c >> 24];
+        }
       }
-      __syncthreads();
+    } else {
+      const uint8_t* b = reinterpret_cast<const uint8_t*>(lo);
+      for (uintptr_t i = 0; i < hi - lo; ++i) c = (c >> 8) ^ T[0][(c ^ b[i]) & 0xFFu];
     }
-    if (threadIdx.x == 0) part[blk] = crc_s[0];
-    __syncthreads();
+    const uint64_t after = a1 - hi;
+    x ^= after ? multmodp(shift_op(D, after), c) : c;
   }
-}
-
-__global__ void __launch_bounds__(1024) crc_merge(const uint32_t* __restrict__ part, const uint64_t* len_a,
-                                                  const uint64_t* len_b, const uint64_t* len_c, uint64_t len_h,
-                                                  uint32_t* out, const uint32_t* status) {
-  __shared__ uint32_t crc_s[1024];
-  __shared__ uint64_t len_s[1024];
-  if (failed(status)) return;
-  const uint64_t len = len_a ? (*len_a + (len_b ? *len_b : 0) + (len_c ? *len_c : 0)) : len_h;
-  const uint64_t span = static_cast<uint64_t>(kChunk) * kCrcBlock;
-  const uint64_t nblocks = (len + span - 1) / span;
-  uint32_t acc = 0;
-  uint64_t acc_len = 0;
-  // fold 1024-wide groups of block CRCs left to right
-  for (uint64_t g = 0; g < nblocks; g += 1024) {
-    const uint64_t b = g + threadIdx.x;
-    crc_s[threadIdx.x] = b < nblocks ? part[b] : 0u;
-    len_s[threadIdx.x] = b < nblocks ? (b + 1 < nblocks ? span : len - b * span) : 0;
-    __syncthreads();
-    for (int stride = 1; stride < 1024; stride <<= 1) {
-      const int i = threadIdx.x;
-      if ((i % (2 * stride)) == 0 && i + stride < 1024) {
-        const uint64_t lb = len_s[i + stride];
-        if (lb) crc_s[i] = crc_combine(crc_s[i], crc_s[i + stride], lb);
-        len_s[i] += lb;
-      }
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-      acc = acc_len ? crc_combine(acc, crc_s[0], len_s[0]) : crc_s[0];
-      acc_len += len_s[0];
-    }
-    __syncthreads();
+  for (int o = 16; o > 0; o >>= 1) x ^= __shfl_xor_sync(kFull, x, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t y = 0;
+    for (int w = 0; w < kCrcBlock / 32; ++w) y ^= red[w];
+    if (y) atomicXor(acc, y);
+    __threadfence();
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
   }
-  if (threadIdx.x == 0) *out = len == 0 ? 0u : acc;
+  __syncthreads();
+  if (last && threadIdx.x == 0) {  // the final block folds in the init term
+    __threadfence();
+    const uint32_t raw = *reinterpret_cast<volatile uint32_t*>(acc);
+    *out = len ? (raw ^ multmodp(shift_op(D, len), 0xFFFFFFFFu) ^ 0xFFFFFFFFu) : 0u;
+    *acc = 0;   // ready for the next range
+    *done = 0;
+  }
 }
 
 // Header (container.cpp:62-73) + CRC trailer (:77-80); lengths from the plan.
@@ -224,12 +222,38 @@ void launch_crc_range(gp_ctx* ctx, const uint8_t* base, const uint64_t* off_dev,
                       const uint64_t* la, const uint64_t* lb, const uint64_t* lc, uint64_t len_host,
                       uint64_t len_bound, uint32_t* out, cudaStream_t s) {
   Workspace& w = ctx->ws;
-  const uint64_t span = static_cast<uint64_t>(kChunk) * kCrcBlock;
-  const uint64_t nblocks = std::max<uint64_t>(1, (len_bound + span - 1) / span);
-  const int grid = static_cast<int>(std::min<uint64_t>(nblocks, static_cast<uint64_t>(ctx->sm_count) * 8));
-  GP_LAUNCH(ctx, crc_chunks, grid, kCrcBlock, 0, s, base, off_dev, off_host, la, lb, lc, len_host, w.crc_part,
-            w.status);
-  GP_LAUNCH(ctx, crc_merge, 1, 1024, 0, s, w.crc_part, la, lb, lc, len_host, out, w.status);
+  if (!w.crc_ready) {  // byte-digit shift operators D[i][b] = x^(8 * b * 256^i) mod P
+    auto mult = [](uint32_t a, uint32_t b) {
+      uint32_t m = 1u << 31, p = 0;
+      for (;;) {
+        if (a & m) {
+          p ^= b;
+          if ((a & (m - 1)) == 0) break;
+        }
+        m >>= 1;
+        b = (b & 1) ? (b >> 1) ^ kPoly : b >> 1;
+      }
+      return p;
+    };
+    uint32_t tab[5 * 256];
+    uint32_t unit = 1u << 23;  // x^8: one byte
+    for (int i = 0; i < 5; ++i) {
+      uint32_t p = 1u << 31;
+      for (int b = 0; b < 256; ++b) {
+        tab[i * 256 + b] = p;
+        p = mult(unit, p);
+      }
+      unit = p;  // x^(8 * 256^(i+1))
+    }
+    cudaMemcpy(w.crc_digits, tab, sizeof(tab), cudaMemcpyHostToDevice);
+    cudaMemset(w.crc_acc, 0, 2 * sizeof(uint32_t));
+    w.crc_ready = true;
+  }
+  const uint64_t nchunks = (len_bound + 127) / 64;
+  const int grid = static_cast<int>(std::max<uint64_t>(
+      1, std::min<uint64_t>((nchunks + kCrcBlock - 1) / kCrcBlock, static_cast<uint64_t>(ctx->sm_count) * 4)));
+  GP_LAUNCH(ctx, crc_chunks, grid, kCrcBlock, 0, s, base, off_dev, off_host, la, lb, lc, len_host, w.crc_digits,
+            w.crc_acc, w.crc_acc + 1, out, w.status);
 }
 
 void launch_finish_container(gp_ctx* ctx, uint8_t* out, uint64_t cap, uint64_t* d_len, uint64_t len_bound,

@@ -81,6 +81,7 @@ struct Workspace {
   uint32_t* p2_sets = nullptr;    // [set_cap]
   uint32_t* p2_table = nullptr;   // [256 * set_cap / 4096 + 256]
   uint32_t* p2_members = nullptr; // [pair_cap]
+  uint32_t* first_touch = nullptr; // per-P earliest visit of a window [D]
   uint32_t* bucket = nullptr;     // per-bit counters [m_cap + 1]
   uint32_t* bucket_off = nullptr; // per-bit offsets [m_cap + 1]
   uint32_t* pairs = nullptr;      // conflict pairs [pair_cap]
@@ -97,7 +98,10 @@ struct Workspace {
   double* f64b = nullptr;         // [D]
   double* partial = nullptr;      // fit chunk partial sums [(D/2048 + 128) * 44]
   uint32_t* sort_table = nullptr; // radix digit table [256 * (D/4096 + 2)]
-  uint32_t* crc_part = nullptr;   // chunk CRCs [crc_cap]
+  uint32_t* crc_part = nullptr;   // (unused)
+  uint32_t* crc_digits = nullptr; // CRC shift-operator digit tables [5 * 256]
+  uint32_t* crc_acc = nullptr;    // XOR accumulator + block counter [2]
+  bool crc_ready = false;
   uint64_t crc_cap = 0;
   uint8_t* scratch = nullptr;     // generic byte scratch [2 * D]
 };
@@ -192,6 +196,10 @@ void launch_bloom_scan(gp_ctx* ctx, uint64_t d_bound, uint64_t m_host, bool deco
 void launch_select_slice(gp_ctx* ctx, uint64_t n_bound, cudaStream_t s);
 void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t k_bound, bool decoding,
                       cudaStream_t s);
+
+// sort.cu
+void launch_table_scan(gp_ctx* ctx, uint32_t* table, const uint64_t* n_dev, uint64_t n_bound, int tile_shift,
+                       cudaStream_t s);
 
 // values.cu
 void launch_gather_values(gp_ctx* ctx, const float* dense, uint64_t n_bound, cudaStream_t s);

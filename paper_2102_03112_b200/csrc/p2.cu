@@ -137,7 +137,7 @@ __global__ void p2_dedupe(const Plan* plan, const uint32_t* __restrict__ off, ui
     for (uint32_t i = 1; i < n; ++i)
       if (mem[i] != mem[u - 1]) mem[u++] = mem[i];
     size[b] = u;
-    if (u > kMaxSetSize) latch(status, GP_CAPACITY);
+    if (u >= kMaxSetSize) latch(status, GP_CAPACITY);
     if (u == 1) atomicOr(&selbits[mem[0] >> 5], 1u << (mem[0] & 31));
   }
 }
@@ -167,23 +167,13 @@ __global__ void __launch_bounds__(kTileBlock) p2_size_hist(const Plan* plan, con
   }
 }
 
-// ... exclusive scan of the digit-major table (one block) ...
-__global__ void __launch_bounds__(1024) p2_table_scan(Plan* plan, uint32_t* table, const uint32_t* status) {
-  __shared__ uint64_t sh[40];
-  if (failed(status) || !p2_active(plan)) return;
-  const uint64_t m = plan->m;
-  const uint64_t ntiles = (m + kTile - 1) / kTile;
-  const uint64_t n = 256 * ntiles;
-  uint64_t carry = 0;
-  for (uint64_t base = 0; base < n; base += 1024) {
-    const uint64_t i = base + threadIdx.x;
-    const uint64_t v = i < n ? table[i] : 0;
-    uint64_t tot;
-    const uint64_t ex = block_exclusive_sum<uint64_t, 1024>(v, sh, tot);
-    if (i < n) table[i] = static_cast<uint32_t>(carry + ex);
-    carry += tot;
-  }
-  if (threadIdx.x == 0) plan->n_sets = carry;
+// n_sets = total over the digit table (last digit's exclusive prefix + its count
+// is not stored, so count it from the sizes' last tile instead: the table is
+// exclusive, total = table[255][last] + h[255][last]; size 255 never occurs).
+__global__ void p2_count_sets(Plan* plan, const uint32_t* __restrict__ table, const uint32_t* status) {
+  if (failed(status) || !p2_active(plan) || threadIdx.x != 0) return;
+  const uint64_t ntiles = (plan->m + kTile - 1) / kTile;
+  plan->n_sets = table[255 * ntiles + ntiles - 1];  // digit 255 is empty: its prefix is the grand total
 }
 
 // ... and the stable downsweep: sets[table[digit][tile] + rank] = bit.
@@ -315,6 +305,181 @@ __global__ void __launch_bounds__(32) p2_engine(Plan* plan, const uint32_t* __re
   if (lane == 0) plan->n_sel = nsel;
 }
 
+// Stage B, windowed: 1024 consecutive visits per round, one thread each.
+// Every visit counts its unselected members against the selection at the
+// window start and registers them with atomicMin(first_touch[p], v).  A visit
+// is dependent iff an earlier visit of the window shares an unselected member
+// (only then can an earlier selection change its outcome).  Visits before the
+// first dependent one are exact: their RNG positions are a prefix sum of the
+// draw flags (a rejected draw ends the window right after its visit), their
+// selections are committed together, and the r cut stops the commit at the
+// selection that reaches r.  The next window starts at the first uncommitted
+// visit, so every round commits >= 1 visit and the result equals the
+// sequential loop of bloom.cpp:198-219 bit for bit.
+template <bool kSmem>
+__device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __restrict__ sets,
+                                               const uint32_t* __restrict__ off, const uint32_t* __restrict__ size,
+                                               const uint32_t* __restrict__ members, uint32_t* selbits,
+                                               uint32_t* first_touch, uint32_t* status);
+
+template <bool kSmem>
+__global__ void __launch_bounds__(1024) p2_engine_win(Plan* plan, const uint32_t* __restrict__ sets,
+                                                      const uint32_t* __restrict__ off,
+                                                      const uint32_t* __restrict__ size,
+                                                      const uint32_t* __restrict__ members, uint32_t* selbits,
+                                                      uint32_t* first_touch, uint32_t* status) {
+  p2_engine_body<kSmem>(plan, sets, off, size, members, selbits, first_touch, status);
+}
+
+template <bool kSmem>
+__device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __restrict__ sets,
+                                                      const uint32_t* __restrict__ off,
+                                                      const uint32_t* __restrict__ size,
+                                                      const uint32_t* __restrict__ members, uint32_t* selbits,
+                                                      uint32_t* first_touch, uint32_t* status) {
+  extern __shared__ uint32_t sbits[];
+  __shared__ uint64_t sh[40];
+  __shared__ uint32_t s_min[32];
+  __shared__ uint32_t s_val;
+  if (failed(status) || !p2_active(plan)) return;
+  constexpr uint32_t W = 1024;
+  const uint32_t v = threadIdx.x;
+  const uint64_t n = plan->n_pos, r = plan->r;
+  const uint64_t nwords = (n + 31) / 32;
+  uint32_t* bits = kSmem ? sbits : selbits;
+  const bool fallback = plan->n_single_sel > r;
+  if (kSmem || fallback)
+    for (uint64_t w = v; w < nwords; w += W) bits[w] = fallback ? 0u : selbits[w];
+  __syncthreads();
+  uint64_t nsel = fallback ? 0 : plan->n_single_sel;
+  const uint64_t nsets = plan->n_sets;
+  const uint64_t start = fallback ? 0 : plan->n_cand;
+  const uint64_t L = nsets - start;
+  const uint64_t seed = hash64(plan->seed_a, plan->seed_b);  // derive_selection_seed (pipeline.cpp:23-25)
+  uint64_t rpos = 0, cursor = 0, last_progress = 0;
+
+  auto block_min = [&](uint32_t x) -> uint32_t {
+    for (int o = 16; o > 0; o >>= 1) x = min(x, __shfl_xor_sync(kFull, x, o));
+    if ((v & 31) == 0) s_min[v >> 5] = x;
+    __syncthreads();
+    if (v < 32) {
+      uint32_t y = s_min[v];
+      for (int o = 16; o > 0; o >>= 1) y = min(y, __shfl_xor_sync(kFull, y, o));
+      if (v == 0) s_val = y;
+    }
+    __syncthreads();
+    const uint32_t res = s_val;
+    __syncthreads();
+    return res;
+  };
+
+  while (nsel < r && L > 0) {
+    const uint64_t si = start + (cursor + v) % L;
+    const uint32_t bit = sets[si];
+    const uint32_t lo = off[bit], sz = size[bit];
+    for (uint32_t j = 0; j < sz; ++j) first_touch[members[lo + j]] = 0xFFFFFFFFu;
+    __syncthreads();
+    uint32_t cnt = 0;
+    for (uint32_t j = 0; j < sz; ++j) {
+      const uint32_t p = members[lo + j];
+      if (!bs_test(bits, p)) {
+        ++cnt;
+        atomicMin(&first_touch[p], v);
+      }
+    }
+    __syncthreads();
+    bool dep = false;
+    if (cnt)
+      for (uint32_t j = 0; j < sz && !dep; ++j) {
+        const uint32_t p = members[lo + j];
+        if (!bs_test(bits, p) && first_touch[p] < v) dep = true;
+      }
+    const uint32_t vstar = block_min(dep ? v : W);
+    // RNG positions of the independent prefix
+    const bool draw = v < vstar && cnt >= 2;
+    uint64_t dtot;
+    const uint64_t dpos = block_exclusive_sum<uint64_t, 1024>(draw ? 1 : 0, sh, dtot);
+    uint32_t target = 0;
+    bool rej = false;
+    uint64_t bound = 0, val = 0;
+    if (draw) {
+      bound = below_bound(cnt);
+      val = rng_at(seed, rpos + dpos);
+      rej = val > bound;
+    }
+    const uint32_t rejv = block_min(rej ? v : W);
+    const uint32_t limit = min(vstar, rejv == W ? W : rejv + 1);
+    uint64_t extra = 0;  // positions consumed beyond one by the rejecting visit
+    if (draw && v < limit) {
+      if (v == rejv) {
+        uint64_t pos = rpos + dpos + 1;
+        do {
+          val = rng_at(seed, pos++);
+        } while (val > bound);
+        extra = pos - (rpos + dpos) - 1;
+      }
+      target = static_cast<uint32_t>(val % cnt);
+    }
+    // selections of the prefix and the r cut
+    const bool sel = v < limit && cnt >= 1;
+    uint64_t stot;
+    const uint64_t spos = block_exclusive_sum<uint64_t, 1024>(sel ? 1 : 0, sh, stot);
+    const uint64_t need = r - nsel;
+    const uint32_t cut = block_min(sel && spos + 1 == need ? v + 1 : W);
+    const uint32_t climit = min(limit, cut);
+    // commit
+    if (sel && v < climit) {
+      uint32_t seen = 0;
+      for (uint32_t j = 0; j < sz; ++j) {
+        const uint32_t p = members[lo + j];
+        if (!bs_test(bits, p)) {
+          if (seen == target) {
+            atomicOr(&bits[p >> 5], 1u << (p & 31));
+            break;
+          }
+          ++seen;
+        }
+      }
+    }
+    // totals over the committed visits
+    uint64_t csel, cdraw;
+    block_exclusive_sum<uint64_t, 1024>((sel && v < climit) ? 1 : 0, sh, csel);
+    block_exclusive_sum<uint64_t, 1024>((draw && v < climit) ? 1 + extra : 0, sh, cdraw);
+    __syncthreads();
+    nsel += csel;
+    rpos += cdraw;
+    cursor += climit;
+    if (csel) last_progress = cursor;
+    if (cursor - last_progress > L + W) {  // a full cycle without a selection: |P| < r
+      if (v == 0) latch(status, GP_ERROR);
+      break;
+    }
+  }
+  __syncthreads();
+  if (kSmem)
+    for (uint64_t w = v; w < nwords; w += W) selbits[w] = bits[w];
+  if (v == 0) {
+    plan->n_sel = nsel;
+    plan->n_multi = cursor;  // visits replayed (diagnostic)
+  }
+}
+
+
+constexpr int kSmemBitsBytes = 160 * 1024;
+
+// |P| is only known on the device: run the shared-memory engine when the
+// selection bitset fits, the global-memory one otherwise.
+__global__ void __launch_bounds__(1024) p2_engine_dispatch(Plan* plan, const uint32_t* __restrict__ sets,
+                                                           const uint32_t* __restrict__ off,
+                                                           const uint32_t* __restrict__ size,
+                                                           const uint32_t* __restrict__ members, uint32_t* selbits,
+                                                           uint32_t* first_touch, uint32_t* status) {
+  if (((plan->n_pos + 31) / 32) * 4 <= static_cast<uint64_t>(kSmemBitsBytes))
+    p2_engine_body<true>(plan, sets, off, size, members, selbits, first_touch, status);
+  else
+    p2_engine_body<false>(plan, sets, off, size, members, selbits, first_touch, status);
+}
+
 // sel = ascending P[p] for flagged p (bloom.cpp:221 sort), count must be r
 __global__ void __launch_bounds__(kTileBlock) flags_compact(const uint32_t* __restrict__ P,
                                                             const uint32_t* __restrict__ selbits, Plan* plan,
@@ -367,23 +532,26 @@ void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t 
             w.selbits, w.status);
   const int tgrid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(mtiles, ctx->sm_count * 4ULL)));
   GP_LAUNCH(ctx, p2_size_hist, tgrid, kTileBlock, 0, s, w.plan, w.p2_size, w.p2_table, w.status);
-  GP_LAUNCH(ctx, p2_table_scan, 1, 1024, 0, s, w.plan, w.p2_table, w.status);
+  launch_table_scan(ctx, w.p2_table, &w.plan->m, m_cap, 12, s);
+  GP_LAUNCH(ctx, p2_count_sets, 1, 32, 0, s, w.plan, w.p2_table, w.status);
   GP_LAUNCH(ctx, p2_size_scatter, tgrid, kTileBlock, 0, s, w.plan, w.p2_size, w.p2_table, w.p2_sets, w.status);
   GP_LAUNCH(ctx, p2_stage_a, 1, 1024, 0, s, w.plan, w.selbits, w.p2_table, w.status);
   stage_end(ctx, s);
   stage_begin(ctx, decoding ? ST_DEC_P2_ENGINE : ST_P2_ENGINE, s);
-  const uint64_t bs_bytes = ((n_bound + 31) / 32) * 4;
-  if (bs_bytes <= 200 * 1024) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(p2_engine<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = true;
-    }
-    GP_LAUNCH(ctx, p2_engine<true>, 1, 32, bs_bytes, s, w.plan, w.p2_sets, w.p2_off, w.p2_size, w.p2_members,
-              w.selbits, w.status);
+  // the selection bitset lives in shared memory when |P| fits (checked on the
+  // device: the smem variant falls back to the global words past kSmemBits)
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(p2_engine_win<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBitsBytes);
+    cudaFuncSetAttribute(p2_engine_dispatch, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBitsBytes);
+    attr = true;
+  }
+  if (((n_bound + 31) / 32) * 4 <= static_cast<uint64_t>(kSmemBitsBytes)) {
+    GP_LAUNCH(ctx, p2_engine_win<true>, 1, 1024, ((n_bound + 31) / 32) * 4, s, w.plan, w.p2_sets, w.p2_off,
+              w.p2_size, w.p2_members, w.selbits, w.first_touch, w.status);
   } else {
-    GP_LAUNCH(ctx, p2_engine<false>, 1, 32, 0, s, w.plan, w.p2_sets, w.p2_off, w.p2_size, w.p2_members,
-              w.selbits, w.status);
+    GP_LAUNCH(ctx, p2_engine_dispatch, 1, 1024, kSmemBitsBytes, s, w.plan, w.p2_sets, w.p2_off, w.p2_size,
+              w.p2_members, w.selbits, w.first_touch, w.status);
   }
   stage_end(ctx, s);
   const uint64_t ptiles = (n_bound + kTile - 1) / kTile;

@@ -5,8 +5,8 @@
 // value order and equal values keep their input order.  The element count is
 // read from a device word, so the sort runs without a host round trip.
 //
-// Per pass: upsweep (per-tile digit histograms, digit-major table), one-block
-// exclusive scan of the table, downsweep (stable in-tile ranks from warp
+// Per pass: upsweep (per-tile digit histograms, digit-major table), a
+// decoupled look-back scan of the table, downsweep (stable in-tile ranks from warp
 // match_any + cross-warp digit counts, 256 elements per round).
 #include "gp_ctx.hpp"
 #include "gp_device.cuh"
@@ -35,22 +35,6 @@ __global__ void __launch_bounds__(kBlock) radix_upsweep(const uint32_t* __restri
     __syncthreads();
     table[threadIdx.x * ntiles + tile] = h[threadIdx.x];
     __syncthreads();
-  }
-}
-
-__global__ void __launch_bounds__(1024) radix_scan(const uint64_t* n_dev, uint32_t* table, const uint32_t* status) {
-  __shared__ uint64_t sh[40];
-  if (failed(status)) return;
-  const uint64_t n = *n_dev;
-  const uint64_t entries = 256 * ((n + kTile - 1) / kTile);
-  uint64_t carry = 0;
-  for (uint64_t base = 0; base < entries; base += 1024) {
-    const uint64_t i = base + threadIdx.x;
-    const uint64_t v = i < entries ? table[i] : 0;
-    uint64_t tot;
-    const uint64_t ex = block_exclusive_sum<uint64_t, 1024>(v, sh, tot);
-    if (i < entries) table[i] = static_cast<uint32_t>(carry + ex);
-    carry += tot;
   }
 }
 
@@ -97,7 +81,50 @@ __global__ void __launch_bounds__(kBlock) radix_downsweep(const uint32_t* __rest
   }
 }
 
+// In-place exclusive scan of a u32 array whose length is n_mul * tiles(*n_dev)
+// entries (n_mul = 256 for digit tables), decoupled look-back, 4096 per tile.
+__global__ void __launch_bounds__(kBlock) scan_u32(uint32_t* data, const uint64_t* n_dev, uint64_t n_mul,
+                                                   int tile_shift, uint64_t* tiles, uint32_t* ticket,
+                                                   const uint32_t* status) {
+  __shared__ uint64_t sh[36];
+  __shared__ uint32_t slot;
+  if (failed(status)) return;
+  const uint64_t n = n_mul * ((*n_dev + (1ull << tile_shift) - 1) >> tile_shift);
+  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  while (true) {
+    const uint32_t tile = claim_tile(ticket, &slot);
+    if (tile >= ntiles) break;
+    const uint64_t base = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(threadIdx.x) * kItems;
+    uint32_t v[kItems];
+    uint64_t sum = 0;
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+      v[q] = base + q < n ? data[base + q] : 0;
+      sum += v[q];
+    }
+    uint64_t tot;
+    uint64_t o = tile_exclusive_offset<kBlock>(sum, tile, tiles, sh, tot);
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+      if (base + q < n) data[base + q] = static_cast<uint32_t>(o);
+      o += v[q];
+    }
+  }
+}
+
 }  // namespace
+
+// Exclusive scan of the digit-major table of 256 * tiles(n) entries (tiles of
+// 1 << tile_shift elements) with n read from a device word.
+void launch_table_scan(gp_ctx* ctx, uint32_t* table, const uint64_t* n_dev, uint64_t n_bound, int tile_shift,
+                       cudaStream_t s) {
+  Workspace& w = ctx->ws;
+  const uint64_t entries = 256 * ((n_bound + (1ull << tile_shift) - 1) >> tile_shift);
+  const uint64_t ntiles = (entries + kTile - 1) / kTile;
+  reset_scan(ctx, s, ntiles + 1);
+  const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, ctx->sm_count * 4ULL)));
+  GP_LAUNCH(ctx, scan_u32, grid, kBlock, 0, s, table, n_dev, 256, tile_shift, w.tiles, w.ticket, w.status);
+}
 
 // Sorts (keys, vals) of length *n_dev in place over `bits` low key bits
 // (multiple of 8), ping-ponging through (ktmp, vtmp).  n_bound sizes grids.
@@ -109,7 +136,7 @@ void launch_radix_sort(gp_ctx* ctx, uint32_t* keys, uint32_t* vals, uint32_t* kt
   uint32_t *ki = keys, *vi = vals, *ko = ktmp, *vo = vtmp;
   for (int shift = 0; shift < bits; shift += 8) {
     GP_LAUNCH(ctx, radix_upsweep, grid, kBlock, 0, s, ki, n_dev, shift, w.sort_table, w.status);
-    GP_LAUNCH(ctx, radix_scan, 1, 1024, 0, s, n_dev, w.sort_table, w.status);
+    launch_table_scan(ctx, w.sort_table, n_dev, n_bound, 12, s);
     GP_LAUNCH(ctx, radix_downsweep, grid, kBlock, 0, s, ki, vi, n_dev, shift, w.sort_table, ko, vo, w.status);
     std::swap(ki, ko);
     std::swap(vi, vo);

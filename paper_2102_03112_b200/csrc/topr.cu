@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kTileBlock) topr_candidates(
       const float4* p = reinterpret_cast<const float4*>(g + base);
 #pragma unroll
       for (int q = 0; q < kTileItems / 4; ++q) {
-        const float4 x = __ldcs(p + q);
+        const float4 x = __ldg(p + q);
         v[4 * q] = x.x;
         v[4 * q + 1] = x.y;
         v[4 * q + 2] = x.z;
