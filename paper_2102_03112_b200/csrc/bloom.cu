@@ -22,9 +22,7 @@ namespace gp {
 namespace {
 
 constexpr int kScanBlock = 256;
-constexpr int kScanItems = 16;
-constexpr int kScanTile = kScanBlock * kScanItems;
-constexpr uint64_t kSmemFilterMax = 160 * 1024;
+constexpr uint64_t kSmemFilterMax = 150 * 1024;
 
 __device__ __forceinline__ bool test_bit(const uint32_t* w, uint64_t pos) {
   return (w[pos >> 5] >> (pos & 31)) & 1u;
@@ -126,15 +124,32 @@ __global__ void bloom_load_words(const uint8_t* __restrict__ in, const Plan* pla
   }
 }
 
-// positive_scan (bloom.cpp:123-128): ordered compaction of {x < d : contains(x)}
+// positive_scan (bloom.cpp:123-128) in two passes.
+//
+// (1) bloom_members: contains() exits at the first clear probe, so ~half the
+// keys stop after one probe, a quarter after two, ...; a lane-per-key loop
+// keeps a warp busy for its slowest lane.  Each warp instead owns 2048-key
+// super-tiles and runs probe ROUNDS: round 1 probes every key (h_a, probe 0,
+// 16 independent keys per lane in flight), the survivors' key offsets
+// (u16, compacted in place in a per-warp shared queue) are the only work of
+// round j+1 (h_a, h_b recomputed, probe j, 4 entries per lane in flight).
+// Rounds stay converged; membership bits land in a per-warp mask that is
+// stored to a d-bit membership bitmap.  No cross-warp ordering is needed.
+// (2) members_compact: ordered compaction of the set bits (look-back scan,
+// 131072 keys per tile) — P ascending, |P| in the plan.
+constexpr int kLaneKeys = 16;
+constexpr int kChunkKeys = 32 * kLaneKeys;   // 512 keys per round-1 chunk
+constexpr int kChunks = 2;
+constexpr int kSuperKeys = kChunks * kChunkKeys;   // 1024 keys per warp super-tile
+constexpr int kWarps = kScanBlock / 32;
+
 template <bool kSmem>
-__global__ void __launch_bounds__(kScanBlock) bloom_scan(const uint32_t* __restrict__ gwords, Plan* plan,
-                                                         uint32_t* __restrict__ pos_out, uint64_t cap,
-                                                         uint64_t* tiles, uint32_t* ticket,
-                                                         const uint32_t* status) {
+__global__ void __launch_bounds__(kScanBlock) bloom_members(const uint32_t* __restrict__ gwords, Plan* plan,
+                                                            uint32_t* __restrict__ bitmap,
+                                                            const uint32_t* status) {
   extern __shared__ uint32_t sw[];
-  __shared__ uint64_t sh[36];
-  __shared__ uint32_t slot;
+  __shared__ uint16_t queue[kWarps][kSuperKeys];
+  __shared__ uint32_t member[kWarps][kSuperKeys / 32];
   if (failed(status)) return;
   const uint8_t im = plan->index_method;
   if (im < GP_INDEX_BLOOM_P0 || im > GP_INDEX_BLOOM_NAIVE) return;
@@ -149,36 +164,126 @@ __global__ void __launch_bounds__(kScanBlock) bloom_scan(const uint32_t* __restr
     __syncthreads();
     words = sw;
   }
-  const uint64_t ntiles = (d + kScanTile - 1) / kScanTile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint16_t* q = queue[warp];
+  uint32_t* wm = member[warp];
+  const uint64_t nsuper = (d + kSuperKeys - 1) / kSuperKeys;
+  const uint64_t gw = static_cast<uint64_t>(gridDim.x) * kWarps;
+  for (uint64_t st = static_cast<uint64_t>(blockIdx.x) * kWarps + warp; st < nsuper; st += gw) {
+    const uint64_t sbase = st * kSuperKeys;
+    for (int i = lane; i < kSuperKeys / 32; i += 32) wm[i] = 0;
+    __syncwarp();
+    uint32_t nq = 0;
+    // ---- round 1
+    for (int c = 0; c < kChunks; ++c) {
+      const uint32_t off0 = c * kChunkKeys + kLaneKeys * lane;
+      uint32_t pass = 0;
+#pragma unroll
+      for (int j = 0; j < kLaneKeys; ++j) {
+        const uint64_t x = sbase + off0 + j;
+        const uint64_t a = mix64(x ^ sa);
+        if (x < d && test_bit(words, fast_mod(mix64(a), fm))) pass |= 1u << j;
+      }
+      if (k == 1) {
+        if (pass) atomicOr(&wm[off0 >> 5], pass << (off0 & 31));
+        continue;
+      }
+      const uint32_t cnt = __popc(pass);
+      const uint32_t inc = warp_inclusive_sum(cnt);
+      uint32_t o = nq + inc - cnt;
+      while (pass) {
+        const int j = __ffs(pass) - 1;
+        q[o++] = static_cast<uint16_t>(off0 + j);
+        pass &= pass - 1;
+      }
+      nq += __shfl_sync(kFull, inc, 31);
+    }
+    __syncwarp();
+    // ---- rounds 2..k
+    for (uint32_t j = 1; j < k && nq; ++j) {
+      uint32_t wr = 0;
+      const bool last = j + 1 == k;
+      // 4 entries per lane in flight while the queue is long, 1 in the thin tail
+      const int per = nq > 64 ? 4 : 1;
+      for (uint32_t base = 0; base < nq; base += 32 * per) {
+        uint16_t kk[4];
+        bool ok[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (u >= per) {
+            ok[u] = false;
+            kk[u] = 0;
+            continue;
+          }
+          const uint32_t e = base + 32 * u + lane;
+          ok[u] = false;
+          kk[u] = 0;
+          if (e < nq) {
+            kk[u] = q[e];
+            const uint64_t x = sbase + kk[u];
+            const uint64_t a = mix64(x ^ sa), b = mix64(x ^ sb);
+            ok[u] = test_bit(words, fast_mod(mix64(a + static_cast<uint64_t>(j) * b), fm));
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (last) {
+            if (ok[u]) atomicOr(&wm[kk[u] >> 5], 1u << (kk[u] & 31));
+          } else {
+            const unsigned bal = __ballot_sync(kFull, ok[u]);
+            if (ok[u]) q[wr + __popc(bal & ((1u << lane) - 1))] = kk[u];
+            wr += __popc(bal);
+          }
+        }
+        __syncwarp();
+      }
+      nq = last ? 0 : wr;
+    }
+    __syncwarp();
+    // ---- membership words (the super-tile is word aligned: 2048 keys = 64 words)
+    const uint64_t nwd = (d + 31) / 32;
+    for (int i = lane; i < kSuperKeys / 32; i += 32)
+      if (sbase / 32 + i < nwd) bitmap[sbase / 32 + i] = wm[i];
+    __syncwarp();
+  }
+}
+
+// ordered compaction of the membership bitmap: 16 words per thread
+__global__ void __launch_bounds__(kScanBlock) members_compact(const uint32_t* __restrict__ bitmap, Plan* plan,
+                                                              uint32_t* __restrict__ pos_out, uint64_t cap,
+                                                              uint64_t* tiles, uint32_t* ticket,
+                                                              const uint32_t* status) {
+  __shared__ uint64_t sh[36];
+  __shared__ uint32_t slot;
+  if (failed(status)) return;
+  const uint8_t im = plan->index_method;
+  if (im < GP_INDEX_BLOOM_P0 || im > GP_INDEX_BLOOM_NAIVE) return;
+  const uint64_t nwd = (plan->d + 31) / 32;
+  constexpr int kW = 16;
+  const uint64_t ntiles = (nwd + kScanBlock * kW - 1) / (kScanBlock * kW);
   while (true) {
     const uint32_t tile = claim_tile(ticket, &slot);
     if (tile >= ntiles) break;
-    const uint64_t base = static_cast<uint64_t>(tile) * kScanTile + static_cast<uint64_t>(threadIdx.x) * kScanItems;
-    uint32_t mask = 0;
-#pragma unroll 4
-    for (int q = 0; q < kScanItems; ++q) {
-      const uint64_t x = base + q;
-      if (x >= d) break;
-      const uint64_t a = mix64(x ^ sa);
-      if (!test_bit(words, fast_mod(mix64(a), fm))) continue;
-      const uint64_t b = mix64(x ^ sb);
-      uint64_t h = a + b;
-      bool in = true;
-      for (uint32_t j = 1; j < k; ++j, h += b) {
-        if (!test_bit(words, fast_mod(mix64(h), fm))) {
-          in = false;
-          break;
-        }
-      }
-      if (in) mask |= 1u << q;
+    const uint64_t w0 = static_cast<uint64_t>(tile) * kScanBlock * kW + static_cast<uint64_t>(threadIdx.x) * kW;
+    uint32_t v[kW];
+    uint64_t c = 0;
+#pragma unroll
+    for (int i = 0; i < kW; ++i) {
+      v[i] = w0 + i < nwd ? bitmap[w0 + i] : 0u;
+      c += __popc(v[i]);
     }
     uint64_t tot;
-    uint64_t o = tile_exclusive_offset<kScanBlock>(__popc(mask), tile, tiles, sh, tot);
-    while (mask) {
-      const int q = __ffs(mask) - 1;
-      if (o < cap) pos_out[o] = static_cast<uint32_t>(base + q);
-      ++o;
-      mask &= mask - 1;
+    uint64_t o = tile_exclusive_offset<kScanBlock>(c, tile, tiles, sh, tot);
+#pragma unroll
+    for (int i = 0; i < kW; ++i) {
+      uint32_t x = v[i];
+      while (x) {
+        const int b = __ffs(x) - 1;
+        if (o < cap) pos_out[o] = static_cast<uint32_t>(32 * (w0 + i) + b);
+        ++o;
+        x &= x - 1;
+      }
     }
     if (tile == ntiles - 1 && threadIdx.x == kScanBlock - 1) plan->n_pos = o;
   }
@@ -245,23 +350,30 @@ void launch_bloom_parse(gp_ctx* ctx, const uint8_t* in, uint64_t m_bound, cudaSt
 // the width is only on the device, so the global-memory variant is used).
 void launch_bloom_scan(gp_ctx* ctx, uint64_t d_bound, uint64_t m_host, bool decoding, cudaStream_t s) {
   Workspace& w = ctx->ws;
-  const uint64_t ntiles = (d_bound + kScanTile - 1) / kScanTile;
-  reset_scan(ctx, s, ntiles + 1);
-  const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, ctx->sm_count * 8ULL)));
   const uint64_t fbytes = ((m_host + 31) / 32) * 4;
+  const uint64_t nsuper = (d_bound + kSuperKeys - 1) / kSuperKeys;
+  uint32_t* bitmap = w.u32c;  // d-bit membership bitmap
   if (m_host && fbytes <= kSmemFilterMax) {
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(bloom_scan<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(bloom_members<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(kSmemFilterMax));
       attr = true;
     }
-    GP_LAUNCH(ctx, bloom_scan<true>, grid, kScanBlock, fbytes, s, w.filter, w.plan, w.pos, ctx->max_d, w.tiles,
-              w.ticket, w.status);
+    const int per_sm = std::max(1, static_cast<int>((200 * 1024) / (fbytes + 40 * 1024)));
+    const int grid = static_cast<int>(std::max<uint64_t>(
+        1, std::min<uint64_t>((nsuper + kWarps - 1) / kWarps, static_cast<uint64_t>(ctx->sm_count) * per_sm)));
+    GP_LAUNCH(ctx, bloom_members<true>, grid, kScanBlock, fbytes, s, w.filter, w.plan, bitmap, w.status);
   } else {
-    GP_LAUNCH(ctx, bloom_scan<false>, grid, kScanBlock, 0, s, w.filter, w.plan, w.pos, ctx->max_d, w.tiles,
-              w.ticket, w.status);
+    const int grid = static_cast<int>(std::max<uint64_t>(
+        1, std::min<uint64_t>((nsuper + kWarps - 1) / kWarps, static_cast<uint64_t>(ctx->sm_count) * 6)));
+    GP_LAUNCH(ctx, bloom_members<false>, grid, kScanBlock, 0, s, w.filter, w.plan, bitmap, w.status);
   }
+  const uint64_t nwd = (d_bound + 31) / 32;
+  const uint64_t ntiles = (nwd + kScanBlock * 16 - 1) / (kScanBlock * 16);
+  reset_scan(ctx, s, ntiles + 1);
+  GP_LAUNCH(ctx, members_compact, static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, ctx->sm_count * 4ULL))),
+            kScanBlock, 0, s, bitmap, w.plan, w.pos, ctx->max_d, w.tiles, w.ticket, w.status);
   GP_LAUNCH(ctx, bloom_after_scan, 1, 1, 0, s, w.plan, ctx->max_d, decoding ? 1 : 0, w.status);
 }
 

@@ -45,8 +45,9 @@ __host__ __device__ __forceinline__ uint64_t below_bound(uint64_t n) {
   return ~0ULL - rem;
 }
 
-// Exact x mod m for 1 <= m < 2^32, with minv = floor((2^64-1)/m): the
-// quotient estimate umulhi(x, minv) is at most 2 below floor(x/m).
+// Exact x mod m for 1 <= m < 2^32, with minv = floor((2^64-1)/m) = (2^64-e)/m,
+// 0 < e <= m: x*minv/2^64 = x/m - x*e/(m*2^64) > x/m - 1, so the quotient
+// estimate umulhi(x, minv) is floor(x/m) or one below it — one correction.
 struct FastMod {
   uint64_t m;
   uint64_t minv;
@@ -54,12 +55,9 @@ struct FastMod {
 inline FastMod make_fastmod(uint64_t m) { return FastMod{m, m ? ~0ULL / m : 0}; }
 
 __device__ __forceinline__ uint64_t fast_mod(uint64_t x, const FastMod& f) {
-  if (f.m >> 32) return x % f.m;
   const uint64_t q = __umul64hi(x, f.minv);
-  uint64_t r = x - q * f.m;
-  if (r >= f.m) r -= f.m;
-  if (r >= f.m) r -= f.m;
-  return r;
+  const uint64_t r = x - q * f.m;
+  return r >= f.m ? r - f.m : r;
 }
 
 // ---------------------------------------------------------------- status
