@@ -144,7 +144,8 @@ void carve(Workspace& w, uint8_t* base, uint64_t D) {
   w.pair_cap = 4 * D;
   w.p2_count = c.take<uint32_t>(w.set_cap + 1);
   w.p2_off = c.take<uint32_t>(w.set_cap + 1);
-  w.p2_size = c.take<uint32_t>(w.set_cap);
+  w.p2_single = c.take<uint32_t>(w.set_cap);
+  w.p2_cursor = c.take<uint32_t>(w.set_cap);
   w.p2_sets = c.take<uint32_t>(w.set_cap);
   w.p2_table = c.take<uint32_t>(256 * (w.set_cap / 4096 + 1) + 256);
   w.pairs = c.take<uint32_t>(w.pair_cap);
@@ -158,6 +159,8 @@ void carve(Workspace& w, uint8_t* base, uint64_t D) {
   w.f64b = c.take<double>(D);
   w.partial = c.take<double>((D / 2048 + 128) * 44);
   w.sort_table = c.take<uint32_t>(256 * (D / 4096 + 2));
+  w.seg_dev = c.take<double>(4 * 2048);
+  w.seg_arg = c.take<uint32_t>(4 * 2048);
   w.crc_cap = 2 * ((64 * D + (1 << 20)) / (64 * 256) + 64);
   w.crc_part = c.take<uint32_t>(64);
   w.crc_digits = c.take<uint32_t>(5 * 256);

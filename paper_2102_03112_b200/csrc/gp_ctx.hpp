@@ -77,7 +77,8 @@ struct Workspace {
   uint64_t set_cap = 0;           // max filter width m for P2
   uint32_t* p2_count = nullptr;   // [set_cap + 1]
   uint32_t* p2_off = nullptr;     // [set_cap + 1]
-  uint32_t* p2_size = nullptr;    // [set_cap]
+  uint32_t* p2_single = nullptr;  // member of size-1 sets [set_cap]
+  uint32_t* p2_cursor = nullptr;  // scatter cursors [set_cap]
   uint32_t* p2_sets = nullptr;    // [set_cap]
   uint32_t* p2_table = nullptr;   // [256 * set_cap / 4096 + 256]
   uint32_t* p2_members = nullptr; // [pair_cap]
@@ -98,6 +99,8 @@ struct Workspace {
   double* f64b = nullptr;         // [D]
   double* partial = nullptr;      // fit chunk partial sums [(D/2048 + 128) * 44]
   uint32_t* sort_table = nullptr; // radix digit table [256 * (D/4096 + 2)]
+  double* seg_dev = nullptr;      // segmentation sweep partials [4 * 2048]
+  uint32_t* seg_arg = nullptr;    // [4 * 2048]
   uint32_t* crc_part = nullptr;   // (unused)
   uint32_t* crc_digits = nullptr; // CRC shift-operator digit tables [5 * 256]
   uint32_t* crc_acc = nullptr;    // XOR accumulator + block counter [2]

@@ -4,11 +4,13 @@
 // conflict_sets: every positive x (in P order) contributes its k probe
 // positions; a bit's set is the ascending, de-duplicated list of positives
 // probing it; sets are ordered by (size, bit).  Device form:
-//   pairs    : one thread per positive, k positions, per-bit counts (atomics)
-//   offsets  : exclusive scan of the counts over [0, m)
-//   scatter  : members into per-bit buckets (arbitrary order)
-//   dedupe   : per bucket, sort + unique (buckets hold ~1-20 entries);
-//              a bucket of one distinct member is a singleton
+//   pairs    : one thread per positive, k positions de-duplicated in
+//              registers, per-bit distinct counts = set sizes (atomics); the
+//              first joiner of a bit is its member if the set stays size 1
+//   offsets  : exclusive scan of the multi-set sizes over [0, m); stage-A
+//              selection of every singleton's member
+//   scatter  : multi-set members into per-bit buckets, then an ascending sort
+//              per bucket (buckets hold 2-~20 entries)
 //   order    : one stable counting-sort pass by size over the bit domain,
 //              which also compacts away empty bits → sets in (size, bit) order
 //
@@ -40,12 +42,18 @@ __device__ __forceinline__ bool p2_active(const Plan* plan) {
   return plan->index_method == GP_INDEX_BLOOM_P2;
 }
 
+// One thread per positive p: its k probe positions, de-duplicated among
+// themselves (one positive joins a set once, the consecutive-duplicate rule of
+// bloom.cpp:159-164), so count[bit] ends as the set's size.  The first
+// joiner of a bit records itself in single[bit]: for a size-1 set it is the
+// member.
 __global__ void p2_pairs(const uint32_t* __restrict__ P, Plan* plan, uint32_t* __restrict__ pairs,
-                         uint32_t* __restrict__ count, uint64_t pair_cap, uint64_t set_cap, uint32_t* status) {
+                         uint32_t* __restrict__ count, uint32_t* __restrict__ single, uint64_t pair_cap,
+                         uint64_t set_cap, uint32_t* status) {
   if (failed(status) || !p2_active(plan)) return;
   const uint64_t n = plan->n_pos, m = plan->m;
   const uint32_t k = plan->k;
-  if (n * k > pair_cap || m > set_cap) {
+  if (n * k > pair_cap || m > set_cap || k > 64) {
     if (blockIdx.x == 0 && threadIdx.x == 0) latch(status, GP_CAPACITY);
     return;
   }
@@ -56,19 +64,27 @@ __global__ void p2_pairs(const uint32_t* __restrict__ P, Plan* plan, uint32_t* _
     const uint64_t x = P[p];
     const uint64_t a = mix64(x ^ sa), b = mix64(x ^ sb);
     uint64_t h = a;
+    uint32_t seen[64];
     for (uint32_t j = 0; j < k; ++j, h += b) {
       const uint32_t bit = static_cast<uint32_t>(fast_mod(mix64(h), fm));
-      pairs[p * k + j] = bit;
-      atomicAdd(&count[bit], 1u);
+      bool dup = false;
+      for (uint32_t i = 0; i < j; ++i) dup |= seen[i] == bit;
+      seen[j] = bit;
+      pairs[p * k + j] = dup ? 0xFFFFFFFFu : bit;
+      if (!dup && atomicAdd(&count[bit], 1u) == 0) single[bit] = static_cast<uint32_t>(p);
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) plan->n_pairs = n * k;
 }
 
-// exclusive scan of count[0, m) into off[0, m]; tiles of 4096 bits
-__global__ void __launch_bounds__(kTileBlock) p2_offsets(const uint32_t* __restrict__ count, Plan* plan,
-                                                         uint32_t* __restrict__ off, uint64_t* tiles,
-                                                         uint32_t* ticket, const uint32_t* status) {
+// Exclusive scan of the multi-set sizes (count >= 2, else 0) into off[0, m];
+// also arms the scatter cursors and writes the stage-A selections: the member
+// of every size-1 set (singletons are visited first, p2_select pass 1).
+__global__ void __launch_bounds__(kTileBlock) p2_offsets(const uint32_t* __restrict__ count,
+                                                         const uint32_t* __restrict__ single, Plan* plan,
+                                                         uint32_t* __restrict__ off, uint32_t* __restrict__ cursor,
+                                                         uint32_t* selbits, uint64_t* tiles, uint32_t* ticket,
+                                                         uint32_t* status) {
   __shared__ uint64_t sh[36];
   __shared__ uint32_t slot;
   if (failed(status) || !p2_active(plan)) return;
@@ -82,48 +98,55 @@ __global__ void __launch_bounds__(kTileBlock) p2_offsets(const uint32_t* __restr
     uint64_t sum = 0;
 #pragma unroll
     for (int q = 0; q < kTileItems; ++q) {
-      c[q] = base + q < m ? count[base + q] : 0;
+      const uint32_t v = base + q < m ? count[base + q] : 0;
+      if (v == 1) {
+        const uint32_t mem = single[base + q];
+        atomicOr(&selbits[mem >> 5], 1u << (mem & 31));
+      }
+      if (v >= kMaxSetSize) latch(status, GP_CAPACITY);
+      c[q] = v >= 2 ? v : 0;
       sum += c[q];
     }
     uint64_t tot;
     uint64_t o = tile_exclusive_offset<kTileBlock>(sum, tile, tiles, sh, tot);
 #pragma unroll
     for (int q = 0; q < kTileItems; ++q) {
-      if (base + q < m) off[base + q] = static_cast<uint32_t>(o);
+      if (base + q < m) {
+        off[base + q] = static_cast<uint32_t>(o);
+        if (c[q]) cursor[base + q] = c[q];
+      }
       o += c[q];
     }
     if (tile == ntiles - 1 && threadIdx.x == kTileBlock - 1) off[m] = static_cast<uint32_t>(o);
   }
 }
 
-__global__ void p2_scatter(const uint32_t* __restrict__ pairs, const Plan* plan, const uint32_t* __restrict__ off,
-                           uint32_t* count, uint32_t* __restrict__ members, const uint32_t* status) {
+// multi-set members into their buckets (arbitrary order within a bucket)
+__global__ void p2_scatter(const uint32_t* __restrict__ pairs, const Plan* plan, const uint32_t* __restrict__ count,
+                           const uint32_t* __restrict__ off, uint32_t* cursor, uint32_t* __restrict__ members,
+                           const uint32_t* status) {
   if (failed(status) || !p2_active(plan)) return;
   const uint64_t np = plan->n_pairs;
   const uint32_t k = plan->k;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < np;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint32_t bit = pairs[i];
-    const uint32_t slot = off[bit] + atomicSub(&count[bit], 1u) - 1u;  // count returns to 0
+    if (bit == 0xFFFFFFFFu || count[bit] < 2) continue;
+    const uint32_t slot = off[bit] + atomicSub(&cursor[bit], 1u) - 1u;
     members[slot] = static_cast<uint32_t>(i / k);
   }
 }
 
-// per bit: sort + unique the bucket; size[bit] = distinct members; stage A flags
-__global__ void p2_dedupe(const Plan* plan, const uint32_t* __restrict__ off, uint32_t* __restrict__ members,
-                          uint32_t* __restrict__ size, uint32_t* __restrict__ selbits, uint32_t* status) {
+// ascending members per multi set (sizes are small)
+__global__ void p2_sort_buckets(const Plan* plan, const uint32_t* __restrict__ off, uint32_t* __restrict__ members,
+                                const uint32_t* status) {
   if (failed(status) || !p2_active(plan)) return;
   const uint64_t m = plan->m;
   for (uint64_t b = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; b < m;
        b += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint32_t lo = off[b], hi = off[b + 1];
-    const uint32_t n = hi - lo;
-    if (n == 0) {
-      size[b] = 0;
-      continue;
-    }
+    const uint32_t lo = off[b], n = off[b + 1] - lo;
+    if (n < 2) continue;
     uint32_t* mem = members + lo;
-    // insertion sort (buckets are tiny: k probes of ~|P|k/m positives)
     for (uint32_t i = 1; i < n; ++i) {
       const uint32_t v = mem[i];
       uint32_t j = i;
@@ -133,12 +156,6 @@ __global__ void p2_dedupe(const Plan* plan, const uint32_t* __restrict__ off, ui
       }
       mem[j] = v;
     }
-    uint32_t u = 1;
-    for (uint32_t i = 1; i < n; ++i)
-      if (mem[i] != mem[u - 1]) mem[u++] = mem[i];
-    size[b] = u;
-    if (u >= kMaxSetSize) latch(status, GP_CAPACITY);
-    if (u == 1) atomicOr(&selbits[mem[0] >> 5], 1u << (mem[0] & 31));
   }
 }
 
@@ -234,76 +251,7 @@ __global__ void __launch_bounds__(1024) p2_stage_a(Plan* plan, const uint32_t* _
   }
 }
 
-// Stage B: one warp replays the sequential greedy loop.
 __device__ __forceinline__ bool bs_test(const uint32_t* bs, uint32_t p) { return (bs[p >> 5] >> (p & 31)) & 1u; }
-
-template <bool kSmem>
-__global__ void __launch_bounds__(32) p2_engine(Plan* plan, const uint32_t* __restrict__ sets,
-                                                const uint32_t* __restrict__ off, const uint32_t* __restrict__ size,
-                                                const uint32_t* __restrict__ members, uint32_t* selbits,
-                                                uint32_t* status) {
-  extern __shared__ uint32_t sbits[];
-  if (failed(status) || !p2_active(plan)) return;
-  const int lane = threadIdx.x;
-  const uint64_t n = plan->n_pos, r = plan->r;
-  const uint64_t nwords = (n + 31) / 32;
-  uint32_t* bits = kSmem ? sbits : selbits;
-  const bool fallback = plan->n_single_sel > r;
-  // selected bitset over P positions: the stage-A singletons (empty on fallback)
-  if (kSmem || fallback)
-    for (uint64_t w = lane; w < nwords; w += 32) bits[w] = fallback ? 0u : selbits[w];
-  __syncwarp();
-  uint64_t nsel = fallback ? 0 : plan->n_single_sel;
-  const uint64_t nsets = plan->n_sets;
-  const uint64_t start = fallback ? 0 : plan->n_cand;
-  const uint64_t seed = hash64(plan->seed_a, plan->seed_b);  // derive_selection_seed
-  uint64_t rpos = 0;                                          // CounterRng draws consumed
-  while (nsel < r && start < nsets) {
-    const uint64_t before = nsel;
-    for (uint64_t si = start; si < nsets && nsel < r; ++si) {
-      const uint32_t bit = sets[si];
-      const uint32_t lo = off[bit], sz = size[bit];
-      // count unselected members (ascending order = lane order within chunks)
-      uint32_t cnt = 0;
-      for (uint32_t c = 0; c < sz; c += 32) {
-        const bool in = c + lane < sz;
-        const uint32_t p = in ? members[lo + c + lane] : 0;
-        cnt += __popc(__ballot_sync(kFull, in && !bs_test(bits, p)));
-      }
-      if (cnt == 0) continue;
-      uint32_t target = 0;
-      if (cnt > 1) {
-        // CounterRng::below(cnt), exact rejection (rng.hpp:52-59)
-        const uint64_t bound = below_bound(cnt);
-        uint64_t v = rng_at(seed, rpos++);
-        while (v > bound) v = rng_at(seed, rpos++);
-        target = static_cast<uint32_t>(v % cnt);
-      }
-      // select the target-th unselected member
-      uint32_t seen = 0;
-      for (uint32_t c = 0; c < sz; c += 32) {
-        const bool in = c + lane < sz;
-        const uint32_t p = in ? members[lo + c + lane] : 0;
-        const bool un = in && !bs_test(bits, p);
-        const unsigned bal = __ballot_sync(kFull, un);
-        const uint32_t here = __popc(bal);
-        if (target < seen + here) {
-          const uint32_t want = target - seen;
-          if (un && __popc(bal & ((1u << lane) - 1)) == want) bits[p >> 5] |= 1u << (p & 31);
-          __syncwarp();
-          break;
-        }
-        seen += here;
-      }
-      ++nsel;
-    }
-    if (nsel == before) break;  // no progress possible (cannot happen with |P| >= r)
-  }
-  __syncwarp();
-  if (kSmem)
-    for (uint64_t w = lane; w < nwords; w += 32) selbits[w] = bits[w];
-  if (lane == 0) plan->n_sel = nsel;
-}
 
 // Stage B, windowed: 1024 consecutive visits per round, one thread each.
 // Every visit counts its unselected members against the selection at the
@@ -319,24 +267,26 @@ __global__ void __launch_bounds__(32) p2_engine(Plan* plan, const uint32_t* __re
 template <bool kSmem>
 __device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __restrict__ sets,
                                                const uint32_t* __restrict__ off, const uint32_t* __restrict__ size,
-                                               const uint32_t* __restrict__ members, uint32_t* selbits,
+                                               const uint32_t* __restrict__ members,
+                                               const uint32_t* __restrict__ single, uint32_t* selbits,
                                                uint32_t* first_touch, uint32_t* status);
 
 template <bool kSmem>
 __global__ void __launch_bounds__(1024) p2_engine_win(Plan* plan, const uint32_t* __restrict__ sets,
                                                       const uint32_t* __restrict__ off,
                                                       const uint32_t* __restrict__ size,
-                                                      const uint32_t* __restrict__ members, uint32_t* selbits,
+                                                      const uint32_t* __restrict__ members,
+                                                      const uint32_t* __restrict__ single, uint32_t* selbits,
                                                       uint32_t* first_touch, uint32_t* status) {
-  p2_engine_body<kSmem>(plan, sets, off, size, members, selbits, first_touch, status);
+  p2_engine_body<kSmem>(plan, sets, off, size, members, single, selbits, first_touch, status);
 }
 
 template <bool kSmem>
 __device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __restrict__ sets,
-                                                      const uint32_t* __restrict__ off,
-                                                      const uint32_t* __restrict__ size,
-                                                      const uint32_t* __restrict__ members, uint32_t* selbits,
-                                                      uint32_t* first_touch, uint32_t* status) {
+                                               const uint32_t* __restrict__ off, const uint32_t* __restrict__ size,
+                                               const uint32_t* __restrict__ members,
+                                               const uint32_t* __restrict__ single, uint32_t* selbits,
+                                               uint32_t* first_touch, uint32_t* status) {
   extern __shared__ uint32_t sbits[];
   __shared__ uint64_t sh[40];
   __shared__ uint32_t s_min[32];
@@ -376,12 +326,15 @@ __device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __res
   while (nsel < r && L > 0) {
     const uint64_t si = start + (cursor + v) % L;
     const uint32_t bit = sets[si];
-    const uint32_t lo = off[bit], sz = size[bit];
-    for (uint32_t j = 0; j < sz; ++j) first_touch[members[lo + j]] = 0xFFFFFFFFu;
+    const uint32_t sz = size[bit];
+    // size-1 sets (visited only on the fallback path) keep their member in single[]
+    const uint32_t* mems = sz == 1 ? single + bit : members + off[bit];
+    const uint32_t lo = 0;
+    for (uint32_t j = 0; j < sz; ++j) first_touch[mems[lo + j]] = 0xFFFFFFFFu;
     __syncthreads();
     uint32_t cnt = 0;
     for (uint32_t j = 0; j < sz; ++j) {
-      const uint32_t p = members[lo + j];
+      const uint32_t p = mems[lo + j];
       if (!bs_test(bits, p)) {
         ++cnt;
         atomicMin(&first_touch[p], v);
@@ -391,7 +344,7 @@ __device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __res
     bool dep = false;
     if (cnt)
       for (uint32_t j = 0; j < sz && !dep; ++j) {
-        const uint32_t p = members[lo + j];
+        const uint32_t p = mems[lo + j];
         if (!bs_test(bits, p) && first_touch[p] < v) dep = true;
       }
     const uint32_t vstar = block_min(dep ? v : W);
@@ -431,7 +384,7 @@ __device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __res
     if (sel && v < climit) {
       uint32_t seen = 0;
       for (uint32_t j = 0; j < sz; ++j) {
-        const uint32_t p = members[lo + j];
+        const uint32_t p = mems[lo + j];
         if (!bs_test(bits, p)) {
           if (seen == target) {
             atomicOr(&bits[p >> 5], 1u << (p & 31));
@@ -472,12 +425,13 @@ constexpr int kSmemBitsBytes = 160 * 1024;
 __global__ void __launch_bounds__(1024) p2_engine_dispatch(Plan* plan, const uint32_t* __restrict__ sets,
                                                            const uint32_t* __restrict__ off,
                                                            const uint32_t* __restrict__ size,
-                                                           const uint32_t* __restrict__ members, uint32_t* selbits,
+                                                           const uint32_t* __restrict__ members,
+                                                           const uint32_t* __restrict__ single, uint32_t* selbits,
                                                            uint32_t* first_touch, uint32_t* status) {
   if (((plan->n_pos + 31) / 32) * 4 <= static_cast<uint64_t>(kSmemBitsBytes))
-    p2_engine_body<true>(plan, sets, off, size, members, selbits, first_touch, status);
+    p2_engine_body<true>(plan, sets, off, size, members, single, selbits, first_touch, status);
   else
-    p2_engine_body<false>(plan, sets, off, size, members, selbits, first_touch, status);
+    p2_engine_body<false>(plan, sets, off, size, members, single, selbits, first_touch, status);
 }
 
 // sel = ascending P[p] for flagged p (bloom.cpp:221 sort), count must be r
@@ -519,27 +473,24 @@ void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t 
   const uint64_t m_cap = std::min<uint64_t>(m_bound, w.set_cap);
   cudaMemsetAsync(w.p2_count, 0, (m_cap + 1) * sizeof(uint32_t), s);
   cudaMemsetAsync(w.selbits, 0, ((n_bound + 31) / 32) * 4, s);
-  GP_LAUNCH(ctx, p2_pairs, grid_for(ctx, n_bound, 128), 128, 0, s, w.pos, w.plan, w.pairs, w.p2_count, w.pair_cap,
-            w.set_cap, w.status);
+  GP_LAUNCH(ctx, p2_pairs, grid_for(ctx, n_bound, 128), 128, 0, s, w.pos, w.plan, w.pairs, w.p2_count, w.p2_single,
+            w.pair_cap, w.set_cap, w.status);
   const uint64_t mtiles = (m_cap + kTile - 1) / kTile;
   reset_scan(ctx, s, mtiles + 1);
-  GP_LAUNCH(ctx, p2_offsets, grid_for(ctx, mtiles * kTileBlock, kTileBlock), kTileBlock, 0, s, w.p2_count, w.plan,
-            w.p2_off, w.tiles, w.ticket, w.status);
+  GP_LAUNCH(ctx, p2_offsets, grid_for(ctx, mtiles * kTileBlock, kTileBlock), kTileBlock, 0, s, w.p2_count,
+            w.p2_single, w.plan, w.p2_off, w.p2_cursor, w.selbits, w.tiles, w.ticket, w.status);
   const uint64_t pair_bound = std::min<uint64_t>(n_bound * k_bound, w.pair_cap);
-  GP_LAUNCH(ctx, p2_scatter, grid_for(ctx, pair_bound, 256), 256, 0, s, w.pairs, w.plan, w.p2_off, w.p2_count,
-            w.p2_members, w.status);
-  GP_LAUNCH(ctx, p2_dedupe, grid_for(ctx, m_cap, 128), 128, 0, s, w.plan, w.p2_off, w.p2_members, w.p2_size,
-            w.selbits, w.status);
+  GP_LAUNCH(ctx, p2_scatter, grid_for(ctx, pair_bound, 256), 256, 0, s, w.pairs, w.plan, w.p2_count, w.p2_off,
+            w.p2_cursor, w.p2_members, w.status);
+  GP_LAUNCH(ctx, p2_sort_buckets, grid_for(ctx, m_cap, 256), 256, 0, s, w.plan, w.p2_off, w.p2_members, w.status);
   const int tgrid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(mtiles, ctx->sm_count * 4ULL)));
-  GP_LAUNCH(ctx, p2_size_hist, tgrid, kTileBlock, 0, s, w.plan, w.p2_size, w.p2_table, w.status);
+  GP_LAUNCH(ctx, p2_size_hist, tgrid, kTileBlock, 0, s, w.plan, w.p2_count, w.p2_table, w.status);
   launch_table_scan(ctx, w.p2_table, &w.plan->m, m_cap, 12, s);
   GP_LAUNCH(ctx, p2_count_sets, 1, 32, 0, s, w.plan, w.p2_table, w.status);
-  GP_LAUNCH(ctx, p2_size_scatter, tgrid, kTileBlock, 0, s, w.plan, w.p2_size, w.p2_table, w.p2_sets, w.status);
+  GP_LAUNCH(ctx, p2_size_scatter, tgrid, kTileBlock, 0, s, w.plan, w.p2_count, w.p2_table, w.p2_sets, w.status);
   GP_LAUNCH(ctx, p2_stage_a, 1, 1024, 0, s, w.plan, w.selbits, w.p2_table, w.status);
   stage_end(ctx, s);
   stage_begin(ctx, decoding ? ST_DEC_P2_ENGINE : ST_P2_ENGINE, s);
-  // the selection bitset lives in shared memory when |P| fits (checked on the
-  // device: the smem variant falls back to the global words past kSmemBits)
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(p2_engine_win<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBitsBytes);
@@ -548,10 +499,10 @@ void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t 
   }
   if (((n_bound + 31) / 32) * 4 <= static_cast<uint64_t>(kSmemBitsBytes)) {
     GP_LAUNCH(ctx, p2_engine_win<true>, 1, 1024, ((n_bound + 31) / 32) * 4, s, w.plan, w.p2_sets, w.p2_off,
-              w.p2_size, w.p2_members, w.selbits, w.first_touch, w.status);
+              w.p2_count, w.p2_members, w.p2_single, w.selbits, w.first_touch, w.status);
   } else {
-    GP_LAUNCH(ctx, p2_engine_dispatch, 1, 1024, kSmemBitsBytes, s, w.plan, w.p2_sets, w.p2_off, w.p2_size,
-              w.p2_members, w.selbits, w.first_touch, w.status);
+    GP_LAUNCH(ctx, p2_engine_dispatch, 1, 1024, kSmemBitsBytes, s, w.plan, w.p2_sets, w.p2_off, w.p2_count,
+              w.p2_members, w.p2_single, w.selbits, w.first_touch, w.status);
   }
   stage_end(ctx, s);
   const uint64_t ptiles = (n_bound + kTile - 1) / kTile;

@@ -23,8 +23,12 @@
 // Decode: fit_parse (parse_fit + reorder checks), reorder_unpack (entries,
 // permutation check), fit_eval (fp64 Horner without FMA, sign unfold,
 // permutation scatter) — bit-exact for a given container.
+#include <cooperative_groups.h>
+
 #include "gp_ctx.hpp"
 #include "gp_device.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace gp {
 
@@ -241,6 +245,196 @@ __global__ void __launch_bounds__(1024) fit_segment(Plan* plan, const double* __
   }
 }
 
+// Grid-cooperative segmentation: every make_piece (curvefit.cpp:50-67) is one
+// sweep in which all blocks scan a slice of the piece, write their block-best
+// (dev, arg) to a double-buffered partial array, grid.sync(), and every block
+// reduces the partials in block order (same result everywhere, same tie rule:
+// max dev, lowest index).  The piece list is replicated per block; children
+// of a split are only evaluated when another split can follow.
+struct SweepRange {
+  uint32_t begin, end;
+};
+
+__device__ void seg_sweep(const double* __restrict__ t, const SweepRange* rr, int nr, uint32_t mp, double* pdev,
+                          uint32_t* parg, Piece* out, double* sdev, uint32_t* sarg, cg::grid_group& grid) {
+  const uint32_t G = gridDim.x;
+  for (int q = 0; q < nr; ++q) {
+    const uint32_t b = rr[q].begin, e = rr[q].end, len = e - b;
+    double best = 0.0;
+    uint32_t arg = 0;
+    if (len >= 3) {
+      const double y0 = t[b];
+      const double slope = __ddiv_rn(__dsub_rn(t[e - 1], y0), static_cast<double>(len - 1));
+      for (uint32_t i = b + 1 + blockIdx.x * blockDim.x + threadIdx.x; i + 1 < e; i += G * blockDim.x) {
+        const double pred = __dadd_rn(y0, __dmul_rn(slope, static_cast<double>(i - b)));
+        const double d = __dsub_rn(t[i], pred);
+        const double d2 = __dmul_rn(d, d);
+        if (d2 > best) {
+          best = d2;
+          arg = i;
+        }
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(kFull, best, o);
+      const uint32_t oa = __shfl_xor_sync(kFull, arg, o);
+      if (ob > best || (ob == best && ob > 0.0 && oa < arg)) {
+        best = ob;
+        arg = oa;
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      sdev[threadIdx.x >> 5] = best;
+      sarg[threadIdx.x >> 5] = arg;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double bb = 0.0;
+      uint32_t aa = 0;
+      for (uint32_t w = 0; w < blockDim.x / 32; ++w)
+        if (sdev[w] > bb || (sdev[w] == bb && bb > 0.0 && sarg[w] < aa)) {
+          bb = sdev[w];
+          aa = sarg[w];
+        }
+      pdev[q * G + blockIdx.x] = bb;
+      parg[q * G + blockIdx.x] = aa;
+    }
+    __syncthreads();
+  }
+  grid.sync();
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < nr; ++q) {
+      double bb = 0.0;
+      uint32_t aa = 0;
+      for (uint32_t j = 0; j < G; ++j) {
+        const double v = pdev[q * G + j];
+        const uint32_t a = parg[q * G + j];
+        if (v > bb || (v == bb && bb > 0.0 && a < aa)) {
+          bb = v;
+          aa = a;
+        }
+      }
+      Piece p{rr[q].begin, rr[q].end, aa, 0u, bb};
+      p.live = (bb > 0.0 && aa - p.begin >= mp && p.end - aa >= mp) ? 1u : 0u;
+      out[q] = p;
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) fit_segment_coop(Plan* plan, const double* __restrict__ t, int degree,
+                                                        int max_segments, double* pdev, uint32_t* parg,
+                                                        uint32_t* status) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sdev[32];
+  __shared__ uint32_t sarg[32];
+  __shared__ Piece pieces[kMaxSeg];
+  __shared__ Piece res[2];
+  __shared__ int s_best;
+  // uniform exit decisions only (every block must reach every grid.sync)
+  if (failed(status) || !fit_active(plan)) return;
+  const uint64_t n = plan->n_values;
+  const uint32_t l = plan->sign_split;
+  const uint32_t un = static_cast<uint32_t>(n);
+  uint32_t pb[2], pe[2];
+  int nparts = 0;
+  if (l > 0) {
+    pb[nparts] = 0;
+    pe[nparts++] = l;
+  }
+  if (l < un) {
+    pb[nparts] = l;
+    pe[nparts++] = un;
+  }
+  const uint32_t mp = static_cast<uint32_t>(degree + 1 > 1 ? degree + 1 : 1);
+  const uint32_t G = gridDim.x;
+  int sweep = 0;
+  uint32_t nseg = 0;
+  bool overflow = false;
+  for (int pi = 0; pi < nparts && !overflow; ++pi) {
+    const uint32_t b = pb[pi], e = pe[pi], len = e - b;
+    int budget;
+    if (max_segments > 0) {  // curvefit.cpp:473-481
+      const long long share = static_cast<long long>(max_segments) * static_cast<long long>(len) /
+                              static_cast<long long>(n);
+      budget = share > 1 ? static_cast<int>(share) : 1;
+      if (pi + 1 == nparts) budget = max_segments - static_cast<int>(nseg) > 1 ? max_segments - static_cast<int>(nseg) : 1;
+    } else if (len < 4) {
+      budget = 1;
+    } else {  // part_budget (curvefit.cpp:101-110, :424-428)
+      const double km = fabs(__dsub_rn(__dsub_rn(t[b], t[b + 1]), __dsub_rn(t[e - 2], t[e - 1])));
+      const double p = ceil(2.0 * sqrt(km > 0.0 ? km : 0.0));
+      const int kc = static_cast<int>(p) > 1 ? static_cast<int>(p) : 1;
+      budget = kc + 1 < 0xffff ? kc + 1 : 0xffff;
+    }
+    int np = 1;
+    if (budget > 1) {
+      SweepRange r0{0, len};
+      seg_sweep(t + b, &r0, 1, mp, pdev + (sweep & 1) * 2 * G, parg + (sweep & 1) * 2 * G, res, sdev, sarg, grid);
+      ++sweep;
+      if (threadIdx.x == 0) pieces[0] = res[0];
+    } else if (threadIdx.x == 0) {
+      pieces[0] = Piece{0, len, 0, 0u, 0.0};
+    }
+    __syncthreads();
+    while (np < budget) {
+      if (threadIdx.x == 0) {
+        int best = -1;
+        for (int i = 0; i < np; ++i) {
+          if (!pieces[i].live) continue;
+          if (best < 0 || pieces[i].dev > pieces[best].dev ||
+              (pieces[i].dev == pieces[best].dev && pieces[i].begin < pieces[best].begin))
+            best = i;
+        }
+        s_best = best;
+      }
+      __syncthreads();
+      const int best = s_best;
+      if (best < 0) break;
+      if (nseg + np + 1 > static_cast<uint32_t>(kMaxSeg)) {
+        overflow = true;
+        break;
+      }
+      const Piece pp = pieces[best];
+      Piece left{pp.begin, pp.arg, 0, 0u, 0.0}, right{pp.arg, pp.end, 0, 0u, 0.0};
+      if (np + 1 < budget) {  // another split may follow: evaluate both children
+        SweepRange rr[2] = {{pp.begin, pp.arg}, {pp.arg, pp.end}};
+        seg_sweep(t + b, rr, 2, mp, pdev + (sweep & 1) * 2 * G, parg + (sweep & 1) * 2 * G, res, sdev, sarg, grid);
+        ++sweep;
+        left = res[0];
+        right = res[1];
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        pieces[best] = left;
+        pieces[np] = right;
+      }
+      ++np;
+      __syncthreads();
+    }
+    if (overflow) break;
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+      for (int i = 1; i < np; ++i) {  // sort by begin
+        const Piece v = pieces[i];
+        int j = i;
+        while (j > 0 && pieces[j - 1].begin > v.begin) {
+          pieces[j] = pieces[j - 1];
+          --j;
+        }
+        pieces[j] = v;
+      }
+      for (int i = 0; i < np; ++i) plan->seg_end[nseg + i] = b + pieces[i].end;
+    }
+    nseg += static_cast<uint32_t>(np);
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (overflow) latch(status, GP_CAPACITY);
+    plan->nseg = nseg;
+    plan->degree = static_cast<uint32_t>(degree);
+  }
+}
+
 // ---------------------------------------------------------------- least squares
 __device__ __forceinline__ void seg_range(const Plan* plan, uint32_t s, uint32_t& b, uint32_t& e) {
   b = s == 0 ? 0 : plan->seg_end[s - 1];
@@ -319,11 +513,28 @@ __global__ void __launch_bounds__(256) fit_accumulate(const Plan* plan, const do
 // one block per segment; thread 0 solves (sizes are <= 8x8)
 __global__ void fit_solve(Plan* plan, const double* __restrict__ t, const double* __restrict__ partial,
                           const uint32_t* status) {
+  __shared__ double sacc[kAcc];
   if (failed(status) || !fit_active(plan)) return;
   const uint32_t seg = blockIdx.x;
-  if (seg >= plan->nseg || threadIdx.x != 0) return;
+  if (seg >= plan->nseg) return;
   uint32_t b, e;
   seg_range(plan, seg, b, e);
+  {  // chunk partials of this segment, summed in chunk order, one accumulator per thread
+    uint64_t c0 = 0;
+    for (uint32_t s2 = 0; s2 < seg; ++s2) {
+      uint32_t bb, ee;
+      seg_range(plan, s2, bb, ee);
+      c0 += (ee - bb + kChunk - 1) / kChunk;
+    }
+    const uint64_t ncs = (e - b + kChunk - 1) / kChunk;
+    if (threadIdx.x < kAcc) {
+      double v = 0.0;
+      for (uint64_t c = 0; c < ncs; ++c) v += partial[(c0 + c) * kAcc + threadIdx.x];
+      sacc[threadIdx.x] = v;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
   const uint32_t len = e - b;
   const int deg = static_cast<int>(plan->degree);
   float* out = plan->coeffs + seg * kCps;
@@ -343,9 +554,9 @@ __global__ void fit_solve(Plan* plan, const double* __restrict__ t, const double
   }
   const uint64_t nc = (len + kChunk - 1) / kChunk;
   double acc[kAcc];
-  for (int j = 0; j < kAcc; ++j) acc[j] = 0.0;
-  for (uint64_t c = 0; c < nc; ++c)
-    for (int j = 0; j < kAcc; ++j) acc[j] += partial[(first + c) * kAcc + j];
+  for (int j = 0; j < kAcc; ++j) acc[j] = sacc[j];
+  (void)nc;
+  (void)first;
   double G[kCps][kCps], rhs[kCps];
   int a = 0;
   for (int j = 0; j <= kMaxDeg; ++j)
@@ -581,10 +792,25 @@ void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, 
   GP_LAUNCH(ctx, fit_keys, grid_for(ctx, n_bound, 256), 256, 0, s, w.values, w.plan, w.u32a, w.u32b, w.status);
   launch_radix_sort(ctx, w.u32a, w.u32b, w.u32c, w.u32d, &w.plan->n_values, n_bound, 32, s);
   GP_LAUNCH(ctx, fit_prepare, grid_for(ctx, n_bound, 256), 256, 0, s, w.values, w.u32b, w.plan, w.f64b, w.status);
-  GP_LAUNCH(ctx, fit_segment, 1, 1024, 0, s, w.plan, w.f64b, degree, max_segments, w.status);
+  {  // cooperative launch: every block of the grid must be resident
+    static int grid = 0;
+    if (!grid) {
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fit_segment_coop, 256, 0);
+      grid = std::max(1, std::min(per_sm, 2)) * ctx->sm_count;
+    }
+    const double* t = w.f64b;
+    Plan* plan = w.plan;
+    double* pdev = w.seg_dev;
+    uint32_t* parg = w.seg_arg;
+    uint32_t* st = w.status;
+    void* args[] = {&plan, &t, &degree, &max_segments, &pdev, &parg, &st};
+    cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fit_segment_coop), grid, 256, args, 0, s);
+    ++ctx->launches;
+  }
   const uint64_t chunks = n_bound / kChunk + kMaxSeg + 1;
   GP_LAUNCH(ctx, fit_accumulate, static_cast<int>(chunks), 256, 0, s, w.plan, w.f64b, w.partial, w.status);
-  GP_LAUNCH(ctx, fit_solve, kMaxSeg, 32, 0, s, w.plan, w.f64b, w.partial, w.status);
+  GP_LAUNCH(ctx, fit_solve, kMaxSeg, 64, 0, s, w.plan, w.f64b, w.partial, w.status);
   GP_LAUNCH(ctx, fit_emit, 1, 32, 0, s, w.plan, out, w.status);
   GP_LAUNCH(ctx, reorder_pack, grid_for(ctx, n_bound * 4, 256), 256, 0, s, w.u32b, w.plan, out, w.status);
 }
