@@ -58,7 +58,8 @@ bool is_bloom(int m) { return m >= GP_INDEX_BLOOM_P0 && m <= GP_INDEX_BLOOM_NAIV
 // Methods with a device implementation on this path (the rest of FORMAT.md's
 // registry returns GP_UNSUPPORTED).
 bool index_supported(int m) {
-  return m == GP_INDEX_NONE || m == GP_INDEX_BITMAP || m == GP_INDEX_BLOOM_P0 || m == GP_INDEX_BLOOM_P2 ||
+  return m == GP_INDEX_NONE || m == GP_INDEX_BITMAP || m == GP_INDEX_BLOOM_P0 || m == GP_INDEX_BLOOM_P1 ||
+         m == GP_INDEX_BLOOM_P2 ||
          m == GP_INDEX_BLOOM_PD || m == GP_INDEX_BLOOM_NAIVE;
 }
 bool value_supported(int m) { return m == GP_VALUE_NONE || m == GP_VALUE_RAW_F64 || m == GP_VALUE_FIT_POLY; }
@@ -146,6 +147,7 @@ void carve(Workspace& w, uint8_t* base, uint64_t D) {
   w.p2_off = c.take<uint32_t>(w.set_cap + 1);
   w.p2_single = c.take<uint32_t>(w.set_cap);
   w.p2_cursor = c.take<uint32_t>(w.set_cap);
+  w.p2_alloc = c.take<uint32_t>(64);
   w.p2_sets = c.take<uint32_t>(w.set_cap);
   w.p2_table = c.take<uint32_t>(256 * (w.set_cap / 4096 + 1) + 256);
   w.pairs = c.take<uint32_t>(w.pair_cap);
@@ -405,6 +407,8 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
       GP_STAGE(ctx, ST_BLOOM_SCAN, s, launch_bloom_scan(ctx, d, pi.m, false, s));
       if (im == GP_INDEX_BLOOM_P2)
         launch_select_p2(ctx, d, pi.m, pi.k, false, s);
+      else if (im == GP_INDEX_BLOOM_P1)
+        GP_STAGE(ctx, ST_SELECT, s, launch_select_p1(ctx, d, r, s));
       else
         GP_STAGE(ctx, ST_SELECT, s, launch_select_slice(ctx, d, s));
       GP_STAGE(ctx, ST_GATHER, s, launch_gather_values(ctx, d_dense, d, s));
@@ -477,6 +481,8 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const u
                                            launch_bloom_scan(ctx, bound, 0, true, s));
       if (im == GP_INDEX_BLOOM_P2)
         launch_select_p2(ctx, bound, ctx->ws.set_cap, 64, true, s);
+      else if (im == GP_INDEX_BLOOM_P1)
+        GP_STAGE(ctx, ST_DEC_SELECT, s, launch_select_p1(ctx, bound, bound, s));
       else
         GP_STAGE(ctx, ST_DEC_SELECT, s, launch_select_slice(ctx, bound, s));
     }

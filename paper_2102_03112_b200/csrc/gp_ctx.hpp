@@ -79,6 +79,7 @@ struct Workspace {
   uint32_t* p2_off = nullptr;     // [set_cap + 1]
   uint32_t* p2_single = nullptr;  // member of size-1 sets [set_cap]
   uint32_t* p2_cursor = nullptr;  // scatter cursors [set_cap]
+  uint32_t* p2_alloc = nullptr;   // bucket-space allocator word
   uint32_t* p2_sets = nullptr;    // [set_cap]
   uint32_t* p2_table = nullptr;   // [256 * set_cap / 4096 + 256]
   uint32_t* p2_members = nullptr; // [pair_cap]
@@ -197,6 +198,8 @@ void launch_bloom_build(gp_ctx* ctx, uint8_t* out, uint64_t m, uint64_t r, cudaS
 void launch_bloom_parse(gp_ctx* ctx, const uint8_t* in, uint64_t m_bound, cudaStream_t s);
 void launch_bloom_scan(gp_ctx* ctx, uint64_t d_bound, uint64_t m_host, bool decoding, cudaStream_t s);
 void launch_select_slice(gp_ctx* ctx, uint64_t n_bound, cudaStream_t s);
+void launch_select_p1(gp_ctx* ctx, uint64_t n_bound, uint64_t r_bound, cudaStream_t s);
+void launch_flags_compact(gp_ctx* ctx, int method, uint64_t n_bound, cudaStream_t s);
 void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t k_bound, bool decoding,
                       cudaStream_t s);
 

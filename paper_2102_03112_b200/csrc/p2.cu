@@ -5,14 +5,14 @@
 // positions; a bit's set is the ascending, de-duplicated list of positives
 // probing it; sets are ordered by (size, bit).  Device form:
 //   pairs    : one thread per positive, k positions de-duplicated in
-//              registers, per-bit distinct counts = set sizes (atomics); the
-//              first joiner of a bit is its member if the set stays size 1
-//   offsets  : exclusive scan of the multi-set sizes over [0, m); stage-A
-//              selection of every singleton's member
-//   scatter  : multi-set members into per-bit buckets, then an ascending sort
-//              per bucket (buckets hold 2-~20 entries)
+//              registers, per-bit distinct counts = set sizes (atomics)
+//   tiles    : per 4096-bit tile: bucket space for multi sets from a global
+//              cursor, and the tile's histogram of set sizes
+//   scatter  : per pair: a singleton's member is recorded and selected
+//              (stage A); multi-set members go to their bucket
 //   order    : one stable counting-sort pass by size over the bit domain,
-//              which also compacts away empty bits → sets in (size, bit) order
+//              which also compacts away empty bits → sets in (size, bit)
+//              order; each multi bucket is sorted ascending on the way
 //
 // p2_select: pass 1 first visits every singleton (bit order) and selects its
 // member.  Singleton members are always true keys (a false positive's probes
@@ -42,14 +42,26 @@ __device__ __forceinline__ bool p2_active(const Plan* plan) {
   return plan->index_method == GP_INDEX_BLOOM_P2;
 }
 
+// count[0, m] = 0 with m read on the device (decode only knows it there)
+__global__ void p2_zero_counts(const Plan* plan, uint32_t* count, uint64_t m_cap, const uint32_t* status) {
+  if (failed(status) || !p2_active(plan)) return;
+  const uint64_t n = (plan->m < m_cap ? plan->m : m_cap) + 1;
+  const uint64_t n4 = n / 4;
+  uint4* c4 = reinterpret_cast<uint4*>(count);
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    c4[i] = make_uint4(0, 0, 0, 0);
+  for (uint64_t i = 4 * n4 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    count[i] = 0;
+}
+
 // One thread per positive p: its k probe positions, de-duplicated among
 // themselves (one positive joins a set once, the consecutive-duplicate rule of
-// bloom.cpp:159-164), so count[bit] ends as the set's size.  The first
-// joiner of a bit records itself in single[bit]: for a size-1 set it is the
-// member.
+// bloom.cpp:159-164), so count[bit] ends as the set's size (fire-and-forget
+// atomics).
 __global__ void p2_pairs(const uint32_t* __restrict__ P, Plan* plan, uint32_t* __restrict__ pairs,
-                         uint32_t* __restrict__ count, uint32_t* __restrict__ single, uint64_t pair_cap,
-                         uint64_t set_cap, uint32_t* status) {
+                         uint32_t* __restrict__ count, uint64_t pair_cap, uint64_t set_cap, uint32_t* status) {
   if (failed(status) || !p2_active(plan)) return;
   const uint64_t n = plan->n_pos, m = plan->m;
   const uint32_t k = plan->k;
@@ -71,116 +83,82 @@ __global__ void p2_pairs(const uint32_t* __restrict__ P, Plan* plan, uint32_t* _
       for (uint32_t i = 0; i < j; ++i) dup |= seen[i] == bit;
       seen[j] = bit;
       pairs[p * k + j] = dup ? 0xFFFFFFFFu : bit;
-      if (!dup && atomicAdd(&count[bit], 1u) == 0) single[bit] = static_cast<uint32_t>(p);
+      if (!dup) atomicAdd(&count[bit], 1u);
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) plan->n_pairs = n * k;
 }
 
-// Exclusive scan of the multi-set sizes (count >= 2, else 0) into off[0, m];
-// also arms the scatter cursors and writes the stage-A selections: the member
-// of every size-1 set (singletons are visited first, p2_select pass 1).
-__global__ void __launch_bounds__(kTileBlock) p2_offsets(const uint32_t* __restrict__ count,
-                                                         const uint32_t* __restrict__ single, Plan* plan,
-                                                         uint32_t* __restrict__ off, uint32_t* __restrict__ cursor,
-                                                         uint32_t* selbits, uint64_t* tiles, uint32_t* ticket,
-                                                         uint32_t* status) {
-  __shared__ uint64_t sh[36];
-  __shared__ uint32_t slot;
-  if (failed(status) || !p2_active(plan)) return;
-  const uint64_t m = plan->m;
-  const uint64_t ntiles = (m + kTile - 1) / kTile;
-  while (true) {
-    const uint32_t tile = claim_tile(ticket, &slot);
-    if (tile >= ntiles) break;
-    const uint64_t base = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(threadIdx.x) * kTileItems;
-    uint32_t c[kTileItems];
-    uint64_t sum = 0;
-#pragma unroll
-    for (int q = 0; q < kTileItems; ++q) {
-      const uint32_t v = base + q < m ? count[base + q] : 0;
-      if (v == 1) {
-        const uint32_t mem = single[base + q];
-        atomicOr(&selbits[mem >> 5], 1u << (mem & 31));
-      }
-      if (v >= kMaxSetSize) latch(status, GP_CAPACITY);
-      c[q] = v >= 2 ? v : 0;
-      sum += c[q];
-    }
-    uint64_t tot;
-    uint64_t o = tile_exclusive_offset<kTileBlock>(sum, tile, tiles, sh, tot);
-#pragma unroll
-    for (int q = 0; q < kTileItems; ++q) {
-      if (base + q < m) {
-        off[base + q] = static_cast<uint32_t>(o);
-        if (c[q]) cursor[base + q] = c[q];
-      }
-      o += c[q];
-    }
-    if (tile == ntiles - 1 && threadIdx.x == kTileBlock - 1) off[m] = static_cast<uint32_t>(o);
-  }
-}
-
-// multi-set members into their buckets (arbitrary order within a bucket)
-__global__ void p2_scatter(const uint32_t* __restrict__ pairs, const Plan* plan, const uint32_t* __restrict__ count,
-                           const uint32_t* __restrict__ off, uint32_t* cursor, uint32_t* __restrict__ members,
-                           const uint32_t* status) {
-  if (failed(status) || !p2_active(plan)) return;
-  const uint64_t np = plan->n_pairs;
-  const uint32_t k = plan->k;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < np;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint32_t bit = pairs[i];
-    if (bit == 0xFFFFFFFFu || count[bit] < 2) continue;
-    const uint32_t slot = off[bit] + atomicSub(&cursor[bit], 1u) - 1u;
-    members[slot] = static_cast<uint32_t>(i / k);
-  }
-}
-
-// ascending members per multi set (sizes are small)
-__global__ void p2_sort_buckets(const Plan* plan, const uint32_t* __restrict__ off, uint32_t* __restrict__ members,
-                                const uint32_t* status) {
-  if (failed(status) || !p2_active(plan)) return;
-  const uint64_t m = plan->m;
-  for (uint64_t b = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; b < m;
-       b += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint32_t lo = off[b], n = off[b + 1] - lo;
-    if (n < 2) continue;
-    uint32_t* mem = members + lo;
-    for (uint32_t i = 1; i < n; ++i) {
-      const uint32_t v = mem[i];
-      uint32_t j = i;
-      while (j > 0 && mem[j - 1] > v) {
-        mem[j] = mem[j - 1];
-        --j;
-      }
-      mem[j] = v;
-    }
-  }
-}
-
-// Stable counting sort of the non-empty bits by size (digit = size <= 255):
-// upsweep per-tile histograms into table[digit * ntiles + tile] ...
-__global__ void __launch_bounds__(kTileBlock) p2_size_hist(const Plan* plan, const uint32_t* __restrict__ size,
-                                                           uint32_t* __restrict__ table, const uint32_t* status) {
+// One 4096-bit tile per block: bucket space for multi sets (count >= 2) from a
+// global cursor (warp-aggregated; the CSR needs contiguity, not bit order),
+// scatter cursors, and the tile's histogram of set sizes for the (size, bit)
+// ordering (digit-major table[size * ntiles + tile]).
+__global__ void __launch_bounds__(kTileBlock) p2_tiles(const uint32_t* __restrict__ count, Plan* plan,
+                                                       uint32_t* __restrict__ off, uint32_t* __restrict__ cursor,
+                                                       uint32_t* __restrict__ table, uint32_t* alloc,
+                                                       uint32_t* status) {
   __shared__ uint32_t h[256];
   if (failed(status) || !p2_active(plan)) return;
   const uint64_t m = plan->m;
   const uint64_t ntiles = (m + kTile - 1) / kTile;
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    h[threadIdx.x] = 0;
-    __syncthreads();
-    const uint64_t base = tile * kTile;
-    for (int q = threadIdx.x; q < kTile; q += kTileBlock) {
-      const uint64_t b = base + q;
-      if (b < m) {
-        const uint32_t s = size[b];
-        if (s) atomicAdd(&h[s], 1u);
+  const uint64_t tile = blockIdx.x;
+  if (tile >= ntiles) return;
+  __shared__ uint32_t sh32[33];
+  __shared__ uint32_t s_base;
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  uint32_t c[kTileItems];
+  uint32_t need = 0;
+#pragma unroll
+  for (int q = 0; q < kTileItems; ++q) {
+    const uint64_t b = tile * kTile + static_cast<uint64_t>(q) * kTileBlock + threadIdx.x;
+    c[q] = b < m ? count[b] : 0;
+    if (c[q] >= kMaxSetSize) latch(status, GP_CAPACITY);
+    if (c[q]) atomicAdd(&h[c[q] < 255 ? c[q] : 255], 1u);
+    need += c[q] >= 2 ? c[q] : 0;
+  }
+  uint32_t tot;
+  uint32_t o = block_exclusive_sum<uint32_t, kTileBlock>(need, sh32, tot);
+  if (threadIdx.x == 0) s_base = tot ? atomicAdd(alloc, tot) : 0;  // one allocation per tile
+  __syncthreads();
+  o += s_base;
+#pragma unroll
+  for (int q = 0; q < kTileItems; ++q) {
+    if (c[q] >= 2) {
+      const uint64_t b = tile * kTile + static_cast<uint64_t>(q) * kTileBlock + threadIdx.x;
+      off[b] = o;
+      cursor[b] = c[q];
+      o += c[q];
+    }
+  }
+  table[threadIdx.x * ntiles + tile] = h[threadIdx.x];
+}
+
+// One thread per positive p and its k pairs: a size-1 set's member is
+// selected in stage A (every singleton is visited first, p2_select pass 1;
+// plain byte flags, idempotent) and recorded in single[]; multi-set members
+// go to their bucket (arbitrary order, sorted later).
+__global__ void p2_scatter(const uint32_t* __restrict__ pairs, const Plan* plan, const uint32_t* __restrict__ count,
+                           const uint32_t* __restrict__ off, uint32_t* cursor, uint32_t* __restrict__ members,
+                           uint32_t* __restrict__ single, uint8_t* __restrict__ flags, const uint32_t* status) {
+  if (failed(status) || !p2_active(plan)) return;
+  const uint64_t n = plan->n_pos;
+  const uint32_t k = plan->k;
+  for (uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; p < n;
+       p += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    bool sel = false;
+    for (uint32_t j = 0; j < k; ++j) {
+      const uint32_t bit = pairs[p * k + j];
+      if (bit == 0xFFFFFFFFu) continue;
+      const uint32_t c = count[bit];
+      if (c == 1) {
+        single[bit] = static_cast<uint32_t>(p);
+        sel = true;
+      } else {
+        members[off[bit] + atomicSub(&cursor[bit], 1u) - 1u] = static_cast<uint32_t>(p);
       }
     }
-    __syncthreads();
-    table[threadIdx.x * ntiles + tile] = h[threadIdx.x];
-    __syncthreads();
+    flags[p] = sel ? 1 : 0;
   }
 }
 
@@ -191,64 +169,99 @@ __global__ void p2_count_sets(Plan* plan, const uint32_t* __restrict__ table, co
   if (failed(status) || !p2_active(plan) || threadIdx.x != 0) return;
   const uint64_t ntiles = (plan->m + kTile - 1) / kTile;
   plan->n_sets = table[255 * ntiles + ntiles - 1];  // digit 255 is empty: its prefix is the grand total
+  const uint64_t n1 = table[2 * ntiles] - table[1 * ntiles];  // sets of size 1
+  plan->n_multi = plan->n_sets - n1;
+  plan->n_cand = n1;  // first multi set in the (size, bit) order
+  plan->n_single_sel = 0;  // counted by p2_stage_a
 }
 
-// ... and the stable downsweep: sets[table[digit][tile] + rank] = bit.
+// Stable placement of the non-empty bits by size (counting sort over the
+// digit table): sets[table[size][tile] + rank] = bit, one tile per block; the
+// thread placing a multi set also sorts its bucket ascending (2-~20 entries).
 __global__ void __launch_bounds__(kTileBlock) p2_size_scatter(const Plan* plan, const uint32_t* __restrict__ size,
                                                               const uint32_t* __restrict__ table,
+                                                              const uint32_t* __restrict__ off,
+                                                              uint32_t* __restrict__ members,
                                                               uint32_t* __restrict__ sets, const uint32_t* status) {
   __shared__ uint32_t run[256];
   __shared__ uint32_t wcnt[kTileBlock / 32][256];
   if (failed(status) || !p2_active(plan)) return;
   const uint64_t m = plan->m;
   const uint64_t ntiles = (m + kTile - 1) / kTile;
+  const uint64_t tile = blockIdx.x;
+  if (tile >= ntiles) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    run[threadIdx.x] = table[threadIdx.x * ntiles + tile];
+  run[threadIdx.x] = table[threadIdx.x * ntiles + tile];
+  __syncthreads();
+  const uint64_t base = tile * kTile;
+  for (int round = 0; round < kTileItems; ++round) {
+    const uint64_t b = base + static_cast<uint64_t>(round) * kTileBlock + threadIdx.x;
+    const uint32_t s = b < m ? size[b] : 0;
+    const unsigned peers = __match_any_sync(kFull, s);
+    const uint32_t lrank = __popc(peers & ((1u << lane) - 1));
+    for (int i = lane; i < 256; i += 32) wcnt[warp][i] = 0;
+    __syncwarp();
+    if (lrank == 0) wcnt[warp][s] = __popc(peers);
     __syncthreads();
-    const uint64_t base = tile * kTile;
-    for (int round = 0; round < kTileItems; ++round) {
-      const uint64_t b = base + static_cast<uint64_t>(round) * kTileBlock + threadIdx.x;
-      const uint32_t s = b < m ? size[b] : 0;
-      const uint32_t dig = s;  // 0 = empty bit, not emitted
-      const unsigned peers = __match_any_sync(kFull, dig);
-      const uint32_t lrank = __popc(peers & ((1u << lane) - 1));
-      for (int i = lane; i < 256; i += 32) wcnt[warp][i] = 0;
-      __syncwarp();
-      if ((peers & ((1u << lane) - 1)) == 0) wcnt[warp][dig] = __popc(peers);
-      __syncthreads();
+    if (s) {
       uint32_t before = 0;
-      for (int w2 = 0; w2 < warp; ++w2) before += wcnt[w2][dig];
-      if (s) sets[run[dig] + before + lrank] = static_cast<uint32_t>(b);
-      __syncthreads();
-      // advance running offsets by this round's per-digit totals
-      {
-        uint32_t tot = 0;
-        for (int w2 = 0; w2 < kTileBlock / 32; ++w2) tot += wcnt[w2][threadIdx.x];
-        run[threadIdx.x] += tot;
-      }
-      __syncthreads();
+      for (int w2 = 0; w2 < warp; ++w2) before += wcnt[w2][s];
+      sets[run[s] + before + lrank] = static_cast<uint32_t>(b);
     }
+    if (s >= 2) {  // ascending members of this set (independent loads, sort in registers)
+      uint32_t* mem = members + off[b];
+      if (s <= 16) {
+        uint32_t v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = i < static_cast<int>(s) ? mem[i] : 0xFFFFFFFFu;
+#pragma unroll
+        for (int i = 1; i < 16; ++i)  // insertion sort network over the padded array
+#pragma unroll
+          for (int j = i; j > 0; --j)
+            if (v[j - 1] > v[j]) {
+              const uint32_t t = v[j];
+              v[j] = v[j - 1];
+              v[j - 1] = t;
+            }
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (i < static_cast<int>(s)) mem[i] = v[i];
+      } else {
+        for (uint32_t i = 1; i < s; ++i) {
+          const uint32_t x = mem[i];
+          uint32_t j = i;
+          while (j > 0 && mem[j - 1] > x) {
+            mem[j] = mem[j - 1];
+            --j;
+          }
+          mem[j] = x;
+        }
+      }
+    }
+    __syncthreads();
+    uint32_t tot = 0;
+    for (int w2 = 0; w2 < kTileBlock / 32; ++w2) tot += wcnt[w2][threadIdx.x];
+    run[threadIdx.x] += tot;
+    __syncthreads();
   }
 }
 
-// stage-A count (distinct singleton members) and the singleton/multi split
-__global__ void __launch_bounds__(1024) p2_stage_a(Plan* plan, const uint32_t* __restrict__ selbits,
-                                                   const uint32_t* __restrict__ table, const uint32_t* status) {
-  __shared__ uint64_t sh[40];
+// stage A as a bitset over P (ballot of the byte flags, one word per warp
+// iteration) and its population count
+__global__ void p2_stage_a(Plan* plan, const uint8_t* __restrict__ flags, uint32_t* __restrict__ selbits,
+                           const uint32_t* status) {
   if (failed(status) || !p2_active(plan)) return;
-  const uint64_t nw = (plan->n_pos + 31) / 32;
-  uint64_t c = 0;
-  for (uint64_t i = threadIdx.x; i < nw; i += 1024) c += __popc(selbits[i]);
-  uint64_t tot;
-  block_exclusive_sum<uint64_t, 1024>(c, sh, tot);
-  if (threadIdx.x == 0) {
-    const uint64_t ntiles = (plan->m + kTile - 1) / kTile;
-    const uint64_t n1 = table[2 * ntiles] - table[1 * ntiles];  // sets of size 1
-    plan->n_single_sel = tot;
-    plan->n_multi = plan->n_sets - n1;
-    plan->n_cand = n1;  // first multi set index in the sorted list
+  const uint64_t n = plan->n_pos;
+  const uint64_t nw = (n + 31) / 32;
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32);
+  uint32_t c = 0;
+  for (uint64_t w = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) / 32; w < nw; w += warps) {
+    const uint64_t p = 32 * w + (threadIdx.x & 31);
+    const unsigned bits = __ballot_sync(kFull, p < n && flags[p]);
+    if ((threadIdx.x & 31) == 0) selbits[w] = bits;
+    c += __popc(bits);
   }
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(reinterpret_cast<unsigned long long*>(&plan->n_single_sel), c);
 }
 
 __device__ __forceinline__ bool bs_test(const uint32_t* bs, uint32_t p) { return (bs[p >> 5] >> (p & 31)) & 1u; }
@@ -466,29 +479,34 @@ __global__ void __launch_bounds__(kTileBlock) flags_compact(const uint32_t* __re
 
 }  // namespace
 
+void launch_flags_compact(gp_ctx* ctx, int method, uint64_t n_bound, cudaStream_t s) {
+  Workspace& w = ctx->ws;
+  const uint64_t ptiles = (n_bound + kTile - 1) / kTile;
+  reset_scan(ctx, s, ptiles + 1);
+  GP_LAUNCH(ctx, flags_compact, grid_for(ctx, ptiles * kTileBlock, kTileBlock), kTileBlock, 0, s, w.pos, w.selbits,
+            w.plan, method, w.sel, w.tiles, w.ticket, w.status);
+}
+
 void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t k_bound, bool decoding,
                       cudaStream_t s) {
   Workspace& w = ctx->ws;
   stage_begin(ctx, decoding ? ST_DEC_P2_SETS : ST_P2_SETS, s);
   const uint64_t m_cap = std::min<uint64_t>(m_bound, w.set_cap);
-  cudaMemsetAsync(w.p2_count, 0, (m_cap + 1) * sizeof(uint32_t), s);
-  cudaMemsetAsync(w.selbits, 0, ((n_bound + 31) / 32) * 4, s);
-  GP_LAUNCH(ctx, p2_pairs, grid_for(ctx, n_bound, 128), 128, 0, s, w.pos, w.plan, w.pairs, w.p2_count, w.p2_single,
-            w.pair_cap, w.set_cap, w.status);
+  GP_LAUNCH(ctx, p2_zero_counts, ctx->sm_count * 4, 256, 0, s, w.plan, w.p2_count, m_cap, w.status);
+  cudaMemsetAsync(w.p2_alloc, 0, sizeof(uint32_t), s);
+  GP_LAUNCH(ctx, p2_pairs, grid_for(ctx, n_bound, 128), 128, 0, s, w.pos, w.plan, w.pairs, w.p2_count, w.pair_cap,
+            w.set_cap, w.status);
   const uint64_t mtiles = (m_cap + kTile - 1) / kTile;
-  reset_scan(ctx, s, mtiles + 1);
-  GP_LAUNCH(ctx, p2_offsets, grid_for(ctx, mtiles * kTileBlock, kTileBlock), kTileBlock, 0, s, w.p2_count,
-            w.p2_single, w.plan, w.p2_off, w.p2_cursor, w.selbits, w.tiles, w.ticket, w.status);
-  const uint64_t pair_bound = std::min<uint64_t>(n_bound * k_bound, w.pair_cap);
-  GP_LAUNCH(ctx, p2_scatter, grid_for(ctx, pair_bound, 256), 256, 0, s, w.pairs, w.plan, w.p2_count, w.p2_off,
-            w.p2_cursor, w.p2_members, w.status);
-  GP_LAUNCH(ctx, p2_sort_buckets, grid_for(ctx, m_cap, 256), 256, 0, s, w.plan, w.p2_off, w.p2_members, w.status);
-  const int tgrid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(mtiles, ctx->sm_count * 4ULL)));
-  GP_LAUNCH(ctx, p2_size_hist, tgrid, kTileBlock, 0, s, w.plan, w.p2_count, w.p2_table, w.status);
+  const int tgrid = static_cast<int>(std::max<uint64_t>(1, mtiles));
+  GP_LAUNCH(ctx, p2_tiles, tgrid, kTileBlock, 0, s, w.p2_count, w.plan, w.p2_off, w.p2_cursor, w.p2_table, w.p2_alloc,
+            w.status);
+  GP_LAUNCH(ctx, p2_scatter, grid_for(ctx, n_bound, 128), 128, 0, s, w.pairs, w.plan, w.p2_count, w.p2_off,
+            w.p2_cursor, w.p2_members, w.p2_single, w.flags, w.status);
   launch_table_scan(ctx, w.p2_table, &w.plan->m, m_cap, 12, s);
   GP_LAUNCH(ctx, p2_count_sets, 1, 32, 0, s, w.plan, w.p2_table, w.status);
-  GP_LAUNCH(ctx, p2_size_scatter, tgrid, kTileBlock, 0, s, w.plan, w.p2_count, w.p2_table, w.p2_sets, w.status);
-  GP_LAUNCH(ctx, p2_stage_a, 1, 1024, 0, s, w.plan, w.selbits, w.p2_table, w.status);
+  GP_LAUNCH(ctx, p2_size_scatter, tgrid, kTileBlock, 0, s, w.plan, w.p2_count, w.p2_table, w.p2_off, w.p2_members,
+            w.p2_sets, w.status);
+  GP_LAUNCH(ctx, p2_stage_a, grid_for(ctx, n_bound, 256), 256, 0, s, w.plan, w.flags, w.selbits, w.status);
   stage_end(ctx, s);
   stage_begin(ctx, decoding ? ST_DEC_P2_ENGINE : ST_P2_ENGINE, s);
   static bool attr = false;
@@ -505,10 +523,7 @@ void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t 
               w.p2_members, w.p2_single, w.selbits, w.first_touch, w.status);
   }
   stage_end(ctx, s);
-  const uint64_t ptiles = (n_bound + kTile - 1) / kTile;
-  reset_scan(ctx, s, ptiles + 1);
-  GP_LAUNCH(ctx, flags_compact, grid_for(ctx, ptiles * kTileBlock, kTileBlock), kTileBlock, 0, s, w.pos, w.selbits,
-            w.plan, static_cast<int>(GP_INDEX_BLOOM_P2), w.sel, w.tiles, w.ticket, w.status);
+  launch_flags_compact(ctx, GP_INDEX_BLOOM_P2, n_bound, s);
 }
 
 }  // namespace gp

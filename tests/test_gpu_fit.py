@@ -67,7 +67,7 @@ def _check_container(got: bytes, want: bytes, oracle):
     assert np.max(np.abs(v1 - v2)) <= 1e-5 * max(1e-30, np.abs(v2).max())
 
 
-@pytest.mark.parametrize("im", [BITMAP, P0, P2, PD])
+@pytest.mark.parametrize("im", [BITMAP, P0, 5, P2, PD])
 def test_fit_encode_matches_oracle(codec, oracle, im):
     from paper_2102_03112_b200 import PipelineConfig
     for d, r, fpr, deg, ms in [(1000, 10, 0.01, 5, 0), (65539, 655, 0.001, 5, 0), (269722, 2697, 0.01, 3, 0),

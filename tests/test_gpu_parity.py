@@ -138,7 +138,7 @@ def test_decode_error_classes_match_oracle(codec, oracle):
             assert float(dense.abs().sum()) == 0.0  # a failed decode never touches the output
 
 
-BLOOM_CASES = [(P0, V_NONE), (P2, V_NONE), (PD, V_NONE), (NAIVE, V_NONE), (P2, V_F64)]
+BLOOM_CASES = [(P0, V_NONE), (P1, V_NONE), (P2, V_NONE), (PD, V_NONE), (NAIVE, V_NONE), (P2, V_F64)]
 
 
 @pytest.mark.parametrize("im,vm", BLOOM_CASES)
