@@ -58,7 +58,8 @@ bool is_bloom(int m) { return m >= GP_INDEX_BLOOM_P0 && m <= GP_INDEX_BLOOM_NAIV
 // Methods with a device implementation on this path (the rest of FORMAT.md's
 // registry returns GP_UNSUPPORTED).
 bool index_supported(int m) {
-  return m == GP_INDEX_NONE || m == GP_INDEX_BITMAP || m == GP_INDEX_BLOOM_P0 || m == GP_INDEX_BLOOM_P1 ||
+  return m == GP_INDEX_NONE || m == GP_INDEX_BITMAP || m == GP_INDEX_RLE || m == GP_INDEX_BLOOM_P0 ||
+         m == GP_INDEX_BLOOM_P1 ||
          m == GP_INDEX_BLOOM_P2 ||
          m == GP_INDEX_BLOOM_PD || m == GP_INDEX_BLOOM_NAIVE;
 }
@@ -319,7 +320,7 @@ uint64_t gp_max_container_bytes(uint64_t d, uint64_t r, const gp_pipeline_config
   switch (cfg->index_method) {
     case GP_INDEX_NONE: il = 4 * r; break;
     case GP_INDEX_BITMAP: il = (d + 7) / 8; break;
-    case GP_INDEX_RLE: il = (d + 7) / 8 * 11 / 8 + 16; break;  // <= 1 + 8 * (runs * <=10 groups)
+    case GP_INDEX_RLE: il = d + 2; break;  // <= one group per coordinate, + the polarity byte
     default: {
       uint64_t m = 0;
       uint32_t k = 0;
@@ -401,6 +402,7 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
   switch (im) {
     case GP_INDEX_NONE: launch_index_none(ctx, d_out, r, s); break;
     case GP_INDEX_BITMAP: launch_index_bitmap(ctx, d_out, d, r, s); break;
+    case GP_INDEX_RLE: GP_STAGE(ctx, ST_INDEX, s, launch_index_rle(ctx, d_out, d, r, s)); break;
     default: {
       GP_STAGE(ctx, ST_BLOOM_BUILD, s, launch_bloom_build(ctx, d_out, pi.m, r, s));
       if (im == GP_INDEX_BLOOM_NAIVE) break;  // values stay in support order (pipeline.cpp:196-199)
@@ -476,6 +478,7 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const u
   switch (im) {
     case GP_INDEX_NONE: launch_decode_index_none(ctx, d_in, bound, s); break;
     case GP_INDEX_BITMAP: launch_decode_index_bitmap(ctx, d_in, bound, s); break;
+    case GP_INDEX_RLE: GP_STAGE(ctx, ST_DEC_INDEX, s, launch_decode_index_rle(ctx, d_in, len, bound, s)); break;
     default: {
       GP_STAGE(ctx, ST_DEC_BLOOM_SCAN, s, launch_bloom_parse(ctx, d_in, ctx->ws.m_cap, s);
                                            launch_bloom_scan(ctx, bound, 0, true, s));

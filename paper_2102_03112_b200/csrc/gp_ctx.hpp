@@ -192,6 +192,8 @@ void launch_index_bitmap(gp_ctx* ctx, uint8_t* out, uint64_t d, uint64_t r, cuda
 void launch_decode_index_none(gp_ctx* ctx, const uint8_t* in, uint64_t r_bound, cudaStream_t s);
 void launch_validate_support(gp_ctx* ctx, uint64_t r_bound, cudaStream_t s);
 void launch_decode_index_bitmap(gp_ctx* ctx, const uint8_t* in, uint64_t d_bound, cudaStream_t s);
+void launch_index_rle(gp_ctx* ctx, uint8_t* out, uint64_t d, uint64_t r, cudaStream_t s);          // rle.cu
+void launch_decode_index_rle(gp_ctx* ctx, const uint8_t* in, uint64_t len_bound, uint64_t d_bound, cudaStream_t s);
 
 // bloom.cu / p2.cu
 void launch_bloom_build(gp_ctx* ctx, uint8_t* out, uint64_t m, uint64_t r, cudaStream_t s);

@@ -1,0 +1,425 @@
+// rle.cu — K3/K4: the run-length index payload (id 2; rle_encode/rle_decode,
+// codecs.cpp:34-70; LEB128 groups inside the bit stream, bitio.hpp:79-99).
+//
+// Wire: 1 polarity bit (coordinate 0), then one varint per run, every group
+// a full byte at bit offset 1 + 8t.  Byte t of the payload is therefore
+// (group[t-1] >> 7) | (group[t] << 1) (byte 0: polarity | group[0] << 1), and
+// the last byte is group[G-1] >> 7 = 0 since a varint's last group has a clear
+// high bit.  Payload = G + 1 bytes.
+//
+// Encode from the ascending support: 1-runs are maximal chains of consecutive
+// keys (ordered compaction of chain starts), each followed by its 0-gap; one
+// thread per chain sizes its groups, a scan places them, the bytes are emitted
+// with the one-bit shift.
+//
+// Decode reproduces the sequential reader's first failure exactly: groups are
+// split into varints at their terminators, run lengths are scanned, and the
+// first varint (in stream order) that is too long (> 10 groups), zero, or
+// overruns d — or the absence of a completing run (truncation) — decides the
+// error; a completed stream must end with < 8 zero slack bits.  The bitmap is
+// the prefix-XOR of run-boundary toggles, and the support its set bits.
+#include "gp_ctx.hpp"
+#include "gp_device.cuh"
+
+namespace gp {
+
+namespace {
+
+constexpr int kBlock = 256;
+constexpr int kItems = 16;
+constexpr int kTile = kBlock * kItems;
+
+__device__ __forceinline__ uint32_t vgroups(uint64_t x) {
+  uint32_t g = 1;
+  while (x >= 128) {
+    x >>= 7;
+    ++g;
+  }
+  return g;
+}
+
+__device__ __forceinline__ uint32_t put_varint(uint8_t* grp, uint64_t x) {
+  uint32_t g = 0;
+  do {
+    uint8_t b = x & 0x7f;
+    x >>= 7;
+    if (x) b |= 0x80;
+    grp[g++] = b;
+  } while (x);
+  return g;
+}
+
+// ---------------------------------------------------------------- encode
+__global__ void __launch_bounds__(kBlock) rle_starts(const uint32_t* __restrict__ sup, uint64_t r,
+                                                     uint32_t* __restrict__ starts, Plan* plan, uint64_t* tiles,
+                                                     uint32_t* ticket, const uint32_t* status) {
+  __shared__ uint64_t sh[36];
+  __shared__ uint32_t slot;
+  if (failed(status)) return;
+  const uint64_t ntiles = (r + kTile - 1) / kTile;
+  while (true) {
+    const uint32_t tile = claim_tile(ticket, &slot);
+    if (tile >= ntiles) break;
+    const uint64_t base = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(threadIdx.x) * kItems;
+    uint32_t mask = 0;
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+      const uint64_t i = base + q;
+      if (i < r && (i == 0 || sup[i - 1] + 1 != sup[i])) mask |= 1u << q;
+    }
+    uint64_t tot;
+    uint64_t o = tile_exclusive_offset<kBlock>(__popc(mask), tile, tiles, sh, tot);
+    while (mask) {
+      const int q = __ffs(mask) - 1;
+      starts[o++] = static_cast<uint32_t>(base + q);
+      mask &= mask - 1;
+    }
+    if (tile == ntiles - 1 && threadIdx.x == kBlock - 1) plan->n_runs = o;
+  }
+}
+
+// group count of chain k (its 1-run + the following 0-gap); exclusive scan
+__global__ void __launch_bounds__(kBlock) rle_sizes(const uint32_t* __restrict__ sup, uint64_t r, uint64_t d,
+                                                    const uint32_t* __restrict__ starts, Plan* plan,
+                                                    uint32_t* __restrict__ goff, uint64_t* tiles, uint32_t* ticket,
+                                                    const uint32_t* status) {
+  __shared__ uint64_t sh[36];
+  __shared__ uint32_t slot;
+  if (failed(status)) return;
+  const uint64_t R = plan->n_runs;
+  const uint64_t lead = sup[0] > 0 ? vgroups(sup[0]) : 0;  // the leading 0-run
+  const uint64_t ntiles = (R + kTile - 1) / kTile;
+  while (true) {
+    const uint32_t tile = claim_tile(ticket, &slot);
+    if (tile >= ntiles) break;
+    const uint64_t base = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(threadIdx.x) * kItems;
+    uint32_t g[kItems];
+    uint64_t sum = 0;
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+      const uint64_t k = base + q;
+      g[q] = 0;
+      if (k < R) {
+        const uint64_t i0 = starts[k], i1 = k + 1 < R ? starts[k + 1] : r;
+        const uint64_t end = sup[i0] + (i1 - i0);
+        const uint64_t gap = (k + 1 < R ? sup[i1] : d) - end;
+        g[q] = vgroups(i1 - i0) + (gap ? vgroups(gap) : 0);
+      }
+      sum += g[q];
+    }
+    uint64_t tot;
+    uint64_t o = tile_exclusive_offset<kBlock>(sum, tile, tiles, sh, tot) + lead;
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+      if (base + q < R) goff[base + q] = static_cast<uint32_t>(o);
+      o += g[q];
+    }
+    if (tile == ntiles - 1 && threadIdx.x == kBlock - 1) {
+      plan->n_groups = o;
+      plan->il = o + 1;
+    }
+  }
+}
+
+__global__ void rle_groups(const uint32_t* __restrict__ sup, uint64_t r, uint64_t d,
+                           const uint32_t* __restrict__ starts, const uint32_t* __restrict__ goff, const Plan* plan,
+                           uint8_t* __restrict__ grp, const uint32_t* status) {
+  if (failed(status)) return;
+  const uint64_t R = plan->n_runs;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && sup[0] > 0) put_varint(grp, sup[0]);
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < R;
+       k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i0 = starts[k], i1 = k + 1 < R ? starts[k + 1] : r;
+    const uint64_t end = sup[i0] + (i1 - i0);
+    const uint64_t gap = (k + 1 < R ? sup[i1] : d) - end;
+    uint8_t* g = grp + goff[k];
+    g += put_varint(g, i1 - i0);
+    if (gap) put_varint(g, gap);
+  }
+}
+
+__global__ void rle_emit(const uint8_t* __restrict__ grp, const uint32_t* __restrict__ sup, const Plan* plan,
+                         uint8_t* out, const uint32_t* status) {
+  if (failed(status)) return;
+  const uint64_t G = plan->n_groups;
+  const uint8_t pol = sup[0] == 0 ? 1 : 0;
+  uint8_t* p = out + 49;
+  for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t <= G;
+       t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t lo = t == 0 ? pol : (grp[t - 1] >> 7);
+    const uint32_t hi = t < G ? static_cast<uint32_t>(grp[t]) << 1 : 0u;
+    p[t] = static_cast<uint8_t>(lo | hi);
+  }
+}
+
+// ---------------------------------------------------------------- decode
+__device__ __forceinline__ uint32_t group_at(const uint8_t* p, uint64_t t) {
+  return ((p[t] >> 1) | (p[t + 1] << 7)) & 0xFFu;
+}
+
+// terminator groups (high bit clear) in order: varint v ends at ends[v]
+__global__ void __launch_bounds__(kBlock) rle_ends(const uint8_t* __restrict__ in, Plan* plan,
+                                                   uint32_t* __restrict__ ends, uint64_t* tiles, uint32_t* ticket,
+                                                   const uint32_t* status) {
+  __shared__ uint64_t sh[36];
+  __shared__ uint32_t slot;
+  if (failed(status) || plan->index_method != GP_INDEX_RLE) return;
+  const uint8_t* p = in + plan->off_index;
+  const uint64_t n = plan->il;
+  const uint64_t gav = n >= 1 ? n - 1 : 0;  // complete groups in the stream
+  const uint64_t ntiles = (gav + kTile - 1) / kTile;
+  while (true) {
+    const uint32_t tile = claim_tile(ticket, &slot);
+    if (tile >= ntiles) break;
+    const uint64_t base = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(threadIdx.x) * kItems;
+    uint32_t mask = 0;
+#pragma unroll
+    for (int q = 0; q < kItems; ++q)
+      if (base + q < gav && !(group_at(p, base + q) & 0x80u)) mask |= 1u << q;
+    uint64_t tot;
+    uint64_t o = tile_exclusive_offset<kBlock>(__popc(mask), tile, tiles, sh, tot);
+    while (mask) {
+      const int q = __ffs(mask) - 1;
+      ends[o++] = static_cast<uint32_t>(base + q);
+      mask &= mask - 1;
+    }
+    if (tile == ntiles - 1 && threadIdx.x == kBlock - 1) plan->n_runs = o;
+  }
+  if (gav == 0 && blockIdx.x == 0 && threadIdx.x == 0) plan->n_runs = 0;
+}
+
+// run length of varint v (a varint longer than 10 groups is flagged in rle_events)
+__global__ void rle_values(const uint8_t* __restrict__ in, const Plan* plan, const uint32_t* __restrict__ ends,
+                           uint64_t* __restrict__ runs, const uint32_t* status) {
+  if (failed(status) || plan->index_method != GP_INDEX_RLE) return;
+  const uint8_t* p = in + plan->off_index;
+  const uint64_t V = plan->n_runs;
+  for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < V;
+       v += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t start = v == 0 ? 0 : ends[v - 1] + 1ull;
+    const uint64_t len = ends[v] - start + 1;
+    uint64_t x = 0;
+    for (uint64_t q = 0; q < len && q < 10; ++q) x |= static_cast<uint64_t>(group_at(p, start + q) & 0x7fu) << (7 * q);
+    // saturate at d + 1 (any run > d overruns; keeps the u64 scan in range)
+    runs[v] = x > plan->d ? plan->d + 1 : x;
+  }
+}
+
+// inclusive scan of run lengths (u64), tiles of 4096 varints
+__global__ void __launch_bounds__(kBlock) rle_scan(const Plan* plan, const uint64_t* __restrict__ runs,
+                                                   uint64_t* __restrict__ cum, uint64_t* tiles, uint32_t* ticket,
+                                                   const uint32_t* status) {
+  __shared__ uint64_t sh[36];
+  __shared__ uint32_t slot;
+  if (failed(status) || plan->index_method != GP_INDEX_RLE) return;
+  const uint64_t V = plan->n_runs;
+  const uint64_t ntiles = (V + kTile - 1) / kTile;
+  while (true) {
+    const uint32_t tile = claim_tile(ticket, &slot);
+    if (tile >= ntiles) break;
+    const uint64_t base = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(threadIdx.x) * kItems;
+    uint64_t x[kItems];
+    uint64_t sum = 0;
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+      x[q] = base + q < V ? runs[base + q] : 0;
+      sum += x[q];
+    }
+    uint64_t tot;
+    uint64_t o = tile_exclusive_offset<kBlock>(sum, tile, tiles, sh, tot);
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+      o += x[q];
+      if (base + q < V) cum[base + q] = o;
+    }
+  }
+}
+
+// first event in stream order: (v << 2) | type, type 0 long, 1 zero, 2 overrun, 3 done
+__global__ void rle_events(const uint8_t* __restrict__ in, const Plan* plan, const uint32_t* __restrict__ ends,
+                           const uint64_t* __restrict__ runs, const uint64_t* __restrict__ cum,
+                           unsigned long long* first, const uint32_t* status) {
+  if (failed(status) || plan->index_method != GP_INDEX_RLE) return;
+  const uint64_t V = plan->n_runs, d = plan->d;
+  for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < V;
+       v += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t start = v == 0 ? 0 : ends[v - 1] + 1ull;
+    const uint64_t len = ends[v] - start + 1;
+    const uint64_t before = v == 0 ? 0 : cum[v - 1];
+    int type = -1;
+    if (len > 10) type = 0;
+    else if (runs[v] == 0) type = 1;
+    else if (runs[v] > d - before) type = 2;
+    else if (cum[v] == d) type = 3;
+    if (type >= 0) atomicMin(first, (static_cast<unsigned long long>(v) << 2) | static_cast<unsigned>(type));
+  }
+}
+
+// decide: error class, or the number of runs and the slack check
+__global__ void rle_finish(const uint8_t* __restrict__ in, Plan* plan, const uint32_t* __restrict__ ends,
+                           const unsigned long long* first, uint32_t* status) {
+  if (failed(status) || plan->index_method != GP_INDEX_RLE) return;
+  const uint8_t* p = in + plan->off_index;
+  const uint64_t n = plan->il, V = plan->n_runs;
+  if (n == 0) return latch(status, GP_TRUNCATED);  // no polarity bit
+  const unsigned long long f = *first;
+  if (f == ~0ULL) {  // no terminating event among the complete varints
+    const uint64_t gav = n - 1;
+    const uint64_t tail = gav - (V ? ends[V - 1] + 1ull : 0);  // continuation groups after the last varint
+    return latch(status, tail >= 10 ? GP_CORRUPT_PAYLOAD : GP_TRUNCATED);
+  }
+  const uint64_t v = f >> 2;
+  const int type = static_cast<int>(f & 3);
+  if (type != 3) return latch(status, GP_CORRUPT_PAYLOAD);
+  const uint64_t e = ends[v];  // last group used
+  if (n != e + 2) return latch(status, GP_CORRUPT_PAYLOAD);            // >= 8 slack bits
+  if ((p[e + 1] >> 1) != 0) return latch(status, GP_CORRUPT_PAYLOAD);  // nonzero slack
+  plan->n_runs = v + 1;
+  plan->pd_variant = p[0] & 1u;  // polarity (scratch field on the decode path)
+}
+
+__global__ void rle_toggles(const Plan* plan, const uint64_t* __restrict__ cum, uint32_t* __restrict__ tog,
+                            const uint32_t* status) {
+  if (failed(status) || plan->index_method != GP_INDEX_RLE) return;
+  const uint64_t V = plan->n_runs, d = plan->d;
+  for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < V;
+       v += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t c = cum[v];
+    if (c < d) atomicOr(&tog[c >> 5], 1u << (c & 31));
+  }
+}
+
+// bitmap = polarity XOR prefix-XOR(toggles); word parity carried by a scan
+__global__ void __launch_bounds__(kBlock) rle_bitmap(const Plan* plan, uint32_t* __restrict__ words, uint64_t* tiles,
+                                                     uint32_t* ticket, const uint32_t* status) {
+  __shared__ uint64_t sh[36];
+  __shared__ uint32_t slot;
+  if (failed(status) || plan->index_method != GP_INDEX_RLE) return;
+  const uint64_t d = plan->d, nw = (d + 31) / 32;
+  const uint32_t pol = plan->pd_variant ? 0xFFFFFFFFu : 0u;
+  const uint64_t ntiles = (nw + kTile - 1) / kTile;
+  while (true) {
+    const uint32_t tile = claim_tile(ticket, &slot);
+    if (tile >= ntiles) break;
+    const uint64_t base = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(threadIdx.x) * kItems;
+    uint32_t x[kItems];
+    uint64_t c = 0;
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+      x[q] = base + q < nw ? words[base + q] : 0u;
+      c += __popc(x[q]);
+    }
+    uint64_t tot;
+    uint64_t o = tile_exclusive_offset<kBlock>(c, tile, tiles, sh, tot);
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+      uint32_t y = x[q];
+      y ^= y << 1;
+      y ^= y << 2;
+      y ^= y << 4;
+      y ^= y << 8;
+      y ^= y << 16;
+      uint32_t b = y ^ ((o & 1) ? 0xFFFFFFFFu : 0u) ^ pol;
+      o += __popc(x[q]);
+      const uint64_t w = base + q;
+      if (w < nw) {
+        if (w == nw - 1 && (d & 31)) b &= (1u << (d & 31)) - 1u;
+        words[w] = b;
+      }
+    }
+  }
+}
+
+// set bits of the bitmap → ascending support (sel), n_sel; popcount must be r
+__global__ void __launch_bounds__(kBlock) rle_support(const uint32_t* __restrict__ words, Plan* plan,
+                                                      uint32_t* __restrict__ sel, uint64_t cap, uint64_t* tiles,
+                                                      uint32_t* ticket, const uint32_t* status) {
+  __shared__ uint64_t sh[36];
+  __shared__ uint32_t slot;
+  if (failed(status) || plan->index_method != GP_INDEX_RLE) return;
+  const uint64_t nw = (plan->d + 31) / 32;
+  const uint64_t ntiles = (nw + kTile - 1) / kTile;
+  while (true) {
+    const uint32_t tile = claim_tile(ticket, &slot);
+    if (tile >= ntiles) break;
+    const uint64_t base = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(threadIdx.x) * kItems;
+    uint32_t x[kItems];
+    uint64_t c = 0;
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+      x[q] = base + q < nw ? words[base + q] : 0u;
+      c += __popc(x[q]);
+    }
+    uint64_t tot;
+    uint64_t o = tile_exclusive_offset<kBlock>(c, tile, tiles, sh, tot);
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+      uint32_t y = x[q];
+      while (y) {
+        const int b = __ffs(y) - 1;
+        if (o < cap) sel[o] = static_cast<uint32_t>(32 * (base + q) + b);
+        ++o;
+        y &= y - 1;
+      }
+    }
+    if (tile == ntiles - 1 && threadIdx.x == kBlock - 1) {
+      plan->n_sel = o;
+      plan->n_values = o;
+    }
+  }
+}
+
+__global__ void rle_check(Plan* plan, uint32_t* status) {
+  if (failed(status) || plan->index_method != GP_INDEX_RLE) return;
+  if (plan->n_sel != plan->r) latch(status, GP_CORRUPT_PAYLOAD);  // pipeline.cpp:249-250
+}
+
+__global__ void rle_reset(unsigned long long* first) { *first = ~0ULL; }
+
+}  // namespace
+
+void launch_index_rle(gp_ctx* ctx, uint8_t* out, uint64_t d, uint64_t r, cudaStream_t s) {
+  Workspace& w = ctx->ws;
+  const uint64_t rt = (r + kTile - 1) / kTile;
+  reset_scan(ctx, s, rt + 1);
+  GP_LAUNCH(ctx, rle_starts, grid_for(ctx, rt * kBlock, kBlock), kBlock, 0, s, w.support, r, w.u32a, w.plan, w.tiles,
+            w.ticket, w.status);
+  reset_scan(ctx, s, rt + 1);
+  GP_LAUNCH(ctx, rle_sizes, grid_for(ctx, rt * kBlock, kBlock), kBlock, 0, s, w.support, r, d, w.u32a, w.plan, w.u32b,
+            w.tiles, w.ticket, w.status);
+  GP_LAUNCH(ctx, rle_groups, grid_for(ctx, r, 256), 256, 0, s, w.support, r, d, w.u32a, w.u32b, w.plan, w.scratch,
+            w.status);
+  GP_LAUNCH(ctx, rle_emit, grid_for(ctx, d + 1, 256), 256, 0, s, w.scratch, w.support, w.plan, out, w.status);
+}
+
+void launch_decode_index_rle(gp_ctx* ctx, const uint8_t* in, uint64_t len_bound, uint64_t d_bound, cudaStream_t s) {
+  Workspace& w = ctx->ws;
+  unsigned long long* first = reinterpret_cast<unsigned long long*>(w.p2_alloc + 2);
+  uint64_t* runs = reinterpret_cast<uint64_t*>(w.f64a);
+  uint64_t* cum = reinterpret_cast<uint64_t*>(w.f64b);
+  const uint64_t gt = (len_bound + kTile - 1) / kTile;
+  GP_LAUNCH(ctx, rle_reset, 1, 1, 0, s, first);
+  reset_scan(ctx, s, gt + 1);
+  GP_LAUNCH(ctx, rle_ends, grid_for(ctx, gt * kBlock, kBlock), kBlock, 0, s, in, w.plan, w.u32a, w.tiles, w.ticket,
+            w.status);
+  GP_LAUNCH(ctx, rle_values, grid_for(ctx, len_bound, 256), 256, 0, s, in, w.plan, w.u32a, runs, w.status);
+  reset_scan(ctx, s, gt + 1);
+  GP_LAUNCH(ctx, rle_scan, grid_for(ctx, gt * kBlock, kBlock), kBlock, 0, s, w.plan, runs, cum, w.tiles, w.ticket,
+            w.status);
+  GP_LAUNCH(ctx, rle_events, grid_for(ctx, len_bound, 256), 256, 0, s, in, w.plan, w.u32a, runs, cum, first,
+            w.status);
+  GP_LAUNCH(ctx, rle_finish, 1, 1, 0, s, in, w.plan, w.u32a, first, w.status);
+  const uint64_t nw = (d_bound + 31) / 32;
+  cudaMemsetAsync(w.u32c, 0, nw * 4, s);
+  GP_LAUNCH(ctx, rle_toggles, grid_for(ctx, len_bound, 256), 256, 0, s, w.plan, cum, w.u32c, w.status);
+  const uint64_t wt = (nw + kTile - 1) / kTile;
+  reset_scan(ctx, s, wt + 1);
+  GP_LAUNCH(ctx, rle_bitmap, grid_for(ctx, wt * kBlock, kBlock), kBlock, 0, s, w.plan, w.u32c, w.tiles, w.ticket,
+            w.status);
+  reset_scan(ctx, s, wt + 1);
+  GP_LAUNCH(ctx, rle_support, grid_for(ctx, wt * kBlock, kBlock), kBlock, 0, s, w.u32c, w.plan, w.sel,
+            static_cast<uint64_t>(ctx->max_d), w.tiles, w.ticket, w.status);
+  GP_LAUNCH(ctx, rle_check, 1, 1, 0, s, w.plan, w.status);
+}
+
+}  // namespace gp
