@@ -164,6 +164,15 @@ GP_API int gp_bloom_positive_scan(gp_ctx* ctx, const uint8_t* d_filter, uint64_t
 GP_API int gp_bloom_select(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter_len, uint64_t d,
                     uint64_t r, int index_method, uint32_t* d_selected, void* stream);
 
+/* volume (container.cpp:148-243) of a HOST copy of a packed container: exact
+ * bit accounting; bits per nonzero = total_bits / r.  Host-only. */
+typedef struct gp_volume_report {
+  uint64_t index_bits, value_bits, reorder_bits, metadata_bits, total_bits;
+  double ratio_dense;   /* total / (32 d) */
+  double ratio_sparse;  /* total / (64 r); 0 when r = 0 */
+} gp_volume_report;
+GP_API int gp_volume(const uint8_t* h_container, uint64_t len, gp_volume_report* out);
+
 /* bloom_params (bloom.cpp:22-31).  Host arithmetic, returns GP_ERROR on bad args. */
 GP_API int gp_bloom_params(double epsilon, uint64_t r, uint64_t* m, uint32_t* k);
 

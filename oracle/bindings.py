@@ -95,6 +95,8 @@ class CpuCodec:
         bind("decode", [_P(_u8), C.c_size_t, _P(_u64), _P(_P(_u32)), _P(_P(C.c_double)),
                         _P(_u64)])
         bind("decode_accumulate", [_P(_u8), C.c_size_t, _P(C.c_double), _u64, C.c_double])
+        if prefix == "gpr":
+            bind("volume", [_P(_u8), C.c_size_t, _P(_u64)])
         if prefix == "gpo":
             bind("rle_encode", [_P(_u32), _u64, _u64, _P(_P(_u8)), _P(C.c_size_t)])
             bind("bitmap_bytes", [_P(_u32), _u64, _u64, _P(_u8)])
@@ -211,6 +213,16 @@ class CpuCodec:
         self._check(self._f["decode_accumulate"](_u8p(a), a.size,
                                                  dense.ctypes.data_as(_P(C.c_double)), dense.size,
                                                  scale))
+
+    def volume(self, data: bytes) -> dict:
+        """volume() of a packed container (reference build only)."""
+        a = np.frombuffer(bytes(data), dtype=np.uint8).copy()
+        out = np.zeros(7, dtype=np.uint64)
+        self._check(self._f["volume"](_u8p(a), a.size, out.ctypes.data_as(_P(_u64))))
+        keys = ["index_bits", "value_bits", "reorder_bits", "metadata_bits", "total_bits"]
+        rep = {k: int(v) for k, v in zip(keys, out[:5])}
+        rep["ratio_dense"], rep["ratio_sparse"] = out[5:7].view(np.float64).tolist()
+        return rep
 
     # restatement-only helpers
     def rle_encode(self, support, d) -> bytes:

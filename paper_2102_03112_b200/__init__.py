@@ -8,5 +8,5 @@ C-ABI of include/gradpack_b200.h.
 from .api import (  # noqa: F401
     CapacityError, ChecksumError, Codec, CorruptPayloadError, CudaError, DecodeError, Error, FitError,
     IndexMethod, PipelineConfig, TruncatedError, UnknownMethodError, UnsupportedMethodError, ValueMethod,
-    bloom_params,
+    bloom_params, volume,
 )

@@ -30,6 +30,14 @@ class GpConfig(C.Structure):
     ]
 
 
+class GpVolume(C.Structure):
+    """gp_volume_report — VolumeReport (container.hpp:75-83)."""
+
+    _fields_ = [("index_bits", C.c_uint64), ("value_bits", C.c_uint64), ("reorder_bits", C.c_uint64),
+                ("metadata_bits", C.c_uint64), ("total_bits", C.c_uint64), ("ratio_dense", C.c_double),
+                ("ratio_sparse", C.c_double)]
+
+
 _P = C.POINTER
 _vp = C.c_void_p
 _u64 = C.c_uint64
@@ -57,6 +65,7 @@ _SIGS = {
     "gp_crc32c": ([_vp, _vp, _u64, _vp, _vp], C.c_int),
     "gp_bloom_positive_scan": ([_vp, _vp, _u64, _u64, _vp, _u64, _vp, _vp], C.c_int),
     "gp_bloom_select": ([_vp, _vp, _u64, _u64, _u64, C.c_int, _vp, _vp], C.c_int),
+    "gp_volume": ([_vp, _u64, _P(GpVolume)], C.c_int),
     "gp_bloom_params": ([C.c_double, _u64, _P(_u64), _P(C.c_uint32)], C.c_int),
 }
 

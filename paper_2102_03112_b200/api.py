@@ -25,7 +25,7 @@ from dataclasses import dataclass, field
 
 import torch
 
-from ._lib import GpConfig, lib
+from ._lib import GpConfig, GpVolume, lib
 
 
 # ---------------------------------------------------------------- errors (errors.hpp:21-53)
@@ -276,6 +276,17 @@ class Codec:
         self._raise(lib.gp_crc32c(self._ctx, _ptr(data), data.numel(), _ptr(out), _stream()))
         self.status()
         return int(out.item()) & 0xFFFFFFFF
+
+
+def volume(container: bytes) -> dict:
+    """volume (container.cpp:148-243) of a packed container held on the host:
+    exact bit accounting; bits per nonzero = total_bits / r."""
+    buf = (C.c_uint8 * max(1, len(container))).from_buffer_copy(bytes(container) or b"\0")
+    rep = GpVolume()
+    rc = lib.gp_volume(buf, len(container), C.byref(rep))
+    if rc != 0:
+        raise _STATUS.get(rc, Error)(f"volume: status {rc}")
+    return {f: getattr(rep, f) for f, _ in GpVolume._fields_}
 
 
 def bloom_params(epsilon: float, r: int) -> tuple[int, int]:

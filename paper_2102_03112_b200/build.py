@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
-SOURCES = ["capi.cu", "topr.cu", "container.cu", "indexcodec.cu", "values.cu", "bloom.cu", "p2.cu", "p1.cu", "rle.cu", "sort.cu", "values_fit.cu"]
+SOURCES = ["capi.cu", "topr.cu", "container.cu", "indexcodec.cu", "values.cu", "bloom.cu", "p2.cu", "p1.cu", "rle.cu", "sort.cu", "values_fit.cu", "volume.cpp"]
 
 
 def _run(cmd):
@@ -38,7 +38,7 @@ def build(verbose: bool = False) -> str:
     newest_dep = max(os.path.getmtime(p) for p in deps)
     for src in SOURCES:
         path = os.path.join(CSRC, src)
-        obj = os.path.join(OBJ, src.replace(".cu", ".o"))
+        obj = os.path.join(OBJ, src.rsplit(".", 1)[0] + ".o")
         if (not os.path.exists(obj) or os.path.getmtime(obj) < os.path.getmtime(path)
                 or os.path.getmtime(obj) < newest_dep):
             out = _run([NVCC, *ARCH, *FLAGS, "-c", path, "-o", obj])
