@@ -2,24 +2,33 @@
 
 The real-process form of the reference's simulated worker loop
 (Simulation::step, harness.cpp:219-293): every rank is one worker with its
-own full d-element gradient; it runs top_r + compress_gradient + pack on its
-device (pipeline seed = Simulation::pipeline_seed(seed, rank, step),
-harness.cpp:201-203), the variable-length containers are exchanged with an
-NCCL allgather — sizes first, then the payloads padded to the largest size
-(NCCL has no allgatherv) — and every rank decodes all N containers in rank
-order into the dense mean (harness.cpp:274-284, f32 accumulate of x/N).
+own full d-element gradient; it runs top_r + compress_gradient + pack
+(pipeline seed = Simulation::pipeline_seed(seed, rank, step),
+harness.cpp:201-203); the variable-length containers are exchanged with an
+allgather — sizes first, then the payloads padded to the largest size (NCCL
+has no allgatherv) — and every rank decodes all N containers in rank order
+into the dense mean (harness.cpp:274-284: f32 accumulate of value / N).
 
-torch.distributed is plumbing only (process group, NCCL communicator); the
-payload bytes are produced and consumed by libgradpack_b200.so.  The same
-code runs on CPU tensors with the gloo backend (tests/test_dp_gloo.py), where
-a host-side codec stands in for the device codec.
+torch.distributed is plumbing only (process group, NCCL communicator); every
+payload byte is produced and consumed by the codec.  The codec is duck-typed
+(encode_into / decode_accumulate / max_container_bytes) so the same exchange
+runs on CUDA tensors with NCCL and on CPU tensors with gloo, where the tests
+plug in a CPU stand-in codec (tests/test_dp_gloo.py).
+
+BucketedSparseAllgather splits very large gradients (BERT-large, 340M) into
+independent per-bucket containers — a convention of this framework with no
+reference equivalent: bucket b of a rank's step uses seed
+hash64(b, pipeline_seed(seed, rank, step)) and r_b = max(1, llround(ratio*d_b)).
+Buckets are spread over several codec contexts on their own CUDA streams, so
+encode, exchange and decode of different buckets overlap.
 """
 from __future__ import annotations
 
+import math
+from dataclasses import replace
+
 import torch
 import torch.distributed as dist
-
-from .api import Codec, PipelineConfig
 
 GAMMA = 0x9E3779B97F4A7C15
 MASK = (1 << 64) - 1
@@ -47,43 +56,101 @@ def pipeline_seed(seed: int, worker: int, step: int) -> int:
 
 def ratio_r(d: int, ratio: float) -> int:
     """r = max(1, llround(ratio * d)) (harness.cpp:212)."""
-    import math
     x = ratio * d
-    return max(1, int(math.floor(x + 0.5)) if x >= 0 else int(math.ceil(x - 0.5)))
+    return max(1, int(math.floor(x + 0.5)))
+
+
+def _world(group):
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(group), dist.get_rank(group)
+    return 1, 0
 
 
 class SparseAllgather:
-    """One DP worker's encode → exchange → decode step on its CUDA device."""
+    """One DP worker's encode → exchange → decode step."""
 
-    def __init__(self, codec: Codec, d: int, r: int, cfg: PipelineConfig, group=None):
+    def __init__(self, codec, d: int, r: int, cfg, group=None, device=None):
         self.codec = codec
         self.d, self.r, self.cfg = d, r, cfg
         self.group = group
-        self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
-        self.rank = dist.get_rank(group) if self.world > 1 else 0
-        dev = torch.device("cuda", torch.cuda.current_device())
-        self.cap = Codec.max_container_bytes(d, r, cfg)
+        self.world, self.rank = _world(group)
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.cap = type(codec).max_container_bytes(d, r, cfg)
         self.out = torch.empty(self.cap, dtype=torch.uint8, device=dev)
         self.length = torch.zeros(1, dtype=torch.int64, device=dev)
         self.sizes = torch.zeros(self.world, dtype=torch.int64, device=dev)
         self.recv = torch.empty(self.world * self.cap, dtype=torch.uint8, device=dev) if self.world > 1 else None
         self.dense = torch.zeros(d, dtype=torch.float32, device=dev)
 
-    def step(self, grad: torch.Tensor, step: int, seed: int = 1) -> torch.Tensor:
-        """Returns the dense mean of every rank's decoded container (device f32[d])."""
-        cfg = PipelineConfig(**{**self.cfg.__dict__, "seed": pipeline_seed(seed, self.rank, step)})
-        self.codec.encode_into(grad, self.r, cfg, self.out, self.length)
-        self.dense.zero_()
+    def step(self, grad: torch.Tensor, step: int, seed: int = 1, dense: torch.Tensor | None = None,
+             stream=None) -> torch.Tensor:
+        """Dense mean of every rank's decoded container (accumulated into `dense`
+        or the exchanger's own buffer)."""
+        cfg = replace(self.cfg, seed=pipeline_seed(seed, self.rank, step))
+        return self.step_seeded(grad, cfg, dense=dense, stream=stream)
+
+    def step_seeded(self, grad, cfg, dense=None, stream=None):
+        out_dense = self.dense if dense is None else dense
+        self.codec.encode_into(grad, self.r, cfg, self.out, self.length, stream=stream)
+        out_dense.zero_()
         n = self.world
-        if n == 1:
-            self.codec.decode_accumulate(self.out, self.dense, scale=1.0, length=self.length, hint=self.cfg)
-            return self.dense
-        # sizes first (one D2H of N words), then the payloads padded to the largest
+        if n == 1:  # no exchange: the device-side length drives the decode (no host sync)
+            self.codec.decode_accumulate(self.out, out_dense, scale=1.0, length=self.length, hint=self.cfg,
+                                         stream=stream)
+            return out_dense
         dist.all_gather_into_tensor(self.sizes, self.length, group=self.group)
-        sizes = self.sizes.tolist()
+        sizes = self.sizes.tolist()  # the one host sync of the step
         mx = max(sizes)
         dist.all_gather_into_tensor(self.recv[: n * mx], self.out[:mx], group=self.group)
-        for j in range(n):  # fixed rank order, like the harness's worker order
-            self.codec.decode_accumulate(self.recv[j * mx: j * mx + sizes[j]], self.dense, scale=1.0 / n,
-                                         hint=self.cfg)
+        for j in range(n):  # fixed rank order, as the harness's worker order
+            self.codec.decode_accumulate(self.recv[j * mx: j * mx + sizes[j]], out_dense, scale=1.0 / n,
+                                         hint=self.cfg, stream=stream)
+        return out_dense
+
+
+class BucketedSparseAllgather:
+    """Bucketed DP step for gradients too large for one container (C5)."""
+
+    def __init__(self, codec_factory, d: int, ratio: float, cfg, buckets: int, streams: int = 3, group=None,
+                 device=None):
+        self.d, self.cfg, self.buckets = d, cfg, buckets
+        self.world, self.rank = _world(group)
+        base, rem = divmod(d, buckets)
+        self.bounds = []
+        at = 0
+        for b in range(buckets):
+            n = base + (1 if b < rem else 0)
+            self.bounds.append((at, at + n))
+            at += n
+        dmax = max(e - s for s, e in self.bounds)
+        self.rs = [ratio_r(e - s, ratio) for s, e in self.bounds]
+        self.nstreams = min(streams, buckets)
+        self.codecs = [codec_factory(dmax) for _ in range(self.nstreams)]
+        cuda = device is None or torch.device(device).type == "cuda"
+        self.streams = [torch.cuda.Stream() for _ in range(self.nstreams)] if cuda else [None] * self.nstreams
+        self.ex = [SparseAllgather(self.codecs[i % self.nstreams], e - s, self.rs[i], cfg, group=group,
+                                   device=device) for i, (s, e) in enumerate(self.bounds)]
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.dense = torch.zeros(d, dtype=torch.float32, device=dev)
+
+    def bucket_seed(self, seed: int, step: int, b: int) -> int:
+        return hash64(b, pipeline_seed(seed, self.rank, step))
+
+    def step(self, grad: torch.Tensor, step: int, seed: int = 1) -> torch.Tensor:
+        cur = torch.cuda.current_stream() if self.streams[0] is not None else None
+        if cur is not None:
+            for s in self.streams:
+                s.wait_stream(cur)
+        for b, (lo, hi) in enumerate(self.bounds):
+            si = b % self.nstreams
+            s = self.streams[si]
+            cfg = replace(self.cfg, seed=self.bucket_seed(seed, step, b))
+            if s is not None:
+                with torch.cuda.stream(s):
+                    self.ex[b].step_seeded(grad[lo:hi], cfg, dense=self.dense[lo:hi], stream=s)
+            else:
+                self.ex[b].step_seeded(grad[lo:hi], cfg, dense=self.dense[lo:hi])
+        if cur is not None:
+            for s in self.streams:
+                cur.wait_stream(s)
         return self.dense

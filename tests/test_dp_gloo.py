@@ -1,0 +1,126 @@
+"""The N > 1 exchange path on CPU: world_size-2 gloo process groups.
+
+paper_2102_03112_b200.dp runs unchanged on CPU tensors with the gloo backend;
+the codec is a CPU stand-in built on the oracle (this file), so the test
+checks the exchange logic itself — sizes-first allgather, padding to the
+largest container, rank-order decode with scale 1/N, the bucket seeding — and
+that both replicas end with identical dense means (harness.cpp:287-288),
+against a sequential replay of Simulation::step's worker loop.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle.bindings import GpConfig, oracle, synthetic_gradient
+from paper_2102_03112_b200 import IndexMethod, PipelineConfig, ValueMethod
+from paper_2102_03112_b200._lib import lib
+
+
+class OracleCodec:
+    """CPU stand-in with Codec's exchange-facing interface (test infrastructure)."""
+
+    @staticmethod
+    def max_container_bytes(d, r, cfg):
+        import ctypes
+        c = cfg.to_c()
+        return int(lib.gp_max_container_bytes(d, r, ctypes.byref(c)))
+
+    @staticmethod
+    def _c(cfg):
+        return GpConfig.make(int(cfg.index_method), int(cfg.value_method), fpr=cfg.fpr, degree=cfg.degree,
+                             max_segments=cfg.max_segments, seed=cfg.seed, pd_variant=cfg.pd_variant)
+
+    def encode_into(self, grad, r, cfg, out, length, support=None, stream=None):
+        b = oracle().encode_dense(grad.contiguous().numpy(), r, self._c(cfg))
+        out[: len(b)] = torch.frombuffer(bytearray(b), dtype=torch.uint8)
+        length[0] = len(b)
+
+    def decode_accumulate(self, container, dense, scale=1.0, length=None, hint=None, stream=None):
+        n = int(length.item()) if isinstance(length, torch.Tensor) else (container.numel() if length is None else length)
+        _, sup, val = oracle().decode(container[:n].contiguous().numpy().tobytes())
+        idx = torch.from_numpy(sup.astype(np.int64))
+        # same arithmetic as the device scatter: fmaf(scale, (float)v, dense)
+        dense[idx] = (np.float32(scale) * torch.from_numpy(val.astype(np.float32)) + dense[idx]).to(torch.float32)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+CFGS = {
+    "p2fit": dict(index_method=IndexMethod.BloomP2, value_method=ValueMethod.FitPoly, fpr=0.01),
+    "bitmap": dict(index_method=IndexMethod.Bitmap, value_method=ValueMethod.None_),
+    "rle": dict(index_method=IndexMethod.Rle, value_method=ValueMethod.None_),
+}
+
+
+def _worker(rank, world, port, name, d, r, steps, buckets, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2102_03112_b200.dp import BucketedSparseAllgather, SparseAllgather
+    cfg = PipelineConfig(**CFGS[name])
+    g = torch.from_numpy(synthetic_gradient(d, rank=rank))
+    outs = []
+    if buckets:
+        ex = BucketedSparseAllgather(lambda dmax: OracleCodec(), d, r / d, cfg, buckets, streams=2,
+                                     device="cpu")
+    else:
+        ex = SparseAllgather(OracleCodec(), d, r, cfg, device="cpu")
+    for step in range(steps):
+        outs.append(ex.step(g, step=step).clone().numpy())
+    q.put((rank, outs))
+    dist.destroy_process_group()
+
+
+def _sequential(name, d, r, steps, world, buckets):
+    """Simulation::step's worker loop, one process: encode every worker, decode, mean."""
+    from paper_2102_03112_b200.dp import hash64, pipeline_seed, ratio_r
+    o = oracle()
+    base = PipelineConfig(**CFGS[name])
+    means = []
+    for step in range(steps):
+        acc = np.zeros(d, np.float32)
+        for w in range(world):  # rank order
+            g = synthetic_gradient(d, rank=w)
+            parts = [(0, d, r, pipeline_seed(1, w, step))]
+            if buckets:
+                lo, parts = 0, []
+                q, rem = divmod(d, buckets)
+                for b in range(buckets):
+                    n = q + (1 if b < rem else 0)
+                    parts.append((lo, lo + n, ratio_r(n, r / d), hash64(b, pipeline_seed(1, w, step))))
+                    lo += n
+            for lo, hi, rb, seed in parts:
+                c = o.encode_dense(g[lo:hi], rb, OracleCodec._c(PipelineConfig(**{**base.__dict__, "seed": seed})))
+                _, sup, val = o.decode(c)
+                a = acc[lo:hi]
+                a[sup] = np.float32(1.0 / world) * val.astype(np.float32) + a[sup]
+        means.append(acc)
+    return means
+
+
+@pytest.mark.parametrize("name,d,r,buckets", [("p2fit", 20_000, 200, 0), ("bitmap", 5_000, 50, 0),
+                                              ("rle", 7_000, 70, 0), ("p2fit", 40_000, 40, 4)])
+def test_gloo_world2_matches_sequential_harness(name, d, r, buckets):
+    world, steps = 2, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(k, world, port, name, d, r, steps, buckets, q)) for k in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = _sequential(name, d, r, steps, world, buckets)
+    for step in range(steps):
+        assert np.array_equal(res[0][step], res[1][step]), "replicas diverged"
+        assert np.array_equal(res[0][step], want[step])
