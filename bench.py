@@ -53,6 +53,15 @@ CONFIGS = {
     "c3": dict(workload="NCF-style natural sparsity (40% zero 64-wide rows), 32M elements, bitmap indices + "
                         "raw f32 values (support = nonzeros)",
                d=31_832_577, ratio=None, index=1, value=0, fpr=0.01, degree=5, max_segments=0, sparse=True),
+    "c3r": dict(workload="NCF-style natural sparsity (40% zero 64-wide rows), 32M elements, RLE indices + "
+                         "raw f32 values (support = nonzeros)",
+                d=31_832_577, ratio=None, index=2, value=0, fpr=0.01, degree=5, max_segments=0, sparse=True),
+    "c2r": dict(workload="ResNet-20-sized 0.27M-element gradient, top-r 1%, RLE indices + raw f32 values",
+                d=269_722, ratio=0.01, index=2, value=0, fpr=0.01, degree=5, max_segments=0, sparse=False),
+    "c5": dict(workload="BERT-large-sized 340M-element gradient, top-r 0.1%, bloom-filter P2 (eps=1e-3) + "
+                        "piecewise curve-fit (8 pieces), 16 independent 21.25M buckets pipelined on 3 streams",
+               d=340_000_000, ratio=0.001, index=6, value=1, fpr=0.001, degree=5, max_segments=8, sparse=False,
+               buckets=16),
 }
 METHOD_NAMES = {0: "none", 1: "bitmap", 2: "rle", 4: "bloom-p0", 5: "bloom-p1", 6: "bloom-p2", 7: "bloom-pd",
                 8: "bloom-naive"}
@@ -142,7 +151,8 @@ def run_cpu_sample(cfg, threads: int, shrink: int, steps: int, seed_step: int = 
     from paper_2102_03112_b200.dp import pipeline_seed, ratio_r
     lib, kind = cpu_codec()
     d = cfg["d"] // shrink
-    grads = [synth.gradient(d, rank=t) for t in range(threads)]
+    gen = synth.natural_sparse_gradient if cfg["sparse"] else synth.gradient
+    grads = [gen(d, rank=t) for t in range(threads)]
     rs = [ratio_r(d, cfg["ratio"]) if cfg["ratio"] else int(np.count_nonzero(g)) for g in grads]
     denses = [np.zeros(d, np.float64) for _ in range(threads)]
     sizes = [0] * threads
@@ -197,7 +207,7 @@ def native_main(args, cfg):
     import torch.distributed as dist
 
     from paper_2102_03112_b200 import Codec, PipelineConfig, synth
-    from paper_2102_03112_b200.dp import SparseAllgather, ratio_r
+    from paper_2102_03112_b200.dp import BucketedSparseAllgather, SparseAllgather, ratio_r
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -208,14 +218,26 @@ def native_main(args, cfg):
     dev = torch.device("cuda", local)
 
     d = cfg["d"]
-    g_host = synth.natural_sparse_gradient(d, rank) if cfg["sparse"] else synth.gradient(d, rank)
-    r = int(np.count_nonzero(g_host)) if cfg["ratio"] is None else ratio_r(d, cfg["ratio"])
-    pinned = torch.from_numpy(g_host).pin_memory()
-    grad = pinned.to(dev)
-    codec = Codec(max_d=d, device=local)
+    if cfg["sparse"]:
+        g_host = synth.natural_sparse_gradient(d, rank)
+        grad = torch.from_numpy(g_host).to(dev)
+    else:  # the BASELINE generator, evaluated on the device (d up to 340M)
+        grad = synth.gradient_torch(d, rank, device=dev)
+    r = int(torch.count_nonzero(grad).item()) if cfg["ratio"] is None else ratio_r(d, cfg["ratio"])
+    pinned = torch.empty(d, dtype=torch.float32).pin_memory()
+    pinned.copy_(grad)
     pcfg = PipelineConfig(index_method=cfg["index"], value_method=cfg["value"], fpr=cfg["fpr"],
                           degree=cfg["degree"], max_segments=cfg["max_segments"])
-    ex = SparseAllgather(codec, d, r, pcfg)
+    if cfg.get("buckets"):
+        ex = BucketedSparseAllgather(lambda dmax: Codec(max_d=dmax, device=local), d, cfg["ratio"], pcfg,
+                                     cfg["buckets"], streams=3)
+        codecs = ex.codecs
+        r_total = sum(ex.rs)
+    else:
+        codec = Codec(max_d=d, device=local)
+        ex = SparseAllgather(codec, d, r, pcfg)
+        codecs = [codec]
+        r_total = r
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
     stream = torch.cuda.current_stream()
 
@@ -224,13 +246,20 @@ def native_main(args, cfg):
             dist.barrier()
         torch.cuda.synchronize()
 
+    def status():
+        for c in codecs:
+            c.status()
+
+    def launches():
+        return sum(c.launches for c in codecs)
+
     for w in range(args.warmup):
         ex.step(grad, step=w)
-    codec.status()
+    status()
 
     # ---- timed region: device time with inputs resident in HBM
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    launches0 = codec.launches
+    launches0 = launches()
     barrier()
     with ClockSampler(local) as clk:
         wall0 = time.perf_counter()
@@ -241,8 +270,8 @@ def native_main(args, cfg):
             evs[i][1].record(stream)
         barrier()
         wall = time.perf_counter() - wall0
-    codec.status()
-    launches = (codec.launches - launches0) // max(1, args.steps)
+    status()
+    n_launch = (launches() - launches0) // max(1, args.steps)
     step_ms = [a.elapsed_time(b) for a, b in evs]
     t_ms = float(sum(step_ms)) / args.steps
     if world > 1:
@@ -250,19 +279,25 @@ def native_main(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_ms = float(t.item())
     clocks = clk.summary()
-    length = int(ex.length.item())
+    if cfg.get("buckets"):
+        length = sum(int(e.length.item()) for e in ex.ex)
+    else:
+        length = int(ex.length.item())
 
     # ---- profiled pass (same steps): per-stage CUDA events on the launch stream
-    codec.profile(True)
+    for c in codecs:
+        c.profile(True)
     stage = {}
     for i in range(args.steps):
         flush.fill_(float(i))
         ex.step(grad, step=args.warmup + i)
-        for k, (ms, n) in codec.stage_times().items():
-            a = stage.setdefault(k, [0.0, 0])
-            a[0] += ms
-            a[1] += n
-    codec.profile(False)
+        for c in codecs:
+            for k, (ms, n) in c.stage_times().items():
+                a = stage.setdefault(k, [0.0, 0])
+                a[0] += ms
+                a[1] += n
+    for c in codecs:
+        c.profile(False)
     prof_total = sum(v[0] for v in stage.values()) / args.steps
 
     # ---- e2e: host gradient in, host dense mean out, through the public API
@@ -290,33 +325,43 @@ def native_main(args, cfg):
 
     # roofline of the dominant stage: algorithmic HBM bytes per launch / its event time
     per_launch = {k: (v[0] / v[1], v[1] / args.steps) for k, v in stage.items()}
-    algo_bytes = {
-        "topr": 4.0 * d,                      # the gradient must be read once
-        "bloom_scan": 4.0 * d * 0 + 4.0 * (2 * r),  # writes |P| keys (compute-bound)
-        "dec_bloom_scan": 4.0 * (2 * r),
-        "dec_scatter": 8.0 * r,
-        "pack_crc": float(length),
+    algo_bytes = {  # minimum DRAM bytes a launch must move
+        "topr": 4.0 * d,                  # read the gradient once
+        "pack_crc": float(length),        # read the payloads once
         "dec_parse_crc": float(length),
+        "dec_scatter": 8.0 * r_total,     # read the support, write the values
+        "gather": 8.0 * r_total,
+        "bloom_scan": d / 8.0 + 8.0 * r_total,      # membership bitmap + positives
+        "dec_bloom_scan": d / 8.0 + 8.0 * r_total,
     }
     dom = max(stage.items(), key=lambda kv: kv[1][0])[0] if stage else None
     roof = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    traffic_tab = {}
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic_tab = json.load(f).get(args.config, {})
     if dom is not None:
         ms_launch, _ = per_launch[dom]
         ab = algo_bytes.get(dom)
         achieved = (ab / (ms_launch * 1e-3) / 1e9) if ab else None
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 3) if achieved else None,
-                "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 5) if achieved else None,
-                "traffic": None, "ms_per_launch": round(ms_launch, 5), "peak_kind": peak_kind}
+                "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 6) if achieved else None,
+                "traffic": traffic_tab.get(dom), "ms_per_launch": round(ms_launch, 5), "peak_kind": peak_kind}
+        if dom in ("bloom_scan", "dec_bloom_scan"):
+            roof["keys_per_s"] = round(d / (ms_launch * 1e-3), 1)
+            roof["note"] = ("full-range Bloom membership scan is integer-issue bound (SplitMix64 + 64x32 "
+                            "modulo per probe), not HBM bound: see DESIGN.md")
     step_hbm_bytes = 8.0 * d + 2.0 * world * length
     step_roof = {"hbm_bytes": step_hbm_bytes, "t_roof_ms": step_hbm_bytes / (hbm * 1e9) * 1e3,
-                 "frac": round(step_hbm_bytes / (hbm * 1e9) / (t_ms * 1e-3), 5)}
+                 "frac": round(step_hbm_bytes / (hbm * 1e9) / (t_ms * 1e-3), 6)}
 
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(t_ms, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32 values, u32 keys, f64 fit", "data": "synthetic",
-        "bits_per_nonzero": round(8.0 * length / r, 4),
-        "config": {"workload": cfg["workload"], "d": d, "r": r, "index_method": METHOD_NAMES[cfg["index"]],
+        "bits_per_nonzero": round(8.0 * length / r_total, 4),
+        "config": {"workload": cfg["workload"], "d": d, "r": r_total, "index_method": METHOD_NAMES[cfg["index"]],
                    "value_method": VALUE_NAMES[cfg["value"]], "fpr": cfg["fpr"], "degree": cfg["degree"],
                    "container_bytes": length, "parallelism": f"dp{world}",
                    "l2": "flushed between steps (256 MiB write outside the timed events)"},
@@ -325,10 +370,10 @@ def native_main(args, cfg):
         "roofline": roof, "step_roofline": step_roof,
         "stages_ms_per_step": {k: round(v[0] / args.steps, 5) for k, v in sorted(stage.items())},
         "profiled_ms_per_step": round(prof_total, 4),
-        "gpu_launches": int(launches), "clocks": clocks, "wall_s_timed": round(wall, 4),
+        "gpu_launches": int(n_launch), "clocks": clocks, "wall_s_timed": round(wall, 4),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        gbs, sec, desc, kind, _ = run_cpu_sample(cfg, 1, 1, 1)
+        gbs, sec, desc, kind, _ = run_cpu_sample(cfg, 1, cfg.get("buckets", 1), 1)
         line["cpu_baseline"] = {"value": round(gbs, 6), "unit": "GB/s", "cores": 1, "kind": kind, "sample": desc,
                                 "seconds": round(sec, 3)}
     if rank == 0:

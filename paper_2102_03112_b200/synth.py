@@ -57,3 +57,38 @@ def natural_sparse_gradient(d: int, rank: int = 0, seed: int = 1, zero_frac: flo
     mask = np.repeat(u < zero_frac, row)[:d]
     g[mask] = 0.0
     return g
+
+
+def _mix64_t(z):
+    import torch
+    m30, m27, m31 = (1 << 34) - 1, (1 << 37) - 1, (1 << 33) - 1
+    z = z ^ ((z >> 30) & m30)
+    z = z * -4658895280553007687  # 0xBF58476D1CE4E5B9 as int64
+    z = z ^ ((z >> 27) & m27)
+    z = z * -7723592293110705685  # 0x94D049BB133111EB as int64
+    return z ^ ((z >> 31) & m31)
+
+
+def _as_i64(x: int) -> int:
+    x &= (1 << 64) - 1
+    return x - (1 << 64) if x >= 1 << 63 else x
+
+
+def gradient_torch(d: int, rank: int = 0, seed: int = 1, device="cuda", chunk: int = 1 << 24):
+    """The same generator on the GPU (int64 two's-complement = u64 arithmetic,
+    logical shifts by masking).  fp64 log/cos are the device's, so a rare
+    element may differ from the host generator in the last f32 bit; used for
+    benchmark inputs only (parity tests use the host/oracle generator)."""
+    import torch
+    s = _as_i64(hash64(rank, hash64(0xBE7C, seed)))
+    g = _as_i64(0x9E3779B97F4A7C15)
+    out = torch.empty(d, dtype=torch.float32, device=device)
+    for b in range(0, d, chunk):
+        m = min(chunk, d - b)
+        pos = torch.arange(2 * b + 1, 2 * (b + m) + 1, dtype=torch.int64, device=device)
+        z = _mix64_t(pos * g + s)
+        u = ((z >> 11) & ((1 << 53) - 1)).to(torch.float64) * (2.0 ** -53)
+        u1 = 1.0 - u[0::2]
+        u2 = u[1::2]
+        out[b:b + m] = (torch.sqrt(-2.0 * torch.log(u1)) * torch.cos(2.0 * np.pi * u2)).to(torch.float32)
+    return out
