@@ -47,7 +47,24 @@ def build(verbose: bool = False) -> str:
         objs.append(obj)
     if not os.path.exists(OUT) or any(os.path.getmtime(o) > os.path.getmtime(OUT) for o in objs):
         _run([NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-Xlinker", "--exclude-libs,ALL"])
+    build_cli()
     return OUT
+
+
+CLI_SRC = os.path.join(HERE, "..", "tests", "cpp", "gp_cli.cpp")
+CLI_OUT = os.path.join(HERE, "..", "tests", "cpp", "gp_cli")
+
+
+def build_cli() -> str:
+    """The C++ host program over include/gradpack_b200.hpp (tests/test_gpu_cpp.py)."""
+    hdr = os.path.join(HERE, "..", "include", "gradpack_b200.hpp")
+    if (os.path.exists(CLI_OUT) and os.path.getmtime(CLI_OUT) > os.path.getmtime(CLI_SRC)
+            and os.path.getmtime(CLI_OUT) > os.path.getmtime(hdr) and os.path.getmtime(CLI_OUT) > os.path.getmtime(OUT)):
+        return CLI_OUT
+    _run(["g++", "-std=c++17", "-O2", "-I/usr/local/cuda/include", CLI_SRC, "-o", CLI_OUT, f"-L{HERE}",
+          "-lgradpack_b200", "-L/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{HERE}",
+          "-Wl,-rpath,/usr/local/cuda/lib64"])
+    return CLI_OUT
 
 
 if __name__ == "__main__":
