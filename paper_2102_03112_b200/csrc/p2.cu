@@ -12,7 +12,7 @@
 //              (stage A); multi-set members go to their bucket
 //   order    : one stable counting-sort pass by size over the bit domain,
 //              which also compacts away empty bits → sets in (size, bit)
-//              order; each multi bucket is sorted ascending on the way
+//              order (members stay unsorted; the engine ranks them)
 //
 // p2_select: pass 1 first visits every singleton (bit order) and selects its
 // member.  Singleton members are always true keys (a false positive's probes
@@ -176,12 +176,10 @@ __global__ void p2_count_sets(Plan* plan, const uint32_t* __restrict__ table, co
 }
 
 // Stable placement of the non-empty bits by size (counting sort over the
-// digit table): sets[table[size][tile] + rank] = bit, one tile per block; the
-// thread placing a multi set also sorts its bucket ascending (2-~20 entries).
+// digit table): sets[table[size][tile] + rank] = bit, one tile per block.
+// Buckets stay unsorted: the engine ranks members by value instead.
 __global__ void __launch_bounds__(kTileBlock) p2_size_scatter(const Plan* plan, const uint32_t* __restrict__ size,
                                                               const uint32_t* __restrict__ table,
-                                                              const uint32_t* __restrict__ off,
-                                                              uint32_t* __restrict__ members,
                                                               uint32_t* __restrict__ sets, const uint32_t* status) {
   __shared__ uint32_t run[256];
   __shared__ uint32_t wcnt[kTileBlock / 32][256];
@@ -207,36 +205,6 @@ __global__ void __launch_bounds__(kTileBlock) p2_size_scatter(const Plan* plan, 
       uint32_t before = 0;
       for (int w2 = 0; w2 < warp; ++w2) before += wcnt[w2][s];
       sets[run[s] + before + lrank] = static_cast<uint32_t>(b);
-    }
-    if (s >= 2) {  // ascending members of this set (independent loads, sort in registers)
-      uint32_t* mem = members + off[b];
-      if (s <= 16) {
-        uint32_t v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = i < static_cast<int>(s) ? mem[i] : 0xFFFFFFFFu;
-#pragma unroll
-        for (int i = 1; i < 16; ++i)  // insertion sort network over the padded array
-#pragma unroll
-          for (int j = i; j > 0; --j)
-            if (v[j - 1] > v[j]) {
-              const uint32_t t = v[j];
-              v[j] = v[j - 1];
-              v[j - 1] = t;
-            }
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if (i < static_cast<int>(s)) mem[i] = v[i];
-      } else {
-        for (uint32_t i = 1; i < s; ++i) {
-          const uint32_t x = mem[i];
-          uint32_t j = i;
-          while (j > 0 && mem[j - 1] > x) {
-            mem[j] = mem[j - 1];
-            --j;
-          }
-          mem[j] = x;
-        }
-      }
     }
     __syncthreads();
     uint32_t tot = 0;
@@ -394,16 +362,18 @@ __device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __res
     const uint32_t cut = block_min(sel && spos + 1 == need ? v + 1 : W);
     const uint32_t climit = min(limit, cut);
     // commit
-    if (sel && v < climit) {
-      uint32_t seen = 0;
+    if (sel && v < climit) {  // the target-th smallest unselected member (buckets are unsorted)
       for (uint32_t j = 0; j < sz; ++j) {
         const uint32_t p = mems[lo + j];
-        if (!bs_test(bits, p)) {
-          if (seen == target) {
-            atomicOr(&bits[p >> 5], 1u << (p & 31));
-            break;
-          }
-          ++seen;
+        if (bs_test(bits, p)) continue;
+        uint32_t rank = 0;
+        for (uint32_t q = 0; q < sz; ++q) {
+          const uint32_t o = mems[lo + q];
+          rank += (o < p && !bs_test(bits, o)) ? 1u : 0u;
+        }
+        if (rank == target) {
+          atomicOr(&bits[p >> 5], 1u << (p & 31));
+          break;
         }
       }
     }
@@ -504,8 +474,7 @@ void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t 
             w.p2_cursor, w.p2_members, w.p2_single, w.flags, w.status);
   launch_table_scan(ctx, w.p2_table, &w.plan->m, m_cap, 12, s);
   GP_LAUNCH(ctx, p2_count_sets, 1, 32, 0, s, w.plan, w.p2_table, w.status);
-  GP_LAUNCH(ctx, p2_size_scatter, tgrid, kTileBlock, 0, s, w.plan, w.p2_count, w.p2_table, w.p2_off, w.p2_members,
-            w.p2_sets, w.status);
+  GP_LAUNCH(ctx, p2_size_scatter, tgrid, kTileBlock, 0, s, w.plan, w.p2_count, w.p2_table, w.p2_sets, w.status);
   GP_LAUNCH(ctx, p2_stage_a, grid_for(ctx, n_bound, 256), 256, 0, s, w.plan, w.flags, w.selbits, w.status);
   stage_end(ctx, s);
   stage_begin(ctx, decoding ? ST_DEC_P2_ENGINE : ST_P2_ENGINE, s);

@@ -110,7 +110,7 @@ def main():
              "| kernel | " + " | ".join(v for _, v in keys) + " |", "|---" * (len(keys) + 1) + "|"]
     traffic = collections.defaultdict(list)
     for rec in recs:
-        k = short(rec.get("Kernel Name", "?"))
+        k = short(rec.get("Kernel Name", "?")).split("<")[0]
         vals = [f"{rec[m]:.4g}" if isinstance(rec.get(m), float) else str(rec.get(m, "")) for m, _ in keys]
         lines.append(f"| `{k}` | " + " | ".join(vals) + " |")
         rd, wr = rec.get("dram__bytes_read.sum"), rec.get("dram__bytes_write.sum")
