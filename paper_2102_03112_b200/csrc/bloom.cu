@@ -24,10 +24,6 @@ namespace {
 constexpr int kScanBlock = 256;
 constexpr uint64_t kSmemFilterMax = 150 * 1024;
 
-__device__ __forceinline__ bool test_bit(const uint32_t* w, uint64_t pos) {
-  return (w[pos >> 5] >> (pos & 31)) & 1u;
-}
-
 __global__ void bloom_insert(const uint32_t* __restrict__ keys, uint64_t r, const Plan* plan, uint32_t* words,
                              const uint32_t* status) {
   if (failed(status)) return;
@@ -128,125 +124,164 @@ __global__ void bloom_load_words(const uint8_t* __restrict__ in, const Plan* pla
 //
 // (1) bloom_members: contains() exits at the first clear probe, so ~half the
 // keys stop after one probe, a quarter after two, ...; a lane-per-key loop
-// keeps a warp busy for its slowest lane.  Each warp instead owns 2048-key
-// super-tiles and runs probe ROUNDS: round 1 probes every key (h_a, probe 0,
-// 16 independent keys per lane in flight), the survivors' key offsets
-// (u16, compacted in place in a per-warp shared queue) are the only work of
-// round j+1 (h_a, h_b recomputed, probe j, 4 entries per lane in flight).
-// Rounds stay converged; membership bits land in a per-warp mask that is
-// stored to a d-bit membership bitmap.  No cross-warp ordering is needed.
-// (2) members_compact: ordered compaction of the set bits (look-back scan,
-// 131072 keys per tile) — P ascending, |P| in the plan.
-constexpr int kLaneKeys = 16;
-constexpr int kChunkKeys = 32 * kLaneKeys;   // 512 keys per round-1 chunk
-constexpr int kChunks = 2;
-constexpr int kSuperKeys = kChunks * kChunkKeys;   // 1024 keys per warp super-tile
+// keeps a warp busy for its slowest lane.  Each warp instead keeps a shared
+// work stack of pending probes (key, next probe j, h = h_a + j*h_b, h_b) and
+// alternates two converged steps:
+//   * first probes: kLaneKeys consecutive keys per lane (a chunk of
+//     32*kLaneKeys keys); survivors are pushed with h_b computed once, in a
+//     lane-strided pass over the new entries;
+//   * a probe batch: pop 32*kLaneBatch entries (kLaneBatch independent probes
+//     per lane in flight), test probe j, push survivors back with j+1 and
+//     h += h_b; a key passing its k-th probe sets its bit in the d-bit
+//     membership bitmap (zeroed beforehand; one atomicOr per member).
+// A batch runs whenever the stack holds a full batch, so lanes stay busy
+// across chunk boundaries instead of idling through each chunk's thin tail.
+// (2) members_compact: ordered compaction of the set bits (look-back scan)
+// — P ascending, |P| in the plan.
 constexpr int kWarps = kScanBlock / 32;
 
-template <bool kSmem>
+template <bool kSmem, int kLaneKeys, int kLaneBatch>
+struct ScanShape {
+  static constexpr int kChunk = 32 * kLaneKeys;
+  static constexpr int kBatch = 32 * kLaneBatch;
+  static constexpr int kCap = kBatch + kChunk;  // stack < kBatch before a chunk pushes <= kChunk
+  static constexpr size_t kStackBytes = static_cast<size_t>(kWarps) * kCap * (8 + 8 + 4 + 2);
+};
+
+// probe position of hash h (mix64(h) mod m): 32-bit tail when m <= 2^31
+template <bool kSmallM>
+__device__ __forceinline__ uint32_t probe_pos(uint64_t h, const FastMod& fm) {
+  if (kSmallM) return fast_mod_small(mix64(h), fm.minv, static_cast<uint32_t>(fm.m));
+  return static_cast<uint32_t>(fast_mod(mix64(h), fm));  // m < 2^32
+}
+
+template <bool kSmallM, int kLaneKeys, int kLaneBatch, int kCap>
+__device__ __forceinline__ void members_body(const uint32_t* __restrict__ words, const Plan* plan,
+                                             uint32_t* __restrict__ bitmap, uint8_t* dyn) {
+  constexpr int kChunk = 32 * kLaneKeys, kBatch = 32 * kLaneBatch;
+  const uint32_t d = static_cast<uint32_t>(plan->d);
+  const uint32_t k = plan->k;
+  const FastMod fm{plan->m, plan->minv};
+  const uint64_t sa = plan->seed_a + kGamma, sb = plan->seed_b + kGamma;
+  // shared layout: [stack h | stack b | stack key | stack j]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* qh = reinterpret_cast<uint64_t*>(dyn) + warp * kCap;
+  uint64_t* qb = reinterpret_cast<uint64_t*>(dyn) + (kWarps + warp) * kCap;
+  uint32_t* qx = reinterpret_cast<uint32_t*>(dyn + 16 * kWarps * kCap) + warp * kCap;
+  uint16_t* qj = reinterpret_cast<uint16_t*>(dyn + 20 * kWarps * kCap) + warp * kCap;  // k <= 65535
+  const uint32_t nchunks = (d + kChunk - 1) / kChunk;
+  const uint32_t nwarps = gridDim.x * kWarps;
+  uint32_t c = blockIdx.x * kWarps + warp;
+  uint32_t top = 0;  // warp-uniform stack height
+  while (true) {
+    if (top >= kBatch || (c >= nchunks && top > 0)) {
+      // ---- probe batch: positions, then every word load, then the tests
+      const uint32_t n = top < kBatch ? top : kBatch;
+      const uint32_t base = top - n;
+      uint32_t x[kLaneBatch], j[kLaneBatch], pos[kLaneBatch], wv[kLaneBatch];
+      uint64_t h[kLaneBatch], hb[kLaneBatch];
+#pragma unroll
+      for (int u = 0; u < kLaneBatch; ++u) {
+        const uint32_t e = min(base + 32 * u + lane, top - 1);  // clamped: duplicates are discarded
+        x[u] = qx[e];
+        j[u] = qj[e];
+        h[u] = qh[e];
+        hb[u] = qb[e];
+        pos[u] = probe_pos<kSmallM>(h[u], fm);
+      }
+#pragma unroll
+      for (int u = 0; u < kLaneBatch; ++u) wv[u] = words[pos[u] >> 5];
+      __syncwarp();
+      uint32_t wr = base;
+#pragma unroll
+      for (int u = 0; u < kLaneBatch; ++u) {
+        const bool ok = base + 32 * u + lane < top && ((wv[u] >> (pos[u] & 31)) & 1u);
+        const bool member = ok && j[u] + 1u == k;
+        if (member) atomicOr(&bitmap[x[u] >> 5], 1u << (x[u] & 31));
+        const bool keep = ok && !member;
+        const unsigned bal = __ballot_sync(kFull, keep);
+        if (keep) {
+          const uint32_t e = wr + __popc(bal & ((1u << lane) - 1));
+          qx[e] = x[u];
+          qj[e] = static_cast<uint16_t>(j[u] + 1);
+          qh[e] = h[u] + hb[u];
+          qb[e] = hb[u];
+        }
+        wr += __popc(bal);
+      }
+      top = wr;
+      __syncwarp();
+    } else if (c < nchunks) {
+      // ---- first probes of one chunk (positions, loads, tests)
+      const uint32_t x0 = c * kChunk + kLaneKeys * lane;
+      uint64_t av[kLaneKeys];
+      uint32_t pos[kLaneKeys], wv[kLaneKeys];
+#pragma unroll
+      for (int q = 0; q < kLaneKeys; ++q) {
+        av[q] = mix64(static_cast<uint64_t>(x0 + q) ^ sa);
+        pos[q] = probe_pos<kSmallM>(av[q], fm);
+      }
+#pragma unroll
+      for (int q = 0; q < kLaneKeys; ++q) wv[q] = words[pos[q] >> 5];
+      uint32_t pass = 0;
+#pragma unroll
+      for (int q = 0; q < kLaneKeys; ++q)
+        pass |= ((wv[q] >> (pos[q] & 31)) & 1u) << q;
+      if (x0 + kLaneKeys > d) pass &= x0 >= d ? 0u : (1u << (d - x0)) - 1u;
+      c += nwarps;
+      if (k == 1) {
+        // kLaneKeys divides 32: a lane's keys share one bitmap word
+        if (pass) atomicOr(&bitmap[x0 >> 5], pass << (x0 & 31));
+        continue;
+      }
+      const uint32_t cnt = __popc(pass);
+      const uint32_t inc = warp_inclusive_sum(cnt);
+      uint32_t o = top + inc - cnt;
+#pragma unroll
+      for (int q = 0; q < kLaneKeys; ++q)
+        if (pass >> q & 1u) {
+          qx[o] = x0 + q;
+          qh[o] = av[q];
+          ++o;
+        }
+      const uint32_t added = __shfl_sync(kFull, inc, 31);
+      __syncwarp();
+      for (uint32_t e = top + lane; e < top + added; e += 32) {  // h_b once per survivor
+        const uint64_t b = mix64(static_cast<uint64_t>(qx[e]) ^ sb);
+        qb[e] = b;
+        qh[e] += b;
+        qj[e] = 1;
+      }
+      top += added;
+      __syncwarp();
+    } else {
+      break;
+    }
+  }
+}
+
+template <bool kSmem, int kLaneKeys, int kLaneBatch>
 __global__ void __launch_bounds__(kScanBlock) bloom_members(const uint32_t* __restrict__ gwords, Plan* plan,
                                                             uint32_t* __restrict__ bitmap,
                                                             const uint32_t* status) {
-  extern __shared__ uint32_t sw[];
-  __shared__ uint16_t queue[kWarps][kSuperKeys];
-  __shared__ uint32_t member[kWarps][kSuperKeys / 32];
+  using S = ScanShape<kSmem, kLaneKeys, kLaneBatch>;
+  extern __shared__ __align__(16) uint8_t dyn[];
   if (failed(status)) return;
   const uint8_t im = plan->index_method;
   if (im < GP_INDEX_BLOOM_P0 || im > GP_INDEX_BLOOM_NAIVE) return;
-  const uint64_t d = plan->d, m = plan->m;
-  const uint32_t k = plan->k;
-  const FastMod fm{m, plan->minv};
-  const uint64_t sa = plan->seed_a + kGamma, sb = plan->seed_b + kGamma;
+  const uint64_t m = plan->m;
   const uint32_t* words = gwords;
   if (kSmem) {
+    uint32_t* sw = reinterpret_cast<uint32_t*>(dyn + (S::kStackBytes + 15) / 16 * 16);
     const uint64_t nw = (m + 31) / 32;
     for (uint64_t i = threadIdx.x; i < nw; i += kScanBlock) sw[i] = gwords[i];
     __syncthreads();
     words = sw;
   }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint16_t* q = queue[warp];
-  uint32_t* wm = member[warp];
-  const uint64_t nsuper = (d + kSuperKeys - 1) / kSuperKeys;
-  const uint64_t gw = static_cast<uint64_t>(gridDim.x) * kWarps;
-  for (uint64_t st = static_cast<uint64_t>(blockIdx.x) * kWarps + warp; st < nsuper; st += gw) {
-    const uint64_t sbase = st * kSuperKeys;
-    for (int i = lane; i < kSuperKeys / 32; i += 32) wm[i] = 0;
-    __syncwarp();
-    uint32_t nq = 0;
-    // ---- round 1
-    for (int c = 0; c < kChunks; ++c) {
-      const uint32_t off0 = c * kChunkKeys + kLaneKeys * lane;
-      uint32_t pass = 0;
-#pragma unroll
-      for (int j = 0; j < kLaneKeys; ++j) {
-        const uint64_t x = sbase + off0 + j;
-        const uint64_t a = mix64(x ^ sa);
-        if (x < d && test_bit(words, fast_mod(mix64(a), fm))) pass |= 1u << j;
-      }
-      if (k == 1) {
-        if (pass) atomicOr(&wm[off0 >> 5], pass << (off0 & 31));
-        continue;
-      }
-      const uint32_t cnt = __popc(pass);
-      const uint32_t inc = warp_inclusive_sum(cnt);
-      uint32_t o = nq + inc - cnt;
-      while (pass) {
-        const int j = __ffs(pass) - 1;
-        q[o++] = static_cast<uint16_t>(off0 + j);
-        pass &= pass - 1;
-      }
-      nq += __shfl_sync(kFull, inc, 31);
-    }
-    __syncwarp();
-    // ---- rounds 2..k
-    for (uint32_t j = 1; j < k && nq; ++j) {
-      uint32_t wr = 0;
-      const bool last = j + 1 == k;
-      // 4 entries per lane in flight while the queue is long, 1 in the thin tail
-      const int per = nq > 64 ? 4 : 1;
-      for (uint32_t base = 0; base < nq; base += 32 * per) {
-        uint16_t kk[4];
-        bool ok[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (u >= per) {
-            ok[u] = false;
-            kk[u] = 0;
-            continue;
-          }
-          const uint32_t e = base + 32 * u + lane;
-          ok[u] = false;
-          kk[u] = 0;
-          if (e < nq) {
-            kk[u] = q[e];
-            const uint64_t x = sbase + kk[u];
-            const uint64_t a = mix64(x ^ sa), b = mix64(x ^ sb);
-            ok[u] = test_bit(words, fast_mod(mix64(a + static_cast<uint64_t>(j) * b), fm));
-          }
-        }
-        __syncwarp();
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (last) {
-            if (ok[u]) atomicOr(&wm[kk[u] >> 5], 1u << (kk[u] & 31));
-          } else {
-            const unsigned bal = __ballot_sync(kFull, ok[u]);
-            if (ok[u]) q[wr + __popc(bal & ((1u << lane) - 1))] = kk[u];
-            wr += __popc(bal);
-          }
-        }
-        __syncwarp();
-      }
-      nq = last ? 0 : wr;
-    }
-    __syncwarp();
-    // ---- membership words (the super-tile is word aligned: 2048 keys = 64 words)
-    const uint64_t nwd = (d + 31) / 32;
-    for (int i = lane; i < kSuperKeys / 32; i += 32)
-      if (sbase / 32 + i < nwd) bitmap[sbase / 32 + i] = wm[i];
-    __syncwarp();
-  }
+  if (m <= (1ull << 31))
+    members_body<true, kLaneKeys, kLaneBatch, S::kCap>(words, plan, bitmap, dyn);
+  else
+    members_body<false, kLaneKeys, kLaneBatch, S::kCap>(words, plan, bitmap, dyn);
 }
 
 // ordered compaction of the membership bitmap: 16 words per thread
@@ -346,30 +381,49 @@ void launch_bloom_parse(gp_ctx* ctx, const uint8_t* in, uint64_t m_bound, cudaSt
             w.status);
 }
 
+template <int kLaneKeys, int kLaneBatch>
+void launch_members_global(gp_ctx* ctx, uint64_t d_bound, uint32_t* bitmap, cudaStream_t s) {
+  Workspace& w = ctx->ws;
+  using S = ScanShape<false, kLaneKeys, kLaneBatch>;
+  auto* kern = bloom_members<false, kLaneKeys, kLaneBatch>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S::kStackBytes));
+    attr = true;
+  }
+  const int per_sm = std::max<int>(1, std::min<int>(8, static_cast<int>((200 * 1024) / (S::kStackBytes + 1024))));
+  const uint64_t nchunks = (d_bound + S::kChunk - 1) / S::kChunk;
+  const int grid = static_cast<int>(std::max<uint64_t>(
+      1, std::min<uint64_t>((nchunks + kWarps - 1) / kWarps, static_cast<uint64_t>(ctx->sm_count) * per_sm)));
+  GP_LAUNCH(ctx, kern, grid, kScanBlock, S::kStackBytes, s, w.filter, w.plan, bitmap, w.status);
+}
+
 // m_host: the filter width when the host knows it (encode), else 0 (decode:
 // the width is only on the device, so the global-memory variant is used).
 void launch_bloom_scan(gp_ctx* ctx, uint64_t d_bound, uint64_t m_host, bool decoding, cudaStream_t s) {
   Workspace& w = ctx->ws;
   const uint64_t fbytes = ((m_host + 31) / 32) * 4;
-  const uint64_t nsuper = (d_bound + kSuperKeys - 1) / kSuperKeys;
   uint32_t* bitmap = w.u32c;  // d-bit membership bitmap
+  const uint64_t nwd = (d_bound + 31) / 32;
+  cudaMemsetAsync(bitmap, 0, nwd * 4, s);
   if (m_host && fbytes <= kSmemFilterMax) {
+    using S = ScanShape<true, 4, 2>;
+    auto* kern = bloom_members<true, 4, 2>;
+    const size_t smem = (S::kStackBytes + 15) / 16 * 16 + fbytes;
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(bloom_members<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(kSmemFilterMax));
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>((S::kStackBytes + 15) / 16 * 16 + kSmemFilterMax));
       attr = true;
     }
-    const int per_sm = std::max(1, static_cast<int>((200 * 1024) / (fbytes + 40 * 1024)));
+    const int per_sm = std::max(1, static_cast<int>((220 * 1024) / (smem + 1024)));
+    const uint64_t nchunks = (d_bound + S::kChunk - 1) / S::kChunk;
     const int grid = static_cast<int>(std::max<uint64_t>(
-        1, std::min<uint64_t>((nsuper + kWarps - 1) / kWarps, static_cast<uint64_t>(ctx->sm_count) * per_sm)));
-    GP_LAUNCH(ctx, bloom_members<true>, grid, kScanBlock, fbytes, s, w.filter, w.plan, bitmap, w.status);
+        1, std::min<uint64_t>((nchunks + kWarps - 1) / kWarps, static_cast<uint64_t>(ctx->sm_count) * per_sm)));
+    GP_LAUNCH(ctx, kern, grid, kScanBlock, smem, s, w.filter, w.plan, bitmap, w.status);
   } else {
-    const int grid = static_cast<int>(std::max<uint64_t>(
-        1, std::min<uint64_t>((nsuper + kWarps - 1) / kWarps, static_cast<uint64_t>(ctx->sm_count) * 6)));
-    GP_LAUNCH(ctx, bloom_members<false>, grid, kScanBlock, 0, s, w.filter, w.plan, bitmap, w.status);
+    launch_members_global<4, 4>(ctx, d_bound, bitmap, s);  // 4 first probes / 4 batch probes per lane in flight
   }
-  const uint64_t nwd = (d_bound + 31) / 32;
   const uint64_t ntiles = (nwd + kScanBlock * 16 - 1) / (kScanBlock * 16);
   reset_scan(ctx, s, ntiles + 1);
   GP_LAUNCH(ctx, members_compact, static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, ctx->sm_count * 4ULL))),

@@ -99,10 +99,11 @@ struct Workspace {
   double* f64a = nullptr;         // [D]
   double* f64b = nullptr;         // [D]
   double* partial = nullptr;      // fit chunk partial sums [(D/2048 + 128) * 44]
-  uint32_t* sort_table = nullptr; // radix digit table [256 * (D/4096 + 2)]
+  uint32_t* sort_table = nullptr; // onesweep per-tile digit state [2][tiles][256]
+  uint32_t* sort_flags = nullptr; // [0,8): pass tickets, [64, 64+tiles): tile flags
+  uint32_t* sort_hist = nullptr;  // global digit histograms [4][256]
   double* seg_dev = nullptr;      // segmentation sweep partials [4 * 2048]
   uint32_t* seg_arg = nullptr;    // [4 * 2048]
-  uint32_t* crc_part = nullptr;   // (unused)
   uint32_t* crc_digits = nullptr; // CRC shift-operator digit tables [5 * 256]
   uint32_t* crc_acc = nullptr;    // XOR accumulator + block counter [2]
   bool crc_ready = false;

@@ -60,6 +60,14 @@ __device__ __forceinline__ uint64_t fast_mod(uint64_t x, const FastMod& f) {
   return r >= f.m ? r - f.m : r;
 }
 
+// The same for m <= 2^31: the pre-correction remainder is < 2m <= 2^32, so
+// it is exact in 32-bit arithmetic.
+__device__ __forceinline__ uint32_t fast_mod_small(uint64_t x, uint64_t minv, uint32_t m) {
+  const uint32_t q = static_cast<uint32_t>(__umul64hi(x, minv));
+  const uint32_t r = static_cast<uint32_t>(x) - q * m;
+  return r >= m ? r - m : r;
+}
+
 // ---------------------------------------------------------------- status
 __device__ __forceinline__ void latch(uint32_t* status, uint32_t code) {
   atomicCAS(status, 0u, code);

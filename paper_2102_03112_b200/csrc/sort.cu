@@ -2,12 +2,17 @@
 //
 // Used by the value codec's sort_view (curvefit.cpp:26-39: std::stable_sort
 // descending) with keys mapped so that ascending key order is descending
-// value order and equal values keep their input order.  The element count is
-// read from a device word, so the sort runs without a host round trip.
+// value order and equal values keep their input order, and by the P1 replay
+// (stable sort of draws).  The element count is read from a device word, so
+// the sort runs without a host round trip.
 //
-// Per pass: upsweep (per-tile digit histograms, digit-major table), a
-// decoupled look-back scan of the table, downsweep (stable in-tile ranks from warp
-// match_any + cross-warp digit counts, 256 elements per round).
+// One histogram kernel computes the global digit counts of every pass in one
+// read; then one "onesweep" kernel per pass: each block claims a 4096-key
+// tile in order, ranks its keys stably (warp match_any + per-warp digit
+// counters, warp-striped so that processing order is index order), publishes
+// its 256 digit counts, resolves its per-digit prefix over earlier tiles with
+// a decoupled look-back done one 32-tile window at a time by warp 0, and
+// scatters.  Tile flags carry the pass number, so they are zeroed once per sort.
 #include "gp_ctx.hpp"
 #include "gp_device.cuh"
 
@@ -18,65 +23,142 @@ namespace {
 constexpr int kBlock = 256;
 constexpr int kItems = 16;
 constexpr int kTile = kBlock * kItems;
+constexpr int kSortWarps = kBlock / 32;
 
-__global__ void __launch_bounds__(kBlock) radix_upsweep(const uint32_t* __restrict__ keys, const uint64_t* n_dev,
-                                                        int shift, uint32_t* __restrict__ table,
-                                                        const uint32_t* status) {
-  __shared__ uint32_t h[256];
+// digit histograms of passes [0, npass) over the keys (shared bins, warp-aggregated)
+__global__ void __launch_bounds__(kBlock) radix_hist(const uint32_t* __restrict__ keys, const uint64_t* n_dev,
+                                                     int npass, uint32_t* __restrict__ ghist,
+                                                     const uint32_t* status) {
+  __shared__ uint32_t h[4][256];
   if (failed(status)) return;
   const uint64_t n = *n_dev;
-  const uint64_t ntiles = (n + kTile - 1) / kTile;
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    h[threadIdx.x] = 0;
-    __syncthreads();
-    const uint64_t base = tile * kTile;
-    for (int q = threadIdx.x; q < kTile; q += kBlock)
-      if (base + q < n) atomicAdd(&h[(keys[base + q] >> shift) & 255u], 1u);
-    __syncthreads();
-    table[threadIdx.x * ntiles + tile] = h[threadIdx.x];
-    __syncthreads();
+  for (int i = threadIdx.x; i < 4 * 256; i += kBlock) h[i >> 8][i & 255] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kBlock;
+  for (uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * kBlock; i0 < n; i0 += stride) {  // warp-uniform trip count
+    const uint64_t i = i0 + threadIdx.x;
+    const bool ok = i < n;
+    const uint32_t key = ok ? keys[i] : 0u;
+    for (int p = 0; p < npass; ++p) {
+      const uint32_t dig = ok ? (key >> (8 * p)) & 255u : 256u;
+      const unsigned peers = __match_any_sync(kFull, dig);
+      if (ok && (peers & ((1u << lane) - 1)) == 0) atomicAdd(&h[p][dig], __popc(peers));
+    }
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < npass * 256; i += kBlock)
+    if (h[i >> 8][i & 255]) atomicAdd(&ghist[i], h[i >> 8][i & 255]);
 }
 
-__global__ void __launch_bounds__(kBlock) radix_downsweep(const uint32_t* __restrict__ kin,
-                                                          const uint32_t* __restrict__ vin, const uint64_t* n_dev,
-                                                          int shift, const uint32_t* __restrict__ table,
-                                                          uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
-                                                          const uint32_t* status) {
-  __shared__ uint32_t run[256];
-  __shared__ uint32_t wcnt[kBlock / 32][256];
+__global__ void __launch_bounds__(kBlock) radix_onesweep(const uint32_t* __restrict__ kin,
+                                                         const uint32_t* __restrict__ vin, const uint64_t* n_dev,
+                                                         int pass, const uint32_t* __restrict__ ghist,
+                                                         uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                         uint32_t* flags, uint32_t* agg, uint32_t* inc,
+                                                         uint32_t* ticket, const uint32_t* status) {
+  __shared__ uint32_t wcnt[kSortWarps][256];
+  __shared__ uint32_t base[256];
+  __shared__ uint64_t sh[40];
+  __shared__ uint32_t slot;
+  __shared__ int s_inc, s_lo;
   if (failed(status)) return;
   const uint64_t n = *n_dev;
-  const uint64_t ntiles = (n + kTile - 1) / kTile;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    run[threadIdx.x] = table[threadIdx.x * ntiles + tile];
-    __syncthreads();
-    const uint64_t base = tile * kTile;
-    for (int round = 0; round < kItems; ++round) {
-      const uint64_t i = base + static_cast<uint64_t>(round) * kBlock + threadIdx.x;
-      const bool ok = i < n;
-      const uint32_t key = ok ? kin[i] : 0xFFFFFFFFu;
-      const uint32_t val = ok ? vin[i] : 0u;
-      const uint32_t dig = ok ? (key >> shift) & 255u : 256u;  // 256: padding, never emitted
-      const unsigned peers = __match_any_sync(kFull, dig);
-      const uint32_t lrank = __popc(peers & ((1u << lane) - 1));
-      for (int j = lane; j < 256; j += 32) wcnt[warp][j] = 0;
-      __syncwarp();
-      if (ok && lrank == 0) wcnt[warp][dig] = __popc(peers);
-      __syncthreads();
-      if (ok) {
-        uint32_t before = 0;
-        for (int w2 = 0; w2 < warp; ++w2) before += wcnt[w2][dig];
-        const uint32_t dst = run[dig] + before + lrank;
-        kout[dst] = key;
-        vout[dst] = val;
+  const uint32_t ntiles = static_cast<uint32_t>((n + kTile - 1) / kTile);
+  const int shift = 8 * pass;
+  const uint32_t kAgg = 2 * pass + 1, kInc = 2 * pass + 2;
+  const uint32_t tile = claim_tile(ticket + pass, &slot);
+  if (tile >= ntiles) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, d = threadIdx.x;
+  for (int w = 0; w < kSortWarps; ++w) wcnt[w][d] = 0;
+  // global digit base of this pass: exclusive scan of the histogram
+  {
+    uint64_t tot;
+    base[d] = static_cast<uint32_t>(block_exclusive_sum<uint64_t, kBlock>(ghist[256 * pass + d], sh, tot));
+  }
+  __syncthreads();
+  // ---- stable in-tile ranks (warp-striped: item j of lane l is seg[32 j + l])
+  const uint64_t seg = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(warp) * (32 * kItems);
+  uint32_t key[kItems], val[kItems];
+  uint16_t rank[kItems];
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const uint64_t i = seg + 32 * j + lane;
+    key[j] = i < n ? kin[i] : 0u;
+    val[j] = i < n ? vin[i] : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    const bool ok = seg + 32 * j + lane < n;
+    const uint32_t dig = ok ? (key[j] >> shift) & 255u : 256u;
+    const unsigned peers = __match_any_sync(kFull, dig);
+    const uint32_t lr = __popc(peers & ((1u << lane) - 1));
+    const uint32_t cur = ok ? wcnt[warp][dig] : 0u;
+    __syncwarp();
+    if (ok && lr == 0) wcnt[warp][dig] = cur + __popc(peers);
+    __syncwarp();
+    rank[j] = static_cast<uint16_t>(cur + lr);
+  }
+  __syncthreads();
+  uint32_t total = 0;  // this tile's count of digit d; wcnt becomes the exclusive prefix over warps
+  for (int w = 0; w < kSortWarps; ++w) {
+    const uint32_t c = wcnt[w][d];
+    wcnt[w][d] = total;
+    total += c;
+  }
+  // ---- publish the aggregate, then look back
+  agg[static_cast<uint64_t>(tile) * 256 + d] = total;
+  if (tile == 0) inc[d] = total;
+  __threadfence();
+  __syncthreads();
+  if (d == 0) atomicExch(&flags[tile], tile == 0 ? kInc : kAgg);
+  uint32_t prefix = 0;
+  if (tile > 0) {
+    if (warp == 0) {
+      // nearest predecessor with an inclusive prefix; everything after it adds its aggregate
+      int start = static_cast<int>(tile);
+      int found = -1;
+      while (true) {
+        const int p = start - 1 - lane;
+        uint32_t f = kInc;
+        if (p >= 0) {
+          do {
+            f = *reinterpret_cast<volatile uint32_t*>(&flags[p]);
+          } while (f < kAgg);
+        }
+        const unsigned im = __ballot_sync(kFull, p < 0 || f == kInc);
+        if (im) {
+          const int q = __ffs(im) - 1;
+          found = start - 1 - q;  // -1: no predecessor published an inclusive prefix
+          break;
+        }
+        start -= 32;
       }
-      __syncthreads();
-      uint32_t tot = 0;
-      for (int w2 = 0; w2 < kBlock / 32; ++w2) tot += wcnt[w2][threadIdx.x];
-      run[threadIdx.x] += tot;
-      __syncthreads();
+      if (lane == 0) {
+        s_inc = found;
+        s_lo = found + 1;
+      }
+    }
+    __syncthreads();
+    __threadfence();
+    const int q = s_inc;
+    if (q >= 0) prefix = __ldcg(&inc[static_cast<uint64_t>(q) * 256 + d]);
+    for (int p = s_lo; p < static_cast<int>(tile); ++p) prefix += __ldcg(&agg[static_cast<uint64_t>(p) * 256 + d]);
+    inc[static_cast<uint64_t>(tile) * 256 + d] = prefix + total;
+    __threadfence();
+    __syncthreads();
+    if (d == 0) atomicExch(&flags[tile], kInc);
+  }
+  base[d] += prefix;
+  __syncthreads();
+  // ---- scatter
+#pragma unroll
+  for (int j = 0; j < kItems; ++j) {
+    if (seg + 32 * j + lane < n) {
+      const uint32_t dig = (key[j] >> shift) & 255u;
+      const uint32_t dst = base[dig] + wcnt[warp][dig] + rank[j];
+      kout[dst] = key[j];
+      vout[dst] = val[j];
     }
   }
 }
@@ -127,17 +209,23 @@ void launch_table_scan(gp_ctx* ctx, uint32_t* table, const uint64_t* n_dev, uint
 }
 
 // Sorts (keys, vals) of length *n_dev in place over `bits` low key bits
-// (multiple of 8), ping-ponging through (ktmp, vtmp).  n_bound sizes grids.
+// (multiple of 8, <= 32), ping-ponging through (ktmp, vtmp).  n_bound sizes grids.
 void launch_radix_sort(gp_ctx* ctx, uint32_t* keys, uint32_t* vals, uint32_t* ktmp, uint32_t* vtmp,
                        const uint64_t* n_dev, uint64_t n_bound, int bits, cudaStream_t s) {
   Workspace& w = ctx->ws;
+  const int npass = bits / 8;
   const uint64_t ntiles = (n_bound + kTile - 1) / kTile;
-  const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, ctx->sm_count * 4ULL)));
+  cudaMemsetAsync(w.sort_flags, 0, (64 + ntiles) * sizeof(uint32_t), s);
+  cudaMemsetAsync(w.sort_hist, 0, 4 * 256 * sizeof(uint32_t), s);
+  const int hgrid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((n_bound + kBlock - 1) / kBlock,
+                                                                               ctx->sm_count * 2ULL)));
+  GP_LAUNCH(ctx, radix_hist, hgrid, kBlock, 0, s, keys, n_dev, npass, w.sort_hist, w.status);
   uint32_t *ki = keys, *vi = vals, *ko = ktmp, *vo = vtmp;
-  for (int shift = 0; shift < bits; shift += 8) {
-    GP_LAUNCH(ctx, radix_upsweep, grid, kBlock, 0, s, ki, n_dev, shift, w.sort_table, w.status);
-    launch_table_scan(ctx, w.sort_table, n_dev, n_bound, 12, s);
-    GP_LAUNCH(ctx, radix_downsweep, grid, kBlock, 0, s, ki, vi, n_dev, shift, w.sort_table, ko, vo, w.status);
+  uint32_t* agg = w.sort_table;
+  uint32_t* inc = w.sort_table + 256 * (ntiles + 1);
+  for (int p = 0; p < npass; ++p) {
+    GP_LAUNCH(ctx, radix_onesweep, static_cast<int>(std::max<uint64_t>(1, ntiles)), kBlock, 0, s, ki, vi, n_dev, p,
+              w.sort_hist, ko, vo, w.sort_flags + 64, agg, inc, w.sort_flags, w.status);
     std::swap(ki, ko);
     std::swap(vi, vo);
   }

@@ -88,163 +88,6 @@ struct Piece {
   double dev;
 };
 
-// block-wide make_piece over t[base + begin, base + end) (curvefit.cpp:50-67)
-__device__ Piece make_piece(const double* __restrict__ t, uint32_t begin, uint32_t end, uint32_t mp,
-                            double* sdev, uint32_t* sarg) {
-  Piece p{begin, end, 0, 0, 0.0};
-  const uint32_t len = end - begin;
-  if (len < 3) return p;
-  const double y0 = t[begin];
-  const double slope = __ddiv_rn(__dsub_rn(t[end - 1], y0), static_cast<double>(len - 1));
-  double best = 0.0;
-  uint32_t arg = 0;
-  for (uint32_t i = begin + 1 + threadIdx.x; i + 1 < end; i += blockDim.x) {
-    const double pred = __dadd_rn(y0, __dmul_rn(slope, static_cast<double>(i - begin)));
-    const double e = __dsub_rn(t[i], pred);
-    const double d2 = __dmul_rn(e, e);
-    if (d2 > best) {  // strict: the first (lowest) index wins within a thread
-      best = d2;
-      arg = i;
-    }
-  }
-  // (max dev, min index among equals); threads with best == 0 never win ties
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ob = __shfl_xor_sync(kFull, best, o);
-    const uint32_t oa = __shfl_xor_sync(kFull, arg, o);
-    if (ob > best || (ob == best && ob > 0.0 && oa < arg)) {
-      best = ob;
-      arg = oa;
-    }
-  }
-  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  if ((threadIdx.x & 31) == 0) {
-    sdev[warp] = best;
-    sarg[warp] = arg;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double b = 0.0;
-    uint32_t a = 0;
-    for (int w = 0; w < nw; ++w)
-      if (sdev[w] > b || (sdev[w] == b && b > 0.0 && sarg[w] < a)) {
-        b = sdev[w];
-        a = sarg[w];
-      }
-    sdev[32] = b;
-    sarg[32] = a;
-  }
-  __syncthreads();
-  p.dev = sdev[32];
-  p.arg = sarg[32];
-  __syncthreads();
-  p.live = (p.dev > 0.0 && p.arg - begin >= mp && end - p.arg >= mp) ? 1u : 0u;
-  return p;
-}
-
-// One block: both sign parts in order (the max_segments share of the last
-// part depends on the segments emitted for the first, curvefit.cpp:473-481).
-__global__ void __launch_bounds__(1024) fit_segment(Plan* plan, const double* __restrict__ t, int degree,
-                                                    int max_segments, uint32_t* status) {
-  __shared__ double sdev[33];
-  __shared__ uint32_t sarg[33];
-  __shared__ Piece pieces[kMaxSeg];
-  __shared__ int s_np, s_best, s_budget;
-  if (failed(status) || !fit_active(plan)) return;
-  const uint64_t n = plan->n_values;
-  const uint32_t l = plan->sign_split;
-  const uint32_t un = static_cast<uint32_t>(n);
-  uint32_t pb[2], pe[2];
-  int nparts = 0;
-  if (l > 0) {
-    pb[nparts] = 0;
-    pe[nparts++] = l;
-  }
-  if (l < un) {
-    pb[nparts] = l;
-    pe[nparts++] = un;
-  }
-  const uint32_t mp = static_cast<uint32_t>(degree + 1 > 1 ? degree + 1 : 1);
-  uint32_t nseg = 0;
-  for (int pi = 0; pi < nparts; ++pi) {
-    const uint32_t b = pb[pi], e = pe[pi], len = e - b;
-    if (threadIdx.x == 0) {
-      int budget;
-      if (max_segments > 0) {
-        const long long share = static_cast<long long>(max_segments) * static_cast<long long>(len) /
-                                static_cast<long long>(n);
-        budget = share > 1 ? static_cast<int>(share) : 1;
-        if (pi + 1 == nparts) budget = max_segments - static_cast<int>(nseg) > 1 ? max_segments - static_cast<int>(nseg) : 1;
-      } else if (len < 4) {
-        budget = 1;
-      } else {  // part_budget: knot_m + knot_count_linear (curvefit.cpp:101-110, :424-428)
-        const double km = fabs(__dsub_rn(__dsub_rn(t[b], t[b + 1]), __dsub_rn(t[e - 2], t[e - 1])));
-        const double p = ceil(2.0 * sqrt(km > 0.0 ? km : 0.0));
-        const int kc = static_cast<int>(p) > 1 ? static_cast<int>(p) : 1;
-        budget = kc + 1 < 0xffff ? kc + 1 : 0xffff;
-      }
-      s_budget = budget;
-    }
-    __syncthreads();
-    const int budget = s_budget;
-    // pieces are in part-local coordinates, stored shifted by b
-    Piece p0 = make_piece(t + b, 0, len, mp, sdev, sarg);
-    if (threadIdx.x == 0) {
-      pieces[0] = p0;
-      s_np = 1;
-    }
-    __syncthreads();
-    while (s_np < budget) {
-      if (threadIdx.x == 0) {
-        int best = -1;
-        for (int i = 0; i < s_np; ++i) {
-          if (!pieces[i].live) continue;
-          if (best < 0 || pieces[i].dev > pieces[best].dev ||
-              (pieces[i].dev == pieces[best].dev && pieces[i].begin < pieces[best].begin))
-            best = i;
-        }
-        s_best = best;
-      }
-      __syncthreads();
-      const int best = s_best;
-      if (best < 0) break;
-      if (s_np >= kMaxSeg || nseg + s_np >= kMaxSeg) {
-        if (threadIdx.x == 0) latch(status, GP_CAPACITY);
-        return;
-      }
-      const Piece pp = pieces[best];
-      const Piece left = make_piece(t + b, pp.begin, pp.arg, mp, sdev, sarg);
-      const Piece right = make_piece(t + b, pp.arg, pp.end, mp, sdev, sarg);
-      if (threadIdx.x == 0) {
-        pieces[best] = left;
-        pieces[s_np] = right;
-        s_np = s_np + 1;
-      }
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-      const int np = s_np;
-      // sort by begin (insertion) and append the bounds
-      for (int i = 1; i < np; ++i) {
-        const Piece v = pieces[i];
-        int j = i;
-        while (j > 0 && pieces[j - 1].begin > v.begin) {
-          pieces[j] = pieces[j - 1];
-          --j;
-        }
-        pieces[j] = v;
-      }
-      for (int i = 0; i < np; ++i) plan->seg_end[nseg + i] = b + pieces[i].end;
-    }
-    __syncthreads();
-    nseg += static_cast<uint32_t>(s_np);
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    plan->nseg = nseg;
-    plan->degree = static_cast<uint32_t>(degree);
-  }
-}
-
 // Grid-cooperative segmentation: every make_piece (curvefit.cpp:50-67) is one
 // sweep in which all blocks scan a slice of the piece, write their block-best
 // (dev, arg) to a double-buffered partial array, grid.sync(), and every block
