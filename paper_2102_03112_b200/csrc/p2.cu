@@ -37,6 +37,7 @@ constexpr int kTileBlock = 256;
 constexpr int kTileItems = 16;
 constexpr int kTile = kTileBlock * kTileItems;
 constexpr int kMaxSetSize = 255;  // counting-sort digit; larger sets → GP_CAPACITY
+constexpr uint32_t kSingleton = 0x80000000u;  // slot flag of a size-1 set (bucket offsets < 2^31)
 
 __device__ __forceinline__ bool p2_active(const Plan* plan) {
   return plan->index_method == GP_INDEX_BLOOM_P2;
@@ -60,31 +61,52 @@ __global__ void p2_zero_counts(const Plan* plan, uint32_t* count, uint64_t m_cap
 // themselves (one positive joins a set once, the consecutive-duplicate rule of
 // bloom.cpp:159-164), so count[bit] ends as the set's size (fire-and-forget
 // atomics).
-__global__ void p2_pairs(const uint32_t* __restrict__ P, Plan* plan, uint32_t* __restrict__ pairs,
-                         uint32_t* __restrict__ count, uint64_t pair_cap, uint64_t set_cap, uint32_t* status) {
-  if (failed(status) || !p2_active(plan)) return;
-  const uint64_t n = plan->n_pos, m = plan->m;
-  const uint32_t k = plan->k;
-  if (n * k > pair_cap || m > set_cap || k > 64) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) latch(status, GP_CAPACITY);
-    return;
-  }
-  const FastMod fm{m, plan->minv};
-  const uint64_t sa = plan->seed_a + kGamma, sb = plan->seed_b + kGamma;
+template <int KM, bool kSmallM>
+__device__ __forceinline__ void pairs_body(const uint32_t* __restrict__ P, uint64_t n, uint32_t k, const FastMod& fm,
+                                           uint64_t sa, uint64_t sb, uint32_t* __restrict__ pairs,
+                                           uint32_t* __restrict__ count) {
   for (uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; p < n;
        p += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t x = P[p];
     const uint64_t a = mix64(x ^ sa), b = mix64(x ^ sb);
     uint64_t h = a;
-    uint32_t seen[64];
-    for (uint32_t j = 0; j < k; ++j, h += b) {
-      const uint32_t bit = static_cast<uint32_t>(fast_mod(mix64(h), fm));
-      bool dup = false;
-      for (uint32_t i = 0; i < j; ++i) dup |= seen[i] == bit;
-      seen[j] = bit;
-      pairs[p * k + j] = dup ? 0xFFFFFFFFu : bit;
-      if (!dup) atomicAdd(&count[bit], 1u);
+    uint32_t seen[KM];  // registers for KM <= 16 (fully unrolled)
+#pragma unroll
+    for (int j = 0; j < KM; ++j) {
+      if (j < static_cast<int>(k)) {
+        const uint32_t bit = kSmallM ? fast_mod_small(mix64(h), fm.minv, static_cast<uint32_t>(fm.m))
+                                     : static_cast<uint32_t>(fast_mod(mix64(h), fm));
+        h += b;
+        bool dup = false;
+#pragma unroll
+        for (int i = 0; i < j; ++i) dup |= seen[i] == bit;
+        seen[j] = bit;
+        pairs[p * k + j] = dup ? 0xFFFFFFFFu : bit;
+        if (!dup) atomicAdd(&count[bit], 1u);
+      }
     }
+  }
+}
+
+__global__ void p2_pairs(const uint32_t* __restrict__ P, Plan* plan, uint32_t* __restrict__ pairs,
+                         uint32_t* __restrict__ count, uint64_t pair_cap, uint64_t set_cap, uint32_t* status) {
+  if (failed(status) || !p2_active(plan)) return;
+  const uint64_t n = plan->n_pos, m = plan->m;
+  const uint32_t k = plan->k;
+  if (n * k > pair_cap || n * k >= kSingleton || m > set_cap || k > 64) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) latch(status, GP_CAPACITY);
+    return;
+  }
+  const FastMod fm{m, plan->minv};
+  const uint64_t sa = plan->seed_a + kGamma, sb = plan->seed_b + kGamma;
+  const bool small = m <= (1ull << 31);
+  if (k <= 16) {
+    if (small)
+      pairs_body<16, true>(P, n, k, fm, sa, sb, pairs, count);
+    else
+      pairs_body<16, false>(P, n, k, fm, sa, sb, pairs, count);
+  } else {
+    pairs_body<64, false>(P, n, k, fm, sa, sb, pairs, count);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) plan->n_pairs = n * k;
 }
@@ -94,71 +116,82 @@ __global__ void p2_pairs(const uint32_t* __restrict__ P, Plan* plan, uint32_t* _
 // scatter cursors, and the tile's histogram of set sizes for the (size, bit)
 // ordering (digit-major table[size * ntiles + tile]).
 __global__ void __launch_bounds__(kTileBlock) p2_tiles(const uint32_t* __restrict__ count, Plan* plan,
-                                                       uint32_t* __restrict__ off, uint32_t* __restrict__ cursor,
-                                                       uint32_t* __restrict__ table, uint32_t* alloc,
-                                                       uint32_t* status) {
+                                                       uint32_t* __restrict__ slot, uint32_t* __restrict__ table,
+                                                       uint32_t* alloc, uint32_t* status) {
   __shared__ uint32_t h[256];
+  __shared__ uint32_t sh32[33];
+  __shared__ uint32_t s_base;
   if (failed(status) || !p2_active(plan)) return;
   const uint64_t m = plan->m;
   const uint64_t ntiles = (m + kTile - 1) / kTile;
-  const uint64_t tile = blockIdx.x;
-  if (tile >= ntiles) return;
-  __shared__ uint32_t sh32[33];
-  __shared__ uint32_t s_base;
-  h[threadIdx.x] = 0;
-  __syncthreads();
-  uint32_t c[kTileItems];
-  uint32_t need = 0;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    uint32_t c[kTileItems];
+    uint32_t need = 0;
+    uint32_t small[4] = {0, 0, 0, 0};  // sizes 1..4 (almost every set) counted in registers
 #pragma unroll
-  for (int q = 0; q < kTileItems; ++q) {
-    const uint64_t b = tile * kTile + static_cast<uint64_t>(q) * kTileBlock + threadIdx.x;
-    c[q] = b < m ? count[b] : 0;
-    if (c[q] >= kMaxSetSize) latch(status, GP_CAPACITY);
-    if (c[q]) atomicAdd(&h[c[q] < 255 ? c[q] : 255], 1u);
-    need += c[q] >= 2 ? c[q] : 0;
-  }
-  uint32_t tot;
-  uint32_t o = block_exclusive_sum<uint32_t, kTileBlock>(need, sh32, tot);
-  if (threadIdx.x == 0) s_base = tot ? atomicAdd(alloc, tot) : 0;  // one allocation per tile
-  __syncthreads();
-  o += s_base;
-#pragma unroll
-  for (int q = 0; q < kTileItems; ++q) {
-    if (c[q] >= 2) {
+    for (int q = 0; q < kTileItems; ++q) {
       const uint64_t b = tile * kTile + static_cast<uint64_t>(q) * kTileBlock + threadIdx.x;
-      off[b] = o;
-      cursor[b] = c[q];
-      o += c[q];
+      c[q] = b < m ? count[b] : 0;
     }
+#pragma unroll
+    for (int q = 0; q < kTileItems; ++q) {
+      if (c[q] >= kMaxSetSize) latch(status, GP_CAPACITY);
+#pragma unroll
+      for (int z = 0; z < 4; ++z) small[z] += c[q] == static_cast<uint32_t>(z + 1) ? 1u : 0u;
+      if (c[q] > 4) atomicAdd(&h[c[q] < 255 ? c[q] : 255], 1u);
+      need += c[q];
+    }
+#pragma unroll
+    for (int z = 0; z < 4; ++z) {
+      const uint32_t v = __reduce_add_sync(kFull, small[z]);
+      if ((threadIdx.x & 31) == 0 && v) atomicAdd(&h[z + 1], v);
+    }
+    uint32_t tot;
+    uint32_t o = block_exclusive_sum<uint32_t, kTileBlock>(need, sh32, tot);
+    if (threadIdx.x == 0) s_base = tot ? atomicAdd(alloc, tot) : 0;  // one allocation per tile
+    __syncthreads();
+    o += s_base;
+#pragma unroll
+    for (int q = 0; q < kTileItems; ++q) {
+      if (c[q]) {
+        const uint64_t b = tile * kTile + static_cast<uint64_t>(q) * kTileBlock + threadIdx.x;
+        o += c[q];
+        slot[b] = o | (c[q] == 1 ? kSingleton : 0u);  // end of the bucket; the scatter counts down
+      }
+    }
+    table[threadIdx.x * ntiles + tile] = h[threadIdx.x];
+    __syncthreads();
   }
-  table[threadIdx.x * ntiles + tile] = h[threadIdx.x];
 }
 
 // One thread per positive p and its k pairs: a size-1 set's member is
 // selected in stage A (every singleton is visited first, p2_select pass 1;
 // plain byte flags, idempotent) and recorded in single[]; multi-set members
 // go to their bucket (arbitrary order, sorted later).
-__global__ void p2_scatter(const uint32_t* __restrict__ pairs, const Plan* plan, const uint32_t* __restrict__ count,
-                           const uint32_t* __restrict__ off, uint32_t* cursor, uint32_t* __restrict__ members,
-                           uint32_t* __restrict__ single, uint8_t* __restrict__ flags, const uint32_t* status) {
+__global__ void p2_scatter(const uint32_t* __restrict__ pairs, const Plan* plan, uint32_t* slot,
+                           uint32_t* __restrict__ members, uint8_t* __restrict__ flags, const uint32_t* status) {
   if (failed(status) || !p2_active(plan)) return;
   const uint64_t n = plan->n_pos;
   const uint32_t k = plan->k;
-  for (uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; p < n;
-       p += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    bool sel = false;
-    for (uint32_t j = 0; j < k; ++j) {
-      const uint32_t bit = pairs[p * k + j];
-      if (bit == 0xFFFFFFFFu) continue;
-      const uint32_t c = count[bit];
-      if (c == 1) {
-        single[bit] = static_cast<uint32_t>(p);
-        sel = true;
-      } else {
-        members[off[bit] + atomicSub(&cursor[bit], 1u) - 1u] = static_cast<uint32_t>(p);
-      }
+  const uint64_t np = n * k;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  // 4 pairs per thread per step, strided by the grid: 4 independent chains in flight
+  for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i0 < np; i0 += 4 * stride) {
+    uint32_t bit[4], v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) bit[u] = i0 + u * stride < np ? pairs[i0 + u * stride] : 0xFFFFFFFFu;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = bit[u] != 0xFFFFFFFFu ? atomicSub(&slot[bit[u]], 1u) : 0u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (bit[u] == 0xFFFFFFFFu) continue;
+      const uint64_t i = i0 + u * stride;
+      const uint32_t p = static_cast<uint32_t>(np < (1ull << 32) ? static_cast<uint32_t>(i) / k : i / k);
+      members[(v[u] & ~kSingleton) - 1u] = p;
+      if (v[u] & kSingleton) flags[p] = 1;  // flags were zeroed; every writer stores the same value
     }
-    flags[p] = sel ? 1 : 0;
   }
 }
 
@@ -181,35 +214,49 @@ __global__ void p2_count_sets(Plan* plan, const uint32_t* __restrict__ table, co
 __global__ void __launch_bounds__(kTileBlock) p2_size_scatter(const Plan* plan, const uint32_t* __restrict__ size,
                                                               const uint32_t* __restrict__ table,
                                                               uint32_t* __restrict__ sets, const uint32_t* status) {
-  __shared__ uint32_t run[256];
-  __shared__ uint32_t wcnt[kTileBlock / 32][256];
+  constexpr int kW = kTileBlock / 32;
+  __shared__ uint32_t wcnt[kW][256];
   if (failed(status) || !p2_active(plan)) return;
   const uint64_t m = plan->m;
   const uint64_t ntiles = (m + kTile - 1) / kTile;
-  const uint64_t tile = blockIdx.x;
-  if (tile >= ntiles) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  run[threadIdx.x] = table[threadIdx.x * ntiles + tile];
-  __syncthreads();
-  const uint64_t base = tile * kTile;
-  for (int round = 0; round < kTileItems; ++round) {
-    const uint64_t b = base + static_cast<uint64_t>(round) * kTileBlock + threadIdx.x;
-    const uint32_t s = b < m ? size[b] : 0;
-    const unsigned peers = __match_any_sync(kFull, s);
-    const uint32_t lrank = __popc(peers & ((1u << lane) - 1));
-    for (int i = lane; i < 256; i += 32) wcnt[warp][i] = 0;
-    __syncwarp();
-    if (lrank == 0) wcnt[warp][s] = __popc(peers);
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int w = 0; w < kW; ++w) wcnt[w][threadIdx.x] = 0;
     __syncthreads();
-    if (s) {
-      uint32_t before = 0;
-      for (int w2 = 0; w2 < warp; ++w2) before += wcnt[w2][s];
-      sets[run[s] + before + lrank] = static_cast<uint32_t>(b);
+    // warp w owns bits [seg, seg + 512): item j of lane l is bit seg + 32 j + l,
+    // so processing order is bit order
+    const uint64_t seg = tile * kTile + static_cast<uint64_t>(warp) * (32 * kTileItems);
+    uint32_t sz[kTileItems];
+    uint16_t rank[kTileItems];
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j) {
+      const uint64_t b = seg + 32 * j + lane;
+      sz[j] = b < m ? size[b] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j) {
+      const uint32_t s = sz[j];
+      const unsigned peers = __match_any_sync(kFull, s);
+      const uint32_t lr = __popc(peers & ((1u << lane) - 1));
+      const uint32_t cur = s ? wcnt[warp][s] : 0u;
+      __syncwarp();
+      if (s && lr == 0) wcnt[warp][s] = cur + __popc(peers);
+      __syncwarp();
+      rank[j] = static_cast<uint16_t>(cur + lr);
     }
     __syncthreads();
-    uint32_t tot = 0;
-    for (int w2 = 0; w2 < kTileBlock / 32; ++w2) tot += wcnt[w2][threadIdx.x];
-    run[threadIdx.x] += tot;
+    {  // exclusive over warps, plus the tile's base for this size from the scanned table
+      uint32_t run = table[threadIdx.x * ntiles + tile];
+      for (int w = 0; w < kW; ++w) {
+        const uint32_t c = wcnt[w][threadIdx.x];
+        wcnt[w][threadIdx.x] = run;
+        run += c;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j)
+      if (sz[j]) sets[wcnt[warp][sz[j]] + rank[j]] = static_cast<uint32_t>(seg + 32 * j + lane);
     __syncthreads();
   }
 }
@@ -308,8 +355,7 @@ __device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __res
     const uint64_t si = start + (cursor + v) % L;
     const uint32_t bit = sets[si];
     const uint32_t sz = size[bit];
-    // size-1 sets (visited only on the fallback path) keep their member in single[]
-    const uint32_t* mems = sz == 1 ? single + bit : members + off[bit];
+    const uint32_t* mems = members + (off[bit] & ~kSingleton);  // slot = bucket start after the scatter
     const uint32_t lo = 0;
     for (uint32_t j = 0; j < sz; ++j) first_touch[mems[lo + j]] = 0xFFFFFFFFu;
     __syncthreads();
@@ -467,11 +513,11 @@ void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t 
   GP_LAUNCH(ctx, p2_pairs, grid_for(ctx, n_bound, 128), 128, 0, s, w.pos, w.plan, w.pairs, w.p2_count, w.pair_cap,
             w.set_cap, w.status);
   const uint64_t mtiles = (m_cap + kTile - 1) / kTile;
-  const int tgrid = static_cast<int>(std::max<uint64_t>(1, mtiles));
-  GP_LAUNCH(ctx, p2_tiles, tgrid, kTileBlock, 0, s, w.p2_count, w.plan, w.p2_off, w.p2_cursor, w.p2_table, w.p2_alloc,
-            w.status);
-  GP_LAUNCH(ctx, p2_scatter, grid_for(ctx, n_bound, 128), 128, 0, s, w.pairs, w.plan, w.p2_count, w.p2_off,
-            w.p2_cursor, w.p2_members, w.p2_single, w.flags, w.status);
+  const int tgrid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(mtiles, ctx->sm_count * 8ULL)));
+  GP_LAUNCH(ctx, p2_tiles, tgrid, kTileBlock, 0, s, w.p2_count, w.plan, w.p2_off, w.p2_table, w.p2_alloc, w.status);
+  cudaMemsetAsync(w.flags, 0, n_bound, s);
+  GP_LAUNCH(ctx, p2_scatter, grid_for(ctx, n_bound * k_bound, 256), 256, 0, s, w.pairs, w.plan, w.p2_off, w.p2_members,
+            w.flags, w.status);
   launch_table_scan(ctx, w.p2_table, &w.plan->m, m_cap, 12, s);
   GP_LAUNCH(ctx, p2_count_sets, 1, 32, 0, s, w.plan, w.p2_table, w.status);
   GP_LAUNCH(ctx, p2_size_scatter, tgrid, kTileBlock, 0, s, w.plan, w.p2_count, w.p2_table, w.p2_sets, w.status);

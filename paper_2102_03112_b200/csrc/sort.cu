@@ -21,7 +21,7 @@ namespace gp {
 namespace {
 
 constexpr int kBlock = 256;
-constexpr int kItems = 16;
+constexpr int kItems = 8;
 constexpr int kTile = kBlock * kItems;
 constexpr int kSortWarps = kBlock / 32;
 
@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(kBlock) radix_onesweep(const uint32_t* __restr
                                                          uint32_t* ticket, const uint32_t* status) {
   __shared__ uint32_t wcnt[kSortWarps][256];
   __shared__ uint32_t base[256];
+  __shared__ __align__(16) uint32_t red_sh[kSortWarps][256];
   __shared__ uint64_t sh[40];
   __shared__ uint32_t slot;
   __shared__ int s_inc, s_lo;
@@ -141,9 +142,31 @@ __global__ void __launch_bounds__(kBlock) radix_onesweep(const uint32_t* __restr
     }
     __syncthreads();
     __threadfence();
-    const int q = s_inc;
-    if (q >= 0) prefix = __ldcg(&inc[static_cast<uint64_t>(q) * 256 + d]);
-    for (int p = s_lo; p < static_cast<int>(tile); ++p) prefix += __ldcg(&agg[static_cast<uint64_t>(p) * 256 + d]);
+    // inclusive prefix of tile q (if any) + aggregates of tiles (q, tile): warp w
+    // sums rows lo + w, lo + w + 8, ... (lane owns 8 digits), then a cross-warp sum
+    {
+      const int q = s_inc, lo = s_lo;
+      uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      auto add_row = [&](const uint32_t* row) {
+        const uint4 x0 = __ldcg(reinterpret_cast<const uint4*>(row) + 2 * lane);
+        const uint4 x1 = __ldcg(reinterpret_cast<const uint4*>(row) + 2 * lane + 1);
+        acc[0] += x0.x; acc[1] += x0.y; acc[2] += x0.z; acc[3] += x0.w;
+        acc[4] += x1.x; acc[5] += x1.y; acc[6] += x1.z; acc[7] += x1.w;
+      };
+      if (warp == 0 && q >= 0) add_row(inc + static_cast<uint64_t>(q) * 256);
+      int p = lo + warp;
+      for (; p + 3 * kSortWarps < static_cast<int>(tile); p += 4 * kSortWarps) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) add_row(agg + static_cast<uint64_t>(p + u * kSortWarps) * 256);
+      }
+      for (; p < static_cast<int>(tile); p += kSortWarps) add_row(agg + static_cast<uint64_t>(p) * 256);
+      uint32_t* red = &red_sh[warp][0];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) red[8 * lane + u] = acc[u];
+      __syncthreads();
+#pragma unroll
+      for (int w = 0; w < kSortWarps; ++w) prefix += red_sh[w][d];
+    }
     inc[static_cast<uint64_t>(tile) * 256 + d] = prefix + total;
     __threadfence();
     __syncthreads();

@@ -145,24 +145,45 @@ __device__ void seg_sweep(const double* __restrict__ t, const SweepRange* rr, in
     __syncthreads();
   }
   grid.sync();
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < nr; ++q) {
+  // every block reduces the G partials of each range, all threads in parallel
+  for (int q = 0; q < nr; ++q) {
+    double best = 0.0;
+    uint32_t arg = 0;
+    for (uint32_t j = threadIdx.x; j < G; j += blockDim.x) {
+      const double v = __ldcg(&pdev[q * G + j]);
+      const uint32_t a = __ldcg(&parg[q * G + j]);
+      if (v > best || (v == best && best > 0.0 && a < arg)) {
+        best = v;
+        arg = a;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(kFull, best, o);
+      const uint32_t oa = __shfl_xor_sync(kFull, arg, o);
+      if (ob > best || (ob == best && ob > 0.0 && oa < arg)) {
+        best = ob;
+        arg = oa;
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      sdev[threadIdx.x >> 5] = best;
+      sarg[threadIdx.x >> 5] = arg;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
       double bb = 0.0;
       uint32_t aa = 0;
-      for (uint32_t j = 0; j < G; ++j) {
-        const double v = pdev[q * G + j];
-        const uint32_t a = parg[q * G + j];
-        if (v > bb || (v == bb && bb > 0.0 && a < aa)) {
-          bb = v;
-          aa = a;
+      for (uint32_t w = 0; w < blockDim.x / 32; ++w)
+        if (sdev[w] > bb || (sdev[w] == bb && bb > 0.0 && sarg[w] < aa)) {
+          bb = sdev[w];
+          aa = sarg[w];
         }
-      }
       Piece p{rr[q].begin, rr[q].end, aa, 0u, bb};
       p.live = (bb > 0.0 && aa - p.begin >= mp && p.end - aa >= mp) ? 1u : 0u;
       out[q] = p;
     }
+    __syncthreads();
   }
-  __syncthreads();
 }
 
 __global__ void __launch_bounds__(256) fit_segment_coop(Plan* plan, const double* __restrict__ t, int degree,
@@ -388,74 +409,100 @@ __global__ void fit_solve(Plan* plan, const double* __restrict__ t, const double
   }
   const int eff = deg < static_cast<int>(len) - 1 ? deg : static_cast<int>(len) - 1;
   const int m = eff + 1;
-  // chunk index range of this segment
-  uint64_t first = 0;
-  for (uint32_t s = 0; s < seg; ++s) {
-    uint32_t bb, ee;
-    seg_range(plan, s, bb, ee);
-    first += (ee - bb + kChunk - 1) / kChunk;
-  }
-  const uint64_t nc = (len + kChunk - 1) / kChunk;
-  double acc[kAcc];
-  for (int j = 0; j < kAcc; ++j) acc[j] = sacc[j];
-  (void)nc;
-  (void)first;
+  // Every loop below runs over the fixed bound kCps with an `< m` guard and is
+  // fully unrolled, so the 8x8 systems live in registers, not local memory.
   double G[kCps][kCps], rhs[kCps];
-  int a = 0;
-  for (int j = 0; j <= kMaxDeg; ++j)
-    for (int q = j; q <= kMaxDeg; ++q, ++a) {
-      if (j < m && q < m) G[j][q] = G[q][j] = acc[a];
-    }
-  for (int j = 0; j < m; ++j) rhs[j] = acc[36 + j];
+  {
+    int a = 0;
+#pragma unroll
+    for (int j = 0; j <= kMaxDeg; ++j)
+#pragma unroll
+      for (int q = j; q <= kMaxDeg; ++q, ++a) G[j][q] = G[q][j] = sacc[a];
+  }
+#pragma unroll
+  for (int j = 0; j < kCps; ++j) rhs[j] = sacc[36 + j];
   // Cholesky G = L L^T (SPD: the Legendre columns are independent for len > eff)
-  double L[kCps][kCps] = {};
-  for (int j = 0; j < m; ++j) {
-    double s = G[j][j];
-    for (int q = 0; q < j; ++q) s -= L[j][q] * L[j][q];
-    L[j][j] = sqrt(s > 0.0 ? s : 0.0);
-    for (int i = j + 1; i < m; ++i) {
-      double v = G[i][j];
-      for (int q = 0; q < j; ++q) v -= L[i][q] * L[j][q];
-      L[i][j] = L[j][j] > 0.0 ? v / L[j][j] : 0.0;
+  double L[kCps][kCps];
+#pragma unroll
+  for (int j = 0; j < kCps; ++j)
+#pragma unroll
+    for (int i = 0; i < kCps; ++i) L[j][i] = 0.0;
+#pragma unroll
+  for (int j = 0; j < kCps; ++j) {
+    if (j < m) {
+      double s = G[j][j];
+#pragma unroll
+      for (int q = 0; q < j; ++q) s -= L[j][q] * L[j][q];
+      L[j][j] = sqrt(s > 0.0 ? s : 0.0);
+#pragma unroll
+      for (int i = j + 1; i < kCps; ++i) {
+        if (i < m) {
+          double v = G[i][j];
+#pragma unroll
+          for (int q = 0; q < j; ++q) v -= L[i][q] * L[j][q];
+          L[i][j] = L[j][j] > 0.0 ? v / L[j][j] : 0.0;
+        }
+      }
     }
   }
   double z[kCps], aL[kCps];
-  for (int i = 0; i < m; ++i) {
+#pragma unroll
+  for (int i = 0; i < kCps; ++i) {
     double v = rhs[i];
+#pragma unroll
     for (int q = 0; q < i; ++q) v -= L[i][q] * z[q];
-    z[i] = L[i][i] > 0.0 ? v / L[i][i] : 0.0;
+    z[i] = (i < m && L[i][i] > 0.0) ? v / L[i][i] : 0.0;
   }
-  for (int i = m - 1; i >= 0; --i) {
+#pragma unroll
+  for (int i = kCps - 1; i >= 0; --i) {
     double v = z[i];
-    for (int q = i + 1; q < m; ++q) v -= L[q][i] * aL[q];
-    aL[i] = L[i][i] > 0.0 ? v / L[i][i] : 0.0;
+#pragma unroll
+    for (int q = i + 1; q < kCps; ++q) v -= L[q][i] * aL[q];  // L[q][i] = 0 for q >= m
+    aL[i] = (i < m && L[i][i] > 0.0) ? v / L[i][i] : 0.0;
   }
   // Legendre → t-monomials: P_{j+1} = ((2j+1) t P_j - j P_{j-1}) / (j+1)
-  double Lc[kCps][kCps] = {};
+  double Lc[kCps][kCps];
+#pragma unroll
+  for (int j = 0; j < kCps; ++j)
+#pragma unroll
+    for (int p = 0; p < kCps; ++p) Lc[j][p] = 0.0;
   Lc[0][0] = 1.0;
-  if (m > 1) Lc[1][1] = 1.0;
-  for (int j = 1; j + 1 < m; ++j)
+  Lc[1][1] = 1.0;
+#pragma unroll
+  for (int j = 1; j + 1 < kCps; ++j)
+#pragma unroll
     for (int p = 0; p <= j + 1; ++p)
       Lc[j + 1][p] = ((2 * j + 1) * (p > 0 ? Lc[j][p - 1] : 0.0) - j * Lc[j - 1][p]) / (j + 1);
   double ct[kCps];
-  for (int p = 0; p < m; ++p) {
+#pragma unroll
+  for (int p = 0; p < kCps; ++p) {
     double v = 0.0;
-    for (int j = p; j < m; ++j) v += aL[j] * Lc[j][p];
+#pragma unroll
+    for (int j = p; j < kCps; ++j) v += aL[j] * Lc[j][p];  // aL[j] = 0 for j >= m
     ct[p] = v;
   }
-  // t-monomials → x-monomials, curvefit.cpp:157-172
+  // t-monomials → x-monomials, curvefit.cpp:157-172 (the same pow() values)
   const double alpha = 2.0 / static_cast<double>(len - 1);
   const double beta = -static_cast<double>(len + 1) / static_cast<double>(len - 1);
-  double binom[kCps][kCps];
-  for (int j = 0; j < m; ++j) {
-    for (int k = 0; k <= j; ++k) binom[j][k] = 1.0;
-    for (int k = 1; k < j; ++k) binom[j][k] = binom[j - 1][k - 1] + binom[j - 1][k];
+  double pa[kCps], pb[kCps];
+#pragma unroll
+  for (int k = 0; k < kCps; ++k) {
+    pa[k] = k < m ? pow(alpha, static_cast<double>(k)) : 0.0;
+    pb[k] = k < m ? pow(beta, static_cast<double>(k)) : 0.0;
   }
-  for (int k = 0; k < m; ++k) {
-    double c = 0.0;
-    const double ak = pow(alpha, static_cast<double>(k));
-    for (int j = k; j < m; ++j) c += ct[j] * binom[j][k] * ak * pow(beta, static_cast<double>(j - k));
-    out[k] = static_cast<float>(c);
+  constexpr double kBinom[kCps][kCps] = {{1, 0, 0, 0, 0, 0, 0, 0},       {1, 1, 0, 0, 0, 0, 0, 0},
+                                         {1, 2, 1, 0, 0, 0, 0, 0},       {1, 3, 3, 1, 0, 0, 0, 0},
+                                         {1, 4, 6, 4, 1, 0, 0, 0},       {1, 5, 10, 10, 5, 1, 0, 0},
+                                         {1, 6, 15, 20, 15, 6, 1, 0},    {1, 7, 21, 35, 35, 21, 7, 1}};
+#pragma unroll
+  for (int k = 0; k < kCps; ++k) {
+    if (k < m) {
+      double c = 0.0;
+#pragma unroll
+      for (int j = k; j < kCps; ++j)
+        if (j < m) c += ct[j] * kBinom[j][k] * pa[k] * pb[j - k];
+      out[k] = static_cast<float>(c);
+    }
   }
 }
 
