@@ -136,7 +136,8 @@ class BucketedSparseAllgather:
     def bucket_seed(self, seed: int, step: int, b: int) -> int:
         return hash64(b, pipeline_seed(seed, self.rank, step))
 
-    def step(self, grad: torch.Tensor, step: int, seed: int = 1) -> torch.Tensor:
+    def step(self, grad: torch.Tensor, step: int, seed: int = 1, dense: torch.Tensor | None = None) -> torch.Tensor:
+        out_dense = self.dense if dense is None else dense
         cur = torch.cuda.current_stream() if self.streams[0] is not None else None
         if cur is not None:
             for s in self.streams:
@@ -147,10 +148,62 @@ class BucketedSparseAllgather:
             cfg = replace(self.cfg, seed=self.bucket_seed(seed, step, b))
             if s is not None:
                 with torch.cuda.stream(s):
-                    self.ex[b].step_seeded(grad[lo:hi], cfg, dense=self.dense[lo:hi], stream=s)
+                    self.ex[b].step_seeded(grad[lo:hi], cfg, dense=out_dense[lo:hi], stream=s)
             else:
-                self.ex[b].step_seeded(grad[lo:hi], cfg, dense=self.dense[lo:hi])
+                self.ex[b].step_seeded(grad[lo:hi], cfg, dense=out_dense[lo:hi])
         if cur is not None:
             for s in self.streams:
                 cur.wait_stream(s)
-        return self.dense
+        return out_dense
+
+
+class HostPipeline:
+    """DP steps on HOST buffers with the copies overlapped across steps.
+
+    The harness's step (harness.cpp:219-293) takes host gradients and produces
+    the host dense mean.  Here step i's gradient is copied in on its own stream
+    while step i-1 computes, and step i-1's mean is copied out on a third stream
+    while step i computes (PCIe is full duplex), through double-buffered device
+    input/output.  submit() only enqueues; drain() waits for the last copy-out.
+    The caller must not overwrite a host output buffer before its step drained
+    (alternate at least two)."""
+
+    def __init__(self, ex, d: int, device=None):
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.ex = ex
+        self.gin = [torch.empty(d, dtype=torch.float32, device=dev) for _ in range(2)]
+        self.dout = [torch.zeros(d, dtype=torch.float32, device=dev) for _ in range(2)]
+        self.s_in = torch.cuda.Stream(dev)
+        self.s_out = torch.cuda.Stream(dev)
+        self.in_ready = [torch.cuda.Event() for _ in range(2)]
+        self.in_free = [torch.cuda.Event() for _ in range(2)]
+        self.out_ready = [torch.cuda.Event() for _ in range(2)]
+        self.out_free = [torch.cuda.Event() for _ in range(2)]
+        self.used = [False, False]
+        self.i = 0
+
+    def submit(self, host_in: torch.Tensor, host_out: torch.Tensor, step: int, seed: int = 1,
+               between=None) -> None:
+        b = self.i & 1
+        compute = torch.cuda.current_stream()
+        if self.used[b]:
+            self.s_in.wait_event(self.in_free[b])    # step i-2 finished reading gin[b]
+            compute.wait_event(self.out_free[b])     # step i-2's copy-out of dout[b] finished
+        with torch.cuda.stream(self.s_in):
+            self.gin[b].copy_(host_in, non_blocking=True)
+            self.in_ready[b].record(self.s_in)
+        if between is not None:
+            between()                                # e.g. the benchmark's L2 flush, on the compute stream
+        compute.wait_event(self.in_ready[b])
+        self.ex.step(self.gin[b], step=step, seed=seed, dense=self.dout[b])
+        self.in_free[b].record(compute)
+        self.out_ready[b].record(compute)
+        self.s_out.wait_event(self.out_ready[b])
+        with torch.cuda.stream(self.s_out):
+            host_out.copy_(self.dout[b], non_blocking=True)
+            self.out_free[b].record(self.s_out)
+        self.used[b] = True
+        self.i += 1
+
+    def drain(self) -> None:
+        self.s_out.synchronize()

@@ -1,0 +1,80 @@
+"""The DP step on one GPU (N = 1): SparseAllgather / BucketedSparseAllgather
+against the oracle's encode → decode of the same pipeline seed, and the
+host-buffer HostPipeline (overlapped copies) against the plain device step."""
+import numpy as np
+import pytest
+import torch
+
+from oracle.bindings import GpConfig, synthetic_gradient
+
+pytestmark = pytest.mark.gpu
+
+BITMAP, P2 = 1, 6
+V_NONE, V_FIT = 0, 1
+
+
+def _pcfg(im, vm, **kw):
+    from paper_2102_03112_b200 import PipelineConfig
+    return PipelineConfig(index_method=im, value_method=vm, **kw)
+
+
+@pytest.mark.parametrize("im,vm,fpr", [(BITMAP, V_NONE, 0.01), (P2, V_FIT, 0.001)])
+def test_dp_step_matches_oracle(oracle, im, vm, fpr):
+    from paper_2102_03112_b200 import Codec
+    from paper_2102_03112_b200.dp import SparseAllgather, pipeline_seed
+    d, r = 300_000, 3_000
+    g = synthetic_gradient(d, rank=0)
+    codec = Codec(max_d=d)
+    ex = SparseAllgather(codec, d, r, _pcfg(im, vm, fpr=fpr))
+    dense = ex.step(torch.from_numpy(g).cuda(), step=5).cpu().numpy()
+    codec.status()
+    c = oracle.encode_dense(g, r, GpConfig.make(im, vm, fpr=fpr, seed=pipeline_seed(1, 0, 5)))
+    assert bytes(ex.out[: int(ex.length.item())].cpu().numpy()) == c
+    ref = np.zeros(d, np.float64)
+    oracle.decode_accumulate(c, ref, 1.0)
+    # one f32 term per coordinate: the decoded value rounded to f32 (fit values are f64)
+    assert np.array_equal(dense, ref.astype(np.float32))
+    codec.close()
+
+
+def test_host_pipeline_matches_device_step():
+    from paper_2102_03112_b200 import Codec
+    from paper_2102_03112_b200.dp import HostPipeline, SparseAllgather
+    d, r = 400_000, 4_000
+    codec = Codec(max_d=d)
+    ex = SparseAllgather(codec, d, r, _pcfg(P2, V_FIT, fpr=0.001))
+    grads = [synthetic_gradient(d, rank=w) for w in range(3)]
+    want = []
+    for i, g in enumerate(grads):
+        want.append(ex.step(torch.from_numpy(g).cuda(), step=i).cpu().numpy().copy())
+    codec.status()
+    pipe = HostPipeline(ex, d)
+    ins = [torch.from_numpy(g).pin_memory() for g in grads]
+    outs = [torch.empty(d, dtype=torch.float32).pin_memory() for _ in grads]
+    for i in range(3):
+        pipe.submit(ins[i], outs[i], step=i)
+    pipe.drain()
+    codec.status()
+    for i in range(3):
+        assert np.array_equal(outs[i].numpy(), want[i])
+    codec.close()
+
+
+def test_bucketed_step_is_bucketwise():
+    from paper_2102_03112_b200 import Codec
+    from paper_2102_03112_b200.dp import BucketedSparseAllgather, SparseAllgather
+    d, ratio, buckets = 600_001, 0.01, 4
+    g = torch.from_numpy(synthetic_gradient(d, rank=2)).cuda()
+    cfg = _pcfg(BITMAP, V_NONE)
+    bex = BucketedSparseAllgather(lambda dm: Codec(max_d=dm), d, ratio, cfg, buckets, streams=2)
+    got = bex.step(g, step=3).clone()
+    torch.cuda.synchronize()
+    for c in bex.codecs:
+        c.status()
+    from dataclasses import replace
+    for b, (lo, hi) in enumerate(bex.bounds):
+        codec = Codec(max_d=hi - lo)
+        one = SparseAllgather(codec, hi - lo, bex.rs[b], cfg)
+        want = one.step_seeded(g[lo:hi], replace(cfg, seed=bex.bucket_seed(1, 3, b)))
+        assert torch.equal(got[lo:hi], want)
+        codec.close()

@@ -1,4 +1,4 @@
-python -m pytest tests/test_gpu_parity.py tests/test_gpu_fit.py tests/test_gpu_rle.py tests/test_gpu_cpp.py -q -m gpu -x > gpurun_out/t.log 2>&1; tail -3 gpurun_out/t.log
+python -m pytest tests -q -m gpu -x > gpurun_out/t.log 2>&1; tail -3 gpurun_out/t.log
 for c in c4 c1 c5; do
 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/b_$c.json 2> gpurun_out/err_$c.log
 python -c "

@@ -1,5 +1,5 @@
 # parity suites + C4 bench + C4 launch list
-python -m pytest tests/test_gpu_parity.py tests/test_gpu_fit.py tests/test_gpu_rle.py tests/test_gpu_cpp.py -q -m gpu -x > gpurun_out/t.log 2>&1; tail -1 gpurun_out/t.log
+python -m pytest tests -q -m gpu -x > gpurun_out/t.log 2>&1; tail -1 gpurun_out/t.log
 python bench.py --config ${1:-c4} --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/b_q.json 2> gpurun_out/err_q.log
 python -c "
 import json; d=json.load(open('gpurun_out/b_q.json')); print(d['ms_per_step'], d['value'], d['e2e']['value'], {k:round(v,3) for k,v in d.get('stages_ms_per_step').items()})"
