@@ -88,9 +88,45 @@ __device__ __forceinline__ void pairs_body(const uint32_t* __restrict__ P, uint6
   }
 }
 
+// k <= 32: a warp holds floor(32/k) positives, one lane per probe (h_a, h_b
+// recomputed per lane); duplicates among a positive's probes are found with
+// match_any inside its lane group — a probe is dropped if a lower lane of the
+// group has the same bit.
+__device__ __forceinline__ void pairs_lanes(const uint32_t* __restrict__ P, uint64_t n, uint32_t k, const FastMod& fm,
+                                            uint64_t sa, uint64_t sb, uint32_t* __restrict__ pairs,
+                                            uint32_t* __restrict__ count) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t per = 32 / k;                 // positives per warp
+  const uint32_t g = lane / k, j = lane - g * k;
+  const bool active = g < per;
+  const unsigned gmask = active ? (((k == 32) ? 0xFFFFFFFFu : ((1u << k) - 1u)) << (g * k)) : 0u;
+  const bool small = fm.m <= (1ull << 31);
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32);
+  for (uint64_t w = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) / 32; w * per < n; w += warps) {
+    const uint64_t p = w * per + g;
+    const bool ok = active && p < n;
+    uint32_t bit = 0xFFFFFFFFu;
+    if (ok) {
+      const uint64_t x = P[p];
+      const uint64_t h = mix64(x ^ sa) + static_cast<uint64_t>(j) * mix64(x ^ sb);
+      bit = small ? fast_mod_small(mix64(h), fm.minv, static_cast<uint32_t>(fm.m))
+                  : static_cast<uint32_t>(fast_mod(mix64(h), fm));
+    }
+    const unsigned peers = __match_any_sync(kFull, bit) & gmask;
+    const bool dup = (peers & ((1u << lane) - 1u)) != 0u;
+    if (ok) {
+      pairs[p * k + j] = dup ? 0xFFFFFFFFu : bit;
+      if (!dup) atomicAdd(&count[bit], 1u);
+    }
+  }
+}
+
+// kWide: the k > 32 form (one thread per positive); launched next to the lane
+// form, each exits unless k is in its range (k is only known on the device).
+template <bool kWide>
 __global__ void p2_pairs(const uint32_t* __restrict__ P, Plan* plan, uint32_t* __restrict__ pairs,
                          uint32_t* __restrict__ count, uint64_t pair_cap, uint64_t set_cap, uint32_t* status) {
-  if (failed(status) || !p2_active(plan)) return;
+  if (failed(status) || !p2_active(plan) || (plan->k > 32) != kWide) return;
   const uint64_t n = plan->n_pos, m = plan->m;
   const uint32_t k = plan->k;
   if (n * k > pair_cap || n * k >= kSingleton || m > set_cap || k > 64) {
@@ -99,15 +135,10 @@ __global__ void p2_pairs(const uint32_t* __restrict__ P, Plan* plan, uint32_t* _
   }
   const FastMod fm{m, plan->minv};
   const uint64_t sa = plan->seed_a + kGamma, sb = plan->seed_b + kGamma;
-  const bool small = m <= (1ull << 31);
-  if (k <= 16) {
-    if (small)
-      pairs_body<16, true>(P, n, k, fm, sa, sb, pairs, count);
-    else
-      pairs_body<16, false>(P, n, k, fm, sa, sb, pairs, count);
-  } else {
+  if (kWide)
     pairs_body<64, false>(P, n, k, fm, sa, sb, pairs, count);
-  }
+  else
+    pairs_lanes(P, n, k, fm, sa, sb, pairs, count);
   if (blockIdx.x == 0 && threadIdx.x == 0) plan->n_pairs = n * k;
 }
 
@@ -177,15 +208,16 @@ __global__ void p2_scatter(const uint32_t* __restrict__ pairs, const Plan* plan,
   const uint32_t k = plan->k;
   const uint64_t np = n * k;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  // 4 pairs per thread per step, strided by the grid: 4 independent chains in flight
-  for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i0 < np; i0 += 4 * stride) {
-    uint32_t bit[4], v[4];
+  // kU pairs per thread per step, strided by the grid: kU independent chains in flight
+  constexpr int kU = 8;
+  for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i0 < np; i0 += kU * stride) {
+    uint32_t bit[kU], v[kU];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) bit[u] = i0 + u * stride < np ? pairs[i0 + u * stride] : 0xFFFFFFFFu;
+    for (int u = 0; u < kU; ++u) bit[u] = i0 + u * stride < np ? pairs[i0 + u * stride] : 0xFFFFFFFFu;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = bit[u] != 0xFFFFFFFFu ? atomicSub(&slot[bit[u]], 1u) : 0u;
+    for (int u = 0; u < kU; ++u) v[u] = bit[u] != 0xFFFFFFFFu ? atomicSub(&slot[bit[u]], 1u) : 0u;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kU; ++u) {
       if (bit[u] == 0xFFFFFFFFu) continue;
       const uint64_t i = i0 + u * stride;
       const uint32_t p = static_cast<uint32_t>(np < (1ull << 32) ? static_cast<uint32_t>(i) / k : i / k);
@@ -351,17 +383,31 @@ __device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __res
     return res;
   };
 
+  constexpr uint32_t kM = 8;  // members of a visit held in registers (larger sets re-read memory)
   while (nsel < r && L > 0) {
     const uint64_t si = start + (cursor + v) % L;
     const uint32_t bit = sets[si];
     const uint32_t sz = size[bit];
     const uint32_t* mems = members + (off[bit] & ~kSingleton);  // slot = bucket start after the scatter
-    const uint32_t lo = 0;
-    for (uint32_t j = 0; j < sz; ++j) first_touch[mems[lo + j]] = 0xFFFFFFFFu;
+    uint32_t mr[kM];
+#pragma unroll
+    for (uint32_t j = 0; j < kM; ++j) mr[j] = j < sz ? mems[j] : 0u;
+#pragma unroll
+    for (uint32_t j = 0; j < kM; ++j)
+      if (j < sz) first_touch[mr[j]] = 0xFFFFFFFFu;
+    for (uint32_t j = kM; j < sz; ++j) first_touch[mems[j]] = 0xFFFFFFFFu;
     __syncthreads();
-    uint32_t cnt = 0;
-    for (uint32_t j = 0; j < sz; ++j) {
-      const uint32_t p = mems[lo + j];
+    uint32_t cnt = 0, unsel = 0;  // unsel: bitmask of unselected register members
+#pragma unroll
+    for (uint32_t j = 0; j < kM; ++j) {
+      if (j < sz && !bs_test(bits, mr[j])) {
+        ++cnt;
+        unsel |= 1u << j;
+        atomicMin(&first_touch[mr[j]], v);
+      }
+    }
+    for (uint32_t j = kM; j < sz; ++j) {
+      const uint32_t p = mems[j];
       if (!bs_test(bits, p)) {
         ++cnt;
         atomicMin(&first_touch[p], v);
@@ -369,11 +415,17 @@ __device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __res
     }
     __syncthreads();
     bool dep = false;
-    if (cnt)
-      for (uint32_t j = 0; j < sz && !dep; ++j) {
-        const uint32_t p = mems[lo + j];
+    if (cnt) {
+      uint32_t ft[kM];
+#pragma unroll
+      for (uint32_t j = 0; j < kM; ++j) ft[j] = (unsel >> j & 1u) ? first_touch[mr[j]] : 0xFFFFFFFFu;
+#pragma unroll
+      for (uint32_t j = 0; j < kM; ++j) dep |= ft[j] < v;
+      for (uint32_t j = kM; j < sz && !dep; ++j) {
+        const uint32_t p = mems[j];
         if (!bs_test(bits, p) && first_touch[p] < v) dep = true;
       }
+    }
     const uint32_t vstar = block_min(dep ? v : W);
     // RNG positions of the independent prefix
     const bool draw = v < vstar && cnt >= 2;
@@ -409,17 +461,27 @@ __device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __res
     const uint32_t climit = min(limit, cut);
     // commit
     if (sel && v < climit) {  // the target-th smallest unselected member (buckets are unsorted)
-      for (uint32_t j = 0; j < sz; ++j) {
-        const uint32_t p = mems[lo + j];
-        if (bs_test(bits, p)) continue;
-        uint32_t rank = 0;
-        for (uint32_t q = 0; q < sz; ++q) {
-          const uint32_t o = mems[lo + q];
-          rank += (o < p && !bs_test(bits, o)) ? 1u : 0u;
+      if (sz <= kM) {  // register members, unselected mask from the count above (no selection since)
+#pragma unroll
+        for (uint32_t j = 0; j < kM; ++j) {
+          uint32_t rank = 0;
+#pragma unroll
+          for (uint32_t q = 0; q < kM; ++q) rank += ((unsel >> q & 1u) && mr[q] < mr[j]) ? 1u : 0u;
+          if ((unsel >> j & 1u) && rank == target) atomicOr(&bits[mr[j] >> 5], 1u << (mr[j] & 31));
         }
-        if (rank == target) {
-          atomicOr(&bits[p >> 5], 1u << (p & 31));
-          break;
+      } else {
+        for (uint32_t j = 0; j < sz; ++j) {
+          const uint32_t p = mems[j];
+          if (bs_test(bits, p)) continue;
+          uint32_t rank = 0;
+          for (uint32_t q = 0; q < sz; ++q) {
+            const uint32_t o = mems[q];
+            rank += (o < p && !bs_test(bits, o)) ? 1u : 0u;
+          }
+          if (rank == target) {
+            atomicOr(&bits[p >> 5], 1u << (p & 31));
+            break;
+          }
         }
       }
     }
@@ -510,7 +572,9 @@ void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t 
   const uint64_t m_cap = std::min<uint64_t>(m_bound, w.set_cap);
   GP_LAUNCH(ctx, p2_zero_counts, ctx->sm_count * 4, 256, 0, s, w.plan, w.p2_count, m_cap, w.status);
   cudaMemsetAsync(w.p2_alloc, 0, sizeof(uint32_t), s);
-  GP_LAUNCH(ctx, p2_pairs, grid_for(ctx, n_bound, 128), 128, 0, s, w.pos, w.plan, w.pairs, w.p2_count, w.pair_cap,
+  GP_LAUNCH(ctx, p2_pairs<false>, grid_for(ctx, n_bound * 32, 256), 256, 0, s, w.pos, w.plan, w.pairs, w.p2_count, w.pair_cap,
+            w.set_cap, w.status);
+  GP_LAUNCH(ctx, p2_pairs<true>, grid_for(ctx, n_bound, 128), 128, 0, s, w.pos, w.plan, w.pairs, w.p2_count, w.pair_cap,
             w.set_cap, w.status);
   const uint64_t mtiles = (m_cap + kTile - 1) / kTile;
   const int tgrid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(mtiles, ctx->sm_count * 8ULL)));
