@@ -102,15 +102,19 @@ __global__ void __launch_bounds__(1024) topr_pick_bin(const uint32_t* __restrict
   }
 }
 
-// One contiguous chunk of the gradient per block (claimed in order): stream it
-// once with float4 loads, buffering in shared memory, in index order, the
-// candidates (bin >= b*) and the keys of bin b* alone; one look-back per block
-// (candidates on warp 0, ties on warp 1) places them.  A chunk whose
-// candidates overflow the buffer (e.g. natural sparsity, r ~ 0.6 d) streams
-// its slice a second time and writes directly.
+// One contiguous chunk of the gradient per block (claimed in order), split
+// into one contiguous segment per warp.  Each warp streams its segment with
+// float4 loads (16 keys per lane in flight) and buffers, in index order, its
+// candidates (bin >= b*) and the keys of bin b* alone in its own shared-memory
+// buffers — warp scans only, no block barriers in the stream.  Then one block
+// combine: per-warp offsets, one look-back per block (candidates on warp 0,
+// ties on warp 1), and every warp copies its buffers out.  A warp whose buffer
+// overflowed (e.g. natural sparsity, r ~ 0.6 d) streams its segment again and
+// writes directly.
 constexpr int kCandBlock = 256;
-constexpr int kCandCap = 3072;
-constexpr int kTieCap = 1536;
+constexpr int kCandWarps = kCandBlock / 32;
+constexpr int kWarpCandCap = 384;
+constexpr int kWarpTieCap = 192;
 
 __device__ __forceinline__ void load4(const float* __restrict__ g, uint64_t i, uint64_t hi, bool aligned, float v[4]) {
   if (aligned && i + 3 < hi) {
@@ -125,116 +129,162 @@ __device__ __forceinline__ void load4(const float* __restrict__ g, uint64_t i, u
   }
 }
 
+// one 512-key step of a warp over [i0, hi): candidate / tie masks of this lane's 16 keys
+__device__ __forceinline__ void masks_of(const float v[16], uint64_t i, uint64_t hi, uint32_t klo, uint32_t bstar,
+                                         bool ties, uint32_t& mc, uint32_t& mt) {
+  mc = 0;
+  mt = 0;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const uint32_t key = key_of(v[q]);
+    const bool in = i + q < hi;
+    if (in && key >= klo) mc |= 1u << q;
+    if (in && ties && (key >> kShift) == bstar) mt |= 1u << q;
+  }
+}
+
+__device__ __forceinline__ void cand_masks(const float* __restrict__ g, uint64_t i, uint64_t hi, bool aligned,
+                                           uint32_t klo, uint32_t bstar, bool ties, float v[16], uint32_t& mc,
+                                           uint32_t& mt) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) load4(g, i + 4 * u, hi, aligned, v + 4 * u);
+  mc = 0;
+  mt = 0;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const uint32_t key = key_of(v[q]);
+    const bool in = i + q < hi;
+    if (in && key >= klo) mc |= 1u << q;
+    if (in && ties && (key >> kShift) == bstar) mt |= 1u << q;
+  }
+}
+
 __global__ void __launch_bounds__(kCandBlock) topr_candidates(
     const float* __restrict__ g, uint64_t d, uint64_t chunk, const Plan* __restrict__ plan, uint32_t* cidx,
     float* cval, uint32_t* sidx, float* sval, uint32_t* tidx, float* tval, uint64_t* tiles_c, uint64_t* tiles_t,
     uint32_t* ticket, const uint32_t* status) {
-  __shared__ uint32_t bidx[kCandCap];
-  __shared__ float bval[kCandCap];
-  __shared__ uint32_t tbidx[kTieCap];
-  __shared__ float tbval[kTieCap];
-  __shared__ uint64_t sh_c[36];
-  __shared__ uint64_t sh_t[36];
+  __shared__ uint32_t bidx[kCandWarps][kWarpCandCap];
+  __shared__ float bval[kCandWarps][kWarpCandCap];
+  __shared__ uint32_t tbidx[kCandWarps][kWarpTieCap];
+  __shared__ float tbval[kCandWarps][kWarpTieCap];
+  __shared__ uint32_t wc[kCandWarps], wt[kCandWarps];
+  __shared__ uint64_t s_pc, s_pt;
   __shared__ uint32_t slot;
   if (failed(status)) return;
   const uint32_t bstar = plan->bin_star;
+  const uint32_t klo = bstar << kShift;
   const bool full = plan->full_bin != 0;
   uint32_t* oidx = full ? sidx : cidx;
   float* oval = full ? sval : cval;
   const bool aligned = (reinterpret_cast<uintptr_t>(g) & 15) == 0;
   const uint64_t nchunks = (d + chunk - 1) / chunk;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t wseg = chunk / kCandWarps;  // chunk is a multiple of 8 * 512
   while (true) {
     const uint32_t c = claim_tile(ticket, &slot);
     if (c >= nchunks) break;
-    const uint64_t lo = static_cast<uint64_t>(c) * chunk, hi = lo + chunk < d ? lo + chunk : d;
-    uint64_t nc = 0, nt = 0;  // block-uniform running counts
-    for (uint64_t base = lo; base < hi; base += 16 * kCandBlock) {
-      const uint64_t i = base + 16 * threadIdx.x;  // 16 consecutive keys per thread, 4 loads in flight
+    const uint64_t clo = static_cast<uint64_t>(c) * chunk, chi = clo + chunk < d ? clo + chunk : d;
+    const uint64_t lo = clo + warp * wseg < chi ? clo + warp * wseg : chi;
+    const uint64_t hi = lo + wseg < chi ? lo + wseg : chi;
+    uint32_t nc = 0, nt = 0;  // warp-uniform running counts
+    float nxt[16];            // software pipeline: the next step's keys load while this step is processed
+#pragma unroll
+    for (int u = 0; u < 4; ++u) load4(g, lo + 16 * lane + 4 * u, hi, aligned, nxt + 4 * u);
+    for (uint64_t base = lo; base < hi; base += 512) {
+      const uint64_t i = base + 16 * lane;
       float v[16];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) load4(g, i + 4 * u, hi, aligned, v + 4 * u);
-      uint32_t mc = 0, mt = 0;
+      for (int q = 0; q < 16; ++q) v[q] = nxt[q];
+      if (base + 512 < hi) {
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const uint32_t bin = key_of(v[q]) >> kShift;
-        if (i + q < hi && bin >= bstar) mc |= 1u << q;
-        if (i + q < hi && bin == bstar && !full) mt |= 1u << q;
+        for (int u = 0; u < 4; ++u) load4(g, i + 512 + 4 * u, hi, aligned, nxt + 4 * u);
       }
-      uint64_t tc, tt;
-      uint64_t oc = nc + block_exclusive_sum<uint64_t, kCandBlock>(__popc(mc), sh_c, tc);
-      uint64_t ot = nt + block_exclusive_sum<uint64_t, kCandBlock>(__popc(mt), sh_t, tt);
+      uint32_t mc, mt;
+      masks_of(v, i, hi, klo, bstar, !full, mc, mt);
+      const uint32_t packed = __popc(mc) | (__popc(mt) << 16);
+      const uint32_t inc = warp_inclusive_sum(packed);
+      uint32_t oc = nc + ((inc - packed) & 0xFFFFu), ot = nt + ((inc - packed) >> 16);
       while (mc) {
         const int q = __ffs(mc) - 1;
-        if (oc < kCandCap) {
-          bidx[oc] = static_cast<uint32_t>(i + q);
-          bval[oc] = v[q];
+        if (oc < kWarpCandCap) {
+          bidx[warp][oc] = static_cast<uint32_t>(i + q);
+          bval[warp][oc] = __ldg(g + i + q);  // re-read (cache hit): no dynamic register indexing
         }
         ++oc;
         mc &= mc - 1;
       }
       while (mt) {
         const int q = __ffs(mt) - 1;
-        if (ot < kTieCap) {
-          tbidx[ot] = static_cast<uint32_t>(i + q);
-          tbval[ot] = v[q];
+        if (ot < kWarpTieCap) {
+          tbidx[warp][ot] = static_cast<uint32_t>(i + q);
+          tbval[warp][ot] = __ldg(g + i + q);
         }
         ++ot;
         mt &= mt - 1;
       }
-      nc += tc;
-      nt += tt;
+      const uint32_t tot = __shfl_sync(kFull, inc, 31);
+      nc += tot & 0xFFFFu;
+      nt += tot >> 16;
     }
-    if (threadIdx.x < 32) {
-      const uint64_t p = lookback_warp(tiles_c, c, nc);
-      if (threadIdx.x == 0) sh_c[34] = p;
-    } else if (threadIdx.x < 64 && !full) {
-      const uint64_t p = lookback_warp(tiles_t, c, nt);
-      if (threadIdx.x == 32) sh_t[34] = p;
+    if (lane == 0) {
+      wc[warp] = nc;
+      wt[warp] = nt;
     }
     __syncthreads();
-    const uint64_t pc = sh_c[34], pt = full ? 0 : sh_t[34];
-    if (nc <= kCandCap && nt <= kTieCap) {
-      for (uint64_t k = threadIdx.x; k < nc; k += kCandBlock) {
-        oidx[pc + k] = bidx[k];
-        oval[pc + k] = bval[k];
+    uint32_t bc = 0, bt = 0, pc_w = 0, pt_w = 0;  // block totals, this warp's offsets in the block
+#pragma unroll
+    for (int w = 0; w < kCandWarps; ++w) {
+      if (w == warp) {
+        pc_w = bc;
+        pt_w = bt;
       }
-      for (uint64_t k = threadIdx.x; k < nt; k += kCandBlock) {
-        tidx[pt + k] = tbidx[k];
-        tval[pt + k] = tbval[k];
+      bc += wc[w];
+      bt += wt[w];
+    }
+    if (warp == 0) {
+      const uint64_t p = lookback_warp(tiles_c, c, bc);
+      if (lane == 0) s_pc = p;
+    } else if (warp == 1 && !full) {
+      const uint64_t p = lookback_warp(tiles_t, c, bt);
+      if (lane == 0) s_pt = p;
+    }
+    __syncthreads();
+    const uint64_t pc = s_pc + pc_w, pt = (full ? 0 : s_pt) + pt_w;
+    if (nc <= kWarpCandCap && nt <= kWarpTieCap) {
+      for (uint32_t k = lane; k < nc; k += 32) {
+        oidx[pc + k] = bidx[warp][k];
+        oval[pc + k] = bval[warp][k];
       }
-    } else {  // overflow: second pass over this chunk, writing directly
+      for (uint32_t k = lane; k < nt; k += 32) {
+        tidx[pt + k] = tbidx[warp][k];
+        tval[pt + k] = tbval[warp][k];
+      }
+    } else {  // overflow: this warp streams its segment again, writing directly
       uint64_t rc = pc, rt = pt;
-      for (uint64_t base = lo; base < hi; base += 16 * kCandBlock) {
-        const uint64_t i = base + 16 * threadIdx.x;
+      for (uint64_t base = lo; base < hi; base += 512) {
+        const uint64_t i = base + 16 * lane;
         float v[16];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) load4(g, i + 4 * u, hi, aligned, v + 4 * u);
-        uint32_t mc = 0, mt = 0;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const uint32_t bin = key_of(v[q]) >> kShift;
-          if (i + q < hi && bin >= bstar) mc |= 1u << q;
-          if (i + q < hi && bin == bstar && !full) mt |= 1u << q;
-        }
-        uint64_t tc, tt;
-        uint64_t oc = rc + block_exclusive_sum<uint64_t, kCandBlock>(__popc(mc), sh_c, tc);
-        uint64_t ot = rt + block_exclusive_sum<uint64_t, kCandBlock>(__popc(mt), sh_t, tt);
+        uint32_t mc, mt;
+        cand_masks(g, i, hi, aligned, klo, bstar, !full, v, mc, mt);
+        const uint32_t cc = __popc(mc), ct = __popc(mt);
+        const uint32_t incc = warp_inclusive_sum(cc), inct = warp_inclusive_sum(ct);
+        uint64_t oc = rc + incc - cc, ot = rt + inct - ct;
         while (mc) {
           const int q = __ffs(mc) - 1;
           oidx[oc] = static_cast<uint32_t>(i + q);
-          oval[oc] = v[q];
+          oval[oc] = __ldg(g + i + q);
           ++oc;
           mc &= mc - 1;
         }
         while (mt) {
           const int q = __ffs(mt) - 1;
           tidx[ot] = static_cast<uint32_t>(i + q);
-          tval[ot] = v[q];
+          tval[ot] = __ldg(g + i + q);
           ++ot;
           mt &= mt - 1;
         }
-        rc += tc;
-        rt += tt;
+        rc += __shfl_sync(kFull, incc, 31);
+        rt += __shfl_sync(kFull, inct, 31);
       }
     }
   }
@@ -318,42 +368,74 @@ __global__ void __launch_bounds__(1024) topr_refine(const uint32_t* __restrict__
   }
 }
 
-// Ordered filter of the candidate list into the final support.
-__global__ void __launch_bounds__(kTileBlock) topr_final(const uint32_t* __restrict__ cidx,
+// Ordered filter of the candidate list into the final support: one chunk of
+// the list per claimed ticket, one segment per warp; a counting pass, one
+// look-back per block, then a writing pass over the (L2-resident) segment.
+__device__ __forceinline__ uint32_t keep_mask(const uint32_t* __restrict__ cidx, const float* __restrict__ cval,
+                                              uint64_t i, uint64_t hi, uint32_t T, uint32_t cut) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    if (i + q < hi) {
+      const uint32_t key = key_of(cval[i + q]);
+      if (key > T || (key == T && cidx[i + q] <= cut)) m |= 1u << q;
+    }
+  }
+  return m;
+}
+
+__global__ void __launch_bounds__(kCandBlock) topr_final(const uint32_t* __restrict__ cidx,
                                                          const float* __restrict__ cval, const Plan* plan,
                                                          uint32_t* sidx, float* sval, uint64_t* tiles,
                                                          uint32_t* ticket, const uint32_t* status) {
-  __shared__ uint64_t sh[36];
+  __shared__ uint32_t wk[kCandWarps];
+  __shared__ uint64_t s_p;
   __shared__ uint32_t slot;
   if (failed(status) || plan->full_bin) return;
   const uint64_t n = plan->n_cand;
   const uint32_t T = plan->thresh, cut = plan->tie_cut;
-  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  const uint64_t chunk = ((n + gridDim.x - 1) / gridDim.x + 4095) / 4096 * 4096;
+  const uint64_t nchunks = (n + chunk - 1) / chunk;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t wseg = chunk / kCandWarps;
   while (true) {
-    const uint32_t tile = claim_tile(ticket, &slot);
-    if (tile >= ntiles) break;
-    const uint64_t base = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(threadIdx.x) * kTileItems;
-    uint32_t m = 0;
-    uint64_t c = 0;
+    const uint32_t c = claim_tile(ticket, &slot);
+    if (c >= nchunks) break;
+    const uint64_t clo = static_cast<uint64_t>(c) * chunk, chi = clo + chunk < n ? clo + chunk : n;
+    const uint64_t lo = clo + warp * wseg < chi ? clo + warp * wseg : chi;
+    const uint64_t hi = lo + wseg < chi ? lo + wseg : chi;
+    uint32_t nk = 0;
+    for (uint64_t base = lo; base < hi; base += 512)
+      nk += __reduce_add_sync(kFull, __popc(keep_mask(cidx, cval, base + 16 * lane, hi, T, cut)));
+    if (lane == 0) wk[warp] = nk;
+    __syncthreads();
+    uint32_t bk = 0, pw = 0;
 #pragma unroll
-    for (int q = 0; q < kTileItems; ++q) {
-      if (base + q < n) {
-        const uint32_t key = key_of(cval[base + q]);
-        if (key > T || (key == T && cidx[base + q] <= cut)) {
-          m |= 1u << q;
-          ++c;
-        }
-      }
+    for (int w = 0; w < kCandWarps; ++w) {
+      if (w == warp) pw = bk;
+      bk += wk[w];
     }
-    uint64_t tot;
-    uint64_t o = tile_exclusive_offset<kTileBlock>(c, tile, tiles, sh, tot);
-#pragma unroll
-    for (int q = 0; q < kTileItems; ++q)
-      if (m >> q & 1u) {
-        sidx[o] = cidx[base + q];
-        sval[o] = cval[base + q];
-        ++o;
+    if (warp == 0) {
+      const uint64_t p = lookback_warp(tiles, c, bk);
+      if (lane == 0) s_p = p;
+    }
+    __syncthreads();
+    uint64_t o = s_p + pw;
+    for (uint64_t base = lo; base < hi; base += 512) {
+      const uint64_t i = base + 16 * lane;
+      uint32_t m = keep_mask(cidx, cval, i, hi, T, cut);
+      const uint32_t cnt = __popc(m);
+      const uint32_t inc = warp_inclusive_sum(cnt);
+      uint64_t oo = o + inc - cnt;
+      while (m) {
+        const int q = __ffs(m) - 1;
+        sidx[oo] = cidx[i + q];
+        sval[oo] = cval[i + q];
+        ++oo;
+        m &= m - 1;
       }
+      o += __shfl_sync(kFull, inc, 31);
+    }
   }
 }
 
@@ -376,7 +458,7 @@ void launch_top_r(gp_ctx* ctx, const float* grad, uint64_t d, uint64_t r, cudaSt
   GP_LAUNCH(ctx, topr_hist, hist_grid, kHistBlock, kBins * 4, s, grad, d, w.hist, w.status);
   GP_LAUNCH(ctx, topr_pick_bin, 1, 1024, 0, s, w.hist, r, w.plan, w.status);
   const uint64_t nblk = static_cast<uint64_t>(ctx->sm_count) * 4;
-  const uint64_t chunk = std::max<uint64_t>(4096, ((d + nblk - 1) / nblk + 4095) / 4096 * 4096);  // multiple of 16*256
+  const uint64_t chunk = std::max<uint64_t>(4096, ((d + nblk - 1) / nblk + 4095) / 4096 * 4096);  // multiple of 8 warps * 512
   const int grid = static_cast<int>(std::max<uint64_t>(1, (d + chunk - 1) / chunk));
   GP_LAUNCH(ctx, topr_candidates, grid, kCandBlock, 0, s, grad, d, chunk, w.plan, w.cand_idx, w.cand_val, w.support,
             w.values, w.u32a, reinterpret_cast<float*>(w.u32b), tiles_c, tiles_t, w.ticket, w.status);
@@ -384,8 +466,7 @@ void launch_top_r(gp_ctx* ctx, const float* grad, uint64_t d, uint64_t r, cudaSt
             w.plan, w.status);
   // final filter: its own scan state (tiles after both previous arrays)
   uint64_t* tiles_f = w.tiles + 2 * (ntiles + 1);
-  const int fgrid = static_cast<int>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(ctx->sm_count) * 4));
-  GP_LAUNCH(ctx, topr_final, std::max(fgrid, 1), kTileBlock, 0, s, w.cand_idx, w.cand_val, w.plan, w.support,
+  GP_LAUNCH(ctx, topr_final, ctx->sm_count * 2, kCandBlock, 0, s, w.cand_idx, w.cand_val, w.plan, w.support,
             w.values, tiles_f, w.ticket + 2, w.status);
 }
 
