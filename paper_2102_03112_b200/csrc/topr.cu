@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(1024) topr_pick_bin(const uint32_t* __restrict
 // into one contiguous segment per warp.  Each warp streams its segment with
 // float4 loads (16 keys per lane in flight) and buffers, in index order, its
 // candidates (bin >= b*) and the keys of bin b* alone in its own shared-memory
-// buffers — warp scans only, no block barriers in the stream.  Then one block
+// buffers — ballot ranks only, no block barriers in the stream.  Then one block
 // combine: per-warp offsets, one look-back per block (candidates on warp 0,
 // ties on warp 1), and every warp copies its buffers out.  A warp whose buffer
 // overflowed (e.g. natural sparsity, r ~ 0.6 d) streams its segment again and
@@ -116,46 +116,77 @@ constexpr int kCandWarps = kCandBlock / 32;
 constexpr int kWarpCandCap = 384;
 constexpr int kWarpTieCap = 192;
 
-__device__ __forceinline__ void load4(const float* __restrict__ g, uint64_t i, uint64_t hi, bool aligned, float v[4]) {
-  if (aligned && i + 3 < hi) {
-    const float4 x = __ldg(reinterpret_cast<const float4*>(g + i));
-    v[0] = x.x;
-    v[1] = x.y;
-    v[2] = x.z;
-    v[3] = x.w;
-  } else {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) v[q] = i + q < hi ? g[i + q] : 0.0f;
-  }
+// One 128-key row of a warp: lane l holds keys 4l..4l+3 (one float4).  Ballots
+// per component give, for every kept key, its rank in index order within the
+// row: keys of lower lanes, then this lane's lower components.
+struct RowRank {
+  uint32_t own;    // this lane's 4-bit mask
+  uint32_t before; // kept keys of the row before this lane's first key
+  uint32_t total;  // kept keys in the row
+};
+__device__ __forceinline__ RowRank row_rank(bool k0, bool k1, bool k2, bool k3, unsigned lt) {
+  const unsigned b0 = __ballot_sync(kFull, k0), b1 = __ballot_sync(kFull, k1);
+  const unsigned b2 = __ballot_sync(kFull, k2), b3 = __ballot_sync(kFull, k3);
+  RowRank r;
+  r.own = (k0 ? 1u : 0u) | (k1 ? 2u : 0u) | (k2 ? 4u : 0u) | (k3 ? 8u : 0u);
+  r.before = __popc(b0 & lt) + __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
+  r.total = __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
+  return r;
 }
 
-// one 512-key step of a warp over [i0, hi): candidate / tie masks of this lane's 16 keys
-__device__ __forceinline__ void masks_of(const float v[16], uint64_t i, uint64_t hi, uint32_t klo, uint32_t bstar,
-                                         bool ties, uint32_t& mc, uint32_t& mt) {
-  mc = 0;
-  mt = 0;
-#pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const uint32_t key = key_of(v[q]);
-    const bool in = i + q < hi;
-    if (in && key >= klo) mc |= 1u << q;
-    if (in && ties && (key >> kShift) == bstar) mt |= 1u << q;
-  }
+__device__ __forceinline__ float4 load_row(const float* __restrict__ g, uint64_t i, uint64_t hi, bool aligned) {
+  if (aligned && i + 3 < hi) return __ldg(reinterpret_cast<const float4*>(g + i));
+  float4 x;
+  x.x = i < hi ? g[i] : 0.0f;
+  x.y = i + 1 < hi ? g[i + 1] : 0.0f;
+  x.z = i + 2 < hi ? g[i + 2] : 0.0f;
+  x.w = i + 3 < hi ? g[i + 3] : 0.0f;
+  return x;
 }
 
-__device__ __forceinline__ void cand_masks(const float* __restrict__ g, uint64_t i, uint64_t hi, bool aligned,
-                                           uint32_t klo, uint32_t bstar, bool ties, float v[16], uint32_t& mc,
-                                           uint32_t& mt) {
+// Streams [lo, hi) of one warp in 128-key rows (4 rows in flight), calling
+// emit_c(rank, index, value) for candidates and emit_t(...) for tie-bin keys
+// with their warp-local ranks; returns the warp's (candidate, tie) counts.
+template <typename EC, typename ET>
+__device__ __forceinline__ void stream_segment(const float* __restrict__ g, uint64_t lo, uint64_t hi, bool aligned,
+                                               uint32_t klo, uint32_t khi, bool ties, uint32_t& nc, uint32_t& nt,
+                                               EC emit_c, ET emit_t) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  nc = 0;
+  nt = 0;
+  for (uint64_t base = lo; base < hi; base += 512) {
+    float4 x[4];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) load4(g, i + 4 * u, hi, aligned, v + 4 * u);
-  mc = 0;
-  mt = 0;
+    for (int u = 0; u < 4; ++u) x[u] = load_row(g, base + 128 * u + 4 * lane, hi, aligned);
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const uint32_t key = key_of(v[q]);
-    const bool in = i + q < hi;
-    if (in && key >= klo) mc |= 1u << q;
-    if (in && ties && (key >> kShift) == bstar) mt |= 1u << q;
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t i = base + 128 * u + 4 * lane;
+      const float v[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+      bool kc[4], kt[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t key = key_of(v[q]);
+        kc[q] = key >= klo && i + q < hi;
+        kt[q] = ties && kc[q] && key < khi;
+      }
+      const RowRank rc = row_rank(kc[0], kc[1], kc[2], kc[3], lt);
+      if (rc.total) {
+        uint32_t o = nc + rc.before;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (rc.own >> q & 1u) emit_c(o++, static_cast<uint32_t>(i + q), v[q]);
+        nc += rc.total;
+        if (ties) {
+          const RowRank rt = row_rank(kt[0], kt[1], kt[2], kt[3], lt);
+          uint32_t ot = nt + rt.before;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (rt.own >> q & 1u) emit_t(ot++, static_cast<uint32_t>(i + q), v[q]);
+          nt += rt.total;
+        }
+      }
+    }
   }
 }
 
@@ -172,7 +203,7 @@ __global__ void __launch_bounds__(kCandBlock) topr_candidates(
   __shared__ uint32_t slot;
   if (failed(status)) return;
   const uint32_t bstar = plan->bin_star;
-  const uint32_t klo = bstar << kShift;
+  const uint32_t klo = bstar << kShift, khi = (bstar + 1) << kShift;
   const bool full = plan->full_bin != 0;
   uint32_t* oidx = full ? sidx : cidx;
   float* oval = full ? sval : cval;
@@ -186,46 +217,21 @@ __global__ void __launch_bounds__(kCandBlock) topr_candidates(
     const uint64_t clo = static_cast<uint64_t>(c) * chunk, chi = clo + chunk < d ? clo + chunk : d;
     const uint64_t lo = clo + warp * wseg < chi ? clo + warp * wseg : chi;
     const uint64_t hi = lo + wseg < chi ? lo + wseg : chi;
-    uint32_t nc = 0, nt = 0;  // warp-uniform running counts
-    float nxt[16];            // software pipeline: the next step's keys load while this step is processed
-#pragma unroll
-    for (int u = 0; u < 4; ++u) load4(g, lo + 16 * lane + 4 * u, hi, aligned, nxt + 4 * u);
-    for (uint64_t base = lo; base < hi; base += 512) {
-      const uint64_t i = base + 16 * lane;
-      float v[16];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) v[q] = nxt[q];
-      if (base + 512 < hi) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) load4(g, i + 512 + 4 * u, hi, aligned, nxt + 4 * u);
-      }
-      uint32_t mc, mt;
-      masks_of(v, i, hi, klo, bstar, !full, mc, mt);
-      const uint32_t packed = __popc(mc) | (__popc(mt) << 16);
-      const uint32_t inc = warp_inclusive_sum(packed);
-      uint32_t oc = nc + ((inc - packed) & 0xFFFFu), ot = nt + ((inc - packed) >> 16);
-      while (mc) {
-        const int q = __ffs(mc) - 1;
-        if (oc < kWarpCandCap) {
-          bidx[warp][oc] = static_cast<uint32_t>(i + q);
-          bval[warp][oc] = __ldg(g + i + q);  // re-read (cache hit): no dynamic register indexing
-        }
-        ++oc;
-        mc &= mc - 1;
-      }
-      while (mt) {
-        const int q = __ffs(mt) - 1;
-        if (ot < kWarpTieCap) {
-          tbidx[warp][ot] = static_cast<uint32_t>(i + q);
-          tbval[warp][ot] = __ldg(g + i + q);
-        }
-        ++ot;
-        mt &= mt - 1;
-      }
-      const uint32_t tot = __shfl_sync(kFull, inc, 31);
-      nc += tot & 0xFFFFu;
-      nt += tot >> 16;
-    }
+    uint32_t nc, nt;
+    stream_segment(
+        g, lo, hi, aligned, klo, khi, !full, nc, nt,
+        [&](uint32_t o, uint32_t idx, float v) {
+          if (o < kWarpCandCap) {
+            bidx[warp][o] = idx;
+            bval[warp][o] = v;
+          }
+        },
+        [&](uint32_t o, uint32_t idx, float v) {
+          if (o < kWarpTieCap) {
+            tbidx[warp][o] = idx;
+            tbval[warp][o] = v;
+          }
+        });
     if (lane == 0) {
       wc[warp] = nc;
       wt[warp] = nt;
@@ -260,32 +266,17 @@ __global__ void __launch_bounds__(kCandBlock) topr_candidates(
         tval[pt + k] = tbval[warp][k];
       }
     } else {  // overflow: this warp streams its segment again, writing directly
-      uint64_t rc = pc, rt = pt;
-      for (uint64_t base = lo; base < hi; base += 512) {
-        const uint64_t i = base + 16 * lane;
-        float v[16];
-        uint32_t mc, mt;
-        cand_masks(g, i, hi, aligned, klo, bstar, !full, v, mc, mt);
-        const uint32_t cc = __popc(mc), ct = __popc(mt);
-        const uint32_t incc = warp_inclusive_sum(cc), inct = warp_inclusive_sum(ct);
-        uint64_t oc = rc + incc - cc, ot = rt + inct - ct;
-        while (mc) {
-          const int q = __ffs(mc) - 1;
-          oidx[oc] = static_cast<uint32_t>(i + q);
-          oval[oc] = __ldg(g + i + q);
-          ++oc;
-          mc &= mc - 1;
-        }
-        while (mt) {
-          const int q = __ffs(mt) - 1;
-          tidx[ot] = static_cast<uint32_t>(i + q);
-          tval[ot] = __ldg(g + i + q);
-          ++ot;
-          mt &= mt - 1;
-        }
-        rc += __shfl_sync(kFull, incc, 31);
-        rt += __shfl_sync(kFull, inct, 31);
-      }
+      uint32_t c2, t2;
+      stream_segment(
+          g, lo, hi, aligned, klo, khi, !full, c2, t2,
+          [&](uint32_t o, uint32_t idx, float v) {
+            oidx[pc + o] = idx;
+            oval[pc + o] = v;
+          },
+          [&](uint32_t o, uint32_t idx, float v) {
+            tidx[pt + o] = idx;
+            tval[pt + o] = v;
+          });
     }
   }
 }
@@ -369,19 +360,45 @@ __global__ void __launch_bounds__(1024) topr_refine(const uint32_t* __restrict__
 }
 
 // Ordered filter of the candidate list into the final support: one chunk of
-// the list per claimed ticket, one segment per warp; a counting pass, one
-// look-back per block, then a writing pass over the (L2-resident) segment.
-__device__ __forceinline__ uint32_t keep_mask(const uint32_t* __restrict__ cidx, const float* __restrict__ cval,
-                                              uint64_t i, uint64_t hi, uint32_t T, uint32_t cut) {
-  uint32_t m = 0;
+// the list per claimed ticket, one segment per warp, 128-entry rows ranked by
+// ballots; a counting pass, one look-back per block, then a writing pass over
+// the (L2-resident) segment.
+template <bool kWrite>
+__device__ __forceinline__ uint32_t final_segment(const uint32_t* __restrict__ cidx, const float* __restrict__ cval,
+                                                  uint64_t lo, uint64_t hi, uint32_t T, uint32_t cut,
+                                                  uint32_t* sidx, float* sval, uint64_t o) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  uint32_t n = 0;
+  for (uint64_t base = lo; base < hi; base += 128) {
+    const uint64_t i = base + 4 * lane;
+    float v[4];
+    uint32_t x[4];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    if (i + q < hi) {
-      const uint32_t key = key_of(cval[i + q]);
-      if (key > T || (key == T && cidx[i + q] <= cut)) m |= 1u << q;
+    for (int q = 0; q < 4; ++q) {
+      v[q] = i + q < hi ? cval[i + q] : 0.0f;
+      x[q] = i + q < hi ? cidx[i + q] : 0u;
     }
+    bool k[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t key = key_of(v[q]);
+      k[q] = i + q < hi && (key > T || (key == T && x[q] <= cut));
+    }
+    const RowRank r = row_rank(k[0], k[1], k[2], k[3], lt);
+    if (kWrite) {
+      uint64_t oo = o + n + r.before;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (k[q]) {
+          sidx[oo] = x[q];
+          sval[oo] = v[q];
+          ++oo;
+        }
+    }
+    n += r.total;
   }
-  return m;
+  return n;
 }
 
 __global__ void __launch_bounds__(kCandBlock) topr_final(const uint32_t* __restrict__ cidx,
@@ -394,19 +411,17 @@ __global__ void __launch_bounds__(kCandBlock) topr_final(const uint32_t* __restr
   if (failed(status) || plan->full_bin) return;
   const uint64_t n = plan->n_cand;
   const uint32_t T = plan->thresh, cut = plan->tie_cut;
-  const uint64_t chunk = ((n + gridDim.x - 1) / gridDim.x + 4095) / 4096 * 4096;
+  const uint64_t chunk = ((n + gridDim.x - 1) / gridDim.x + 1023) / 1024 * 1024;
   const uint64_t nchunks = (n + chunk - 1) / chunk;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint64_t wseg = chunk / kCandWarps;
+  const uint64_t wseg = chunk / kCandWarps;  // multiple of 128
   while (true) {
     const uint32_t c = claim_tile(ticket, &slot);
     if (c >= nchunks) break;
     const uint64_t clo = static_cast<uint64_t>(c) * chunk, chi = clo + chunk < n ? clo + chunk : n;
     const uint64_t lo = clo + warp * wseg < chi ? clo + warp * wseg : chi;
     const uint64_t hi = lo + wseg < chi ? lo + wseg : chi;
-    uint32_t nk = 0;
-    for (uint64_t base = lo; base < hi; base += 512)
-      nk += __reduce_add_sync(kFull, __popc(keep_mask(cidx, cval, base + 16 * lane, hi, T, cut)));
+    const uint32_t nk = final_segment<false>(cidx, cval, lo, hi, T, cut, sidx, sval, 0);
     if (lane == 0) wk[warp] = nk;
     __syncthreads();
     uint32_t bk = 0, pw = 0;
@@ -420,22 +435,7 @@ __global__ void __launch_bounds__(kCandBlock) topr_final(const uint32_t* __restr
       if (lane == 0) s_p = p;
     }
     __syncthreads();
-    uint64_t o = s_p + pw;
-    for (uint64_t base = lo; base < hi; base += 512) {
-      const uint64_t i = base + 16 * lane;
-      uint32_t m = keep_mask(cidx, cval, i, hi, T, cut);
-      const uint32_t cnt = __popc(m);
-      const uint32_t inc = warp_inclusive_sum(cnt);
-      uint64_t oo = o + inc - cnt;
-      while (m) {
-        const int q = __ffs(m) - 1;
-        sidx[oo] = cidx[i + q];
-        sval[oo] = cval[i + q];
-        ++oo;
-        m &= m - 1;
-      }
-      o += __shfl_sync(kFull, inc, 31);
-    }
+    final_segment<true>(cidx, cval, lo, hi, T, cut, sidx, sval, s_p + pw);
   }
 }
 
@@ -445,7 +445,8 @@ void launch_top_r(gp_ctx* ctx, const float* grad, uint64_t d, uint64_t r, cudaSt
   Workspace& w = ctx->ws;
   const uint64_t ntiles = (d + kTile - 1) / kTile;
   cudaMemsetAsync(w.hist, 0, kBins * sizeof(uint32_t), s);
-  reset_scan(ctx, s, 3 * (ntiles + 1));
+  const int fgrid = ctx->sm_count * 2;  // topr_final blocks = its chunk count bound
+  reset_scan(ctx, s, 2 * (ntiles + 1) + fgrid + 1);
   uint64_t* tiles_c = w.tiles;
   uint64_t* tiles_t = w.tiles + ntiles + 1;
   const int hist_grid = static_cast<int>(std::min<uint64_t>((d / 4 + kHistBlock - 1) / kHistBlock + 1,
@@ -466,7 +467,7 @@ void launch_top_r(gp_ctx* ctx, const float* grad, uint64_t d, uint64_t r, cudaSt
             w.plan, w.status);
   // final filter: its own scan state (tiles after both previous arrays)
   uint64_t* tiles_f = w.tiles + 2 * (ntiles + 1);
-  GP_LAUNCH(ctx, topr_final, ctx->sm_count * 2, kCandBlock, 0, s, w.cand_idx, w.cand_val, w.plan, w.support,
+  GP_LAUNCH(ctx, topr_final, fgrid, kCandBlock, 0, s, w.cand_idx, w.cand_val, w.plan, w.support,
             w.values, tiles_f, w.ticket + 2, w.status);
 }
 
