@@ -277,6 +277,25 @@ class Codec:
         self.status()
         return int(out.item()) & 0xFFFFFFFF
 
+    def bloom_positive_scan(self, filt: torch.Tensor, d: int) -> torch.Tensor:
+        """positive_scan (bloom.cpp:123-128) of a serialized filter (device u8
+        tensor, FORMAT.md:58-75) over [0, d) → ascending positives (int32)."""
+        out = torch.empty(d, dtype=torch.int32, device=filt.device)
+        count = torch.zeros(1, dtype=torch.int64, device=filt.device)
+        self._raise(lib.gp_bloom_positive_scan(self._ctx, _ptr(filt), filt.numel(), d, _ptr(out), d, _ptr(count),
+                                               _stream()))
+        self.status()
+        return out[: int(count.item())]
+
+    def bloom_select(self, filt: torch.Tensor, d: int, r: int, index_method: int) -> torch.Tensor:
+        """p1_select / p2_select (bloom.cpp:140-154, :175-222) over the positives
+        of a serialized filter, seeded derive_selection_seed(seed_a, seed_b)."""
+        out = torch.empty(r, dtype=torch.int32, device=filt.device)
+        self._raise(lib.gp_bloom_select(self._ctx, _ptr(filt), filt.numel(), d, r, int(index_method), _ptr(out),
+                                        _stream()))
+        self.status()
+        return out
+
 
 def volume(container: bytes) -> dict:
     """volume (container.cpp:148-243) of a packed container held on the host:

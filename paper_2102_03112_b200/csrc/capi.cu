@@ -110,6 +110,28 @@ __global__ void take_support(const float* __restrict__ dense, const uint32_t* __
   }
 }
 
+// component calls: the filter payload starts at offset 0 of the caller's buffer
+__global__ void component_offsets(Plan* plan) {
+  plan->off_index = 0;
+  plan->off_value = plan->il;
+  plan->off_reorder = plan->il;
+}
+
+// P (ascending positives) to the caller, |P| to *count; GP_CAPACITY past cap
+__global__ void copy_positions(const uint32_t* __restrict__ pos, const Plan* plan, uint32_t* __restrict__ out,
+                               uint64_t cap, uint64_t* count, uint32_t* status) {
+  if (failed(status)) return;
+  const uint64_t n = plan->n_pos;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *count = n;
+    if (n > cap) latch(status, GP_CAPACITY);
+  }
+  if (n > cap) return;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = pos[i];
+}
+
 // ---------------------------------------------------------------- workspace
 struct Carver {
   uint8_t* base;
@@ -550,12 +572,50 @@ int gp_crc32c(gp_ctx* ctx, const uint8_t* d_data, uint64_t n, uint32_t* d_crc, v
   return check_launch(ctx, "crc32c");
 }
 
-int gp_bloom_positive_scan(gp_ctx* ctx, const uint8_t*, uint64_t, uint64_t, uint32_t*, uint64_t, uint64_t*, void*) {
-  return set_error(ctx, GP_UNSUPPORTED, "bloom positive scan not built yet");
+// Component calls over a bare serialized filter (no container): the plan is
+// set up as for a decode whose index payload is the filter at offset 0.
+static int bloom_component(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter_len, uint64_t d, uint64_t r,
+                           int method, cudaStream_t s) {
+  if (d < 1 || d > ctx->max_d) return set_error(ctx, GP_CAPACITY, "bloom: d exceeds the context's max_d");
+  PlanInit pi{};
+  pi.d = d;
+  pi.r = r;
+  pi.il = filter_len;
+  pi.index_method = static_cast<uint8_t>(method);
+  pi.value_method = GP_VALUE_NONE;
+  GP_LAUNCH(ctx, init_plan, 1, 1, 0, s, ctx->ws.plan, pi);
+  GP_LAUNCH(ctx, component_offsets, 1, 1, 0, s, ctx->ws.plan);
+  launch_bloom_parse(ctx, d_filter, ctx->ws.m_cap, s);
+  launch_bloom_scan(ctx, d, 0, false, s);
+  return GP_OK;
 }
 
-int gp_bloom_select(gp_ctx* ctx, const uint8_t*, uint64_t, uint64_t, uint64_t, int, uint32_t*, void*) {
-  return set_error(ctx, GP_UNSUPPORTED, "bloom selection not built yet");
+int gp_bloom_positive_scan(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter_len, uint64_t d,
+                           uint32_t* d_positives, uint64_t cap, uint64_t* d_count, void* stream) {
+  if (!ctx || !d_filter || !d_positives || !d_count) return set_error(ctx, GP_ERROR, "positive_scan: null argument");
+  auto s = static_cast<cudaStream_t>(stream);
+  const int rc = bloom_component(ctx, d_filter, filter_len, d, 0, GP_INDEX_BLOOM_P0, s);
+  if (rc != GP_OK) return rc;
+  GP_LAUNCH(ctx, copy_positions, grid_for(ctx, d, 256), 256, 0, s, ctx->ws.pos, ctx->ws.plan, d_positives, cap,
+            d_count, ctx->ws.status);
+  return check_launch(ctx, "positive_scan");
+}
+
+int gp_bloom_select(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter_len, uint64_t d, uint64_t r,
+                    int index_method, uint32_t* d_selected, void* stream) {
+  if (!ctx || !d_filter || !d_selected) return set_error(ctx, GP_ERROR, "bloom_select: null argument");
+  if (index_method != GP_INDEX_BLOOM_P1 && index_method != GP_INDEX_BLOOM_P2)
+    return set_error(ctx, GP_ERROR, "bloom_select: index_method must be P1 (5) or P2 (6)");
+  if (r < 1) return set_error(ctx, GP_ERROR, "bloom_select: r must be >= 1");
+  auto s = static_cast<cudaStream_t>(stream);
+  const int rc = bloom_component(ctx, d_filter, filter_len, d, r, index_method, s);
+  if (rc != GP_OK) return rc;
+  if (index_method == GP_INDEX_BLOOM_P2)
+    launch_select_p2(ctx, d, ctx->ws.set_cap, 64, false, s);
+  else
+    launch_select_p1(ctx, d, d, s);
+  cudaMemcpyAsync(d_selected, ctx->ws.sel, r * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s);
+  return check_launch(ctx, "bloom_select");
 }
 
 }  // extern "C"

@@ -29,7 +29,7 @@ def codec():
 
 
 def _dev(a):
-    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    return torch.from_numpy(np.array(a, copy=True)).cuda()
 
 
 def _cfg(im, vm, **kw):
@@ -163,3 +163,31 @@ def test_bloom_decode_bit_exact(codec, oracle, im, vm):
         od, osup, oval = oracle.decode(c)
         assert gd == od and np.array_equal(sup.cpu().numpy().astype(np.uint32), osup)
         assert np.array_equal(val.cpu().numpy(), oval)
+
+
+@pytest.mark.parametrize("d,r,eps", [(50_000, 500, 0.01), (300_000, 3_000, 0.001), (1_000_000, 10_000, 0.05)])
+def test_bloom_components_bit_exact(codec, oracle, d, r, eps):
+    """gp_bloom_positive_scan / gp_bloom_select on a bare serialized filter."""
+    g = synthetic_gradient(d, rank=3)
+    sup = oracle.top_r(g, r)
+    filt = oracle.bloom_build(sup, eps, 0x1234, 0x5678)
+    f = _dev(np.frombuffer(filt, np.uint8))
+    pos = codec.bloom_positive_scan(f, d).cpu().numpy().astype(np.uint32)
+    assert np.array_equal(pos, oracle.positive_scan(filt, d))
+    for im in (P1, P2):
+        got = codec.bloom_select(f, d, r, im).cpu().numpy().astype(np.uint32)
+        assert np.array_equal(got, oracle.bloom_select(filt, d, r, im)), im
+
+
+def test_bloom_components_errors(codec, oracle):
+    from paper_2102_03112_b200 import CorruptPayloadError, Error
+    d, r = 20_000, 200
+    sup = oracle.top_r(synthetic_gradient(d, rank=1), r)
+    filt = bytearray(oracle.bloom_build(sup, 0.01, 1, 2))
+    f = _dev(np.frombuffer(bytes(filt), np.uint8))
+    with pytest.raises(Error):  # |P| < r for the selection
+        codec.bloom_select(f, d, d, P2)
+    bad = bytearray(filt)
+    bad[8] = bad[9] = 0  # k = 0
+    with pytest.raises(CorruptPayloadError):
+        codec.bloom_positive_scan(_dev(np.frombuffer(bytes(bad), np.uint8)), d)
