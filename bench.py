@@ -47,6 +47,10 @@ CONFIGS = {
                d=25_557_032, ratio=0.01, index=6, value=1, fpr=0.001, degree=5, max_segments=0, sparse=False),
     "c4s": dict(workload="C4 stress point: bloom-filter P2 at eps=1e-2 + polynomial curve-fit",
                 d=25_557_032, ratio=0.01, index=6, value=1, fpr=0.01, degree=5, max_segments=0, sparse=False),
+    "c4ef": dict(workload="C4 with error feedback (memory compensation, harness.cpp:230/269-271): encode of "
+                          "g + residual, residual <- input - decode(own container), then allgather + decode",
+                 d=25_557_032, ratio=0.01, index=6, value=1, fpr=0.001, degree=5, max_segments=0, sparse=False,
+                 ef=True),
     "c1": dict(workload="synthetic 1M-element gradient, top-r 1%, bloom-filter P0 (eps=1e-2) + polynomial "
                         "curve-fit, single-worker round trip",
                d=1_000_000, ratio=0.01, index=4, value=1, fpr=0.01, degree=5, max_segments=0, sparse=False),
@@ -232,12 +236,12 @@ def native_main(args, cfg):
                           degree=cfg["degree"], max_segments=cfg["max_segments"])
     if cfg.get("buckets"):
         ex = BucketedSparseAllgather(lambda dmax: Codec(max_d=dmax, device=local), d, cfg["ratio"], pcfg,
-                                     cfg["buckets"], streams=3)
+                                     cfg["buckets"], streams=3, ef=cfg.get("ef", False))
         codecs = ex.codecs
         r_total = sum(ex.rs)
     else:
         codec = Codec(max_d=d, device=local)
-        ex = SparseAllgather(codec, d, r, pcfg)
+        ex = SparseAllgather(codec, d, r, pcfg, ef=cfg.get("ef", False))
         codecs = [codec]
         r_total = r
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2

@@ -105,6 +105,17 @@ GP_API int gp_encode_topr(gp_ctx* ctx, const float* d_grad, uint64_t d, uint64_t
                    const gp_pipeline_config* cfg, uint8_t* d_out, uint64_t cap,
                    uint64_t* d_len, void* stream);
 
+/* Error-feedback encode, the compensation step of the reference worker loop
+ * (harness.cpp:230 input = g + residual; :250 compress_gradient(top_r(input),
+ * cfg, &input) + pack; :269-271 residual = input - to_dense(decode(wire))).
+ * d_grad: f32[d]; d_residual: f32[d], read as e and overwritten with the new
+ * residual.  The add is fused into top-r's first pass (f32, round to
+ * nearest); the subtraction is the decode scatter with scale -1.  Writes the
+ * container and its length word as gp_encode_topr does. */
+GP_API int gp_encode_topr_ef(gp_ctx* ctx, const float* d_grad, float* d_residual, uint64_t d, uint64_t r,
+                             const gp_pipeline_config* cfg, uint8_t* d_out, uint64_t cap,
+                             uint64_t* d_len, void* stream);
+
 /* compress_gradient(sg, cfg, &dense) + pack for a caller-chosen support:
  * d_support: u32[r] strictly increasing (validated, gradient.cpp:19-30),
  * values are gathered from d_dense (pipeline.cpp:38-54). */

@@ -214,6 +214,26 @@ class Codec:
                                        _ptr(length), _stream(stream))
         self._raise(rc)
 
+    def encode_ef_into(self, grad: torch.Tensor, residual: torch.Tensor, r: int, cfg: PipelineConfig,
+                       out: torch.Tensor, length: torch.Tensor, stream=None):
+        """Error-feedback step of the reference worker loop (harness.cpp:230, :250,
+        :269-271), asynchronous: input = grad + residual; the container of
+        top_r(input) goes to ``out`` (length word in ``length``); ``residual`` is
+        overwritten with input - decode(container)."""
+        for t in (grad, residual):
+            assert t.dtype == torch.float32 and t.is_cuda and t.is_contiguous()
+        assert residual.numel() == grad.numel() and out.dtype == torch.uint8 and out.is_cuda
+        c = cfg.to_c()
+        self._raise(lib.gp_encode_topr_ef(self._ctx, _ptr(grad), _ptr(residual), grad.numel(), r, C.byref(c),
+                                          _ptr(out), out.numel(), _ptr(length), _stream(stream)))
+
+    def compress_ef(self, grad: torch.Tensor, residual: torch.Tensor, r: int, cfg: PipelineConfig) -> torch.Tensor:
+        """encode_ef_into, synchronised; returns the packed container (device u8)."""
+        out = torch.empty(self.max_container_bytes(grad.numel(), r, cfg), dtype=torch.uint8, device=grad.device)
+        self.encode_ef_into(grad, residual, r, cfg, out, self._len[0:1])
+        self.status()
+        return out[: int(self._len[0].item())]
+
     def compress(self, grad: torch.Tensor, r: int, cfg: PipelineConfig,
                  support: torch.Tensor | None = None) -> torch.Tensor:
         """top_r + compress_gradient + pack; returns the packed container (device u8)."""

@@ -371,7 +371,7 @@ uint64_t gp_max_container_bytes(uint64_t d, uint64_t r, const gp_pipeline_config
 
 static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const uint32_t* d_support, uint64_t r,
                          const gp_pipeline_config* cfg, uint8_t* d_out, uint64_t cap, uint64_t* d_len,
-                         void* stream) {
+                         void* stream, float* ef_residual = nullptr) {
   if (!ctx || !cfg || !d_dense || !d_out) return set_error(ctx, GP_ERROR, "encode: null argument");
   auto s = static_cast<cudaStream_t>(stream);
   if (d < 1) return set_error(ctx, GP_ERROR, "sparsifier: dim must be >= 1");
@@ -420,7 +420,8 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
     GP_LAUNCH(ctx, take_support, grid_for(ctx, r, 256), 256, 0, s, d_dense, d_support, r, d, ctx->ws.support,
               ctx->ws.values, ctx->ws.status);
   } else {
-    GP_STAGE(ctx, ST_TOPR, s, launch_top_r(ctx, d_dense, d, r, s));
+    GP_STAGE(ctx, ST_TOPR, s, launch_top_r(ctx, d_dense, d, r, s, ef_residual));
+    if (ef_residual) d_dense = ef_residual;  // the input g + e, written by top-r's first pass
   }
   switch (im) {
     case GP_INDEX_NONE: launch_index_none(ctx, d_out, r, s); break;
@@ -464,10 +465,16 @@ int gp_encode_support(gp_ctx* ctx, const float* d_dense, uint64_t d, const uint3
   return encode_common(ctx, d_dense, d, d_support, r, cfg, d_out, cap, d_len, stream);
 }
 
+// own: the container this context just encoded (error feedback).  The index
+// stage is skipped where the encoder's state already holds the decoded
+// support — the selection in ws.sel for Bloom P0/P1/P2/Pd, the top-r support
+// for none/bitmap/RLE (copied to ws.sel) — since decoding the index payload
+// reproduces exactly that set; Bloom-naive (whose decoded support is all of P,
+// never computed by the encoder) takes the full decode.
 static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const uint64_t* d_len,
                          const gp_pipeline_config* hint,
                          float* d_dense, uint64_t dense_d, float scale, uint32_t* d_support, double* d_values,
-                         uint64_t cap, uint64_t* d_count, uint64_t* d_dim, void* stream) {
+                         uint64_t cap, uint64_t* d_count, uint64_t* d_dim, void* stream, bool own = false) {
   if (!ctx || !d_in) return set_error(ctx, GP_ERROR, "decode: null argument");
   auto s = static_cast<cudaStream_t>(stream);
   gp_pipeline_config h{};
@@ -498,7 +505,9 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const u
   }
   if (!known) return check_launch(ctx, "decode");  // verify_container latches UnknownMethod
   const uint64_t bound = ctx->max_d;
-  switch (im) {
+  if (own && im != GP_INDEX_BLOOM_NAIVE) {
+    if (!is_bloom(im)) launch_own_support(ctx, bound, s);
+  } else switch (im) {
     case GP_INDEX_NONE: launch_decode_index_none(ctx, d_in, bound, s); break;
     case GP_INDEX_BITMAP: launch_decode_index_bitmap(ctx, d_in, bound, s); break;
     case GP_INDEX_RLE: GP_STAGE(ctx, ST_DEC_INDEX, s, launch_decode_index_rle(ctx, d_in, len, bound, s)); break;
@@ -519,7 +528,7 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const u
     case GP_VALUE_FIT_POLY: GP_STAGE(ctx, ST_DEC_VALUES, s, launch_decode_fit(ctx, d_in, bound, s)); break;
     default: break;
   }
-  if (im == GP_INDEX_NONE) launch_validate_support(ctx, bound, s);
+  if (im == GP_INDEX_NONE && !own) launch_validate_support(ctx, bound, s);
   (void)dense_d;
   GP_STAGE(ctx, ST_DEC_SCATTER, s,
            launch_decode_scatter(ctx, d_in, bound, d_dense, scale, d_support, d_values, cap, d_count, d_dim, s));
@@ -550,6 +559,16 @@ int gp_decode_sparse(gp_ctx* ctx, const uint8_t* d_container, uint64_t len, uint
   if (!d_support || !d_values) return set_error(ctx, GP_ERROR, "decode_sparse: null output");
   return decode_common(ctx, d_container, len, nullptr, nullptr, nullptr, 0, 0.0f, d_support, d_values, cap, d_count,
                        d_dim, stream);
+}
+
+int gp_encode_topr_ef(gp_ctx* ctx, const float* d_grad, float* d_residual, uint64_t d, uint64_t r,
+                      const gp_pipeline_config* cfg, uint8_t* d_out, uint64_t cap, uint64_t* d_len, void* stream) {
+  if (!d_residual || !d_grad) return set_error(ctx, GP_ERROR, "encode_topr_ef: null argument");
+  const int rc = encode_common(ctx, d_grad, d, nullptr, r, cfg, d_out, cap, d_len, stream, d_residual);
+  if (rc != GP_OK) return rc;
+  // residual <- input - decode(container)  (harness.cpp:269-271)
+  return decode_common(ctx, d_out, cap, d_len, cfg, d_residual, d, -1.0f, nullptr, nullptr, 0, nullptr, nullptr,
+                       stream, true);
 }
 
 int gp_top_r(gp_ctx* ctx, const float* d_grad, uint64_t d, uint64_t r, uint32_t* d_support, float* d_values,

@@ -175,7 +175,8 @@ int check_launch(gp_ctx* ctx, const char* what);
 void reset_scan(gp_ctx* ctx, cudaStream_t s, uint64_t ntiles_bound);  // capi.cu
 
 // topr.cu: ws.support / ws.values <- top-r of grad
-void launch_top_r(gp_ctx* ctx, const float* grad, uint64_t d, uint64_t r, cudaStream_t s);
+void launch_top_r(gp_ctx* ctx, const float* grad, uint64_t d, uint64_t r, cudaStream_t s, float* residual = nullptr);
+void launch_own_support(gp_ctx* ctx, uint64_t r_bound, cudaStream_t s);
 
 // container.cu
 void launch_crc_range(gp_ctx* ctx, const uint8_t* base, const uint64_t* off_dev, uint64_t off_host,

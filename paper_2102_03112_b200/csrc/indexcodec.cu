@@ -170,4 +170,25 @@ void launch_decode_index_bitmap(gp_ctx* ctx, const uint8_t* in, uint64_t d_bound
   GP_LAUNCH(ctx, bitmap_popcount_check, 1, 1, 0, s, w.plan, w.status);
 }
 
+// error feedback, own container: the decoded support of a none/bitmap/RLE
+// container is the encoder's top-r support
+namespace {
+__global__ void own_support(Plan* plan, const uint32_t* __restrict__ support, uint32_t* sel, const uint32_t* status) {
+  if (failed(status)) return;
+  const uint64_t r = plan->r;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < r;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    sel[i] = support[i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    plan->n_sel = r;
+    plan->n_values = r;
+  }
+}
+}  // namespace
+
+void launch_own_support(gp_ctx* ctx, uint64_t r_bound, cudaStream_t s) {
+  Workspace& w = ctx->ws;
+  GP_LAUNCH(ctx, own_support, grid_for(ctx, r_bound, 256), 256, 0, s, w.plan, w.support, w.sel, w.status);
+}
+
 }  // namespace gp

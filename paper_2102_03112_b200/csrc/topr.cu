@@ -33,21 +33,37 @@ constexpr int kTile = kTileBlock * kTileItems;
 
 __device__ __forceinline__ uint32_t key_of(float v) { return __float_as_uint(v) & 0x7FFFFFFFu; }
 
-__global__ void __launch_bounds__(kHistBlock) topr_hist(const float* __restrict__ g, uint64_t d,
-                                                        uint32_t* __restrict__ ghist,
+// kEF: error feedback fused into the first pass (harness.cpp:230): the pass
+// reads g and the residual e, writes input = g + e over e (every later pass
+// and the value gather read e as the dense input) and histograms the input.
+template <bool kEF>
+__global__ void __launch_bounds__(kHistBlock) topr_hist(const float* __restrict__ g, float* __restrict__ e,
+                                                        uint64_t d, uint32_t* __restrict__ ghist,
                                                         const uint32_t* status) {
   extern __shared__ uint32_t h[];  // kBins counters
   if (failed(status)) return;
   for (int i = threadIdx.x; i < kBins; i += kHistBlock) h[i] = 0;
   __syncthreads();
-  const bool aligned = (reinterpret_cast<uintptr_t>(g) & 15) == 0;
+  const bool aligned = (reinterpret_cast<uintptr_t>(g) & 15) == 0 && (!kEF || (reinterpret_cast<uintptr_t>(e) & 15) == 0);
   const uint64_t n4 = aligned ? d / 4 : 0;
   const float4* g4 = reinterpret_cast<const float4*>(g);
+  float4* e4 = reinterpret_cast<float4*>(e);
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kHistBlock;
   for (uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * kHistBlock + threadIdx.x; i0 < n4; i0 += 4 * stride) {
     float4 v[4];  // four independent 16-byte loads in flight per thread
 #pragma unroll
     for (int u = 0; u < 4; ++u) v[u] = i0 + u * stride < n4 ? __ldcs(&g4[i0 + u * stride]) : make_float4(-1, -1, -1, -1);
+    if (kEF) {
+      float4 r4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) r4[u] = i0 + u * stride < n4 ? e4[i0 + u * stride] : make_float4(0, 0, 0, 0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        v[u] = make_float4(__fadd_rn(v[u].x, r4[u].x), __fadd_rn(v[u].y, r4[u].y), __fadd_rn(v[u].z, r4[u].z),
+                           __fadd_rn(v[u].w, r4[u].w));
+        if (i0 + u * stride < n4) e4[i0 + u * stride] = v[u];
+      }
+    }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       if (i0 + u * stride < n4) {
@@ -58,8 +74,14 @@ __global__ void __launch_bounds__(kHistBlock) topr_hist(const float* __restrict_
       }
     }
   }
-  for (uint64_t i = n4 * 4 + static_cast<uint64_t>(blockIdx.x) * kHistBlock + threadIdx.x; i < d; i += stride)
-    atomicAdd(&h[key_of(g[i]) >> kShift], 1u);
+  for (uint64_t i = n4 * 4 + static_cast<uint64_t>(blockIdx.x) * kHistBlock + threadIdx.x; i < d; i += stride) {
+    float v = g[i];
+    if (kEF) {
+      v = __fadd_rn(v, e[i]);
+      e[i] = v;
+    }
+    atomicAdd(&h[key_of(v) >> kShift], 1u);
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < kBins; i += kHistBlock)
     if (h[i]) atomicAdd(&ghist[i], h[i]);
@@ -441,7 +463,9 @@ __global__ void __launch_bounds__(kCandBlock) topr_final(const uint32_t* __restr
 
 }  // namespace
 
-void launch_top_r(gp_ctx* ctx, const float* grad, uint64_t d, uint64_t r, cudaStream_t s) {
+// residual != nullptr: error feedback — the first pass writes grad + residual
+// over residual, and the selection runs on that input.
+void launch_top_r(gp_ctx* ctx, const float* grad, uint64_t d, uint64_t r, cudaStream_t s, float* residual) {
   Workspace& w = ctx->ws;
   const uint64_t ntiles = (d + kTile - 1) / kTile;
   cudaMemsetAsync(w.hist, 0, kBins * sizeof(uint32_t), s);
@@ -453,10 +477,16 @@ void launch_top_r(gp_ctx* ctx, const float* grad, uint64_t d, uint64_t r, cudaSt
                                                             static_cast<uint64_t>(ctx->sm_count)));
   static bool attr = false;  // opt in to the 128 KiB shared histogram once per process
   if (!attr) {
-    cudaFuncSetAttribute(topr_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, kBins * 4);
+    cudaFuncSetAttribute(topr_hist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBins * 4);
+    cudaFuncSetAttribute(topr_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBins * 4);
     attr = true;
   }
-  GP_LAUNCH(ctx, topr_hist, hist_grid, kHistBlock, kBins * 4, s, grad, d, w.hist, w.status);
+  if (residual) {
+    GP_LAUNCH(ctx, topr_hist<true>, hist_grid, kHistBlock, kBins * 4, s, grad, residual, d, w.hist, w.status);
+    grad = residual;
+  } else {
+    GP_LAUNCH(ctx, topr_hist<false>, hist_grid, kHistBlock, kBins * 4, s, grad, nullptr, d, w.hist, w.status);
+  }
   GP_LAUNCH(ctx, topr_pick_bin, 1, 1024, 0, s, w.hist, r, w.plan, w.status);
   const uint64_t nblk = static_cast<uint64_t>(ctx->sm_count) * 4;
   const uint64_t chunk = std::max<uint64_t>(4096, ((d + nblk - 1) / nblk + 4095) / 4096 * 4096);  // multiple of 8 warps * 512

@@ -67,9 +67,12 @@ def _world(group):
 
 
 class SparseAllgather:
-    """One DP worker's encode → exchange → decode step."""
+    """One DP worker's encode → exchange → decode step.  ef=True adds the
+    reference's memory compensation (TrainConfig::compensation,
+    harness.cpp:230, :269-271): the rank encodes g + residual and keeps
+    input - decode(own container) as the next step's residual."""
 
-    def __init__(self, codec, d: int, r: int, cfg, group=None, device=None):
+    def __init__(self, codec, d: int, r: int, cfg, group=None, device=None, ef: bool = False):
         self.codec = codec
         self.d, self.r, self.cfg = d, r, cfg
         self.group = group
@@ -81,6 +84,7 @@ class SparseAllgather:
         self.sizes = torch.zeros(self.world, dtype=torch.int64, device=dev)
         self.recv = torch.empty(self.world * self.cap, dtype=torch.uint8, device=dev) if self.world > 1 else None
         self.dense = torch.zeros(d, dtype=torch.float32, device=dev)
+        self.residual = torch.zeros(d, dtype=torch.float32, device=dev) if ef else None
 
     def step(self, grad: torch.Tensor, step: int, seed: int = 1, dense: torch.Tensor | None = None,
              stream=None) -> torch.Tensor:
@@ -91,7 +95,10 @@ class SparseAllgather:
 
     def step_seeded(self, grad, cfg, dense=None, stream=None):
         out_dense = self.dense if dense is None else dense
-        self.codec.encode_into(grad, self.r, cfg, self.out, self.length, stream=stream)
+        if self.residual is not None:
+            self.codec.encode_ef_into(grad, self.residual, self.r, cfg, self.out, self.length, stream=stream)
+        else:
+            self.codec.encode_into(grad, self.r, cfg, self.out, self.length, stream=stream)
         out_dense.zero_()
         n = self.world
         if n == 1:  # no exchange: the device-side length drives the decode (no host sync)
@@ -112,7 +119,7 @@ class BucketedSparseAllgather:
     """Bucketed DP step for gradients too large for one container (C5)."""
 
     def __init__(self, codec_factory, d: int, ratio: float, cfg, buckets: int, streams: int = 3, group=None,
-                 device=None):
+                 device=None, ef: bool = False):
         self.d, self.cfg, self.buckets = d, cfg, buckets
         self.world, self.rank = _world(group)
         base, rem = divmod(d, buckets)
@@ -129,7 +136,7 @@ class BucketedSparseAllgather:
         cuda = device is None or torch.device(device).type == "cuda"
         self.streams = [torch.cuda.Stream() for _ in range(self.nstreams)] if cuda else [None] * self.nstreams
         self.ex = [SparseAllgather(self.codecs[i % self.nstreams], e - s, self.rs[i], cfg, group=group,
-                                   device=device) for i, (s, e) in enumerate(self.bounds)]
+                                   device=device, ef=ef) for i, (s, e) in enumerate(self.bounds)]
         dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.dense = torch.zeros(d, dtype=torch.float32, device=dev)
 

@@ -40,6 +40,13 @@ class OracleCodec:
         out[: len(b)] = torch.frombuffer(bytearray(b), dtype=torch.uint8)
         length[0] = len(b)
 
+    def encode_ef_into(self, grad, residual, r, cfg, out, length, stream=None):
+        from oracle.ef import ef_step
+        b, res = ef_step(oracle(), grad.contiguous().numpy(), residual.numpy(), r, self._c(cfg))
+        out[: len(b)] = torch.frombuffer(bytearray(b), dtype=torch.uint8)
+        length[0] = len(b)
+        residual.copy_(torch.from_numpy(res))
+
     def decode_accumulate(self, container, dense, scale=1.0, length=None, hint=None, stream=None):
         n = int(length.item()) if isinstance(length, torch.Tensor) else (container.numel() if length is None else length)
         _, sup, val = oracle().decode(container[:n].contiguous().numpy().tobytes())
@@ -61,7 +68,7 @@ CFGS = {
 }
 
 
-def _worker(rank, world, port, name, d, r, steps, buckets, q):
+def _worker(rank, world, port, name, d, r, steps, buckets, q, ef=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2102_03112_b200.dp import BucketedSparseAllgather, SparseAllgather
@@ -70,25 +77,29 @@ def _worker(rank, world, port, name, d, r, steps, buckets, q):
     outs = []
     if buckets:
         ex = BucketedSparseAllgather(lambda dmax: OracleCodec(), d, r / d, cfg, buckets, streams=2,
-                                     device="cpu")
+                                     device="cpu", ef=ef)
     else:
-        ex = SparseAllgather(OracleCodec(), d, r, cfg, device="cpu")
+        ex = SparseAllgather(OracleCodec(), d, r, cfg, device="cpu", ef=ef)
     for step in range(steps):
         outs.append(ex.step(g, step=step).clone().numpy())
     q.put((rank, outs))
     dist.destroy_process_group()
 
 
-def _sequential(name, d, r, steps, world, buckets):
-    """Simulation::step's worker loop, one process: encode every worker, decode, mean."""
+def _sequential(name, d, r, steps, world, buckets, ef=False):
+    """Simulation::step's worker loop, one process: encode every worker, decode, mean
+    (with compensation: input = g + residual, residual = input - decoded)."""
     from paper_2102_03112_b200.dp import hash64, pipeline_seed, ratio_r
     o = oracle()
     base = PipelineConfig(**CFGS[name])
     means = []
+    resid = [np.zeros(d, np.float32) for _ in range(world)]
     for step in range(steps):
         acc = np.zeros(d, np.float32)
         for w in range(world):  # rank order
             g = synthetic_gradient(d, rank=w)
+            if ef:
+                g = (g + resid[w]).astype(np.float32)
             parts = [(0, d, r, pipeline_seed(1, w, step))]
             if buckets:
                 lo, parts = 0, []
@@ -100,27 +111,33 @@ def _sequential(name, d, r, steps, world, buckets):
             for lo, hi, rb, seed in parts:
                 c = o.encode_dense(g[lo:hi], rb, OracleCodec._c(PipelineConfig(**{**base.__dict__, "seed": seed})))
                 _, sup, val = o.decode(c)
+                if ef:
+                    res = g[lo:hi].copy()
+                    res[sup] = (g[lo:hi][sup] - val.astype(np.float32)).astype(np.float32)
+                    resid[w][lo:hi] = res
                 a = acc[lo:hi]
                 a[sup] = np.float32(1.0 / world) * val.astype(np.float32) + a[sup]
         means.append(acc)
     return means
 
 
-@pytest.mark.parametrize("name,d,r,buckets", [("p2fit", 20_000, 200, 0), ("bitmap", 5_000, 50, 0),
-                                              ("rle", 7_000, 70, 0), ("p2fit", 40_000, 40, 4)])
-def test_gloo_world2_matches_sequential_harness(name, d, r, buckets):
-    world, steps = 2, 2
+@pytest.mark.parametrize("name,d,r,buckets,ef", [("p2fit", 20_000, 200, 0, False), ("bitmap", 5_000, 50, 0, False),
+                                                 ("rle", 7_000, 70, 0, False), ("p2fit", 40_000, 40, 4, False),
+                                                 ("p2fit", 20_000, 200, 0, True), ("bitmap", 40_000, 40, 4, True)])
+def test_gloo_world2_matches_sequential_harness(name, d, r, buckets, ef):
+    world, steps = 2, 3 if ef else 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(k, world, port, name, d, r, steps, buckets, q)) for k in range(world)]
+    procs = [ctx.Process(target=_worker, args=(k, world, port, name, d, r, steps, buckets, q, ef))
+             for k in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in range(world))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    want = _sequential(name, d, r, steps, world, buckets)
+    want = _sequential(name, d, r, steps, world, buckets, ef)
     for step in range(steps):
         assert np.array_equal(res[0][step], res[1][step]), "replicas diverged"
         assert np.array_equal(res[0][step], want[step])

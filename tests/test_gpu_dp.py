@@ -78,3 +78,25 @@ def test_bucketed_step_is_bucketwise():
         want = one.step_seeded(g[lo:hi], replace(cfg, seed=bex.bucket_seed(1, 3, b)))
         assert torch.equal(got[lo:hi], want)
         codec.close()
+
+
+def test_dp_step_with_error_feedback_matches_oracle(oracle):
+    """ef=True: three compensated steps at N = 1 against the oracle's worker loop."""
+    from oracle.ef import ef_step
+    from paper_2102_03112_b200 import Codec
+    from paper_2102_03112_b200.dp import SparseAllgather, pipeline_seed
+    d, r = 250_000, 2_500
+    codec = Codec(max_d=d)
+    ex = SparseAllgather(codec, d, r, _pcfg(P2, V_NONE, fpr=0.001), ef=True)
+    e = np.zeros(d, np.float32)
+    for step in range(3):
+        g = synthetic_gradient(d, rank=step)
+        dense = ex.step(torch.from_numpy(g).cuda(), step=step).cpu().numpy()
+        codec.status()
+        c, e = ef_step(oracle, g, e, r, GpConfig.make(P2, V_NONE, fpr=0.001, seed=pipeline_seed(1, 0, step)))
+        assert bytes(ex.out[: int(ex.length.item())].cpu().numpy()) == c
+        assert np.array_equal(ex.residual.cpu().numpy(), e)
+        ref = np.zeros(d, np.float64)
+        oracle.decode_accumulate(c, ref, 1.0)
+        assert np.array_equal(dense, ref.astype(np.float32))
+    codec.close()

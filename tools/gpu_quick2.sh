@@ -1,0 +1,7 @@
+# full GPU suite + a list of configs
+python -m pytest tests -q -m gpu -x > gpurun_out/t.log 2>&1; tail -3 gpurun_out/t.log
+for c in ${@:-c4}; do
+python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/b_$c.json 2> gpurun_out/err_$c.log
+python -c "
+import json; d=json.load(open('gpurun_out/b_$c.json')); print('$c', d['ms_per_step'], d['value'], d['e2e']['value'], {k:round(v,3) for k,v in d.get('stages_ms_per_step',{}).items()})"
+done
