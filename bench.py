@@ -65,7 +65,7 @@ CONFIGS = {
     "c2r": dict(workload="ResNet-20-sized 0.27M-element gradient, top-r 1%, RLE indices + raw f32 values",
                 d=269_722, ratio=0.01, index=2, value=0, fpr=0.01, degree=5, max_segments=0, sparse=False),
     "c5": dict(workload="BERT-large-sized 340M-element gradient, top-r 0.1%, bloom-filter P2 (eps=1e-3) + "
-                        "piecewise curve-fit (8 pieces), 16 independent 21.25M buckets pipelined on 3 streams",
+                        "piecewise curve-fit (8 pieces), 16 independent 21.25M buckets pipelined on 8 streams",
                d=340_000_000, ratio=0.001, index=6, value=1, fpr=0.001, degree=5, max_segments=8, sparse=False,
                buckets=16),
 }
@@ -236,7 +236,7 @@ def native_main(args, cfg):
                           degree=cfg["degree"], max_segments=cfg["max_segments"])
     if cfg.get("buckets"):
         ex = BucketedSparseAllgather(lambda dmax: Codec(max_d=dmax, device=local), d, cfg["ratio"], pcfg,
-                                     cfg["buckets"], streams=3, ef=cfg.get("ef", False))
+                                     cfg["buckets"], streams=args.streams, ef=cfg.get("ef", False))
         codecs = ex.codecs
         r_total = sum(ex.rs)
     else:
@@ -407,6 +407,7 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--ref-shrink", type=int, default=8, help="reference arm: d/shrink-element sample per thread")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", type=int, default=8, help="bucketed configs: codec contexts / CUDA streams")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
