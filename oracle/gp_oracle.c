@@ -1284,6 +1284,70 @@ static double* gather_values(const sparse_t* sg, const float* dense, const uint3
   return out;
 }
 
+/* quantize + serialize_quant (codecs.cpp:290-351): per bucket the f32 scale
+ * 2*max|v|; code = floor(u) + [unit() < frac(u)], u = (v/scale + 0.5)*levels
+ * clamped to [0, levels]; unit() is drawn only when scale > 0; codes packed
+ * LSB-first at `bits` each.  Payload: bits u8, bucket u32, scales f32[nb], codes. */
+static void quantize_serialize(const double* v, uint64_t n, int bits, uint32_t bucket, rng_t* g, bytes_t* out) {
+  if (bits < 1 || bits > 16) fail(GP_ERROR, "quantize: bits out of range [1, 16]");
+  if (bucket < 1) fail(GP_ERROR, "quantize: bucket must be >= 1");
+  const uint64_t levels = (1ULL << bits) - 1;
+  const uint64_t nb = (n + bucket - 1) / bucket;
+  put_u8(out, (uint8_t)bits);
+  put_le(out, bucket, 4);
+  float* scales = (float*)xalloc((nb ? nb : 1) * sizeof(float));
+  for (uint64_t b = 0; b < nb; ++b) {
+    const uint64_t lo = b * bucket, hi = lo + bucket < n ? lo + bucket : n;
+    double mx = 0.0;
+    for (uint64_t i = lo; i < hi; ++i) mx = fabs(v[i]) > mx ? fabs(v[i]) : mx;
+    scales[b] = (float)(2.0 * mx);
+    put_f32(out, scales[b]);
+  }
+  bitw_t w;
+  bw_init(&w, (n * (uint64_t)bits + 7) / 8 + 1);
+  for (uint64_t i = 0; i < n; ++i) {
+    const float scale = scales[i / bucket];
+    uint64_t code = 0;
+    if (scale > 0.0f) {
+      double u = (v[i] / (double)scale + 0.5) * (double)levels;
+      u = u < 0.0 ? 0.0 : (u > (double)levels ? (double)levels : u);
+      const double lo = floor(u);
+      const double frac = u - lo;
+      code = (uint64_t)lo;
+      if (rng_unit(g) < frac) ++code;
+      if (code > levels) code = levels;
+    }
+    bw_bits(&w, code, (unsigned)bits);
+  }
+  put_bytes(out, w.b.p, w.b.n);
+}
+
+/* parse_quant + dequantize (codecs.cpp:327-368, pipeline.cpp:124-129) */
+static double* parse_dequantize(const uint8_t* p, size_t len, uint64_t count) {
+  breader_t r = {p, len, 0};
+  const unsigned bits = (unsigned)get_le(&r, 1);
+  if (bits < 1 || bits > 16) fail(GP_CORRUPT_PAYLOAD, "quant: bits out of range");
+  const uint32_t bucket = (uint32_t)get_le(&r, 4);
+  if (bucket < 1) fail(GP_CORRUPT_PAYLOAD, "quant: bucket must be >= 1");
+  const uint64_t nb = (count + bucket - 1) / bucket;
+  float* scales = (float*)xalloc((nb ? nb : 1) * sizeof(float));
+  for (uint64_t b = 0; b < nb; ++b) scales[b] = get_f32(&r);
+  const uint64_t code_bytes = (count * bits + 7) / 8;
+  const uint8_t* codes = get_bytes(&r, code_bytes);
+  if (r.pos != r.n) fail(GP_CORRUPT_PAYLOAD, "pipeline: quant payload trailing bytes");
+  const uint64_t levels = (1ULL << bits) - 1;
+  double* out = (double*)xalloc((count ? count : 1) * 8);
+  for (uint64_t i = 0; i < count; ++i) {
+    uint64_t code = 0;
+    for (unsigned j = 0; j < bits; ++j) {
+      const uint64_t bit = i * bits + j;
+      code |= (uint64_t)((codes[bit / 8] >> (bit % 8)) & 1u) << j;
+    }
+    out[i] = (double)scales[i / bucket] * ((double)code / (double)levels - 0.5);
+  }
+  return out;
+}
+
 static void encode_values(const double* values, uint64_t n, const gp_pipeline_config* cfg, uint64_t d,
                           bytes_t* vout, bitw_t* rout) { /* pipeline.cpp:56-93 */
   switch (cfg->value_method) {
@@ -1300,6 +1364,19 @@ static void encode_values(const double* values, uint64_t n, const gp_pipeline_co
       value_compress(values, n, cfg->degree, cfg->max_segments, &m, &map, &map_len);
       if (map_len) reorder_encode(map, map_len, d, rout);
       serialize_fit(&m, vout);
+      return;
+    }
+    case GP_VALUE_QUANT: {
+      rng_t g = {gpo_hash64(0xC, cfg->seed)}; /* derive_quant_seed, pipeline.cpp:26, :81-84 */
+      quantize_serialize(values, n, cfg->quant_bits, cfg->quant_bucket, &g, vout);
+      return;
+    }
+    case GP_VALUE_DEFLATE_SLOT: { /* pipeline.cpp:85-90 + byte_compress codecs.cpp:244-266 */
+      if (cfg->slot_codec == 1) fail(GP_UNSUPPORTED, "oracle: the deflate byte codec is out of scope");
+      if (cfg->slot_codec != 0) fail(GP_UNKNOWN_METHOD, "byte_compress: unknown codec id");
+      put_u8(vout, 0);
+      put_le(vout, 4 * n, 8);
+      for (uint64_t i = 0; i < n; ++i) put_f32(vout, (float)values[i]);
       return;
     }
     default:
@@ -1414,6 +1491,21 @@ static double* decode_values(const container_t* c, uint64_t count) { /* pipeline
         rn = count;
       }
       return value_decompress(&m, reorder, rn, count);
+    }
+    case GP_VALUE_QUANT:
+      return parse_dequantize(c->vp, c->vl, count);
+    case GP_VALUE_DEFLATE_SLOT: { /* byte_decompress (codecs.cpp:268-288) + pipeline.cpp:130-139 */
+      breader_t r = {c->vp, c->vl, 0};
+      const unsigned id = (unsigned)get_le(&r, 1);
+      const uint64_t raw_len = get_le(&r, 8);
+      const size_t body = r.n - r.pos;
+      if (id == 1) fail(GP_UNSUPPORTED, "oracle: the deflate byte codec is out of scope");
+      if (id != 0) fail(GP_UNKNOWN_METHOD, "byte_decompress: unknown codec id");
+      if (body != raw_len) fail(GP_CORRUPT_PAYLOAD, "store: length mismatch");
+      if (raw_len != 4 * count) fail(GP_CORRUPT_PAYLOAD, "pipeline: deflate slot length mismatch");
+      double* out = (double*)xalloc((count ? count : 1) * 8);
+      for (uint64_t i = 0; i < count; ++i) out[i] = (double)get_f32(&r);
+      return out;
     }
     default:
       fail(GP_UNSUPPORTED, "oracle: value method %d is out of scope", c->value_method);
@@ -1626,8 +1718,25 @@ int gpo_volume(const uint8_t* bytes, size_t len, gpo_volume_report* v) { /* cont
       if (c.vl < 9) fail(GP_CORRUPT_PAYLOAD, "container: deflate slot payload too short");
       v->value_bits = 8 * (c.vl - 9);
       break;
+    case GP_VALUE_QUANT: { /* container.cpp:213-225 */
+      if (c.index_method == GP_INDEX_BLOOM_P0) {
+        breader_t br = {c.ip, c.il, 0};
+        bloom_t f;
+        bloom_deserialize(&br, &f);
+        uint64_t np = 0;
+        positive_scan(&f, c.d, &np);  /* arena allocations, released on return */
+        value_count = np;
+      }
+      breader_t r = {c.vp, c.vl, 0};
+      const unsigned bits = (unsigned)get_le(&r, 1);
+      const uint32_t bucket = (uint32_t)get_le(&r, 4);
+      if (bits < 1 || bucket < 1) fail(GP_CORRUPT_PAYLOAD, "container: bad quant header");
+      const uint64_t nb = (value_count + bucket - 1) / bucket;
+      v->value_bits = 32 * nb + (uint64_t)bits * value_count;
+      break;
+    }
     default:
-      fail(GP_UNSUPPORTED, "oracle: quant volume is out of scope");
+      fail(GP_UNSUPPORTED, "oracle: value method %d is out of scope", c.value_method);
   }
   if (c.rl) {
     const unsigned width = reorder_entry_bits(c.d);

@@ -63,7 +63,10 @@ bool index_supported(int m) {
          m == GP_INDEX_BLOOM_P2 ||
          m == GP_INDEX_BLOOM_PD || m == GP_INDEX_BLOOM_NAIVE;
 }
-bool value_supported(int m) { return m == GP_VALUE_NONE || m == GP_VALUE_RAW_F64 || m == GP_VALUE_FIT_POLY; }
+bool value_supported(int m) {
+  return m == GP_VALUE_NONE || m == GP_VALUE_RAW_F64 || m == GP_VALUE_FIT_POLY || m == GP_VALUE_QUANT ||
+         m == GP_VALUE_DEFLATE_SLOT;
+}
 
 struct PlanInit {
   uint64_t d, r, il, n_values;
@@ -364,6 +367,13 @@ uint64_t gp_max_container_bytes(uint64_t d, uint64_t r, const gp_pipeline_config
       rl = (n * w + 7) / 8;
       break;
     }
+    case GP_VALUE_QUANT: {
+      const uint64_t bits = cfg->quant_bits < 1 ? 1 : (cfg->quant_bits > 16 ? 16 : cfg->quant_bits);
+      const uint64_t bucket = cfg->quant_bucket < 1 ? 1 : cfg->quant_bucket;
+      vl = 5 + 4 * ((n + bucket - 1) / bucket) + (n * bits + 7) / 8;
+      break;
+    }
+    case GP_VALUE_DEFLATE_SLOT: vl = 9 + 4 * n; break;
     default: vl = 4 * n; break;
   }
   return 49 + il + vl + rl + 4;
@@ -386,6 +396,14 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
   if (vm == GP_VALUE_FIT_POLY) {
     if (cfg->degree < 0 || cfg->degree > 60) return set_error(ctx, GP_ERROR, "value_compress: bad degree");
     if (cfg->degree > 7) return set_error(ctx, GP_UNSUPPORTED, "fit degree > 7 is not on the device path");
+  }
+  if (vm == GP_VALUE_QUANT) {
+    if (cfg->quant_bits < 1 || cfg->quant_bits > 16) return set_error(ctx, GP_ERROR, "quantize: bits out of range [1, 16]");
+    if (cfg->quant_bucket < 1) return set_error(ctx, GP_ERROR, "quantize: bucket must be >= 1");
+  }
+  if (vm == GP_VALUE_DEFLATE_SLOT) {
+    if (cfg->slot_codec == 1) return set_error(ctx, GP_UNSUPPORTED, "the deflate byte codec is not on the device path");
+    if (cfg->slot_codec != 0) return set_error(ctx, GP_UNKNOWN_METHOD, "byte_compress: unknown codec id");
   }
   const uint64_t bound = gp_max_container_bytes(d, r, cfg);
   if (cap < bound) return set_error(ctx, GP_CAPACITY, "encode: output capacity below gp_max_container_bytes");
@@ -447,6 +465,12 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
     case GP_VALUE_FIT_POLY:
       GP_STAGE(ctx, ST_VALUES, s, launch_values_fit(ctx, d_out, cfg->degree, cfg->max_segments, n_bound, s));
       break;
+    case GP_VALUE_QUANT:  // derive_quant_seed (pipeline.cpp:26)
+      GP_STAGE(ctx, ST_VALUES, s,
+               launch_values_quant(ctx, d_out, cfg->quant_bits, cfg->quant_bucket, gp::hash64(0xC, cfg->seed),
+                                   n_bound, s));
+      break;
+    case GP_VALUE_DEFLATE_SLOT: launch_values_slot(ctx, d_out, n_bound, s); break;
     default: break;
   }
   GP_STAGE(ctx, ST_PACK, s, launch_finish_container(ctx, d_out, cap, d_len, bound, s));
@@ -526,6 +550,8 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const u
     case GP_VALUE_NONE:
     case GP_VALUE_RAW_F64: launch_values_raw_check(ctx, s); break;
     case GP_VALUE_FIT_POLY: GP_STAGE(ctx, ST_DEC_VALUES, s, launch_decode_fit(ctx, d_in, bound, s)); break;
+    case GP_VALUE_QUANT: GP_STAGE(ctx, ST_DEC_VALUES, s, launch_decode_quant(ctx, d_in, bound, s)); break;
+    case GP_VALUE_DEFLATE_SLOT: launch_decode_slot(ctx, d_in, s); break;
     default: break;
   }
   if (im == GP_INDEX_NONE && !own) launch_validate_support(ctx, bound, s);

@@ -42,6 +42,7 @@ struct Plan {
   // ---- value codec
   uint32_t sign_split, identity;
   uint32_t nseg, degree;
+  uint32_t q_bits, q_bucket;    // quantizer header (decode)
   uint32_t seg_end[64];         // fit bounds (<= 64 segments on this path)
   float coeffs[64 * 8];
   // ---- decode
@@ -217,6 +218,11 @@ void launch_values_raw(gp_ctx* ctx, uint8_t* out, bool f64, uint64_t n_bound, cu
 void launch_values_raw_check(gp_ctx* ctx, cudaStream_t s);
 void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, uint64_t n_bound, cudaStream_t s);
 void launch_decode_fit(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, cudaStream_t s);
+void launch_values_quant(gp_ctx* ctx, uint8_t* out, int bits, uint32_t bucket, uint64_t seed, uint64_t n_bound,
+                         cudaStream_t s);                                                            // values_quant.cu
+void launch_decode_quant(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, cudaStream_t s);
+void launch_values_slot(gp_ctx* ctx, uint8_t* out, uint64_t n_bound, cudaStream_t s);
+void launch_decode_slot(gp_ctx* ctx, const uint8_t* in, cudaStream_t s);
 void launch_decode_scatter(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, float* dense, float scale,
                            uint32_t* out_support, double* out_values, uint64_t cap, uint64_t* d_count,
                            uint64_t* d_dim, cudaStream_t s);

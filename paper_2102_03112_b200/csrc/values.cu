@@ -48,13 +48,14 @@ __global__ void values_raw_check(Plan* plan, uint32_t* status) {
   const uint64_t n = plan->n_values;
   if (vm == GP_VALUE_NONE && plan->vl != 4 * n) latch(status, GP_CORRUPT_PAYLOAD);
   if (vm == GP_VALUE_RAW_F64 && plan->vl != 8 * n) latch(status, GP_CORRUPT_PAYLOAD);
-  if (vm == GP_VALUE_QUANT || vm == GP_VALUE_DEFLATE_SLOT || vm == GP_VALUE_FIT_DEXP) latch(status, GP_UNSUPPORTED);
+  if (vm == GP_VALUE_FIT_DEXP) latch(status, GP_UNSUPPORTED);
 }
 
 // value i of the decoded container: raw payload bytes or the fit evaluation
 __device__ __forceinline__ double value_at(const uint8_t* vp, uint8_t vm, const double* fitv, uint64_t i) {
   if (vm == GP_VALUE_NONE) return static_cast<double>(__uint_as_float(ld_u32_unaligned(vp + 4 * i)));
   if (vm == GP_VALUE_RAW_F64) return __longlong_as_double(static_cast<long long>(ld_u64_unaligned(vp + 8 * i)));
+  if (vm == GP_VALUE_DEFLATE_SLOT) return static_cast<double>(__uint_as_float(ld_u32_unaligned(vp + 9 + 4 * i)));
   return fitv[i];
 }
 

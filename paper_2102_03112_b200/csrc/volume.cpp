@@ -80,6 +80,18 @@ extern "C" GP_API int gp_volume(const uint8_t* h, uint64_t len, gp_volume_report
       count = last;
       break;
     }
+    case GP_VALUE_QUANT: {  // container.cpp:213-225
+      // with Bloom-P0 indices the value count is |P|, which needs the full
+      // positive scan: out of this host-side header accounting
+      if (im == GP_INDEX_BLOOM_P0) return GP_UNSUPPORTED;
+      if (vl < 1) return GP_TRUNCATED;
+      const uint8_t bits = vp[0];
+      if (vl < 5) return GP_TRUNCATED;
+      const uint32_t bucket = rd32(vp + 1);
+      if (bits < 1 || bucket < 1) return GP_CORRUPT_PAYLOAD;
+      out->value_bits = 32 * ((count + bucket - 1) / bucket) + static_cast<uint64_t>(bits) * count;
+      break;
+    }
     case GP_VALUE_DEFLATE_SLOT:
       if (vl < 9) return GP_CORRUPT_PAYLOAD;
       out->value_bits = 8 * (vl - 9);

@@ -45,13 +45,15 @@ def test_library_is_sm100a():
     assert "sm_100a" in out
 
 
-@pytest.mark.parametrize("im,vm", [(0, 0), (1, 0), (2, 0), (4, 1), (5, 5), (6, 1), (7, 0), (8, 1), (1, 1)])
-def test_volume_matches_reference(oracle, reference, im, vm):
+@pytest.mark.parametrize("im,vm,kw", [(0, 0, {}), (1, 0, {}), (2, 0, {}), (4, 1, {}), (5, 5, {}), (6, 1, {}),
+                                      (7, 0, {}), (8, 1, {}), (1, 1, {}), (1, 3, {}), (6, 3, dict(quant_bits=3)),
+                                      (2, 3, dict(quant_bits=16, quant_bucket=7)), (6, 4, dict(slot_codec=0))])
+def test_volume_matches_reference(oracle, reference, im, vm, kw):
     # gp_volume is host code: it runs here, against the reference's own volume()
     from oracle.bindings import GpConfig as OC, synthetic_gradient
     from paper_2102_03112_b200 import volume
     g = synthetic_gradient(20_000, rank=im)
-    c = oracle.encode_dense(g, 200, OC.make(im, vm, fpr=0.01, seed=5))
+    c = oracle.encode_dense(g, 200, OC.make(im, vm, fpr=0.01, seed=5, **kw))
     got, want = volume(c), reference.volume(c)
     for k in want:
         assert got[k] == pytest.approx(want[k], rel=0, abs=0), k

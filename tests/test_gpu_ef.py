@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 NONE, BITMAP, RLE, P0, P1, P2, PD, NAIVE = 0, 1, 2, 4, 5, 6, 7, 8
 V_NONE, V_FIT, V_F64 = 0, 1, 5
 CASES = [(BITMAP, V_NONE), (RLE, V_NONE), (NONE, V_F64), (BITMAP, V_FIT), (P0, V_FIT), (P1, V_NONE),
-         (P2, V_FIT), (P2, V_NONE), (PD, V_NONE), (NAIVE, V_NONE), (NAIVE, V_FIT)]
+         (P2, V_FIT), (P2, V_NONE), (PD, V_NONE), (NAIVE, V_NONE), (NAIVE, V_FIT), (BITMAP, 3), (P2, 3), (RLE, 4)]
 
 
 @pytest.fixture(scope="module")
@@ -33,8 +33,9 @@ def codec():
 def test_ef_steps_bit_exact(codec, oracle, im, vm):
     from paper_2102_03112_b200 import PipelineConfig
     d, r = 200_003, 2_000
-    cfg = PipelineConfig(index_method=im, value_method=vm, fpr=0.01, seed=21)
-    ocfg = GpConfig.make(im, vm, fpr=0.01, seed=21)
+    kw = dict(slot_codec=0) if vm == 4 else {}
+    cfg = PipelineConfig(index_method=im, value_method=vm, fpr=0.01, seed=21, **kw)
+    ocfg = GpConfig.make(im, vm, fpr=0.01, seed=21, **kw)
     e = torch.zeros(d, dtype=torch.float32, device="cuda")
     for step in range(3):
         g = synthetic_gradient(d, rank=step + 1)

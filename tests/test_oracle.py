@@ -231,3 +231,55 @@ def test_value_codec_matches_reference(oracle, reference):
         co = np.frombuffer(fo[4 + 4 * segs:-4], "<f4")
         cr = np.frombuffer(fr[4 + 4 * segs:-4], "<f4")
         assert np.allclose(co, cr, rtol=1e-5, atol=1e-6 * np.abs(cr).max())
+
+
+QUANT_CASES = [(3, dict(quant_bits=7, quant_bucket=512)), (3, dict(quant_bits=1, quant_bucket=1)),
+               (3, dict(quant_bits=16, quant_bucket=3)), (3, dict(quant_bits=5, quant_bucket=100)),
+               (4, dict(slot_codec=0))]
+
+
+@pytest.mark.parametrize("im", [0, 1, 2, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("vm,kw", QUANT_CASES)
+def test_quant_and_store_slot_match_reference(oracle, im, vm, kw):
+    """Quantizer (codecs.cpp:290-368) and the Store byte-codec slot
+    (codecs.cpp:244-288): containers and decodes byte-identical to the
+    reference build, including zero buckets (no draws) and 1-bit codes."""
+    from oracle.bindings import GpConfig, reference, synthetic_gradient
+    ref = reference()
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    d, r = 20_000, 300
+    g = synthetic_gradient(d, rank=im)
+    g[:5000] = 0.0  # all-zero buckets when the support reaches them
+    cfg = GpConfig.make(im, vm, seed=9, **kw)
+    a, b = oracle.encode_dense(g, r, cfg), ref.encode_dense(g, r, cfg)
+    assert a == b
+    _, sa, va = oracle.decode(a)
+    _, sb, vb = ref.decode(b)
+    assert np.array_equal(sa, sb) and np.array_equal(va, vb)
+
+
+def test_quant_decode_errors_match_reference(oracle):
+    from oracle.bindings import GpConfig, OracleError, reference, synthetic_gradient
+    ref = reference()
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    g = synthetic_gradient(5_000, rank=1)
+    for vm, kw in QUANT_CASES:
+        c = bytearray(oracle.encode_dense(g, 50, GpConfig.make(1, vm, seed=2, **kw)))
+        il = int.from_bytes(c[25:33], "little")
+        vo = 49 + il
+        muts = [bytes(c[:vo]) + bytes([0]) + bytes(c[vo + 1:]), bytes(c[:vo]) + bytes([17]) + bytes(c[vo + 1:]),
+                bytes(c[:vo]) + bytes([9]) + bytes(c[vo + 1:]), bytes(c[:vo + 1]) + bytes(4) + bytes(c[vo + 5:])]
+        for m in muts:
+            m = bytearray(m)
+            m[-4:] = oracle.crc32c(bytes(m[49:-4])).to_bytes(4, "little")  # valid CRC: reach the payload checks
+            m = bytes(m)
+            outs = []
+            for cod in (oracle, ref):
+                try:
+                    cod.decode(m)
+                    outs.append("ok")
+                except OracleError as e:
+                    outs.append(e.code)
+            assert outs[0] == outs[1], (vm, kw, outs)
