@@ -241,7 +241,8 @@ def native_main(args, cfg):
         r_total = sum(ex.rs)
     else:
         codec = Codec(max_d=d, device=local)
-        ex = SparseAllgather(codec, d, r, pcfg, ef=cfg.get("ef", False))
+        # N = 1: the step is one CUDA graph (replayed per step with the step's seed)
+        ex = SparseAllgather(codec, d, r, pcfg, ef=cfg.get("ef", False), graph=(world == 1 and not args.no_graph))
         codecs = [codec]
         r_total = r
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
@@ -278,6 +279,9 @@ def native_main(args, cfg):
         wall = time.perf_counter() - wall0
     status()
     n_launch = (launches() - launches0) // max(1, args.steps)
+    graphed = bool(getattr(ex, "graph", False))
+    if graphed:  # replays enqueue no host launches: the captured kernel count per step
+        n_launch = ex.kernels_per_step
     step_ms = [a.elapsed_time(b) for a, b in evs]
     t_ms = float(sum(step_ms)) / args.steps
     if world > 1:
@@ -290,7 +294,9 @@ def native_main(args, cfg):
     else:
         length = int(ex.length.item())
 
-    # ---- profiled pass (same steps): per-stage CUDA events on the launch stream
+    # ---- profiled pass (same steps, eager: stage events need host launches)
+    if graphed:
+        ex.graph = False
     for c in codecs:
         c.profile(True)
     stage = {}
@@ -304,6 +310,7 @@ def native_main(args, cfg):
                 a[1] += n
     for c in codecs:
         c.profile(False)
+    ex.graph = graphed
     prof_total = sum(v[0] for v in stage.values()) / args.steps
 
     # ---- e2e: host gradient in, host dense mean out, through the public API
@@ -385,7 +392,7 @@ def native_main(args, cfg):
         "roofline": roof, "step_roofline": step_roof,
         "stages_ms_per_step": {k: round(v[0] / args.steps, 5) for k, v in sorted(stage.items())},
         "profiled_ms_per_step": round(prof_total, 4),
-        "gpu_launches": int(n_launch), "clocks": clocks, "wall_s_timed": round(wall, 4),
+        "gpu_launches": int(n_launch), "cuda_graph": graphed, "clocks": clocks, "wall_s_timed": round(wall, 4),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         gbs, sec, desc, kind, _ = run_cpu_sample(cfg, 1, cfg.get("buckets", 1), 1)
@@ -407,6 +414,7 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--ref-shrink", type=int, default=8, help="reference arm: d/shrink-element sample per thread")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="N = 1: launch the step eagerly instead of as a CUDA graph")
     ap.add_argument("--streams", type=int, default=8, help="bucketed configs: codec contexts / CUDA streams")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]

@@ -96,6 +96,18 @@ GP_API const char* gp_stage_name(int stage);
  * r kept (container.cpp:58-82 layout).  Host-only arithmetic. */
 GP_API uint64_t gp_max_container_bytes(uint64_t d, uint64_t r, const gp_pipeline_config* cfg);
 
+/* Seed source for CUDA-graph replay.  With a non-null d_seed, every encode on
+ * this context reads its pipeline seed from the device word *d_seed when the
+ * step executes (cfg->seed is ignored), so one captured step replays with a
+ * new seed per step.  NULL restores cfg->seed.  Host-only bookkeeping. */
+GP_API int gp_ctx_set_seed_source(gp_ctx* ctx, const uint64_t* d_seed);
+
+/* *d_seed = Simulation::pipeline_seed(seed, worker, *d_step) (harness.cpp:201-203)
+ * computed on the device (one tiny kernel on `stream`): the per-(worker, step)
+ * seed of the DP loop without a host round trip. */
+GP_API int gp_pipeline_seed_device(uint64_t* d_seed, const uint64_t* d_step, uint64_t seed, uint32_t worker,
+                                   void* stream);
+
 /* ---------------------------------------------------------------- encode */
 /* top_r (sparsify.cpp:32-46) + compress_gradient(sg, cfg, &dense)
  * (pipeline.cpp:146-221) + pack (container.cpp:58-82), fused.

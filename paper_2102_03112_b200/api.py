@@ -190,6 +190,14 @@ class Codec:
                 out[name.decode()] = (ms[i], int(cnt[i]))
         return out
 
+    def set_seed_source(self, seed: torch.Tensor | None):
+        """Read every encode's pipeline seed from the device word ``seed`` (int64,
+        1 element) when the step executes — the hook that lets a captured CUDA
+        graph replay with a new seed per step.  None restores cfg.seed."""
+        if seed is not None:
+            assert seed.dtype == torch.int64 and seed.is_cuda and seed.numel() >= 1
+        self._raise(lib.gp_ctx_set_seed_source(self._ctx, _ptr(seed)))
+
     # -------------------------------------------------------------- encode
     @staticmethod
     def max_container_bytes(d: int, r: int, cfg: PipelineConfig) -> int:
@@ -315,6 +323,15 @@ class Codec:
                                         _stream()))
         self.status()
         return out
+
+
+def pipeline_seed_device(seed_out: torch.Tensor, step: torch.Tensor, seed: int, worker: int, stream=None):
+    """seed_out[0] = Simulation::pipeline_seed(seed, worker, step[0]) on the device
+    (harness.cpp:201-203), enqueued on ``stream``."""
+    rc = lib.gp_pipeline_seed_device(_ptr(seed_out), _ptr(step), int(seed) & 0xFFFFFFFFFFFFFFFF, int(worker),
+                                     _stream(stream))
+    if rc != 0:
+        raise _STATUS.get(rc, Error)("gp_pipeline_seed_device failed")
 
 
 def volume(container: bytes) -> dict:

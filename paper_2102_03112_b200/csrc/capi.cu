@@ -71,6 +71,8 @@ bool value_supported(int m) {
 struct PlanInit {
   uint64_t d, r, il, n_values;
   uint64_t m, seed_a, seed_b, minv;
+  uint64_t seed;
+  const uint64_t* seed_dev;  // non-null: the pipeline seed is read here at execution time
   uint32_t k;
   uint8_t index_method, value_method, pd_variant;
 };
@@ -92,9 +94,20 @@ __global__ void init_plan(Plan* plan, PlanInit p) {
   plan->off_reorder = 49 + p.il;
   plan->m = p.m;
   plan->k = p.k;
-  plan->seed_a = p.seed_a;
-  plan->seed_b = p.seed_b;
+  // derive_filter_seed_a/b (pipeline.cpp:21-22) from the pipeline seed, on
+  // the device so a captured graph can replay with a new seed per step
+  const uint64_t seed = p.seed_dev ? *p.seed_dev : p.seed;
+  plan->seed = seed;
+  plan->seed_a = hash64(0xA, seed);
+  plan->seed_b = hash64(0xB, seed);
   plan->minv = p.minv;
+}
+
+// Simulation::pipeline_seed(seed, worker, *step) (harness.cpp:201-203, over
+// Problem::batch_seed :47-51) into *seed_out, on the device.
+__global__ void pipeline_seed_kernel(uint64_t* seed_out, const uint64_t* step, uint64_t seed, uint32_t worker) {
+  const uint64_t key = (static_cast<uint64_t>(worker) << 32) | (*step & 0xFFFFFFFFULL);
+  *seed_out = hash64(0xC0DEC, hash64(key, hash64(0xDA7A, seed)));
 }
 
 // compress_gradient's validate(sg) (gradient.cpp:19-30) + gather(dense, support)
@@ -265,6 +278,19 @@ void gp_ctx_destroy(gp_ctx* ctx) {
   delete ctx;
 }
 
+int gp_ctx_set_seed_source(gp_ctx* ctx, const uint64_t* d_seed) {
+  if (!ctx) return GP_ERROR;
+  ctx->seed_dev = d_seed;
+  return GP_OK;
+}
+
+int gp_pipeline_seed_device(uint64_t* d_seed, const uint64_t* d_step, uint64_t seed, uint32_t worker,
+                            void* stream) {
+  if (!d_seed || !d_step) return GP_ERROR;
+  pipeline_seed_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(d_seed, d_step, seed, worker);
+  return cudaGetLastError() == cudaSuccess ? GP_OK : GP_CUDA;
+}
+
 const char* gp_last_error(const gp_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "null context"; }
 
 uint64_t gp_ctx_launch_count(const gp_ctx* ctx) { return ctx ? ctx->launches : 0; }
@@ -425,13 +451,13 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
     if (im == GP_INDEX_BLOOM_PD && cfg->pd_variant > 2) return set_error(ctx, GP_ERROR, "pd_select: unknown variant");
     pi.m = m;
     pi.k = k;
-    pi.seed_a = gp::hash64(0xA, cfg->seed);  // derive_filter_seed_a, pipeline.cpp:21
-    pi.seed_b = gp::hash64(0xB, cfg->seed);  // derive_filter_seed_b, pipeline.cpp:22
     pi.minv = ~0ULL / m;
     pi.il = 26 + (m + 7) / 8 + (im == GP_INDEX_BLOOM_PD ? 1 : 0);
   } else {
     pi.il = im == GP_INDEX_NONE ? 4 * r : (d + 7) / 8;
   }
+  pi.seed = cfg->seed;
+  pi.seed_dev = ctx->seed_dev;
   GP_LAUNCH(ctx, init_plan, 1, 1, 0, s, ctx->ws.plan, pi);
 
   if (d_support) {
@@ -467,8 +493,7 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
       break;
     case GP_VALUE_QUANT:  // derive_quant_seed (pipeline.cpp:26)
       GP_STAGE(ctx, ST_VALUES, s,
-               launch_values_quant(ctx, d_out, cfg->quant_bits, cfg->quant_bucket, gp::hash64(0xC, cfg->seed),
-                                   n_bound, s));
+               launch_values_quant(ctx, d_out, cfg->quant_bits, cfg->quant_bucket, n_bound, s));
       break;
     case GP_VALUE_DEFLATE_SLOT: launch_values_slot(ctx, d_out, n_bound, s); break;
     default: break;
@@ -628,7 +653,7 @@ static int bloom_component(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter
   pi.il = filter_len;
   pi.index_method = static_cast<uint8_t>(method);
   pi.value_method = GP_VALUE_NONE;
-  GP_LAUNCH(ctx, init_plan, 1, 1, 0, s, ctx->ws.plan, pi);
+  GP_LAUNCH(ctx, init_plan, 1, 1, 0, s, ctx->ws.plan, pi);  // the filter seeds come from its payload
   GP_LAUNCH(ctx, component_offsets, 1, 1, 0, s, ctx->ws.plan);
   launch_bloom_parse(ctx, d_filter, ctx->ws.m_cap, s);
   launch_bloom_scan(ctx, d, 0, false, s);

@@ -34,6 +34,7 @@ struct Plan {
   uint64_t above, n_cand;       // keys in bins above bin_star; candidates emitted
   // ---- bloom
   uint64_t m, seed_a, seed_b, minv;
+  uint64_t seed;                // the pipeline seed of this encode
   uint32_t k, pad1;
   uint64_t n_pos;               // |P|
   uint64_t n_pairs, n_sets, n_multi, n_single_sel;
@@ -140,6 +141,7 @@ struct gp_ctx {
   std::string last_error;
   uint64_t launches = 0;
   gp::Profiler prof;
+  const uint64_t* seed_dev = nullptr;  // gp_ctx_set_seed_source: pipeline seed read on the device
 };
 
 namespace gp {
@@ -218,7 +220,7 @@ void launch_values_raw(gp_ctx* ctx, uint8_t* out, bool f64, uint64_t n_bound, cu
 void launch_values_raw_check(gp_ctx* ctx, cudaStream_t s);
 void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, uint64_t n_bound, cudaStream_t s);
 void launch_decode_fit(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, cudaStream_t s);
-void launch_values_quant(gp_ctx* ctx, uint8_t* out, int bits, uint32_t bucket, uint64_t seed, uint64_t n_bound,
+void launch_values_quant(gp_ctx* ctx, uint8_t* out, int bits, uint32_t bucket, uint64_t n_bound,
                          cudaStream_t s);                                                            // values_quant.cu
 void launch_decode_quant(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, cudaStream_t s);
 void launch_values_slot(gp_ctx* ctx, uint8_t* out, uint64_t n_bound, cudaStream_t s);

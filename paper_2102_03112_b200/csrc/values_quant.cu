@@ -66,13 +66,14 @@ __global__ void __launch_bounds__(1024) quant_zscan(const Plan* plan, uint32_t b
 }
 
 __global__ void quant_codes(const float* __restrict__ values, const Plan* plan, const uint8_t* __restrict__ out,
-                            uint32_t bits, uint32_t bucket, uint64_t seed, const uint32_t* __restrict__ zbefore,
+                            uint32_t bits, uint32_t bucket, const uint32_t* __restrict__ zbefore,
                             uint32_t* __restrict__ codes, const uint32_t* status) {
   if (failed(status)) return;
   const uint64_t n = plan->n_values;
   const uint8_t* sp = out + 49 + plan->il + 5;
   const uint64_t levels = (1ull << bits) - 1;
   const double lv = static_cast<double>(levels);
+  const uint64_t seed = hash64(0xC, plan->seed);  // derive_quant_seed (pipeline.cpp:26)
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t b = i / bucket;
@@ -196,15 +197,14 @@ __global__ void slot_parse(const uint8_t* __restrict__ in, const Plan* plan, uin
 
 }  // namespace
 
-void launch_values_quant(gp_ctx* ctx, uint8_t* out, int bits, uint32_t bucket, uint64_t seed, uint64_t n_bound,
-                         cudaStream_t s) {
+void launch_values_quant(gp_ctx* ctx, uint8_t* out, int bits, uint32_t bucket, uint64_t n_bound, cudaStream_t s) {
   Workspace& w = ctx->ws;
   const uint64_t nb_bound = (n_bound + bucket - 1) / bucket;
   GP_LAUNCH(ctx, quant_scales, grid_for(ctx, nb_bound * 32, 256), 256, 0, s, w.values, w.plan, out, bucket, w.u32b,
             w.status);
   GP_LAUNCH(ctx, quant_zscan, 1, 1024, 0, s, w.plan, bucket, w.u32b, w.status);
   GP_LAUNCH(ctx, quant_codes, grid_for(ctx, n_bound, 256), 256, 0, s, w.values, w.plan, out,
-            static_cast<uint32_t>(bits), bucket, seed, w.u32b, w.u32a, w.status);
+            static_cast<uint32_t>(bits), bucket, w.u32b, w.u32a, w.status);
   GP_LAUNCH(ctx, quant_pack, grid_for(ctx, (n_bound * bits + 7) / 8, 256), 256, 0, s, w.u32a, w.plan, out,
             static_cast<uint32_t>(bits), bucket, w.status);
 }

@@ -72,7 +72,8 @@ class SparseAllgather:
     harness.cpp:230, :269-271): the rank encodes g + residual and keeps
     input - decode(own container) as the next step's residual."""
 
-    def __init__(self, codec, d: int, r: int, cfg, group=None, device=None, ef: bool = False):
+    def __init__(self, codec, d: int, r: int, cfg, group=None, device=None, ef: bool = False,
+                 graph: bool = False):
         self.codec = codec
         self.d, self.r, self.cfg = d, r, cfg
         self.group = group
@@ -85,11 +86,56 @@ class SparseAllgather:
         self.recv = torch.empty(self.world * self.cap, dtype=torch.uint8, device=dev) if self.world > 1 else None
         self.dense = torch.zeros(d, dtype=torch.float32, device=dev)
         self.residual = torch.zeros(d, dtype=torch.float32, device=dev) if ef else None
+        # graph=True (one rank, CUDA): the whole step — pipeline seed from a device
+        # step counter, encode, zero, decode — is captured once per (input,
+        # output, base seed) and replayed; the step number is the only host input
+        # (one fill of the counter before each replay).
+        self.graph = bool(graph) and self.world == 1 and torch.device(dev).type == "cuda"
+        self.graphs = {}
+        self.kernels_per_step = None
+        if self.graph:
+            self.step_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+            self.seed_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def _captured(self, grad, out_dense, seed):
+        from .api import pipeline_seed_device
+        key = (grad.data_ptr(), out_dense.data_ptr(), seed)
+        g = self.graphs.get(key)
+        if g is None:
+            if len(self.graphs) >= 8:  # callers should reuse buffers; bound the cache anyway
+                self.graphs.pop(next(iter(self.graphs)))
+            torch.cuda.synchronize()
+            self.codec.set_seed_source(self.seed_dev)
+            try:
+                # one warm step outside the capture (one-time kernel attributes, tables);
+                # the error-feedback residual is restored so the warm step leaves no trace
+                keep = self.residual.clone() if self.residual is not None else None
+                self.step_seeded(grad, self.cfg, dense=out_dense)
+                if keep is not None:
+                    self.residual.copy_(keep)
+                torch.cuda.synchronize()
+                n0 = self.codec.launches
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    s = torch.cuda.current_stream()
+                    pipeline_seed_device(self.seed_dev, self.step_dev, seed, self.rank, stream=s)
+                    self.step_seeded(grad, self.cfg, dense=out_dense, stream=s)
+                self.kernels_per_step = self.codec.launches - n0 + 1
+            finally:
+                self.codec.set_seed_source(None)
+            self.graphs[key] = g
+        return g
 
     def step(self, grad: torch.Tensor, step: int, seed: int = 1, dense: torch.Tensor | None = None,
              stream=None) -> torch.Tensor:
         """Dense mean of every rank's decoded container (accumulated into `dense`
         or the exchanger's own buffer)."""
+        if self.graph and stream is None:
+            out_dense = self.dense if dense is None else dense
+            g = self._captured(grad, out_dense, seed)
+            self.step_dev.fill_(step)
+            g.replay()
+            return out_dense
         cfg = replace(self.cfg, seed=pipeline_seed(seed, self.rank, step))
         return self.step_seeded(grad, cfg, dense=dense, stream=stream)
 
