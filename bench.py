@@ -236,7 +236,8 @@ def native_main(args, cfg):
                           degree=cfg["degree"], max_segments=cfg["max_segments"])
     if cfg.get("buckets"):
         ex = BucketedSparseAllgather(lambda dmax: Codec(max_d=dmax, device=local), d, cfg["ratio"], pcfg,
-                                     cfg["buckets"], streams=args.streams, ef=cfg.get("ef", False))
+                                     cfg["buckets"], streams=args.streams, ef=cfg.get("ef", False),
+                                     graph=(world == 1 and not args.no_graph))
         codecs = ex.codecs
         r_total = sum(ex.rs)
     else:

@@ -102,11 +102,13 @@ GP_API uint64_t gp_max_container_bytes(uint64_t d, uint64_t r, const gp_pipeline
  * new seed per step.  NULL restores cfg->seed.  Host-only bookkeeping. */
 GP_API int gp_ctx_set_seed_source(gp_ctx* ctx, const uint64_t* d_seed);
 
-/* *d_seed = Simulation::pipeline_seed(seed, worker, *d_step) (harness.cpp:201-203)
- * computed on the device (one tiny kernel on `stream`): the per-(worker, step)
- * seed of the DP loop without a host round trip. */
+/* d_seed[0] = Simulation::pipeline_seed(seed, worker, *d_step)
+ * (harness.cpp:201-203) computed on the device (one tiny kernel on `stream`):
+ * the per-(worker, step) seed of the DP loop without a host round trip.  With
+ * buckets > 0, d_seed[b] = hash64(b, that seed) for b < buckets (the bucketed
+ * step's per-bucket seeds). */
 GP_API int gp_pipeline_seed_device(uint64_t* d_seed, const uint64_t* d_step, uint64_t seed, uint32_t worker,
-                                   void* stream);
+                                   uint32_t buckets, void* stream);
 
 /* ---------------------------------------------------------------- encode */
 /* top_r (sparsify.cpp:32-46) + compress_gradient(sg, cfg, &dense)

@@ -57,7 +57,7 @@ _SIGS = {
     "gp_max_container_bytes": ([_u64, _u64, _P(GpConfig)], _u64),
     "gp_encode_topr": ([_vp, _vp, _u64, _u64, _P(GpConfig), _vp, _u64, _vp, _vp], C.c_int),
     "gp_ctx_set_seed_source": ([_vp, _vp], C.c_int),
-    "gp_pipeline_seed_device": ([_vp, _vp, _u64, C.c_uint32, _vp], C.c_int),
+    "gp_pipeline_seed_device": ([_vp, _vp, _u64, C.c_uint32, C.c_uint32, _vp], C.c_int),
     "gp_encode_topr_ef": ([_vp, _vp, _vp, _u64, _u64, _P(GpConfig), _vp, _u64, _vp, _vp], C.c_int),
     "gp_encode_support": ([_vp, _vp, _u64, _vp, _u64, _P(GpConfig), _vp, _u64, _vp, _vp], C.c_int),
     "gp_decode_accumulate": ([_vp, _vp, _u64, _vp, _u64, C.c_float, _vp], C.c_int),

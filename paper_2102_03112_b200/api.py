@@ -325,11 +325,14 @@ class Codec:
         return out
 
 
-def pipeline_seed_device(seed_out: torch.Tensor, step: torch.Tensor, seed: int, worker: int, stream=None):
+def pipeline_seed_device(seed_out: torch.Tensor, step: torch.Tensor, seed: int, worker: int, buckets: int = 0,
+                         stream=None):
     """seed_out[0] = Simulation::pipeline_seed(seed, worker, step[0]) on the device
-    (harness.cpp:201-203), enqueued on ``stream``."""
+    (harness.cpp:201-203), enqueued on ``stream``; with buckets > 0,
+    seed_out[b] = hash64(b, that seed) for every bucket."""
+    assert seed_out.numel() >= max(1, buckets)
     rc = lib.gp_pipeline_seed_device(_ptr(seed_out), _ptr(step), int(seed) & 0xFFFFFFFFFFFFFFFF, int(worker),
-                                     _stream(stream))
+                                     int(buckets), _stream(stream))
     if rc != 0:
         raise _STATUS.get(rc, Error)("gp_pipeline_seed_device failed")
 

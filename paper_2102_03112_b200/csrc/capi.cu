@@ -104,10 +104,17 @@ __global__ void init_plan(Plan* plan, PlanInit p) {
 }
 
 // Simulation::pipeline_seed(seed, worker, *step) (harness.cpp:201-203, over
-// Problem::batch_seed :47-51) into *seed_out, on the device.
-__global__ void pipeline_seed_kernel(uint64_t* seed_out, const uint64_t* step, uint64_t seed, uint32_t worker) {
+// Problem::batch_seed :47-51) into seed_out[0], on the device; with buckets,
+// seed_out[b] = hash64(b, that seed) (the bucketed convention of dp.py).
+__global__ void pipeline_seed_kernel(uint64_t* seed_out, const uint64_t* step, uint64_t seed, uint32_t worker,
+                                     uint32_t buckets) {
   const uint64_t key = (static_cast<uint64_t>(worker) << 32) | (*step & 0xFFFFFFFFULL);
-  *seed_out = hash64(0xC0DEC, hash64(key, hash64(0xDA7A, seed)));
+  const uint64_t ps = hash64(0xC0DEC, hash64(key, hash64(0xDA7A, seed)));
+  if (buckets == 0) {
+    if (threadIdx.x == 0) *seed_out = ps;
+    return;
+  }
+  for (uint32_t b = threadIdx.x; b < buckets; b += blockDim.x) seed_out[b] = hash64(b, ps);
 }
 
 // compress_gradient's validate(sg) (gradient.cpp:19-30) + gather(dense, support)
@@ -285,9 +292,9 @@ int gp_ctx_set_seed_source(gp_ctx* ctx, const uint64_t* d_seed) {
 }
 
 int gp_pipeline_seed_device(uint64_t* d_seed, const uint64_t* d_step, uint64_t seed, uint32_t worker,
-                            void* stream) {
+                            uint32_t buckets, void* stream) {
   if (!d_seed || !d_step) return GP_ERROR;
-  pipeline_seed_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(d_seed, d_step, seed, worker);
+  pipeline_seed_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(d_seed, d_step, seed, worker, buckets);
   return cudaGetLastError() == cudaSuccess ? GP_OK : GP_CUDA;
 }
 

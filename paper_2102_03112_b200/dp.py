@@ -165,7 +165,7 @@ class BucketedSparseAllgather:
     """Bucketed DP step for gradients too large for one container (C5)."""
 
     def __init__(self, codec_factory, d: int, ratio: float, cfg, buckets: int, streams: int = 3, group=None,
-                 device=None, ef: bool = False):
+                 device=None, ef: bool = False, graph: bool = False):
         self.d, self.cfg, self.buckets = d, cfg, buckets
         self.world, self.rank = _world(group)
         base, rem = divmod(d, buckets)
@@ -185,12 +185,60 @@ class BucketedSparseAllgather:
                                    device=device, ef=ef) for i, (s, e) in enumerate(self.bounds)]
         dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.dense = torch.zeros(d, dtype=torch.float32, device=dev)
+        # graph=True (one rank): the whole multi-stream step is one CUDA graph;
+        # per-bucket seeds come from the device (gp_pipeline_seed_device)
+        self.graph = bool(graph) and self.world == 1 and cuda
+        self.graphs = {}
+        self.kernels_per_step = None
+        if self.graph:
+            self.step_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+            self.seeds_dev = torch.zeros(buckets, dtype=torch.int64, device=dev)
 
     def bucket_seed(self, seed: int, step: int, b: int) -> int:
         return hash64(b, pipeline_seed(seed, self.rank, step))
 
+    def _captured(self, grad, out_dense, seed):
+        from .api import pipeline_seed_device
+        key = (grad.data_ptr(), out_dense.data_ptr(), seed)
+        g = self.graphs.get(key)
+        if g is not None:
+            return g
+        if len(self.graphs) >= 8:
+            self.graphs.pop(next(iter(self.graphs)))
+        torch.cuda.synchronize()
+        keep = [e.residual.clone() if e.residual is not None else None for e in self.ex]
+        self._run(grad, out_dense, lambda b: self.cfg)  # warm outside the capture
+        for e, k in zip(self.ex, keep):
+            if k is not None:
+                e.residual.copy_(k)
+        torch.cuda.synchronize()
+        n0 = sum(c.launches for c in self.codecs)
+        g = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.graph(g):
+                pipeline_seed_device(self.seeds_dev, self.step_dev, seed, self.rank, buckets=self.buckets)
+
+                def seeded(b):  # the captured init_plan of bucket b reads seeds_dev[b]
+                    self.ex[b].codec.set_seed_source(self.seeds_dev[b:b + 1])
+                    return self.cfg
+                self._run(grad, out_dense, seeded)
+        finally:
+            for c in self.codecs:
+                c.set_seed_source(None)
+        self.kernels_per_step = sum(c.launches for c in self.codecs) - n0 + 1
+        self.graphs[key] = g
+        return g
+
     def step(self, grad: torch.Tensor, step: int, seed: int = 1, dense: torch.Tensor | None = None) -> torch.Tensor:
         out_dense = self.dense if dense is None else dense
+        if self.graph:
+            g = self._captured(grad, out_dense, seed)
+            self.step_dev.fill_(step)
+            g.replay()
+            return out_dense
+        return self._run(grad, out_dense, lambda b: replace(self.cfg, seed=self.bucket_seed(seed, step, b)))
+
+    def _run(self, grad, out_dense, cfg_of):
         cur = torch.cuda.current_stream() if self.streams[0] is not None else None
         if cur is not None:
             for s in self.streams:
@@ -198,12 +246,11 @@ class BucketedSparseAllgather:
         for b, (lo, hi) in enumerate(self.bounds):
             si = b % self.nstreams
             s = self.streams[si]
-            cfg = replace(self.cfg, seed=self.bucket_seed(seed, step, b))
             if s is not None:
                 with torch.cuda.stream(s):
-                    self.ex[b].step_seeded(grad[lo:hi], cfg, dense=out_dense[lo:hi], stream=s)
+                    self.ex[b].step_seeded(grad[lo:hi], cfg_of(b), dense=out_dense[lo:hi], stream=s)
             else:
-                self.ex[b].step_seeded(grad[lo:hi], cfg, dense=out_dense[lo:hi])
+                self.ex[b].step_seeded(grad[lo:hi], cfg_of(b), dense=out_dense[lo:hi])
         if cur is not None:
             for s in self.streams:
                 cur.wait_stream(s)

@@ -67,3 +67,29 @@ def test_host_pipeline_over_graphs():
     assert len(graph.graphs) == 2  # one per double-buffer slot
     ca.close()
     cb.close()
+
+
+@pytest.mark.parametrize("ef", [False, True])
+def test_bucketed_graph_equals_eager(ef):
+    from paper_2102_03112_b200 import Codec, PipelineConfig
+    from paper_2102_03112_b200.dp import BucketedSparseAllgather
+    d, ratio, buckets = 800_003, 0.005, 5
+    cfg = PipelineConfig(index_method=6, value_method=1, fpr=0.001, max_segments=8)
+    eager = BucketedSparseAllgather(lambda dm: Codec(max_d=dm), d, ratio, cfg, buckets, streams=3, ef=ef)
+    graph = BucketedSparseAllgather(lambda dm: Codec(max_d=dm), d, ratio, cfg, buckets, streams=3, ef=ef, graph=True)
+    assert graph.graph
+    g = torch.empty(d, dtype=torch.float32, device="cuda")
+    for step in [2, 3, 7]:
+        g.copy_(torch.from_numpy(synthetic_gradient(d, rank=step)))
+        want = eager.step(g, step=step).clone()
+        got = graph.step(g, step=step).clone()
+        torch.cuda.synchronize()
+        for c in eager.codecs + graph.codecs:
+            c.status()
+        for ea, eb in zip(eager.ex, graph.ex):
+            n = int(ea.length.item())
+            assert int(eb.length.item()) == n and torch.equal(ea.out[:n], eb.out[:n])
+            if ef:
+                assert torch.equal(ea.residual, eb.residual)
+        assert torch.equal(want, got), f"step {step}"
+    assert len(graph.graphs) == 1
