@@ -97,6 +97,7 @@ class CpuCodec:
         bind("decode_accumulate", [_P(_u8), C.c_size_t, _P(C.c_double), _u64, C.c_double])
         if prefix == "gpr":
             bind("volume", [_P(_u8), C.c_size_t, _P(_u64)])
+            bind("random_r", [_u64, _u64, _u64, _P(_u32)])
         if prefix == "gpo":
             bind("rle_encode", [_P(_u32), _u64, _u64, _P(_P(_u8)), _P(C.c_size_t)])
             bind("bitmap_bytes", [_P(_u32), _u64, _u64, _P(_u8)])
@@ -129,6 +130,12 @@ class CpuCodec:
         out = np.zeros(r, dtype=np.uint32)
         self._check(self._f["top_r"](g.ctypes.data_as(_P(C.c_float)), g.size, r,
                                      out.ctypes.data_as(_P(_u32))))
+        return out
+
+    def random_r(self, d: int, r: int, seed: int) -> np.ndarray:
+        """random_r (sparsify.cpp:48-58) with CounterRng(seed): the sorted support (reference build only)."""
+        out = np.zeros(r, dtype=np.uint32)
+        self._check(self._f["random_r"](d, r, seed, out.ctypes.data_as(_P(_u32))))
         return out
 
     def bloom_params(self, eps: float, r: int):

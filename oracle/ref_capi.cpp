@@ -108,6 +108,16 @@ int gpr_top_r(const float* g, std::uint64_t d, std::uint64_t r, std::uint32_t* s
   });
 }
 
+// random_r (sparsify.cpp:48-58) over a zero vector: the support only
+int gpr_random_r(std::uint64_t d, std::uint64_t r, std::uint64_t seed, std::uint32_t* support) {
+  return guarded([&] {
+    const Vector v = Vector::Zero(static_cast<Index>(d));
+    CounterRng rng(seed);
+    const SparseGradient sg = random_r(v, static_cast<Index>(r), rng);
+    std::memcpy(support, sg.support.data(), sg.support.size() * 4);
+  });
+}
+
 int gpr_bloom_params(double eps, std::uint64_t r, std::uint64_t* m, std::uint32_t* k) {
   return guarded([&] {
     const BloomParams p = bloom_params(eps, r);

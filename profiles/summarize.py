@@ -23,6 +23,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 STAGE_KERNELS = {
     "bloom_scan": ["bloom_members", "members_compact"],
     "dec_bloom_scan": ["bloom_members", "members_compact"],
+    "p2_sets": ["p2_pairs", "p2_scatter"],
+    "dec_p2_sets": ["p2_pairs", "p2_scatter"],
     "topr": ["topr_candidates"],
     "p2_engine": ["p2_engine"],
     "dec_p2_engine": ["p2_engine"],

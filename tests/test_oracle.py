@@ -283,3 +283,14 @@ def test_quant_decode_errors_match_reference(oracle):
                 except OracleError as e:
                     outs.append(e.code)
             assert outs[0] == outs[1], (vm, kw, outs)
+
+
+def test_driver_random_r_matches_reference():
+    """drivers.random_r (the sweep's random-r sparsifier) against sparsify.cpp:48-58."""
+    from oracle.bindings import reference
+    from paper_2102_03112_b200.drivers import random_r
+    ref = reference()
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    for d, r, seed in [(10, 10, 1), (1000, 10, 2), (5000, 2500, 3), (70_000, 700, 4)]:
+        assert np.array_equal(random_r(d, r, seed), ref.random_r(d, r, seed))
