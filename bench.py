@@ -358,10 +358,12 @@ def native_main(args, cfg):
     dom = max(stage.items(), key=lambda kv: kv[1][0])[0] if stage else None
     roof = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    traffic_tab = {}
+    traffic_tab, instr_tab = {}, {}
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic_tab = json.load(f).get(args.config, {})
+            tt = json.load(f)
+        traffic_tab = tt.get(args.config, {})
+        instr_tab = tt.get(args.config + ":warp_instr", {})
     if dom is not None:
         ms_launch, _ = per_launch[dom]
         ab = algo_bytes.get(dom)
@@ -373,6 +375,12 @@ def native_main(args, cfg):
             roof["keys_per_s"] = round(d / (ms_launch * 1e-3), 1)
             roof["note"] = ("full-range Bloom membership scan is integer-issue bound (SplitMix64 + 64x32 "
                             "modulo per probe), not HBM bound: see DESIGN.md")
+            if instr_tab.get(dom):  # warp instructions per launch (ncu, profiles/) over this launch time
+                peak_wi = 148 * 4 * clocks.get("sm_mhz", 1965.0) * 1e6
+                ach = instr_tab[dom] / (ms_launch * 1e-3)
+                roof["issue"] = {"achieved_warp_instr_per_s": round(ach, 1), "peak": peak_wi,
+                                 "frac": round(ach / peak_wi, 4),
+                                 "source": "smsp__inst_executed.sum of the ncu full capture (profiles/r1)"}
     step_hbm_bytes = 8.0 * d + 2.0 * world * length
     step_roof = {"hbm_bytes": step_hbm_bytes, "t_roof_ms": step_hbm_bytes / (hbm * 1e9) * 1e3,
                  "frac": round(step_hbm_bytes / (hbm * 1e9) / (t_ms * 1e-3), 6)}

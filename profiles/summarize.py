@@ -73,7 +73,7 @@ def full(path):
         rec = {}
         for h, u, v in zip(hdr, units, r):
             x = num(v)
-            rec[h] = x * scale[u] if (x is not None and u in scale) else v
+            rec[h] = (x * scale[u] if u in scale else x) if x is not None else v
         res.append(rec)
     return res
 
@@ -111,6 +111,7 @@ def main():
     lines = [f"# ncu --set full — bench.py --config {cfg}", "",
              "| kernel | " + " | ".join(v for _, v in keys) + " |", "|---" * (len(keys) + 1) + "|"]
     traffic = collections.defaultdict(list)
+    instr = collections.defaultdict(list)
     for rec in recs:
         k = short(rec.get("Kernel Name", "?")).split("<")[0]
         vals = [f"{rec[m]:.4g}" if isinstance(rec.get(m), float) else str(rec.get(m, "")) for m, _ in keys]
@@ -118,6 +119,8 @@ def main():
         rd, wr = rec.get("dram__bytes_read.sum"), rec.get("dram__bytes_write.sum")
         if isinstance(rd, float) and isinstance(wr, float):
             traffic[k].append(rd + wr)
+        if isinstance(rec.get("smsp__inst_executed.sum"), float):
+            instr[k].append(rec["smsp__inst_executed.sum"])
     open(os.path.join(outdir, f"full_{cfg}.md"), "w").write("\n".join(lines) + "\n")
     tpath = os.path.join(HERE, "ncu_traffic.json")
     tab = json.load(open(tpath)) if os.path.exists(tpath) else {}
@@ -127,6 +130,9 @@ def main():
         if parts:
             per_stage[stage] = sum(parts)
     tab[cfg] = per_stage
+    # warp instructions per launch of the stage's main kernel (the issue roofline)
+    tab[cfg + ":warp_instr"] = {stage: sum(instr[k]) / len(instr[k]) for stage, kernels in STAGE_KERNELS.items()
+                                for k in kernels[:1] if instr.get(k)}
     json.dump(tab, open(tpath, "w"), indent=1)
 
 
