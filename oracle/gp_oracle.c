@@ -1348,6 +1348,150 @@ static double* parse_dequantize(const uint8_t* p, size_t len, uint64_t count) {
   return out;
 }
 
+/* ---- canonical Huffman over index bytes (codecs.cpp:72-242) ---- */
+typedef struct {
+  uint8_t len[256];
+  uint64_t code[256];
+  uint8_t sorted[256];
+  unsigned nsym, max_len;
+  uint64_t first_code[64];
+  uint32_t first_index[64], count[64];
+} huff_t;
+
+static void huff_freqs(uint64_t d, uint64_t freq[256]) { /* index_byte_frequencies, codecs.cpp:72-91 */
+  if (d < 1) fail(GP_ERROR, "index_byte_frequencies: d must be >= 1");
+  if (d > 0x100000000ULL) fail(GP_ERROR, "index_byte_frequencies: d exceeds 32-bit index space");
+  memset(freq, 0, 256 * sizeof(uint64_t));
+  for (unsigned j = 0; j < 4; ++j) {
+    const uint64_t width = 1ULL << (8 * j);
+    const uint64_t high = d >> (8 * (j + 1));
+    const uint64_t mid = (d >> (8 * j)) & 0xff;
+    const uint64_t low = d & (width - 1);
+    for (unsigned b = 0; b < 256; ++b) {
+      uint64_t n = high * width;
+      if (b < mid) n += width;
+      else if (b == mid) n += low;
+      freq[b] += n;
+    }
+  }
+}
+
+/* from_frequencies (codecs.cpp:93-170): min-heap on (weight, creation order),
+ * lengths by depth, canonical codes by (length, symbol) */
+static void huff_build(uint64_t d, huff_t* h) {
+  uint64_t freq[256];
+  huff_freqs(d, freq);
+  uint64_t w[511];
+  int left[511], right[511], sym[511];
+  int heap[511], hn = 0, nn = 0;
+  memset(h, 0, sizeof *h);
+#define HLESS(a, b) (w[a] < w[b] || (w[a] == w[b] && (a) < (b)))
+  for (int s = 0; s < 256; ++s) {
+    if (!freq[s]) continue;
+    w[nn] = freq[s]; left[nn] = right[nn] = -1; sym[nn] = s;
+    int i = hn++; heap[i] = nn++;
+    while (i > 0 && HLESS(heap[i], heap[(i - 1) / 2])) { int t = heap[i]; heap[i] = heap[(i - 1) / 2]; heap[(i - 1) / 2] = t; i = (i - 1) / 2; }
+  }
+  if (nn == 0) fail(GP_ERROR, "huffman: empty alphabet");
+  if (nn == 1) {
+    h->len[sym[0]] = 1;
+  } else {
+    while (hn > 1) {
+      int ab[2];
+      for (int q = 0; q < 2; ++q) {
+        ab[q] = heap[0];
+        heap[0] = heap[--hn];
+        int i = 0;
+        for (;;) {
+          int l = 2 * i + 1, r = l + 1, m = i;
+          if (l < hn && HLESS(heap[l], heap[m])) m = l;
+          if (r < hn && HLESS(heap[r], heap[m])) m = r;
+          if (m == i) break;
+          int t = heap[i]; heap[i] = heap[m]; heap[m] = t; i = m;
+        }
+      }
+      w[nn] = w[ab[0]] + w[ab[1]]; left[nn] = ab[0]; right[nn] = ab[1]; sym[nn] = -1;
+      int i = hn++; heap[i] = nn++;
+      while (i > 0 && HLESS(heap[i], heap[(i - 1) / 2])) { int t = heap[i]; heap[i] = heap[(i - 1) / 2]; heap[(i - 1) / 2] = t; i = (i - 1) / 2; }
+    }
+    int st[511], dp[511], sn = 0;
+    st[sn] = nn - 1; dp[sn++] = 0;
+    while (sn) {
+      const int id = st[--sn], dep = dp[sn];
+      if (sym[id] >= 0) {
+        if (dep > 57) fail(GP_ERROR, "huffman: code length exceeds 57 bits");
+        h->len[sym[id]] = (uint8_t)dep;
+      } else {
+        st[sn] = left[id]; dp[sn++] = dep + 1;
+        st[sn] = right[id]; dp[sn++] = dep + 1;
+      }
+    }
+  }
+#undef HLESS
+  for (unsigned L = 1; L <= 57; ++L)
+    for (int s = 0; s < 256; ++s)
+      if (h->len[s] == L) h->sorted[h->nsym++] = (uint8_t)s;
+  h->max_len = h->len[h->sorted[h->nsym - 1]];
+  uint64_t code = 0;
+  unsigned prev = h->len[h->sorted[0]];
+  for (unsigned i = 0; i < h->nsym; ++i) {
+    const unsigned L = h->len[h->sorted[i]];
+    code = i ? (code + 1) << (L - prev) : 0;
+    h->code[h->sorted[i]] = code;
+    prev = L;
+    if (h->count[L] == 0) {
+      h->first_index[L] = i;
+      h->first_code[L] = code;
+    }
+    ++h->count[L];
+  }
+}
+
+static void huff_encode_indices(const huff_t* h, const uint32_t* idx, uint64_t r, uint64_t d, bitw_t* w) {
+  for (uint64_t i = 0; i < r; ++i) { /* encode_indices, codecs.cpp:219-229 */
+    if (idx[i] >= d) fail(GP_ERROR, "huffman: index out of range");
+    for (unsigned j = 0; j < 4; ++j) {
+      const uint8_t s = (uint8_t)(idx[i] >> (8 * j));
+      const unsigned L = h->len[s];
+      if (L == 0) fail(GP_ERROR, "huffman: symbol absent from codec");
+      for (unsigned b = L; b-- > 0;) bw_bit(w, (int)((h->code[s] >> b) & 1u)); /* MSB first */
+    }
+  }
+}
+
+/* decode + decode_indices (codecs.cpp:196-242); *bits_used = bits consumed */
+static uint32_t* huff_decode_indices(const huff_t* h, const uint8_t* p, size_t n, uint64_t count, uint64_t d,
+                                     uint64_t* bits_used) {
+  const uint64_t nbits = 8 * (uint64_t)n;
+  uint64_t pos = 0;
+  uint8_t* bytes = (uint8_t*)xalloc(4 * count + 1);
+  for (uint64_t i = 0; i < 4 * count; ++i) {
+    uint64_t code = 0;
+    int found = -1;
+    for (unsigned L = 1; L <= h->max_len; ++L) {
+      if (pos >= nbits) fail(GP_TRUNCATED, "bit stream exhausted");
+      code = (code << 1) | ((p[pos / 8] >> (pos % 8)) & 1u);
+      ++pos;
+      if (h->count[L] && code >= h->first_code[L] && code - h->first_code[L] < h->count[L]) {
+        found = h->sorted[h->first_index[L] + (uint32_t)(code - h->first_code[L])];
+        break;
+      }
+    }
+    if (found < 0) fail(GP_CORRUPT_PAYLOAD, "huffman: invalid code");
+    bytes[i] = (uint8_t)found;
+  }
+  if (nbits - pos >= 8) fail(GP_CORRUPT_PAYLOAD, "huffman: trailing garbage");
+  if (bits_used) *bits_used = pos;
+  uint32_t* out = (uint32_t*)xalloc((count ? count : 1) * 4);
+  for (uint64_t i = 0; i < count; ++i) {
+    uint32_t v = 0;
+    for (unsigned j = 0; j < 4; ++j) v |= (uint32_t)bytes[4 * i + j] << (8 * j);
+    if (v >= d) fail(GP_CORRUPT_PAYLOAD, "huffman: decoded index out of range");
+    out[i] = v;
+  }
+  return out;
+}
+
 static void encode_values(const double* values, uint64_t n, const gp_pipeline_config* cfg, uint64_t d,
                           bytes_t* vout, bitw_t* rout) { /* pipeline.cpp:56-93 */
   switch (cfg->value_method) {
@@ -1417,6 +1561,15 @@ static void compress(const sparse_t* sg, const gp_pipeline_config* cfg, const fl
       bitw_t w;
       bw_init(&w, 64);
       rle_encode(to_bitmap(sg->support, r, d), d, &w);
+      ip = w.b;
+      break;
+    }
+    case GP_INDEX_HUFFMAN: { /* pipeline.cpp:179-184 */
+      huff_t h;
+      huff_build(d, &h);
+      bitw_t w;
+      bw_init(&w, 64);
+      huff_encode_indices(&h, sg->support, r, d, &w);
       ip = w.b;
       break;
     }
@@ -1535,6 +1688,13 @@ static void decompress(const container_t* c, sparse_t* out) { /* pipeline.cpp:22
         fail(GP_CORRUPT_PAYLOAD, c->index_method == GP_INDEX_BITMAP ? "pipeline: bitmap popcount != r"
                                                                      : "pipeline: rle popcount != r");
       out->support = bitmap_support(w, d, c->r);
+      out->count = c->r;
+      break;
+    }
+    case GP_INDEX_HUFFMAN: { /* pipeline.cpp:254-258 */
+      huff_t h;
+      huff_build(d, &h);
+      out->support = huff_decode_indices(&h, c->ip, c->il, c->r, d, NULL);
       out->count = c->r;
       break;
     }
@@ -1685,9 +1845,14 @@ int gpo_volume(const uint8_t* bytes, size_t len, gpo_volume_report* v) { /* cont
       if (c.il == 0) fail(GP_CORRUPT_PAYLOAD, "container: empty rle payload");
       v->index_bits = 8 * c.il - 7;
       break;
-    case GP_INDEX_HUFFMAN:
-      fail(GP_UNSUPPORTED, "oracle: huffman volume is out of scope");
+    case GP_INDEX_HUFFMAN: { /* container.cpp:171-178: bits of the 4r decoded codes */
+      huff_t h;
+      huff_build(c.d, &h);
+      uint64_t used = 0;
+      huff_decode_indices(&h, c.ip, c.il, c.r, c.d, &used);
+      v->index_bits = used;
       break;
+    }
     default: {
       breader_t r = {c.ip, c.il, 0};
       v->index_bits = get_le(&r, 8);

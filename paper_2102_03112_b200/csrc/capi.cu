@@ -13,6 +13,7 @@
 #include <new>
 
 #include "gp_ctx.hpp"
+#include "huffman.cuh"
 #include "gp_device.cuh"
 
 namespace gp {
@@ -58,7 +59,8 @@ bool is_bloom(int m) { return m >= GP_INDEX_BLOOM_P0 && m <= GP_INDEX_BLOOM_NAIV
 // Methods with a device implementation on this path (the rest of FORMAT.md's
 // registry returns GP_UNSUPPORTED).
 bool index_supported(int m) {
-  return m == GP_INDEX_NONE || m == GP_INDEX_BITMAP || m == GP_INDEX_RLE || m == GP_INDEX_BLOOM_P0 ||
+  return m == GP_INDEX_NONE || m == GP_INDEX_BITMAP || m == GP_INDEX_RLE || m == GP_INDEX_HUFFMAN ||
+         m == GP_INDEX_BLOOM_P0 ||
          m == GP_INDEX_BLOOM_P1 ||
          m == GP_INDEX_BLOOM_P2 ||
          m == GP_INDEX_BLOOM_PD || m == GP_INDEX_BLOOM_NAIVE;
@@ -215,6 +217,8 @@ void carve(Workspace& w, uint8_t* base, uint64_t D) {
   w.crc_digits = c.take<uint32_t>(5 * 256);
   w.crc_acc = c.take<uint32_t>(64);
   w.scratch = c.take<uint8_t>(2 * D);
+  w.huff = c.take<HuffTable>(1);
+  w.huff_res = c.take<uint64_t>(16);
   w.bytes_total = c.off;
 }
 
@@ -268,6 +272,7 @@ int gp_ctx_create(int device, uint64_t max_d, gp_ctx** out) {
   ctx->ws.bytes = bytes;
   e = cudaMemset(ctx->ws.status, 0, 64 * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMemset(ctx->ws.plan, 0, sizeof(Plan));
+  if (e == cudaSuccess) e = cudaMemset(ctx->ws.huff, 0, sizeof(HuffTable));  // empty Huffman table cache
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     cudaFree(base);
@@ -380,6 +385,7 @@ uint64_t gp_max_container_bytes(uint64_t d, uint64_t r, const gp_pipeline_config
     case GP_INDEX_NONE: il = 4 * r; break;
     case GP_INDEX_BITMAP: il = (d + 7) / 8; break;
     case GP_INDEX_RLE: il = d + 2; break;  // <= one group per coordinate, + the polarity byte
+    case GP_INDEX_HUFFMAN: il = huffman_il_bound(d, r) + 8; break;  // 4 codes of <= max_len bits per key
     default: {
       uint64_t m = 0;
       uint32_t k = 0;
@@ -461,7 +467,7 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
     pi.minv = ~0ULL / m;
     pi.il = 26 + (m + 7) / 8 + (im == GP_INDEX_BLOOM_PD ? 1 : 0);
   } else {
-    pi.il = im == GP_INDEX_NONE ? 4 * r : (d + 7) / 8;
+    pi.il = im == GP_INDEX_NONE ? 4 * r : im == GP_INDEX_HUFFMAN ? 0 : (d + 7) / 8;  // Huffman: set on the device
   }
   pi.seed = cfg->seed;
   pi.seed_dev = ctx->seed_dev;
@@ -478,6 +484,9 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
     case GP_INDEX_NONE: launch_index_none(ctx, d_out, r, s); break;
     case GP_INDEX_BITMAP: launch_index_bitmap(ctx, d_out, d, r, s); break;
     case GP_INDEX_RLE: GP_STAGE(ctx, ST_INDEX, s, launch_index_rle(ctx, d_out, d, r, s)); break;
+    case GP_INDEX_HUFFMAN:
+      GP_STAGE(ctx, ST_INDEX, s, launch_index_huffman(ctx, d_out, r, huffman_il_bound(d, r) + 8, s));
+      break;
     default: {
       GP_STAGE(ctx, ST_BLOOM_BUILD, s, launch_bloom_build(ctx, d_out, pi.m, r, s));
       if (im == GP_INDEX_BLOOM_NAIVE) break;  // values stay in support order (pipeline.cpp:196-199)
@@ -567,6 +576,7 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const u
     case GP_INDEX_NONE: launch_decode_index_none(ctx, d_in, bound, s); break;
     case GP_INDEX_BITMAP: launch_decode_index_bitmap(ctx, d_in, bound, s); break;
     case GP_INDEX_RLE: GP_STAGE(ctx, ST_DEC_INDEX, s, launch_decode_index_rle(ctx, d_in, len, bound, s)); break;
+    case GP_INDEX_HUFFMAN: GP_STAGE(ctx, ST_DEC_INDEX, s, launch_decode_index_huffman(ctx, d_in, len, s)); break;
     default: {
       GP_STAGE(ctx, ST_DEC_BLOOM_SCAN, s, launch_bloom_parse(ctx, d_in, ctx->ws.m_cap, s);
                                            launch_bloom_scan(ctx, bound, 0, true, s));
@@ -586,7 +596,7 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const u
     case GP_VALUE_DEFLATE_SLOT: launch_decode_slot(ctx, d_in, s); break;
     default: break;
   }
-  if (im == GP_INDEX_NONE && !own) launch_validate_support(ctx, bound, s);
+  if ((im == GP_INDEX_NONE || im == GP_INDEX_HUFFMAN) && !own) launch_validate_support(ctx, bound, s);
   (void)dense_d;
   GP_STAGE(ctx, ST_DEC_SCATTER, s,
            launch_decode_scatter(ctx, d_in, bound, d_dense, scale, d_support, d_values, cap, d_count, d_dim, s));

@@ -54,6 +54,8 @@ struct Plan {
 
 constexpr int kMaxSeg = 64;
 
+struct HuffTable;  // huffman.cuh
+
 struct Workspace {
   void* base = nullptr;
   size_t bytes = 0;
@@ -111,6 +113,8 @@ struct Workspace {
   bool crc_ready = false;
   uint64_t crc_cap = 0;
   uint8_t* scratch = nullptr;     // generic byte scratch [2 * D]
+  HuffTable* huff = nullptr;      // Huffman index table of the current container
+  uint64_t* huff_res = nullptr;   // Huffman decode verdict words + round flags [16]
 };
 
 }  // namespace gp
@@ -198,6 +202,9 @@ void launch_decode_index_none(gp_ctx* ctx, const uint8_t* in, uint64_t r_bound, 
 void launch_validate_support(gp_ctx* ctx, uint64_t r_bound, cudaStream_t s);
 void launch_decode_index_bitmap(gp_ctx* ctx, const uint8_t* in, uint64_t d_bound, cudaStream_t s);
 void launch_index_rle(gp_ctx* ctx, uint8_t* out, uint64_t d, uint64_t r, cudaStream_t s);          // rle.cu
+void launch_index_huffman(gp_ctx* ctx, uint8_t* out, uint64_t r, uint64_t il_bound, cudaStream_t s);  // huffman.cu
+void launch_decode_index_huffman(gp_ctx* ctx, const uint8_t* in, uint64_t len_bound, cudaStream_t s);
+uint64_t huffman_il_bound(uint64_t d, uint64_t r);
 void launch_decode_index_rle(gp_ctx* ctx, const uint8_t* in, uint64_t len_bound, uint64_t d_bound, cudaStream_t s);
 
 // bloom.cu / p2.cu

@@ -71,7 +71,7 @@ __global__ void index_none_decode(const uint8_t* __restrict__ in, Plan* plan, ui
 
 // validate strictly increasing & < d (pipeline.cpp:299-305) — after the values
 __global__ void support_validate(const Plan* plan, const uint32_t* __restrict__ sel, uint32_t* status) {
-  if (failed(status) || plan->index_method != GP_INDEX_NONE) return;
+  if (failed(status) || (plan->index_method != GP_INDEX_NONE && plan->index_method != GP_INDEX_HUFFMAN)) return;
   const uint64_t n = plan->n_sel, d = plan->d;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {

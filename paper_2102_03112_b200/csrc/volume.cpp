@@ -9,6 +9,7 @@
 #include <cstring>
 
 #include "../../include/gradpack_b200.h"
+#include "huffman.cuh"
 
 namespace {
 
@@ -47,8 +48,31 @@ extern "C" GP_API int gp_volume(const uint8_t* h, uint64_t len, gp_volume_report
       if (il == 0) return GP_CORRUPT_PAYLOAD;
       out->index_bits = 8 * il - 7;  // 1 lead bit plus whole groups (the writer pads < 8 bits)
       break;
-    case GP_INDEX_HUFFMAN:
-      return GP_UNSUPPORTED;
+    case GP_INDEX_HUFFMAN: {  // container.cpp:171-178: the bits of the 4r decoded codes
+      gp::HuffTable t;
+      gp::HuffScratch x;
+      gp::huff_build(d, &t, x);
+      if (t.error) return GP_ERROR;
+      const uint64_t nbits = 8 * il;
+      uint64_t pos = 0;
+      for (uint64_t i = 0; i < 4 * r; ++i) {
+        uint64_t win = 0;
+        for (int k = 0; k < 9; ++k) {
+          const uint64_t b = pos / 8 + k;
+          const uint64_t byte = b < il ? ip[b] : 0;
+          const int sh = 8 * k - static_cast<int>(pos % 8);
+          if (sh >= 64) break;
+          win |= sh >= 0 ? byte << sh : byte >> -sh;
+        }
+        unsigned L = 0;
+        const int sym = gp::huff_decode_one(t, win, nbits - pos, L);
+        if (sym < 0) return sym == -1 ? GP_CORRUPT_PAYLOAD : GP_TRUNCATED;
+        pos += L;
+      }
+      if (nbits - pos >= 8) return GP_CORRUPT_PAYLOAD;
+      out->index_bits = pos;
+      break;
+    }
     default:
       if (im > GP_INDEX_BLOOM_NAIVE) return GP_UNKNOWN_METHOD;
       if (il < 8) return GP_TRUNCATED;

@@ -47,7 +47,8 @@ def test_library_is_sm100a():
 
 @pytest.mark.parametrize("im,vm,kw", [(0, 0, {}), (1, 0, {}), (2, 0, {}), (4, 1, {}), (5, 5, {}), (6, 1, {}),
                                       (7, 0, {}), (8, 1, {}), (1, 1, {}), (1, 3, {}), (6, 3, dict(quant_bits=3)),
-                                      (2, 3, dict(quant_bits=16, quant_bucket=7)), (6, 4, dict(slot_codec=0))])
+                                      (2, 3, dict(quant_bits=16, quant_bucket=7)), (6, 4, dict(slot_codec=0)),
+                                      (3, 0, {}), (3, 1, {})])
 def test_volume_matches_reference(oracle, reference, im, vm, kw):
     # gp_volume is host code: it runs here, against the reference's own volume()
     from oracle.bindings import GpConfig as OC, synthetic_gradient

@@ -294,3 +294,58 @@ def test_driver_random_r_matches_reference():
         pytest.skip("oracle/_ref not built")
     for d, r, seed in [(10, 10, 1), (1000, 10, 2), (5000, 2500, 3), (70_000, 700, 4)]:
         assert np.array_equal(random_r(d, r, seed), ref.random_r(d, r, seed))
+
+
+@pytest.mark.parametrize("d", [1, 2, 7, 255, 256, 257, 1000, 65536, 65537, 100_003, 2_000_000])
+def test_huffman_index_matches_reference(oracle, d):
+    """Huffman index (codecs.cpp:72-242, pipeline.cpp:179-184, :254-258): the
+    canonical table derived from d alone, MSB-first codes, byte-identical."""
+    from oracle.bindings import GpConfig, reference, synthetic_gradient
+    ref = reference()
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    g = synthetic_gradient(d, rank=d % 7)
+    for r in sorted({1, max(1, d // 100), max(1, d // 3), d}):
+        if r > 100_000:
+            continue
+        cfg = GpConfig.make(3, 0, seed=4)
+        a, b = oracle.encode_dense(g, r, cfg), ref.encode_dense(g, r, cfg)
+        assert a == b, r
+        _, sa, va = oracle.decode(a)
+        _, sb, vb = ref.decode(b)
+        assert np.array_equal(sa, sb) and np.array_equal(va, vb)
+
+
+def test_huffman_decode_errors_match_reference(oracle):
+    from oracle.bindings import GpConfig, OracleError, reference, synthetic_gradient
+    ref = reference()
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(3)
+    for d, r in [(1000, 10), (70_000, 300), (300, 300)]:
+        c = bytearray(oracle.encode_dense(synthetic_gradient(d, rank=1), r, GpConfig.make(3, 0, seed=2)))
+        il = int.from_bytes(c[25:33], "little")
+        muts = []
+        for _ in range(12):  # bit flips inside the index payload
+            m = bytearray(c)
+            pos = 49 + int(rng.integers(0, il))
+            m[pos] ^= 1 << int(rng.integers(0, 8))
+            muts.append(m)
+        for cut in (1, 2):  # index payload shortened (lengths rewritten)
+            m = bytearray(c[:49 + il - cut] + c[49 + il:])
+            m[25:33] = (il - cut).to_bytes(8, "little")
+            muts.append(m)
+        m = bytearray(c[:49 + il] + b"\x00" + c[49 + il:])  # one trailing byte
+        m[25:33] = (il + 1).to_bytes(8, "little")
+        muts.append(m)
+        for m in muts:
+            m[-4:] = oracle.crc32c(bytes(m[49:-4])).to_bytes(4, "little")
+            outs = []
+            for cod in (oracle, ref):
+                try:
+                    _, s, v = cod.decode(bytes(m))
+                    outs.append(("ok", s.tobytes(), v.tobytes()))
+                except OracleError as e:
+                    outs.append(e.code)
+            assert outs[0] == outs[1], (d, r, outs[0] if not isinstance(outs[0], tuple) else "ok",
+                                        outs[1] if not isinstance(outs[1], tuple) else "ok")
