@@ -66,8 +66,8 @@ bool index_supported(int m) {
          m == GP_INDEX_BLOOM_PD || m == GP_INDEX_BLOOM_NAIVE;
 }
 bool value_supported(int m) {
-  return m == GP_VALUE_NONE || m == GP_VALUE_RAW_F64 || m == GP_VALUE_FIT_POLY || m == GP_VALUE_QUANT ||
-         m == GP_VALUE_DEFLATE_SLOT;
+  return m == GP_VALUE_NONE || m == GP_VALUE_RAW_F64 || m == GP_VALUE_FIT_POLY || m == GP_VALUE_FIT_DEXP ||
+         m == GP_VALUE_QUANT || m == GP_VALUE_DEFLATE_SLOT;
 }
 
 struct PlanInit {
@@ -432,7 +432,7 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
     return set_error(ctx, GP_ERROR, "container: unregistered method");
   if (!index_supported(im) || !value_supported(vm))
     return set_error(ctx, GP_UNSUPPORTED, "method not implemented on the device path");
-  if (vm == GP_VALUE_FIT_POLY) {
+  if (vm == GP_VALUE_FIT_POLY || vm == GP_VALUE_FIT_DEXP) {
     if (cfg->degree < 0 || cfg->degree > 60) return set_error(ctx, GP_ERROR, "value_compress: bad degree");
     if (cfg->degree > 7) return set_error(ctx, GP_UNSUPPORTED, "fit degree > 7 is not on the device path");
   }
@@ -505,7 +505,9 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
     case GP_VALUE_NONE:
     case GP_VALUE_RAW_F64: launch_values_raw(ctx, d_out, vm == GP_VALUE_RAW_F64, n_bound, s); break;
     case GP_VALUE_FIT_POLY:
-      GP_STAGE(ctx, ST_VALUES, s, launch_values_fit(ctx, d_out, cfg->degree, cfg->max_segments, n_bound, s));
+    case GP_VALUE_FIT_DEXP:
+      GP_STAGE(ctx, ST_VALUES, s, launch_values_fit(ctx, d_out, cfg->degree, cfg->max_segments, n_bound, s,
+                                                    vm == GP_VALUE_FIT_DEXP));
       break;
     case GP_VALUE_QUANT:  // derive_quant_seed (pipeline.cpp:26)
       GP_STAGE(ctx, ST_VALUES, s,
@@ -591,7 +593,8 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const u
   switch (vm) {
     case GP_VALUE_NONE:
     case GP_VALUE_RAW_F64: launch_values_raw_check(ctx, s); break;
-    case GP_VALUE_FIT_POLY: GP_STAGE(ctx, ST_DEC_VALUES, s, launch_decode_fit(ctx, d_in, bound, s)); break;
+    case GP_VALUE_FIT_POLY:
+    case GP_VALUE_FIT_DEXP: GP_STAGE(ctx, ST_DEC_VALUES, s, launch_decode_fit(ctx, d_in, bound, s)); break;
     case GP_VALUE_QUANT: GP_STAGE(ctx, ST_DEC_VALUES, s, launch_decode_quant(ctx, d_in, bound, s)); break;
     case GP_VALUE_DEFLATE_SLOT: launch_decode_slot(ctx, d_in, s); break;
     default: break;

@@ -44,6 +44,7 @@ struct Plan {
   uint32_t sign_split, identity;
   uint32_t nseg, degree;
   uint32_t q_bits, q_bucket;    // quantizer header (decode)
+  uint32_t fit_kind, dexp_fail; // fit model kind (0 poly, 1 dexp); a dexp part failed (fallback)
   uint32_t seg_end[64];         // fit bounds (<= 64 segments on this path)
   float coeffs[64 * 8];
   // ---- decode
@@ -225,7 +226,8 @@ void launch_table_scan(gp_ctx* ctx, uint32_t* table, const uint64_t* n_dev, uint
 void launch_gather_values(gp_ctx* ctx, const float* dense, uint64_t n_bound, cudaStream_t s);
 void launch_values_raw(gp_ctx* ctx, uint8_t* out, bool f64, uint64_t n_bound, cudaStream_t s);
 void launch_values_raw_check(gp_ctx* ctx, cudaStream_t s);
-void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, uint64_t n_bound, cudaStream_t s);
+void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, uint64_t n_bound, cudaStream_t s,
+                       bool dexp = false);
 void launch_decode_fit(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, cudaStream_t s);
 void launch_values_quant(gp_ctx* ctx, uint8_t* out, int bits, uint32_t bucket, uint64_t n_bound,
                          cudaStream_t s);                                                            // values_quant.cu

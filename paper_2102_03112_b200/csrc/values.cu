@@ -48,7 +48,6 @@ __global__ void values_raw_check(Plan* plan, uint32_t* status) {
   const uint64_t n = plan->n_values;
   if (vm == GP_VALUE_NONE && plan->vl != 4 * n) latch(status, GP_CORRUPT_PAYLOAD);
   if (vm == GP_VALUE_RAW_F64 && plan->vl != 8 * n) latch(status, GP_CORRUPT_PAYLOAD);
-  if (vm == GP_VALUE_FIT_DEXP) latch(status, GP_UNSUPPORTED);
 }
 
 // value i of the decoded container: raw payload bytes or the fit evaluation

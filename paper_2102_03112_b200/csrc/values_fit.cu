@@ -40,7 +40,18 @@ constexpr int kChunk = 2048;                // points per accumulate block
 constexpr int kAcc = 36 + 8;                // Gram upper triangle (<= 36) + rhs (<= 8)
 
 __device__ __forceinline__ bool fit_active(const Plan* plan) {
-  return plan->value_method == GP_VALUE_FIT_POLY;
+  return plan->value_method == GP_VALUE_FIT_POLY || plan->value_method == GP_VALUE_FIT_DEXP;
+}
+// the piecewise-polynomial encode stages: skipped when a dexp model stands
+__device__ __forceinline__ bool poly_active(const Plan* plan) { return fit_active(plan) && plan->fit_kind == 0; }
+
+constexpr double kExpClamp = 700.0;
+__device__ __forceinline__ double safe_exp(double x) { return exp(x < kExpClamp ? x : kExpClamp); }
+
+// eval_dexp (curvefit.cpp:365-368)
+__device__ __forceinline__ double eval_dexp(const float* c, double x) {
+  return __dadd_rn(__dmul_rn(static_cast<double>(c[0]), safe_exp(__dmul_rn(static_cast<double>(c[1]), x))),
+                   __dmul_rn(static_cast<double>(c[2]), safe_exp(__dmul_rn(static_cast<double>(c[3]), x))));
 }
 
 __global__ void fit_keys(const float* __restrict__ values, Plan* plan, uint32_t* __restrict__ keys,
@@ -196,7 +207,7 @@ __global__ void __launch_bounds__(256) fit_segment_coop(Plan* plan, const double
   __shared__ Piece res[2];
   __shared__ int s_best;
   // uniform exit decisions only (every block must reach every grid.sync)
-  if (failed(status) || !fit_active(plan)) return;
+  if (failed(status) || !poly_active(plan)) return;
   const uint64_t n = plan->n_values;
   const uint32_t l = plan->sign_split;
   const uint32_t un = static_cast<uint32_t>(n);
@@ -326,7 +337,7 @@ __device__ bool locate_chunk(const Plan* plan, uint64_t c, uint32_t& seg, uint32
 __global__ void __launch_bounds__(256) fit_accumulate(const Plan* plan, const double* __restrict__ t,
                                                       double* __restrict__ partial, const uint32_t* status) {
   __shared__ double red[8][kAcc];
-  if (failed(status) || !fit_active(plan)) return;
+  if (failed(status) || !poly_active(plan)) return;
   uint32_t seg, start, stop;
   if (!locate_chunk(plan, blockIdx.x, seg, start, stop)) return;
   uint32_t b, e;
@@ -378,7 +389,7 @@ __global__ void __launch_bounds__(256) fit_accumulate(const Plan* plan, const do
 __global__ void fit_solve(Plan* plan, const double* __restrict__ t, const double* __restrict__ partial,
                           const uint32_t* status) {
   __shared__ double sacc[kAcc];
-  if (failed(status) || !fit_active(plan)) return;
+  if (failed(status) || !poly_active(plan)) return;
   const uint32_t seg = blockIdx.x;
   if (seg >= plan->nseg) return;
   uint32_t b, e;
@@ -507,20 +518,22 @@ __global__ void fit_solve(Plan* plan, const double* __restrict__ t, const double
 }
 
 // serialize_fit (curvefit.cpp:285-298) + reorder payload size; vl, rl, flags
-__global__ void fit_emit(Plan* plan, uint8_t* out, const uint32_t* status) {
+__global__ void fit_emit(Plan* plan, uint8_t* out, int cfg_degree, const uint32_t* status) {
   if (failed(status) || !fit_active(plan) || threadIdx.x != 0) return;
-  const uint32_t S = plan->nseg, deg = plan->degree;
+  const uint32_t kind = plan->fit_kind;
+  const uint32_t S = plan->nseg, deg = kind ? static_cast<uint32_t>(cfg_degree) : plan->degree;
+  const uint32_t cps = kind ? 4 : deg + 1;  // coeffs_per_segment
   uint8_t* p = out + 49 + plan->il;
-  p[0] = 0;  // kind: piecewise polynomial
+  p[0] = static_cast<uint8_t>(kind);  // 0 piecewise polynomial, 1 double exponential
   p[1] = static_cast<uint8_t>(S);
   p[2] = static_cast<uint8_t>(S >> 8);
   uint8_t* q = p + 3;
   for (uint32_t s = 0; s < S; ++s, q += 4) st_u32_unaligned(q, plan->seg_end[s]);
   *q++ = static_cast<uint8_t>(deg);
   for (uint32_t s = 0; s < S; ++s)
-    for (uint32_t j = 0; j <= deg; ++j, q += 4) st_u32_unaligned(q, __float_as_uint(plan->coeffs[s * kCps + j]));
+    for (uint32_t j = 0; j < cps; ++j, q += 4) st_u32_unaligned(q, __float_as_uint(plan->coeffs[s * kCps + j]));
   st_u32_unaligned(q, plan->sign_split);
-  plan->vl = 1 + 2 + 4ull * S + 1 + 4ull * S * (deg + 1) + 4;
+  plan->vl = 1 + 2 + 4ull * S + 1 + 4ull * S * cps + 4;
   uint32_t w = 0;
   for (uint64_t x = plan->d - 1; x; x >>= 1) ++w;
   plan->rl = plan->identity ? 0 : (plan->n_values * w + 7) / 8;
@@ -603,13 +616,13 @@ __global__ void fit_parse(const uint8_t* __restrict__ in, Plan* plan, uint32_t* 
       if (last >> (need % 8)) return latch(status, GP_CORRUPT_PAYLOAD);
     }
   }
-  if (kind == 1) return latch(status, GP_UNSUPPORTED);  // dexp evaluation is out of scope
-  if (S > kMaxSeg || deg > kMaxDeg) return latch(status, GP_CAPACITY);
+  if (S > kMaxSeg || (kind == 0 && deg > kMaxDeg)) return latch(status, GP_CAPACITY);
   plan->nseg = S;
   plan->degree = deg;
+  plan->fit_kind = kind;
   plan->sign_split = l;
   for (uint32_t s = 0; s < S; ++s)
-    for (uint32_t j = 0; j <= deg; ++j)
+    for (uint32_t j = 0; j < cps; ++j)
       plan->coeffs[s * kCps + j] = __uint_as_float(ld_u32_unaligned(p + coeff_at + 4 * (s * cps + j)));
 }
 
@@ -645,6 +658,7 @@ __global__ void fit_eval(const Plan* plan, const uint32_t* __restrict__ map, dou
   __shared__ float coeffs[kMaxSeg * kCps];
   if (failed(status) || !fit_active(plan)) return;
   const uint32_t S = plan->nseg, cps = plan->degree + 1;
+  const bool dexp = plan->fit_kind == 1;
   for (uint32_t i = threadIdx.x; i < S; i += blockDim.x) bounds[i] = plan->seg_end[i];
   for (uint32_t i = threadIdx.x; i < S * kCps; i += blockDim.x) coeffs[i] = plan->coeffs[i];
   __syncthreads();
@@ -660,10 +674,256 @@ __global__ void fit_eval(const Plan* plan, const uint32_t* __restrict__ map, dou
     const double x = static_cast<double>(j - begin + 1);
     const float* c = coeffs + seg * kCps;
     double acc = 0.0;
-    for (int q = static_cast<int>(cps) - 1; q >= 0; --q) acc = __dadd_rn(__dmul_rn(acc, x), static_cast<double>(c[q]));
+    if (dexp)
+      acc = eval_dexp(c, x);
+    else
+      for (int q = static_cast<int>(cps) - 1; q >= 0; --q) acc = __dadd_rn(__dmul_rn(acc, x), static_cast<double>(c[q]));
     const double v = s < l ? acc : -acc;
     out[reorder ? map[s] : s] = v;
   }
+}
+
+// ---------------------------------------------------------------- dexp
+// fit_dexp (curvefit.cpp:225-283) of one sign part per block: log-linear
+// starts on the two halves (:194-221), then Levenberg-Marquardt with the
+// reference's damping schedule, acceptance and convergence tests; every sum
+// over the part is a block reduction in fp64.  The 4x4 damped system is solved
+// by LDLT (SPD for lambda > 0; Eigen's pivoted LDLT gives the same solution up
+// to rounding).  A part shorter than 4 points or a non-finite fit makes the
+// whole model fall back to the polynomial fit (value_compress, :464-491).
+constexpr int kDexpBlock = 1024;
+
+template <int N>
+__device__ __forceinline__ void block_sum(double (&v)[N], double* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < N; ++k)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v[k] += __shfl_xor_sync(kFull, v[k], o);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < N; ++k) sh[warp * N + k] = v[k];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    double a = 0.0;
+    for (int w = 0; w < kDexpBlock / 32; ++w) a += sh[w * N + k];
+    v[k] = a;
+  }
+  __syncthreads();
+}
+
+__device__ double dexp_sse(const double* y, uint32_t n, const double* p, double* sh) {
+  double v[1] = {0.0};
+  for (uint32_t i = threadIdx.x; i < n; i += kDexpBlock) {
+    const double x = static_cast<double>(i + 1);
+    const double r = p[0] * safe_exp(p[1] * x) + p[2] * safe_exp(p[3] * x) - y[i];
+    v[0] += r * r;
+  }
+  block_sum<1>(v, sh);
+  return v[0];
+}
+
+// amp * e^{rate x} over 1-based positions begin+1 .. begin+len (positive samples)
+__device__ void log_linear(const double* y, uint32_t begin, uint32_t len, double* sh, double& amp, double& rate) {
+  double v[5] = {0, 0, 0, 0, 0};  // sx, sy, sxx, sxy, m
+  double lastpos = -1.0;          // index of the last positive sample
+  for (uint32_t i = begin + threadIdx.x; i < begin + len; i += kDexpBlock) {
+    if (!(y[i] > 0.0)) continue;
+    const double x = static_cast<double>(i + 1), ly = log(y[i]);
+    v[0] += x;
+    v[1] += ly;
+    v[2] += x * x;
+    v[3] += x * ly;
+    v[4] += 1.0;
+    lastpos = static_cast<double>(i);
+  }
+  double lp[1] = {lastpos};
+  block_sum<5>(v, sh);
+  {  // max over threads of the last positive index
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int o = 16; o; o >>= 1) lp[0] = fmax(lp[0], __shfl_xor_sync(kFull, lp[0], o));
+    if (lane == 0) sh[warp] = lp[0];
+    __syncthreads();
+    double a = -1.0;
+    for (int w = 0; w < kDexpBlock / 32; ++w) a = fmax(a, sh[w]);
+    lp[0] = a;
+    __syncthreads();
+  }
+  const double m = v[4];
+  if (m >= 2) {
+    const double denom = m * v[2] - v[0] * v[0];
+    if (fabs(denom) > 1e-12) {
+      const double r = (m * v[3] - v[0] * v[1]) / denom;
+      const double lamp = (v[1] - r * v[0]) / m;
+      if (isfinite(r) && isfinite(lamp)) {
+        amp = exp(fmin(fmax(lamp, -kExpClamp), kExpClamp));
+        rate = r;
+        return;
+      }
+    }
+  }
+  if (m >= 1) {
+    amp = y[static_cast<uint32_t>(lp[0])];
+    rate = 0.0;
+    return;
+  }
+  amp = 1e-12;
+  rate = 0.0;
+}
+
+__global__ void __launch_bounds__(kDexpBlock) dexp_fit(Plan* plan, const double* __restrict__ t,
+                                                        const uint32_t* status) {
+  __shared__ double sh[(kDexpBlock / 32) * 14];
+  __shared__ double sp[4], scand[4], sbest, slambda;
+  __shared__ int sflag;  // bit0 accepted, bit1 converged, bit2 stop attempts
+  if (failed(status) || plan->value_method != GP_VALUE_FIT_DEXP) return;
+  const uint32_t n = static_cast<uint32_t>(plan->n_values), l = plan->sign_split;
+  uint32_t parts[2][2], np = 0;
+  if (l > 0) { parts[np][0] = 0; parts[np][1] = l; ++np; }
+  if (l < n) { parts[np][0] = l; parts[np][1] = n; ++np; }
+  if (blockIdx.x >= np) return;
+  const uint32_t begin = parts[blockIdx.x][0], len = parts[blockIdx.x][1] - begin;
+  if (len < 4) {
+    if (threadIdx.x == 0) atomicOr(&plan->dexp_fail, 1u);
+    return;
+  }
+  const double* y = t + begin;
+  const uint32_t half = len / 2;
+  double a0, b0, c0, d0;
+  log_linear(y, 0, half, sh, a0, b0);
+  log_linear(y, half, len - half, sh, c0, d0);
+  if (threadIdx.x == 0) {
+    sp[0] = a0; sp[1] = b0; sp[2] = c0; sp[3] = d0;
+    slambda = 1e-3;
+  }
+  __syncthreads();
+  double best = dexp_sse(y, len, sp, sh);
+  if (!isfinite(best)) {
+    if (threadIdx.x == 0) atomicOr(&plan->dexp_fail, 1u);
+    return;
+  }
+  bool converged = false;
+  for (int it = 0; it < 300 && !converged; ++it) {
+    double v[14];
+#pragma unroll
+    for (int k = 0; k < 14; ++k) v[k] = 0.0;
+    const double p0 = sp[0], p1 = sp[1], p2 = sp[2], p3 = sp[3];
+    for (uint32_t i = threadIdx.x; i < len; i += kDexpBlock) {
+      const double x = static_cast<double>(i + 1);
+      const double eb = safe_exp(p1 * x), ed = safe_exp(p3 * x);
+      const double j[4] = {eb, p0 * x * eb, ed, p2 * x * ed};
+      const double r = p0 * eb + p2 * ed - y[i];
+      int q = 0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = a; b < 4; ++b) v[q++] += j[a] * j[b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) v[10 + a] += j[a] * r;
+    }
+    block_sum<14>(v, sh);
+    bool accepted = false;
+    for (int attempt = 0; attempt < 24; ++attempt) {
+      if (threadIdx.x == 0) {
+        // (JtJ + lambda I) delta = -Jtr by LDLT
+        double A[4][4];
+        int q = 0;
+        for (int a = 0; a < 4; ++a)
+          for (int b = a; b < 4; ++b) {
+            A[a][b] = A[b][a] = v[q++];
+          }
+        for (int a = 0; a < 4; ++a) A[a][a] += slambda;
+        double L[4][4] = {}, D[4];
+        for (int j2 = 0; j2 < 4; ++j2) {
+          double dd = A[j2][j2];
+          for (int k2 = 0; k2 < j2; ++k2) dd -= L[j2][k2] * L[j2][k2] * D[k2];
+          D[j2] = dd;
+          L[j2][j2] = 1.0;
+          for (int i2 = j2 + 1; i2 < 4; ++i2) {
+            double s2 = A[i2][j2];
+            for (int k2 = 0; k2 < j2; ++k2) s2 -= L[i2][k2] * L[j2][k2] * D[k2];
+            L[i2][j2] = s2 / dd;
+          }
+        }
+        double z[4], delta[4];
+        for (int i2 = 0; i2 < 4; ++i2) {
+          double s2 = -v[10 + i2];
+          for (int k2 = 0; k2 < i2; ++k2) s2 -= L[i2][k2] * z[k2];
+          z[i2] = s2;
+        }
+        for (int i2 = 3; i2 >= 0; --i2) {
+          double s2 = z[i2] / D[i2];
+          for (int k2 = i2 + 1; k2 < 4; ++k2) s2 -= L[k2][i2] * delta[k2];
+          delta[i2] = s2;
+        }
+        for (int a = 0; a < 4; ++a) scand[a] = sp[a] + delta[a];
+        double dn = 0.0;
+        for (int a = 0; a < 4; ++a) dn += delta[a] * delta[a];
+        sh[(kDexpBlock / 32) * 14 - 1] = sqrt(dn);  // |delta|, read back by thread 0 below
+      }
+      __syncthreads();
+      const double dnorm = sh[(kDexpBlock / 32) * 14 - 1];
+      __syncthreads();
+      const double sse = dexp_sse(y, len, scand, sh);
+      if (threadIdx.x == 0) {
+        int f = 0;
+        if (isfinite(sse) && sse < best) {
+          const double gain = best - sse;
+          double pn = 0.0;
+          for (int a = 0; a < 4; ++a) {
+            sp[a] = scand[a];
+            pn += sp[a] * sp[a];
+          }
+          sbest = sse;
+          slambda = fmax(slambda / 10.0, 1e-12);
+          f = 1;
+          if (gain <= 1e-14 * (sse + 1e-300) || dnorm <= 1e-12 * (1.0 + sqrt(pn))) f |= 2;
+        } else {
+          slambda *= 10.0;
+          if (slambda > 1e14) f = 4;
+        }
+        sflag = f;
+      }
+      __syncthreads();
+      const int f = sflag;
+      if (f & 1) {
+        best = sbest;
+        accepted = true;
+        converged = (f & 2) != 0;
+        break;
+      }
+      if (f & 4) break;
+    }
+    if (!accepted) break;
+  }
+  if (threadIdx.x == 0) {
+    double a = sp[0], b = sp[1], c = sp[2], d = sp[3];
+    if (!(isfinite(a) && isfinite(b) && isfinite(c) && isfinite(d) && isfinite(best))) {
+      atomicOr(&plan->dexp_fail, 1u);
+      return;
+    }
+    if (b > d) {  // the slower exponential first (curvefit.cpp:277-281)
+      double tmp = a; a = c; c = tmp;
+      tmp = b; b = d; d = tmp;
+    }
+    float* co = plan->coeffs + blockIdx.x * kCps;
+    co[0] = static_cast<float>(a);
+    co[1] = static_cast<float>(b);
+    co[2] = static_cast<float>(c);
+    co[3] = static_cast<float>(d);
+    plan->seg_end[blockIdx.x] = parts[blockIdx.x][1];
+  }
+}
+
+// dexp model or the polynomial fallback (value_compress attempt 1)
+__global__ void dexp_decide(Plan* plan, const uint32_t* status) {
+  if (failed(status) || plan->value_method != GP_VALUE_FIT_DEXP) return;
+  if (plan->dexp_fail) return;  // fit_kind stays 0: the polynomial path runs
+  const uint32_t n = static_cast<uint32_t>(plan->n_values), l = plan->sign_split;
+  plan->nseg = (l > 0 ? 1u : 0u) + (l < n ? 1u : 0u);
+  plan->fit_kind = 1;
 }
 
 }  // namespace
@@ -674,14 +934,21 @@ void launch_radix_sort(gp_ctx* ctx, uint32_t* keys, uint32_t* vals, uint32_t* kt
 __global__ void fit_reset(Plan* plan) {
   plan->sign_split = 0;
   plan->identity = 1;
+  plan->fit_kind = 0;
+  plan->dexp_fail = 0;
 }
 
-void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, uint64_t n_bound, cudaStream_t s) {
+void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, uint64_t n_bound, cudaStream_t s,
+                       bool dexp) {
   Workspace& w = ctx->ws;
   GP_LAUNCH(ctx, fit_reset, 1, 1, 0, s, w.plan);
   GP_LAUNCH(ctx, fit_keys, grid_for(ctx, n_bound, 256), 256, 0, s, w.values, w.plan, w.u32a, w.u32b, w.status);
   launch_radix_sort(ctx, w.u32a, w.u32b, w.u32c, w.u32d, &w.plan->n_values, n_bound, 32, s);
   GP_LAUNCH(ctx, fit_prepare, grid_for(ctx, n_bound, 256), 256, 0, s, w.values, w.u32b, w.plan, w.f64b, w.status);
+  if (dexp) {
+    GP_LAUNCH(ctx, dexp_fit, 2, kDexpBlock, 0, s, w.plan, w.f64b, w.status);
+    GP_LAUNCH(ctx, dexp_decide, 1, 1, 0, s, w.plan, w.status);
+  }
   {  // cooperative launch: every block of the grid must be resident
     static int grid = 0;
     if (!grid) {
@@ -701,7 +968,7 @@ void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, 
   const uint64_t chunks = n_bound / kChunk + kMaxSeg + 1;
   GP_LAUNCH(ctx, fit_accumulate, static_cast<int>(chunks), 256, 0, s, w.plan, w.f64b, w.partial, w.status);
   GP_LAUNCH(ctx, fit_solve, kMaxSeg, 64, 0, s, w.plan, w.f64b, w.partial, w.status);
-  GP_LAUNCH(ctx, fit_emit, 1, 32, 0, s, w.plan, out, w.status);
+  GP_LAUNCH(ctx, fit_emit, 1, 32, 0, s, w.plan, out, degree, w.status);
   GP_LAUNCH(ctx, reorder_pack, grid_for(ctx, n_bound * 4, 256), 256, 0, s, w.u32b, w.plan, out, w.status);
 }
 

@@ -11,9 +11,9 @@ sweep : cmd_sweep (gradpack_main.cpp:216-267) — for every sparsifier (top-r,
         sparse gradient at wire precision, over `seeds` draws.  Same CSV.
 bench : cmd_bench (gradpack_main.cpp:269-353) — per method row: total bits and
         the median encode / decode time, measured on the device with CUDA
-        events (the reference times its CPU calls with steady_clock).  Rows the
-        device path does not run (huffman, fit-dexp, the deflate codec) are
-        reported as "unsupported"; deflate-slot runs with the Store codec.  The
+        events (the reference times its CPU calls with steady_clock).  The
+        deflate-slot row runs with the Store codec (the Deflate codec is not on
+        the device path; a row the device cannot run is reported "unsupported").  The
         rle-clustered row gathers its values from g at the clustered support
         (the CLI reuses the uniform row's values); with raw f32 values the
         container size and work are the same.

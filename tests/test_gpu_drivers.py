@@ -64,7 +64,4 @@ def test_method_bench_rows():
     assert names == [r[0] for r in BENCH_ROWS]
     for ln in lines[1:]:
         f = ln.split(",")
-        if f[0] == "fit-dexp":
-            assert f[1] == "unsupported"
-        else:
-            assert int(f[1]) > 0 and int(f[2]) > 0 and int(f[3]) > 0
+        assert int(f[1]) > 0 and int(f[2]) > 0 and int(f[3]) > 0, ln
