@@ -65,3 +65,29 @@ def test_method_bench_rows():
     for ln in lines[1:]:
         f = ln.split(",")
         assert int(f[1]) > 0 and int(f[2]) > 0 and int(f[3]) > 0, ln
+
+
+@pytest.mark.parametrize("args,im,vm,kw", [(["--index", "bitmap"], 1, 0, {}), (["--policy", "p2", "--fpr", "0.001"], 6, 0,
+                                                                                dict(fpr=0.001)),
+                                           (["--index", "huffman", "--value", "quant", "--bits", "5"], 3, 3,
+                                            dict(quant_bits=5)),
+                                           (["--index", "rle", "--value", "deflate-slot", "--codec", "store"], 2, 4,
+                                            dict(slot_codec=0))])
+def test_cli_compress_decompress(tmp_path, oracle, args, im, vm, kw):
+    """cmd_compress / cmd_decompress: the container file equals the oracle's
+    compress of the same tensor; the decompressed tensor equals to_dense."""
+    from oracle.bindings import GpConfig, synthetic_gradient
+    from paper_2102_03112_b200.cli import main, read_tensor, write_tensor
+    from paper_2102_03112_b200.dp import ratio_r
+    d = 30_000
+    g = synthetic_gradient(d, rank=3)
+    write_tensor(str(tmp_path / "g.drt"), g)
+    assert main(["compress", str(tmp_path / "g.drt"), str(tmp_path / "g.drc"), *args, "--topr", "0.01",
+                 "--seed", "7"]) == 0
+    c = (tmp_path / "g.drc").read_bytes()
+    assert c == oracle.encode_dense(g, ratio_r(d, 0.01), GpConfig.make(im, vm, seed=7, **kw))
+    assert main(["decompress", str(tmp_path / "g.drc"), str(tmp_path / "out.drt")]) == 0
+    _, sup, val = oracle.decode(c)
+    want = np.zeros(d, np.float32)
+    want[sup.astype(np.int64)] = val.astype(np.float32)
+    assert np.array_equal(read_tensor(str(tmp_path / "out.drt")), want)
