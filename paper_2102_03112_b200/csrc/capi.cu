@@ -214,7 +214,7 @@ void carve(Workspace& w, uint8_t* base, uint64_t D) {
   w.seg_dev = c.take<double>(4 * 2048);
   w.seg_arg = c.take<uint32_t>(4 * 2048);
   w.crc_cap = 2 * ((64 * D + (1 << 20)) / (64 * 256) + 64);
-  w.crc_digits = c.take<uint32_t>(5 * 256);
+  w.crc_digits = c.take<uint32_t>(9 * 256);  // 5 byte-digit shift tables + 4 lane-stride multiply tables
   w.crc_acc = c.take<uint32_t>(64);
   w.scratch = c.take<uint8_t>(2 * D);
   w.huff = c.take<HuffTable>(1);

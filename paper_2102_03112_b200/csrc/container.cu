@@ -21,6 +21,7 @@ namespace {
 
 constexpr uint32_t kPoly = 0x82F63B78u;
 constexpr int kCrcBlock = 256;
+constexpr int kCrcBlocksPerSm = 4;  // the CRC grid is fixed: sm_count * 4 blocks (the lane stride is baked into M)
 
 __device__ __forceinline__ uint32_t multmodp(uint32_t a, uint32_t b) {
   // a * b mod P in the reflected representation (bit 31 = x^0)
@@ -56,6 +57,17 @@ __device__ __forceinline__ uint32_t shift_op(const uint32_t (*D)[256], uint64_t 
   return op;
 }
 
+// Lane l of the fixed grid (kCrcLanes lanes) folds chunks l, l + kCrcLanes,
+// ... in order, carrying its running value A across the kCrcLanes * 64-byte
+// gap with one multiply by the constant x^(8 * 64 * kCrcLanes) mod P — a
+// 4-lookup byte-table product (M) — instead of one bit-serial shift per
+// chunk; a single variable shift per lane (digit tables D) carries A to the
+// end of the range.  A chunk cut short by the range end is joined with a
+// variable shift.  Tables: slice-by-4 T, constant multiply M, digits D.
+__device__ __forceinline__ uint32_t mul_const(const uint32_t (*M)[256], uint32_t v) {
+  return M[0][v & 0xFFu] ^ M[1][(v >> 8) & 0xFFu] ^ M[2][(v >> 16) & 0xFFu] ^ M[3][v >> 24];
+}
+
 __global__ void __launch_bounds__(kCrcBlock) crc_chunks(const uint8_t* __restrict__ base, const uint64_t* off_p,
                                                         uint64_t off_h, const uint64_t* len_a, const uint64_t* len_b,
                                                         const uint64_t* len_c, uint64_t len_h,
@@ -63,6 +75,7 @@ __global__ void __launch_bounds__(kCrcBlock) crc_chunks(const uint8_t* __restric
                                                         uint32_t* done, uint32_t* out, const uint32_t* status) {
   __shared__ uint32_t T[4][256];
   __shared__ uint32_t D[5][256];
+  __shared__ uint32_t M[4][256];
   __shared__ uint32_t red[kCrcBlock / 32];
   __shared__ bool last;
   if (failed(status)) return;
@@ -72,6 +85,7 @@ __global__ void __launch_bounds__(kCrcBlock) crc_chunks(const uint8_t* __restric
     T[0][i] = c;
   }
   for (int i = threadIdx.x; i < 5 * 256; i += kCrcBlock) D[i / 256][i % 256] = digits[i];
+  for (int i = threadIdx.x; i < 4 * 256; i += kCrcBlock) M[i / 256][i % 256] = digits[5 * 256 + i];
   __syncthreads();
   for (int i = threadIdx.x; i < 256; i += kCrcBlock) {
     uint32_t c = T[0][i];
@@ -87,18 +101,21 @@ __global__ void __launch_bounds__(kCrcBlock) crc_chunks(const uint8_t* __restric
   const uintptr_t a1 = a0 + len;
   const uintptr_t c0 = a0 & ~static_cast<uintptr_t>(63);
   const uint64_t nchunks = len ? (a1 - c0 + 63) / 64 : 0;
-  uint32_t x = 0;
-  for (uint64_t q = blockIdx.x * static_cast<uint64_t>(kCrcBlock) + threadIdx.x; q < nchunks;
-       q += static_cast<uint64_t>(gridDim.x) * kCrcBlock) {
+  const uint64_t lanes = static_cast<uint64_t>(gridDim.x) * kCrcBlock;  // == kCrcLanes (host)
+  uint32_t A = 0;
+  uintptr_t prev_end = 0;
+  for (uint64_t q = blockIdx.x * static_cast<uint64_t>(kCrcBlock) + threadIdx.x; q < nchunks; q += lanes) {
     const uintptr_t cs = c0 + 64 * q;
     const uintptr_t lo = cs < a0 ? a0 : cs, hi = cs + 64 > a1 ? a1 : cs + 64;
-    uint32_t c = 0;  // raw register, init 0
+    uint32_t c = 0;  // raw register of the chunk, init 0
     if (lo == cs && hi == cs + 64) {
       const uint4* p4 = reinterpret_cast<const uint4*>(cs);
+      uint4 v4[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v4[k] = p4[k];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const uint4 v = p4[k];
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        const uint32_t w[4] = {v4[k].x, v4[k].y, v4[k].z, v4[k].w};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           c ^= w[j];
@@ -109,9 +126,12 @@ __global__ void __launch_bounds__(kCrcBlock) crc_chunks(const uint8_t* __restric
       const uint8_t* b = reinterpret_cast<const uint8_t*>(lo);
       for (uintptr_t i = 0; i < hi - lo; ++i) c = (c >> 8) ^ T[0][(c ^ b[i]) & 0xFFu];
     }
-    const uint64_t after = a1 - hi;
-    x ^= after ? multmodp(shift_op(D, after), c) : c;
+    if (prev_end) A = (hi == cs + 64) ? mul_const(M, A) : multmodp(shift_op(D, hi - prev_end), A);
+    A ^= c;
+    prev_end = hi;
   }
+  const uint64_t after = prev_end ? a1 - prev_end : 0;
+  uint32_t x = after ? multmodp(shift_op(D, after), A) : A;
   for (int o = 16; o > 0; o >>= 1) x ^= __shfl_xor_sync(kFull, x, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
   __syncthreads();
@@ -235,7 +255,7 @@ void launch_crc_range(gp_ctx* ctx, const uint8_t* base, const uint64_t* off_dev,
       }
       return p;
     };
-    uint32_t tab[5 * 256];
+    uint32_t tab[9 * 256];
     uint32_t unit = 1u << 23;  // x^8: one byte
     for (int i = 0; i < 5; ++i) {
       uint32_t p = 1u << 31;
@@ -245,13 +265,19 @@ void launch_crc_range(gp_ctx* ctx, const uint8_t* base, const uint64_t* off_dev,
       }
       unit = p;  // x^(8 * 256^(i+1))
     }
+    // M[j][b] = (b at byte j) * x^(8 * 64 * lanes) mod P: the lane stride of the fixed grid
+    uint64_t stride = 64ull * static_cast<uint64_t>(ctx->sm_count) * kCrcBlocksPerSm * kCrcBlock;
+    uint32_t S = 1u << 31;
+    for (int i = 0; stride; ++i, stride >>= 8)
+      if (stride & 0xFF) S = mult(tab[i * 256 + (stride & 0xFF)], S);
+    for (int j = 0; j < 4; ++j)
+      for (int b = 0; b < 256; ++b) tab[(5 + j) * 256 + b] = b ? mult(static_cast<uint32_t>(b) << (8 * j), S) : 0u;
     cudaMemcpy(w.crc_digits, tab, sizeof(tab), cudaMemcpyHostToDevice);
     cudaMemset(w.crc_acc, 0, 2 * sizeof(uint32_t));
     w.crc_ready = true;
   }
-  const uint64_t nchunks = (len_bound + 127) / 64;
-  const int grid = static_cast<int>(std::max<uint64_t>(
-      1, std::min<uint64_t>((nchunks + kCrcBlock - 1) / kCrcBlock, static_cast<uint64_t>(ctx->sm_count) * 4)));
+  (void)len_bound;
+  const int grid = ctx->sm_count * kCrcBlocksPerSm;
   GP_LAUNCH(ctx, crc_chunks, grid, kCrcBlock, 0, s, base, off_dev, off_host, la, lb, lc, len_host, w.crc_digits,
             w.crc_acc, w.crc_acc + 1, out, w.status);
 }

@@ -109,7 +109,7 @@ struct Workspace {
   uint32_t* sort_hist = nullptr;  // global digit histograms [4][256]
   double* seg_dev = nullptr;      // segmentation sweep partials [4 * 2048]
   uint32_t* seg_arg = nullptr;    // [4 * 2048]
-  uint32_t* crc_digits = nullptr; // CRC shift-operator digit tables [5 * 256]
+  uint32_t* crc_digits = nullptr; // CRC shift-operator digit tables [5 * 256] + lane-stride multiply [4 * 256]
   uint32_t* crc_acc = nullptr;    // XOR accumulator + block counter [2]
   bool crc_ready = false;
   uint64_t crc_cap = 0;
