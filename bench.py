@@ -218,9 +218,17 @@ def native_main(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # GP_DIST_BACKEND=gloo: a functional check of the N > 1 path on a one-GPU box
+    # (ranks share the device; numbers from such a run are not bench values)
+    backend = os.environ.get("GP_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
 
     d = cfg["d"]
@@ -243,8 +251,11 @@ def native_main(args, cfg):
     else:
         codec = Codec(max_d=d, device=local)
         # N = 1: the step is one CUDA graph (replayed per step with the step's seed)
-        ex = SparseAllgather(codec, d, r, pcfg, ef=cfg.get("ef", False), graph=(world == 1 and not args.no_graph))
-        codecs = [codec]
+        # N > 1: peers' containers decode concurrently on extra contexts (rank-order scatters)
+        extra = [Codec(max_d=d, device=local) for _ in range(min(world, 4) - 1)] if world > 1 else []
+        ex = SparseAllgather(codec, d, r, pcfg, ef=cfg.get("ef", False), graph=(world == 1 and not args.no_graph),
+                             decode_codecs=extra)
+        codecs = [codec] + extra
         r_total = r
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
     stream = torch.cuda.current_stream()

@@ -160,6 +160,19 @@ GP_API int gp_decode_accumulate_dlen(gp_ctx* ctx, const uint8_t* d_container, ui
                                      const uint64_t* d_len, const gp_pipeline_config* hint,
                                      float* d_dense, uint64_t d, float scale, void* stream);
 
+/* A decode split in two for concurrent peers: gp_decode_prepare runs everything
+ * of gp_decode_accumulate_dlen but the final scatter (parse, CRC, index and
+ * value decode, validation) into the context's workspace; gp_decode_finish
+ * then applies d_dense[support[i]] += scale * value[i] from that state.  With
+ * one context per container, the prepares of several peers run concurrently
+ * on their own streams while the finishes keep the rank order of the
+ * accumulation (each finish must follow its prepare; a context holds one
+ * prepared container at a time). */
+GP_API int gp_decode_prepare(gp_ctx* ctx, const uint8_t* d_container, uint64_t cap, const uint64_t* d_len,
+                             const gp_pipeline_config* hint, void* stream);
+GP_API int gp_decode_finish(gp_ctx* ctx, const uint8_t* d_container, float* d_dense, uint64_t d, float scale,
+                            void* stream);
+
 /* unpack + decompress_gradient to sparse form.  Writes up to cap entries of
  * support (u32) and values (f64) and the count to the device word *d_count.
  * *d_dim receives the container's d. */

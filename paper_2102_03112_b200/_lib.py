@@ -63,6 +63,8 @@ _SIGS = {
     "gp_decode_accumulate": ([_vp, _vp, _u64, _vp, _u64, C.c_float, _vp], C.c_int),
     "gp_decode_accumulate_hint": ([_vp, _vp, _u64, _P(GpConfig), _vp, _u64, C.c_float, _vp], C.c_int),
     "gp_decode_accumulate_dlen": ([_vp, _vp, _u64, _vp, _P(GpConfig), _vp, _u64, C.c_float, _vp], C.c_int),
+    "gp_decode_prepare": ([_vp, _vp, _u64, _vp, _P(GpConfig), _vp], C.c_int),
+    "gp_decode_finish": ([_vp, _vp, _vp, _u64, C.c_float, _vp], C.c_int),
     "gp_decode_sparse":([_vp, _vp, _u64, _vp, _vp, _u64, _vp, _vp, _vp], C.c_int),
     "gp_top_r": ([_vp, _vp, _u64, _u64, _vp, _vp, _vp], C.c_int),
     "gp_crc32c": ([_vp, _vp, _u64, _vp, _vp], C.c_int),

@@ -275,6 +275,18 @@ class Codec:
                                                dense.numel(), float(scale), _stream(stream))
         self._raise(rc)
 
+    def decode_prepare(self, container: torch.Tensor, length: torch.Tensor, hint: PipelineConfig, stream=None):
+        """Asynchronous decode without the final scatter (parse, CRC, index and value
+        decode, validation) into this context; ``length`` is the device length word."""
+        h = hint.to_c()
+        self._raise(lib.gp_decode_prepare(self._ctx, _ptr(container), container.numel(), _ptr(length), C.byref(h),
+                                          _stream(stream)))
+
+    def decode_finish(self, container: torch.Tensor, dense: torch.Tensor, scale: float = 1.0, stream=None):
+        """dense[support] += scale * values of the container this context prepared."""
+        self._raise(lib.gp_decode_finish(self._ctx, _ptr(container), _ptr(dense), dense.numel(), float(scale),
+                                         _stream(stream)))
+
     def decompress(self, container: torch.Tensor, length: int | None = None):
         """unpack + decompress_gradient → (d, support int32 tensor, values float64 tensor)."""
         n = container.numel() if length is None else length

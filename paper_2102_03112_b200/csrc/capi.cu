@@ -541,7 +541,8 @@ int gp_encode_support(gp_ctx* ctx, const float* d_dense, uint64_t d, const uint3
 static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const uint64_t* d_len,
                          const gp_pipeline_config* hint,
                          float* d_dense, uint64_t dense_d, float scale, uint32_t* d_support, double* d_values,
-                         uint64_t cap, uint64_t* d_count, uint64_t* d_dim, void* stream, bool own = false) {
+                         uint64_t cap, uint64_t* d_count, uint64_t* d_dim, void* stream, bool own = false,
+                         bool scatter = true) {
   if (!ctx || !d_in) return set_error(ctx, GP_ERROR, "decode: null argument");
   auto s = static_cast<cudaStream_t>(stream);
   gp_pipeline_config h{};
@@ -601,8 +602,9 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const u
   }
   if ((im == GP_INDEX_NONE || im == GP_INDEX_HUFFMAN) && !own) launch_validate_support(ctx, bound, s);
   (void)dense_d;
-  GP_STAGE(ctx, ST_DEC_SCATTER, s,
-           launch_decode_scatter(ctx, d_in, bound, d_dense, scale, d_support, d_values, cap, d_count, d_dim, s));
+  if (scatter)
+    GP_STAGE(ctx, ST_DEC_SCATTER, s,
+             launch_decode_scatter(ctx, d_in, bound, d_dense, scale, d_support, d_values, cap, d_count, d_dim, s));
   return check_launch(ctx, "decode");
 }
 
@@ -623,6 +625,24 @@ int gp_decode_accumulate_hint(gp_ctx* ctx, const uint8_t* d_container, uint64_t 
                               float* d_dense, uint64_t d, float scale, void* stream) {
   return decode_common(ctx, d_container, len, nullptr, hint, d_dense, d, scale, nullptr, nullptr, 0, nullptr,
                        nullptr, stream);
+}
+
+int gp_decode_prepare(gp_ctx* ctx, const uint8_t* d_container, uint64_t cap, const uint64_t* d_len,
+                      const gp_pipeline_config* hint, void* stream) {
+  if (!hint) return set_error(ctx, GP_ERROR, "decode_prepare: needs a hint");
+  return decode_common(ctx, d_container, cap, d_len, hint, nullptr, 0, 0.0f, nullptr, nullptr, 0, nullptr, nullptr,
+                       stream, false, false);
+}
+
+int gp_decode_finish(gp_ctx* ctx, const uint8_t* d_container, float* d_dense, uint64_t d, float scale,
+                     void* stream) {
+  if (!ctx || !d_container || !d_dense) return set_error(ctx, GP_ERROR, "decode_finish: null argument");
+  auto s = static_cast<cudaStream_t>(stream);
+  (void)d;
+  GP_STAGE(ctx, ST_DEC_SCATTER, s,
+           launch_decode_scatter(ctx, d_container, ctx->max_d, d_dense, scale, nullptr, nullptr, 0, nullptr, nullptr,
+                                 s));
+  return check_launch(ctx, "decode_finish");
 }
 
 int gp_decode_sparse(gp_ctx* ctx, const uint8_t* d_container, uint64_t len, uint32_t* d_support, double* d_values,

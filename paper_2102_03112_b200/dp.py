@@ -73,7 +73,7 @@ class SparseAllgather:
     input - decode(own container) as the next step's residual."""
 
     def __init__(self, codec, d: int, r: int, cfg, group=None, device=None, ef: bool = False,
-                 graph: bool = False):
+                 graph: bool = False, decode_codecs=None):
         self.codec = codec
         self.d, self.r, self.cfg = d, r, cfg
         self.group = group
@@ -86,6 +86,13 @@ class SparseAllgather:
         self.recv = torch.empty(self.world * self.cap, dtype=torch.uint8, device=dev) if self.world > 1 else None
         self.dense = torch.zeros(d, dtype=torch.float32, device=dev)
         self.residual = torch.zeros(d, dtype=torch.float32, device=dev) if ef else None
+        # decode_codecs (N > 1, CUDA): extra contexts that decode peers concurrently,
+        # each on its own stream, up to the final scatter; the scatters then run
+        # in rank order on the step's stream (gp_decode_prepare / gp_decode_finish),
+        # so the accumulation order — and the result — is the sequential one.
+        self.dec = [codec] + list(decode_codecs or [])
+        self.dec_streams = ([torch.cuda.Stream(dev) for _ in self.dec]
+                            if len(self.dec) > 1 and torch.device(dev).type == "cuda" else None)
         # graph=True (one rank, CUDA): the whole step — pipeline seed from a device
         # step counter, encode, zero, decode — is captured once per (input,
         # output, base seed) and replayed; the step number is the only host input
@@ -155,10 +162,35 @@ class SparseAllgather:
         sizes = self.sizes.tolist()  # the one host sync of the step
         mx = max(sizes)
         dist.all_gather_into_tensor(self.recv[: n * mx], self.out[:mx], group=self.group)
-        for j in range(n):  # fixed rank order, as the harness's worker order
-            self.codec.decode_accumulate(self.recv[j * mx: j * mx + sizes[j]], out_dense, scale=1.0 / n,
-                                         hint=self.cfg, stream=stream)
+        if self.dec_streams is None:
+            for j in range(n):  # fixed rank order, as the harness's worker order
+                self.codec.decode_accumulate(self.recv[j * mx: j * mx + sizes[j]], out_dense, scale=1.0 / n,
+                                             hint=self.cfg, stream=stream)
+            return out_dense
+        main = stream if stream is not None else torch.cuda.current_stream()
+        self._decode_concurrent(n, mx, out_dense, main)
         return out_dense
+
+    def _decode_concurrent(self, n, mx, out_dense, main):
+        D = len(self.dec)
+        gathered = torch.cuda.Event()
+        gathered.record(main)
+        finished = [None] * n
+        for k in range(min(D, n)):
+            self.dec_streams[k].wait_event(gathered)
+        for j in range(n):
+            k = j % D
+            st = self.dec_streams[k]
+            if j >= D:  # the context is free once its previous container's scatter ran
+                st.wait_event(finished[j - D])
+            part = self.recv[j * mx: (j + 1) * mx]
+            self.dec[k].decode_prepare(part, self.sizes[j:j + 1], self.cfg, stream=st)
+            ready = torch.cuda.Event()
+            ready.record(st)
+            main.wait_event(ready)
+            self.dec[k].decode_finish(part, out_dense, 1.0 / n, stream=main)  # rank order
+            finished[j] = torch.cuda.Event()
+            finished[j].record(main)
 
 
 class BucketedSparseAllgather:
