@@ -253,8 +253,13 @@ def native_main(args, cfg):
         # N = 1: the step is one CUDA graph (replayed per step with the step's seed)
         # N > 1: peers' containers decode concurrently on extra contexts (rank-order scatters)
         extra = [Codec(max_d=d, device=local) for _ in range(min(world, 4) - 1)] if world > 1 else []
+        # N = 1, Bloom P0/P1/P2/Pd: the own container's index stage runs early on a second context
+        early = (Codec(max_d=d, device=local) if world == 1 and 4 <= cfg["index"] <= 7 and not cfg.get("ef")
+                 and not args.no_early else None)
         ex = SparseAllgather(codec, d, r, pcfg, ef=cfg.get("ef", False), graph=(world == 1 and not args.no_graph),
-                             decode_codecs=extra)
+                             decode_codecs=extra, early_codec=early)
+        if early is not None:
+            extra = extra + [early]
         codecs = [codec] + extra
         r_total = r
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
@@ -434,6 +439,7 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--ref-shrink", type=int, default=8, help="reference arm: d/shrink-element sample per thread")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-early", action="store_true", help="N = 1: no early index decode on a second context")
     ap.add_argument("--no-graph", action="store_true", help="N = 1: launch the step eagerly instead of as a CUDA graph")
     ap.add_argument("--streams", type=int, default=8, help="bucketed configs: codec contexts / CUDA streams")
     args = ap.parse_args()

@@ -160,6 +160,23 @@ GP_API int gp_decode_accumulate_dlen(gp_ctx* ctx, const uint8_t* d_container, ui
                                      const uint64_t* d_len, const gp_pipeline_config* hint,
                                      float* d_dense, uint64_t d, float scale, void* stream);
 
+/* Early index decode (one rank's own container, N = 1 and the own peer at
+ * N > 1): the Bloom filter payload of a container is final as soon as its
+ * encode built the filter, so its positive scan and P0/P1/P2/Pd selection can
+ * run on a second context and stream while the encode finishes (selection,
+ * values, pack).  gp_ctx_set_index_event(enc_ctx, ev) makes encode record the
+ * CUDA event `ev` at that point; gp_decode_index_prepare(dec_ctx, filter at
+ * container + 49, 26 + ceil(m/8) [+1 for Pd], d, r, method, stream) runs the
+ * index stage; gp_decode_accumulate_own(dec_ctx, ...) then decodes the finished
+ * container (parse, CRC, method check, values, scatter) with that prepared
+ * index stage.  The work is the full decode; only its schedule moves. */
+GP_API int gp_ctx_set_index_event(gp_ctx* ctx, void* event);
+GP_API int gp_decode_index_prepare(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter_len, uint64_t d,
+                                   uint64_t r, int index_method, void* stream);
+GP_API int gp_decode_accumulate_own(gp_ctx* ctx, const uint8_t* d_container, uint64_t cap, const uint64_t* d_len,
+                                    const gp_pipeline_config* hint, float* d_dense, uint64_t d, float scale,
+                                    void* stream);
+
 /* A decode split in two for concurrent peers: gp_decode_prepare runs everything
  * of gp_decode_accumulate_dlen but the final scatter (parse, CRC, index and
  * value decode, validation) into the context's workspace; gp_decode_finish

@@ -275,6 +275,24 @@ class Codec:
                                                dense.numel(), float(scale), _stream(stream))
         self._raise(rc)
 
+    def set_index_event(self, event: torch.cuda.Event | None):
+        """Encodes record ``event`` once their index payload (the Bloom filter) is final."""
+        self._raise(lib.gp_ctx_set_index_event(self._ctx, C.c_void_p(event.cuda_event) if event is not None else None))
+
+    def decode_index_prepare(self, filt: torch.Tensor, d: int, r: int, index_method: int, stream=None):
+        """The Bloom index stage (positive scan + selection) of a container's filter
+        payload ``filt``, into this context (for decode_accumulate_own)."""
+        self._raise(lib.gp_decode_index_prepare(self._ctx, _ptr(filt), filt.numel(), d, r, int(index_method),
+                                                _stream(stream)))
+
+    def decode_accumulate_own(self, container: torch.Tensor, dense: torch.Tensor, length: torch.Tensor,
+                              hint: PipelineConfig, scale: float = 1.0, stream=None):
+        """Decode of a container whose index stage this context prepared."""
+        h = hint.to_c()
+        self._raise(lib.gp_decode_accumulate_own(self._ctx, _ptr(container), container.numel(), _ptr(length),
+                                                 C.byref(h), _ptr(dense), dense.numel(), float(scale),
+                                                 _stream(stream)))
+
     def decode_prepare(self, container: torch.Tensor, length: torch.Tensor, hint: PipelineConfig, stream=None):
         """Asynchronous decode without the final scatter (parse, CRC, index and value
         decode, validation) into this context; ``length`` is the device length word."""

@@ -290,6 +290,12 @@ void gp_ctx_destroy(gp_ctx* ctx) {
   delete ctx;
 }
 
+int gp_ctx_set_index_event(gp_ctx* ctx, void* event) {
+  if (!ctx) return GP_ERROR;
+  ctx->index_event = static_cast<cudaEvent_t>(event);
+  return GP_OK;
+}
+
 int gp_ctx_set_seed_source(gp_ctx* ctx, const uint64_t* d_seed) {
   if (!ctx) return GP_ERROR;
   ctx->seed_dev = d_seed;
@@ -489,6 +495,7 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
       break;
     default: {
       GP_STAGE(ctx, ST_BLOOM_BUILD, s, launch_bloom_build(ctx, d_out, pi.m, r, s));
+      if (ctx->index_event) cudaEventRecord(ctx->index_event, s);  // the filter payload is final
       if (im == GP_INDEX_BLOOM_NAIVE) break;  // values stay in support order (pipeline.cpp:196-199)
       GP_STAGE(ctx, ST_BLOOM_SCAN, s, launch_bloom_scan(ctx, d, pi.m, false, s));
       if (im == GP_INDEX_BLOOM_P2)
@@ -709,6 +716,33 @@ int gp_bloom_positive_scan(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter
   GP_LAUNCH(ctx, copy_positions, grid_for(ctx, d, 256), 256, 0, s, ctx->ws.pos, ctx->ws.plan, d_positives, cap,
             d_count, ctx->ws.status);
   return check_launch(ctx, "positive_scan");
+}
+
+int gp_decode_index_prepare(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter_len, uint64_t d, uint64_t r,
+                            int index_method, void* stream) {
+  if (!ctx || !d_filter) return set_error(ctx, GP_ERROR, "decode_index_prepare: null argument");
+  if (index_method < GP_INDEX_BLOOM_P0 || index_method > GP_INDEX_BLOOM_PD)
+    return set_error(ctx, GP_ERROR, "decode_index_prepare: index_method must be Bloom P0, P1, P2 or Pd");
+  if (r < 1) return set_error(ctx, GP_ERROR, "decode_index_prepare: r must be >= 1");
+  auto s = static_cast<cudaStream_t>(stream);
+  const int rc = bloom_component(ctx, d_filter, filter_len, d, r, index_method, s);
+  if (rc != GP_OK) return rc;
+  if (index_method == GP_INDEX_BLOOM_P2)
+    launch_select_p2(ctx, d, ctx->ws.set_cap, 64, false, s);
+  else if (index_method == GP_INDEX_BLOOM_P1)
+    launch_select_p1(ctx, d, d, s);
+  else
+    launch_select_slice(ctx, d, s);
+  return check_launch(ctx, "decode_index_prepare");
+}
+
+int gp_decode_accumulate_own(gp_ctx* ctx, const uint8_t* d_container, uint64_t cap, const uint64_t* d_len,
+                             const gp_pipeline_config* hint, float* d_dense, uint64_t d, float scale, void* stream) {
+  if (!hint || !d_len) return set_error(ctx, GP_ERROR, "decode_accumulate_own: needs a hint and a length word");
+  if (hint->index_method < GP_INDEX_BLOOM_P0 || hint->index_method > GP_INDEX_BLOOM_PD)
+    return set_error(ctx, GP_ERROR, "decode_accumulate_own: Bloom P0, P1, P2 or Pd containers only");
+  return decode_common(ctx, d_container, cap, d_len, hint, d_dense, d, scale, nullptr, nullptr, 0, nullptr, nullptr,
+                       stream, true);
 }
 
 int gp_bloom_select(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter_len, uint64_t d, uint64_t r,

@@ -147,6 +147,7 @@ struct gp_ctx {
   uint64_t launches = 0;
   gp::Profiler prof;
   const uint64_t* seed_dev = nullptr;  // gp_ctx_set_seed_source: pipeline seed read on the device
+  cudaEvent_t index_event = nullptr;   // gp_ctx_set_index_event: recorded once encode's index payload is final
 };
 
 namespace gp {

@@ -73,7 +73,7 @@ class SparseAllgather:
     input - decode(own container) as the next step's residual."""
 
     def __init__(self, codec, d: int, r: int, cfg, group=None, device=None, ef: bool = False,
-                 graph: bool = False, decode_codecs=None):
+                 graph: bool = False, decode_codecs=None, early_codec=None):
         self.codec = codec
         self.d, self.r, self.cfg = d, r, cfg
         self.group = group
@@ -91,6 +91,21 @@ class SparseAllgather:
         # in rank order on the step's stream (gp_decode_prepare / gp_decode_finish),
         # so the accumulation order — and the result — is the sequential one.
         self.dec = [codec] + list(decode_codecs or [])
+        # early_codec (N = 1, Bloom P0/P1/P2/Pd, CUDA): the own container's index
+        # stage (positive scan + selection) runs on this second context and stream
+        # as soon as the encode has built the filter, overlapping the rest of the
+        # encode; the decode then finishes with that prepared index stage.
+        im = int(cfg.index_method)
+        self.early = (early_codec if early_codec is not None and self.world == 1 and not ef and 4 <= im <= 7
+                      and torch.device(dev).type == "cuda" else None)
+        if self.early is not None:
+            from .api import bloom_params
+            m, _ = bloom_params(cfg.fpr, r)
+            self.filter_len = 26 + (m + 7) // 8 + (1 if im == 7 else 0)
+            self.early_stream = torch.cuda.Stream(dev)
+            self.ev_index = torch.cuda.Event()
+            self.ev_index.record()  # materialise the CUDA event handle
+            self.ev_early = torch.cuda.Event()
         self.dec_streams = ([torch.cuda.Stream(dev) for _ in self.dec]
                             if len(self.dec) > 1 and torch.device(dev).type == "cuda" else None)
         # graph=True (one rank, CUDA): the whole step — pipeline seed from a device
@@ -148,6 +163,8 @@ class SparseAllgather:
 
     def step_seeded(self, grad, cfg, dense=None, stream=None):
         out_dense = self.dense if dense is None else dense
+        if self.early is not None:
+            return self._step_early(grad, cfg, out_dense, stream)
         if self.residual is not None:
             self.codec.encode_ef_into(grad, self.residual, self.r, cfg, self.out, self.length, stream=stream)
         else:
@@ -169,6 +186,23 @@ class SparseAllgather:
             return out_dense
         main = stream if stream is not None else torch.cuda.current_stream()
         self._decode_concurrent(n, mx, out_dense, main)
+        return out_dense
+
+    def _step_early(self, grad, cfg, out_dense, stream):
+        main = stream if stream is not None else torch.cuda.current_stream()
+        self.codec.set_index_event(self.ev_index)
+        try:
+            self.codec.encode_into(grad, self.r, cfg, self.out, self.length, stream=main)
+        finally:
+            self.codec.set_index_event(None)
+        side = self.early_stream
+        side.wait_event(self.ev_index)
+        self.early.decode_index_prepare(self.out[49:49 + self.filter_len], self.d, self.r,
+                                        int(self.cfg.index_method), stream=side)
+        self.ev_early.record(side)
+        out_dense.zero_()
+        main.wait_event(self.ev_early)
+        self.early.decode_accumulate_own(self.out, out_dense, self.length, self.cfg, scale=1.0, stream=main)
         return out_dense
 
     def _decode_concurrent(self, n, mx, out_dense, main):

@@ -93,3 +93,33 @@ def test_bucketed_graph_equals_eager(ef):
                 assert torch.equal(ea.residual, eb.residual)
         assert torch.equal(want, got), f"step {step}"
     assert len(graph.graphs) == 1
+
+
+@pytest.mark.parametrize("graph", [False, True])
+@pytest.mark.parametrize("kw", [dict(index_method=6, value_method=1, fpr=0.001), dict(index_method=4, value_method=0),
+                                dict(index_method=5, value_method=3), dict(index_method=7, value_method=0, pd_variant=1)])
+def test_early_index_decode_equals_plain(kw, graph):
+    """The own container's Bloom index stage run early on a second context
+    (gp_decode_index_prepare + gp_decode_accumulate_own) equals the plain
+    encode → decode step bit for bit."""
+    from paper_2102_03112_b200 import Codec, PipelineConfig
+    from paper_2102_03112_b200.dp import SparseAllgather
+    d, r = 300_001, 3_000
+    cfg = PipelineConfig(**kw)
+    ca, cb, ce = Codec(max_d=d), Codec(max_d=d), Codec(max_d=d)
+    plain = SparseAllgather(ca, d, r, cfg)
+    early = SparseAllgather(cb, d, r, cfg, graph=graph, early_codec=ce)
+    assert early.early is not None
+    g = torch.empty(d, dtype=torch.float32, device="cuda")
+    for step in [1, 2, 6]:
+        g.copy_(torch.from_numpy(synthetic_gradient(d, rank=step)))
+        want = plain.step(g, step=step).clone()
+        got = early.step(g, step=step).clone()
+        torch.cuda.synchronize()
+        for c in (ca, cb, ce):
+            c.status()
+        n = int(plain.length.item())
+        assert int(early.length.item()) == n and torch.equal(plain.out[:n], early.out[:n])
+        assert torch.equal(want, got), f"step {step}"
+    for c in (ca, cb, ce):
+        c.close()
