@@ -254,8 +254,8 @@ def native_main(args, cfg):
         # N > 1: peers' containers decode concurrently on extra contexts (rank-order scatters)
         extra = [Codec(max_d=d, device=local) for _ in range(min(world, 4) - 1)] if world > 1 else []
         # N = 1, Bloom P0/P1/P2/Pd: the own container's index stage runs early on a second context
-        early = (Codec(max_d=d, device=local) if world == 1 and 4 <= cfg["index"] <= 7 and not cfg.get("ef")
-                 and not args.no_early else None)
+        early = (Codec(max_d=d, device=local) if world == 1 and 4 <= cfg["index"] <= 7 and not args.no_early
+                 else None)
         ex = SparseAllgather(codec, d, r, pcfg, ef=cfg.get("ef", False), graph=(world == 1 and not args.no_graph),
                              decode_codecs=extra, early_codec=early)
         if early is not None:

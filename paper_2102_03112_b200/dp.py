@@ -96,7 +96,7 @@ class SparseAllgather:
         # as soon as the encode has built the filter, overlapping the rest of the
         # encode; the decode then finishes with that prepared index stage.
         im = int(cfg.index_method)
-        self.early = (early_codec if early_codec is not None and self.world == 1 and not ef and 4 <= im <= 7
+        self.early = (early_codec if early_codec is not None and self.world == 1 and 4 <= im <= 7
                       and torch.device(dev).type == "cuda" else None)
         if self.early is not None:
             from .api import bloom_params
@@ -192,7 +192,10 @@ class SparseAllgather:
         main = stream if stream is not None else torch.cuda.current_stream()
         self.codec.set_index_event(self.ev_index)
         try:
-            self.codec.encode_into(grad, self.r, cfg, self.out, self.length, stream=main)
+            if self.residual is not None:
+                self.codec.encode_ef_into(grad, self.residual, self.r, cfg, self.out, self.length, stream=main)
+            else:
+                self.codec.encode_into(grad, self.r, cfg, self.out, self.length, stream=main)
         finally:
             self.codec.set_index_event(None)
         side = self.early_stream

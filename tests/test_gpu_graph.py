@@ -95,10 +95,11 @@ def test_bucketed_graph_equals_eager(ef):
     assert len(graph.graphs) == 1
 
 
+@pytest.mark.parametrize("ef", [False, True])
 @pytest.mark.parametrize("graph", [False, True])
 @pytest.mark.parametrize("kw", [dict(index_method=6, value_method=1, fpr=0.001), dict(index_method=4, value_method=0),
                                 dict(index_method=5, value_method=3), dict(index_method=7, value_method=0, pd_variant=1)])
-def test_early_index_decode_equals_plain(kw, graph):
+def test_early_index_decode_equals_plain(kw, graph, ef):
     """The own container's Bloom index stage run early on a second context
     (gp_decode_index_prepare + gp_decode_accumulate_own) equals the plain
     encode → decode step bit for bit."""
@@ -107,8 +108,8 @@ def test_early_index_decode_equals_plain(kw, graph):
     d, r = 300_001, 3_000
     cfg = PipelineConfig(**kw)
     ca, cb, ce = Codec(max_d=d), Codec(max_d=d), Codec(max_d=d)
-    plain = SparseAllgather(ca, d, r, cfg)
-    early = SparseAllgather(cb, d, r, cfg, graph=graph, early_codec=ce)
+    plain = SparseAllgather(ca, d, r, cfg, ef=ef)
+    early = SparseAllgather(cb, d, r, cfg, graph=graph, early_codec=ce, ef=ef)
     assert early.early is not None
     g = torch.empty(d, dtype=torch.float32, device="cuda")
     for step in [1, 2, 6]:
@@ -121,5 +122,7 @@ def test_early_index_decode_equals_plain(kw, graph):
         n = int(plain.length.item())
         assert int(early.length.item()) == n and torch.equal(plain.out[:n], early.out[:n])
         assert torch.equal(want, got), f"step {step}"
+        if ef:
+            assert torch.equal(plain.residual, early.residual)
     for c in (ca, cb, ce):
         c.close()
