@@ -136,13 +136,14 @@ class SparseAllgather:
                 if keep is not None:
                     self.residual.copy_(keep)
                 torch.cuda.synchronize()
-                n0 = self.codec.launches
+                users = [self.codec] + ([self.early] if self.early is not None else [])
+                n0 = sum(c.launches for c in users)
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g):
                     s = torch.cuda.current_stream()
                     pipeline_seed_device(self.seed_dev, self.step_dev, seed, self.rank, stream=s)
                     self.step_seeded(grad, self.cfg, dense=out_dense, stream=s)
-                self.kernels_per_step = self.codec.launches - n0 + 1
+                self.kernels_per_step = sum(c.launches for c in users) - n0 + 1
             finally:
                 self.codec.set_seed_source(None)
             self.graphs[key] = g
