@@ -311,9 +311,13 @@ def native_main(args, cfg):
     else:
         length = int(ex.length.item())
 
-    # ---- profiled pass (same steps, eager: stage events need host launches)
+    # ---- profiled pass (same steps, eager: stage events need host launches; no
+    # early-decode overlap, so every stage is timed alone on the GPU)
     if graphed:
         ex.graph = False
+    early_ctx = getattr(ex, "early", None)
+    if early_ctx is not None:
+        ex.early = None
     for c in codecs:
         c.profile(True)
     stage = {}
@@ -328,6 +332,8 @@ def native_main(args, cfg):
     for c in codecs:
         c.profile(False)
     ex.graph = graphed
+    if early_ctx is not None:
+        ex.early = early_ctx
     prof_total = sum(v[0] for v in stage.values()) / args.steps
 
     # ---- e2e: host gradient in, host dense mean out, through the public API
