@@ -386,11 +386,6 @@ void launch_members_global(gp_ctx* ctx, uint64_t d_bound, uint32_t* bitmap, cuda
   Workspace& w = ctx->ws;
   using S = ScanShape<false, kLaneKeys, kLaneBatch>;
   auto* kern = bloom_members<false, kLaneKeys, kLaneBatch>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S::kStackBytes));
-    attr = true;
-  }
   const int per_sm = std::max<int>(1, std::min<int>(8, static_cast<int>((200 * 1024) / (S::kStackBytes + 1024))));
   const uint64_t nchunks = (d_bound + S::kChunk - 1) / S::kChunk;
   const int grid = static_cast<int>(std::max<uint64_t>(
@@ -410,12 +405,6 @@ void launch_bloom_scan(gp_ctx* ctx, uint64_t d_bound, uint64_t m_host, bool deco
     using S = ScanShape<true, 4, 2>;
     auto* kern = bloom_members<true, 4, 2>;
     const size_t smem = (S::kStackBytes + 15) / 16 * 16 + fbytes;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>((S::kStackBytes + 15) / 16 * 16 + kSmemFilterMax));
-      attr = true;
-    }
     const int per_sm = std::max(1, static_cast<int>((220 * 1024) / (smem + 1024)));
     const uint64_t nchunks = (d_bound + S::kChunk - 1) / S::kChunk;
     const int grid = static_cast<int>(std::max<uint64_t>(
@@ -434,6 +423,17 @@ void launch_bloom_scan(gp_ctx* ctx, uint64_t d_bound, uint64_t m_host, bool deco
 void launch_select_slice(gp_ctx* ctx, uint64_t n_bound, cudaStream_t s) {
   Workspace& w = ctx->ws;
   GP_LAUNCH(ctx, select_slice, grid_for(ctx, n_bound, 256), 256, 0, s, w.pos, w.plan, w.sel, w.status);
+}
+
+// dynamic shared-memory opt-ins of this file's kernels, on the current device
+// (gp_ctx_create runs it once per context)
+void kernel_attrs_bloom() {
+  using G = ScanShape<false, 4, 4>;
+  using M = ScanShape<true, 4, 2>;
+  cudaFuncSetAttribute(bloom_members<false, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>(G::kStackBytes));
+  cudaFuncSetAttribute(bloom_members<true, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       static_cast<int>((M::kStackBytes + 15) / 16 * 16 + kSmemFilterMax));
 }
 
 }  // namespace gp

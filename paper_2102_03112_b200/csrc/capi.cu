@@ -254,6 +254,12 @@ int gp_ctx_create(int device, uint64_t max_d, gp_ctx** out) {
   ctx->max_d = max_d;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess) {  // kernel attributes are per device: set them for this one
+    kernel_attrs_bloom();
+    kernel_attrs_p2();
+    kernel_attrs_topr();
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess) {
     delete ctx;
     return GP_CUDA;

@@ -182,6 +182,10 @@ int check_launch(gp_ctx* ctx, const char* what);
 
 // ---- host launchers, grouped by translation unit ----
 void reset_scan(gp_ctx* ctx, cudaStream_t s, uint64_t ntiles_bound);  // capi.cu
+// dynamic shared-memory opt-ins, per device (called by gp_ctx_create)
+void kernel_attrs_bloom();
+void kernel_attrs_p2();
+void kernel_attrs_topr();
 
 // topr.cu: ws.support / ws.values <- top-r of grad
 void launch_top_r(gp_ctx* ctx, const float* grad, uint64_t d, uint64_t r, cudaStream_t s, float* residual = nullptr);

@@ -588,12 +588,6 @@ void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t 
   GP_LAUNCH(ctx, p2_stage_a, grid_for(ctx, n_bound, 256), 256, 0, s, w.plan, w.flags, w.selbits, w.status);
   stage_end(ctx, s);
   stage_begin(ctx, decoding ? ST_DEC_P2_ENGINE : ST_P2_ENGINE, s);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(p2_engine_win<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBitsBytes);
-    cudaFuncSetAttribute(p2_engine_dispatch, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBitsBytes);
-    attr = true;
-  }
   if (((n_bound + 31) / 32) * 4 <= static_cast<uint64_t>(kSmemBitsBytes)) {
     GP_LAUNCH(ctx, p2_engine_win<true>, 1, 1024, ((n_bound + 31) / 32) * 4, s, w.plan, w.p2_sets, w.p2_off,
               w.p2_count, w.p2_members, w.p2_single, w.selbits, w.first_touch, w.status);
@@ -603,6 +597,11 @@ void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t 
   }
   stage_end(ctx, s);
   launch_flags_compact(ctx, GP_INDEX_BLOOM_P2, n_bound, s);
+}
+
+void kernel_attrs_p2() {
+  cudaFuncSetAttribute(p2_engine_win<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBitsBytes);
+  cudaFuncSetAttribute(p2_engine_dispatch, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBitsBytes);
 }
 
 }  // namespace gp

@@ -475,12 +475,6 @@ void launch_top_r(gp_ctx* ctx, const float* grad, uint64_t d, uint64_t r, cudaSt
   uint64_t* tiles_t = w.tiles + ntiles + 1;
   const int hist_grid = static_cast<int>(std::min<uint64_t>((d / 4 + kHistBlock - 1) / kHistBlock + 1,
                                                             static_cast<uint64_t>(ctx->sm_count)));
-  static bool attr = false;  // opt in to the 128 KiB shared histogram once per process
-  if (!attr) {
-    cudaFuncSetAttribute(topr_hist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBins * 4);
-    cudaFuncSetAttribute(topr_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBins * 4);
-    attr = true;
-  }
   if (residual) {
     GP_LAUNCH(ctx, topr_hist<true>, hist_grid, kHistBlock, kBins * 4, s, grad, residual, d, w.hist, w.status);
     grad = residual;
@@ -499,6 +493,11 @@ void launch_top_r(gp_ctx* ctx, const float* grad, uint64_t d, uint64_t r, cudaSt
   uint64_t* tiles_f = w.tiles + 2 * (ntiles + 1);
   GP_LAUNCH(ctx, topr_final, fgrid, kCandBlock, 0, s, w.cand_idx, w.cand_val, w.plan, w.support,
             w.values, tiles_f, w.ticket + 2, w.status);
+}
+
+void kernel_attrs_topr() {  // the 128 KiB shared histogram
+  cudaFuncSetAttribute(topr_hist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBins * 4);
+  cudaFuncSetAttribute(topr_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBins * 4);
 }
 
 }  // namespace gp
