@@ -610,7 +610,10 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const u
     case GP_VALUE_FIT_POLY:
     case GP_VALUE_FIT_DEXP: GP_STAGE(ctx, ST_DEC_VALUES, s, launch_decode_fit(ctx, d_in, bound, s)); break;
     case GP_VALUE_QUANT: GP_STAGE(ctx, ST_DEC_VALUES, s, launch_decode_quant(ctx, d_in, bound, s)); break;
-    case GP_VALUE_DEFLATE_SLOT: launch_decode_slot(ctx, d_in, s); break;
+    case GP_VALUE_DEFLATE_SLOT:
+      launch_decode_slot(ctx, d_in, s);
+      GP_STAGE(ctx, ST_DEC_VALUES, s, launch_decode_inflate(ctx, d_in, bound, s));
+      break;
     default: break;
   }
   if ((im == GP_INDEX_NONE || im == GP_INDEX_HUFFMAN) && !own) launch_validate_support(ctx, bound, s);

@@ -45,6 +45,7 @@ struct Plan {
   uint32_t nseg, degree;
   uint32_t q_bits, q_bucket;    // quantizer header (decode)
   uint32_t fit_kind, dexp_fail; // fit model kind (0 poly, 1 dexp); a dexp part failed (fallback)
+  uint32_t slot_id, pad2;       // byte codec of a value-id-4 slot (0 store, 1 deflate; decode)
   uint32_t seg_end[64];         // fit bounds (<= 64 segments on this path)
   float coeffs[64 * 8];
   // ---- decode
@@ -239,6 +240,7 @@ void launch_values_quant(gp_ctx* ctx, uint8_t* out, int bits, uint32_t bucket, u
 void launch_decode_quant(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, cudaStream_t s);
 void launch_values_slot(gp_ctx* ctx, uint8_t* out, uint64_t n_bound, cudaStream_t s);
 void launch_decode_slot(gp_ctx* ctx, const uint8_t* in, cudaStream_t s);
+void launch_decode_inflate(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, cudaStream_t s);
 void launch_decode_scatter(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, float* dense, float scale,
                            uint32_t* out_support, double* out_values, uint64_t cap, uint64_t* d_count,
                            uint64_t* d_dim, cudaStream_t s);

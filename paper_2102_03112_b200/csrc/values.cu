@@ -69,7 +69,10 @@ __global__ void decode_scatter(const uint8_t* __restrict__ in, const Plan* plan,
     if (blockIdx.x == 0 && threadIdx.x == 0) latch(status, GP_CAPACITY);
     return;
   }
-  const uint8_t vm = plan->value_method;
+  // an inflated Deflate slot was widened into fitv (inflate.cu)
+  const uint8_t vm = plan->value_method == GP_VALUE_DEFLATE_SLOT && plan->slot_id == 1
+                         ? static_cast<uint8_t>(GP_VALUE_FIT_POLY)
+                         : plan->value_method;
   const uint8_t* vp = in + plan->off_value;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {

@@ -182,16 +182,18 @@ __global__ void slot_encode(const float* __restrict__ values, Plan* plan, uint8_
 }
 
 // byte_decompress (codecs.cpp:268-288) + pipeline.cpp:131-133
-__global__ void slot_parse(const uint8_t* __restrict__ in, const Plan* plan, uint32_t* status) {
+__global__ void slot_parse(const uint8_t* __restrict__ in, Plan* plan, uint32_t* status) {
   if (failed(status)) return;
   const uint64_t vl = plan->vl, count = plan->n_values;
   const uint8_t* p = in + plan->off_value;
   if (vl < 9) return latch(status, GP_TRUNCATED);
   const uint8_t id = p[0];
   const uint64_t raw_len = ld_u64_unaligned(p + 1);
-  if (id == 1) return latch(status, GP_UNSUPPORTED);  // Deflate: not on the device path
-  if (id != 0) return latch(status, GP_UNKNOWN_METHOD);
-  if (vl - 9 != raw_len) return latch(status, GP_CORRUPT_PAYLOAD);
+  if (id > 1) return latch(status, GP_UNKNOWN_METHOD);
+  plan->slot_id = id;
+  // Deflate (id 1): an inflate that is not exactly 4·count bytes fails either
+  // in uncompress or in pipeline.cpp:132-133 — CorruptPayloadError both ways
+  if (id == 0 && vl - 9 != raw_len) return latch(status, GP_CORRUPT_PAYLOAD);
   if (raw_len != 4 * count) return latch(status, GP_CORRUPT_PAYLOAD);
 }
 

@@ -91,3 +91,18 @@ def test_cli_compress_decompress(tmp_path, oracle, args, im, vm, kw):
     want = np.zeros(d, np.float32)
     want[sup.astype(np.int64)] = val.astype(np.float32)
     assert np.array_equal(read_tensor(str(tmp_path / "out.drt")), want)
+
+
+def test_cli_decompress_reference_deflate(tmp_path, reference):
+    """cmd_decompress of a container the reference wrote with its default codec (Deflate)."""
+    from oracle.bindings import GpConfig, synthetic_gradient
+    from paper_2102_03112_b200.cli import main, read_tensor
+    d = 30_000
+    g = synthetic_gradient(d, rank=5)
+    c = reference.encode_dense(g, 300, GpConfig.make(1, 4, seed=7, slot_codec=1))
+    (tmp_path / "g.drc").write_bytes(c)
+    assert main(["decompress", str(tmp_path / "g.drc"), str(tmp_path / "out.drt")]) == 0
+    _, sup, val = reference.decode(c)
+    want = np.zeros(d, np.float32)
+    want[sup.astype(np.int64)] = val.astype(np.float32)
+    assert np.array_equal(read_tensor(str(tmp_path / "out.drt")), want)
