@@ -49,6 +49,19 @@ struct Bits {
   uint64_t buf;
   int cnt;
   __device__ __forceinline__ void fill() {
+    if (cnt > 56) return;
+    if (pos + 16 <= end) {  // two aligned 8-byte loads + funnel shift: whole bytes up to 57+ bits
+      const uintptr_t a = reinterpret_cast<uintptr_t>(p + pos);
+      const uint64_t* w = reinterpret_cast<const uint64_t*>(a & ~uintptr_t{7});
+      const uint32_t sh = static_cast<uint32_t>(a & 7) * 8;
+      const uint64_t w0 = __ldg(w), w1 = __ldg(w + 1);
+      const uint64_t v = sh ? (w0 >> sh) | (w1 << (64 - sh)) : w0;
+      const int k = (64 - cnt) >> 3;  // bytes that fit
+      buf |= (k >= 8 ? v : v & ((1ull << (8 * k)) - 1)) << cnt;
+      pos += k;
+      cnt += 8 * k;
+      return;
+    }
     while (cnt <= 56 && pos < end) {
       buf |= static_cast<uint64_t>(p[pos++]) << cnt;
       cnt += 8;
@@ -112,8 +125,16 @@ __device__ bool build(Code& c, const uint8_t* len, int n, int kind) {
 }
 
 // one symbol, or -1 (invalid code / input ended)
-__device__ __forceinline__ int decode(const Code& c, Bits& b) {
-  b.fill();
+// the kernel's tables and window live at namespace scope so every access is a
+// direct LDS/STS (through a reference the compiler re-derives the shared
+// window base from the CTA id on every symbol)
+__shared__ uint8_t s_win[32768];
+__shared__ Code s_lit, s_dist;
+
+template <bool kDist>
+__device__ __forceinline__ int decode(Bits& b) {
+  const Code& c = kDist ? s_dist : s_lit;
+  if (b.cnt < 15) b.fill();  // a refill (a global load) every few symbols, not on every symbol's chain
   const uint32_t e = c.lut[b.buf & ((1u << kLutBits) - 1)];
   if (e) {
     const int l = e & 15;
@@ -136,12 +157,11 @@ __device__ __forceinline__ int decode(const Code& c, Bits& b) {
 
 struct Out {
   uint8_t* dst;
-  uint8_t* win;  // 32 KiB history
   uint64_t o, cap;
   uint32_t s1, s2, run;
   __device__ __forceinline__ void put(uint8_t v) {
     dst[o] = v;
-    win[o & 32767] = v;
+    s_win[o & 32767] = v;
     ++o;
     s1 += v;
     s2 += s1;
@@ -157,8 +177,6 @@ __global__ void slot_inflate(const uint8_t* __restrict__ in, const Plan* plan, u
                              uint32_t* status) {
   if (failed(status)) return;
   if (plan->value_method != GP_VALUE_DEFLATE_SLOT || plan->slot_id != 1) return;
-  __shared__ uint8_t win[32768];
-  __shared__ Code lit, dist;
   __shared__ uint8_t lens[320];
   __shared__ uint8_t cl[19];
 #define GP_INFLATE_FAIL()                   \
@@ -167,7 +185,7 @@ __global__ void slot_inflate(const uint8_t* __restrict__ in, const Plan* plan, u
     return;                                 \
   } while (0)
   Bits b{in + plan->off_value + 9, 0, plan->vl - 9, 0, 0};
-  Out w{out, win, 0, 4 * plan->n_values, 1, 0, 0};
+  Out w{out, 0, 4 * plan->n_values, 1, 0, 0};
   // RFC 1950 header (inflate.c HEAD)
   if (!b.need(16)) GP_INFLATE_FAIL();
   const uint32_t cmf = b.take(8), flg = b.take(8);
@@ -195,9 +213,9 @@ __global__ void slot_inflate(const uint8_t* __restrict__ in, const Plan* plan, u
     if (type == 3) GP_INFLATE_FAIL();
     if (type == 1) {  // fixed codes (RFC 1951 §3.2.6)
       for (int s = 0; s < 288; ++s) lens[s] = s < 144 ? 8 : s < 256 ? 9 : s < 280 ? 7 : 8;
-      build(lit, lens, 288, kLens);
+      build(s_lit, lens, 288, kLens);
       for (int s = 0; s < 32; ++s) lens[s] = 5;
-      build(dist, lens, 32, kDists);
+      build(s_dist, lens, 32, kDists);
     } else {  // dynamic codes (inflate.c TABLE / LENLENS / CODELENS)
       if (!b.need(14)) GP_INFLATE_FAIL();
       const int nlen = static_cast<int>(b.take(5)) + 257, ndist = static_cast<int>(b.take(5)) + 1;
@@ -208,10 +226,10 @@ __global__ void slot_inflate(const uint8_t* __restrict__ in, const Plan* plan, u
         if (!b.need(3)) GP_INFLATE_FAIL();
         cl[kClOrder[k]] = static_cast<uint8_t>(b.take(3));
       }
-      if (!build(lit, cl, 19, kCodes)) GP_INFLATE_FAIL();
+      if (!build(s_lit, cl, 19, kCodes)) GP_INFLATE_FAIL();
       int have = 0;
       while (have < nlen + ndist) {
-        const int sym = decode(lit, b);
+        const int sym = decode<false>(b);
         if (sym < 0) GP_INFLATE_FAIL();
         if (sym < 16) {
           lens[have++] = static_cast<uint8_t>(sym);
@@ -235,11 +253,11 @@ __global__ void slot_inflate(const uint8_t* __restrict__ in, const Plan* plan, u
         while (copy--) lens[have++] = l;
       }
       if (lens[256] == 0) GP_INFLATE_FAIL();  // missing end-of-block code
-      if (!build(lit, lens, nlen, kLens)) GP_INFLATE_FAIL();
-      if (!build(dist, lens + nlen, ndist, kDists)) GP_INFLATE_FAIL();
+      if (!build(s_lit, lens, nlen, kLens)) GP_INFLATE_FAIL();
+      if (!build(s_dist, lens + nlen, ndist, kDists)) GP_INFLATE_FAIL();
     }
     for (;;) {
-      int sym = decode(lit, b);
+      int sym = decode<false>(b);
       if (sym < 0) GP_INFLATE_FAIL();
       if (sym < 256) {
         if (w.o >= w.cap) GP_INFLATE_FAIL();
@@ -251,13 +269,23 @@ __global__ void slot_inflate(const uint8_t* __restrict__ in, const Plan* plan, u
       if (sym >= 29) GP_INFLATE_FAIL();  // symbols 286, 287
       if (!b.need(kLenExtra[sym])) GP_INFLATE_FAIL();
       const uint32_t len = kLenBase[sym] + b.take(kLenExtra[sym]);
-      const int ds = decode(dist, b);
+      const int ds = decode<true>(b);
       if (ds < 0 || ds >= 30) GP_INFLATE_FAIL();
       if (!b.need(kDistExtra[ds])) GP_INFLATE_FAIL();
       const uint32_t dd = kDistBase[ds] + b.take(kDistExtra[ds]);
       if (dd > w.o) GP_INFLATE_FAIL();  // too far back (no dictionary)
       if (w.o + len > w.cap) GP_INFLATE_FAIL();
-      for (uint32_t k = 0; k < len; ++k) w.put(win[(w.o - dd) & 32767]);
+      uint32_t k = 0;
+      if (dd >= 8) {  // source bytes all precede the destination run: batch the window loads
+        for (; k + 8 <= len; k += 8) {
+          uint8_t t[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) t[j] = s_win[(w.o - dd + j) & 32767];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) w.put(t[j]);
+        }
+      }
+      for (; k < len; ++k) w.put(s_win[(w.o - dd) & 32767]);
     }
   }
   // RFC 1950 trailer: Adler-32 of the output, big-endian, at the next byte

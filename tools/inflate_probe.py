@@ -7,7 +7,9 @@ from paper_2102_03112_b200 import Codec
 
 ref = reference()
 codec = Codec(max_d=1 << 22)
-for d, r in [(1_000_000, 10_000), (4_000_000, 400_000)]:
+import sys
+sizes = [(1_000_000, 10_000)] if "--small" in sys.argv else [(1_000_000, 10_000), (4_000_000, 400_000)]
+for d, r in sizes:
     g = synthetic_gradient(d, rank=1)
     for slot in (0, 1):
         c = ref.encode_dense(g, r, GpConfig.make(1, 4, seed=3, slot_codec=slot))
