@@ -130,11 +130,16 @@ struct ScanState {
   uint32_t* ticket;  // zeroed before the scan
 };
 
+// GPU-scope relaxed accesses (a volatile access compiles to a system-scope
+// strong one, which the descriptors never need: producers and consumers are
+// CTAs of the same grid)
 __device__ __forceinline__ void st_volatile(uint64_t* p, uint64_t v) {
-  *reinterpret_cast<volatile uint64_t*>(p) = v;
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ uint64_t ld_volatile(const uint64_t* p) {
-  return *reinterpret_cast<const volatile uint64_t*>(p);
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
 // Called by warp 0 of the block after the block aggregate is known.
@@ -193,6 +198,55 @@ __device__ __forceinline__ uint64_t tile_exclusive_offset(uint64_t count, uint32
   tile_total = total;
   __syncthreads();
   return prefix + local;
+}
+
+// One block: in-place exclusive scan of per-chunk counts (`b` may be null).
+// For passes with thousands of small chunks a separate count pass + this scan
+// replaces the decoupled look-back, whose chain of L2 round trips dominates
+// when every chunk carries little work.  Counts and prefixes are < 2^32 (they
+// count u32-indexed keys), so 8192 of them are staged as u32 in shared memory:
+// coalesced loads, one block scan over per-thread runs of kPer, coalesced stores.
+template <int kPer>
+__global__ void __launch_bounds__(1024) scan_chunk_counts(uint64_t* a, uint64_t* b, uint64_t n,
+                                                          const uint32_t* status) {
+  __shared__ uint64_t sh[40];
+  __shared__ uint32_t st[1024 * kPer];
+  if (failed(status)) return;
+  for (int k = 0; k < 2; ++k) {
+    uint64_t* x = k == 0 ? a : b;
+    if (x == nullptr) continue;
+    uint64_t carry = 0;
+    for (uint64_t base = 0; base < n; base += 1024 * kPer) {
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const uint64_t i = base + q * 1024 + threadIdx.x;
+        st[q * 1024 + threadIdx.x] = i < n ? static_cast<uint32_t>(x[i]) : 0u;
+      }
+      __syncthreads();
+      uint32_t v[kPer];
+      uint64_t sum = 0;
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        v[q] = st[threadIdx.x * kPer + q];
+        sum += v[q];
+      }
+      uint64_t tot;
+      uint64_t e = block_exclusive_sum<uint64_t, 1024>(sum, sh, tot);  // ends with a barrier
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        st[threadIdx.x * kPer + q] = static_cast<uint32_t>(e);
+        e += v[q];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const uint64_t i = base + q * 1024 + threadIdx.x;
+        if (i < n) x[i] = carry + st[q * 1024 + threadIdx.x];
+      }
+      carry += tot;
+      __syncthreads();
+    }
+  }
 }
 
 // ---------------------------------------------------------------- misc

@@ -89,23 +89,21 @@ __global__ void bitmap_check(const uint8_t* __restrict__ in, Plan* plan, uint32_
 
 // ordered extraction of set bits, 4 KiB of bitmap per tile.  Warp w of a tile
 // owns bytes [512w, 512w + 512) in four rounds of 128 bytes (4 per lane, so
-// the byte loads are coalesced); a round's <= 1024 positions are staged in the
-// warp's shared slice in order and then stored with consecutive lanes on
-// consecutive sel entries (a per-lane position loop stores 32 scattered runs
-// per instruction, ~5x the sectors at 60% density).
+// the byte loads are coalesced).  Emission is transposed: for each of the
+// round's 32 words, the lanes whose bit is set store at their rank in the word,
+// so every store instruction writes one contiguous run (a per-lane ffs loop
+// stores 32 scattered runs per instruction and stalls on FLO/STS latency).
 __global__ void __launch_bounds__(kTileBlock) bitmap_support(const uint8_t* __restrict__ in, Plan* plan,
                                                              uint32_t* sel, uint64_t* tiles, uint32_t* ticket,
                                                              uint64_t cap, uint32_t* status) {
   constexpr int kRounds = kTileItems / 4;
   __shared__ uint64_t sh[36];
   __shared__ uint32_t slot;
-  __shared__ uint32_t stage[kTileBlock / 32][1024];
   if (failed(status) || plan->index_method != GP_INDEX_BITMAP) return;
   const uint64_t nbytes = plan->il;
   const uint8_t* p = in + plan->off_index;
   const uint64_t ntiles = (nbytes + kTile - 1) / kTile;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* st = stage[warp];
   while (true) {
     const uint32_t tile = claim_tile(ticket, &slot);
     if (tile >= ntiles) break;
@@ -126,6 +124,7 @@ __global__ void __launch_bounds__(kTileBlock) bitmap_support(const uint8_t* __re
     uint64_t tot;
     uint64_t o = tile_exclusive_offset<kTileBlock>(lane == 0 ? wc : 0, tile, tiles, sh, tot);
     o = __shfl_sync(kFull, o, 0);
+    const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
     for (int q = 0; q < kRounds; ++q) {
       const uint32_t n = __popc(x[q]);
@@ -136,13 +135,27 @@ __global__ void __launch_bounds__(kTileBlock) bitmap_support(const uint8_t* __re
         if (lane >= k) incl += t;
       }
       const uint32_t total = __shfl_sync(kFull, incl, 31);
-      uint32_t e = incl - n;
-      const uint32_t bit0 = static_cast<uint32_t>(8 * (wbase + q * 128 + 4 * lane));
-      for (uint32_t v = x[q]; v; v &= v - 1) st[e++] = bit0 + static_cast<uint32_t>(__ffs(v) - 1);
-      __syncwarp();
-      for (uint32_t i = lane; i < total; i += 32)
-        if (o + i < cap) sel[o + i] = st[i];
-      __syncwarp();
+      const uint32_t excl = incl - n;
+      // transposed emission: word k's set bits are written by the lanes whose
+      // bit is set, each at its rank in the word -> one contiguous run per word
+      const uint32_t bit0 = static_cast<uint32_t>(8 * (wbase + q * 128));
+      if (__reduce_max_sync(kFull, n) <= 8) {  // sparse round: each lane stores its own few bits
+        uint64_t at = o + excl;
+        for (uint32_t v = x[q]; v; v &= v - 1, ++at)
+          if (at < cap) sel[at] = bit0 + 32u * lane + static_cast<uint32_t>(__ffs(v) - 1);
+        o += total;
+        continue;
+      }
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) {
+        const uint32_t wk = __shfl_sync(kFull, x[q], k);
+        if (wk == 0) continue;  // warp-uniform: sparse bitmaps skip their empty words
+        const uint32_t ok = __shfl_sync(kFull, excl, k);
+        if (wk >> lane & 1u) {
+          const uint64_t at = o + ok + __popc(wk & lt);
+          if (at < cap) sel[at] = bit0 + 32u * k + lane;
+        }
+      }
       o += total;
     }
     if (tile == ntiles - 1 && threadIdx.x == kTileBlock - 1) {

@@ -50,25 +50,50 @@ __device__ __forceinline__ uint32_t put_varint(uint8_t* grp, uint64_t x) {
 }
 
 // ---------------------------------------------------------------- encode
-__global__ void __launch_bounds__(kBlock) rle_starts(const uint32_t* __restrict__ sup, uint64_t r,
-                                                     uint32_t* __restrict__ starts, Plan* plan, uint64_t* tiles,
-                                                     uint32_t* ticket, const uint32_t* status) {
-  __shared__ uint64_t sh[36];
-  __shared__ uint32_t slot;
+// chain starts of the ascending support: i == 0 or sup[i-1] + 1 != sup[i]
+__device__ __forceinline__ uint32_t start_mask(const uint32_t* __restrict__ sup, uint64_t r, uint64_t base) {
+  uint32_t mask = 0;
+#pragma unroll
+  for (int q = 0; q < kItems; ++q) {
+    const uint64_t i = base + q;
+    if (i < r && (i == 0 || sup[i - 1] + 1 != sup[i])) mask |= 1u << q;
+  }
+  return mask;
+}
+
+// Starts are few (one per 1-run) and the support is long (r/4096 tiles), so
+// the per-tile work is small and a look-back chain across thousands of tiles
+// dominated; per-tile counts + one scan (scan_chunk_counts) place them instead.
+__global__ void __launch_bounds__(kBlock) rle_starts_count(const uint32_t* __restrict__ sup, uint64_t r,
+                                                           uint64_t* counts, const uint32_t* status) {
+  __shared__ uint32_t wc[kBlock / 32];
   if (failed(status)) return;
   const uint64_t ntiles = (r + kTile - 1) / kTile;
-  while (true) {
-    const uint32_t tile = claim_tile(ticket, &slot);
-    if (tile >= ntiles) break;
-    const uint64_t base = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(threadIdx.x) * kItems;
-    uint32_t mask = 0;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t c = __reduce_add_sync(kFull, __popc(start_mask(sup, r, tile * kTile + threadIdx.x * kItems)));
+    if ((threadIdx.x & 31) == 0) wc[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint64_t t = 0;
 #pragma unroll
-    for (int q = 0; q < kItems; ++q) {
-      const uint64_t i = base + q;
-      if (i < r && (i == 0 || sup[i - 1] + 1 != sup[i])) mask |= 1u << q;
+      for (int w = 0; w < kBlock / 32; ++w) t += wc[w];
+      counts[tile] = t;
     }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) rle_starts(const uint32_t* __restrict__ sup, uint64_t r,
+                                                     uint32_t* __restrict__ starts, Plan* plan,
+                                                     const uint64_t* tile_offs, const uint32_t* status) {
+  __shared__ uint64_t sh[36];
+  if (failed(status)) return;
+  const uint64_t ntiles = (r + kTile - 1) / kTile;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint64_t base = tile * kTile + static_cast<uint64_t>(threadIdx.x) * kItems;
+    uint32_t mask = start_mask(sup, r, base);
     uint64_t tot;
-    uint64_t o = tile_exclusive_offset<kBlock>(__popc(mask), tile, tiles, sh, tot);
+    uint64_t o = tile_offs[tile] + block_exclusive_sum<uint64_t, kBlock>(__popc(mask), sh, tot);
     while (mask) {
       const int q = __ffs(mask) - 1;
       starts[o++] = static_cast<uint32_t>(base + q);
@@ -330,37 +355,68 @@ __global__ void __launch_bounds__(kBlock) rle_bitmap(const Plan* plan, uint32_t*
   }
 }
 
-// set bits of the bitmap → ascending support (sel), n_sel; popcount must be r
+// set bits of the bitmap → ascending support (sel), n_sel; popcount must be r.
+// Warp w of a tile owns words [512w, 512w + 512) in 16 rounds of 32 (lane l
+// on word 32q + l: coalesced loads); emission is transposed as in
+// bitmap_support (indexcodec.cu): for each word of a round the lanes whose
+// bit is set store at their rank, one contiguous run per store instruction.
 __global__ void __launch_bounds__(kBlock) rle_support(const uint32_t* __restrict__ words, Plan* plan,
                                                       uint32_t* __restrict__ sel, uint64_t cap, uint64_t* tiles,
                                                       uint32_t* ticket, const uint32_t* status) {
+  constexpr int kRounds = kItems;
   __shared__ uint64_t sh[36];
   __shared__ uint32_t slot;
   if (failed(status) || plan->index_method != GP_INDEX_RLE) return;
   const uint64_t nw = (plan->d + 31) / 32;
   const uint64_t ntiles = (nw + kTile - 1) / kTile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
   while (true) {
     const uint32_t tile = claim_tile(ticket, &slot);
     if (tile >= ntiles) break;
-    const uint64_t base = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(threadIdx.x) * kItems;
-    uint32_t x[kItems];
-    uint64_t c = 0;
+    const uint64_t wbase = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(warp) * (32 * kRounds);
+    uint32_t x[kRounds];
+    uint32_t c = 0;
 #pragma unroll
-    for (int q = 0; q < kItems; ++q) {
-      x[q] = base + q < nw ? words[base + q] : 0u;
+    for (int q = 0; q < kRounds; ++q) {
+      const uint64_t w = wbase + 32 * q + lane;
+      x[q] = w < nw ? words[w] : 0u;
       c += __popc(x[q]);
     }
+    const uint32_t wc = __reduce_add_sync(kFull, c);
     uint64_t tot;
-    uint64_t o = tile_exclusive_offset<kBlock>(c, tile, tiles, sh, tot);
+    uint64_t o = tile_exclusive_offset<kBlock>(lane == 0 ? wc : 0, tile, tiles, sh, tot);
+    o = __shfl_sync(kFull, o, 0);
 #pragma unroll
-    for (int q = 0; q < kItems; ++q) {
-      uint32_t y = x[q];
-      while (y) {
-        const int b = __ffs(y) - 1;
-        if (o < cap) sel[o] = static_cast<uint32_t>(32 * (base + q) + b);
-        ++o;
-        y &= y - 1;
+    for (int q = 0; q < kRounds; ++q) {
+      const uint32_t n = __popc(x[q]);
+      uint32_t incl = n;
+#pragma unroll
+      for (int k = 1; k < 32; k <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, incl, k);
+        if (lane >= k) incl += t;
       }
+      const uint32_t total = __shfl_sync(kFull, incl, 31);
+      const uint32_t excl = incl - n;
+      const uint32_t bit0 = static_cast<uint32_t>(32 * (wbase + 32 * q));
+      if (__reduce_max_sync(kFull, n) <= 8) {  // sparse round: each lane stores its own few bits
+        uint64_t at = o + excl;
+        for (uint32_t v = x[q]; v; v &= v - 1, ++at)
+          if (at < cap) sel[at] = bit0 + 32u * lane + static_cast<uint32_t>(__ffs(v) - 1);
+        o += total;
+        continue;
+      }
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) {
+        const uint32_t wk = __shfl_sync(kFull, x[q], k);
+        if (wk == 0) continue;
+        const uint32_t ok = __shfl_sync(kFull, excl, k);
+        if (wk >> lane & 1u) {
+          const uint64_t at = o + ok + __popc(wk & lt);
+          if (at < cap) sel[at] = bit0 + 32u * k + lane;
+        }
+      }
+      o += total;
     }
     if (tile == ntiles - 1 && threadIdx.x == kBlock - 1) {
       plan->n_sel = o;
@@ -381,9 +437,11 @@ __global__ void rle_reset(unsigned long long* first) { *first = ~0ULL; }
 void launch_index_rle(gp_ctx* ctx, uint8_t* out, uint64_t d, uint64_t r, cudaStream_t s) {
   Workspace& w = ctx->ws;
   const uint64_t rt = (r + kTile - 1) / kTile;
-  reset_scan(ctx, s, rt + 1);
+  GP_LAUNCH(ctx, rle_starts_count, grid_for(ctx, rt * kBlock, kBlock), kBlock, 0, s, w.support, r, w.tiles,
+            w.status);
+  GP_LAUNCH(ctx, scan_chunk_counts<8>, 1, 1024, 0, s, w.tiles, nullptr, rt, w.status);
   GP_LAUNCH(ctx, rle_starts, grid_for(ctx, rt * kBlock, kBlock), kBlock, 0, s, w.support, r, w.u32a, w.plan, w.tiles,
-            w.ticket, w.status);
+            w.status);
   reset_scan(ctx, s, rt + 1);
   GP_LAUNCH(ctx, rle_sizes, grid_for(ctx, rt * kBlock, kBlock), kBlock, 0, s, w.support, r, d, w.u32a, w.plan, w.u32b,
             w.tiles, w.ticket, w.status);

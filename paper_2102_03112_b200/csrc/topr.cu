@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(1024) topr_pick_bin(const uint32_t* __restrict
 // writes directly.
 constexpr int kCandBlock = 256;
 constexpr int kCandWarps = kCandBlock / 32;
-constexpr int kWarpCandCap = 384;
+constexpr int kWarpCandCap = 512;  // = one 512-key warp segment: dense segments never overflow
 constexpr int kWarpTieCap = 192;
 
 // One 128-key row of a warp: lane l holds keys 4l..4l+3 (one float4).  Ballots
@@ -215,7 +215,7 @@ __device__ __forceinline__ void stream_segment(const float* __restrict__ g, uint
 __global__ void __launch_bounds__(kCandBlock) topr_candidates(
     const float* __restrict__ g, uint64_t d, uint64_t chunk, const Plan* __restrict__ plan, uint32_t* cidx,
     float* cval, uint32_t* sidx, float* sval, uint32_t* tidx, float* tval, uint64_t* tiles_c, uint64_t* tiles_t,
-    uint32_t* ticket, const uint32_t* status) {
+    uint32_t* ticket, bool counted, const uint32_t* status) {
   __shared__ uint32_t bidx[kCandWarps][kWarpCandCap];
   __shared__ float bval[kCandWarps][kWarpCandCap];
   __shared__ uint32_t tbidx[kCandWarps][kWarpTieCap];
@@ -269,7 +269,12 @@ __global__ void __launch_bounds__(kCandBlock) topr_candidates(
       bc += wc[w];
       bt += wt[w];
     }
-    if (warp == 0) {
+    if (counted) {  // dense selections: exclusive chunk offsets from topr_count_chunks + scan_chunk_counts
+      if (threadIdx.x == 0) {
+        s_pc = tiles_c[c];
+        s_pt = full ? 0 : tiles_t[c];
+      }
+    } else if (warp == 0) {
       const uint64_t p = lookback_warp(tiles_c, c, bc);
       if (lane == 0) s_pc = p;
     } else if (warp == 1 && !full) {
@@ -300,6 +305,46 @@ __global__ void __launch_bounds__(kCandBlock) topr_candidates(
             tval[pt + o] = v;
           });
     }
+  }
+}
+
+// Dense selections (r > d/16): the candidates pass over 4096-key chunks would
+// spend most of its time in the look-back chain (thousands of chunks, each
+// walking back over aggregates at L2 latency), so the chunk counts come from
+// their own streaming pass and one scan instead.
+__global__ void __launch_bounds__(kCandBlock) topr_count_chunks(const float* __restrict__ g, uint64_t d,
+                                                                const Plan* __restrict__ plan, uint64_t* cnt_c,
+                                                                uint64_t* cnt_t, const uint32_t* status) {
+  __shared__ uint32_t wc[kCandWarps], wt[kCandWarps];
+  if (failed(status)) return;
+  const uint32_t bstar = plan->bin_star;
+  const uint32_t klo = bstar << kShift, khi = (bstar + 1) << kShift;
+  const bool full = plan->full_bin != 0;
+  const bool aligned = (reinterpret_cast<uintptr_t>(g) & 15) == 0;
+  const uint64_t nchunks = (d + 4095) / 4096;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const uint64_t lo = c * 4096 + warp * 512 < d ? c * 4096 + warp * 512 : d;
+    const uint64_t hi = lo + 512 < d ? lo + 512 : d;
+    uint32_t nc, nt;
+    stream_segment(g, lo, hi, aligned, klo, khi, !full, nc, nt, [](uint32_t, uint32_t, float) {},
+                   [](uint32_t, uint32_t, float) {});
+    if (lane == 0) {
+      wc[warp] = nc;
+      wt[warp] = nt;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint64_t a = 0, b = 0;
+#pragma unroll
+      for (int w = 0; w < kCandWarps; ++w) {
+        a += wc[w];
+        b += wt[w];
+      }
+      cnt_c[c] = a;
+      cnt_t[c] = b;
+    }
+    __syncthreads();
   }
 }
 
@@ -483,10 +528,19 @@ void launch_top_r(gp_ctx* ctx, const float* grad, uint64_t d, uint64_t r, cudaSt
   }
   GP_LAUNCH(ctx, topr_pick_bin, 1, 1024, 0, s, w.hist, r, w.plan, w.status);
   const uint64_t nblk = static_cast<uint64_t>(ctx->sm_count) * 4;
-  const uint64_t chunk = std::max<uint64_t>(4096, ((d + nblk - 1) / nblk + 4095) / 4096 * 4096);  // multiple of 8 warps * 512
+  // multiple of 8 warps * 512.  Dense selections (r > d/16, e.g. natural
+  // sparsity with r = nnz) take 4096-key chunks: one 512-key segment per warp
+  // fits the staging buffers, so no segment is streamed twice.
+  const uint64_t chunk = r > d / 16 ? 4096 : std::max<uint64_t>(4096, ((d + nblk - 1) / nblk + 4095) / 4096 * 4096);
   const int grid = static_cast<int>(std::max<uint64_t>(1, (d + chunk - 1) / chunk));
+  const bool counted = r > d / 16;
+  if (counted) {
+    GP_LAUNCH(ctx, topr_count_chunks, ctx->sm_count * 8, kCandBlock, 0, s, grad, d, w.plan, tiles_c, tiles_t,
+              w.status);
+    GP_LAUNCH(ctx, scan_chunk_counts<8>, 1, 1024, 0, s, tiles_c, tiles_t, static_cast<uint64_t>(grid), w.status);
+  }
   GP_LAUNCH(ctx, topr_candidates, grid, kCandBlock, 0, s, grad, d, chunk, w.plan, w.cand_idx, w.cand_val, w.support,
-            w.values, w.u32a, reinterpret_cast<float*>(w.u32b), tiles_c, tiles_t, w.ticket, w.status);
+            w.values, w.u32a, reinterpret_cast<float*>(w.u32b), tiles_c, tiles_t, w.ticket, counted, w.status);
   GP_LAUNCH(ctx, topr_refine, 1, 1024, 0, s, w.u32a, reinterpret_cast<const float*>(w.u32b), w.hist, r,
             w.plan, w.status);
   // final filter: its own scan state (tiles after both previous arrays)
