@@ -50,28 +50,32 @@ __device__ __forceinline__ uint32_t put_varint(uint8_t* grp, uint64_t x) {
 }
 
 // ---------------------------------------------------------------- encode
-// chain starts of the ascending support: i == 0 or sup[i-1] + 1 != sup[i]
-__device__ __forceinline__ uint32_t start_mask(const uint32_t* __restrict__ sup, uint64_t r, uint64_t base) {
-  uint32_t mask = 0;
-#pragma unroll
-  for (int q = 0; q < kItems; ++q) {
-    const uint64_t i = base + q;
-    if (i < r && (i == 0 || sup[i - 1] + 1 != sup[i])) mask |= 1u << q;
-  }
-  return mask;
+// chain starts of the ascending support: i == 0 or sup[i-1] + 1 != sup[i].
+// Warp w of a tile owns entries [512w, 512w + 512) in 16 rounds of 32, lane l
+// on entry 32q + l (coalesced; the predecessor comes from the lane below).
+// Returns the round's start ballot.
+__device__ __forceinline__ uint32_t start_ballot(const uint32_t* __restrict__ sup, uint64_t r, uint64_t i) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t cur = i < r ? sup[i] : 0u;
+  uint32_t prev = __shfl_up_sync(kFull, cur, 1);
+  if (lane == 0 && i > 0 && i < r) prev = sup[i - 1];
+  return __ballot_sync(kFull, i < r && (i == 0 || prev + 1 != cur));
 }
 
-// Starts are few (one per 1-run) and the support is long (r/4096 tiles), so
-// the per-tile work is small and a look-back chain across thousands of tiles
-// dominated; per-tile counts + one scan (scan_chunk_counts) place them instead.
+// Starts are few (one per 1-run) and the support is long (r/4096 tiles):
+// per-tile counts + one scan (scan_chunk_counts) place them.
 __global__ void __launch_bounds__(kBlock) rle_starts_count(const uint32_t* __restrict__ sup, uint64_t r,
                                                            uint64_t* counts, const uint32_t* status) {
   __shared__ uint32_t wc[kBlock / 32];
   if (failed(status)) return;
   const uint64_t ntiles = (r + kTile - 1) / kTile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint32_t c = __reduce_add_sync(kFull, __popc(start_mask(sup, r, tile * kTile + threadIdx.x * kItems)));
-    if ((threadIdx.x & 31) == 0) wc[threadIdx.x >> 5] = c;
+    const uint64_t wb = tile * kTile + static_cast<uint64_t>(warp) * (32 * kItems);
+    uint32_t c = 0;
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) c += __popc(start_ballot(sup, r, wb + 32 * q + lane));
+    if (lane == 0) wc[warp] = c;
     __syncthreads();
     if (threadIdx.x == 0) {
       uint64_t t = 0;
@@ -89,15 +93,24 @@ __global__ void __launch_bounds__(kBlock) rle_starts(const uint32_t* __restrict_
   __shared__ uint64_t sh[36];
   if (failed(status)) return;
   const uint64_t ntiles = (r + kTile - 1) / kTile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint64_t base = tile * kTile + static_cast<uint64_t>(threadIdx.x) * kItems;
-    uint32_t mask = start_mask(sup, r, base);
+    const uint64_t wb = tile * kTile + static_cast<uint64_t>(warp) * (32 * kItems);
+    uint32_t bal[kItems];
+    uint32_t c = 0;
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+      bal[q] = start_ballot(sup, r, wb + 32 * q + lane);
+      c += __popc(bal[q]);
+    }
     uint64_t tot;
-    uint64_t o = tile_offs[tile] + block_exclusive_sum<uint64_t, kBlock>(__popc(mask), sh, tot);
-    while (mask) {
-      const int q = __ffs(mask) - 1;
-      starts[o++] = static_cast<uint32_t>(base + q);
-      mask &= mask - 1;
+    uint64_t o = tile_offs[tile] + block_exclusive_sum<uint64_t, kBlock>(lane == 0 ? c : 0, sh, tot);
+    o = __shfl_sync(kFull, o, 0);
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+      if (bal[q] >> lane & 1u) starts[o + __popc(bal[q] & lt)] = static_cast<uint32_t>(wb + 32 * q + lane);
+      o += __popc(bal[q]);
     }
     if (tile == ntiles - 1 && threadIdx.x == kBlock - 1) plan->n_runs = o;
   }
@@ -114,15 +127,17 @@ __global__ void __launch_bounds__(kBlock) rle_sizes(const uint32_t* __restrict__
   const uint64_t R = plan->n_runs;
   const uint64_t lead = sup[0] > 0 ? vgroups(sup[0]) : 0;  // the leading 0-run
   const uint64_t ntiles = (R + kTile - 1) / kTile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   while (true) {
     const uint32_t tile = claim_tile(ticket, &slot);
     if (tile >= ntiles) break;
-    const uint64_t base = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(threadIdx.x) * kItems;
+    // warp rounds: lane l on chain wb + 32q + l (coalesced loads of starts)
+    const uint64_t wb = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(warp) * (32 * kItems);
     uint32_t g[kItems];
-    uint64_t sum = 0;
+    uint32_t sum = 0;
 #pragma unroll
     for (int q = 0; q < kItems; ++q) {
-      const uint64_t k = base + q;
+      const uint64_t k = wb + 32 * q + lane;
       g[q] = 0;
       if (k < R) {
         const uint64_t i0 = starts[k], i1 = k + 1 < R ? starts[k + 1] : r;
@@ -132,12 +147,16 @@ __global__ void __launch_bounds__(kBlock) rle_sizes(const uint32_t* __restrict__
       }
       sum += g[q];
     }
+    const uint32_t wsum = __reduce_add_sync(kFull, sum);
     uint64_t tot;
-    uint64_t o = tile_exclusive_offset<kBlock>(sum, tile, tiles, sh, tot) + lead;
+    uint64_t o = tile_exclusive_offset<kBlock>(lane == 0 ? wsum : 0, tile, tiles, sh, tot) + lead;
+    o = __shfl_sync(kFull, o, 0);
 #pragma unroll
     for (int q = 0; q < kItems; ++q) {
-      if (base + q < R) goff[base + q] = static_cast<uint32_t>(o);
-      o += g[q];
+      const uint32_t incl = warp_inclusive_sum(g[q]);
+      const uint64_t k = wb + 32 * q + lane;
+      if (k < R) goff[k] = static_cast<uint32_t>(o + incl - g[q]);
+      o += __shfl_sync(kFull, incl, 31);
     }
     if (tile == ntiles - 1 && threadIdx.x == kBlock - 1) {
       plan->n_groups = o;
