@@ -21,18 +21,32 @@ __global__ void gather_values(const float* __restrict__ dense, const uint32_t* _
     values[i] = dense[sel[i]];
 }
 
+// 4 values per thread per step, blockDim apart (each store instruction stays
+// coalesced) with all four loads issued ahead of the stores: one value per
+// thread leaves too few bytes in flight for HBM.
 __global__ void values_raw_encode(const float* __restrict__ values, Plan* plan, uint8_t* out, int f64,
                                   const uint32_t* status) {
   if (failed(status)) return;
   const uint64_t n = plan->n_values;
   uint8_t* p = out + 49 + plan->il;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    if (f64) {
-      const double v = static_cast<double>(values[i]);
-      st_u64_unaligned(p + 8 * i, static_cast<uint64_t>(__double_as_longlong(v)));
-    } else {
-      st_u32_unaligned(p + 4 * i, __float_as_uint(values[i]));
+  const uint64_t step = 4ull * gridDim.x * blockDim.x;
+  for (uint64_t i0 = 4ull * blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += step) {
+    float v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t i = i0 + static_cast<uint64_t>(q) * blockDim.x;
+      v[q] = i < n ? values[i] : 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t i = i0 + static_cast<uint64_t>(q) * blockDim.x;
+      if (i >= n) break;
+      if (f64) {
+        const double dv = static_cast<double>(v[q]);
+        st_u64_unaligned(p + 8 * i, static_cast<uint64_t>(__double_as_longlong(dv)));
+      } else {
+        st_u32_unaligned(p + 4 * i, __float_as_uint(v[q]));
+      }
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -74,14 +88,34 @@ __global__ void decode_scatter(const uint8_t* __restrict__ in, const Plan* plan,
                          ? static_cast<uint8_t>(GP_VALUE_FIT_POLY)
                          : plan->value_method;
   const uint8_t* vp = in + plan->off_value;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint32_t s = sel[i];
-    const double v = i < nv ? value_at(vp, vm, fitv, i) : 0.0;
-    if (dense) dense[s] = fmaf(scale, static_cast<float>(v), dense[s]);
-    if (out_support) {
-      out_support[i] = s;
-      out_values[i] = v;
+  // 4 coordinates per thread per step, blockDim apart (coalesced per
+  // instruction): selections, values and the dense reads of all four are
+  // issued before the dependent read-modify-writes
+  const uint64_t step = 4ull * gridDim.x * blockDim.x;
+  for (uint64_t i0 = 4ull * blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += step) {
+    uint32_t s[4];
+    double v[4];
+    float dv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t i = i0 + static_cast<uint64_t>(q) * blockDim.x;
+      s[q] = i < n ? sel[i] : 0u;
+      v[q] = i < n && i < nv ? value_at(vp, vm, fitv, i) : 0.0;
+    }
+    if (dense) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (i0 + static_cast<uint64_t>(q) * blockDim.x < n) dv[q] = dense[s[q]];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t i = i0 + static_cast<uint64_t>(q) * blockDim.x;
+      if (i >= n) break;
+      if (dense) dense[s[q]] = fmaf(scale, static_cast<float>(v[q]), dv[q]);
+      if (out_support) {
+        out_support[i] = s[q];
+        out_values[i] = v[q];
+      }
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
