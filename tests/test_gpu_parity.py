@@ -66,6 +66,27 @@ def test_top_r_bit_exact(codec, oracle):
             assert np.array_equal(val.cpu().numpy().view(np.uint32), g[want].view(np.uint32))
 
 
+def test_top_r_dense_selections(codec, oracle):
+    """r > d/16 takes the counted candidates path (topr.cu): natural sparsity
+    with r = nnz and its neighbours, 64-wide zero rows (C3's shape), half-dense
+    ties, and an input pointer that is not 16-byte aligned."""
+    rng = np.random.default_rng(5)
+    for d in [4096 * 3 + 17, 100_000, 1_000_003]:
+        g = synthetic_gradient(d, rank=2)
+        rows = rng.random((d + 63) // 64) < 0.4
+        g[np.repeat(rows, 64)[:d]] = 0.0
+        nnz = int(np.count_nonzero(g))
+        ties = np.round(g * 2).astype(np.float32)
+        for x in (g, ties):
+            for r in sorted({nnz - 1, nnz, min(d, nnz + 1), d // 16 + 1, d // 2}):
+                sup, val = codec.top_r(_dev(x), r)
+                want = oracle.top_r(x, r)
+                assert np.array_equal(sup.cpu().numpy().astype(np.uint32), want), (d, r)
+        buf = _dev(np.concatenate([np.zeros(1, np.float32), g]))
+        sup, _ = codec.top_r(buf[1:], nnz)
+        assert np.array_equal(sup.cpu().numpy().astype(np.uint32), oracle.top_r(g, nnz)), d
+
+
 def test_crc32c_bit_exact(codec, oracle):
     rng = np.random.default_rng(1)
     for n in [0, 1, 9, 1023, 1024, 1025, 262143, 262144, 262145, 3_000_001]:
