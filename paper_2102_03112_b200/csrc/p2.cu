@@ -349,8 +349,10 @@ __device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __res
                                                uint32_t* first_touch, uint32_t* status) {
   extern __shared__ uint32_t sbits[];
   __shared__ uint64_t sh[40];
-  __shared__ uint32_t s_min[32];
-  __shared__ uint32_t s_val;
+  // per-round block results: one barrier each (shared atomicMin / the single
+  // writer) instead of a three-barrier block reduction
+  __shared__ uint32_t s_vstar, s_rejv, s_cut;
+  __shared__ uint64_t s_cdraw;
   if (failed(status) || !p2_active(plan)) return;
   constexpr uint32_t W = 1024;
   const uint32_t v = threadIdx.x;
@@ -368,23 +370,13 @@ __device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __res
   const uint64_t seed = hash64(plan->seed_a, plan->seed_b);  // derive_selection_seed (pipeline.cpp:23-25)
   uint64_t rpos = 0, cursor = 0, last_progress = 0;
 
-  auto block_min = [&](uint32_t x) -> uint32_t {
-    for (int o = 16; o > 0; o >>= 1) x = min(x, __shfl_xor_sync(kFull, x, o));
-    if ((v & 31) == 0) s_min[v >> 5] = x;
-    __syncthreads();
-    if (v < 32) {
-      uint32_t y = s_min[v];
-      for (int o = 16; o > 0; o >>= 1) y = min(y, __shfl_xor_sync(kFull, y, o));
-      if (v == 0) s_val = y;
-    }
-    __syncthreads();
-    const uint32_t res = s_val;
-    __syncthreads();
-    return res;
-  };
-
   constexpr uint32_t kM = 8;  // members of a visit held in registers (larger sets re-read memory)
   while (nsel < r && L > 0) {
+    if (v == 0) {  // the previous round read these before its closing barrier
+      s_vstar = W;
+      s_rejv = W;
+      s_cut = W;
+    }
     const uint64_t si = start + (cursor + v) % L;
     const uint32_t bit = sets[si];
     const uint32_t sz = size[bit];
@@ -426,7 +418,9 @@ __device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __res
         if (!bs_test(bits, p) && first_touch[p] < v) dep = true;
       }
     }
-    const uint32_t vstar = block_min(dep ? v : W);
+    if (dep) atomicMin(&s_vstar, v);
+    __syncthreads();
+    const uint32_t vstar = s_vstar;
     // RNG positions of the independent prefix
     const bool draw = v < vstar && cnt >= 2;
     uint64_t dtot;
@@ -439,7 +433,9 @@ __device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __res
       val = rng_at(seed, rpos + dpos);
       rej = val > bound;
     }
-    const uint32_t rejv = block_min(rej ? v : W);
+    if (rej) atomicMin(&s_rejv, v);
+    __syncthreads();
+    const uint32_t rejv = s_rejv;
     const uint32_t limit = min(vstar, rejv == W ? W : rejv + 1);
     uint64_t extra = 0;  // positions consumed beyond one by the rejecting visit
     if (draw && v < limit) {
@@ -457,7 +453,9 @@ __device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __res
     uint64_t stot;
     const uint64_t spos = block_exclusive_sum<uint64_t, 1024>(sel ? 1 : 0, sh, stot);
     const uint64_t need = r - nsel;
-    const uint32_t cut = block_min(sel && spos + 1 == need ? v + 1 : W);
+    if (sel && spos + 1 == need) s_cut = v + 1;  // at most one visit: spos rises along the selections
+    __syncthreads();
+    const uint32_t cut = s_cut;
     const uint32_t climit = min(limit, cut);
     // commit
     if (sel && v < climit) {  // the target-th smallest unselected member (buckets are unsorted)
@@ -485,11 +483,13 @@ __device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __res
         }
       }
     }
-    // totals over the committed visits
-    uint64_t csel, cdraw;
-    block_exclusive_sum<uint64_t, 1024>((sel && v < climit) ? 1 : 0, sh, csel);
-    block_exclusive_sum<uint64_t, 1024>((draw && v < climit) ? 1 + extra : 0, sh, cdraw);
+    // totals over the committed visits [0, climit), climit >= 1: the
+    // selections are min(stot, need) (the cut is the need-th); the draws up to
+    // visit climit - 1 inclusive, which is the rejecting visit if one commits
+    const uint64_t csel = stot < need ? stot : need;
+    if (v == climit - 1) s_cdraw = dpos + (draw ? 1 + extra : 0);
     __syncthreads();
+    const uint64_t cdraw = s_cdraw;
     nsel += csel;
     rpos += cdraw;
     cursor += climit;
