@@ -352,7 +352,7 @@ __device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __res
   // per-round block results: one barrier each (shared atomicMin / the single
   // writer) instead of a three-barrier block reduction
   __shared__ uint32_t s_vstar, s_rejv, s_cut;
-  __shared__ uint64_t s_cdraw;
+  __shared__ uint64_t s_cdraw, s_csel;
   if (failed(status) || !p2_active(plan)) return;
   constexpr uint32_t W = 1024;
   const uint32_t v = threadIdx.x;
@@ -423,8 +423,13 @@ __device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __res
     const uint32_t vstar = s_vstar;
     // RNG positions of the independent prefix
     const bool draw = v < vstar && cnt >= 2;
-    uint64_t dtot;
-    const uint64_t dpos = block_exclusive_sum<uint64_t, 1024>(draw ? 1 : 0, sh, dtot);
+    // one scan for both prefixes: draws (low half) and visits with an
+    // unselected member (high half) — below `limit` the latter are exactly
+    // the selecting visits, so the selection prefix needs no second scan
+    uint64_t tot2;
+    const uint64_t pk = block_exclusive_sum<uint64_t, 1024>((draw ? 1ull : 0ull) | (cnt >= 1 ? 1ull << 32 : 0ull),
+                                                            sh, tot2);
+    const uint64_t dpos = pk & 0xFFFFFFFFull, spos = pk >> 32;
     uint32_t target = 0;
     bool rej = false;
     uint64_t bound = 0, val = 0;
@@ -450,8 +455,6 @@ __device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __res
     }
     // selections of the prefix and the r cut
     const bool sel = v < limit && cnt >= 1;
-    uint64_t stot;
-    const uint64_t spos = block_exclusive_sum<uint64_t, 1024>(sel ? 1 : 0, sh, stot);
     const uint64_t need = r - nsel;
     if (sel && spos + 1 == need) s_cut = v + 1;  // at most one visit: spos rises along the selections
     __syncthreads();
@@ -483,12 +486,15 @@ __device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __res
         }
       }
     }
-    // totals over the committed visits [0, climit), climit >= 1: the
-    // selections are min(stot, need) (the cut is the need-th); the draws up to
-    // visit climit - 1 inclusive, which is the rejecting visit if one commits
-    const uint64_t csel = stot < need ? stot : need;
-    if (v == climit - 1) s_cdraw = dpos + (draw ? 1 + extra : 0);
+    // totals over the committed visits [0, climit), climit >= 1, from its
+    // last visit: selections = its inclusive selection prefix, draws = its
+    // inclusive draw prefix (it is the rejecting visit if one commits)
+    if (v == climit - 1) {
+      s_csel = spos + (cnt >= 1 ? 1 : 0);
+      s_cdraw = dpos + (draw ? 1 + extra : 0);
+    }
     __syncthreads();
+    const uint64_t csel = s_csel;
     const uint64_t cdraw = s_cdraw;
     nsel += csel;
     rpos += cdraw;
