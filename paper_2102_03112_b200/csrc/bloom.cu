@@ -284,7 +284,9 @@ __global__ void __launch_bounds__(kScanBlock) bloom_members(const uint32_t* __re
     members_body<false, kLaneKeys, kLaneBatch, S::kCap>(words, plan, bitmap, dyn);
 }
 
-// ordered compaction of the membership bitmap: 16 words per thread
+// ordered compaction of the membership bitmap: 16 words per thread, in warp
+// rounds (lane l on word 32q + l of its warp's 512: coalesced loads); P is
+// ~1% of d, so each lane stores its own few bits at its rank
 __global__ void __launch_bounds__(kScanBlock) members_compact(const uint32_t* __restrict__ bitmap, Plan* plan,
                                                               uint32_t* __restrict__ pos_out, uint64_t cap,
                                                               uint64_t* tiles, uint32_t* ticket,
@@ -297,28 +299,31 @@ __global__ void __launch_bounds__(kScanBlock) members_compact(const uint32_t* __
   const uint64_t nwd = (plan->d + 31) / 32;
   constexpr int kW = 16;
   const uint64_t ntiles = (nwd + kScanBlock * kW - 1) / (kScanBlock * kW);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   while (true) {
     const uint32_t tile = claim_tile(ticket, &slot);
     if (tile >= ntiles) break;
-    const uint64_t w0 = static_cast<uint64_t>(tile) * kScanBlock * kW + static_cast<uint64_t>(threadIdx.x) * kW;
+    const uint64_t wb = static_cast<uint64_t>(tile) * kScanBlock * kW + static_cast<uint64_t>(warp) * (32 * kW);
     uint32_t v[kW];
-    uint64_t c = 0;
+    uint32_t c = 0;
 #pragma unroll
     for (int i = 0; i < kW; ++i) {
-      v[i] = w0 + i < nwd ? bitmap[w0 + i] : 0u;
+      const uint64_t w = wb + 32 * i + lane;
+      v[i] = w < nwd ? bitmap[w] : 0u;
       c += __popc(v[i]);
     }
+    const uint32_t wc = __reduce_add_sync(kFull, c);
     uint64_t tot;
-    uint64_t o = tile_exclusive_offset<kScanBlock>(c, tile, tiles, sh, tot);
+    uint64_t o = tile_exclusive_offset<kScanBlock>(lane == 0 ? wc : 0, tile, tiles, sh, tot);
+    o = __shfl_sync(kFull, o, 0);
 #pragma unroll
     for (int i = 0; i < kW; ++i) {
-      uint32_t x = v[i];
-      while (x) {
-        const int b = __ffs(x) - 1;
-        if (o < cap) pos_out[o] = static_cast<uint32_t>(32 * (w0 + i) + b);
-        ++o;
-        x &= x - 1;
-      }
+      const uint32_t n = __popc(v[i]);
+      const uint32_t incl = warp_inclusive_sum(n);
+      uint64_t at = o + incl - n;
+      for (uint32_t x = v[i]; x; x &= x - 1, ++at)
+        if (at < cap) pos_out[at] = static_cast<uint32_t>(32 * (wb + 32 * i + lane) + (__ffs(x) - 1));
+      o += __shfl_sync(kFull, incl, 31);
     }
     if (tile == ntiles - 1 && threadIdx.x == kScanBlock - 1) plan->n_pos = o;
   }
