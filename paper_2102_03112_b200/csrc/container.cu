@@ -79,57 +79,62 @@ __global__ void __launch_bounds__(kCrcBlock) crc_chunks(const uint8_t* __restric
   __shared__ uint32_t red[kCrcBlock / 32];
   __shared__ bool last;
   if (failed(status)) return;
-  for (int i = threadIdx.x; i < 256; i += kCrcBlock) {
-    uint32_t c = static_cast<uint32_t>(i);
-    for (int j = 0; j < 8; ++j) c = (c >> 1) ^ ((c & 1u) ? kPoly : 0u);
-    T[0][i] = c;
-  }
-  for (int i = threadIdx.x; i < 5 * 256; i += kCrcBlock) D[i / 256][i % 256] = digits[i];
-  for (int i = threadIdx.x; i < 4 * 256; i += kCrcBlock) M[i / 256][i % 256] = digits[5 * 256 + i];
-  __syncthreads();
-  for (int i = threadIdx.x; i < 256; i += kCrcBlock) {
-    uint32_t c = T[0][i];
-    for (int k = 1; k < 4; ++k) {
-      c = (c >> 8) ^ T[0][c & 0xFFu];
-      T[k][i] = c;
-    }
-  }
-  __syncthreads();
   const uint64_t off = off_p ? *off_p : off_h;
   const uint64_t len = range_len(len_a, len_b, len_c, len_h);
   const uintptr_t a0 = reinterpret_cast<uintptr_t>(base + off);
   const uintptr_t a1 = a0 + len;
   const uintptr_t c0 = a0 & ~static_cast<uintptr_t>(63);
   const uint64_t nchunks = len ? (a1 - c0 + 63) / 64 : 0;
-  const uint64_t lanes = static_cast<uint64_t>(gridDim.x) * kCrcBlock;  // == kCrcLanes (host)
+  // blocks without chunks (most of the fixed grid for a small container) skip
+  // the table setup and only join the reduction
+  const bool active = static_cast<uint64_t>(blockIdx.x) * kCrcBlock < nchunks;
   uint32_t A = 0;
   uintptr_t prev_end = 0;
-  for (uint64_t q = blockIdx.x * static_cast<uint64_t>(kCrcBlock) + threadIdx.x; q < nchunks; q += lanes) {
-    const uintptr_t cs = c0 + 64 * q;
-    const uintptr_t lo = cs < a0 ? a0 : cs, hi = cs + 64 > a1 ? a1 : cs + 64;
-    uint32_t c = 0;  // raw register of the chunk, init 0
-    if (lo == cs && hi == cs + 64) {
-      const uint4* p4 = reinterpret_cast<const uint4*>(cs);
-      uint4 v4[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) v4[k] = p4[k];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t w[4] = {v4[k].x, v4[k].y, v4[k].z, v4[k].w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          c ^= w[j];
-          c = T[3][c & 0xFFu] ^ T[2][(c >> 8) & 0xFFu] ^ T[1][(c >> 16) & 0xFFu] ^ T[0][c >> 24];
-        }
-      }
-    } else {
-      const uint8_t* b = reinterpret_cast<const uint8_t*>(lo);
-      for (uintptr_t i = 0; i < hi - lo; ++i) c = (c >> 8) ^ T[0][(c ^ b[i]) & 0xFFu];
+  if (active) {
+    for (int i = threadIdx.x; i < 256; i += kCrcBlock) {
+      uint32_t c = static_cast<uint32_t>(i);
+      for (int j = 0; j < 8; ++j) c = (c >> 1) ^ ((c & 1u) ? kPoly : 0u);
+      T[0][i] = c;
     }
-    if (prev_end) A = (hi == cs + 64) ? mul_const(M, A) : multmodp(shift_op(D, hi - prev_end), A);
-    A ^= c;
-    prev_end = hi;
-  }
+    for (int i = threadIdx.x; i < 5 * 256; i += kCrcBlock) D[i / 256][i % 256] = digits[i];
+    for (int i = threadIdx.x; i < 4 * 256; i += kCrcBlock) M[i / 256][i % 256] = digits[5 * 256 + i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += kCrcBlock) {
+      uint32_t c = T[0][i];
+      for (int k = 1; k < 4; ++k) {
+        c = (c >> 8) ^ T[0][c & 0xFFu];
+        T[k][i] = c;
+      }
+    }
+    __syncthreads();
+    const uint64_t lanes = static_cast<uint64_t>(gridDim.x) * kCrcBlock;  // == kCrcLanes (host)
+    for (uint64_t q = blockIdx.x * static_cast<uint64_t>(kCrcBlock) + threadIdx.x; q < nchunks; q += lanes) {
+      const uintptr_t cs = c0 + 64 * q;
+      const uintptr_t lo = cs < a0 ? a0 : cs, hi = cs + 64 > a1 ? a1 : cs + 64;
+      uint32_t c = 0;  // raw register of the chunk, init 0
+      if (lo == cs && hi == cs + 64) {
+        const uint4* p4 = reinterpret_cast<const uint4*>(cs);
+        uint4 v4[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v4[k] = p4[k];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t w[4] = {v4[k].x, v4[k].y, v4[k].z, v4[k].w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            c ^= w[j];
+            c = T[3][c & 0xFFu] ^ T[2][(c >> 8) & 0xFFu] ^ T[1][(c >> 16) & 0xFFu] ^ T[0][c >> 24];
+          }
+        }
+      } else {
+        const uint8_t* b = reinterpret_cast<const uint8_t*>(lo);
+        for (uintptr_t i = 0; i < hi - lo; ++i) c = (c >> 8) ^ T[0][(c ^ b[i]) & 0xFFu];
+      }
+      if (prev_end) A = (hi == cs + 64) ? mul_const(M, A) : multmodp(shift_op(D, hi - prev_end), A);
+      A ^= c;
+      prev_end = hi;
+    }
+  }  // active
   const uint64_t after = prev_end ? a1 - prev_end : 0;
   uint32_t x = after ? multmodp(shift_op(D, after), A) : A;
   for (int o = 16; o > 0; o >>= 1) x ^= __shfl_xor_sync(kFull, x, o);
@@ -146,7 +151,9 @@ __global__ void __launch_bounds__(kCrcBlock) crc_chunks(const uint8_t* __restric
   if (last && threadIdx.x == 0) {  // the final block folds in the init term
     __threadfence();
     const uint32_t raw = *reinterpret_cast<volatile uint32_t*>(acc);
-    *out = len ? (raw ^ multmodp(shift_op(D, len), 0xFFFFFFFFu) ^ 0xFFFFFFFFu) : 0u;
+    // an inactive last block has no shared tables: read the digits directly
+    const uint32_t(*Dg)[256] = active ? D : reinterpret_cast<const uint32_t(*)[256]>(digits);
+    *out = len ? (raw ^ multmodp(shift_op(Dg, len), 0xFFFFFFFFu) ^ 0xFFFFFFFFu) : 0u;
     *acc = 0;   // ready for the next range
     *done = 0;
   }
