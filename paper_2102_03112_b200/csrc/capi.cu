@@ -208,8 +208,8 @@ void carve(Workspace& w, uint8_t* base, uint64_t D) {
   w.f64a = c.take<double>(D);
   w.f64b = c.take<double>(D);
   w.partial = c.take<double>((D / 2048 + 128) * 44);
-  w.sort_table = c.take<uint32_t>(2 * 256 * (D / 2048 + 2));  // per-tile digit aggregates + inclusive prefixes
-  w.sort_flags = c.take<uint32_t>(64 + D / 2048 + 2);         // 8 tickets, 1024 histogram bins follow below
+  w.sort_table = c.take<uint32_t>(2 * 256 * (D / kSortTileKeys + 2));  // per-tile digit aggregates + inclusive prefixes
+  w.sort_flags = c.take<uint32_t>(64 + D / kSortTileKeys + 2);        // 8 tickets, 1024 histogram bins follow below
   w.sort_hist = c.take<uint32_t>(4 * 256);
   w.seg_dev = c.take<double>(4 * 2048);
   w.seg_arg = c.take<uint32_t>(4 * 2048);

@@ -55,6 +55,7 @@ struct Plan {
 };
 
 constexpr int kMaxSeg = 64;
+constexpr uint64_t kSortTileKeys = 2048;  // radix sort tile (sort.cu kTile): sizes sort_table / sort_flags
 
 struct HuffTable;  // huffman.cuh
 

@@ -23,6 +23,7 @@ namespace {
 constexpr int kBlock = 256;
 constexpr int kItems = 8;
 constexpr int kTile = kBlock * kItems;
+static_assert(kTile == kSortTileKeys, "the workspace sizes the per-tile tables for kSortTileKeys");
 constexpr int kSortWarps = kBlock / 32;
 
 // digit histograms of passes [0, npass) over the keys (shared bins, warp-aggregated)
