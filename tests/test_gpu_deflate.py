@@ -132,15 +132,12 @@ def test_raw_length_mismatches(codec, reference):
         assert _same(_device_decode(codec, c), _ref_decode(reference, c))
 
 
-def test_error_paths(codec, reference):
-    """Hand-built malformed streams: each rejected by zlib and by the device with the same class."""
-    g = synthetic_gradient(2000, rank=4)
-    base = reference.encode_dense(g, 64, GpConfig.make(BITMAP, SLOT, seed=1, slot_codec=0))
-    raw = _raw_of(base)
+def _error_cases(raw: bytes) -> dict:
+    """One malformed stream per zlib rejection rule the device mirrors."""
     good = zlib.compress(raw, 6)
     fixed = zlib.compressobj(6, zlib.DEFLATED, 15, 8, zlib.Z_FIXED)
     fixed = fixed.compress(raw) + fixed.flush()
-    cases = {
+    return {
         "truncated_header": good[:1],
         "bad_fcheck": bytes([good[0], good[1] ^ 1]) + good[2:],
         "cm7": bytes([0x77, (31 - (0x7700 % 31)) % 31]) + good[2:],
@@ -157,7 +154,14 @@ def test_error_paths(codec, reference):
         "fixed_truncated": fixed[:-6],
         "empty": b"",
     }
-    for name, body in cases.items():
+
+
+def test_error_paths(codec, reference):
+    """Hand-built malformed streams: each rejected by zlib and by the device with the same class."""
+    g = synthetic_gradient(2000, rank=4)
+    base = reference.encode_dense(g, 64, GpConfig.make(BITMAP, SLOT, seed=1, slot_codec=0))
+    raw = _raw_of(base)
+    for name, body in _error_cases(raw).items():
         c = _with_body(reference, base, body, len(raw))
         want = _ref_decode(reference, c)
         assert want == "CorruptPayloadError", (name, want)
