@@ -137,6 +137,10 @@ __global__ void __launch_bounds__(kCrcBlock) crc_chunks(const uint8_t* __restric
   }  // active
   const uint64_t after = prev_end ? a1 - prev_end : 0;
   uint32_t x = after ? multmodp(shift_op(D, after), A) : A;
+  // the init term x^(8 len) * 0xFFFFFFFF joins the XOR reduction from block 0
+  // (active whenever len > 0, tables in shared memory), so the last block
+  // — often one without tables — only applies the final inversion
+  if (active && blockIdx.x == 0 && threadIdx.x == 0) x ^= multmodp(shift_op(D, len), 0xFFFFFFFFu);
   for (int o = 16; o > 0; o >>= 1) x ^= __shfl_xor_sync(kFull, x, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
   __syncthreads();
@@ -148,12 +152,10 @@ __global__ void __launch_bounds__(kCrcBlock) crc_chunks(const uint8_t* __restric
     last = atomicAdd(done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {  // the final block folds in the init term
+  if (last && threadIdx.x == 0) {  // the final block applies the final inversion
     __threadfence();
     const uint32_t raw = *reinterpret_cast<volatile uint32_t*>(acc);
-    // an inactive last block has no shared tables: read the digits directly
-    const uint32_t(*Dg)[256] = active ? D : reinterpret_cast<const uint32_t(*)[256]>(digits);
-    *out = len ? (raw ^ multmodp(shift_op(Dg, len), 0xFFFFFFFFu) ^ 0xFFFFFFFFu) : 0u;
+    *out = len ? (raw ^ 0xFFFFFFFFu) : 0u;
     *acc = 0;   // ready for the next range
     *done = 0;
   }

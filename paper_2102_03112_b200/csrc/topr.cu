@@ -382,15 +382,35 @@ __global__ void __launch_bounds__(1024) topr_refine(const uint32_t* __restrict__
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      uint64_t rem = remaining;
-      int dig = 255;
-      for (; dig > 0; --dig) {
-        if (rem <= h[dig]) break;
-        rem -= h[dig];
+    // digit of the remaining-th key from the top: dig = the largest digit
+    // with rem <= h[dig] after subtracting the digits above it (digit 0 if none
+    // above it qualifies).  Warp 0, lane l owning digits 255-8l .. 248-8l: a
+    // warp scan of the lane sums from the top finds the crossing lane, which
+    // walks its eight digits — the same result as the sequential walk down
+    // from 255, without 255 dependent shared-memory steps.
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      uint32_t cnt[8];
+      uint64_t sum = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        cnt[u] = h[255 - 8 * lane - u];
+        sum += cnt[u];
       }
-      s_digit = static_cast<uint32_t>(dig);
-      s_rem = rem;
+      const uint64_t incl = warp_inclusive_sum(sum);
+      const unsigned cross = __ballot_sync(kFull, incl >= remaining);
+      const int owner = cross ? __ffs(cross) - 1 : 31;
+      if (lane == owner) {
+        uint64_t rem = remaining - (incl - sum);
+        int dig = 255 - 8 * lane;
+#pragma unroll
+        for (int u = 0; u < 8; ++u, --dig) {
+          if (dig == 0 || rem <= cnt[u]) break;
+          rem -= cnt[u];
+        }
+        s_digit = static_cast<uint32_t>(dig);
+        s_rem = rem;
+      }
     }
     __syncthreads();
     prefix |= s_digit << sh_bits;
