@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(kBlock) radix_onesweep(const uint32_t* __restr
         uint32_t f = kInc;
         if (p >= 0) {
           do {
-            f = *reinterpret_cast<volatile uint32_t*>(&flags[p]);
+            f = ld_relaxed_u32(&flags[p]);
           } while (f < kAgg);
         }
         const unsigned im = __ballot_sync(kFull, p < 0 || f == kInc);
