@@ -584,7 +584,7 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const u
     if (st != GP_OK) return st;
     return set_error(ctx, GP_UNSUPPORTED, "method not implemented on the device path");
   }
-  if (!known) return check_launch(ctx, "decode");  // verify_container latches UnknownMethod
+  if (!known) return check_launch(ctx, "decode");  // the CRC verdict step latches UnknownMethod
   const uint64_t bound = ctx->max_d;
   if (own && im != GP_INDEX_BLOOM_NAIVE) {
     if (!is_bloom(im)) launch_own_support(ctx, bound, s);

@@ -57,6 +57,46 @@ __device__ __forceinline__ uint32_t shift_op(const uint32_t (*D)[256], uint64_t 
   return op;
 }
 
+// Header (container.cpp:62-73) + CRC trailer (:77-80); lengths from the plan.
+// Run by the CRC kernel's last block once the CRC is known (one thread).
+__device__ void finish_body(uint8_t* out, uint64_t cap, uint64_t* d_len, Plan* plan, uint32_t crc,
+                            uint32_t* status) {
+  const uint64_t total = 49 + plan->il + plan->vl + plan->rl + 4;
+  if (total > cap) return latch(status, GP_CAPACITY);
+  out[0] = 'D';
+  out[1] = 'R';
+  out[2] = 'C';
+  out[3] = '1';
+  out[4] = 1;
+  out[5] = 0;
+  out[6] = plan->index_method;
+  out[7] = plan->value_method;
+  out[8] = plan->rl ? 1 : 0;
+  st_u64_unaligned(out + 9, plan->d);
+  st_u64_unaligned(out + 17, plan->r);
+  st_u64_unaligned(out + 25, plan->il);
+  st_u64_unaligned(out + 33, plan->vl);
+  st_u64_unaligned(out + 41, plan->rl);
+  st_u32_unaligned(out + total - 4, crc);
+  plan->total_len = total;
+  if (d_len) *d_len = total;
+}
+
+// the CRC verdict of unpack, then the post-CRC checks parse_container deferred
+__device__ void verify_body(Plan* plan, uint32_t crc, uint32_t* status) {
+  if (static_cast<uint64_t>(crc) != plan->crc_stored) return latch(status, GP_CHECKSUM);
+  if (plan->post_crc_error) latch(status, plan->post_crc_error);
+}
+
+// what the CRC kernel's last block does with the result
+struct CrcEpilogue {
+  int mode = 0;  // 0 store only, 1 verify (unpack), 2 finish (pack)
+  Plan* plan = nullptr;
+  uint8_t* out = nullptr;
+  uint64_t cap = 0;
+  uint64_t* d_len = nullptr;
+};
+
 // Lane l of the fixed grid (kCrcLanes lanes) folds chunks l, l + kCrcLanes,
 // ... in order, carrying its running value A across the kCrcLanes * 64-byte
 // gap with one multiply by the constant x^(8 * 64 * kCrcLanes) mod P — a
@@ -72,7 +112,8 @@ __global__ void __launch_bounds__(kCrcBlock) crc_chunks(const uint8_t* __restric
                                                         uint64_t off_h, const uint64_t* len_a, const uint64_t* len_b,
                                                         const uint64_t* len_c, uint64_t len_h,
                                                         const uint32_t* __restrict__ digits, uint32_t* acc,
-                                                        uint32_t* done, uint32_t* out, const uint32_t* status) {
+                                                        uint32_t* done, uint32_t* out, const CrcEpilogue ep,
+                                                        uint32_t* status) {
   __shared__ uint32_t T[4][256];
   __shared__ uint32_t D[5][256];
   __shared__ uint32_t M[4][256];
@@ -155,40 +196,12 @@ __global__ void __launch_bounds__(kCrcBlock) crc_chunks(const uint8_t* __restric
   if (last && threadIdx.x == 0) {  // the final block applies the final inversion
     __threadfence();
     const uint32_t raw = *reinterpret_cast<volatile uint32_t*>(acc);
-    *out = len ? (raw ^ 0xFFFFFFFFu) : 0u;
+    const uint32_t crc = len ? (raw ^ 0xFFFFFFFFu) : 0u;
+    *out = crc;
+    if (ep.mode == 1) verify_body(ep.plan, crc, status);
+    if (ep.mode == 2) finish_body(ep.out, ep.cap, ep.d_len, ep.plan, crc, status);
     *acc = 0;   // ready for the next range
     *done = 0;
-  }
-}
-
-// Header (container.cpp:62-73) + CRC trailer (:77-80); lengths from the plan.
-__global__ void finish_container(uint8_t* out, uint64_t cap, uint64_t* d_len, Plan* plan,
-                                 const uint32_t* crc, uint32_t* status) {
-  if (failed(status)) return;
-  const uint64_t total = 49 + plan->il + plan->vl + plan->rl + 4;
-  if (total > cap) {
-    latch(status, GP_CAPACITY);
-    return;
-  }
-  const int t = threadIdx.x;
-  if (t == 0) {
-    out[0] = 'D';
-    out[1] = 'R';
-    out[2] = 'C';
-    out[3] = '1';
-    out[4] = 1;
-    out[5] = 0;
-    out[6] = plan->index_method;
-    out[7] = plan->value_method;
-    out[8] = plan->rl ? 1 : 0;
-    st_u64_unaligned(out + 9, plan->d);
-    st_u64_unaligned(out + 17, plan->r);
-    st_u64_unaligned(out + 25, plan->il);
-    st_u64_unaligned(out + 33, plan->vl);
-    st_u64_unaligned(out + 41, plan->rl);
-    st_u32_unaligned(out + total - 4, *crc);
-    plan->total_len = total;
-    if (d_len) *d_len = total;
   }
 }
 
@@ -239,17 +252,13 @@ __global__ void parse_container(const uint8_t* __restrict__ in, uint64_t len_hos
   plan->post_crc_error = post;
 }
 
-__global__ void verify_container(Plan* plan, const uint32_t* crc, uint32_t* status) {
-  if (failed(status)) return;
-  if (static_cast<uint64_t>(*crc) != plan->crc_stored) return latch(status, GP_CHECKSUM);
-  if (plan->post_crc_error) latch(status, plan->post_crc_error);
-}
 
 }  // namespace
 
-void launch_crc_range(gp_ctx* ctx, const uint8_t* base, const uint64_t* off_dev, uint64_t off_host,
-                      const uint64_t* la, const uint64_t* lb, const uint64_t* lc, uint64_t len_host,
-                      uint64_t len_bound, uint32_t* out, cudaStream_t s) {
+namespace {
+void crc_range(gp_ctx* ctx, const uint8_t* base, const uint64_t* off_dev, uint64_t off_host, const uint64_t* la,
+               const uint64_t* lb, const uint64_t* lc, uint64_t len_host, uint32_t* out, cudaStream_t s,
+               const CrcEpilogue& ep) {
   Workspace& w = ctx->ws;
   if (!w.crc_ready) {  // byte-digit shift operators D[i][b] = x^(8 * b * 256^i) mod P
     auto mult = [](uint32_t a, uint32_t b) {
@@ -285,18 +294,31 @@ void launch_crc_range(gp_ctx* ctx, const uint8_t* base, const uint64_t* off_dev,
     cudaMemset(w.crc_acc, 0, 2 * sizeof(uint32_t));
     w.crc_ready = true;
   }
-  (void)len_bound;
   const int grid = ctx->sm_count * kCrcBlocksPerSm;
   GP_LAUNCH(ctx, crc_chunks, grid, kCrcBlock, 0, s, base, off_dev, off_host, la, lb, lc, len_host, w.crc_digits,
-            w.crc_acc, w.crc_acc + 1, out, w.status);
+            w.crc_acc, w.crc_acc + 1, out, ep, w.status);
+}
+}  // namespace
+
+void launch_crc_range(gp_ctx* ctx, const uint8_t* base, const uint64_t* off_dev, uint64_t off_host,
+                      const uint64_t* la, const uint64_t* lb, const uint64_t* lc, uint64_t len_host,
+                      uint64_t len_bound, uint32_t* out, cudaStream_t s) {
+  (void)len_bound;
+  crc_range(ctx, base, off_dev, off_host, la, lb, lc, len_host, out, s, CrcEpilogue{});
 }
 
 void launch_finish_container(gp_ctx* ctx, uint8_t* out, uint64_t cap, uint64_t* d_len, uint64_t len_bound,
                              cudaStream_t s) {
   Workspace& w = ctx->ws;
   uint32_t* crc = reinterpret_cast<uint32_t*>(&w.plan->crc_calc);
-  launch_crc_range(ctx, out, &w.plan->off_index, 0, &w.plan->il, &w.plan->vl, &w.plan->rl, 0, len_bound, crc, s);
-  GP_LAUNCH(ctx, finish_container, 1, 32, 0, s, out, cap, d_len, w.plan, crc, w.status);
+  CrcEpilogue ep;
+  ep.mode = 2;
+  ep.plan = w.plan;
+  ep.out = out;
+  ep.cap = cap;
+  ep.d_len = d_len;
+  (void)len_bound;
+  crc_range(ctx, out, &w.plan->off_index, 0, &w.plan->il, &w.plan->vl, &w.plan->rl, 0, crc, s, ep);
 }
 
 void launch_parse_container(gp_ctx* ctx, const uint8_t* in, uint64_t len, const uint64_t* len_dev,
@@ -306,8 +328,10 @@ void launch_parse_container(gp_ctx* ctx, const uint8_t* in, uint64_t len, const 
   if (hint) h = *hint;
   GP_LAUNCH(ctx, parse_container, 1, 1, 0, s, in, len, len_dev, ctx->max_d, w.plan, h, hint ? 1 : 0, w.status);
   uint32_t* crc = reinterpret_cast<uint32_t*>(&w.plan->crc_calc);
-  launch_crc_range(ctx, in, &w.plan->off_index, 0, &w.plan->il, &w.plan->vl, &w.plan->rl, 0, len, crc, s);
-  GP_LAUNCH(ctx, verify_container, 1, 1, 0, s, w.plan, crc, w.status);
+  CrcEpilogue ep;
+  ep.mode = 1;
+  ep.plan = w.plan;
+  crc_range(ctx, in, &w.plan->off_index, 0, &w.plan->il, &w.plan->vl, &w.plan->rl, 0, crc, s, ep);
 }
 
 void launch_crc_host_range(gp_ctx* ctx, const uint8_t* data, uint64_t n, uint32_t* out, cudaStream_t s) {
