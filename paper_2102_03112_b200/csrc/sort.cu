@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kBlock) radix_onesweep(const uint32_t* __restr
 }
 
 // In-place exclusive scan of a u32 array whose length is n_mul * tiles(*n_dev)
-// entries (n_mul = 256 for digit tables), decoupled look-back, 4096 per tile.
+// entries (n_mul = 256 for digit tables), decoupled look-back, kTile per tile.
 __global__ void __launch_bounds__(kBlock) scan_u32(uint32_t* data, const uint64_t* n_dev, uint64_t n_mul,
                                                    int tile_shift, uint64_t* tiles, uint32_t* ticket,
                                                    const uint32_t* status) {
@@ -197,23 +197,31 @@ __global__ void __launch_bounds__(kBlock) scan_u32(uint32_t* data, const uint64_
   if (failed(status)) return;
   const uint64_t n = n_mul * ((*n_dev + (1ull << tile_shift) - 1) >> tile_shift);
   const uint64_t ntiles = (n + kTile - 1) / kTile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   while (true) {
     const uint32_t tile = claim_tile(ticket, &slot);
     if (tile >= ntiles) break;
-    const uint64_t base = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(threadIdx.x) * kItems;
+    // warp rounds: lane l on entry wb + 32q + l (coalesced); index order is
+    // round-major within the warp, warp-major within the tile
+    const uint64_t wb = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(warp) * (32 * kItems);
     uint32_t v[kItems];
-    uint64_t sum = 0;
+    uint32_t sum = 0;
 #pragma unroll
     for (int q = 0; q < kItems; ++q) {
-      v[q] = base + q < n ? data[base + q] : 0;
+      const uint64_t i = wb + 32 * q + lane;
+      v[q] = i < n ? data[i] : 0;
       sum += v[q];
     }
+    const uint32_t wsum = __reduce_add_sync(kFull, sum);
     uint64_t tot;
-    uint64_t o = tile_exclusive_offset<kBlock>(sum, tile, tiles, sh, tot);
+    uint64_t o = tile_exclusive_offset<kBlock>(lane == 0 ? wsum : 0, tile, tiles, sh, tot);
+    o = __shfl_sync(kFull, o, 0);
 #pragma unroll
     for (int q = 0; q < kItems; ++q) {
-      if (base + q < n) data[base + q] = static_cast<uint32_t>(o);
-      o += v[q];
+      const uint32_t incl = warp_inclusive_sum(v[q]);
+      const uint64_t i = wb + 32 * q + lane;
+      if (i < n) data[i] = static_cast<uint32_t>(o + incl - v[q]);
+      o += __shfl_sync(kFull, incl, 31);
     }
   }
 }
