@@ -212,20 +212,28 @@ __global__ void __launch_bounds__(kBlock) rle_ends(const uint8_t* __restrict__ i
   const uint64_t n = plan->il;
   const uint64_t gav = n >= 1 ? n - 1 : 0;  // complete groups in the stream
   const uint64_t ntiles = (gav + kTile - 1) / kTile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
   while (true) {
     const uint32_t tile = claim_tile(ticket, &slot);
     if (tile >= ntiles) break;
-    const uint64_t base = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(threadIdx.x) * kItems;
-    uint32_t mask = 0;
+    // warp rounds: lane l on group wb + 32q + l (coalesced byte loads)
+    const uint64_t wb = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(warp) * (32 * kItems);
+    uint32_t bal[kItems];
+    uint32_t c = 0;
 #pragma unroll
-    for (int q = 0; q < kItems; ++q)
-      if (base + q < gav && !(group_at(p, base + q) & 0x80u)) mask |= 1u << q;
+    for (int q = 0; q < kItems; ++q) {
+      const uint64_t t = wb + 32 * q + lane;
+      bal[q] = __ballot_sync(kFull, t < gav && !(group_at(p, t) & 0x80u));
+      c += __popc(bal[q]);
+    }
     uint64_t tot;
-    uint64_t o = tile_exclusive_offset<kBlock>(__popc(mask), tile, tiles, sh, tot);
-    while (mask) {
-      const int q = __ffs(mask) - 1;
-      ends[o++] = static_cast<uint32_t>(base + q);
-      mask &= mask - 1;
+    uint64_t o = tile_exclusive_offset<kBlock>(lane == 0 ? c : 0, tile, tiles, sh, tot);
+    o = __shfl_sync(kFull, o, 0);
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+      if (bal[q] >> lane & 1u) ends[o + __popc(bal[q] & lt)] = static_cast<uint32_t>(wb + 32 * q + lane);
+      o += __popc(bal[q]);
     }
     if (tile == ntiles - 1 && threadIdx.x == kBlock - 1) plan->n_runs = o;
   }
@@ -258,23 +266,30 @@ __global__ void __launch_bounds__(kBlock) rle_scan(const Plan* plan, const uint6
   if (failed(status) || plan->index_method != GP_INDEX_RLE) return;
   const uint64_t V = plan->n_runs;
   const uint64_t ntiles = (V + kTile - 1) / kTile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   while (true) {
     const uint32_t tile = claim_tile(ticket, &slot);
     if (tile >= ntiles) break;
-    const uint64_t base = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(threadIdx.x) * kItems;
+    // warp rounds (coalesced): lane l on varint wb + 32q + l
+    const uint64_t wb = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(warp) * (32 * kItems);
     uint64_t x[kItems];
     uint64_t sum = 0;
 #pragma unroll
     for (int q = 0; q < kItems; ++q) {
-      x[q] = base + q < V ? runs[base + q] : 0;
+      const uint64_t v = wb + 32 * q + lane;
+      x[q] = v < V ? runs[v] : 0;
       sum += x[q];
     }
+    const uint64_t wsum = __shfl_sync(kFull, warp_inclusive_sum(sum), 31);
     uint64_t tot;
-    uint64_t o = tile_exclusive_offset<kBlock>(sum, tile, tiles, sh, tot);
+    uint64_t o = tile_exclusive_offset<kBlock>(lane == 0 ? wsum : 0, tile, tiles, sh, tot);
+    o = __shfl_sync(kFull, o, 0);
 #pragma unroll
     for (int q = 0; q < kItems; ++q) {
-      o += x[q];
-      if (base + q < V) cum[base + q] = o;
+      const uint64_t incl = warp_inclusive_sum(x[q]);
+      const uint64_t v = wb + 32 * q + lane;
+      if (v < V) cum[v] = o + incl;
+      o += __shfl_sync(kFull, incl, 31);
     }
   }
 }
@@ -342,34 +357,42 @@ __global__ void __launch_bounds__(kBlock) rle_bitmap(const Plan* plan, uint32_t*
   const uint64_t d = plan->d, nw = (d + 31) / 32;
   const uint32_t pol = plan->pd_variant ? 0xFFFFFFFFu : 0u;
   const uint64_t ntiles = (nw + kTile - 1) / kTile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   while (true) {
     const uint32_t tile = claim_tile(ticket, &slot);
     if (tile >= ntiles) break;
-    const uint64_t base = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(threadIdx.x) * kItems;
+    // warp rounds (coalesced): lane l on word wb + 32q + l; the inversion of a
+    // word is the parity of the toggles in all earlier words
+    const uint64_t wb = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(warp) * (32 * kItems);
     uint32_t x[kItems];
-    uint64_t c = 0;
+    uint32_t c = 0;
 #pragma unroll
     for (int q = 0; q < kItems; ++q) {
-      x[q] = base + q < nw ? words[base + q] : 0u;
+      const uint64_t w = wb + 32 * q + lane;
+      x[q] = w < nw ? words[w] : 0u;
       c += __popc(x[q]);
     }
+    const uint32_t wc = __reduce_add_sync(kFull, c);
     uint64_t tot;
-    uint64_t o = tile_exclusive_offset<kBlock>(c, tile, tiles, sh, tot);
+    uint64_t o = tile_exclusive_offset<kBlock>(lane == 0 ? wc : 0, tile, tiles, sh, tot);
+    o = __shfl_sync(kFull, o, 0);
 #pragma unroll
     for (int q = 0; q < kItems; ++q) {
+      const uint32_t n = __popc(x[q]);
+      const uint32_t incl = warp_inclusive_sum(n);
       uint32_t y = x[q];
       y ^= y << 1;
       y ^= y << 2;
       y ^= y << 4;
       y ^= y << 8;
       y ^= y << 16;
-      uint32_t b = y ^ ((o & 1) ? 0xFFFFFFFFu : 0u) ^ pol;
-      o += __popc(x[q]);
-      const uint64_t w = base + q;
+      uint32_t b = y ^ (((o + incl - n) & 1) ? 0xFFFFFFFFu : 0u) ^ pol;
+      const uint64_t w = wb + 32 * q + lane;
       if (w < nw) {
         if (w == nw - 1 && (d & 31)) b &= (1u << (d & 31)) - 1u;
         words[w] = b;
       }
+      o += __shfl_sync(kFull, incl, 31);
     }
   }
 }
