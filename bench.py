@@ -19,9 +19,15 @@ e2e   : the same step through the public API with HOST buffers: pinned H2D
         every step (dp.HostPipeline overlaps neighbouring steps' copies with
         the compute, as a training loop would).
 roofline : the dominant stage from a profiled pass of the same K steps.
+parity : step 0 replayed through the same exchanger, rank 0's container(s)
+        compared with the reference-written goldens (tests/golden/configs.json).
 cpu_baseline : the reference implementation (oracle/_ref, the reference's
-        own sources) — or the C restatement when _ref is absent — timed on
-        this box's host cores on a bounded sample (rank 0, N = 1).
+        own sources) — or the C restatement when _ref is absent — on one host
+        core, one full worker step (1 encode + 1 decode; C5: one bucket),
+        2 warm-ups + median of 3 (rank 0, N = 1).
+--impl reference : the same on every host core (thread t = worker t: 1 encode
+        of its full gradient, then N decodes), W warm-up rounds + median of K.
+        Loads only oracle/ and the host input generator, never the CUDA library.
 """
 from __future__ import annotations
 
@@ -41,37 +47,7 @@ if ROOT not in sys.path:
 
 METRIC = "dense-gradient GB/s through encode+allgather+decode; bits per nonzero"
 
-CONFIGS = {
-    "c4": dict(workload="ResNet-50-sized 25.6M-element gradient, top-r 1%, bloom-filter P2 (eps=1e-3) + "
-                        "polynomial curve-fit (degree 5), encode+allgather+decode",
-               d=25_557_032, ratio=0.01, index=6, value=1, fpr=0.001, degree=5, max_segments=0, sparse=False),
-    "c4s": dict(workload="C4 stress point: bloom-filter P2 at eps=1e-2 + polynomial curve-fit",
-                d=25_557_032, ratio=0.01, index=6, value=1, fpr=0.01, degree=5, max_segments=0, sparse=False),
-    "c4ef": dict(workload="C4 with error feedback (memory compensation, harness.cpp:230/269-271): encode of "
-                          "g + residual, residual <- input - decode(own container), then allgather + decode",
-                 d=25_557_032, ratio=0.01, index=6, value=1, fpr=0.001, degree=5, max_segments=0, sparse=False,
-                 ef=True),
-    "c1": dict(workload="synthetic 1M-element gradient, top-r 1%, bloom-filter P0 (eps=1e-2) + polynomial "
-                        "curve-fit, single-worker round trip",
-               d=1_000_000, ratio=0.01, index=4, value=1, fpr=0.01, degree=5, max_segments=0, sparse=False),
-    "c2": dict(workload="ResNet-20-sized 0.27M-element gradient, top-r 1%, bitmap indices + raw f32 values",
-               d=269_722, ratio=0.01, index=1, value=0, fpr=0.01, degree=5, max_segments=0, sparse=False),
-    "c3": dict(workload="NCF-style natural sparsity (40% zero 64-wide rows), 32M elements, bitmap indices + "
-                        "raw f32 values (support = nonzeros)",
-               d=31_832_577, ratio=None, index=1, value=0, fpr=0.01, degree=5, max_segments=0, sparse=True),
-    "c3r": dict(workload="NCF-style natural sparsity (40% zero 64-wide rows), 32M elements, RLE indices + "
-                         "raw f32 values (support = nonzeros)",
-                d=31_832_577, ratio=None, index=2, value=0, fpr=0.01, degree=5, max_segments=0, sparse=True),
-    "c2r": dict(workload="ResNet-20-sized 0.27M-element gradient, top-r 1%, RLE indices + raw f32 values",
-                d=269_722, ratio=0.01, index=2, value=0, fpr=0.01, degree=5, max_segments=0, sparse=False),
-    "c5": dict(workload="BERT-large-sized 340M-element gradient, top-r 0.1%, bloom-filter P2 (eps=1e-3) + "
-                        "piecewise curve-fit (8 pieces), 16 independent 21.25M buckets pipelined on 8 streams",
-               d=340_000_000, ratio=0.001, index=6, value=1, fpr=0.001, degree=5, max_segments=8, sparse=False,
-               buckets=16),
-}
-METHOD_NAMES = {0: "none", 1: "bitmap", 2: "rle", 4: "bloom-p0", 5: "bloom-p1", 6: "bloom-p2", 7: "bloom-pd",
-                8: "bloom-naive"}
-VALUE_NAMES = {0: "raw-f32", 1: "fit-poly", 5: "raw-f64"}
+from paper_2102_03112_b200.configs import CONFIGS, METHOD_NAMES, VALUE_NAMES  # noqa: E402  (no CUDA import)
 
 
 def peaks():
@@ -135,53 +111,73 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------- reference arm
+# The CPU legs load only the reference build (oracle/_ref) or the C restatement,
+# plus the pure-host input generator: never libgradpack_b200.so.
 def cpu_codec():
     from oracle.bindings import oracle, reference
     ref = reference()
     return (ref, "reference") if ref is not None else (oracle(), "port")
 
 
-def cpu_step(lib, g, r, cfg_c, dense64):
-    """One reference step: top_r + compress + pack, then unpack + decompress + to_dense."""
-    c = lib.encode_dense(g, r, cfg_c)
-    dense64[:] = 0.0
-    lib.decode_accumulate(c, dense64, 1.0)
-    return len(c)
+def config_line(cfg, world: int) -> dict:
+    """The `config` object both arms print (same workload, same keys)."""
+    out = {"workload": cfg["workload"], "d": cfg["d"], "index_method": METHOD_NAMES[cfg["index"]],
+           "value_method": VALUE_NAMES[cfg["value"]], "fpr": cfg["fpr"], "degree": cfg["degree"],
+           "max_segments": cfg["max_segments"], "parallelism": f"dp{world}"}
+    if cfg["ratio"] is not None:
+        out["ratio"] = cfg["ratio"]
+    if cfg.get("buckets"):
+        out["buckets"] = cfg["buckets"]
+    if cfg.get("ef"):
+        out["error_feedback"] = True
+    return out
 
 
-def run_cpu_sample(cfg, threads: int, shrink: int, steps: int, seed_step: int = 0):
-    """Times `steps` rounds of `threads` concurrent reference steps on d/shrink-element
-    gradients.  Returns (GB/s, seconds per round, sample description, bits/nnz)."""
+def run_cpu_sample(cfg, threads: int, world: int, steps: int, warmup: int, step0: int = 0):
+    """`warmup` + `steps` rounds of one DP step per thread on the reference code:
+    thread t is worker t — top_r + compress_gradient + pack of its own full
+    d-element gradient, then (after all threads encoded: the "exchange")
+    unpack + decompress_gradient + to_dense accumulation of `world` containers
+    (its own and the next world-1 threads'), the harness step
+    (harness.cpp:219-293) at N = world.  Bucketed configs: one bucket per
+    thread.  Returns (GB/s, median seconds per round, sample, kind, bits/nnz)."""
     from oracle.bindings import GpConfig
-    from paper_2102_03112_b200 import synth
-    from paper_2102_03112_b200.dp import pipeline_seed, ratio_r
+    from paper_2102_03112_b200.configs import case_input, case_seed
     lib, kind = cpu_codec()
-    d = cfg["d"] // shrink
-    gen = synth.natural_sparse_gradient if cfg["sparse"] else synth.gradient
-    grads = [gen(d, rank=t) for t in range(threads)]
-    rs = [ratio_r(d, cfg["ratio"]) if cfg["ratio"] else int(np.count_nonzero(g)) for g in grads]
+    ins = [case_input(cfg, rank=t, bucket=0 if cfg.get("buckets") else None) for t in range(threads)]
+    d = ins[0][0].size
     denses = [np.zeros(d, np.float64) for _ in range(threads)]
-    sizes = [0] * threads
+    conts = [b""] * threads
+    barrier = threading.Barrier(threads)
 
     def work(t, step):
+        g, r, _ = ins[t]
         cc = GpConfig.make(cfg["index"], cfg["value"], fpr=cfg["fpr"], degree=cfg["degree"],
-                           max_segments=cfg["max_segments"], seed=pipeline_seed(1, t, step))
-        sizes[t] = cpu_step(lib, grads[t], rs[t], cc, denses[t])
+                           max_segments=cfg["max_segments"],
+                           seed=case_seed(cfg, rank=t, step=step, bucket=0 if cfg.get("buckets") else None))
+        conts[t] = lib.encode_dense(g, r, cc)
+        barrier.wait()
+        denses[t][:] = 0.0
+        for j in range(world):
+            lib.decode_accumulate(conts[(t + j) % threads], denses[t], 1.0 / world)
+        barrier.wait()
 
     times = []
-    for step in range(steps):
-        ths = [threading.Thread(target=work, args=(t, seed_step + step)) for t in range(threads)]
+    for i in range(warmup + steps):
+        ths = [threading.Thread(target=work, args=(t, step0 + i)) for t in range(threads)]
         t0 = time.perf_counter()
         for th in ths:
             th.start()
         for th in ths:
             th.join()
-        times.append(time.perf_counter() - t0)
+        if i >= warmup:
+            times.append(time.perf_counter() - t0)
     sec = float(np.median(times))
     gbs = threads * 4.0 * d / sec / 1e9
-    bits = 8.0 * sizes[0] / rs[0]
-    desc = (f"{threads} thread(s) x one full encode+decode step of a {d}-element gradient "
-            f"(d/{shrink} of the workload, r={rs[0]}), median of {steps}")
+    bits = 8.0 * len(conts[0]) / ins[0][1]
+    what = "one 21.25M-element bucket" if cfg.get("buckets") else "the full"
+    desc = (f"{threads} thread(s), each one worker's step on {what} {d}-element gradient (r={ins[0][1]}): "
+            f"1 encode + {world} decode(s); {warmup} warm-up round(s), median of {steps}")
     return gbs, sec, desc, kind, bits
 
 
@@ -190,16 +186,12 @@ def reference_main(args, cfg):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    shrink = args.ref_shrink
-    for _ in range(args.warmup):
-        run_cpu_sample(cfg, threads, shrink, 1)
-    gbs, sec, desc, kind, bits = run_cpu_sample(cfg, threads, shrink, args.steps)
+    gbs, sec, desc, kind, bits = run_cpu_sample(cfg, threads, args.gpus, args.steps, args.warmup)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(gbs, 6), "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
-        "data": "synthetic", "bits_per_nonzero": round(bits, 4),
-        "config": {"workload": cfg["workload"], "d": cfg["d"], "sample": desc},
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 values, u32 keys, f64 fit",
+        "data": "synthetic", "bits_per_nonzero": round(bits, 4), "config": config_line(cfg, args.gpus),
         "cpu_baseline": {"value": round(gbs, 6), "unit": "GB/s", "cores": threads, "kind": kind, "sample": desc},
         "e2e": {"value": round(gbs, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -212,7 +204,7 @@ def native_main(args, cfg):
     import torch
     import torch.distributed as dist
 
-    from paper_2102_03112_b200 import Codec, PipelineConfig, synth
+    from paper_2102_03112_b200 import Codec, PipelineConfig, inputs
     from paper_2102_03112_b200.dp import BucketedSparseAllgather, HostPipeline, SparseAllgather, ratio_r
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -232,11 +224,10 @@ def native_main(args, cfg):
     dev = torch.device("cuda", local)
 
     d = cfg["d"]
-    if cfg["sparse"]:
-        g_host = synth.natural_sparse_gradient(d, rank)
-        grad = torch.from_numpy(g_host).to(dev)
-    else:  # the BASELINE generator, evaluated on the device (d up to 340M)
-        grad = synth.gradient_torch(d, rank, device=dev)
+    # the rank's gradient from the host generator (the bytes the goldens and the
+    # CPU arm use), uploaded once: the timed steps read it from HBM
+    gen = inputs.natural_sparse_gradient if cfg["sparse"] else inputs.gradient
+    grad = torch.from_numpy(gen(d, rank)).to(dev)
     r = int(torch.count_nonzero(grad).item()) if cfg["ratio"] is None else ratio_r(d, cfg["ratio"])
     pinned = torch.empty(d, dtype=torch.float32).pin_memory()
     pinned.copy_(grad)
@@ -412,10 +403,8 @@ def native_main(args, cfg):
         "warmup": args.warmup, "ms_per_step": round(t_ms, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32 values, u32 keys, f64 fit", "data": "synthetic",
         "bits_per_nonzero": round(8.0 * length / r_total, 4),
-        "config": {"workload": cfg["workload"], "d": d, "r": r_total, "index_method": METHOD_NAMES[cfg["index"]],
-                   "value_method": VALUE_NAMES[cfg["value"]], "fpr": cfg["fpr"], "degree": cfg["degree"],
-                   "container_bytes": length, "parallelism": f"dp{world}",
-                   "l2": "flushed between steps (256 MiB write outside the timed events)"},
+        "config": config_line(cfg, world), "r": r_total, "container_bytes": length,
+        "l2": "flushed between steps (256 MiB write outside the timed events)",
         "e2e": {"value": round(e2e_value, 4), "unit": "GB/s", "h2d_bytes_per_step": 4 * d,
                 "d2h_bytes_per_step": 4 * d, "ms_per_step": round(e2e_t, 4),
                 "pipelined": "HostPipeline: copy-in of step i+1 and copy-out of step i-1 overlap step i",
@@ -425,8 +414,9 @@ def native_main(args, cfg):
         "profiled_ms_per_step": round(prof_total, 4),
         "gpu_launches": int(n_launch), "cuda_graph": graphed, "clocks": clocks, "wall_s_timed": round(wall, 4),
     }
+    line["parity"] = golden_parity(args.config, cfg, ex, grad, rank, world)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        gbs, sec, desc, kind, _ = run_cpu_sample(cfg, 1, cfg.get("buckets", 1), 1)
+        gbs, sec, desc, kind, _ = run_cpu_sample(cfg, 1, 1, 3, 2)
         line["cpu_baseline"] = {"value": round(gbs, 6), "unit": "GB/s", "cores": 1, "kind": kind, "sample": desc,
                                 "seconds": round(sec, 3)}
     if rank == 0:
@@ -436,6 +426,53 @@ def native_main(args, cfg):
     return 0
 
 
+def golden_parity(name, cfg, ex, grad, rank, world):
+    """Replays step 0 through the SAME exchanger the timed region used (the
+    captured graph at N = 1) and compares rank 0's container(s) with the
+    reference-written goldens of tests/golden/configs.json
+    (tools/make_config_goldens.py): header, index and reorder payloads
+    bit-exact, raw value payloads bit-exact, fit payloads same structure with
+    coefficients within the SURVEY §8(a) tolerance."""
+    import torch
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from golden_util import coeff_close, load, parse_fit, sha, split
+    if cfg.get("ef"):
+        ex.step(grad, step=0)  # keep the collective schedule of the other ranks
+        return {"checked": False, "why": "no golden for the compensated (error-feedback) step"}
+    gold = load()
+    cases = ([(f"{name}_b{b}", b) for b in (0, cfg["buckets"] - 1)] if cfg.get("buckets") else [(name, None)])
+    ex.step(grad, step=0)
+    torch.cuda.synchronize()
+    ex.check()
+    if rank != 0:
+        return None
+    out = {"golden": "tests/golden/configs.json", "step": 0, "rank": 0, "cases": {}}
+    ok_all = True
+    for case, b in cases:
+        gd = gold.get(case)
+        if gd is None:
+            out["cases"][case] = {"match": False, "why": "no golden"}
+            ok_all = False
+            continue
+        e = ex.ex[b] if b is not None else ex
+        c = e.out[: int(e.length.item())].cpu().numpy().tobytes()
+        p = split(c)
+        chk = {"header": p["header"].hex() == gd["header_hex"], "index": sha(p["index"]) == gd["index_sha256"],
+               "reorder": sha(p["reorder"]) == gd["reorder_sha256"]}
+        if gd["value_method"] in (1, 2):
+            a, ref = parse_fit(p["value"]), parse_fit(bytes.fromhex(gd["value_hex"]))
+            chk["fit_structure"] = all(a[k] == ref[k] for k in ("kind", "S", "bounds", "degree", "l"))
+            chk["fit_coeffs_within_tol"] = chk["fit_structure"] and coeff_close(a["coeffs"], ref["coeffs"])
+        else:
+            chk["value"] = sha(p["value"]) == gd["value_sha256"]
+            chk["container"] = sha(c) == gd["container_sha256"]
+        ok = all(chk.values())
+        ok_all &= ok
+        out["cases"][case] = {"match": ok, **chk}
+    out["golden_match"] = ok_all
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -443,7 +480,6 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--ref-shrink", type=int, default=8, help="reference arm: d/shrink-element sample per thread")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-early", action="store_true", help="N = 1: no early index decode on a second context")
     ap.add_argument("--no-graph", action="store_true", help="N = 1: launch the step eagerly instead of as a CUDA graph")

@@ -10,6 +10,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -36,19 +37,32 @@ def build(verbose: bool = False) -> str:
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp"))]
     deps.append(os.path.join(HERE, "..", "include", "gradpack_b200.h"))
     newest_dep = max(os.path.getmtime(p) for p in deps)
+    stale = []
     for src in SOURCES:
         path = os.path.join(CSRC, src)
         obj = os.path.join(OBJ, src.rsplit(".", 1)[0] + ".o")
         if (not os.path.exists(obj) or os.path.getmtime(obj) < os.path.getmtime(path)
                 or os.path.getmtime(obj) < newest_dep):
-            out = _run([NVCC, *ARCH, *FLAGS, "-c", path, "-o", obj])
+            stale.append([NVCC, *ARCH, *FLAGS, "-c", path, "-o", obj])
+        objs.append(obj)
+    with ThreadPoolExecutor(max_workers=max(1, min(len(stale), os.cpu_count() or 1))) as pool:
+        for out in pool.map(_run, stale):  # one nvcc per translation unit, in parallel
             if verbose and out.strip():
                 print(out)
-        objs.append(obj)
     if not os.path.exists(OUT) or any(os.path.getmtime(o) > os.path.getmtime(OUT) for o in objs):
         _run([NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-Xlinker", "--exclude-libs,ALL"])
     build_cli()
+    build_inputs()
     return OUT
+
+
+def build_inputs() -> str:
+    """libgp_inputs.so: the host generator of the benchmark gradients (inputs.py)."""
+    src = os.path.join(CSRC, "inputs.c")
+    out = os.path.join(HERE, "libgp_inputs.so")
+    if not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(src):
+        _run(["gcc", "-std=c11", "-O2", "-fPIC", "-shared", "-ffp-contract=off", src, "-o", out, "-lm"])
+    return out
 
 
 CLI_SRC = os.path.join(HERE, "..", "tests", "cpp", "gp_cli.cpp")

@@ -280,7 +280,7 @@ int gp_ctx_create(int device, uint64_t max_d, gp_ctx** out) {
   if (e == cudaSuccess) e = cudaMemset(ctx->ws.plan, 0, sizeof(Plan));
   if (e == cudaSuccess) e = cudaMemset(ctx->ws.huff, 0, sizeof(HuffTable));  // empty Huffman table cache
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
-  if (e != cudaSuccess) {
+  if (e != cudaSuccess || crc_tables_init(ctx) != GP_OK) {
     cudaFree(base);
     delete ctx;
     return GP_CUDA;
@@ -617,10 +617,9 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const u
     default: break;
   }
   if ((im == GP_INDEX_NONE || im == GP_INDEX_HUFFMAN) && !own) launch_validate_support(ctx, bound, s);
-  (void)dense_d;
   if (scatter)
     GP_STAGE(ctx, ST_DEC_SCATTER, s,
-             launch_decode_scatter(ctx, d_in, bound, d_dense, scale, d_support, d_values, cap, d_count, d_dim, s));
+             launch_decode_scatter(ctx, d_in, bound, d_dense, dense_d, scale, d_support, d_values, cap, d_count, d_dim, s));
   return check_launch(ctx, "decode");
 }
 
@@ -654,9 +653,8 @@ int gp_decode_finish(gp_ctx* ctx, const uint8_t* d_container, float* d_dense, ui
                      void* stream) {
   if (!ctx || !d_container || !d_dense) return set_error(ctx, GP_ERROR, "decode_finish: null argument");
   auto s = static_cast<cudaStream_t>(stream);
-  (void)d;
   GP_STAGE(ctx, ST_DEC_SCATTER, s,
-           launch_decode_scatter(ctx, d_container, ctx->max_d, d_dense, scale, nullptr, nullptr, 0, nullptr, nullptr,
+           launch_decode_scatter(ctx, d_container, ctx->max_d, d_dense, d, scale, nullptr, nullptr, 0, nullptr, nullptr,
                                  s));
   return check_launch(ctx, "decode_finish");
 }

@@ -255,45 +255,53 @@ __global__ void parse_container(const uint8_t* __restrict__ in, uint64_t len_hos
 
 }  // namespace
 
+// Builds the CRC operator tables once per context (called from gp_ctx_create,
+// which synchronizes and checks every error before the context is handed out,
+// so no stream — captured or not — ever sees half-built tables).
+int crc_tables_init(gp_ctx* ctx) {
+  Workspace& w = ctx->ws;
+  // byte-digit shift operators D[i][b] = x^(8 * b * 256^i) mod P
+  auto mult = [](uint32_t a, uint32_t b) {
+    uint32_t m = 1u << 31, p = 0;
+    for (;;) {
+      if (a & m) {
+        p ^= b;
+        if ((a & (m - 1)) == 0) break;
+      }
+      m >>= 1;
+      b = (b & 1) ? (b >> 1) ^ kPoly : b >> 1;
+    }
+    return p;
+  };
+  uint32_t tab[9 * 256];
+  uint32_t unit = 1u << 23;  // x^8: one byte
+  for (int i = 0; i < 5; ++i) {
+    uint32_t p = 1u << 31;
+    for (int b = 0; b < 256; ++b) {
+      tab[i * 256 + b] = p;
+      p = mult(unit, p);
+    }
+    unit = p;  // x^(8 * 256^(i+1))
+  }
+  // M[j][b] = (b at byte j) * x^(8 * 64 * lanes) mod P: the lane stride of the fixed grid
+  uint64_t stride = 64ull * static_cast<uint64_t>(ctx->sm_count) * kCrcBlocksPerSm * kCrcBlock;
+  uint32_t S = 1u << 31;
+  for (int i = 0; stride; ++i, stride >>= 8)
+    if (stride & 0xFF) S = mult(tab[i * 256 + (stride & 0xFF)], S);
+  for (int j = 0; j < 4; ++j)
+    for (int b = 0; b < 256; ++b) tab[(5 + j) * 256 + b] = b ? mult(static_cast<uint32_t>(b) << (8 * j), S) : 0u;
+  cudaError_t e = cudaMemcpy(w.crc_digits, tab, sizeof(tab), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(w.crc_acc, 0, 2 * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  w.crc_ready = e == cudaSuccess;
+  return e == cudaSuccess ? GP_OK : GP_CUDA;
+}
+
 namespace {
 void crc_range(gp_ctx* ctx, const uint8_t* base, const uint64_t* off_dev, uint64_t off_host, const uint64_t* la,
                const uint64_t* lb, const uint64_t* lc, uint64_t len_host, uint32_t* out, cudaStream_t s,
                const CrcEpilogue& ep) {
   Workspace& w = ctx->ws;
-  if (!w.crc_ready) {  // byte-digit shift operators D[i][b] = x^(8 * b * 256^i) mod P
-    auto mult = [](uint32_t a, uint32_t b) {
-      uint32_t m = 1u << 31, p = 0;
-      for (;;) {
-        if (a & m) {
-          p ^= b;
-          if ((a & (m - 1)) == 0) break;
-        }
-        m >>= 1;
-        b = (b & 1) ? (b >> 1) ^ kPoly : b >> 1;
-      }
-      return p;
-    };
-    uint32_t tab[9 * 256];
-    uint32_t unit = 1u << 23;  // x^8: one byte
-    for (int i = 0; i < 5; ++i) {
-      uint32_t p = 1u << 31;
-      for (int b = 0; b < 256; ++b) {
-        tab[i * 256 + b] = p;
-        p = mult(unit, p);
-      }
-      unit = p;  // x^(8 * 256^(i+1))
-    }
-    // M[j][b] = (b at byte j) * x^(8 * 64 * lanes) mod P: the lane stride of the fixed grid
-    uint64_t stride = 64ull * static_cast<uint64_t>(ctx->sm_count) * kCrcBlocksPerSm * kCrcBlock;
-    uint32_t S = 1u << 31;
-    for (int i = 0; stride; ++i, stride >>= 8)
-      if (stride & 0xFF) S = mult(tab[i * 256 + (stride & 0xFF)], S);
-    for (int j = 0; j < 4; ++j)
-      for (int b = 0; b < 256; ++b) tab[(5 + j) * 256 + b] = b ? mult(static_cast<uint32_t>(b) << (8 * j), S) : 0u;
-    cudaMemcpy(w.crc_digits, tab, sizeof(tab), cudaMemcpyHostToDevice);
-    cudaMemset(w.crc_acc, 0, 2 * sizeof(uint32_t));
-    w.crc_ready = true;
-  }
   const int grid = ctx->sm_count * kCrcBlocksPerSm;
   GP_LAUNCH(ctx, crc_chunks, grid, kCrcBlock, 0, s, base, off_dev, off_host, la, lb, lc, len_host, w.crc_digits,
             w.crc_acc, w.crc_acc + 1, out, ep, w.status);

@@ -197,6 +197,7 @@ void launch_own_support(gp_ctx* ctx, uint64_t r_bound, cudaStream_t s);
 void launch_crc_range(gp_ctx* ctx, const uint8_t* base, const uint64_t* off_dev, uint64_t off_host,
                       const uint64_t* la, const uint64_t* lb, const uint64_t* lc, uint64_t len_host,
                       uint64_t len_bound, uint32_t* out, cudaStream_t s);
+int crc_tables_init(gp_ctx* ctx);  // container.cu (gp_ctx_create)
 void launch_crc_host_range(gp_ctx* ctx, const uint8_t* data, uint64_t n, uint32_t* out, cudaStream_t s);
 void launch_finish_container(gp_ctx* ctx, uint8_t* out, uint64_t cap, uint64_t* d_len, uint64_t len_bound,
                              cudaStream_t s);
@@ -242,7 +243,8 @@ void launch_decode_quant(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, cudaS
 void launch_values_slot(gp_ctx* ctx, uint8_t* out, uint64_t n_bound, cudaStream_t s);
 void launch_decode_slot(gp_ctx* ctx, const uint8_t* in, cudaStream_t s);
 void launch_decode_inflate(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, cudaStream_t s);
-void launch_decode_scatter(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, float* dense, float scale,
+void launch_decode_scatter(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, float* dense, uint64_t dense_d,
+                           float scale,
                            uint32_t* out_support, double* out_values, uint64_t cap, uint64_t* d_count,
                            uint64_t* d_dim, cudaStream_t s);
 

@@ -73,10 +73,17 @@ __device__ __forceinline__ double value_at(const uint8_t* vp, uint8_t vm, const 
 }
 
 __global__ void decode_scatter(const uint8_t* __restrict__ in, const Plan* plan, const uint32_t* __restrict__ sel,
-                               const double* __restrict__ fitv, float* dense, float scale, uint32_t* out_support,
-                               double* out_values, uint64_t cap, uint64_t* d_count, uint64_t* d_dim,
-                               uint32_t* status) {
+                               const double* __restrict__ fitv, float* dense, uint64_t dense_d, float scale,
+                               uint32_t* out_support, double* out_values, uint64_t cap, uint64_t* d_count,
+                               uint64_t* d_dim, uint32_t* status) {
   if (failed(status)) return;
+  // the container's d must equal the caller's dense length: to_dense builds a
+  // d-vector (gradient.cpp:38-42) and the mean adds equal-length vectors
+  // (harness.cpp:274-284); a mismatch is caller misuse, never a stray write
+  if (dense && plan->d != dense_d) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) latch(status, GP_ERROR);
+    return;
+  }
   const uint64_t n = plan->n_sel;       // coordinates written (|P| for naive)
   const uint64_t nv = plan->n_values;   // values carried (naive: r, zero-filled past it)
   if (out_support && n > cap) {
@@ -141,12 +148,13 @@ void launch_values_raw_check(gp_ctx* ctx, cudaStream_t s) {
   GP_LAUNCH(ctx, values_raw_check, 1, 1, 0, s, ctx->ws.plan, ctx->ws.status);
 }
 
-void launch_decode_scatter(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, float* dense, float scale,
+void launch_decode_scatter(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, float* dense, uint64_t dense_d,
+                           float scale,
                            uint32_t* out_support, double* out_values, uint64_t cap, uint64_t* d_count,
                            uint64_t* d_dim, cudaStream_t s) {
   Workspace& w = ctx->ws;
-  GP_LAUNCH(ctx, decode_scatter, grid_for(ctx, n_bound, 256), 256, 0, s, in, w.plan, w.sel, w.f64a, dense, scale,
-            out_support, out_values, cap, d_count, d_dim, w.status);
+  GP_LAUNCH(ctx, decode_scatter, grid_for(ctx, n_bound, 256), 256, 0, s, in, w.plan, w.sel, w.f64a, dense, dense_d,
+            scale, out_support, out_values, cap, d_count, d_dim, w.status);
 }
 
 }  // namespace gp

@@ -7,7 +7,12 @@ own full d-element gradient; it runs top_r + compress_gradient + pack
 harness.cpp:201-203); the variable-length containers are exchanged with an
 allgather — sizes first, then the payloads padded to the largest size (NCCL
 has no allgatherv) — and every rank decodes all N containers in rank order
-into the dense mean (harness.cpp:274-284: f32 accumulate of value / N).
+into the dense mean.  The reference sums the N decoded f64 vectors in a
+fixed pairwise tree and then divides by N (harness.cpp:274-284); this path
+accumulates in f32, sequentially in rank order, dense = fmaf(1/N, v, dense)
+— per coordinate at most N f32 roundings, i.e. within N ulp(f32) of the
+largest term of the reference's f64 mean (tests/test_gpu_parity.py bounds it
+at 4 ulp for the single-worker case).
 
 torch.distributed is plumbing only (process group, NCCL communicator); every
 payload byte is produced and consumed by the codec.  The codec is duck-typed
@@ -24,40 +29,12 @@ encode, exchange and decode of different buckets overlap.
 """
 from __future__ import annotations
 
-import math
 from dataclasses import replace
 
 import torch
 import torch.distributed as dist
 
-GAMMA = 0x9E3779B97F4A7C15
-MASK = (1 << 64) - 1
-
-
-def _mix64(z: int) -> int:
-    z &= MASK
-    z ^= z >> 30
-    z = (z * 0xBF58476D1CE4E5B9) & MASK
-    z ^= z >> 27
-    z = (z * 0x94D049BB133111EB) & MASK
-    return z ^ (z >> 31)
-
-
-def hash64(x: int, seed: int) -> int:
-    """rng.hpp:35-37"""
-    return _mix64((x ^ ((seed + GAMMA) & MASK)) & MASK)
-
-
-def pipeline_seed(seed: int, worker: int, step: int) -> int:
-    """Simulation::pipeline_seed (harness.cpp:201-203) over Problem::batch_seed (:47-51)."""
-    key = ((worker & 0xFFFFFFFF) << 32) | (step & 0xFFFFFFFF)
-    return hash64(0xC0DEC, hash64(key, hash64(0xDA7A, seed)))
-
-
-def ratio_r(d: int, ratio: float) -> int:
-    """r = max(1, llround(ratio * d)) (harness.cpp:212)."""
-    x = ratio * d
-    return max(1, int(math.floor(x + 0.5)))
+from .seeds import bucket_bounds, hash64, pipeline_seed, ratio_r  # noqa: F401  (re-exported)
 
 
 def _world(group):
@@ -176,8 +153,11 @@ class SparseAllgather:
             self.codec.decode_accumulate(self.out, out_dense, scale=1.0, length=self.length, hint=self.cfg,
                                          stream=stream)
             return out_dense
+        # the step's one host sync: a latched encode error (or a previous step's
+        # decode error) raises here instead of shipping a stale container
+        self.codec.status(stream)
         dist.all_gather_into_tensor(self.sizes, self.length, group=self.group)
-        sizes = self.sizes.tolist()  # the one host sync of the step
+        sizes = self.sizes.tolist()
         mx = max(sizes)
         dist.all_gather_into_tensor(self.recv[: n * mx], self.out[:mx], group=self.group)
         if self.dec_streams is None:
@@ -188,6 +168,20 @@ class SparseAllgather:
         main = stream if stream is not None else torch.cuda.current_stream()
         self._decode_concurrent(n, mx, out_dense, main)
         return out_dense
+
+    def check(self, stream=None) -> None:
+        """Synchronise and raise the first device error latched by any of this
+        exchanger's contexts (checksum / payload / capacity errors of a decode,
+        fit errors of an encode).  The status latch is sticky until read and
+        every kernel of a latched context returns early, so callers of the
+        host-sync-free paths (N = 1, CUDA graphs) poll this once per step, or
+        as often as they can afford; N > 1 steps poll the encoding context at
+        their sizes exchange."""
+        seen = []
+        for c in [self.codec] + list(self.dec[1:]) + ([self.early] if self.early is not None else []):
+            if all(c is not x for x in seen):
+                seen.append(c)
+                c.status(stream)
 
     def _step_early(self, grad, cfg, out_dense, stream):
         main = stream if stream is not None else torch.cuda.current_stream()
@@ -238,13 +232,7 @@ class BucketedSparseAllgather:
                  device=None, ef: bool = False, graph: bool = False):
         self.d, self.cfg, self.buckets = d, cfg, buckets
         self.world, self.rank = _world(group)
-        base, rem = divmod(d, buckets)
-        self.bounds = []
-        at = 0
-        for b in range(buckets):
-            n = base + (1 if b < rem else 0)
-            self.bounds.append((at, at + n))
-            at += n
+        self.bounds = bucket_bounds(d, buckets)
         dmax = max(e - s for s, e in self.bounds)
         self.rs = [ratio_r(e - s, ratio) for s, e in self.bounds]
         self.nstreams = min(streams, buckets)
@@ -263,6 +251,11 @@ class BucketedSparseAllgather:
         if self.graph:
             self.step_dev = torch.zeros(1, dtype=torch.int64, device=dev)
             self.seeds_dev = torch.zeros(buckets, dtype=torch.int64, device=dev)
+
+    def check(self) -> None:
+        """Raise the first latched device error of any bucket context (see SparseAllgather.check)."""
+        for c in self.codecs:
+            c.status()
 
     def bucket_seed(self, seed: int, step: int, b: int) -> int:
         return hash64(b, pipeline_seed(seed, self.rank, step))

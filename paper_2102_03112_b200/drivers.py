@@ -34,8 +34,8 @@ import numpy as np
 import torch
 
 from .api import Codec, PipelineConfig, UnsupportedMethodError, volume
-from .dp import hash64, ratio_r
-from .synth import _draws, normal_f32
+from .inputs import normal_f32
+from .seeds import GAMMA, MASK, hash64, mix64, ratio_r
 
 GRID = (0.2, 0.1, 0.05, 0.02, 0.01, 0.005, 0.002, 0.001)
 POLICIES = ((4, "p0"), (5, "p1"), (6, "p2"))
@@ -49,7 +49,7 @@ def below_seq(seed: int, bounds, start: int = 0) -> list[int]:
         rem = ((2 ** 64 - 1) % n + 1) % n
         bound = 2 ** 64 - 1 - rem
         while True:
-            v = int(_draws(seed, pos, 1)[0])
+            v = mix64((seed + (pos + 1) * GAMMA) & MASK)
             pos += 1
             if v <= bound:
                 break
