@@ -15,7 +15,7 @@ def test_sweep_matches_reference_loop():
     from paper_2102_03112_b200 import Codec
     from paper_2102_03112_b200.dp import hash64, ratio_r
     from paper_2102_03112_b200.drivers import random_r, sweep
-    from paper_2102_03112_b200.synth import normal_f32
+    from paper_2102_03112_b200.inputs import normal_f32
     ref = reference()
     if ref is None:
         pytest.skip("oracle/_ref missing")
