@@ -160,6 +160,14 @@ GP_API int gp_decode_accumulate_dlen(gp_ctx* ctx, const uint8_t* d_container, ui
                                      const uint64_t* d_len, const gp_pipeline_config* hint,
                                      float* d_dense, uint64_t d, float scale, void* stream);
 
+/* Overwrite mode (on = 1) for this context's following decodes into a dense
+ * buffer: d_dense = scale * decoded on the support and 0 elsewhere — exactly
+ * what zeroing the buffer and accumulating would produce (the first container
+ * of a DP step's mean, harness.cpp:274-284), without the separate zero pass.
+ * Bitmap + raw containers then write the whole buffer in one pass (dense.cu).
+ * When a decode latches an error the buffer's contents are unspecified. */
+GP_API int gp_ctx_set_decode_overwrite(gp_ctx* ctx, int on);
+
 /* Early index decode (one rank's own container, N = 1 and the own peer at
  * N > 1): the Bloom filter payload of a container is final as soon as its
  * encode built the filter, so its positive scan and P0/P1/P2/Pd selection can

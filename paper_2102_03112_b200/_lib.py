@@ -64,6 +64,7 @@ _SIGS = {
     "gp_decode_accumulate_hint": ([_vp, _vp, _u64, _P(GpConfig), _vp, _u64, C.c_float, _vp], C.c_int),
     "gp_decode_accumulate_dlen": ([_vp, _vp, _u64, _vp, _P(GpConfig), _vp, _u64, C.c_float, _vp], C.c_int),
     "gp_ctx_set_index_event": ([_vp, _vp], C.c_int),
+    "gp_ctx_set_decode_overwrite": ([_vp, C.c_int], C.c_int),
     "gp_decode_index_prepare": ([_vp, _vp, _u64, _u64, _u64, C.c_int, _vp], C.c_int),
     "gp_decode_accumulate_own": ([_vp, _vp, _u64, _vp, _P(GpConfig), _vp, _u64, C.c_float, _vp], C.c_int),
     "gp_decode_prepare": ([_vp, _vp, _u64, _vp, _P(GpConfig), _vp], C.c_int),

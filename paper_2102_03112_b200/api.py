@@ -253,10 +253,23 @@ class Codec:
         return out[: int(self._len[0].item())]
 
     # -------------------------------------------------------------- decode
+    def set_decode_overwrite(self, on: bool):
+        """Following decodes write dense = scale * decoded (zeros off the support)
+        instead of accumulating — zero + accumulate in one pass."""
+        self._raise(lib.gp_ctx_set_decode_overwrite(self._ctx, 1 if on else 0))
+
     def decode_accumulate(self, container: torch.Tensor, dense: torch.Tensor, scale: float = 1.0,
-                          length: int | None = None, hint: PipelineConfig | None = None, stream=None):
-        """Asynchronous unpack + decompress_gradient + dense[support] += scale * values."""
+                          length: int | None = None, hint: PipelineConfig | None = None, stream=None,
+                          overwrite: bool = False):
+        """Asynchronous unpack + decompress_gradient + dense[support] += scale * values
+        (overwrite=True: dense = scale * decoded, zeros elsewhere)."""
         assert dense.dtype == torch.float32 and dense.is_cuda and dense.is_contiguous()
+        if overwrite:
+            self.set_decode_overwrite(True)
+            try:
+                return self.decode_accumulate(container, dense, scale, length, hint, stream)
+            finally:
+                self.set_decode_overwrite(False)
         if isinstance(length, torch.Tensor):  # device length word: fully asynchronous path
             assert hint is not None, "a device-side length needs a dispatch hint"
             c = hint.to_c()
@@ -300,8 +313,16 @@ class Codec:
         self._raise(lib.gp_decode_prepare(self._ctx, _ptr(container), container.numel(), _ptr(length), C.byref(h),
                                           _stream(stream)))
 
-    def decode_finish(self, container: torch.Tensor, dense: torch.Tensor, scale: float = 1.0, stream=None):
-        """dense[support] += scale * values of the container this context prepared."""
+    def decode_finish(self, container: torch.Tensor, dense: torch.Tensor, scale: float = 1.0, stream=None,
+                      overwrite: bool = False):
+        """dense[support] += scale * values of the container this context prepared
+        (overwrite=True: dense = scale * decoded, zeros elsewhere)."""
+        if overwrite:
+            self.set_decode_overwrite(True)
+            try:
+                return self.decode_finish(container, dense, scale, stream)
+            finally:
+                self.set_decode_overwrite(False)
         self._raise(lib.gp_decode_finish(self._ctx, _ptr(container), _ptr(dense), dense.numel(), float(scale),
                                          _stream(stream)))
 

@@ -302,6 +302,12 @@ int gp_ctx_set_index_event(gp_ctx* ctx, void* event) {
   return GP_OK;
 }
 
+int gp_ctx_set_decode_overwrite(gp_ctx* ctx, int on) {
+  if (!ctx) return GP_ERROR;
+  ctx->decode_overwrite = on != 0;
+  return GP_OK;
+}
+
 int gp_ctx_set_seed_source(gp_ctx* ctx, const uint64_t* d_seed) {
   if (!ctx) return GP_ERROR;
   ctx->seed_dev = d_seed;
@@ -485,6 +491,15 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
   pi.seed_dev = ctx->seed_dev;
   GP_LAUNCH(ctx, init_plan, 1, 1, 0, s, ctx->ws.plan, pi);
 
+  // dense-selection fast path (dense.cu): one pass writes bitmap + raw values
+  // when top_r(g, r) is the nonzero set; the general kernels below then run
+  // against the gate word and return at once (or run, when r != nnz)
+  const bool nz = !d_support && !ef_residual && nz_fast_path_eligible(d, r, im, vm);
+  uint32_t* const real_status = ctx->ws.status;
+  if (nz) {
+    GP_STAGE(ctx, ST_INDEX, s, launch_nz_encode(ctx, d_dense, d, r, d_out, s));
+    ctx->ws.status = gate_word(ctx);
+  }
   if (d_support) {
     GP_LAUNCH(ctx, take_support, grid_for(ctx, r, 256), 256, 0, s, d_dense, d_support, r, d, ctx->ws.support,
               ctx->ws.values, ctx->ws.status);
@@ -528,6 +543,10 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
       break;
     case GP_VALUE_DEFLATE_SLOT: launch_values_slot(ctx, d_out, n_bound, s); break;
     default: break;
+  }
+  if (nz) {
+    ctx->ws.status = real_status;
+    launch_gate_merge(ctx, s);
   }
   GP_STAGE(ctx, ST_PACK, s, launch_finish_container(ctx, d_out, cap, d_len, bound, s));
   return check_launch(ctx, "encode");
@@ -586,11 +605,22 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const u
   }
   if (!known) return check_launch(ctx, "decode");  // the CRC verdict step latches UnknownMethod
   const uint64_t bound = ctx->max_d;
+  // bitmap + raw values into a dense buffer (or a prepare for one): the fused
+  // dense path (dense.cu) — per-tile counts and checks now, one scatter pass
+  // reading bitmap words and value runs, no materialised support
+  const bool fused = im == GP_INDEX_BITMAP && (vm == GP_VALUE_NONE || vm == GP_VALUE_RAW_F64) && !own &&
+                     !d_support && (d_dense || !scatter);
   if (own && im != GP_INDEX_BLOOM_NAIVE) {
     if (!is_bloom(im)) launch_own_support(ctx, bound, s);
   } else switch (im) {
     case GP_INDEX_NONE: launch_decode_index_none(ctx, d_in, bound, s); break;
-    case GP_INDEX_BITMAP: launch_decode_index_bitmap(ctx, d_in, bound, s); break;
+    case GP_INDEX_BITMAP:
+      if (fused) {
+        GP_STAGE(ctx, ST_DEC_INDEX, s, launch_decode_bitmap_check(ctx, d_in, s); launch_bm_prepare(ctx, d_in, bound, s));
+      } else {
+        launch_decode_index_bitmap(ctx, d_in, bound, s);
+      }
+      break;
     case GP_INDEX_RLE: GP_STAGE(ctx, ST_DEC_INDEX, s, launch_decode_index_rle(ctx, d_in, len, bound, s)); break;
     case GP_INDEX_HUFFMAN: GP_STAGE(ctx, ST_DEC_INDEX, s, launch_decode_index_huffman(ctx, d_in, len, s)); break;
     default: {
@@ -617,6 +647,12 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const u
     default: break;
   }
   if ((im == GP_INDEX_NONE || im == GP_INDEX_HUFFMAN) && !own) launch_validate_support(ctx, bound, s);
+  if (scatter && fused) {
+    GP_STAGE(ctx, ST_DEC_SCATTER, s,
+             launch_bm_scatter(ctx, d_in, bound, d_dense, dense_d, scale, ctx->decode_overwrite, s));
+    return check_launch(ctx, "decode");
+  }
+  if (scatter && d_dense && ctx->decode_overwrite) launch_dense_zero(ctx, d_dense, dense_d, s);
   if (scatter)
     GP_STAGE(ctx, ST_DEC_SCATTER, s,
              launch_decode_scatter(ctx, d_in, bound, d_dense, dense_d, scale, d_support, d_values, cap, d_count, d_dim, s));
@@ -653,6 +689,9 @@ int gp_decode_finish(gp_ctx* ctx, const uint8_t* d_container, float* d_dense, ui
                      void* stream) {
   if (!ctx || !d_container || !d_dense) return set_error(ctx, GP_ERROR, "decode_finish: null argument");
   auto s = static_cast<cudaStream_t>(stream);
+  // the prepare chose the path on the device: exactly one of the two scatters runs
+  if (ctx->decode_overwrite) launch_dense_zero(ctx, d_dense, d, s);
+  launch_bm_scatter(ctx, d_container, ctx->max_d, d_dense, d, scale, ctx->decode_overwrite, s);
   GP_STAGE(ctx, ST_DEC_SCATTER, s,
            launch_decode_scatter(ctx, d_container, ctx->max_d, d_dense, d, scale, nullptr, nullptr, 0, nullptr, nullptr,
                                  s));

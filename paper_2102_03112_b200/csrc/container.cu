@@ -20,8 +20,13 @@ namespace gp {
 namespace {
 
 constexpr uint32_t kPoly = 0x82F63B78u;
-constexpr int kCrcBlock = 256;
-constexpr int kCrcBlocksPerSm = 4;  // the CRC grid is fixed: sm_count * 4 blocks (the lane stride is baked into M)
+constexpr int kCrcBlock = 1024;
+constexpr int kCrcBlocksPerSm = 1;  // the CRC grid is fixed: one 1024-lane block per SM (the lane stride is baked into M)
+// slice-by-4 tables replicated per warp lane: entry e of table k for lane l at
+// word (k * 256 + e) * 32 + l, so lane l only ever reads bank l — the random
+// byte-indexed lookups of a warp are conflict-free (a shared 256-entry table
+// serialises ~3.5-way on average).  128 KiB of dynamic shared memory.
+constexpr int kCrcLaneTableWords = 4 * 256 * 32;
 
 __device__ __forceinline__ uint32_t multmodp(uint32_t a, uint32_t b) {
   // a * b mod P in the reflected representation (bit 31 = x^0)
@@ -114,7 +119,8 @@ __global__ void __launch_bounds__(kCrcBlock) crc_chunks(const uint8_t* __restric
                                                         const uint32_t* __restrict__ digits, uint32_t* acc,
                                                         uint32_t* done, uint32_t* out, const CrcEpilogue ep,
                                                         uint32_t* status) {
-  __shared__ uint32_t T[4][256];
+  extern __shared__ uint32_t TL[];  // [4][256][32] per-lane slice-by-4 tables
+  __shared__ uint32_t T0[256];
   __shared__ uint32_t D[5][256];
   __shared__ uint32_t M[4][256];
   __shared__ uint32_t red[kCrcBlock / 32];
@@ -129,23 +135,27 @@ __global__ void __launch_bounds__(kCrcBlock) crc_chunks(const uint8_t* __restric
   // blocks without chunks (most of the fixed grid for a small container) skip
   // the table setup and only join the reduction
   const bool active = static_cast<uint64_t>(blockIdx.x) * kCrcBlock < nchunks;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t* TLl = TL + lane;
   uint32_t A = 0;
   uintptr_t prev_end = 0;
   if (active) {
     for (int i = threadIdx.x; i < 256; i += kCrcBlock) {
       uint32_t c = static_cast<uint32_t>(i);
       for (int j = 0; j < 8; ++j) c = (c >> 1) ^ ((c & 1u) ? kPoly : 0u);
-      T[0][i] = c;
+      T0[i] = c;
     }
     for (int i = threadIdx.x; i < 5 * 256; i += kCrcBlock) D[i / 256][i % 256] = digits[i];
     for (int i = threadIdx.x; i < 4 * 256; i += kCrcBlock) M[i / 256][i % 256] = digits[5 * 256 + i];
     __syncthreads();
-    for (int i = threadIdx.x; i < 256; i += kCrcBlock) {
-      uint32_t c = T[0][i];
-      for (int k = 1; k < 4; ++k) {
-        c = (c >> 8) ^ T[0][c & 0xFFu];
-        T[k][i] = c;
-      }
+    // T_k[e] = T_{k-1}[e] advanced by one zero byte; replicate into every lane's column
+    for (int i = threadIdx.x; i < 4 * 256; i += kCrcBlock) {
+      const int k = i >> 8, e = i & 255;
+      uint32_t c = T0[e];
+      for (int j = 0; j < k; ++j) c = (c >> 8) ^ T0[c & 0xFFu];
+      uint32_t* dst = TL + static_cast<uint32_t>(i) * 32;
+#pragma unroll 8
+      for (int l = 0; l < 32; ++l) dst[(l + threadIdx.x) & 31] = c;  // rotate the start: spread the banks
     }
     __syncthreads();
     const uint64_t lanes = static_cast<uint64_t>(gridDim.x) * kCrcBlock;  // == kCrcLanes (host)
@@ -164,12 +174,13 @@ __global__ void __launch_bounds__(kCrcBlock) crc_chunks(const uint8_t* __restric
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             c ^= w[j];
-            c = T[3][c & 0xFFu] ^ T[2][(c >> 8) & 0xFFu] ^ T[1][(c >> 16) & 0xFFu] ^ T[0][c >> 24];
+            c = TLl[(3 * 256 + (c & 0xFFu)) * 32] ^ TLl[(2 * 256 + ((c >> 8) & 0xFFu)) * 32] ^
+                TLl[(256 + ((c >> 16) & 0xFFu)) * 32] ^ TLl[(c >> 24) * 32];
           }
         }
       } else {
         const uint8_t* b = reinterpret_cast<const uint8_t*>(lo);
-        for (uintptr_t i = 0; i < hi - lo; ++i) c = (c >> 8) ^ T[0][(c ^ b[i]) & 0xFFu];
+        for (uintptr_t i = 0; i < hi - lo; ++i) c = (c >> 8) ^ T0[(c ^ b[i]) & 0xFFu];
       }
       if (prev_end) A = (hi == cs + 64) ? mul_const(M, A) : multmodp(shift_op(D, hi - prev_end), A);
       A ^= c;
@@ -239,6 +250,7 @@ __global__ void parse_container(const uint8_t* __restrict__ in, uint64_t len_hos
   plan->value_method = value_id;
   plan->flags = flags;
   plan->crc_stored = ld_u32_unaligned(in + 49 + il + vl + rl);
+  plan->fused_bitmap = 0;
   // post-CRC checks, in container.cpp order, then pipeline.cpp:224-225
   uint32_t post = 0;
   if (index_id > GP_INDEX_BLOOM_NAIVE || value_id > GP_VALUE_RAW_F64) post = GP_UNKNOWN_METHOD;
@@ -290,7 +302,9 @@ int crc_tables_init(gp_ctx* ctx) {
     if (stride & 0xFF) S = mult(tab[i * 256 + (stride & 0xFF)], S);
   for (int j = 0; j < 4; ++j)
     for (int b = 0; b < 256; ++b) tab[(5 + j) * 256 + b] = b ? mult(static_cast<uint32_t>(b) << (8 * j), S) : 0u;
-  cudaError_t e = cudaMemcpy(w.crc_digits, tab, sizeof(tab), cudaMemcpyHostToDevice);
+  cudaError_t e = cudaFuncSetAttribute(crc_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kCrcLaneTableWords * static_cast<int>(sizeof(uint32_t)));
+  if (e == cudaSuccess) e = cudaMemcpy(w.crc_digits, tab, sizeof(tab), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemset(w.crc_acc, 0, 2 * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   w.crc_ready = e == cudaSuccess;
@@ -303,7 +317,7 @@ void crc_range(gp_ctx* ctx, const uint8_t* base, const uint64_t* off_dev, uint64
                const CrcEpilogue& ep) {
   Workspace& w = ctx->ws;
   const int grid = ctx->sm_count * kCrcBlocksPerSm;
-  GP_LAUNCH(ctx, crc_chunks, grid, kCrcBlock, 0, s, base, off_dev, off_host, la, lb, lc, len_host, w.crc_digits,
+  GP_LAUNCH(ctx, crc_chunks, grid, kCrcBlock, kCrcLaneTableWords * sizeof(uint32_t), s, base, off_dev, off_host, la, lb, lc, len_host, w.crc_digits,
             w.crc_acc, w.crc_acc + 1, out, ep, w.status);
 }
 }  // namespace

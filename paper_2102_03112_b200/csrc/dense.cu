@@ -1,0 +1,350 @@
+// dense.cu — the dense-selection fast path: bitmap index + raw f32 values in
+// one pass each way (C3, NCF-style natural sparsity, where the support is the
+// nonzeros: top_r(g, nnz)).
+//
+// Encode (`nz_encode`, one read of g): every 8192-element tile ballots its
+// nonzeros into the bitmap words (gradient.cpp:56-65, :81-86: bit i of byte
+// i/8, LSB-first), compacts the nonzero values in shared memory and, with the
+// tile's value offset from a decoupled look-back, stores both straight into
+// the container (index payload at 49, value payload at 49 + ceil(d/8);
+// pipeline.cpp:171-173, :56-93 raw f32) with 16-byte stores.  The selection
+// is SPECULATIVE: top_r(g, r) is the nonzero set exactly when r equals the
+// nonzero count (the r largest |g| are then all nonzero keys and ties cannot
+// straddle the cut, sparsify.cpp:32-46), which only the last tile knows.  It
+// opens a gate word: SKIP when the count matched (the general top-r + bitmap +
+// raw kernels that follow on the stream, launched against the gate as their
+// status word, return at once), 0 otherwise (they run and overwrite every
+// byte).  gate_merge then moves any error the general path latched into the
+// context status.
+//
+// Decode (`bm_counts` → one-block scan → `bm_total` → `bm_scatter`): per-tile
+// popcounts of the bitmap, their prefix, the popcount == r check
+// (pipeline.cpp:242-243) BEFORE any write, then one pass that reads each
+// tile's bitmap words and contiguous value run and writes the tile's dense
+// slice: dense = fmaf(scale, v, dense) on the support (accumulate), or, in
+// overwrite mode, the whole slice (scale·v on the support, 0 elsewhere —
+// identical to accumulating into a zeroed vector) without reading it.
+#include "gp_ctx.hpp"
+#include "gp_device.cuh"
+
+namespace gp {
+
+namespace {
+
+constexpr int kNzBlock = 256;                  // 8 warps
+constexpr int kNzTile = kNzBlock * 32;         // elements per tile: 32 per lane, 1024 per warp
+constexpr uint32_t kGateSkip = 0xFFFFu;        // gate value: the fast path produced the payloads
+
+// Copies n bytes from 4-byte-aligned shared memory to an arbitrary global
+// address: single bytes up to the first 16-byte boundary and after the last,
+// 16-byte stores in between (each assembled from five shared words with funnel
+// shifts).  Neighbouring tiles write the other bytes of the boundary words.
+// `src` must be readable 16 bytes past n.
+__device__ __forceinline__ void block_store_bytes(uint8_t* dst, const uint32_t* src, uint64_t n) {
+  const uint8_t* sb = reinterpret_cast<const uint8_t*>(src);
+  const uint32_t head = static_cast<uint32_t>((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15);
+  if (n <= head + 16) {
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = sb[i];
+    return;
+  }
+  for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) dst[i] = sb[i];
+  const uint64_t nvec = (n - head) / 16;
+  const uint32_t sh = 8 * (head & 3);
+  uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+  for (uint64_t v = threadIdx.x; v < nvec; v += blockDim.x) {
+    const uint32_t* s = src + ((head + 16 * v) >> 2);
+    const uint32_t w0 = s[0], w1 = s[1], w2 = s[2], w3 = s[3], w4 = s[4];
+    uint4 o;
+    o.x = __funnelshift_r(w0, w1, sh);
+    o.y = __funnelshift_r(w1, w2, sh);
+    o.z = __funnelshift_r(w2, w3, sh);
+    o.w = __funnelshift_r(w3, w4, sh);
+    d4[v] = o;
+  }
+  for (uint64_t i = head + 16 * nvec + threadIdx.x; i < n; i += blockDim.x) dst[i] = sb[i];
+}
+
+// Loads n bytes from an arbitrary global address into 4-byte-aligned shared
+// memory (the mirror of block_store_bytes).
+__device__ __forceinline__ void block_load_bytes(uint32_t* dst, const uint8_t* src, uint64_t n) {
+  uint8_t* db = reinterpret_cast<uint8_t*>(dst);
+  const uint32_t head = static_cast<uint32_t>((16 - (reinterpret_cast<uintptr_t>(src) & 15)) & 15);
+  if (n <= head + 16) {
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) db[i] = src[i];
+    return;
+  }
+  for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) db[i] = src[i];
+  const uint64_t nvec = (n - head) / 16;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
+  for (uint64_t v = threadIdx.x; v < nvec; v += blockDim.x) {
+    const uint4 x = __ldcs(s4 + v);  // streamed once
+    uint8_t* o = db + head + 16 * v;
+    // byte-granular shared stores of the 16 bytes (o is only 1-aligned in general)
+    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+    if ((head & 3) == 0) {
+      uint32_t* o32 = reinterpret_cast<uint32_t*>(o);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o32[k] = w[k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) o[k] = static_cast<uint8_t>(w[k >> 2] >> (8 * (k & 3)));
+    }
+  }
+  for (uint64_t i = head + 16 * nvec + threadIdx.x; i < n; i += blockDim.x) db[i] = src[i];
+}
+
+__global__ void __launch_bounds__(kNzBlock) nz_encode(const float* __restrict__ g, uint64_t d, uint64_t r,
+                                                      uint8_t* out, Plan* plan, uint64_t* tiles, uint32_t* ticket,
+                                                      uint32_t* gate, const uint32_t* status) {
+  __shared__ uint32_t vals[kNzTile + 8];
+  __shared__ uint32_t words[kNzBlock + 8];
+  __shared__ uint64_t sh[36];
+  __shared__ uint32_t slot;
+  if (failed(status)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *gate = ld_relaxed_u32(status);  // the general path stays shut
+    return;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const uint64_t ntiles = (d + kNzTile - 1) / kNzTile;
+  const uint64_t bm_bytes = (d + 7) / 8;
+  uint8_t* bm_out = out + 49;
+  uint8_t* val_out = out + 49 + bm_bytes;
+  while (true) {
+    const uint32_t tile = claim_tile(ticket, &slot);
+    if (tile >= ntiles) break;
+    const uint64_t base = static_cast<uint64_t>(tile) * kNzTile + static_cast<uint64_t>(warp) * 1024;
+    uint32_t x[32];
+    if (base + 1024 <= d) {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) x[k] = __float_as_uint(__ldcs(g + base + 32 * k + lane));
+    } else {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const uint64_t i = base + 32 * k + lane;
+        x[k] = i < d ? __float_as_uint(__ldcs(g + i)) : 0u;
+      }
+    }
+    uint32_t cnt = 0, myword = 0;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const unsigned b = __ballot_sync(kFull, (x[k] & 0x7FFFFFFFu) != 0u);
+      if (lane == k) myword = b;
+      cnt += __popc(b);
+    }
+    words[threadIdx.x] = myword;  // word warp*32 + lane of the tile
+    uint64_t tile_total;
+    // lane 0 of warp w: tile prefix + values of warps < w (the block scan inside)
+    const uint64_t wo = tile_exclusive_offset<kNzBlock>(lane == 0 ? cnt : 0, tile, tiles, sh, tile_total);
+    const uint64_t tile_prefix = sh[34];  // the tile's global value offset (published by the look-back)
+    uint32_t at = static_cast<uint32_t>(__shfl_sync(kFull, wo, 0) - tile_prefix);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const bool nz = (x[k] & 0x7FFFFFFFu) != 0u;
+      const unsigned b = __ballot_sync(kFull, nz);
+      if (nz) vals[at + __popc(b & lt)] = x[k];
+      at += __popc(b);
+    }
+    __syncthreads();
+    // bitmap bytes of the tile (the last tile stops at ceil(d/8))
+    const uint64_t b0 = static_cast<uint64_t>(tile) * (kNzTile / 8);
+    const uint64_t nb = b0 + kNzTile / 8 <= bm_bytes ? kNzTile / 8 : bm_bytes - b0;
+    block_store_bytes(bm_out + b0, words, nb);
+    block_store_bytes(val_out + 4 * tile_prefix, vals, 4 * tile_total);
+    if (tile == ntiles - 1 && threadIdx.x == 0) {
+      const uint64_t nnz = tile_prefix + tile_total;
+      if (nnz == r) {
+        plan->vl = 4 * r;
+        plan->n_values = r;
+        plan->n_sel = r;
+        *gate = kGateSkip;
+      }
+    }
+    __syncthreads();  // vals / words are rewritten by the next tile
+  }
+}
+
+__global__ void gate_merge(const uint32_t* gate, uint32_t* status) {
+  const uint32_t gv = *gate;
+  if (gv != 0u && gv != kGateSkip) latch(status, gv);
+}
+
+// ------------------------------------------------------------ decode
+constexpr int kBmTileBytes = kNzTile / 8;  // 1 KiB of bitmap = 8192 coordinates per tile
+
+// per-tile popcounts of the bitmap payload (tiles[t], u64)
+__global__ void bm_counts(const uint8_t* __restrict__ in, const Plan* plan, uint64_t* counts,
+                          const uint32_t* status) {
+  if (failed(status) || plan->index_method != GP_INDEX_BITMAP) return;
+  const uint64_t nbytes = plan->il;
+  const uint8_t* p = in + plan->off_index;
+  const uint64_t ntiles = (nbytes + kBmTileBytes - 1) / kBmTileBytes;
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); t < ntiles;
+       t += warps) {
+    uint32_t c = 0;
+    const uint64_t b0 = t * kBmTileBytes;
+#pragma unroll
+    for (int q = 0; q < kBmTileBytes / 128; ++q) {
+      const uint64_t at = b0 + q * 128 + 4 * lane;
+      uint32_t v = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (at + k < nbytes) v |= static_cast<uint32_t>(p[at + k]) << (8 * k);
+      c += __popc(v);
+    }
+    c = __reduce_add_sync(kFull, c);
+    if (lane == 0) counts[t] = c;
+  }
+}
+
+// after the scan: total popcount, the decode's support size, the r check
+__global__ void bm_total(Plan* plan, const uint64_t* counts_excl, const uint64_t* counts, uint32_t* status) {
+  if (failed(status) || plan->index_method != GP_INDEX_BITMAP) return;
+  const uint64_t ntiles = (plan->il + kBmTileBytes - 1) / kBmTileBytes;
+  const uint64_t n = ntiles ? counts_excl[ntiles - 1] + counts[ntiles - 1] : 0;
+  plan->n_sel = n;
+  plan->n_values = n;
+  plan->fused_bitmap = 1;
+  if (n != plan->r) latch(status, GP_CORRUPT_PAYLOAD);  // pipeline.cpp:242-243
+}
+
+// One tile (8192 coordinates) per block iteration: the tile's value run is
+// staged in shared memory, then warp w writes coordinates [1024w, 1024w+1024)
+// of the tile, lane l coordinate 32k + l of word k (coalesced).
+__global__ void __launch_bounds__(kNzBlock) bm_scatter(const uint8_t* __restrict__ in, const Plan* plan,
+                                                       const uint64_t* offs, float* dense, uint64_t dense_d,
+                                                       float scale, int overwrite, uint32_t* status) {
+  __shared__ uint32_t vals[kNzTile + 8];
+  __shared__ uint32_t words[kNzBlock + 8];
+  __shared__ uint32_t woff[kNzBlock / 32];
+  if (failed(status) || !plan->fused_bitmap) return;
+  const uint64_t d = plan->d;
+  if (d != dense_d) {  // to_dense builds a d-vector (gradient.cpp:38-42): a mismatch is caller misuse
+    if (blockIdx.x == 0 && threadIdx.x == 0) latch(status, GP_ERROR);
+    return;
+  }
+  const uint64_t nbytes = plan->il;
+  const uint8_t* bm = in + plan->off_index;
+  const uint8_t* vp = in + plan->off_value;
+  const bool f64 = plan->value_method == GP_VALUE_RAW_F64;
+  const uint64_t ntiles = (nbytes + kBmTileBytes - 1) / kBmTileBytes;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const uint64_t b0 = t * kBmTileBytes;
+    const uint64_t nb = b0 + kBmTileBytes <= nbytes ? kBmTileBytes : nbytes - b0;
+    if (threadIdx.x < kNzBlock) {
+      const uint64_t at = b0 + 4 * static_cast<uint64_t>(threadIdx.x);
+      uint32_t v = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (at + k < b0 + nb) v |= static_cast<uint32_t>(bm[at + k]) << (8 * k);
+      words[threadIdx.x] = v;
+    }
+    const uint64_t off = offs[t];
+    __syncthreads();
+    const uint32_t cnt_w = __reduce_add_sync(kFull, __popc(words[threadIdx.x]));
+    if (lane == 0) woff[warp] = cnt_w;
+    __syncthreads();
+    uint32_t tile_n = 0, my_off = 0;
+    for (int w = 0; w < kNzBlock / 32; ++w) {
+      if (w == warp) my_off = tile_n;
+      tile_n += woff[w];
+    }
+    if (!f64) {
+      block_load_bytes(vals, vp + 4 * off, 4ull * tile_n);
+    }
+    __syncthreads();
+    const uint64_t base = t * kNzTile + static_cast<uint64_t>(warp) * 1024;
+    uint32_t at = my_off;
+#pragma unroll 4
+    for (int k = 0; k < 32; ++k) {
+      const uint32_t wk = words[warp * 32 + k];
+      const uint64_t i = base + 32 * k + lane;
+      const bool on = (wk >> lane) & 1u;
+      if (i < d) {
+        float v = 0.0f;
+        if (on) {
+          const uint32_t j = at + __popc(wk & lt);
+          v = f64 ? static_cast<float>(__longlong_as_double(static_cast<long long>(
+                        ld_u64_unaligned(vp + 8 * (off + j)))))
+                  : __uint_as_float(vals[j]);
+        }
+        if (overwrite) {
+          dense[i] = on ? fmaf(scale, v, 0.0f) : 0.0f;
+        } else if (on) {
+          dense[i] = fmaf(scale, v, dense[i]);
+        }
+      }
+      at += __popc(wk);
+    }
+    __syncthreads();
+  }
+}
+
+// overwrite mode on the general scatter path: zero the dense buffer first
+// (skipped when the fused bitmap scatter writes every coordinate itself)
+__global__ void dense_zero(float* dense, uint64_t n, const Plan* plan, const uint32_t* status) {
+  if (failed(status) || plan->fused_bitmap) return;
+  float4* d4 = reinterpret_cast<float4*>(dense);
+  const uint64_t n4 = (reinterpret_cast<uintptr_t>(dense) & 15) ? 0 : n / 4;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n4; i += stride)
+    d4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (uint64_t i = 4 * n4 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+    dense[i] = 0.f;
+}
+
+}  // namespace
+
+void launch_dense_zero(gp_ctx* ctx, float* dense, uint64_t n, cudaStream_t s) {
+  GP_LAUNCH(ctx, dense_zero, grid_for(ctx, (n + 3) / 4, 256), 256, 0, s, dense, n, ctx->ws.plan, ctx->ws.status);
+}
+
+bool nz_fast_path_eligible(uint64_t d, uint64_t r, int index_method, int value_method) {
+  // nonzero-selection workloads keep most coordinates; a top-1% selection
+  // would always miss the speculation and pay an extra pass over g
+  return index_method == GP_INDEX_BITMAP && value_method == GP_VALUE_NONE && 4 * r >= d && d >= kNzTile;
+}
+
+uint32_t* gate_word(gp_ctx* ctx) { return ctx->ws.status + 32; }
+
+void launch_nz_encode(gp_ctx* ctx, const float* g, uint64_t d, uint64_t r, uint8_t* out, cudaStream_t s) {
+  Workspace& w = ctx->ws;
+  const uint64_t ntiles = (d + kNzTile - 1) / kNzTile;
+  cudaMemsetAsync(gate_word(ctx), 0, sizeof(uint32_t), s);
+  reset_scan(ctx, s, ntiles + 1);
+  const int grid = static_cast<int>(ntiles < static_cast<uint64_t>(ctx->sm_count) * 6 ? ntiles
+                                                                                       : ctx->sm_count * 6);
+  GP_LAUNCH(ctx, nz_encode, grid, kNzBlock, 0, s, g, d, r, out, w.plan, w.tiles, w.ticket, gate_word(ctx), w.status);
+}
+
+void launch_gate_merge(gp_ctx* ctx, cudaStream_t s) {
+  GP_LAUNCH(ctx, gate_merge, 1, 1, 0, s, gate_word(ctx), ctx->ws.status);
+}
+
+// decode: counts → scan → total/check (the scatter is launch_bm_scatter)
+void launch_bm_prepare(gp_ctx* ctx, const uint8_t* in, uint64_t d_bound, cudaStream_t s) {
+  Workspace& w = ctx->ws;
+  const uint64_t ntiles = ((d_bound + 7) / 8 + kBmTileBytes - 1) / kBmTileBytes;
+  uint64_t* counts = w.tiles;
+  uint64_t* excl = w.tiles + ntiles + 1;
+  GP_LAUNCH(ctx, bm_counts, grid_for(ctx, ntiles * 32, 256), 256, 0, s, in, w.plan, counts, w.status);
+  cudaMemcpyAsync(excl, counts, ntiles * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s);
+  GP_LAUNCH(ctx, scan_chunk_counts<8>, 1, 1024, 0, s, excl, nullptr, ntiles, w.status);
+  GP_LAUNCH(ctx, bm_total, 1, 1, 0, s, w.plan, excl, counts, w.status);
+}
+
+void launch_bm_scatter(gp_ctx* ctx, const uint8_t* in, uint64_t d_bound, float* dense, uint64_t dense_d, float scale,
+                       bool overwrite, cudaStream_t s) {
+  Workspace& w = ctx->ws;
+  const uint64_t ntiles = ((d_bound + 7) / 8 + kBmTileBytes - 1) / kBmTileBytes;
+  const uint64_t cap = static_cast<uint64_t>(ctx->sm_count) * 6;
+  const int grid = static_cast<int>(ntiles < cap ? (ntiles ? ntiles : 1) : cap);
+  GP_LAUNCH(ctx, bm_scatter, grid, kNzBlock, 0, s, in, w.plan, w.tiles + ntiles + 1, dense, dense_d, scale,
+            overwrite ? 1 : 0, w.status);
+}
+
+}  // namespace gp

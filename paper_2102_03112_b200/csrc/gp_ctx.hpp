@@ -45,7 +45,8 @@ struct Plan {
   uint32_t nseg, degree;
   uint32_t q_bits, q_bucket;    // quantizer header (decode)
   uint32_t fit_kind, dexp_fail; // fit model kind (0 poly, 1 dexp); a dexp part failed (fallback)
-  uint32_t slot_id, pad2;       // byte codec of a value-id-4 slot (0 store, 1 deflate; decode)
+  uint32_t slot_id, fused_bitmap;  // byte codec of a value-id-4 slot (0 store, 1 deflate; decode);
+                                   // bitmap decode on the fused dense path (dense.cu), else 0
   uint32_t seg_end[64];         // fit bounds (<= 64 segments on this path)
   float coeffs[64 * 8];
   // ---- decode
@@ -150,6 +151,7 @@ struct gp_ctx {
   gp::Profiler prof;
   const uint64_t* seed_dev = nullptr;  // gp_ctx_set_seed_source: pipeline seed read on the device
   cudaEvent_t index_event = nullptr;   // gp_ctx_set_index_event: recorded once encode's index payload is final
+  bool decode_overwrite = false;       // gp_ctx_set_decode_overwrite: dense = scale * decoded (zeros off the support)
 };
 
 namespace gp {
@@ -198,6 +200,15 @@ void launch_crc_range(gp_ctx* ctx, const uint8_t* base, const uint64_t* off_dev,
                       const uint64_t* la, const uint64_t* lb, const uint64_t* lc, uint64_t len_host,
                       uint64_t len_bound, uint32_t* out, cudaStream_t s);
 int crc_tables_init(gp_ctx* ctx);  // container.cu (gp_ctx_create)
+bool nz_fast_path_eligible(uint64_t d, uint64_t r, int index_method, int value_method);  // dense.cu
+uint32_t* gate_word(gp_ctx* ctx);
+void launch_nz_encode(gp_ctx* ctx, const float* g, uint64_t d, uint64_t r, uint8_t* out, cudaStream_t s);
+void launch_gate_merge(gp_ctx* ctx, cudaStream_t s);
+void launch_dense_zero(gp_ctx* ctx, float* dense, uint64_t n, cudaStream_t s);
+void launch_decode_bitmap_check(gp_ctx* ctx, const uint8_t* in, cudaStream_t s);  // indexcodec.cu
+void launch_bm_prepare(gp_ctx* ctx, const uint8_t* in, uint64_t d_bound, cudaStream_t s);
+void launch_bm_scatter(gp_ctx* ctx, const uint8_t* in, uint64_t d_bound, float* dense, uint64_t dense_d, float scale,
+                       bool overwrite, cudaStream_t s);
 void launch_crc_host_range(gp_ctx* ctx, const uint8_t* data, uint64_t n, uint32_t* out, cudaStream_t s);
 void launch_finish_container(gp_ctx* ctx, uint8_t* out, uint64_t cap, uint64_t* d_len, uint64_t len_bound,
                              cudaStream_t s);

@@ -198,6 +198,10 @@ void launch_validate_support(gp_ctx* ctx, uint64_t r_bound, cudaStream_t s) {
   GP_LAUNCH(ctx, support_validate, grid_for(ctx, r_bound, 256), 256, 0, s, w.plan, w.sel, w.status);
 }
 
+void launch_decode_bitmap_check(gp_ctx* ctx, const uint8_t* in, cudaStream_t s) {
+  GP_LAUNCH(ctx, bitmap_check, 1, 1, 0, s, in, ctx->ws.plan, ctx->ws.status);
+}
+
 void launch_decode_index_bitmap(gp_ctx* ctx, const uint8_t* in, uint64_t d_bound, cudaStream_t s) {
   Workspace& w = ctx->ws;
   GP_LAUNCH(ctx, bitmap_check, 1, 1, 0, s, in, w.plan, w.status);

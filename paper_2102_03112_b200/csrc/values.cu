@@ -76,7 +76,7 @@ __global__ void decode_scatter(const uint8_t* __restrict__ in, const Plan* plan,
                                const double* __restrict__ fitv, float* dense, uint64_t dense_d, float scale,
                                uint32_t* out_support, double* out_values, uint64_t cap, uint64_t* d_count,
                                uint64_t* d_dim, uint32_t* status) {
-  if (failed(status)) return;
+  if (failed(status) || plan->fused_bitmap) return;  // bitmap containers on the fused path: dense.cu bm_scatter
   // the container's d must equal the caller's dense length: to_dense builds a
   // d-vector (gradient.cpp:38-42) and the mean adds equal-length vectors
   // (harness.cpp:274-284); a mismatch is caller misuse, never a stray write

@@ -147,11 +147,11 @@ class SparseAllgather:
             self.codec.encode_ef_into(grad, self.residual, self.r, cfg, self.out, self.length, stream=stream)
         else:
             self.codec.encode_into(grad, self.r, cfg, self.out, self.length, stream=stream)
-        out_dense.zero_()
         n = self.world
+        # the first container of the mean overwrites the output (zero + accumulate in one pass)
         if n == 1:  # no exchange: the device-side length drives the decode (no host sync)
             self.codec.decode_accumulate(self.out, out_dense, scale=1.0, length=self.length, hint=self.cfg,
-                                         stream=stream)
+                                         stream=stream, overwrite=True)
             return out_dense
         # the step's one host sync: a latched encode error (or a previous step's
         # decode error) raises here instead of shipping a stale container
@@ -163,7 +163,7 @@ class SparseAllgather:
         if self.dec_streams is None:
             for j in range(n):  # fixed rank order, as the harness's worker order
                 self.codec.decode_accumulate(self.recv[j * mx: j * mx + sizes[j]], out_dense, scale=1.0 / n,
-                                             hint=self.cfg, stream=stream)
+                                             hint=self.cfg, stream=stream, overwrite=(j == 0))
             return out_dense
         main = stream if stream is not None else torch.cuda.current_stream()
         self._decode_concurrent(n, mx, out_dense, main)
@@ -220,7 +220,7 @@ class SparseAllgather:
             ready = torch.cuda.Event()
             ready.record(st)
             main.wait_event(ready)
-            self.dec[k].decode_finish(part, out_dense, 1.0 / n, stream=main)  # rank order
+            self.dec[k].decode_finish(part, out_dense, 1.0 / n, stream=main, overwrite=(j == 0))  # rank order
             finished[j] = torch.cuda.Event()
             finished[j].record(main)
 

@@ -50,7 +50,9 @@ class OracleCodec:
     def status(self, stream=None):
         pass  # the oracle raises at the call that fails
 
-    def decode_accumulate(self, container, dense, scale=1.0, length=None, hint=None, stream=None):
+    def decode_accumulate(self, container, dense, scale=1.0, length=None, hint=None, stream=None, overwrite=False):
+        if overwrite:
+            dense.zero_()
         n = int(length.item()) if isinstance(length, torch.Tensor) else (container.numel() if length is None else length)
         _, sup, val = oracle().decode(container[:n].contiguous().numpy().tobytes())
         idx = torch.from_numpy(sup.astype(np.int64))
