@@ -258,6 +258,7 @@ int gp_ctx_create(int device, uint64_t max_d, gp_ctx** out) {
     kernel_attrs_bloom();
     kernel_attrs_p2();
     kernel_attrs_topr();
+    kernel_attrs_dense();
     e = cudaGetLastError();
   }
   if (e != cudaSuccess) {

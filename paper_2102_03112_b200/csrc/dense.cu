@@ -34,6 +34,7 @@ namespace {
 constexpr int kNzBlock = 256;                  // 8 warps
 constexpr int kNzTile = kNzBlock * 32;         // elements per tile: 32 per lane, 1024 per warp
 constexpr uint32_t kGateSkip = 0xFFFFu;        // gate value: the fast path produced the payloads
+constexpr int kNzSmem = 4 * 2 * ((kNzTile + 8) + (kNzBlock + 8));  // nz_encode's double buffers
 
 // Copies n bytes from 4-byte-aligned shared memory to an arbitrary global
 // address: single bytes up to the first 16-byte boundary and after the last,
@@ -65,41 +66,59 @@ __device__ __forceinline__ void block_store_bytes(uint8_t* dst, const uint32_t* 
 }
 
 // Loads n bytes from an arbitrary global address into 4-byte-aligned shared
-// memory (the mirror of block_store_bytes).
+// memory (the mirror of block_store_bytes): 16-byte loads from the enclosing
+// aligned blocks, each output word assembled with one funnel shift (plus one
+// 4-byte load of the following word); no byte-granular shared stores.  Only
+// aligned blocks holding at least one wanted byte are read, so nothing past
+// the source's last page is touched.  `dst` must hold ceil(n/4) + 4 words.
 __device__ __forceinline__ void block_load_bytes(uint32_t* dst, const uint8_t* src, uint64_t n) {
-  uint8_t* db = reinterpret_cast<uint8_t*>(dst);
-  const uint32_t head = static_cast<uint32_t>((16 - (reinterpret_cast<uintptr_t>(src) & 15)) & 15);
-  if (n <= head + 16) {
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) db[i] = src[i];
-    return;
-  }
-  for (uint32_t i = threadIdx.x; i < head; i += blockDim.x) db[i] = src[i];
-  const uint64_t nvec = (n - head) / 16;
-  const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
-  for (uint64_t v = threadIdx.x; v < nvec; v += blockDim.x) {
-    const uint4 x = __ldcs(s4 + v);  // streamed once
-    uint8_t* o = db + head + 16 * v;
-    // byte-granular shared stores of the 16 bytes (o is only 1-aligned in general)
-    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-    if ((head & 3) == 0) {
-      uint32_t* o32 = reinterpret_cast<uint32_t*>(o);
+  if (n == 0) return;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(src) & ~static_cast<uintptr_t>(15);
+  const uint32_t delta = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(src) - a);
+  const uint32_t q = delta >> 2, sh = 8 * (delta & 3);
+  const uintptr_t end = reinterpret_cast<uintptr_t>(src) + n;
+  const uint64_t nwords = (n + 3) / 4;
+  const uint64_t nblk = (end - a + 15) / 16;
+  for (uint64_t v = threadIdx.x; v < nblk; v += blockDim.x) {
+    const uintptr_t at = a + 16 * v;
+    const uint4 x = __ldcs(reinterpret_cast<const uint4*>(at));  // streamed once
+    const uint32_t nx = at + 16 < end ? __ldg(reinterpret_cast<const uint32_t*>(at + 16)) : 0u;
+    const uint32_t w[5] = {x.x, x.y, x.z, x.w, nx};
 #pragma unroll
-      for (int k = 0; k < 4; ++k) o32[k] = w[k];
-    } else {
-#pragma unroll
-      for (int k = 0; k < 16; ++k) o[k] = static_cast<uint8_t>(w[k >> 2] >> (8 * (k & 3)));
+    for (int t = 0; t < 4; ++t) {
+      const int64_t j = static_cast<int64_t>(4 * v + t) - q;
+      if (j >= 0 && static_cast<uint64_t>(j) < nwords) dst[j] = __funnelshift_r(w[t], w[t + 1], sh);
     }
   }
-  for (uint64_t i = head + 16 * nvec + threadIdx.x; i < n; i += blockDim.x) db[i] = src[i];
 }
 
+__device__ __forceinline__ void nz_load(const float* __restrict__ g, uint64_t d, uint64_t base, uint32_t (&x)[32]) {
+  const int lane = threadIdx.x & 31;
+  if (base + 1024 <= d) {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) x[k] = __float_as_uint(__ldcs(g + base + 32 * k + lane));
+  } else {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const uint64_t i = base + 32 * k + lane;
+      x[k] = i < d ? __float_as_uint(__ldcs(g + i)) : 0u;
+    }
+  }
+}
+
+// Software-pipelined over tiles: the loads of the block's next tile are in
+// flight while warp 0 walks the look-back of the current one and while the
+// current tile's payload bytes go out from shared memory (double-buffered), so
+// the look-back's L2 round trips no longer serialise with HBM latency.
 __global__ void __launch_bounds__(kNzBlock) nz_encode(const float* __restrict__ g, uint64_t d, uint64_t r,
                                                       uint8_t* out, Plan* plan, uint64_t* tiles, uint32_t* ticket,
                                                       uint32_t* gate, const uint32_t* status) {
-  __shared__ uint32_t vals[kNzTile + 8];
-  __shared__ uint32_t words[kNzBlock + 8];
-  __shared__ uint64_t sh[36];
-  __shared__ uint32_t slot;
+  extern __shared__ uint32_t nz_smem[];  // vals[2][kNzTile + 8] | words[2][kNzBlock + 8]
+  uint32_t(*vals)[kNzTile + 8] = reinterpret_cast<uint32_t(*)[kNzTile + 8]>(nz_smem);
+  uint32_t(*words)[kNzBlock + 8] = reinterpret_cast<uint32_t(*)[kNzBlock + 8]>(nz_smem + 2 * (kNzTile + 8));
+  __shared__ uint32_t wcnt[2][kNzBlock / 32];
+  __shared__ uint64_t s_prefix[2];
+  __shared__ uint32_t s_tile[2];
   if (failed(status)) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *gate = ld_relaxed_u32(status);  // the general path stays shut
     return;
@@ -110,47 +129,51 @@ __global__ void __launch_bounds__(kNzBlock) nz_encode(const float* __restrict__ 
   const uint64_t bm_bytes = (d + 7) / 8;
   uint8_t* bm_out = out + 49;
   uint8_t* val_out = out + 49 + bm_bytes;
-  while (true) {
-    const uint32_t tile = claim_tile(ticket, &slot);
-    if (tile >= ntiles) break;
-    const uint64_t base = static_cast<uint64_t>(tile) * kNzTile + static_cast<uint64_t>(warp) * 1024;
-    uint32_t x[32];
-    if (base + 1024 <= d) {
-#pragma unroll
-      for (int k = 0; k < 32; ++k) x[k] = __float_as_uint(__ldcs(g + base + 32 * k + lane));
-    } else {
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const uint64_t i = base + 32 * k + lane;
-        x[k] = i < d ? __float_as_uint(__ldcs(g + i)) : 0u;
-      }
-    }
+  if (threadIdx.x == 0) s_tile[0] = atomicAdd(ticket, 1u);
+  __syncthreads();
+  uint32_t tile = s_tile[0];
+  uint32_t x[32];
+  if (tile < ntiles) nz_load(g, d, static_cast<uint64_t>(tile) * kNzTile + static_cast<uint64_t>(warp) * 1024, x);
+  int b = 0;
+  while (tile < ntiles) {
+    if (threadIdx.x == 0) s_tile[b ^ 1] = atomicAdd(ticket, 1u);  // the next tile, read after barrier (1)
     uint32_t cnt = 0, myword = 0;
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
-      const unsigned b = __ballot_sync(kFull, (x[k] & 0x7FFFFFFFu) != 0u);
-      if (lane == k) myword = b;
-      cnt += __popc(b);
+      const unsigned bal = __ballot_sync(kFull, (x[k] & 0x7FFFFFFFu) != 0u);
+      if (lane == k) myword = bal;
+      cnt += __popc(bal);
     }
-    words[threadIdx.x] = myword;  // word warp*32 + lane of the tile
-    uint64_t tile_total;
-    // lane 0 of warp w: tile prefix + values of warps < w (the block scan inside)
-    const uint64_t wo = tile_exclusive_offset<kNzBlock>(lane == 0 ? cnt : 0, tile, tiles, sh, tile_total);
-    const uint64_t tile_prefix = sh[34];  // the tile's global value offset (published by the look-back)
-    uint32_t at = static_cast<uint32_t>(__shfl_sync(kFull, wo, 0) - tile_prefix);
+    words[b][threadIdx.x] = myword;  // word warp*32 + lane of the tile
+    if (lane == 0) wcnt[b][warp] = cnt;
+    __syncthreads();  // (1)
+    uint32_t at = 0, tile_total = 0;
+#pragma unroll
+    for (int w = 0; w < kNzBlock / 32; ++w) {
+      const uint32_t c = wcnt[b][w];
+      at += w < warp ? c : 0u;
+      tile_total += c;
+    }
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
       const bool nz = (x[k] & 0x7FFFFFFFu) != 0u;
-      const unsigned b = __ballot_sync(kFull, nz);
-      if (nz) vals[at + __popc(b & lt)] = x[k];
-      at += __popc(b);
+      const unsigned bal = __ballot_sync(kFull, nz);
+      if (nz) vals[b][at + __popc(bal & lt)] = x[k];
+      at += __popc(bal);
     }
-    __syncthreads();
+    if (warp == 0) {
+      const uint64_t p = lookback_warp(tiles, tile, tile_total);
+      if (lane == 0) s_prefix[b] = p;
+    }
+    const uint32_t next = s_tile[b ^ 1];
+    if (next < ntiles) nz_load(g, d, static_cast<uint64_t>(next) * kNzTile + static_cast<uint64_t>(warp) * 1024, x);
+    __syncthreads();  // (2) vals[b] complete, prefix known
+    const uint64_t tile_prefix = s_prefix[b];
     // bitmap bytes of the tile (the last tile stops at ceil(d/8))
     const uint64_t b0 = static_cast<uint64_t>(tile) * (kNzTile / 8);
     const uint64_t nb = b0 + kNzTile / 8 <= bm_bytes ? kNzTile / 8 : bm_bytes - b0;
-    block_store_bytes(bm_out + b0, words, nb);
-    block_store_bytes(val_out + 4 * tile_prefix, vals, 4 * tile_total);
+    block_store_bytes(bm_out + b0, words[b], nb);
+    block_store_bytes(val_out + 4 * tile_prefix, vals[b], 4ull * tile_total);
     if (tile == ntiles - 1 && threadIdx.x == 0) {
       const uint64_t nnz = tile_prefix + tile_total;
       if (nnz == r) {
@@ -160,7 +183,8 @@ __global__ void __launch_bounds__(kNzBlock) nz_encode(const float* __restrict__ 
         *gate = kGateSkip;
       }
     }
-    __syncthreads();  // vals / words are rewritten by the next tile
+    tile = next;
+    b ^= 1;
   }
 }
 
@@ -259,6 +283,37 @@ __global__ void __launch_bounds__(kNzBlock) bm_scatter(const uint8_t* __restrict
     __syncthreads();
     const uint64_t base = t * kNzTile + static_cast<uint64_t>(warp) * 1024;
     uint32_t at = my_off;
+    if (!f64 && base + 1024 <= d && (reinterpret_cast<uintptr_t>(dense) & 15) == 0) {
+      // 16-byte stores: row u = coordinates [128u, 128u + 128) of the warp's
+      // 1024 = words 4u .. 4u + 3; lane l owns coordinates 4l .. 4l + 3 of the
+      // row = bits 4(l % 8) .. +3 of word 4u + l / 8
+      const uint32_t* ww = words + warp * 32;
+      const int sub = lane >> 3, sh = 4 * (lane & 7);
+#pragma unroll 2
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t w0 = ww[4 * u], w1 = ww[4 * u + 1], w2 = ww[4 * u + 2], w3 = ww[4 * u + 3];
+        const uint32_t wk = sub == 0 ? w0 : sub == 1 ? w1 : sub == 2 ? w2 : w3;
+        const uint32_t before = (sub > 0 ? __popc(w0) : 0) + (sub > 1 ? __popc(w1) : 0) + (sub > 2 ? __popc(w2) : 0);
+        const uint32_t nib = (wk >> sh) & 0xFu;
+        uint32_t j = at + before + __popc(wk & ((1u << sh) - 1u));
+        float4* p = reinterpret_cast<float4*>(dense + base + 128 * u + 4 * lane);
+        float v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = (nib >> q & 1u) ? __uint_as_float(vals[j++]) : 0.0f;
+        if (overwrite) {
+          *p = make_float4((nib & 1u) ? fmaf(scale, v[0], 0.0f) : 0.0f, (nib & 2u) ? fmaf(scale, v[1], 0.0f) : 0.0f,
+                           (nib & 4u) ? fmaf(scale, v[2], 0.0f) : 0.0f, (nib & 8u) ? fmaf(scale, v[3], 0.0f) : 0.0f);
+        } else if (nib) {
+          float4 o = *p;
+          if (nib & 1u) o.x = fmaf(scale, v[0], o.x);
+          if (nib & 2u) o.y = fmaf(scale, v[1], o.y);
+          if (nib & 4u) o.z = fmaf(scale, v[2], o.z);
+          if (nib & 8u) o.w = fmaf(scale, v[3], o.w);
+          *p = o;
+        }
+        at += __popc(w0) + __popc(w1) + __popc(w2) + __popc(w3);
+      }
+    } else {
 #pragma unroll 4
     for (int k = 0; k < 32; ++k) {
       const uint32_t wk = words[warp * 32 + k];
@@ -279,6 +334,7 @@ __global__ void __launch_bounds__(kNzBlock) bm_scatter(const uint8_t* __restrict
         }
       }
       at += __popc(wk);
+    }
     }
     __syncthreads();
   }
@@ -309,6 +365,10 @@ bool nz_fast_path_eligible(uint64_t d, uint64_t r, int index_method, int value_m
   return index_method == GP_INDEX_BITMAP && value_method == GP_VALUE_NONE && 4 * r >= d && d >= kNzTile;
 }
 
+void kernel_attrs_dense() {
+  cudaFuncSetAttribute(nz_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, kNzSmem);
+}
+
 uint32_t* gate_word(gp_ctx* ctx) { return ctx->ws.status + 32; }
 
 void launch_nz_encode(gp_ctx* ctx, const float* g, uint64_t d, uint64_t r, uint8_t* out, cudaStream_t s) {
@@ -316,9 +376,9 @@ void launch_nz_encode(gp_ctx* ctx, const float* g, uint64_t d, uint64_t r, uint8
   const uint64_t ntiles = (d + kNzTile - 1) / kNzTile;
   cudaMemsetAsync(gate_word(ctx), 0, sizeof(uint32_t), s);
   reset_scan(ctx, s, ntiles + 1);
-  const int grid = static_cast<int>(ntiles < static_cast<uint64_t>(ctx->sm_count) * 6 ? ntiles
-                                                                                       : ctx->sm_count * 6);
-  GP_LAUNCH(ctx, nz_encode, grid, kNzBlock, 0, s, g, d, r, out, w.plan, w.tiles, w.ticket, gate_word(ctx), w.status);
+  const uint64_t cap = static_cast<uint64_t>(ctx->sm_count) * 3;  // resident: 3 x 68 KiB of shared memory per SM
+  const int grid = static_cast<int>(ntiles < cap ? ntiles : cap);
+  GP_LAUNCH(ctx, nz_encode, grid, kNzBlock, kNzSmem, s, g, d, r, out, w.plan, w.tiles, w.ticket, gate_word(ctx), w.status);
 }
 
 void launch_gate_merge(gp_ctx* ctx, cudaStream_t s) {

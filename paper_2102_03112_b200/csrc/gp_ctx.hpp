@@ -190,6 +190,7 @@ void reset_scan(gp_ctx* ctx, cudaStream_t s, uint64_t ntiles_bound);  // capi.cu
 void kernel_attrs_bloom();
 void kernel_attrs_p2();
 void kernel_attrs_topr();
+void kernel_attrs_dense();
 
 // topr.cu: ws.support / ws.values <- top-r of grad
 void launch_top_r(gp_ctx* ctx, const float* grad, uint64_t d, uint64_t r, cudaStream_t s, float* residual = nullptr);

@@ -176,10 +176,10 @@ __device__ __forceinline__ uint64_t lookback_warp(uint64_t* tiles, uint32_t tile
     if (inc_mask) break;
     base -= 32;
   }
-  if (lane == 0) {
-    __threadfence();
-    st_volatile(&tiles[tile], kFlagInc | (exclusive + aggregate));
-  }
+  // flag and value travel in one 64-bit word and readers use nothing else the
+  // tile wrote, so no fence (it would wait for this thread's payload stores of
+  // the previous tile to drain)
+  if (lane == 0) st_volatile(&tiles[tile], kFlagInc | (exclusive + aggregate));
   return exclusive;
 }
 

@@ -552,12 +552,16 @@ void launch_top_r(gp_ctx* ctx, const float* grad, uint64_t d, uint64_t r, cudaSt
   // sparsity with r = nnz) take 4096-key chunks: one 512-key segment per warp
   // fits the staging buffers, so no segment is streamed twice.
   const uint64_t chunk = r > d / 16 ? 4096 : std::max<uint64_t>(4096, ((d + nblk - 1) / nblk + 4095) / 4096 * 4096);
-  const int grid = static_cast<int>(std::max<uint64_t>(1, (d + chunk - 1) / chunk));
+  // chunks are claimed through a ticket, so the grid only needs to fill the
+  // machine (5 x 44 KiB blocks per SM); a gated-off launch (dense.cu fast
+  // path) then costs one wave of empty blocks instead of d / 4096
+  const uint64_t nchunks = std::max<uint64_t>(1, (d + chunk - 1) / chunk);
+  const int grid = static_cast<int>(std::min<uint64_t>(nchunks, static_cast<uint64_t>(ctx->sm_count) * 5));
   const bool counted = r > d / 16;
   if (counted) {
     GP_LAUNCH(ctx, topr_count_chunks, ctx->sm_count * 8, kCandBlock, 0, s, grad, d, w.plan, tiles_c, tiles_t,
               w.status);
-    GP_LAUNCH(ctx, scan_chunk_counts<8>, 1, 1024, 0, s, tiles_c, tiles_t, static_cast<uint64_t>(grid), w.status);
+    GP_LAUNCH(ctx, scan_chunk_counts<8>, 1, 1024, 0, s, tiles_c, tiles_t, nchunks, w.status);
   }
   GP_LAUNCH(ctx, topr_candidates, grid, kCandBlock, 0, s, grad, d, chunk, w.plan, w.cand_idx, w.cand_val, w.support,
             w.values, w.u32a, reinterpret_cast<float*>(w.u32b), tiles_c, tiles_t, w.ticket, counted, w.status);
