@@ -207,12 +207,23 @@ void carve(Workspace& w, uint8_t* base, uint64_t D) {
   w.u32d = c.take<uint32_t>(D);
   w.f64a = c.take<double>(D);
   w.f64b = c.take<double>(D);
-  w.partial = c.take<double>((D / 2048 + 128) * 44);
+  w.seg_cap = std::min<uint64_t>(2 * kFitMaxSeg, D) + 2;
+  w.node_cap = static_cast<uint32_t>(std::min<uint64_t>(4 * (kFitMaxSeg + 1), 2 * D) + 64);
+  w.partial = c.take<double>((D / 2048 + w.seg_cap + 2) * 44);
   w.sort_table = c.take<uint32_t>(2 * 256 * (D / kSortTileKeys + 2));  // per-tile digit aggregates + inclusive prefixes
   w.sort_flags = c.take<uint32_t>(64 + D / kSortTileKeys + 2);        // 8 tickets, 1024 histogram bins follow below
   w.sort_hist = c.take<uint32_t>(4 * 256);
   w.seg_dev = c.take<double>(4 * 2048);
   w.seg_arg = c.take<uint32_t>(4 * 2048);
+  w.seg_end = c.take<uint32_t>(w.seg_cap);
+  w.coeffs = c.take<float>(w.seg_cap * kFitMaxCps);
+  w.seg_nodes = c.take<uint8_t>(32ull * w.node_cap);
+  w.seg_heap = c.take<uint32_t>(w.node_cap);
+  w.seg_pend = c.take<uint32_t>(w.node_cap);
+  w.seg_off = c.take<uint64_t>(w.node_cap + 1);
+  w.seg_state = c.take<uint32_t>(8);
+  w.seg_chunk = c.take<uint64_t>(w.seg_cap + 1);
+  w.fit_scratch = c.take<double>(static_cast<uint64_t>(kWideBlocks) * 3 * kFitMaxCps * kFitMaxCps);
   w.crc_cap = 2 * ((64 * D + (1 << 20)) / (64 * 256) + 64);
   w.crc_digits = c.take<uint32_t>(9 * 256);  // 5 byte-digit shift tables + 4 lane-stride multiply tables
   w.crc_acc = c.take<uint32_t>(64);
@@ -280,6 +291,7 @@ int gp_ctx_create(int device, uint64_t max_d, gp_ctx** out) {
   e = cudaMemset(ctx->ws.status, 0, 64 * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMemset(ctx->ws.plan, 0, sizeof(Plan));
   if (e == cudaSuccess) e = cudaMemset(ctx->ws.huff, 0, sizeof(HuffTable));  // empty Huffman table cache
+  if (e == cudaSuccess) e = cudaMemset(ctx->ws.seg_state, 0, 8 * sizeof(uint32_t));  // fit segmentation control words
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess || crc_tables_init(ctx) != GP_OK) {
     cudaFree(base);
@@ -418,7 +430,7 @@ uint64_t gp_max_container_bytes(uint64_t d, uint64_t r, const gp_pipeline_config
     case GP_VALUE_RAW_F64: vl = 8 * n; break;
     case GP_VALUE_FIT_POLY:
     case GP_VALUE_FIT_DEXP: {
-      const uint64_t segs = kMaxSeg;
+      const uint64_t segs = std::min<uint64_t>(kFitMaxSeg, n < 1 ? 1 : n);
       vl = 1 + 2 + 4 * segs + 1 + 4 * segs * (static_cast<uint64_t>(cfg->degree) + 1) + 4;
       uint64_t w = 0;
       for (uint64_t x = d - 1; x; x >>= 1) ++w;
@@ -453,7 +465,6 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
     return set_error(ctx, GP_UNSUPPORTED, "method not implemented on the device path");
   if (vm == GP_VALUE_FIT_POLY || vm == GP_VALUE_FIT_DEXP) {
     if (cfg->degree < 0 || cfg->degree > 60) return set_error(ctx, GP_ERROR, "value_compress: bad degree");
-    if (cfg->degree > 7) return set_error(ctx, GP_UNSUPPORTED, "fit degree > 7 is not on the device path");
   }
   if (vm == GP_VALUE_QUANT) {
     if (cfg->quant_bits < 1 || cfg->quant_bits > 16) return set_error(ctx, GP_ERROR, "quantize: bits out of range [1, 16]");

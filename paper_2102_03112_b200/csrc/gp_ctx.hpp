@@ -38,24 +38,28 @@ struct Plan {
   uint32_t k, pad1;
   uint64_t n_pos;               // |P|
   uint64_t n_pairs, n_sets, n_multi, n_single_sel;
+  uint64_t n_large;             // conflict sets of >= 255 members (ordered by a second pass)
   // ---- rle
   uint64_t n_runs, n_groups;
   // ---- value codec
   uint32_t sign_split, identity;
   uint32_t nseg, degree;
+  uint64_t fit_bounds_at, fit_coeffs_at;  // decode: container offsets of the fit bounds / coefficients
   uint32_t q_bits, q_bucket;    // quantizer header (decode)
   uint32_t fit_kind, dexp_fail; // fit model kind (0 poly, 1 dexp); a dexp part failed (fallback)
   uint32_t slot_id, fused_bitmap;  // byte codec of a value-id-4 slot (0 store, 1 deflate; decode);
                                    // bitmap decode on the fused dense path (dense.cu), else 0
-  uint32_t seg_end[64];         // fit bounds (<= 64 segments on this path)
-  float coeffs[64 * 8];
   // ---- decode
   uint64_t crc_stored;
   uint32_t crc_calc, post_crc_error;
   uint64_t off_index, off_value, off_reorder;
 };
 
-constexpr int kMaxSeg = 64;
+// fit models: up to 0xffff segments (u16 in the payload, curvefit.cpp:287)
+// of up to 61 coefficients (degree <= 60, curvefit.cpp:130)
+constexpr uint64_t kFitMaxSeg = 0xffff;
+constexpr uint64_t kFitMaxCps = 61;
+constexpr uint32_t kWideBlocks = 160;  // fit_solve_wide grid (its per-block scratch)
 constexpr uint64_t kSortTileKeys = 2048;  // radix sort tile (sort.cu kTile): sizes sort_table / sort_flags
 
 struct HuffTable;  // huffman.cuh
@@ -112,6 +116,17 @@ struct Workspace {
   uint32_t* sort_hist = nullptr;  // global digit histograms [4][256]
   double* seg_dev = nullptr;      // segmentation sweep partials [4 * 2048]
   uint32_t* seg_arg = nullptr;    // [4 * 2048]
+  uint32_t* seg_end = nullptr;    // fit segment bounds [seg_cap]
+  float* coeffs = nullptr;        // fit coefficients, segment-major [seg_cap * 61]
+  uint64_t seg_cap = 0;           // segments both sign parts may produce before the 0xffff check
+  uint8_t* seg_nodes = nullptr;   // segmentation tree, 32-byte nodes [node_cap]
+  uint32_t* seg_heap = nullptr;   // [node_cap]
+  uint32_t* seg_pend = nullptr;   // pending nodes / traversal stack [node_cap]
+  uint64_t* seg_off = nullptr;    // interior-length prefix of the pending nodes [node_cap + 1]
+  uint32_t node_cap = 0;
+  uint32_t* seg_state = nullptr;  // SegState control words [8]
+  uint64_t* seg_chunk = nullptr;  // accumulate chunk starts per segment [seg_cap + 1]
+  double* fit_scratch = nullptr;  // fit_solve_wide per-block matrices [kWideBlocks * 3 * 61 * 61]
   uint32_t* crc_digits = nullptr; // CRC shift-operator digit tables [5 * 256] + lane-stride multiply [4 * 256]
   uint32_t* crc_acc = nullptr;    // XOR accumulator + block counter [2]
   bool crc_ready = false;

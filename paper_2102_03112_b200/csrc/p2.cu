@@ -36,7 +36,7 @@ namespace {
 constexpr int kTileBlock = 256;
 constexpr int kTileItems = 16;
 constexpr int kTile = kTileBlock * kTileItems;
-constexpr int kMaxSetSize = 255;  // counting-sort digit; larger sets → GP_CAPACITY
+constexpr uint32_t kBigSet = 255;  // counting-sort digit of every set of >= 255 members (p2_sort_large orders them)
 constexpr uint32_t kSingleton = 0x80000000u;  // slot flag of a size-1 set (bucket offsets < 2^31)
 
 __device__ __forceinline__ bool p2_active(const Plan* plan) {
@@ -44,9 +44,10 @@ __device__ __forceinline__ bool p2_active(const Plan* plan) {
 }
 
 // count[0, m] = 0 with m read on the device (decode only knows it there)
-__global__ void p2_zero_counts(const Plan* plan, uint32_t* count, uint64_t m_cap, const uint32_t* status) {
+__global__ void p2_zero_counts(Plan* plan, uint32_t* count, uint64_t m_cap, const uint32_t* status) {
   if (failed(status) || !p2_active(plan)) return;
   const uint64_t n = (plan->m < m_cap ? plan->m : m_cap) + 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) plan->n_large = 0;
   const uint64_t n4 = n / 4;
   uint4* c4 = reinterpret_cast<uint4*>(count);
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n4;
@@ -166,14 +167,17 @@ __global__ void __launch_bounds__(kTileBlock) p2_tiles(const uint32_t* __restric
       const uint64_t b = tile * kTile + static_cast<uint64_t>(q) * kTileBlock + threadIdx.x;
       c[q] = b < m ? count[b] : 0;
     }
+    uint32_t big = 0;
 #pragma unroll
     for (int q = 0; q < kTileItems; ++q) {
-      if (c[q] >= kMaxSetSize) latch(status, GP_CAPACITY);
 #pragma unroll
       for (int z = 0; z < 4; ++z) small[z] += c[q] == static_cast<uint32_t>(z + 1) ? 1u : 0u;
-      if (c[q] > 4) atomicAdd(&h[c[q] < 255 ? c[q] : 255], 1u);
+      if (c[q] > 4) atomicAdd(&h[c[q] < kBigSet ? c[q] : kBigSet], 1u);
+      big += c[q] >= kBigSet ? 1u : 0u;
       need += c[q];
     }
+    big = __reduce_add_sync(kFull, big);
+    if ((threadIdx.x & 31) == 0 && big) atomicAdd(reinterpret_cast<unsigned long long*>(&plan->n_large), big);
 #pragma unroll
     for (int z = 0; z < 4; ++z) {
       const uint32_t v = __reduce_add_sync(kFull, small[z]);
@@ -227,13 +231,12 @@ __global__ void p2_scatter(const uint32_t* __restrict__ pairs, const Plan* plan,
   }
 }
 
-// n_sets = total over the digit table (last digit's exclusive prefix + its count
-// is not stored, so count it from the sizes' last tile instead: the table is
-// exclusive, total = table[255][last] + h[255][last]; size 255 never occurs).
+// n_sets = total over the digit table: the exclusive prefix at the first cell
+// of digit 255 counts every set below 255 members, p2_tiles counted the rest.
 __global__ void p2_count_sets(Plan* plan, const uint32_t* __restrict__ table, const uint32_t* status) {
   if (failed(status) || !p2_active(plan) || threadIdx.x != 0) return;
   const uint64_t ntiles = (plan->m + kTile - 1) / kTile;
-  plan->n_sets = table[255 * ntiles + ntiles - 1];  // digit 255 is empty: its prefix is the grand total
+  plan->n_sets = table[kBigSet * ntiles] + plan->n_large;
   const uint64_t n1 = table[2 * ntiles] - table[1 * ntiles];  // sets of size 1
   plan->n_multi = plan->n_sets - n1;
   plan->n_cand = n1;  // first multi set in the (size, bit) order
@@ -263,7 +266,7 @@ __global__ void __launch_bounds__(kTileBlock) p2_size_scatter(const Plan* plan, 
 #pragma unroll
     for (int j = 0; j < kTileItems; ++j) {
       const uint64_t b = seg + 32 * j + lane;
-      sz[j] = b < m ? size[b] : 0u;
+      sz[j] = b < m ? min(size[b], kBigSet) : 0u;  // the digit
     }
 #pragma unroll
     for (int j = 0; j < kTileItems; ++j) {
@@ -291,6 +294,44 @@ __global__ void __launch_bounds__(kTileBlock) p2_size_scatter(const Plan* plan, 
       if (sz[j]) sets[wcnt[warp][sz[j]] + rank[j]] = static_cast<uint32_t>(seg + 32 * j + lane);
     __syncthreads();
   }
+}
+
+// Sets of >= 255 members share digit 255 and leave p2_size_scatter in bit
+// order; this orders them by (size, bit) as conflict_sets' stable sort does
+// (bloom.cpp:166-172).  Nothing to do in practice (it takes 255 positives
+// probing one bit); when there is, one block merge-sorts the composite keys
+// size << 32 | bit (all distinct) with a binary-search merge per pass.
+__global__ void __launch_bounds__(1024) p2_sort_large(const Plan* plan, const uint32_t* __restrict__ size,
+                                                      uint32_t* sets, uint64_t* ka, uint64_t* kb,
+                                                      const uint32_t* status) {
+  if (failed(status) || !p2_active(plan)) return;
+  const uint64_t n = plan->n_large;
+  if (n < 2) return;
+  uint32_t* big = sets + (plan->n_sets - n);
+  for (uint64_t i = threadIdx.x; i < n; i += blockDim.x)
+    ka[i] = static_cast<uint64_t>(size[big[i]]) << 32 | big[i];
+  __syncthreads();
+  uint64_t* src = ka;
+  uint64_t* dst = kb;
+  for (uint64_t w = 1; w < n; w *= 2) {  // merge runs [a, a+w) and [a+w, a+2w)
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint64_t a = i / (2 * w) * (2 * w), mid = min(a + w, n), e = min(a + 2 * w, n);
+      const uint64_t x = src[i];
+      const bool left = i < mid;
+      uint64_t lo = left ? mid : a, hi = left ? e : mid;  // count the other run's keys below x
+      const uint64_t base = lo;
+      while (lo < hi) {
+        const uint64_t md = (lo + hi) / 2;
+        if (src[md] < x) lo = md + 1; else hi = md;
+      }
+      dst[a + (left ? i - a : i - mid) + (lo - base)] = x;
+    }
+    __syncthreads();
+    uint64_t* t = src;
+    src = dst;
+    dst = t;
+  }
+  for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) big[i] = static_cast<uint32_t>(src[i]);
 }
 
 // stage A as a bitset over P (ballot of the byte flags, one word per warp
@@ -606,6 +647,8 @@ void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t 
   launch_table_scan(ctx, w.p2_table, &w.plan->m, m_cap, 12, s);
   GP_LAUNCH(ctx, p2_count_sets, 1, 32, 0, s, w.plan, w.p2_table, w.status);
   GP_LAUNCH(ctx, p2_size_scatter, tgrid, kTileBlock, 0, s, w.plan, w.p2_count, w.p2_table, w.p2_sets, w.status);
+  GP_LAUNCH(ctx, p2_sort_large, 1, 1024, 0, s, w.plan, w.p2_count, w.p2_sets, reinterpret_cast<uint64_t*>(w.f64a),
+            reinterpret_cast<uint64_t*>(w.f64b), w.status);
   GP_LAUNCH(ctx, p2_stage_a, grid_for(ctx, n_bound, 256), 256, 0, s, w.plan, w.flags, w.selbits, w.status);
   stage_end(ctx, s);
   stage_begin(ctx, decoding ? ST_DEC_P2_ENGINE : ST_P2_ENGINE, s);

@@ -10,8 +10,8 @@
 //   fit_segment  : greedy max-chord-deviation splitting per sign part, fp64
 //                  with no contraction and lowest-index ties (curvefit.cpp:50-99)
 //                  — bit-exact boundaries
-//   fit_accumulate / fit_solve : least squares of degree <= 7 per segment on
-//                  t in [-1, 1].  The reference solves the Vandermonde system
+//   fit_accumulate / fit_solve : least squares per segment on t in [-1, 1]
+//                  (degree <= 7 in registers; degree 8..60: fit_solve_wide).  The reference solves the Vandermonde system
 //                  with Eigen's column-pivoted QR (curvefit.cpp:154); here the
 //                  normal equations are formed in the Legendre basis (Gram
 //                  matrix ~ diagonal, condition ~ 2*degree+1) with fixed-order
@@ -34,10 +34,16 @@ namespace gp {
 
 namespace {
 
-constexpr int kMaxDeg = 7;
-constexpr int kCps = kMaxDeg + 1;           // coefficient stride in Plan::coeffs
+constexpr int kMaxDeg = 7;                  // register path (fit_accumulate / fit_solve)
+constexpr int kCps = kMaxDeg + 1;
+constexpr int kWideDeg = 60;                // fit_poly's range (curvefit.cpp:130)
+constexpr int kWideCps = kWideDeg + 1;
 constexpr int kChunk = 2048;                // points per accumulate block
 constexpr int kAcc = 36 + 8;                // Gram upper triangle (<= 36) + rhs (<= 8)
+
+// coefficients of segment s live at coeffs[s * cps + j], cps = the serialized
+// coeffs_per_segment (FORMAT.md: degree + 1 for poly, 4 for dexp)
+__device__ __forceinline__ uint32_t cps_of(const Plan* plan) { return plan->fit_kind ? 4u : plan->degree + 1u; }
 
 __device__ __forceinline__ bool fit_active(const Plan* plan) {
   return plan->value_method == GP_VALUE_FIT_POLY || plan->value_method == GP_VALUE_FIT_DEXP;
@@ -94,26 +100,84 @@ __global__ void fit_prepare(const float* __restrict__ values, const uint32_t* __
 }
 
 // ---------------------------------------------------------------- segmentation
-struct Piece {
-  uint32_t begin, end, arg, live;
+// segment() (curvefit.cpp:69-99) is a best-first expansion: repeatedly split
+// the live piece of largest deviation (ties: lowest begin) until the budget is
+// reached.  The device keeps the expansion tree in global memory and runs it
+// in ROUNDS inside one cooperative kernel:
+//   1. evaluate the pending nodes (make_piece: max squared chord deviation,
+//      lowest index on ties) — a grid sweep over the disjoint ranges;
+//   2. one thread replays the reference's selection loop on a binary heap
+//      keyed (dev desc, begin asc), popping while the top's children are
+//      known (the budget's last split needs none);
+//   3. when it stalls, the children of EVERY heap node not yet expanded
+//      become the next round's pending nodes (only heap nodes can ever be
+//      popped, and their ranges are disjoint, so a round sweeps <= n points).
+// A round costs one sweep however many pieces it evaluates, so budgets up to
+// 0xffff (part_budget, curvefit.cpp:424-428) take about log2(budget) rounds on
+// balanced data instead of one sweep per split.  Segments are the unsplit
+// nodes in tree (= begin) order.
+struct SegNode {
+  uint32_t begin, end;  // part-relative range
+  uint32_t arg, live;
   double dev;
+  uint32_t left, split;  // first child id (right = left + 1) or kNoChild; popped by the replay
+};
+constexpr uint32_t kNoChild = 0xFFFFFFFFu;
+constexpr int kFewRanges = 8;  // rounds with <= 8 pending nodes reduce partials instead of atomics
+
+// control words shared by the blocks of fit_segment_coop (global memory)
+struct SegState {
+  uint32_t npend, nnodes, heapn, pops, done, overflow, pad0, pad1;
 };
 
-// Grid-cooperative segmentation: every make_piece (curvefit.cpp:50-67) is one
-// sweep in which all blocks scan a slice of the piece, write their block-best
-// (dev, arg) to a double-buffered partial array, grid.sync(), and every block
-// reduces the partials in block order (same result everywhere, same tie rule:
-// max dev, lowest index).  The piece list is replicated per block; children
-// of a split are only evaluated when another split can follow.
-struct SweepRange {
-  uint32_t begin, end;
-};
+__device__ __forceinline__ bool seg_before(const SegNode& a, const SegNode& b) {  // a pops before b
+  return a.dev > b.dev || (a.dev == b.dev && a.begin < b.begin);
+}
 
-__device__ void seg_sweep(const double* __restrict__ t, const SweepRange* rr, int nr, uint32_t mp, double* pdev,
-                          uint32_t* parg, Piece* out, double* sdev, uint32_t* sarg, cg::grid_group& grid) {
+__device__ void heap_push(uint32_t* heap, uint32_t& n, const SegNode* nodes, uint32_t id) {
+  uint32_t i = n++;
+  while (i > 0) {
+    const uint32_t p = (i - 1) / 2;
+    if (!seg_before(nodes[id], nodes[heap[p]])) break;
+    heap[i] = heap[p];
+    i = p;
+  }
+  heap[i] = id;
+}
+
+__device__ uint32_t heap_pop(uint32_t* heap, uint32_t& n, const SegNode* nodes) {
+  const uint32_t top = heap[0];
+  const uint32_t last = heap[--n];
+  uint32_t i = 0;
+  while (true) {
+    const uint32_t l = 2 * i + 1;
+    if (l >= n) break;
+    const uint32_t c = (l + 1 < n && seg_before(nodes[heap[l + 1]], nodes[heap[l]])) ? l + 1 : l;
+    if (!seg_before(nodes[heap[c]], nodes[last])) break;
+    heap[i] = heap[c];
+    i = c;
+  }
+  if (n) heap[i] = last;
+  return top;
+}
+
+__device__ __forceinline__ void make_live(SegNode& p, uint32_t mp) {
+  if (!(p.dev > 0.0)) p.arg = 0;
+  p.live = (p.dev > 0.0 && p.arg - p.begin >= mp && p.end - p.arg >= mp) ? 1u : 0u;
+}
+
+// Few pending ranges: every block scans a slice of each, writes its block-best
+// (dev, arg) to a double-buffered partial array; after grid.sync() block 0
+// reduces the partials in block order (same tie rule) into the nodes.
+// Every block reduces (replicated, identical results in sres); block 0 also
+// stores them in the nodes.  rb/re give the ranges when nodes is null.
+__device__ void seg_sweep_few(const double* __restrict__ t, SegNode* nodes, const uint32_t* pend, int nr,
+                              const uint32_t* rb, const uint32_t* re, double* pdev, uint32_t* parg, double* sdev,
+                              uint32_t* sarg, double* sres_dev, uint32_t* sres_arg, cg::grid_group& grid) {
   const uint32_t G = gridDim.x;
   for (int q = 0; q < nr; ++q) {
-    const uint32_t b = rr[q].begin, e = rr[q].end, len = e - b;
+    const uint32_t b = nodes ? nodes[pend[q]].begin : rb[q], e = nodes ? nodes[pend[q]].end : re[q];
+    const uint32_t len = e - b;
     double best = 0.0;
     uint32_t arg = 0;
     if (len >= 3) {
@@ -156,7 +220,6 @@ __device__ void seg_sweep(const double* __restrict__ t, const SweepRange* rr, in
     __syncthreads();
   }
   grid.sync();
-  // every block reduces the G partials of each range, all threads in parallel
   for (int q = 0; q < nr; ++q) {
     double best = 0.0;
     uint32_t arg = 0;
@@ -189,23 +252,88 @@ __device__ void seg_sweep(const double* __restrict__ t, const SweepRange* rr, in
           bb = sdev[w];
           aa = sarg[w];
         }
-      Piece p{rr[q].begin, rr[q].end, aa, 0u, bb};
-      p.live = (bb > 0.0 && aa - p.begin >= mp && p.end - aa >= mp) ? 1u : 0u;
-      out[q] = p;
+      sres_dev[q] = bb;
+      sres_arg[q] = aa;
+      if (nodes && blockIdx.x == 0) {
+        nodes[pend[q]].dev = bb;
+        nodes[pend[q]].arg = aa;
+      }
     }
     __syncthreads();
   }
 }
 
+// Many pending ranges: the interior points of all of them, concatenated
+// (off = exclusive prefix of interior lengths), 32 consecutive points per
+// thread; the maximum by atomicMax on the non-negative doubles' bit patterns,
+// then the lowest index attaining it by atomicMin (two sweeps, exact ties).
+constexpr uint32_t kSweepRun = 32;
+__device__ __forceinline__ uint32_t find_pend(const uint64_t* off, uint32_t npend, uint64_t j) {
+  uint32_t lo = 0, hi = npend;  // last q with off[q] <= j
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) / 2;
+    if (off[mid] <= j) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+template <bool kArg>
+__device__ void seg_sweep_many_pass(const double* __restrict__ t, SegNode* nodes, const uint32_t* pend,
+                                    const uint64_t* off, uint32_t npend) {
+  const uint64_t total = off[npend];
+  const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t j0 = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) * kSweepRun; j0 < total;
+       j0 += nthreads * kSweepRun) {
+    const uint64_t j1 = j0 + kSweepRun < total ? j0 + kSweepRun : total;
+    uint32_t q = find_pend(off, npend, j0);
+    uint64_t qend = off[q + 1];
+    while (true) {
+      SegNode* nd = &nodes[pend[q]];
+      const uint32_t b = nd->begin, e = nd->end;
+      const double y0 = t[b];
+      const double slope = __ddiv_rn(__dsub_rn(t[e - 1], y0), static_cast<double>(e - b - 1));
+      const double target = kArg ? __longlong_as_double(static_cast<long long>(
+                                       *reinterpret_cast<volatile unsigned long long*>(&nd->dev)))
+                                 : 0.0;
+      const uint64_t stop = qend < j1 ? qend : j1;
+      double best = 0.0;
+      for (uint64_t j = j0; j < stop; ++j) {
+        const uint32_t i = b + 1 + static_cast<uint32_t>(j - off[q]);
+        const double pred = __dadd_rn(y0, __dmul_rn(slope, static_cast<double>(i - b)));
+        const double d = __dsub_rn(t[i], pred);
+        const double d2 = __dmul_rn(d, d);
+        if (kArg) {
+          if (d2 == target && target > 0.0) {
+            atomicMin(&nd->arg, i);
+            break;  // the run's lowest index
+          }
+        } else if (d2 > best) {
+          best = d2;
+        }
+      }
+      if (!kArg && best > 0.0)
+        atomicMax(reinterpret_cast<unsigned long long*>(&nd->dev),
+                  static_cast<unsigned long long>(__double_as_longlong(best)));
+      if (stop >= j1) break;
+      j0 = stop;
+      ++q;
+      qend = off[q + 1];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) fit_segment_coop(Plan* plan, const double* __restrict__ t, int degree,
                                                         int max_segments, double* pdev, uint32_t* parg,
+                                                        SegNode* nodes, uint32_t* heap, uint32_t* pend,
+                                                        uint64_t* off, SegState* st, uint32_t* seg_end,
+                                                        uint64_t* chunk, uint32_t node_cap, uint32_t seg_cap,
                                                         uint32_t* status) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double sdev[32];
   __shared__ uint32_t sarg[32];
-  __shared__ Piece pieces[kMaxSeg];
-  __shared__ Piece res[2];
-  __shared__ int s_best;
+  __shared__ double sres_dev[kFewRanges];
+  __shared__ uint32_t sres_arg[kFewRanges];
+  __shared__ uint64_t sh[40];
   // uniform exit decisions only (every block must reach every grid.sync)
   if (failed(status) || !poly_active(plan)) return;
   const uint64_t n = plan->n_values;
@@ -223,17 +351,21 @@ __global__ void __launch_bounds__(256) fit_segment_coop(Plan* plan, const double
   }
   const uint32_t mp = static_cast<uint32_t>(degree + 1 > 1 ? degree + 1 : 1);
   const uint32_t G = gridDim.x;
+  const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
   int sweep = 0;
-  uint32_t nseg = 0;
+  uint32_t nseg = 0;  // replicated in every block
   bool overflow = false;
-  for (int pi = 0; pi < nparts && !overflow; ++pi) {
+  for (int pi = 0; pi < nparts; ++pi) {
     const uint32_t b = pb[pi], e = pe[pi], len = e - b;
-    int budget;
+    long long budget;
     if (max_segments > 0) {  // curvefit.cpp:473-481
       const long long share = static_cast<long long>(max_segments) * static_cast<long long>(len) /
                               static_cast<long long>(n);
-      budget = share > 1 ? static_cast<int>(share) : 1;
-      if (pi + 1 == nparts) budget = max_segments - static_cast<int>(nseg) > 1 ? max_segments - static_cast<int>(nseg) : 1;
+      budget = share > 1 ? share : 1;
+      if (pi + 1 == nparts) {
+        const long long used = static_cast<long long>(nseg);  // segments of part 0
+        budget = max_segments - used > 1 ? max_segments - used : 1;
+      }
     } else if (len < 4) {
       budget = 1;
     } else {  // part_budget (curvefit.cpp:101-110, :424-428)
@@ -242,301 +374,564 @@ __global__ void __launch_bounds__(256) fit_segment_coop(Plan* plan, const double
       const int kc = static_cast<int>(p) > 1 ? static_cast<int>(p) : 1;
       budget = kc + 1 < 0xffff ? kc + 1 : 0xffff;
     }
-    int np = 1;
-    if (budget > 1) {
-      SweepRange r0{0, len};
-      seg_sweep(t + b, &r0, 1, mp, pdev + (sweep & 1) * 2 * G, parg + (sweep & 1) * 2 * G, res, sdev, sarg, grid);
-      ++sweep;
-      if (threadIdx.x == 0) pieces[0] = res[0];
-    } else if (threadIdx.x == 0) {
-      pieces[0] = Piece{0, len, 0, 0u, 0.0};
-    }
-    __syncthreads();
-    while (np < budget) {
-      if (threadIdx.x == 0) {
-        int best = -1;
-        for (int i = 0; i < np; ++i) {
-          if (!pieces[i].live) continue;
-          if (best < 0 || pieces[i].dev > pieces[best].dev ||
-              (pieces[i].dev == pieces[best].dev && pieces[i].begin < pieces[best].begin))
-            best = i;
-        }
-        s_best = best;
+    if (budget <= 2) {  // at most one split: the root's, decided in every block (no tree, no replay)
+      uint32_t split = 0;
+      if (budget == 2) {
+        const uint32_t rb = 0, re = len;
+        seg_sweep_few(t + b, nullptr, nullptr, 1, &rb, &re, pdev + (sweep & 1) * kFewRanges * G,
+                      parg + (sweep & 1) * kFewRanges * G, sdev, sarg, sres_dev, sres_arg, grid);
+        ++sweep;
+        SegNode root{0, len, sres_arg[0], 0u, sres_dev[0], kNoChild, 0u};
+        make_live(root, mp);
+        if (root.live) split = root.arg;
       }
-      __syncthreads();
-      const int best = s_best;
-      if (best < 0) break;
-      if (nseg + np + 1 > static_cast<uint32_t>(kMaxSeg)) {
+      if (nseg + 2 > seg_cap) {
         overflow = true;
         break;
       }
-      const Piece pp = pieces[best];
-      Piece left{pp.begin, pp.arg, 0, 0u, 0.0}, right{pp.arg, pp.end, 0, 0u, 0.0};
-      if (np + 1 < budget) {  // another split may follow: evaluate both children
-        SweepRange rr[2] = {{pp.begin, pp.arg}, {pp.arg, pp.end}};
-        seg_sweep(t + b, rr, 2, mp, pdev + (sweep & 1) * 2 * G, parg + (sweep & 1) * 2 * G, res, sdev, sarg, grid);
+      if (leader) {
+        if (split) seg_end[nseg] = b + split;
+        seg_end[nseg + (split ? 1 : 0)] = e;
+      }
+      nseg += split ? 2 : 1;
+      continue;
+    }
+    if (leader) {
+      nodes[0] = SegNode{0, len, kNoChild, 0u, 0.0, kNoChild, 0u};
+      pend[0] = 0;
+      off[0] = 0;
+      off[1] = len >= 3 ? len - 2 : 0;
+      st->npend = 1u;
+      st->nnodes = 1;
+      st->heapn = 0;
+      st->pops = 0;
+      st->done = 0u;
+      st->pad0 = nseg;
+    }
+    grid.sync();
+    while (!ld_relaxed_u32(&st->done)) {
+      const uint32_t npend = ld_relaxed_u32(&st->npend);
+      if (npend <= kFewRanges) {
+        seg_sweep_few(t + b, nodes, pend, static_cast<int>(npend), nullptr, nullptr,
+                      pdev + (sweep & 1) * kFewRanges * G, parg + (sweep & 1) * kFewRanges * G, sdev, sarg,
+                      sres_dev, sres_arg, grid);
         ++sweep;
-        left = res[0];
-        right = res[1];
+      } else {
+        seg_sweep_many_pass<false>(t + b, nodes, pend, off, npend);
+        grid.sync();
+        seg_sweep_many_pass<true>(t + b, nodes, pend, off, npend);
+        grid.sync();
       }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        pieces[best] = left;
-        pieces[np] = right;
-      }
-      ++np;
-      __syncthreads();
-    }
-    if (overflow) break;
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-      for (int i = 1; i < np; ++i) {  // sort by begin
-        const Piece v = pieces[i];
-        int j = i;
-        while (j > 0 && pieces[j - 1].begin > v.begin) {
-          pieces[j] = pieces[j - 1];
-          --j;
+      if (leader) {  // the reference's selection loop, resumed
+        for (uint32_t q = 0; q < npend; ++q) make_live(nodes[pend[q]], mp);
+        uint32_t heapn = st->heapn, pops = st->pops, nnodes = st->nnodes;
+        if (pops == 0 && heapn == 0 && nodes[0].live && nodes[0].split == 0) heap_push(heap, heapn, nodes, 0);
+        bool stall = false;
+        while (pops + 1 < budget && heapn > 0) {
+          const uint32_t top = heap[0];
+          const bool last = pops + 2 >= budget;  // this pop reaches the budget
+          if (nodes[top].left == kNoChild && !last) {
+            stall = true;
+            break;
+          }
+          heap_pop(heap, heapn, nodes);
+          ++pops;
+          nodes[top].split = 1;
+          if (nodes[top].left == kNoChild) {  // the budget's last split: ranges only
+            if (nnodes + 2 > node_cap) {
+              overflow = true;
+              break;
+            }
+            nodes[nnodes] = SegNode{nodes[top].begin, nodes[top].arg, kNoChild, 0u, 0.0, kNoChild, 0u};
+            nodes[nnodes + 1] = SegNode{nodes[top].arg, nodes[top].end, kNoChild, 0u, 0.0, kNoChild, 0u};
+            nodes[top].left = nnodes;
+            nnodes += 2;
+          } else {
+            const uint32_t c = nodes[top].left;
+            if (nodes[c].live) heap_push(heap, heapn, nodes, c);
+            if (nodes[c + 1].live) heap_push(heap, heapn, nodes, c + 1);
+          }
         }
-        pieces[j] = v;
+        uint32_t np = 0;
+        if (stall && !overflow) {  // expand every heap node with unknown children
+          uint64_t acc = 0;
+          for (uint32_t h = 0; h < heapn; ++h) {
+            const uint32_t id = heap[h];
+            if (nodes[id].left != kNoChild) continue;
+            if (nnodes + 2 > node_cap) {
+              overflow = true;
+              break;
+            }
+            const SegNode pn = nodes[id];
+            nodes[nnodes] = SegNode{pn.begin, pn.arg, kNoChild, 0u, 0.0, kNoChild, 0u};
+            nodes[nnodes + 1] = SegNode{pn.arg, pn.end, kNoChild, 0u, 0.0, kNoChild, 0u};
+            nodes[id].left = nnodes;
+            for (int c = 0; c < 2; ++c) {
+              const uint32_t cl = nodes[nnodes + c].end - nodes[nnodes + c].begin;
+              pend[np] = nnodes + c;
+              off[np] = acc;
+              acc += cl >= 3 ? cl - 2 : 0;
+              ++np;
+            }
+            nnodes += 2;
+          }
+          off[np] = acc;
+        }
+        st->heapn = heapn;
+        st->pops = pops;
+        st->nnodes = nnodes;
+        st->npend = np;
+        st->done = (!stall || overflow) ? 1u : 0u;
+        if (overflow) st->overflow = 1;
       }
-      for (int i = 0; i < np; ++i) plan->seg_end[nseg + i] = b + pieces[i].end;
+      grid.sync();
     }
-    nseg += static_cast<uint32_t>(np);
-    __syncthreads();
+    if (leader && !st->overflow) {  // unsplit nodes in tree order = segments by begin
+      uint32_t sp = 0;
+      nseg = st->pad0;
+      pend[sp++] = 0;
+      while (sp) {
+        const uint32_t id = pend[--sp];
+        if (nodes[id].split) {
+          pend[sp++] = nodes[id].left + 1;
+          pend[sp++] = nodes[id].left;
+        } else {
+          if (nseg >= seg_cap) {
+            st->overflow = 1;
+            break;
+          }
+          seg_end[nseg++] = b + nodes[id].end;
+        }
+      }
+      st->pad0 = nseg;  // every block's segment count
+    }
+    if (leader && st->overflow) st->pad0 = nseg;
+    grid.sync();
+    nseg = ld_relaxed_u32(&st->pad0);
+    if (ld_relaxed_u32(&st->overflow)) {
+      overflow = true;
+      break;
+    }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    if (overflow) latch(status, GP_CAPACITY);
+  if (blockIdx.x != 0) return;
+  if (threadIdx.x == 0) {
+    // more pieces than the node / segment arrays hold means more than 0xffff
+    // segments: serialize_fit's "too many segments" (curvefit.cpp:287)
+    if (overflow || st->overflow) latch(status, GP_ERROR);
     plan->nseg = nseg;
     plan->degree = static_cast<uint32_t>(degree);
+    st->overflow = 0;
+    st->pad0 = 0;
   }
+  if (overflow) return;
+  // fit_accumulate's chunk starts: chunk[s] = sum over earlier segments of ceil(len / kChunk)
+  uint64_t carry = 0;
+  for (uint32_t base = 0; base < nseg; base += blockDim.x) {
+    const uint32_t q = base + threadIdx.x;
+    uint64_t c = 0;
+    if (q < nseg) {
+      const uint32_t sb = q == 0 ? 0 : seg_end[q - 1];
+      c = (seg_end[q] - sb + kChunk - 1) / kChunk;
+    }
+    uint64_t tot;
+    const uint64_t ex = block_exclusive_sum<uint64_t, 256>(c, sh, tot);
+    if (q < nseg) chunk[q] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) chunk[nseg] = carry;
 }
 
 // ---------------------------------------------------------------- least squares
-__device__ __forceinline__ void seg_range(const Plan* plan, uint32_t s, uint32_t& b, uint32_t& e) {
-  b = s == 0 ? 0 : plan->seg_end[s - 1];
-  e = plan->seg_end[s];
+__device__ __forceinline__ void seg_range(const uint32_t* seg_end, uint32_t s, uint32_t& b, uint32_t& e) {
+  b = s == 0 ? 0 : seg_end[s - 1];
+  e = seg_end[s];
 }
 
-// chunk c of the concatenated per-segment chunk lists → (segment, start)
-__device__ bool locate_chunk(const Plan* plan, uint64_t c, uint32_t& seg, uint32_t& start, uint32_t& stop) {
-  uint64_t acc = 0;
-  for (uint32_t s = 0; s < plan->nseg; ++s) {
-    uint32_t b, e;
-    seg_range(plan, s, b, e);
-    const uint64_t nc = (e - b + kChunk - 1) / kChunk;
-    if (c < acc + nc) {
-      seg = s;
-      start = b + static_cast<uint32_t>((c - acc) * kChunk);
-      stop = start + kChunk < e ? start + kChunk : e;
-      return true;
-    }
-    acc += nc;
+__device__ __forceinline__ uint32_t chunk_segment(const uint64_t* chunk, uint32_t S, uint64_t c) {
+  uint32_t lo = 0, hi = S;  // last s with chunk[s] <= c
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) / 2;
+    if (chunk[mid] <= c) lo = mid; else hi = mid;
   }
-  return false;
+  return lo;
 }
 
+// degree <= 7: Legendre Gram upper triangle + rhs per 2048-point chunk, fixed-order sums
 __global__ void __launch_bounds__(256) fit_accumulate(const Plan* plan, const double* __restrict__ t,
+                                                      const uint32_t* __restrict__ seg_end,
+                                                      const uint64_t* __restrict__ chunk,
                                                       double* __restrict__ partial, const uint32_t* status) {
   __shared__ double red[8][kAcc];
-  if (failed(status) || !poly_active(plan)) return;
-  uint32_t seg, start, stop;
-  if (!locate_chunk(plan, blockIdx.x, seg, start, stop)) return;
-  uint32_t b, e;
-  seg_range(plan, seg, b, e);
-  const uint32_t len = e - b;
-  const int deg = static_cast<int>(plan->degree);
-  const int eff = deg < static_cast<int>(len) - 1 ? deg : static_cast<int>(len) - 1;
-  double acc[kAcc];
+  if (failed(status) || !poly_active(plan) || plan->degree > kMaxDeg) return;
+  const uint32_t S = plan->nseg;
+  const uint64_t nchunks = chunk[S];
+  for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const uint32_t seg = chunk_segment(chunk, S, c);
+    uint32_t b, e;
+    seg_range(seg_end, seg, b, e);
+    const uint32_t start = b + static_cast<uint32_t>((c - chunk[seg]) * kChunk);
+    const uint32_t stop = start + kChunk < e ? start + kChunk : e;
+    const uint32_t len = e - b;
+    const int deg = static_cast<int>(plan->degree);
+    const int eff = deg < static_cast<int>(len) - 1 ? deg : static_cast<int>(len) - 1;
+    double acc[kAcc];
 #pragma unroll
-  for (int j = 0; j < kAcc; ++j) acc[j] = 0.0;
-  if (len > 1) {
-    const double alpha = 2.0 / static_cast<double>(len - 1);
-    const double beta = -static_cast<double>(len + 1) / static_cast<double>(len - 1);
-    for (uint32_t i = start + threadIdx.x; i < stop; i += 256) {
-      const double x = alpha * static_cast<double>(i - b + 1) + beta;  // t in [-1, 1]
-      const double y = t[i];
-      double P[kCps];
-      P[0] = 1.0;
-      P[1] = x;
+    for (int j = 0; j < kAcc; ++j) acc[j] = 0.0;
+    if (len > 1) {
+      const double alpha = 2.0 / static_cast<double>(len - 1);
+      const double beta = -static_cast<double>(len + 1) / static_cast<double>(len - 1);
+      for (uint32_t i = start + threadIdx.x; i < stop; i += 256) {
+        const double x = alpha * static_cast<double>(i - b + 1) + beta;  // t in [-1, 1]
+        const double y = t[i];
+        double P[kCps];
+        P[0] = 1.0;
+        P[1] = x;
 #pragma unroll
-      for (int j = 1; j < kMaxDeg; ++j) P[j + 1] = ((2 * j + 1) * x * P[j] - j * P[j - 1]) / (j + 1);
-      int a = 0;
+        for (int j = 1; j < kMaxDeg; ++j) P[j + 1] = ((2 * j + 1) * x * P[j] - j * P[j - 1]) / (j + 1);
+        int a = 0;
 #pragma unroll
-      for (int j = 0; j <= kMaxDeg; ++j)
+        for (int j = 0; j <= kMaxDeg; ++j)
 #pragma unroll
-        for (int q = j; q <= kMaxDeg; ++q, ++a)
-          if (q <= eff) acc[a] += P[j] * P[q];
+          for (int q = j; q <= kMaxDeg; ++q, ++a)
+            if (q <= eff) acc[a] += P[j] * P[q];
 #pragma unroll
-      for (int j = 0; j <= kMaxDeg; ++j)
-        if (j <= eff) acc[36 + j] += P[j] * y;
+        for (int j = 0; j <= kMaxDeg; ++j)
+          if (j <= eff) acc[36 + j] += P[j] * y;
+      }
     }
-  }
-  // fixed-order reduction: warp tree, then warps in index order
+    // fixed-order reduction: warp tree, then warps in index order
 #pragma unroll
-  for (int j = 0; j < kAcc; ++j) {
-    double v = acc[j];
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][j] = v;
-  }
-  __syncthreads();
-  if (threadIdx.x < kAcc) {
-    double v = 0.0;
-    for (int w = 0; w < 8; ++w) v += red[w][threadIdx.x];
-    partial[static_cast<uint64_t>(blockIdx.x) * kAcc + threadIdx.x] = v;
-  }
-}
-
-// one block per segment; thread 0 solves (sizes are <= 8x8)
-__global__ void fit_solve(Plan* plan, const double* __restrict__ t, const double* __restrict__ partial,
-                          const uint32_t* status) {
-  __shared__ double sacc[kAcc];
-  if (failed(status) || !poly_active(plan)) return;
-  const uint32_t seg = blockIdx.x;
-  if (seg >= plan->nseg) return;
-  uint32_t b, e;
-  seg_range(plan, seg, b, e);
-  {  // chunk partials of this segment, summed in chunk order, one accumulator per thread
-    uint64_t c0 = 0;
-    for (uint32_t s2 = 0; s2 < seg; ++s2) {
-      uint32_t bb, ee;
-      seg_range(plan, s2, bb, ee);
-      c0 += (ee - bb + kChunk - 1) / kChunk;
+    for (int j = 0; j < kAcc; ++j) {
+      double v = acc[j];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][j] = v;
     }
-    const uint64_t ncs = (e - b + kChunk - 1) / kChunk;
+    __syncthreads();
     if (threadIdx.x < kAcc) {
       double v = 0.0;
-      for (uint64_t c = 0; c < ncs; ++c) v += partial[(c0 + c) * kAcc + threadIdx.x];
-      sacc[threadIdx.x] = v;
+      for (int w = 0; w < 8; ++w) v += red[w][threadIdx.x];
+      partial[c * kAcc + threadIdx.x] = v;
     }
     __syncthreads();
   }
-  if (threadIdx.x != 0) return;
-  const uint32_t len = e - b;
+}
+
+// degree <= 7: one segment per block iteration; thread 0 solves (sizes <= 8x8)
+__global__ void fit_solve(Plan* plan, const double* __restrict__ t, const uint32_t* __restrict__ seg_end,
+                          const uint64_t* __restrict__ chunk, const double* __restrict__ partial, float* coeffs,
+                          const uint32_t* status) {
+  __shared__ double sacc[kAcc];
+  if (failed(status) || !poly_active(plan) || plan->degree > kMaxDeg) return;
+  const uint32_t S = plan->nseg;
   const int deg = static_cast<int>(plan->degree);
-  float* out = plan->coeffs + seg * kCps;
-  for (int j = 0; j <= deg; ++j) out[j] = 0.0f;
-  if (len == 1) {  // curvefit.cpp:134-138
-    out[0] = static_cast<float>(t[b]);
-    return;
-  }
-  const int eff = deg < static_cast<int>(len) - 1 ? deg : static_cast<int>(len) - 1;
-  const int m = eff + 1;
-  // Every loop below runs over the fixed bound kCps with an `< m` guard and is
-  // fully unrolled, so the 8x8 systems live in registers, not local memory.
-  double G[kCps][kCps], rhs[kCps];
-  {
-    int a = 0;
+  const uint32_t cps = static_cast<uint32_t>(deg) + 1;
+  for (uint32_t seg = blockIdx.x; seg < S; seg += gridDim.x) {
+    uint32_t b, e;
+    seg_range(seg_end, seg, b, e);
+    {  // chunk partials of this segment, summed in chunk order, one accumulator per thread
+      const uint64_t c0 = chunk[seg], ncs = chunk[seg + 1] - c0;
+      if (threadIdx.x < kAcc) {
+        double v = 0.0;
+        for (uint64_t c = 0; c < ncs; ++c) v += partial[(c0 + c) * kAcc + threadIdx.x];
+        sacc[threadIdx.x] = v;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      const uint32_t len = e - b;
+      float* out = coeffs + static_cast<uint64_t>(seg) * cps;
+      for (int j = 0; j <= deg; ++j) out[j] = 0.0f;
+      if (len == 1) {  // curvefit.cpp:134-138
+        out[0] = static_cast<float>(t[b]);
+      } else {
+        const int eff = deg < static_cast<int>(len) - 1 ? deg : static_cast<int>(len) - 1;
+        const int m = eff + 1;
+        // Every loop below runs over the fixed bound kCps with an `< m` guard and is
+        // fully unrolled, so the 8x8 systems live in registers, not local memory.
+        double G[kCps][kCps], rhs[kCps];
+        {
+          int a = 0;
 #pragma unroll
-    for (int j = 0; j <= kMaxDeg; ++j)
+          for (int j = 0; j <= kMaxDeg; ++j)
 #pragma unroll
-      for (int q = j; q <= kMaxDeg; ++q, ++a) G[j][q] = G[q][j] = sacc[a];
-  }
+            for (int q = j; q <= kMaxDeg; ++q, ++a) G[j][q] = G[q][j] = sacc[a];
+        }
 #pragma unroll
-  for (int j = 0; j < kCps; ++j) rhs[j] = sacc[36 + j];
-  // Cholesky G = L L^T (SPD: the Legendre columns are independent for len > eff)
-  double L[kCps][kCps];
+        for (int j = 0; j < kCps; ++j) rhs[j] = sacc[36 + j];
+        // Cholesky G = L L^T (SPD: the Legendre columns are independent for len > eff)
+        double L[kCps][kCps];
 #pragma unroll
-  for (int j = 0; j < kCps; ++j)
+        for (int j = 0; j < kCps; ++j)
 #pragma unroll
-    for (int i = 0; i < kCps; ++i) L[j][i] = 0.0;
+          for (int i = 0; i < kCps; ++i) L[j][i] = 0.0;
 #pragma unroll
-  for (int j = 0; j < kCps; ++j) {
-    if (j < m) {
-      double s = G[j][j];
+        for (int j = 0; j < kCps; ++j) {
+          if (j < m) {
+            double s2 = G[j][j];
 #pragma unroll
-      for (int q = 0; q < j; ++q) s -= L[j][q] * L[j][q];
-      L[j][j] = sqrt(s > 0.0 ? s : 0.0);
+            for (int q = 0; q < j; ++q) s2 -= L[j][q] * L[j][q];
+            L[j][j] = sqrt(s2 > 0.0 ? s2 : 0.0);
 #pragma unroll
-      for (int i = j + 1; i < kCps; ++i) {
-        if (i < m) {
-          double v = G[i][j];
+            for (int i = j + 1; i < kCps; ++i) {
+              if (i < m) {
+                double v = G[i][j];
 #pragma unroll
-          for (int q = 0; q < j; ++q) v -= L[i][q] * L[j][q];
-          L[i][j] = L[j][j] > 0.0 ? v / L[j][j] : 0.0;
+                for (int q = 0; q < j; ++q) v -= L[i][q] * L[j][q];
+                L[i][j] = L[j][j] > 0.0 ? v / L[j][j] : 0.0;
+              }
+            }
+          }
+        }
+        double z[kCps], aL[kCps];
+#pragma unroll
+        for (int i = 0; i < kCps; ++i) {
+          double v = rhs[i];
+#pragma unroll
+          for (int q = 0; q < i; ++q) v -= L[i][q] * z[q];
+          z[i] = (i < m && L[i][i] > 0.0) ? v / L[i][i] : 0.0;
+        }
+#pragma unroll
+        for (int i = kCps - 1; i >= 0; --i) {
+          double v = z[i];
+#pragma unroll
+          for (int q = i + 1; q < kCps; ++q) v -= L[q][i] * aL[q];  // L[q][i] = 0 for q >= m
+          aL[i] = (i < m && L[i][i] > 0.0) ? v / L[i][i] : 0.0;
+        }
+        // Legendre → t-monomials: P_{j+1} = ((2j+1) t P_j - j P_{j-1}) / (j+1)
+        double Lc[kCps][kCps];
+#pragma unroll
+        for (int j = 0; j < kCps; ++j)
+#pragma unroll
+          for (int p = 0; p < kCps; ++p) Lc[j][p] = 0.0;
+        Lc[0][0] = 1.0;
+        Lc[1][1] = 1.0;
+#pragma unroll
+        for (int j = 1; j + 1 < kCps; ++j)
+#pragma unroll
+          for (int p = 0; p <= j + 1; ++p)
+            Lc[j + 1][p] = ((2 * j + 1) * (p > 0 ? Lc[j][p - 1] : 0.0) - j * Lc[j - 1][p]) / (j + 1);
+        double ct[kCps];
+#pragma unroll
+        for (int p = 0; p < kCps; ++p) {
+          double v = 0.0;
+#pragma unroll
+          for (int j = p; j < kCps; ++j) v += aL[j] * Lc[j][p];  // aL[j] = 0 for j >= m
+          ct[p] = v;
+        }
+        // t-monomials → x-monomials, curvefit.cpp:157-172 (the same pow() values)
+        const double alpha = 2.0 / static_cast<double>(len - 1);
+        const double beta = -static_cast<double>(len + 1) / static_cast<double>(len - 1);
+        double pa[kCps], pb[kCps];
+#pragma unroll
+        for (int k = 0; k < kCps; ++k) {
+          pa[k] = k < m ? pow(alpha, static_cast<double>(k)) : 0.0;
+          pb[k] = k < m ? pow(beta, static_cast<double>(k)) : 0.0;
+        }
+        constexpr double kBinom[kCps][kCps] = {{1, 0, 0, 0, 0, 0, 0, 0},       {1, 1, 0, 0, 0, 0, 0, 0},
+                                               {1, 2, 1, 0, 0, 0, 0, 0},       {1, 3, 3, 1, 0, 0, 0, 0},
+                                               {1, 4, 6, 4, 1, 0, 0, 0},       {1, 5, 10, 10, 5, 1, 0, 0},
+                                               {1, 6, 15, 20, 15, 6, 1, 0},    {1, 7, 21, 35, 35, 21, 7, 1}};
+#pragma unroll
+        for (int k = 0; k < kCps; ++k) {
+          if (k < m) {
+            double c = 0.0;
+#pragma unroll
+            for (int j = k; j < kCps; ++j)
+              if (j < m) c += ct[j] * kBinom[j][k] * pa[k] * pb[j - k];
+            out[k] = static_cast<float>(c);
+          }
         }
       }
     }
+    __syncthreads();
   }
-  double z[kCps], aL[kCps];
-#pragma unroll
-  for (int i = 0; i < kCps; ++i) {
-    double v = rhs[i];
-#pragma unroll
-    for (int q = 0; q < i; ++q) v -= L[i][q] * z[q];
-    z[i] = (i < m && L[i][i] > 0.0) ? v / L[i][i] : 0.0;
-  }
-#pragma unroll
-  for (int i = kCps - 1; i >= 0; --i) {
-    double v = z[i];
-#pragma unroll
-    for (int q = i + 1; q < kCps; ++q) v -= L[q][i] * aL[q];  // L[q][i] = 0 for q >= m
-    aL[i] = (i < m && L[i][i] > 0.0) ? v / L[i][i] : 0.0;
-  }
-  // Legendre → t-monomials: P_{j+1} = ((2j+1) t P_j - j P_{j-1}) / (j+1)
-  double Lc[kCps][kCps];
-#pragma unroll
-  for (int j = 0; j < kCps; ++j)
-#pragma unroll
-    for (int p = 0; p < kCps; ++p) Lc[j][p] = 0.0;
-  Lc[0][0] = 1.0;
-  Lc[1][1] = 1.0;
-#pragma unroll
-  for (int j = 1; j + 1 < kCps; ++j)
-#pragma unroll
-    for (int p = 0; p <= j + 1; ++p)
-      Lc[j + 1][p] = ((2 * j + 1) * (p > 0 ? Lc[j][p - 1] : 0.0) - j * Lc[j - 1][p]) / (j + 1);
-  double ct[kCps];
-#pragma unroll
-  for (int p = 0; p < kCps; ++p) {
-    double v = 0.0;
-#pragma unroll
-    for (int j = p; j < kCps; ++j) v += aL[j] * Lc[j][p];  // aL[j] = 0 for j >= m
-    ct[p] = v;
-  }
-  // t-monomials → x-monomials, curvefit.cpp:157-172 (the same pow() values)
-  const double alpha = 2.0 / static_cast<double>(len - 1);
-  const double beta = -static_cast<double>(len + 1) / static_cast<double>(len - 1);
-  double pa[kCps], pb[kCps];
-#pragma unroll
-  for (int k = 0; k < kCps; ++k) {
-    pa[k] = k < m ? pow(alpha, static_cast<double>(k)) : 0.0;
-    pb[k] = k < m ? pow(beta, static_cast<double>(k)) : 0.0;
-  }
-  constexpr double kBinom[kCps][kCps] = {{1, 0, 0, 0, 0, 0, 0, 0},       {1, 1, 0, 0, 0, 0, 0, 0},
-                                         {1, 2, 1, 0, 0, 0, 0, 0},       {1, 3, 3, 1, 0, 0, 0, 0},
-                                         {1, 4, 6, 4, 1, 0, 0, 0},       {1, 5, 10, 10, 5, 1, 0, 0},
-                                         {1, 6, 15, 20, 15, 6, 1, 0},    {1, 7, 21, 35, 35, 21, 7, 1}};
-#pragma unroll
-  for (int k = 0; k < kCps; ++k) {
-    if (k < m) {
-      double c = 0.0;
-#pragma unroll
-      for (int j = k; j < kCps; ++j)
-        if (j < m) c += ct[j] * kBinom[j][k] * pa[k] * pb[j - k];
-      out[k] = static_cast<float>(c);
+}
+
+// Degree 8..60 (fit_poly's range, curvefit.cpp:130): one block per segment.
+// The normal equations in the Legendre basis are accumulated in batches of 64
+// points whose basis values sit in shared memory; each thread owns a fixed
+// set of Gram / rhs entries and sums them in point order (deterministic).
+// Cholesky, Legendre → t-monomials and the x expansion (Pascal binomials in
+// double, as curvefit.cpp:159-165 builds them) run in one thread on the
+// block's global scratch.  The Vandermonde system the reference hands to
+// Eigen's QR is ill-conditioned at these degrees, so the coefficients are not
+// expected to match it beyond the reconstructed values' tolerance.
+constexpr int kWideBatch = 64;
+constexpr int kWideEntries = kWideCps * (kWideCps + 1) / 2 + kWideCps;  // 1891 + 61
+constexpr int kWideScratch = 3 * kWideCps * kWideCps;                    // G | L | Lc (doubles)
+__global__ void __launch_bounds__(256) fit_solve_wide(Plan* plan, const double* __restrict__ t,
+                                                      const uint32_t* __restrict__ seg_end, float* coeffs,
+                                                      double* scratch, const uint32_t* status) {
+  __shared__ double V[kWideBatch][kWideCps];
+  __shared__ double Y[kWideBatch];
+  __shared__ int16_t ej[kWideEntries], eq[kWideEntries];  // entry → (row, column); column -1 = rhs
+  if (failed(status) || !poly_active(plan) || plan->degree <= kMaxDeg) return;
+  const uint32_t S = plan->nseg;
+  const int deg = static_cast<int>(plan->degree);
+  const uint32_t cps = static_cast<uint32_t>(deg) + 1;
+  double* G = scratch + static_cast<uint64_t>(blockIdx.x) * kWideScratch;
+  double* L = G + kWideCps * kWideCps;
+  double* Lc = L + kWideCps * kWideCps;
+  for (uint32_t seg = blockIdx.x; seg < S; seg += gridDim.x) {
+    uint32_t b, e;
+    seg_range(seg_end, seg, b, e);
+    const uint32_t len = e - b;
+    float* out = coeffs + static_cast<uint64_t>(seg) * cps;
+    if (len == 1) {
+      if (threadIdx.x == 0) {
+        for (int j = 0; j <= deg; ++j) out[j] = 0.0f;
+        out[0] = static_cast<float>(t[b]);
+      }
+      continue;
     }
+    const int eff = deg < static_cast<int>(len) - 1 ? deg : static_cast<int>(len) - 1;
+    const int m = eff + 1;
+    const int ne = m * (m + 1) / 2 + m;
+    if (threadIdx.x == 0) {
+      int a = 0;
+      for (int j = 0; j < m; ++j)
+        for (int q = j; q < m; ++q, ++a) {
+          ej[a] = static_cast<int16_t>(j);
+          eq[a] = static_cast<int16_t>(q);
+        }
+      for (int j = 0; j < m; ++j, ++a) {
+        ej[a] = static_cast<int16_t>(j);
+        eq[a] = -1;
+      }
+    }
+    __syncthreads();
+    constexpr int kOwn = (kWideEntries + 255) / 256;
+    double acc[kOwn];
+#pragma unroll
+    for (int u = 0; u < kOwn; ++u) acc[u] = 0.0;
+    const double alpha = 2.0 / static_cast<double>(len - 1);
+    const double beta = -static_cast<double>(len + 1) / static_cast<double>(len - 1);
+    for (uint32_t p0 = 0; p0 < len; p0 += kWideBatch) {
+      const uint32_t nb = len - p0 < kWideBatch ? len - p0 : kWideBatch;
+      if (threadIdx.x < nb) {
+        const uint32_t i = p0 + threadIdx.x;
+        const double x = alpha * static_cast<double>(i + 1) + beta;
+        V[threadIdx.x][0] = 1.0;
+        if (m > 1) V[threadIdx.x][1] = x;
+        for (int j = 1; j + 1 < m; ++j)
+          V[threadIdx.x][j + 1] = ((2 * j + 1) * x * V[threadIdx.x][j] - j * V[threadIdx.x][j - 1]) / (j + 1);
+        Y[threadIdx.x] = t[b + i];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < kOwn; ++u) {
+        const int a = threadIdx.x + 256 * u;
+        if (a < ne) {
+          const int j = ej[a], q = eq[a];
+          double v = acc[u];
+          if (q >= 0)
+            for (uint32_t k = 0; k < nb; ++k) v += V[k][j] * V[k][q];
+          else
+            for (uint32_t k = 0; k < nb; ++k) v += V[k][j] * Y[k];
+          acc[u] = v;
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < kOwn; ++u) {
+      const int a = threadIdx.x + 256 * u;
+      if (a < ne) {
+        const int j = ej[a], q = eq[a];
+        if (q >= 0) {
+          G[j * kWideCps + q] = acc[u];
+          G[q * kWideCps + j] = acc[u];
+        } else {
+          Lc[j] = acc[u];  // rhs, parked in the Lc area until the solve
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double rhs[kWideCps], z[kWideCps], aL[kWideCps], ct[kWideCps];
+      for (int j = 0; j < m; ++j) rhs[j] = Lc[j];
+      for (int j = 0; j < m; ++j) {  // Cholesky
+        double s2 = G[j * kWideCps + j];
+        for (int q = 0; q < j; ++q) s2 -= L[j * kWideCps + q] * L[j * kWideCps + q];
+        L[j * kWideCps + j] = sqrt(s2 > 0.0 ? s2 : 0.0);
+        for (int i = j + 1; i < m; ++i) {
+          double v = G[i * kWideCps + j];
+          for (int q = 0; q < j; ++q) v -= L[i * kWideCps + q] * L[j * kWideCps + q];
+          L[i * kWideCps + j] = L[j * kWideCps + j] > 0.0 ? v / L[j * kWideCps + j] : 0.0;
+        }
+      }
+      for (int i = 0; i < m; ++i) {
+        double v = rhs[i];
+        for (int q = 0; q < i; ++q) v -= L[i * kWideCps + q] * z[q];
+        z[i] = L[i * kWideCps + i] > 0.0 ? v / L[i * kWideCps + i] : 0.0;
+      }
+      for (int i = m - 1; i >= 0; --i) {
+        double v = z[i];
+        for (int q = i + 1; q < m; ++q) v -= L[q * kWideCps + i] * aL[q];
+        aL[i] = L[i * kWideCps + i] > 0.0 ? v / L[i * kWideCps + i] : 0.0;
+      }
+      // Legendre → t-monomials, row by row in the Lc area
+      for (int j = 0; j < m; ++j)
+        for (int p = 0; p < m; ++p) Lc[j * kWideCps + p] = 0.0;
+      Lc[0] = 1.0;
+      if (m > 1) Lc[kWideCps + 1] = 1.0;
+      for (int j = 1; j + 1 < m; ++j)
+        for (int p = 0; p <= j + 1; ++p)
+          Lc[(j + 1) * kWideCps + p] =
+              ((2 * j + 1) * (p > 0 ? Lc[j * kWideCps + p - 1] : 0.0) - j * Lc[(j - 1) * kWideCps + p]) / (j + 1);
+      for (int p = 0; p < m; ++p) {
+        double v = 0.0;
+        for (int j = p; j < m; ++j) v += aL[j] * Lc[j * kWideCps + p];
+        ct[p] = v;
+      }
+      // binomials by Pascal's rule (curvefit.cpp:159-165) into the L area
+      double* B = L;
+      for (int j = 0; j < m; ++j) {
+        for (int k = 0; k <= j; ++k) B[j * kWideCps + k] = 1.0;
+        for (int k = 1; k < j; ++k) B[j * kWideCps + k] = B[(j - 1) * kWideCps + k - 1] + B[(j - 1) * kWideCps + k];
+      }
+      for (int j = 0; j <= deg; ++j) out[j] = 0.0f;
+      for (int k = 0; k < m; ++k) {
+        double c = 0.0;
+        const double ak = pow(alpha, static_cast<double>(k));
+        for (int j = k; j < m; ++j) c += ct[j] * B[j * kWideCps + k] * ak * pow(beta, static_cast<double>(j - k));
+        out[k] = static_cast<float>(c);
+      }
+    }
+    __syncthreads();
   }
 }
 
 // serialize_fit (curvefit.cpp:285-298) + reorder payload size; vl, rl, flags
-__global__ void fit_emit(Plan* plan, uint8_t* out, int cfg_degree, const uint32_t* status) {
-  if (failed(status) || !fit_active(plan) || threadIdx.x != 0) return;
+__global__ void fit_emit(Plan* plan, uint8_t* out, int cfg_degree, const uint32_t* __restrict__ seg_end,
+                         const float* __restrict__ coeffs, uint32_t* status) {
+  if (failed(status) || !fit_active(plan)) return;
   const uint32_t kind = plan->fit_kind;
   const uint32_t S = plan->nseg, deg = kind ? static_cast<uint32_t>(cfg_degree) : plan->degree;
   const uint32_t cps = kind ? 4 : deg + 1;  // coeffs_per_segment
+  if (S > 0xffff) {  // curvefit.cpp:287
+    if (threadIdx.x == 0) latch(status, GP_ERROR);
+    return;
+  }
   uint8_t* p = out + 49 + plan->il;
-  p[0] = static_cast<uint8_t>(kind);  // 0 piecewise polynomial, 1 double exponential
-  p[1] = static_cast<uint8_t>(S);
-  p[2] = static_cast<uint8_t>(S >> 8);
-  uint8_t* q = p + 3;
-  for (uint32_t s = 0; s < S; ++s, q += 4) st_u32_unaligned(q, plan->seg_end[s]);
-  *q++ = static_cast<uint8_t>(deg);
-  for (uint32_t s = 0; s < S; ++s)
-    for (uint32_t j = 0; j < cps; ++j, q += 4) st_u32_unaligned(q, __float_as_uint(plan->coeffs[s * kCps + j]));
-  st_u32_unaligned(q, plan->sign_split);
-  plan->vl = 1 + 2 + 4ull * S + 1 + 4ull * S * cps + 4;
-  uint32_t w = 0;
-  for (uint64_t x = plan->d - 1; x; x >>= 1) ++w;
-  plan->rl = plan->identity ? 0 : (plan->n_values * w + 7) / 8;
+  if (threadIdx.x == 0) {
+    p[0] = static_cast<uint8_t>(kind);  // 0 piecewise polynomial, 1 double exponential
+    p[1] = static_cast<uint8_t>(S);
+    p[2] = static_cast<uint8_t>(S >> 8);
+  }
+  for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) st_u32_unaligned(p + 3 + 4ull * s, seg_end[s]);
+  uint8_t* q = p + 3 + 4ull * S;
+  if (threadIdx.x == 0) *q = static_cast<uint8_t>(deg);
+  ++q;
+  const uint64_t nc = static_cast<uint64_t>(S) * cps;
+  for (uint64_t i = threadIdx.x; i < nc; i += blockDim.x) st_u32_unaligned(q + 4 * i, __float_as_uint(coeffs[i]));
+  if (threadIdx.x == 0) {
+    st_u32_unaligned(q + 4 * nc, plan->sign_split);
+    plan->vl = 1 + 2 + 4ull * S + 1 + 4ull * S * cps + 4;
+    uint32_t w = 0;
+    for (uint64_t x = plan->d - 1; x; x >>= 1) ++w;
+    plan->rl = plan->identity ? 0 : (plan->n_values * w + 7) / 8;
+  }
 }
 
 // reorder_encode (curvefit.cpp:332-340): entries of w bits, LSB-first
@@ -567,63 +962,114 @@ __global__ void reorder_pack(const uint32_t* __restrict__ map, Plan* plan, uint8
 
 // ---------------------------------------------------------------- decode
 // parse_fit (curvefit.cpp:300-325), pipeline.cpp:117-118 trailing bytes, and
-// the reorder_decode length/slack rules (curvefit.cpp:342-356).
-__global__ void fit_parse(const uint8_t* __restrict__ in, Plan* plan, uint32_t* status) {
+// the reorder_decode length/slack rules (curvefit.cpp:342-356).  One block:
+// the sequential parse's first failure is the lowest failing bound index
+// (truncation before bound i, or bound i not increasing), found in parallel.
+__global__ void __launch_bounds__(256) fit_parse(const uint8_t* __restrict__ in, Plan* plan, uint32_t* status) {
+  __shared__ uint32_t s_first;
+  __shared__ uint32_t s_found;
+  __shared__ int s_err;
   if (failed(status) || !fit_active(plan)) return;
   const uint8_t* p = in + plan->off_value;
   const uint64_t vl = plan->vl, count = plan->n_values;
-  if (vl < 1) return latch(status, GP_TRUNCATED);
-  if (p[0] > 1) return latch(status, GP_UNKNOWN_METHOD);
-  const uint8_t kind = p[0];
-  if (vl < 3) return latch(status, GP_TRUNCATED);
-  const uint32_t S = p[1] | (p[2] << 8);
-  if (S < 1) return latch(status, GP_CORRUPT_PAYLOAD);
-  uint32_t prev = 0;
-  for (uint32_t i = 0; i < S; ++i) {
-    if (vl < 3 + 4ull * (i + 1)) return latch(status, GP_TRUNCATED);
-    const uint32_t e = ld_u32_unaligned(p + 3 + 4 * i);
-    if (e <= prev && !(i == 0 && e > 0)) return latch(status, GP_CORRUPT_PAYLOAD);
-    prev = e;
-    if (i < kMaxSeg) plan->seg_end[i] = e;
+  if (threadIdx.x == 0) {
+    s_err = 0;
+    s_first = 0xFFFFFFFFu;
+    s_found = 0;
+    if (vl < 1) s_err = GP_TRUNCATED;
+    else if (p[0] > 1) s_err = GP_UNKNOWN_METHOD;
+    else if (vl < 3) s_err = GP_TRUNCATED;
+    else if ((p[1] | (p[2] << 8)) < 1) s_err = GP_CORRUPT_PAYLOAD;
   }
-  if (prev != count) return latch(status, GP_CORRUPT_PAYLOAD);
+  __syncthreads();
+  if (s_err) {
+    if (threadIdx.x == 0) latch(status, s_err);
+    return;
+  }
+  const uint8_t kind = p[0];
+  const uint32_t S = p[1] | (p[2] << 8);
+  for (uint32_t i = threadIdx.x; i < S; i += blockDim.x) {
+    bool bad = vl < 3 + 4ull * (i + 1);
+    if (!bad) {
+      const uint32_t e = ld_u32_unaligned(p + 3 + 4ull * i);
+      const uint32_t prev = i == 0 ? 0u : ld_u32_unaligned(p + 3 + 4ull * (i - 1));
+      bad = e <= prev && !(i == 0 && e > 0);
+    }
+    if (bad) atomicMin(&s_first, i);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t f = s_first;
+    if (f != 0xFFFFFFFFu) {
+      s_err = vl < 3 + 4ull * (f + 1) ? GP_TRUNCATED : GP_CORRUPT_PAYLOAD;
+    } else if (ld_u32_unaligned(p + 3 + 4ull * (S - 1)) != count) {
+      s_err = GP_CORRUPT_PAYLOAD;
+    }
+  }
+  __syncthreads();
+  if (s_err) {
+    if (threadIdx.x == 0) latch(status, s_err);
+    return;
+  }
   uint64_t at = 3 + 4ull * S;
-  if (vl < at + 1) return latch(status, GP_TRUNCATED);
+  if (vl < at + 1) {
+    if (threadIdx.x == 0) latch(status, GP_TRUNCATED);
+    return;
+  }
   const uint32_t deg = p[at++];
   const uint64_t cps = kind == 1 ? 4 : deg + 1;
-  if (vl < at + 4 * S * cps) return latch(status, GP_TRUNCATED);
+  const uint64_t nc = S * cps;
+  if (vl < at + 4 * nc) {
+    if (threadIdx.x == 0) latch(status, GP_TRUNCATED);
+    return;
+  }
   const uint64_t coeff_at = at;
-  at += 4 * S * cps;
-  if (vl < at + 4) return latch(status, GP_TRUNCATED);
+  at += 4 * nc;
+  if (vl < at + 4) {
+    if (threadIdx.x == 0) latch(status, GP_TRUNCATED);
+    return;
+  }
   const uint32_t l = ld_u32_unaligned(p + at);
   at += 4;
-  if (l > count) return latch(status, GP_CORRUPT_PAYLOAD);
-  if (l > 0 && l < count) {
-    bool found = false;
-    for (uint32_t i = 0; i < S; ++i) found |= ld_u32_unaligned(p + 3 + 4 * i) == l;
-    if (!found) return latch(status, GP_CORRUPT_PAYLOAD);
+  if (l > count) {
+    if (threadIdx.x == 0) latch(status, GP_CORRUPT_PAYLOAD);
+    return;
   }
-  if (at != vl) return latch(status, GP_CORRUPT_PAYLOAD);
+  if (l > 0 && l < count) {  // binary_search over the (increasing) bounds
+    for (uint32_t i = threadIdx.x; i < S; i += blockDim.x)
+      if (ld_u32_unaligned(p + 3 + 4ull * i) == l) s_found = 1;
+    __syncthreads();
+    if (!s_found) {
+      if (threadIdx.x == 0) latch(status, GP_CORRUPT_PAYLOAD);
+      return;
+    }
+  }
+  if (at != vl) {
+    if (threadIdx.x == 0) latch(status, GP_CORRUPT_PAYLOAD);
+    return;
+  }
   // reorder_decode structure: count entries of w bits, < 8 slack bits, zero slack
   if (plan->rl) {
     uint32_t w = 0;
     for (uint64_t x = plan->d - 1; x; x >>= 1) ++w;
     const uint64_t need = count * w, have = 8 * plan->rl;
-    if (have < need) return latch(status, GP_TRUNCATED);
-    if (have - need >= 8) return latch(status, GP_CORRUPT_PAYLOAD);
-    if (have > need) {
-      const uint8_t last = in[plan->off_reorder + plan->rl - 1];
-      if (last >> (need % 8)) return latch(status, GP_CORRUPT_PAYLOAD);
+    int err = 0;
+    if (have < need) err = GP_TRUNCATED;
+    else if (have - need >= 8) err = GP_CORRUPT_PAYLOAD;
+    else if (have > need && (in[plan->off_reorder + plan->rl - 1] >> (need % 8))) err = GP_CORRUPT_PAYLOAD;
+    if (err) {
+      if (threadIdx.x == 0) latch(status, err);
+      return;
     }
   }
-  if (S > kMaxSeg || (kind == 0 && deg > kMaxDeg)) return latch(status, GP_CAPACITY);
-  plan->nseg = S;
-  plan->degree = deg;
-  plan->fit_kind = kind;
-  plan->sign_split = l;
-  for (uint32_t s = 0; s < S; ++s)
-    for (uint32_t j = 0; j < cps; ++j)
-      plan->coeffs[s * kCps + j] = __uint_as_float(ld_u32_unaligned(p + coeff_at + 4 * (s * cps + j)));
+  if (threadIdx.x == 0) {  // fit_eval reads bounds and coefficients from the payload itself
+    plan->fit_bounds_at = plan->off_value + 3;
+    plan->fit_coeffs_at = plan->off_value + coeff_at;
+    plan->nseg = S;
+    plan->degree = deg;
+    plan->fit_kind = kind;
+    plan->sign_split = l;
+  }
 }
 
 // reorder entries (entry >= d → corrupt) + permutation check (curvefit.cpp:531-538)
@@ -651,33 +1097,64 @@ __global__ void reorder_unpack(const uint8_t* __restrict__ in, Plan* plan, uint3
   }
 }
 
-// value_decompress evaluate + unfold + scatter (curvefit.cpp:517-541)
-__global__ void fit_eval(const Plan* plan, const uint32_t* __restrict__ map, double* __restrict__ out,
-                         const uint32_t* status) {
-  __shared__ uint32_t bounds[kMaxSeg];
-  __shared__ float coeffs[kMaxSeg * kCps];
+// value_decompress evaluate + unfold + scatter (curvefit.cpp:517-541).  Bounds
+// and coefficients come straight from the payload (any degree byte and up to
+// 0xffff segments); models of <= 64 segments and <= 8 coefficients are staged
+// in shared memory, larger ones searched in place (binary search of the bounds).
+constexpr int kEvalSmemSeg = 64;
+__global__ void fit_eval(const uint8_t* __restrict__ in, const Plan* plan, const uint32_t* __restrict__ map,
+                         double* __restrict__ out, const uint32_t* status) {
+  __shared__ uint32_t sb[kEvalSmemSeg];
+  __shared__ float sc[kEvalSmemSeg * kCps];
   if (failed(status) || !fit_active(plan)) return;
-  const uint32_t S = plan->nseg, cps = plan->degree + 1;
+  const uint32_t S = plan->nseg, cps = cps_of(plan);
+  const uint8_t* bp = in + plan->fit_bounds_at;
+  const uint8_t* cp = in + plan->fit_coeffs_at;
   const bool dexp = plan->fit_kind == 1;
-  for (uint32_t i = threadIdx.x; i < S; i += blockDim.x) bounds[i] = plan->seg_end[i];
-  for (uint32_t i = threadIdx.x; i < S * kCps; i += blockDim.x) coeffs[i] = plan->coeffs[i];
-  __syncthreads();
+  const bool small = S <= kEvalSmemSeg && cps <= kCps;
+  if (small) {
+    for (uint32_t i = threadIdx.x; i < S; i += blockDim.x) sb[i] = ld_u32_unaligned(bp + 4ull * i);
+    for (uint32_t i = threadIdx.x; i < S * cps; i += blockDim.x) sc[i] = __uint_as_float(ld_u32_unaligned(cp + 4ull * i));
+    __syncthreads();
+  }
   const uint64_t n = plan->n_values;
   const uint64_t l = plan->sign_split;
   const bool reorder = plan->rl != 0;
   for (uint64_t s = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; s < n;
        s += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t j = s < l ? s : l + (n - 1 - s);  // position in the folded sequence
-    uint32_t seg = 0;
-    while (bounds[seg] <= j) ++seg;
-    const uint32_t begin = seg == 0 ? 0 : bounds[seg - 1];
-    const double x = static_cast<double>(j - begin + 1);
-    const float* c = coeffs + seg * kCps;
+    uint32_t seg, begin;
     double acc = 0.0;
-    if (dexp)
-      acc = eval_dexp(c, x);
-    else
-      for (int q = static_cast<int>(cps) - 1; q >= 0; --q) acc = __dadd_rn(__dmul_rn(acc, x), static_cast<double>(c[q]));
+    if (small) {
+      seg = 0;
+      while (sb[seg] <= j) ++seg;
+      begin = seg == 0 ? 0 : sb[seg - 1];
+      const double x = static_cast<double>(j - begin + 1);
+      const float* c = sc + seg * cps;
+      if (dexp)
+        acc = eval_dexp(c, x);
+      else
+        for (int q = static_cast<int>(cps) - 1; q >= 0; --q)
+          acc = __dadd_rn(__dmul_rn(acc, x), static_cast<double>(c[q]));
+    } else {  // first bound > j
+      uint32_t lo = 0, hi = S - 1;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) / 2;
+        if (ld_u32_unaligned(bp + 4ull * mid) > j) hi = mid; else lo = mid + 1;
+      }
+      seg = lo;
+      begin = seg == 0 ? 0 : ld_u32_unaligned(bp + 4ull * (seg - 1));
+      const double x = static_cast<double>(j - begin + 1);
+      const uint8_t* c = cp + 4ull * seg * cps;
+      if (dexp) {
+        float cc[4];
+        for (int q = 0; q < 4; ++q) cc[q] = __uint_as_float(ld_u32_unaligned(c + 4 * q));
+        acc = eval_dexp(cc, x);
+      } else {
+        for (int q = static_cast<int>(cps) - 1; q >= 0; --q)
+          acc = __dadd_rn(__dmul_rn(acc, x), static_cast<double>(__uint_as_float(ld_u32_unaligned(c + 4ull * q))));
+      }
+    }
     const double v = s < l ? acc : -acc;
     out[reorder ? map[s] : s] = v;
   }
@@ -773,8 +1250,8 @@ __device__ void log_linear(const double* y, uint32_t begin, uint32_t len, double
   rate = 0.0;
 }
 
-__global__ void __launch_bounds__(kDexpBlock) dexp_fit(Plan* plan, const double* __restrict__ t,
-                                                        const uint32_t* status) {
+__global__ void __launch_bounds__(kDexpBlock) dexp_fit(Plan* plan, const double* __restrict__ t, uint32_t* seg_end,
+                                                        float* coeffs, const uint32_t* status) {
   __shared__ double sh[(kDexpBlock / 32) * 14];
   __shared__ double sp[4], scand[4], sbest, slambda;
   __shared__ int sflag;  // bit0 accepted, bit1 converged, bit2 stop attempts
@@ -908,12 +1385,12 @@ __global__ void __launch_bounds__(kDexpBlock) dexp_fit(Plan* plan, const double*
       double tmp = a; a = c; c = tmp;
       tmp = b; b = d; d = tmp;
     }
-    float* co = plan->coeffs + blockIdx.x * kCps;
+    float* co = coeffs + blockIdx.x * 4;
     co[0] = static_cast<float>(a);
     co[1] = static_cast<float>(b);
     co[2] = static_cast<float>(c);
     co[3] = static_cast<float>(d);
-    plan->seg_end[blockIdx.x] = parts[blockIdx.x][1];
+    seg_end[blockIdx.x] = parts[blockIdx.x][1];
   }
 }
 
@@ -938,6 +1415,9 @@ __global__ void fit_reset(Plan* plan) {
   plan->dexp_fail = 0;
 }
 
+static_assert(sizeof(SegNode) == 32, "workspace sizes SegNode at 32 bytes");
+static_assert(sizeof(SegState) == 32, "workspace sizes SegState at 32 bytes");
+
 void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, uint64_t n_bound, cudaStream_t s,
                        bool dexp) {
   Workspace& w = ctx->ws;
@@ -946,7 +1426,7 @@ void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, 
   launch_radix_sort(ctx, w.u32a, w.u32b, w.u32c, w.u32d, &w.plan->n_values, n_bound, 32, s);
   GP_LAUNCH(ctx, fit_prepare, grid_for(ctx, n_bound, 256), 256, 0, s, w.values, w.u32b, w.plan, w.f64b, w.status);
   if (dexp) {
-    GP_LAUNCH(ctx, dexp_fit, 2, kDexpBlock, 0, s, w.plan, w.f64b, w.status);
+    GP_LAUNCH(ctx, dexp_fit, 2, kDexpBlock, 0, s, w.plan, w.f64b, w.seg_end, w.coeffs, w.status);
     GP_LAUNCH(ctx, dexp_decide, 1, 1, 0, s, w.plan, w.status);
   }
   {  // cooperative launch: every block of the grid must be resident
@@ -960,24 +1440,39 @@ void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, 
     Plan* plan = w.plan;
     double* pdev = w.seg_dev;
     uint32_t* parg = w.seg_arg;
-    uint32_t* st = w.status;
-    void* args[] = {&plan, &t, &degree, &max_segments, &pdev, &parg, &st};
+    SegNode* nodes = reinterpret_cast<SegNode*>(w.seg_nodes);
+    uint32_t* heap = w.seg_heap;
+    uint32_t* pend = w.seg_pend;
+    uint64_t* off = w.seg_off;
+    SegState* st = reinterpret_cast<SegState*>(w.seg_state);
+    uint32_t* seg_end = w.seg_end;
+    uint64_t* chunk = w.seg_chunk;
+    uint32_t node_cap = w.node_cap;
+    uint32_t seg_cap = static_cast<uint32_t>(w.seg_cap);
+    uint32_t* status = w.status;
+    void* args[] = {&plan, &t, &degree, &max_segments, &pdev, &parg, &nodes, &heap, &pend, &off, &st,
+                    &seg_end, &chunk, &node_cap, &seg_cap, &status};
     cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fit_segment_coop), grid, 256, args, 0, s);
     ++ctx->launches;
   }
-  const uint64_t chunks = n_bound / kChunk + kMaxSeg + 1;
-  GP_LAUNCH(ctx, fit_accumulate, static_cast<int>(chunks), 256, 0, s, w.plan, w.f64b, w.partial, w.status);
-  GP_LAUNCH(ctx, fit_solve, kMaxSeg, 64, 0, s, w.plan, w.f64b, w.partial, w.status);
-  GP_LAUNCH(ctx, fit_emit, 1, 32, 0, s, w.plan, out, degree, w.status);
+  const uint64_t seg_bound = std::min<uint64_t>(n_bound, w.seg_cap);
+  GP_LAUNCH(ctx, fit_accumulate, grid_for(ctx, (n_bound / kChunk + seg_bound + 1) * 256, 256), 256, 0, s, w.plan,
+            w.f64b, w.seg_end, w.seg_chunk, w.partial, w.status);
+  GP_LAUNCH(ctx, fit_solve, grid_for(ctx, seg_bound * 64, 64), 64, 0, s, w.plan, w.f64b, w.seg_end, w.seg_chunk,
+            w.partial, w.coeffs, w.status);
+  if (degree > kMaxDeg)
+    GP_LAUNCH(ctx, fit_solve_wide, static_cast<int>(std::min<uint64_t>(seg_bound, kWideBlocks)), 256, 0, s, w.plan,
+              w.f64b, w.seg_end, w.coeffs, w.fit_scratch, w.status);
+  GP_LAUNCH(ctx, fit_emit, 1, 256, 0, s, w.plan, out, degree, w.seg_end, w.coeffs, w.status);
   GP_LAUNCH(ctx, reorder_pack, grid_for(ctx, n_bound * 4, 256), 256, 0, s, w.u32b, w.plan, out, w.status);
 }
 
 void launch_decode_fit(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, cudaStream_t s) {
   Workspace& w = ctx->ws;
-  GP_LAUNCH(ctx, fit_parse, 1, 1, 0, s, in, w.plan, w.status);
+  GP_LAUNCH(ctx, fit_parse, 1, 256, 0, s, in, w.plan, w.status);
   cudaMemsetAsync(w.u32c, 0, ((n_bound + 31) / 32) * 4, s);
   GP_LAUNCH(ctx, reorder_unpack, grid_for(ctx, n_bound, 256), 256, 0, s, in, w.plan, w.u32b, w.u32c, w.status);
-  GP_LAUNCH(ctx, fit_eval, grid_for(ctx, n_bound, 256), 256, 0, s, w.plan, w.u32b, w.f64a, w.status);
+  GP_LAUNCH(ctx, fit_eval, grid_for(ctx, n_bound, 256), 256, 0, s, in, w.plan, w.u32b, w.f64a, w.status);
 }
 
 }  // namespace gp
