@@ -130,6 +130,25 @@ GP_API int gp_encode_topr_ef(gp_ctx* ctx, const float* d_grad, float* d_residual
                              const gp_pipeline_config* cfg, uint8_t* d_out, uint64_t cap,
                              uint64_t* d_len, void* stream);
 
+/* The same step in the reference's own precision: d_residual is f64[d]
+ * (Simulation::residual_, a VectorXd, gradient.hpp:29), input = double(g) +
+ * residual in f64, top_r over the f64 input (63-bit keys), the value codec on
+ * the f64 values, and residual = input - decoded in f64.  Containers and
+ * residuals are bit-identical to the reference loop fed double(g). */
+GP_API int gp_encode_topr_ef64(gp_ctx* ctx, const float* d_grad, double* d_residual, uint64_t d, uint64_t r,
+                               const gp_pipeline_config* cfg, uint8_t* d_out, uint64_t cap,
+                               uint64_t* d_len, void* stream);
+
+/* compress_gradient(sg, cfg, dense) + pack with the reference's own value
+ * type (pipeline.cpp:146-221): sg = (d, d_support u32[r] strictly increasing,
+ * d_values f64[r]); d_dense f64[d] or NULL.  Bloom policies take values from
+ * d_dense when given, else from sg with zeros off its support
+ * (pipeline.cpp:38-54).  r = 0 is legal for index method NONE with raw value
+ * methods (empty payloads), an Error otherwise, as in the reference. */
+GP_API int gp_encode_sparse(gp_ctx* ctx, uint64_t d, const uint32_t* d_support, const double* d_values,
+                            uint64_t r, const double* d_dense, const gp_pipeline_config* cfg, uint8_t* d_out,
+                            uint64_t cap, uint64_t* d_len, void* stream);
+
 /* compress_gradient(sg, cfg, &dense) + pack for a caller-chosen support:
  * d_support: u32[r] strictly increasing (validated, gradient.cpp:19-30),
  * values are gathered from d_dense (pipeline.cpp:38-54). */

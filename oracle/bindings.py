@@ -98,6 +98,10 @@ class CpuCodec:
         if prefix == "gpr":
             bind("volume", [_P(_u8), C.c_size_t, _P(_u64)])
             bind("random_r", [_u64, _u64, _u64, _P(_u32)])
+            bind("encode_sparse64", [_u64, _P(_u32), _P(C.c_double), _u64, _P(C.c_double), _P(GpConfig),
+                                     _P(_P(_u8)), _P(C.c_size_t)])
+            bind("ef_step64", [_P(C.c_float), _P(C.c_double), _u64, _u64, _P(GpConfig), _P(_P(_u8)),
+                               _P(C.c_size_t)])
         if prefix == "gpo":
             bind("rle_encode", [_P(_u32), _u64, _u64, _P(_P(_u8)), _P(C.c_size_t)])
             bind("bitmap_bytes", [_P(_u32), _u64, _u64, _P(_u8)])
@@ -204,6 +208,29 @@ class CpuCodec:
         p, n = _P(_u8)(), C.c_size_t()
         self._check(self._f["encode_dense"](g.ctypes.data_as(_P(C.c_float)), g.size, r,
                                             C.byref(cfg), C.byref(p), C.byref(n)))
+        return self._take(p, n.value, np.uint8).tobytes()
+
+    def encode_sparse64(self, d: int, support, values, cfg: GpConfig, dense=None) -> bytes:
+        """compress_gradient(sg, cfg, dense) + pack with f64 values (reference build only)."""
+        s = np.ascontiguousarray(support, dtype=np.uint32)
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        dp = None
+        if dense is not None:
+            dense = np.ascontiguousarray(dense, dtype=np.float64)
+            dp = dense.ctypes.data_as(_P(C.c_double))
+        p, n = _P(_u8)(), C.c_size_t()
+        self._check(self._f["encode_sparse64"](d, s.ctypes.data_as(_P(_u32)), v.ctypes.data_as(_P(C.c_double)),
+                                               s.size, dp, C.byref(cfg), C.byref(p), C.byref(n)))
+        return self._take(p, n.value, np.uint8).tobytes()
+
+    def ef_step64(self, g: np.ndarray, residual: np.ndarray, r: int, cfg: GpConfig) -> bytes:
+        """One compensated worker step in f64 (harness.cpp:230-271); `residual` (f64) is updated in place."""
+        g = np.ascontiguousarray(g, dtype=np.float32)
+        assert residual.dtype == np.float64 and residual.flags.c_contiguous
+        p, n = _P(_u8)(), C.c_size_t()
+        self._check(self._f["ef_step64"](g.ctypes.data_as(_P(C.c_float)),
+                                         residual.ctypes.data_as(_P(C.c_double)), g.size, r, C.byref(cfg),
+                                         C.byref(p), C.byref(n)))
         return self._take(p, n.value, np.uint8).tobytes()
 
     def decode(self, data: bytes):

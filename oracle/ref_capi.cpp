@@ -238,6 +238,49 @@ int gpr_encode_dense(const float* g, std::uint64_t d, std::uint64_t r,
   });
 }
 
+// compress_gradient(sg, cfg, dense) + pack with f64 values and an optional
+// f64 dense vector: the reference's own value type (pipeline.hpp:53-54).
+int gpr_encode_sparse64(std::uint64_t d, const std::uint32_t* support, const double* values, std::uint64_t r,
+                        const double* dense, const gp_pipeline_config* cfg, std::uint8_t** out, std::size_t* len) {
+  return guarded([&] {
+    SparseGradient sg;
+    sg.dim = static_cast<Index>(d);
+    sg.support.assign(support, support + r);
+    sg.values.resize(static_cast<Index>(r));
+    for (std::uint64_t i = 0; i < r; ++i) sg.values(static_cast<Index>(i)) = values[i];
+    Vector dv;
+    if (dense) {
+      dv.resize(static_cast<Index>(d));
+      for (std::uint64_t i = 0; i < d; ++i) dv(static_cast<Index>(i)) = dense[i];
+    }
+    const Container c = compress_gradient(sg, to_cfg(cfg), dense ? &dv : nullptr);
+    const std::vector<std::uint8_t> b = pack(c);
+    *len = b.size();
+    *out = out_copy(b.data(), b.size());
+  });
+}
+
+// One worker's compensated step of Simulation::step in the reference's own
+// f64 arithmetic (harness.cpp:230, :242-251, :257-258, :269-271):
+// input = g + residual; wire = pack(compress_gradient(top_r(input, r), cfg,
+// &input)); residual = input - to_dense(decompress_gradient(unpack(wire))).
+int gpr_ef_step64(const float* g, double* residual, std::uint64_t d, std::uint64_t r,
+                  const gp_pipeline_config* cfg, std::uint8_t** out, std::size_t* len) {
+  return guarded([&] {
+    Vector res(static_cast<Index>(d));
+    for (std::uint64_t i = 0; i < d; ++i) res(static_cast<Index>(i)) = residual[i];
+    const Vector gv = dense_of(g, d);
+    const Vector input = gv + res;
+    const SparseGradient sg = top_r(input, static_cast<Index>(r));
+    const std::vector<std::uint8_t> wire = pack(compress_gradient(sg, to_cfg(cfg), &input));
+    const Vector decoded = to_dense(decompress_gradient(unpack(wire)));
+    const Vector next = input - decoded;
+    for (std::uint64_t i = 0; i < d; ++i) residual[i] = next(static_cast<Index>(i));
+    *len = wire.size();
+    *out = out_copy(wire.data(), wire.size());
+  });
+}
+
 int gpr_decode(const std::uint8_t* bytes, std::size_t len, std::uint64_t* d, std::uint32_t** support,
                double** values, std::uint64_t* n) {
   return guarded([&] {

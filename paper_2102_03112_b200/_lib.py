@@ -60,6 +60,8 @@ _SIGS = {
     "gp_pipeline_seed_device": ([_vp, _vp, _u64, C.c_uint32, C.c_uint32, _vp], C.c_int),
     "gp_encode_topr_ef": ([_vp, _vp, _vp, _u64, _u64, _P(GpConfig), _vp, _u64, _vp, _vp], C.c_int),
     "gp_encode_support": ([_vp, _vp, _u64, _vp, _u64, _P(GpConfig), _vp, _u64, _vp, _vp], C.c_int),
+    "gp_encode_topr_ef64": ([_vp, _vp, _vp, _u64, _u64, _P(GpConfig), _vp, _u64, _vp, _vp], C.c_int),
+    "gp_encode_sparse": ([_vp, _u64, _vp, _vp, _u64, _vp, _P(GpConfig), _vp, _u64, _vp, _vp], C.c_int),
     "gp_decode_accumulate": ([_vp, _vp, _u64, _vp, _u64, C.c_float, _vp], C.c_int),
     "gp_decode_accumulate_hint": ([_vp, _vp, _u64, _P(GpConfig), _vp, _u64, C.c_float, _vp], C.c_int),
     "gp_decode_accumulate_dlen": ([_vp, _vp, _u64, _vp, _P(GpConfig), _vp, _u64, C.c_float, _vp], C.c_int),

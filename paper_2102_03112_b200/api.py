@@ -235,6 +235,43 @@ class Codec:
         self._raise(lib.gp_encode_topr_ef(self._ctx, _ptr(grad), _ptr(residual), grad.numel(), r, C.byref(c),
                                           _ptr(out), out.numel(), _ptr(length), _stream(stream)))
 
+    def encode_ef64_into(self, grad: torch.Tensor, residual: torch.Tensor, r: int, cfg: PipelineConfig,
+                         out: torch.Tensor, length: torch.Tensor, stream=None):
+        """encode_ef_into in the reference's own precision: ``residual`` is f64
+        (Simulation::residual_), input = double(grad) + residual, top_r, the value
+        codec and residual = input - decoded all in f64."""
+        assert grad.dtype == torch.float32 and grad.is_cuda and grad.is_contiguous()
+        assert residual.dtype == torch.float64 and residual.is_cuda and residual.is_contiguous()
+        assert residual.numel() == grad.numel() and out.dtype == torch.uint8 and out.is_cuda
+        c = cfg.to_c()
+        self._raise(lib.gp_encode_topr_ef64(self._ctx, _ptr(grad), _ptr(residual), grad.numel(), r, C.byref(c),
+                                            _ptr(out), out.numel(), _ptr(length), _stream(stream)))
+
+    def compress_ef64(self, grad: torch.Tensor, residual: torch.Tensor, r: int, cfg: PipelineConfig) -> torch.Tensor:
+        """encode_ef64_into, synchronised; returns the packed container (device u8)."""
+        out = torch.empty(self.max_container_bytes(grad.numel(), r, cfg), dtype=torch.uint8, device=grad.device)
+        self.encode_ef64_into(grad, residual, r, cfg, out, self._len[0:1])
+        self.status()
+        return out[: int(self._len[0].item())]
+
+    def compress_sparse(self, d: int, support: torch.Tensor, values: torch.Tensor, cfg: PipelineConfig,
+                        dense: torch.Tensor | None = None) -> torch.Tensor:
+        """compress_gradient(sg, cfg, dense) + pack with the reference's f64 values
+        (pipeline.cpp:146-221): ``support`` int32/uint32 [r] strictly increasing,
+        ``values`` f64 [r], ``dense`` f64 [d] or None."""
+        r = support.numel()
+        assert values.dtype == torch.float64 and values.numel() == r
+        if dense is not None:
+            assert dense.dtype == torch.float64 and dense.numel() == d and dense.is_cuda
+        dev = support.device if r else torch.device("cuda")
+        out = torch.empty(self.max_container_bytes(d, max(r, 1), cfg), dtype=torch.uint8, device=dev)
+        c = cfg.to_c()
+        self._raise(lib.gp_encode_sparse(self._ctx, d, _ptr(support) if r else None, _ptr(values) if r else None,
+                                         r, _ptr(dense), C.byref(c), _ptr(out), out.numel(), _ptr(self._len[0:1]),
+                                         _stream(None)))
+        self.status()
+        return out[: int(self._len[0].item())]
+
     def compress_ef(self, grad: torch.Tensor, residual: torch.Tensor, r: int, cfg: PipelineConfig) -> torch.Tensor:
         """encode_ef_into, synchronised; returns the packed container (device u8)."""
         out = torch.empty(self.max_container_bytes(grad.numel(), r, cfg), dtype=torch.uint8, device=grad.device)

@@ -131,7 +131,7 @@ __global__ void take_support(const float* __restrict__ dense, const uint32_t* __
       return;
     }
     ws_support[i] = s;
-    ws_values[i] = dense[s];
+    if (dense) ws_values[i] = dense[s];
   }
 }
 
@@ -270,6 +270,7 @@ int gp_ctx_create(int device, uint64_t max_d, gp_ctx** out) {
     kernel_attrs_p2();
     kernel_attrs_topr();
     kernel_attrs_dense();
+    kernel_attrs_topr64();
     e = cudaGetLastError();
   }
   if (e != cudaSuccess) {
@@ -451,12 +452,25 @@ uint64_t gp_max_container_bytes(uint64_t d, uint64_t r, const gp_pipeline_config
 
 static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const uint32_t* d_support, uint64_t r,
                          const gp_pipeline_config* cfg, uint8_t* d_out, uint64_t cap, uint64_t* d_len,
-                         void* stream, float* ef_residual = nullptr) {
-  if (!ctx || !cfg || !d_dense || !d_out) return set_error(ctx, GP_ERROR, "encode: null argument");
+                         void* stream, float* ef_residual = nullptr, const double* d_values64 = nullptr,
+                         const double* d_dense64 = nullptr, double* ef_residual64 = nullptr) {
+  // f64 value sequences: compress_gradient's Vector values (gp_encode_sparse)
+  // or the f64 error-feedback input (gp_encode_topr_ef64)
+  const bool f64 = d_values64 || ef_residual64;
+  if (!ctx || !cfg || !d_out || (!d_dense && !f64) || (ef_residual64 && !d_dense))
+    return set_error(ctx, GP_ERROR, "encode: null argument");
   auto s = static_cast<cudaStream_t>(stream);
   if (d < 1) return set_error(ctx, GP_ERROR, "sparsifier: dim must be >= 1");
   if (d > 0xFFFFFFFFULL) return set_error(ctx, GP_ERROR, "sparsifier: dim exceeds 32-bit index space");
-  if (r < 1 || r > d) return set_error(ctx, GP_ERROR, "sparsifier: r out of range [1, d]");
+  if (d_values64 && r == 0) {  // compress_gradient of an empty support (pipeline.cpp:152-154, :215-218)
+    if (cfg->index_method != GP_INDEX_NONE)
+      return set_error(ctx, GP_ERROR, "pipeline: empty support requires the raw index method");
+    if (cfg->value_method == GP_VALUE_FIT_POLY || cfg->value_method == GP_VALUE_FIT_DEXP ||
+        cfg->value_method == GP_VALUE_QUANT)
+      return set_error(ctx, GP_ERROR, "pipeline: fit/quant value methods need a nonempty value sequence");
+  } else if (r < 1 || r > d) {
+    return set_error(ctx, GP_ERROR, "sparsifier: r out of range [1, d]");
+  }
   if (d > ctx->max_d) return set_error(ctx, GP_CAPACITY, "encode: d exceeds the context's max_d");
   const int im = cfg->index_method, vm = cfg->value_method;
   if (im > GP_INDEX_BLOOM_NAIVE || vm > GP_VALUE_RAW_F64)
@@ -506,15 +520,21 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
   // dense-selection fast path (dense.cu): one pass writes bitmap + raw values
   // when top_r(g, r) is the nonzero set; the general kernels below then run
   // against the gate word and return at once (or run, when r != nnz)
-  const bool nz = !d_support && !ef_residual && nz_fast_path_eligible(d, r, im, vm);
+  const bool nz = !d_support && !ef_residual && !f64 && nz_fast_path_eligible(d, r, im, vm);
   uint32_t* const real_status = ctx->ws.status;
   if (nz) {
     GP_STAGE(ctx, ST_INDEX, s, launch_nz_encode(ctx, d_dense, d, r, d_out, s));
     ctx->ws.status = gate_word(ctx);
   }
+  const double* dense64 = d_dense64;
   if (d_support) {
-    GP_LAUNCH(ctx, take_support, grid_for(ctx, r, 256), 256, 0, s, d_dense, d_support, r, d, ctx->ws.support,
-              ctx->ws.values, ctx->ws.status);
+    GP_LAUNCH(ctx, take_support, grid_for(ctx, r, 256), 256, 0, s, f64 ? nullptr : d_dense, d_support, r, d,
+              ctx->ws.support, ctx->ws.values, ctx->ws.status);
+    ctx->vals64 = d_values64;  // sg.values in support order (a Bloom gather below replaces them)
+  } else if (ef_residual64) {
+    GP_STAGE(ctx, ST_TOPR, s, launch_top_r64(ctx, d_dense, ef_residual64, d, r, s));
+    dense64 = ef_residual64;  // the input g + e, written by top-r's first pass
+    ctx->vals64 = ctx->ws.f64a;
   } else {
     GP_STAGE(ctx, ST_TOPR, s, launch_top_r(ctx, d_dense, d, r, s, ef_residual));
     if (ef_residual) d_dense = ef_residual;  // the input g + e, written by top-r's first pass
@@ -537,7 +557,12 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
         GP_STAGE(ctx, ST_SELECT, s, launch_select_p1(ctx, d, r, s));
       else
         GP_STAGE(ctx, ST_SELECT, s, launch_select_slice(ctx, d, s));
-      GP_STAGE(ctx, ST_GATHER, s, launch_gather_values(ctx, d_dense, d, s));
+      if (f64) {
+        GP_STAGE(ctx, ST_GATHER, s, launch_gather_values64(ctx, dense64, d_support, d_values64, r, d, s));
+        ctx->vals64 = ctx->ws.f64a;
+      } else {
+        GP_STAGE(ctx, ST_GATHER, s, launch_gather_values(ctx, d_dense, d, s));
+      }
     }
   }
   const uint64_t n_bound = im == GP_INDEX_BLOOM_P0 ? d : r;
@@ -561,6 +586,7 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
     launch_gate_merge(ctx, s);
   }
   GP_STAGE(ctx, ST_PACK, s, launch_finish_container(ctx, d_out, cap, d_len, bound, s));
+  ctx->vals64 = nullptr;  // captured by the launches above
   return check_launch(ctx, "encode");
 }
 
@@ -586,7 +612,7 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const u
                          const gp_pipeline_config* hint,
                          float* d_dense, uint64_t dense_d, float scale, uint32_t* d_support, double* d_values,
                          uint64_t cap, uint64_t* d_count, uint64_t* d_dim, void* stream, bool own = false,
-                         bool scatter = true) {
+                         bool scatter = true, double* d_dense64 = nullptr) {
   if (!ctx || !d_in) return set_error(ctx, GP_ERROR, "decode: null argument");
   auto s = static_cast<cudaStream_t>(stream);
   gp_pipeline_config h{};
@@ -621,7 +647,7 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const u
   // dense path (dense.cu) — per-tile counts and checks now, one scatter pass
   // reading bitmap words and value runs, no materialised support
   const bool fused = im == GP_INDEX_BITMAP && (vm == GP_VALUE_NONE || vm == GP_VALUE_RAW_F64) && !own &&
-                     !d_support && (d_dense || !scatter);
+                     !d_support && !d_dense64 && (d_dense || !scatter);
   if (own && im != GP_INDEX_BLOOM_NAIVE) {
     if (!is_bloom(im)) launch_own_support(ctx, bound, s);
   } else switch (im) {
@@ -667,7 +693,8 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const u
   if (scatter && d_dense && ctx->decode_overwrite) launch_dense_zero(ctx, d_dense, dense_d, s);
   if (scatter)
     GP_STAGE(ctx, ST_DEC_SCATTER, s,
-             launch_decode_scatter(ctx, d_in, bound, d_dense, dense_d, scale, d_support, d_values, cap, d_count, d_dim, s));
+             launch_decode_scatter(ctx, d_in, bound, d_dense, dense_d, scale, d_support, d_values, cap, d_count, d_dim, s,
+                                   d_dense64));
   return check_launch(ctx, "decode");
 }
 
@@ -725,6 +752,29 @@ int gp_encode_topr_ef(gp_ctx* ctx, const float* d_grad, float* d_residual, uint6
   // residual <- input - decode(container)  (harness.cpp:269-271)
   return decode_common(ctx, d_out, cap, d_len, cfg, d_residual, d, -1.0f, nullptr, nullptr, 0, nullptr, nullptr,
                        stream, true);
+}
+
+int gp_encode_topr_ef64(gp_ctx* ctx, const float* d_grad, double* d_residual, uint64_t d, uint64_t r,
+                        const gp_pipeline_config* cfg, uint8_t* d_out, uint64_t cap, uint64_t* d_len, void* stream) {
+  if (!d_residual || !d_grad) return set_error(ctx, GP_ERROR, "encode_topr_ef64: null argument");
+  const int rc = encode_common(ctx, d_grad, d, nullptr, r, cfg, d_out, cap, d_len, stream, nullptr, nullptr, nullptr,
+                               d_residual);
+  if (rc != GP_OK) return rc;
+  // residual <- input - to_dense(decode(container)), all f64 (harness.cpp:269-271)
+  return decode_common(ctx, d_out, cap, d_len, cfg, nullptr, d, -1.0f, nullptr, nullptr, 0, nullptr, nullptr, stream,
+                       true, true, d_residual);
+}
+
+int gp_encode_sparse(gp_ctx* ctx, uint64_t d, const uint32_t* d_support, const double* d_values, uint64_t r,
+                     const double* d_dense, const gp_pipeline_config* cfg, uint8_t* d_out, uint64_t cap,
+                     uint64_t* d_len, void* stream) {
+  if (r > 0 && (!d_support || !d_values)) return set_error(ctx, GP_ERROR, "encode_sparse: null support or values");
+  // r = 0 (index None only): the kernels read no support or value; any
+  // non-null pointer selects the caller-support path
+  static const uint32_t kNoSupport = 0;
+  static const double kNoValue = 0.0;
+  return encode_common(ctx, nullptr, d, r ? d_support : &kNoSupport, r, cfg, d_out, cap, d_len, stream, nullptr,
+                       r ? d_values : &kNoValue, d_dense);
 }
 
 int gp_top_r(gp_ctx* ctx, const float* d_grad, uint64_t d, uint64_t r, uint32_t* d_support, float* d_values,

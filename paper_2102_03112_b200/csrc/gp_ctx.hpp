@@ -32,6 +32,7 @@ struct Plan {
   uint32_t bin_star, full_bin;  // threshold bin of key >> kTopShift; bin fully kept?
   uint32_t thresh, tie_cut;     // exact threshold key; last kept index among ties
   uint64_t above, n_cand;       // keys in bins above bin_star; candidates emitted
+  uint64_t thresh64;            // f64 input (topr64.cu): exact threshold key
   // ---- bloom
   uint64_t m, seed_a, seed_b, minv;
   uint64_t seed;                // the pipeline seed of this encode
@@ -166,7 +167,8 @@ struct gp_ctx {
   gp::Profiler prof;
   const uint64_t* seed_dev = nullptr;  // gp_ctx_set_seed_source: pipeline seed read on the device
   cudaEvent_t index_event = nullptr;   // gp_ctx_set_index_event: recorded once encode's index payload is final
-  bool decode_overwrite = false;       // gp_ctx_set_decode_overwrite: dense = scale * decoded (zeros off the support)
+  bool decode_overwrite = false;
+  const double* vals64 = nullptr;      // this encode's f64 value sequence (null: ws.values, f32)       // gp_ctx_set_decode_overwrite: dense = scale * decoded (zeros off the support)
 };
 
 namespace gp {
@@ -206,10 +208,13 @@ void kernel_attrs_bloom();
 void kernel_attrs_p2();
 void kernel_attrs_topr();
 void kernel_attrs_dense();
+void kernel_attrs_topr64();
 
 // topr.cu: ws.support / ws.values <- top-r of grad
 void launch_top_r(gp_ctx* ctx, const float* grad, uint64_t d, uint64_t r, cudaStream_t s, float* residual = nullptr);
 void launch_own_support(gp_ctx* ctx, uint64_t r_bound, cudaStream_t s);
+// topr64.cu: ws.support / ws.f64a <- top-r of double(grad) + residual (written over residual)
+void launch_top_r64(gp_ctx* ctx, const float* grad, double* residual, uint64_t d, uint64_t r, cudaStream_t s);
 
 // container.cu
 void launch_crc_range(gp_ctx* ctx, const uint8_t* base, const uint64_t* off_dev, uint64_t off_host,
@@ -259,6 +264,8 @@ void launch_table_scan(gp_ctx* ctx, uint32_t* table, const uint64_t* n_dev, uint
 
 // values.cu
 void launch_gather_values(gp_ctx* ctx, const float* dense, uint64_t n_bound, cudaStream_t s);
+void launch_gather_values64(gp_ctx* ctx, const double* dense, const uint32_t* sup, const double* sval, uint64_t r,
+                            uint64_t n_bound, cudaStream_t s);
 void launch_values_raw(gp_ctx* ctx, uint8_t* out, bool f64, uint64_t n_bound, cudaStream_t s);
 void launch_values_raw_check(gp_ctx* ctx, cudaStream_t s);
 void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, uint64_t n_bound, cudaStream_t s,
@@ -273,6 +280,6 @@ void launch_decode_inflate(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, cud
 void launch_decode_scatter(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, float* dense, uint64_t dense_d,
                            float scale,
                            uint32_t* out_support, double* out_values, uint64_t cap, uint64_t* d_count,
-                           uint64_t* d_dim, cudaStream_t s);
+                           uint64_t* d_dim, cudaStream_t s, double* dense64 = nullptr);
 
 }  // namespace gp

@@ -277,4 +277,15 @@ __device__ __forceinline__ void st_u64_unaligned(uint8_t* p, uint64_t v) {
   st_u32_unaligned(p + 4, static_cast<uint32_t>(v >> 32));
 }
 
+// The value sequence an encode hands to the value codec: f32 (top-r of an f32
+// gradient, exact as doubles) or f64 (compress_gradient's own Vector values,
+// pipeline.cpp:146-221, and the f64 error-feedback input).  Read as double.
+struct ValSrc {
+  const float* f32;
+  const double* f64;
+  __device__ __forceinline__ double operator[](uint64_t i) const {
+    return f64 ? f64[i] : static_cast<double>(f32[i]);
+  }
+};
+
 }  // namespace gp

@@ -573,6 +573,10 @@ void launch_top_r(gp_ctx* ctx, const float* grad, uint64_t d, uint64_t r, cudaSt
             w.values, tiles_f, w.ticket + 2, w.status);
 }
 
+void launch_topr_pick_bin(gp_ctx* ctx, uint64_t r, cudaStream_t s) {
+  GP_LAUNCH(ctx, topr_pick_bin, 1, 1024, 0, s, ctx->ws.hist, r, ctx->ws.plan, ctx->ws.status);
+}
+
 void kernel_attrs_topr() {  // the 128 KiB shared histogram
   cudaFuncSetAttribute(topr_hist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBins * 4);
   cudaFuncSetAttribute(topr_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBins * 4);

@@ -24,29 +24,51 @@ __global__ void gather_values(const float* __restrict__ dense, const uint32_t* _
 // 4 values per thread per step, blockDim apart (each store instruction stays
 // coalesced) with all four loads issued ahead of the stores: one value per
 // thread leaves too few bytes in flight for HBM.
-__global__ void values_raw_encode(const float* __restrict__ values, Plan* plan, uint8_t* out, int f64,
+// f64 gather for compress_gradient(sg, cfg, dense) with Vector values
+// (pipeline.cpp:38-54): dense[idx] when the dense vector is given, otherwise
+// the sparse gradient's value at idx (binary search of the support) or 0
+__global__ void gather_values64(const double* __restrict__ dense, const uint32_t* __restrict__ sup,
+                                const double* __restrict__ sval, uint64_t r, const uint32_t* __restrict__ sel,
+                                const Plan* plan, double* __restrict__ values, const uint32_t* status) {
+  if (failed(status)) return;
+  const uint64_t n = plan->n_values;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t x = sel[i];
+    if (dense) {
+      values[i] = dense[x];
+    } else {
+      uint64_t lo = 0, hi = r;  // lower_bound
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi) / 2;
+        if (sup[mid] < x) lo = mid + 1; else hi = mid;
+      }
+      values[i] = lo < r && sup[lo] == x ? sval[lo] : 0.0;
+    }
+  }
+}
+
+__global__ void values_raw_encode(const ValSrc values, Plan* plan, uint8_t* out, int f64,
                                   const uint32_t* status) {
   if (failed(status)) return;
   const uint64_t n = plan->n_values;
   uint8_t* p = out + 49 + plan->il;
   const uint64_t step = 4ull * gridDim.x * blockDim.x;
   for (uint64_t i0 = 4ull * blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += step) {
-    float v[4];
+    double v[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const uint64_t i = i0 + static_cast<uint64_t>(q) * blockDim.x;
-      v[q] = i < n ? values[i] : 0.f;
+      v[q] = i < n ? values[i] : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const uint64_t i = i0 + static_cast<uint64_t>(q) * blockDim.x;
       if (i >= n) break;
-      if (f64) {
-        const double dv = static_cast<double>(v[q]);
-        st_u64_unaligned(p + 8 * i, static_cast<uint64_t>(__double_as_longlong(dv)));
-      } else {
-        st_u32_unaligned(p + 4 * i, __float_as_uint(v[q]));
-      }
+      if (f64)  // put_f64(values(i))
+        st_u64_unaligned(p + 8 * i, static_cast<uint64_t>(__double_as_longlong(v[q])));
+      else      // put_f32(static_cast<float>(values(i)))
+        st_u32_unaligned(p + 4 * i, __float_as_uint(__double2float_rn(v[q])));
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -75,12 +97,12 @@ __device__ __forceinline__ double value_at(const uint8_t* vp, uint8_t vm, const 
 __global__ void decode_scatter(const uint8_t* __restrict__ in, const Plan* plan, const uint32_t* __restrict__ sel,
                                const double* __restrict__ fitv, float* dense, uint64_t dense_d, float scale,
                                uint32_t* out_support, double* out_values, uint64_t cap, uint64_t* d_count,
-                               uint64_t* d_dim, uint32_t* status) {
+                               uint64_t* d_dim, double* dense64, uint32_t* status) {
   if (failed(status) || plan->fused_bitmap) return;  // bitmap containers on the fused path: dense.cu bm_scatter
   // the container's d must equal the caller's dense length: to_dense builds a
   // d-vector (gradient.cpp:38-42) and the mean adds equal-length vectors
   // (harness.cpp:274-284); a mismatch is caller misuse, never a stray write
-  if (dense && plan->d != dense_d) {
+  if ((dense || dense64) && plan->d != dense_d) {
     if (blockIdx.x == 0 && threadIdx.x == 0) latch(status, GP_ERROR);
     return;
   }
@@ -119,6 +141,8 @@ __global__ void decode_scatter(const uint8_t* __restrict__ in, const Plan* plan,
       const uint64_t i = i0 + static_cast<uint64_t>(q) * blockDim.x;
       if (i >= n) break;
       if (dense) dense[s[q]] = fmaf(scale, static_cast<float>(v[q]), dv[q]);
+      if (dense64)  // the f64 error-feedback residual: e = input - decoded (scale = -1, exact)
+        dense64[s[q]] = __dadd_rn(dense64[s[q]], __dmul_rn(static_cast<double>(scale), v[q]));
       if (out_support) {
         out_support[i] = s[q];
         out_values[i] = v[q];
@@ -138,10 +162,17 @@ void launch_gather_values(gp_ctx* ctx, const float* dense, uint64_t n_bound, cud
   GP_LAUNCH(ctx, gather_values, grid_for(ctx, n_bound, 256), 256, 0, s, dense, w.sel, w.plan, w.values, w.status);
 }
 
+void launch_gather_values64(gp_ctx* ctx, const double* dense, const uint32_t* sup, const double* sval, uint64_t r,
+                            uint64_t n_bound, cudaStream_t s) {
+  Workspace& w = ctx->ws;
+  GP_LAUNCH(ctx, gather_values64, grid_for(ctx, n_bound, 256), 256, 0, s, dense, sup, sval, r, w.sel, w.plan, w.f64a,
+            w.status);
+}
+
 void launch_values_raw(gp_ctx* ctx, uint8_t* out, bool f64, uint64_t n_bound, cudaStream_t s) {
   Workspace& w = ctx->ws;
-  GP_LAUNCH(ctx, values_raw_encode, grid_for(ctx, n_bound, 256), 256, 0, s, w.values, w.plan, out, f64 ? 1 : 0,
-            w.status);
+  GP_LAUNCH(ctx, values_raw_encode, grid_for(ctx, n_bound, 256), 256, 0, s, ValSrc{w.values, ctx->vals64}, w.plan,
+            out, f64 ? 1 : 0, w.status);
 }
 
 void launch_values_raw_check(gp_ctx* ctx, cudaStream_t s) {
@@ -151,10 +182,10 @@ void launch_values_raw_check(gp_ctx* ctx, cudaStream_t s) {
 void launch_decode_scatter(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, float* dense, uint64_t dense_d,
                            float scale,
                            uint32_t* out_support, double* out_values, uint64_t cap, uint64_t* d_count,
-                           uint64_t* d_dim, cudaStream_t s) {
+                           uint64_t* d_dim, cudaStream_t s, double* dense64) {
   Workspace& w = ctx->ws;
   GP_LAUNCH(ctx, decode_scatter, grid_for(ctx, n_bound, 256), 256, 0, s, in, w.plan, w.sel, w.f64a, dense, dense_d,
-            scale, out_support, out_values, cap, d_count, d_dim, w.status);
+            scale, out_support, out_values, cap, d_count, d_dim, dense64, w.status);
 }
 
 }  // namespace gp

@@ -60,7 +60,18 @@ __device__ __forceinline__ double eval_dexp(const float* c, double x) {
                    __dmul_rn(static_cast<double>(c[2]), safe_exp(__dmul_rn(static_cast<double>(c[3]), x))));
 }
 
-__global__ void fit_keys(const float* __restrict__ values, Plan* plan, uint32_t* __restrict__ keys,
+// Sort keys of sort_view (curvefit.cpp:26-39): descending, stable, -0.0 equal
+// to +0.0 (operator>).  f32 values: one 32-bit key.  f64 values: the 64-bit
+// key is sorted as two stable 32-bit LSD passes — the low word here (pass 1),
+// the high word gathered through pass 1's permutation by fit_keys_hi.
+__device__ __forceinline__ uint64_t desc_key64(double v) {
+  uint64_t b = static_cast<uint64_t>(__double_as_longlong(v));
+  if (b == 0x8000000000000000ull) b = 0;
+  const uint64_t asc = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+  return ~asc;
+}
+
+__global__ void fit_keys(const ValSrc values, Plan* plan, uint32_t* __restrict__ keys,
                          uint32_t* __restrict__ idx, const uint32_t* status) {
   __shared__ uint32_t cnt;
   if (failed(status) || !fit_active(plan)) return;
@@ -70,13 +81,19 @@ __global__ void fit_keys(const float* __restrict__ values, Plan* plan, uint32_t*
   uint32_t nonneg = 0;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const float v = values[i];
-    uint32_t b = __float_as_uint(v);
-    if (b == 0x80000000u) b = 0;  // -0.0 == +0.0 under operator>
-    const uint32_t asc = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-    keys[i] = ~asc;  // ascending key order == descending value order
+    if (values.f64) {
+      const double v = values.f64[i];
+      keys[i] = static_cast<uint32_t>(desc_key64(v));
+      nonneg += v >= 0.0 ? 1u : 0u;
+    } else {
+      const float v = values.f32[i];
+      uint32_t b = __float_as_uint(v);
+      if (b == 0x80000000u) b = 0;  // -0.0 == +0.0 under operator>
+      const uint32_t asc = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+      keys[i] = ~asc;  // ascending key order == descending value order
+      nonneg += v >= 0.0f ? 1u : 0u;
+    }
     idx[i] = static_cast<uint32_t>(i);
-    nonneg += v >= 0.0f ? 1u : 0u;
   }
   nonneg = warp_sum(nonneg);
   if ((threadIdx.x & 31) == 0 && nonneg) atomicAdd(&cnt, nonneg);
@@ -84,8 +101,18 @@ __global__ void fit_keys(const float* __restrict__ values, Plan* plan, uint32_t*
   if (threadIdx.x == 0 && cnt) atomicAdd(&plan->sign_split, cnt);
 }
 
+// f64 pass 2 keys: the high words in pass 1's order
+__global__ void fit_keys_hi(const double* __restrict__ v64, const Plan* plan, const uint32_t* __restrict__ idx,
+                            uint32_t* __restrict__ keys, const uint32_t* status) {
+  if (failed(status) || !fit_active(plan)) return;
+  const uint64_t n = plan->n_values;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    keys[i] = static_cast<uint32_t>(desc_key64(v64[idx[i]]) >> 32);
+}
+
 // t[s] and the identity flag; map = sorted idx
-__global__ void fit_prepare(const float* __restrict__ values, const uint32_t* __restrict__ map, Plan* plan,
+__global__ void fit_prepare(const ValSrc values, const uint32_t* __restrict__ map, Plan* plan,
                             double* __restrict__ t, const uint32_t* status) {
   if (failed(status) || !fit_active(plan)) return;
   const uint64_t n = plan->n_values;
@@ -94,7 +121,7 @@ __global__ void fit_prepare(const float* __restrict__ values, const uint32_t* __
   for (uint64_t s = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; s < n;
        s += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     if (map[s] != s) ident = false;
-    t[s] = s < l ? static_cast<double>(values[map[s]]) : -static_cast<double>(values[map[n - 1 - (s - l)]]);
+    t[s] = s < l ? values[map[s]] : -values[map[n - 1 - (s - l)]];
   }
   if (__any_sync(kFull, !ident) && (threadIdx.x & 31) == 0) atomicAnd(&plan->identity, 0u);
 }
@@ -1422,9 +1449,14 @@ void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, 
                        bool dexp) {
   Workspace& w = ctx->ws;
   GP_LAUNCH(ctx, fit_reset, 1, 1, 0, s, w.plan);
-  GP_LAUNCH(ctx, fit_keys, grid_for(ctx, n_bound, 256), 256, 0, s, w.values, w.plan, w.u32a, w.u32b, w.status);
+  const ValSrc vals{w.values, ctx->vals64};
+  GP_LAUNCH(ctx, fit_keys, grid_for(ctx, n_bound, 256), 256, 0, s, vals, w.plan, w.u32a, w.u32b, w.status);
   launch_radix_sort(ctx, w.u32a, w.u32b, w.u32c, w.u32d, &w.plan->n_values, n_bound, 32, s);
-  GP_LAUNCH(ctx, fit_prepare, grid_for(ctx, n_bound, 256), 256, 0, s, w.values, w.u32b, w.plan, w.f64b, w.status);
+  if (ctx->vals64) {  // the high words, stable on top of the low-word order
+    GP_LAUNCH(ctx, fit_keys_hi, grid_for(ctx, n_bound, 256), 256, 0, s, ctx->vals64, w.plan, w.u32b, w.u32a, w.status);
+    launch_radix_sort(ctx, w.u32a, w.u32b, w.u32c, w.u32d, &w.plan->n_values, n_bound, 32, s);
+  }
+  GP_LAUNCH(ctx, fit_prepare, grid_for(ctx, n_bound, 256), 256, 0, s, vals, w.u32b, w.plan, w.f64b, w.status);
   if (dexp) {
     GP_LAUNCH(ctx, dexp_fit, 2, kDexpBlock, 0, s, w.plan, w.f64b, w.seg_end, w.coeffs, w.status);
     GP_LAUNCH(ctx, dexp_decide, 1, 1, 0, s, w.plan, w.status);

@@ -24,7 +24,7 @@ namespace gp {
 
 namespace {
 
-__global__ void quant_scales(const float* __restrict__ values, Plan* plan, uint8_t* out, uint32_t bucket,
+__global__ void quant_scales(const ValSrc values, Plan* plan, uint8_t* out, uint32_t bucket,
                              uint32_t* __restrict__ zlen, const uint32_t* status) {
   if (failed(status)) return;
   const uint64_t n = plan->n_values;
@@ -34,12 +34,12 @@ __global__ void quant_scales(const float* __restrict__ values, Plan* plan, uint8
   const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
   for (uint64_t b = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; b < nb; b += warps) {
     const uint64_t lo = b * bucket, hi = lo + bucket < n ? lo + bucket : n;
-    float mx = 0.0f;  // max |v| of f32 values: exact, as the reference's f64 max
-    for (uint64_t i = lo + lane; i < hi; i += 32) mx = fmaxf(mx, fabsf(values[i]));
+    double mx = 0.0;  // cwiseAbs().maxCoeff() (codecs.cpp:306)
+    for (uint64_t i = lo + lane; i < hi; i += 32) mx = fmax(mx, fabs(values[i]));
 #pragma unroll
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
     if (lane == 0) {
-      const float scale = __double2float_rn(2.0 * static_cast<double>(mx));
+      const float scale = __double2float_rn(2.0 * mx);
       st_u32_unaligned(p + 4 * b, __float_as_uint(scale));
       zlen[b] = scale > 0.0f ? 0u : static_cast<uint32_t>(hi - lo);
     }
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(1024) quant_zscan(const Plan* plan, uint32_t b
   }
 }
 
-__global__ void quant_codes(const float* __restrict__ values, const Plan* plan, const uint8_t* __restrict__ out,
+__global__ void quant_codes(const ValSrc values, const Plan* plan, const uint8_t* __restrict__ out,
                             uint32_t bits, uint32_t bucket, const uint32_t* __restrict__ zbefore,
                             uint32_t* __restrict__ codes, const uint32_t* status) {
   if (failed(status)) return;
@@ -80,7 +80,7 @@ __global__ void quant_codes(const float* __restrict__ values, const Plan* plan, 
     const float scale = __uint_as_float(ld_u32_unaligned(sp + 4 * b));
     uint64_t code = 0;
     if (scale > 0.0f) {
-      double u = __dmul_rn(__dadd_rn(__ddiv_rn(static_cast<double>(values[i]), static_cast<double>(scale)), 0.5), lv);
+      double u = __dmul_rn(__dadd_rn(__ddiv_rn(values[i], static_cast<double>(scale)), 0.5), lv);
       u = u < 0.0 ? 0.0 : (u > lv ? lv : u);
       const double lo = floor(u);
       const double frac = __dsub_rn(u, lo);
@@ -166,13 +166,13 @@ __global__ void quant_values(const uint8_t* __restrict__ in, const Plan* plan, d
   }
 }
 
-__global__ void slot_encode(const float* __restrict__ values, Plan* plan, uint8_t* out, const uint32_t* status) {
+__global__ void slot_encode(const ValSrc values, Plan* plan, uint8_t* out, const uint32_t* status) {
   if (failed(status)) return;
   const uint64_t n = plan->n_values;
   uint8_t* p = out + 49 + plan->il;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    st_u32_unaligned(p + 9 + 4 * i, __float_as_uint(values[i]));
+    st_u32_unaligned(p + 9 + 4 * i, __float_as_uint(__double2float_rn(values[i])));
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     p[0] = 0;  // ByteCodec::Store
     st_u64_unaligned(p + 1, 4 * n);
@@ -202,10 +202,11 @@ __global__ void slot_parse(const uint8_t* __restrict__ in, Plan* plan, uint32_t*
 void launch_values_quant(gp_ctx* ctx, uint8_t* out, int bits, uint32_t bucket, uint64_t n_bound, cudaStream_t s) {
   Workspace& w = ctx->ws;
   const uint64_t nb_bound = (n_bound + bucket - 1) / bucket;
-  GP_LAUNCH(ctx, quant_scales, grid_for(ctx, nb_bound * 32, 256), 256, 0, s, w.values, w.plan, out, bucket, w.u32b,
+  const ValSrc vals{w.values, ctx->vals64};
+  GP_LAUNCH(ctx, quant_scales, grid_for(ctx, nb_bound * 32, 256), 256, 0, s, vals, w.plan, out, bucket, w.u32b,
             w.status);
   GP_LAUNCH(ctx, quant_zscan, 1, 1024, 0, s, w.plan, bucket, w.u32b, w.status);
-  GP_LAUNCH(ctx, quant_codes, grid_for(ctx, n_bound, 256), 256, 0, s, w.values, w.plan, out,
+  GP_LAUNCH(ctx, quant_codes, grid_for(ctx, n_bound, 256), 256, 0, s, vals, w.plan, out,
             static_cast<uint32_t>(bits), bucket, w.u32b, w.u32a, w.status);
   GP_LAUNCH(ctx, quant_pack, grid_for(ctx, (n_bound * bits + 7) / 8, 256), 256, 0, s, w.u32a, w.plan, out,
             static_cast<uint32_t>(bits), bucket, w.status);
@@ -219,7 +220,8 @@ void launch_decode_quant(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, cudaS
 
 void launch_values_slot(gp_ctx* ctx, uint8_t* out, uint64_t n_bound, cudaStream_t s) {
   Workspace& w = ctx->ws;
-  GP_LAUNCH(ctx, slot_encode, grid_for(ctx, n_bound, 256), 256, 0, s, w.values, w.plan, out, w.status);
+  GP_LAUNCH(ctx, slot_encode, grid_for(ctx, n_bound, 256), 256, 0, s, ValSrc{w.values, ctx->vals64}, w.plan, out,
+            w.status);
 }
 
 void launch_decode_slot(gp_ctx* ctx, const uint8_t* in, cudaStream_t s) {
