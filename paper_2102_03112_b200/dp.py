@@ -43,11 +43,24 @@ def _world(group):
     return 1, 0
 
 
+def _ef_mode(ef) -> str | None:
+    """ef: False/None (off), "f64" or True (the reference's precision: the
+    residual is a VectorXd, gradient.hpp:29), "f32" (an f32 residual)."""
+    if ef is True:
+        return "f64"
+    if not ef:
+        return None
+    if ef not in ("f32", "f64"):
+        raise ValueError(f"ef must be False, True, 'f32' or 'f64', not {ef!r}")
+    return ef
+
+
 class SparseAllgather:
-    """One DP worker's encode → exchange → decode step.  ef=True adds the
+    """One DP worker's encode → exchange → decode step.  ef adds the
     reference's memory compensation (TrainConfig::compensation,
     harness.cpp:230, :269-271): the rank encodes g + residual and keeps
-    input - decode(own container) as the next step's residual."""
+    input - decode(own container) as the next step's residual — in f64 as the
+    reference does (ef=True / "f64"), or in f32 (ef="f32")."""
 
     def __init__(self, codec, d: int, r: int, cfg, group=None, device=None, ef: bool = False,
                  graph: bool = False, decode_codecs=None, early_codec=None):
@@ -62,7 +75,9 @@ class SparseAllgather:
         self.sizes = torch.zeros(self.world, dtype=torch.int64, device=dev)
         self.recv = torch.empty(self.world * self.cap, dtype=torch.uint8, device=dev) if self.world > 1 else None
         self.dense = torch.zeros(d, dtype=torch.float32, device=dev)
-        self.residual = torch.zeros(d, dtype=torch.float32, device=dev) if ef else None
+        self.ef = _ef_mode(ef)
+        self.residual = (torch.zeros(d, dtype=torch.float64 if self.ef == "f64" else torch.float32, device=dev)
+                         if self.ef else None)
         # decode_codecs (N > 1, CUDA): extra contexts that decode peers concurrently,
         # each on its own stream, up to the final scatter; the scatters then run
         # in rank order on the step's stream (gp_decode_prepare / gp_decode_finish),
@@ -143,10 +158,7 @@ class SparseAllgather:
         out_dense = self.dense if dense is None else dense
         if self.early is not None:
             return self._step_early(grad, cfg, out_dense, stream)
-        if self.residual is not None:
-            self.codec.encode_ef_into(grad, self.residual, self.r, cfg, self.out, self.length, stream=stream)
-        else:
-            self.codec.encode_into(grad, self.r, cfg, self.out, self.length, stream=stream)
+        self._encode(grad, cfg, stream)
         n = self.world
         # the first container of the mean overwrites the output (zero + accumulate in one pass)
         if n == 1:  # no exchange: the device-side length drives the decode (no host sync)
@@ -169,6 +181,14 @@ class SparseAllgather:
         self._decode_concurrent(n, mx, out_dense, main)
         return out_dense
 
+    def _encode(self, grad, cfg, stream):
+        if self.ef == "f64":
+            self.codec.encode_ef64_into(grad, self.residual, self.r, cfg, self.out, self.length, stream=stream)
+        elif self.ef == "f32":
+            self.codec.encode_ef_into(grad, self.residual, self.r, cfg, self.out, self.length, stream=stream)
+        else:
+            self.codec.encode_into(grad, self.r, cfg, self.out, self.length, stream=stream)
+
     def check(self, stream=None) -> None:
         """Synchronise and raise the first device error latched by any of this
         exchanger's contexts (checksum / payload / capacity errors of a decode,
@@ -187,10 +207,7 @@ class SparseAllgather:
         main = stream if stream is not None else torch.cuda.current_stream()
         self.codec.set_index_event(self.ev_index)
         try:
-            if self.residual is not None:
-                self.codec.encode_ef_into(grad, self.residual, self.r, cfg, self.out, self.length, stream=main)
-            else:
-                self.codec.encode_into(grad, self.r, cfg, self.out, self.length, stream=main)
+            self._encode(grad, cfg, main)
         finally:
             self.codec.set_index_event(None)
         side = self.early_stream

@@ -47,6 +47,13 @@ class OracleCodec:
         length[0] = len(b)
         residual.copy_(torch.from_numpy(res))
 
+    def encode_ef64_into(self, grad, residual, r, cfg, out, length, stream=None):
+        from oracle.bindings import reference
+        res = residual.numpy()  # f64, updated in place by the reference's own loop
+        b = reference().ef_step64(grad.contiguous().numpy(), res, r, self._c(cfg))
+        out[: len(b)] = torch.frombuffer(bytearray(b), dtype=torch.uint8)
+        length[0] = len(b)
+
     def status(self, stream=None):
         pass  # the oracle raises at the call that fails
 
@@ -98,6 +105,20 @@ def _sequential(name, d, r, steps, world, buckets, ef=False):
     o = oracle()
     base = PipelineConfig(**CFGS[name])
     means = []
+    if ef == "f64":  # the reference's own f64 loop (harness.cpp:230-271) through oracle/_ref
+        from oracle.bindings import reference
+        ref = reference()
+        resid64 = [np.zeros(d, np.float64) for _ in range(world)]
+        for step in range(steps):
+            acc = np.zeros(d, np.float32)
+            for w in range(world):
+                g = synthetic_gradient(d, rank=w)
+                c = ref.ef_step64(g, resid64[w], r, OracleCodec._c(PipelineConfig(
+                    **{**base.__dict__, "seed": pipeline_seed(1, w, step)})))
+                _, sup, val = o.decode(c)
+                acc[sup] = np.float32(1.0 / world) * val.astype(np.float32) + acc[sup]
+            means.append(acc)
+        return means
     resid = [np.zeros(d, np.float32) for _ in range(world)]
     for step in range(steps):
         acc = np.zeros(d, np.float32)
@@ -128,8 +149,14 @@ def _sequential(name, d, r, steps, world, buckets, ef=False):
 
 @pytest.mark.parametrize("name,d,r,buckets,ef", [("p2fit", 20_000, 200, 0, False), ("bitmap", 5_000, 50, 0, False),
                                                  ("rle", 7_000, 70, 0, False), ("p2fit", 40_000, 40, 4, False),
-                                                 ("p2fit", 20_000, 200, 0, True), ("bitmap", 40_000, 40, 4, True)])
+                                                 ("p2fit", 20_000, 200, 0, "f32"), ("bitmap", 40_000, 40, 4, "f32"),
+                                                 ("p2fit", 20_000, 200, 0, "f64"), ("rle", 20_000, 200, 0, True)])
 def test_gloo_world2_matches_sequential_harness(name, d, r, buckets, ef):
+    if ef in ("f64", True):
+        from oracle.bindings import reference
+        if reference() is None:
+            pytest.skip("oracle/_ref not built")
+        ef = "f64"
     world, steps = 2, 3 if ef else 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()

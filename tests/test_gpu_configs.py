@@ -24,7 +24,8 @@ import pytest
 from golden_util import coeff_close, load, parse_fit, repack, sha, split
 
 GOLD = load()
-CASES = sorted(k for k in GOLD if not k.startswith("_"))
+CASES = sorted(k for k in GOLD if not k.startswith("_") and "ef_steps" not in GOLD[k])
+EF_CASES = sorted(k for k in GOLD if not k.startswith("_") and "ef_steps" in GOLD[k])
 
 
 def _run(name, oracle):
@@ -90,3 +91,32 @@ def _run(name, oracle):
 @pytest.mark.parametrize("name", CASES)
 def test_config_parity(name, oracle):
     _run(name, oracle)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", EF_CASES)
+def test_config_ef_parity(name):
+    """Error feedback at the C4 size in the reference's own f64 loop
+    (harness.cpp:230-271): every step's container and the residual after it
+    are bit-identical to the reference build's (tools/make_config_goldens.py)."""
+    import torch
+
+    from paper_2102_03112_b200 import Codec, PipelineConfig
+    from paper_2102_03112_b200.configs import CONFIGS, case_input
+
+    gd = GOLD[name]
+    cfg = CONFIGS[gd["config"]]
+    g, r, _ = case_input(cfg)
+    assert sha(g.view(np.uint32)) == gd["input_sha256"]
+    codec = Codec(max_d=gd["d"])
+    try:
+        gdev = torch.from_numpy(g).cuda()
+        e = torch.zeros(gd["d"], dtype=torch.float64, device="cuda")
+        for k, st in enumerate(gd["ef_steps"]):
+            pc = PipelineConfig(index_method=gd["index_method"], value_method=gd["value_method"], fpr=gd["fpr"],
+                                seed=st["seed"])
+            c = codec.compress_ef64(gdev, e, r, pc).cpu().numpy().tobytes()
+            assert sha(c) == st["container_sha256"], f"step {k}: container differs"
+            assert sha(e.cpu().numpy().astype("<f8")) == st["residual_sha256"], f"step {k}: residual differs"
+    finally:
+        codec.close()

@@ -66,6 +66,32 @@ def make(name, cfg_name, bucket, ref):
     return out
 
 
+# error feedback at C4 size in the reference's f64 loop (harness.cpp:230-271):
+# three compensated steps of rank 0 on the same gradient, P2 (eps 1e-3) with
+# raw f32 values, so every step's container and the final residual are
+# bit-exact targets (with a fit value codec the coefficient tolerance feeds
+# into the residual and the next step's selection; tests/test_gpu_ef64.py
+# covers fit EF bit-exactly against the reference loop at 200k elements)
+EF_CASES = [("c4ef_raw", "c4", 3)]
+
+
+def make_ef(name, cfg_name, steps, ref):
+    cfg = CONFIGS[cfg_name]
+    g, r, lo = case_input(cfg)
+    res = np.zeros(g.size, np.float64)
+    out = dict(config=cfg_name, bucket=None, first=lo, d=int(g.size), r=r, index_method=cfg["index"],
+               value_method=0, fpr=cfg["fpr"], degree=cfg["degree"], max_segments=cfg["max_segments"],
+               input_sha256=sha(g.view(np.uint32)), ef_steps=[])
+    for step in range(steps):
+        seed = case_seed(cfg, step=step)
+        cc = GpConfig.make(cfg["index"], 0, fpr=cfg["fpr"], seed=seed)
+        t0 = time.perf_counter()
+        c = ref.ef_step64(g, res, r, cc)
+        out["ef_steps"].append(dict(seed=seed, container_len=len(c), container_sha256=sha(c),
+                                    residual_sha256=sha(res.astype("<f8")), ref_step_s=round(time.perf_counter() - t0, 3)))
+    return out
+
+
 def main(argv):
     ref = reference()
     if ref is None:
@@ -81,6 +107,13 @@ def main(argv):
         gold[name] = make(name, cfg_name, bucket, ref)
         print(name, {k: gold[name][k] for k in ("d", "r", "container_len", "ref_encode_s", "ref_decode_s")},
               flush=True)
+    if not argv:
+        want |= {c[0] for c in EF_CASES}
+    for name, cfg_name, steps in EF_CASES:
+        if name not in want:
+            continue
+        gold[name] = make_ef(name, cfg_name, steps, ref)
+        print(name, gold[name]["ef_steps"], flush=True)
     gold["_meta"] = {"generator": "tools/make_config_goldens.py",
                      "reference": "oracle/_ref/libgpref.so (unmodified /root/reference/proj/src, oracle/Makefile)",
                      "inputs": "paper_2102_03112_b200/inputs.py (rank 0, master seed 1, step 0)"}
