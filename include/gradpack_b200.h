@@ -41,7 +41,8 @@ enum gp_status {
   GP_FIT = 7,                /* gradpack::FitError         errors.hpp:51 */
   GP_CUDA = 8,               /* CUDA runtime failure (no reference equivalent) */
   GP_UNSUPPORTED = 9,        /* method id registered in FORMAT.md but not on this device path */
-  GP_CAPACITY = 10           /* device workspace / output buffer too small */
+  GP_CAPACITY = 10,          /* device workspace / output buffer too small */
+  GP_NCCL = 11               /* NCCL failure / library not loadable (no reference equivalent) */
 };
 
 /* Stable wire ids (container.hpp:23-43, FORMAT.md:46-89). */
@@ -257,6 +258,38 @@ GP_API int gp_volume(const uint8_t* h_container, uint64_t len, gp_volume_report*
 
 /* bloom_params (bloom.cpp:22-31).  Host arithmetic, returns GP_ERROR on bad args. */
 GP_API int gp_bloom_params(double epsilon, uint64_t r, uint64_t* m, uint32_t* k);
+
+/* ---------------------------------------------------------------- data-parallel step
+ * Simulation::step's exchange between real workers (harness.cpp:219-293),
+ * one process (or host thread) per GPU: encode own gradient (with
+ * compensation: gp_encode_topr_ef64 on a device-resident f64 residual), the
+ * container lengths allgathered, ONE host sync on them (and on this rank's
+ * encode status), the containers allgathered padded to the longest, then every
+ * rank's container decoded in rank order into the dense mean
+ * (dense = fmaf(1/N, v, dense), the first overwriting).  Replaces the worker
+ * loop + pairwise mean of harness.cpp:227-284; the mean is the f32 sequential
+ * accumulation (within N ulp(f32) of the reference's f64 pairwise tree).
+ *
+ * gp_dp_unique_id: ncclGetUniqueId (rank 0), to be shared by the caller.
+ * gp_dp_create: NCCL communicator of `nranks` (libnccl.so.2 resolved at run
+ * time), device buffers sized by gp_max_container_bytes(d, r, cfg).
+ * gp_dp_create_local: an in-process group over `nranks` contexts (one host
+ * thread per rank must call gp_dp_step concurrently): the allgathers are
+ * device copies ordered by events — the same step on one GPU.
+ * gp_dp_step: pipeline seed = Simulation::pipeline_seed(seed, rank, step)
+ * (harness.cpp:201-203); d_grad f32[d]; d_mean f32[d] receives the mean.
+ * An encode error is returned at the host sync; the group cannot continue
+ * (peers block in the exchange), as an exception ends the reference's loop. */
+#define GP_DP_UNIQUE_ID_BYTES 128
+typedef struct gp_dp gp_dp;
+GP_API int gp_dp_unique_id(uint8_t* out_id);
+GP_API int gp_dp_create(gp_ctx* ctx, const uint8_t* id, int nranks, int rank, uint64_t d, uint64_t r,
+                        const gp_pipeline_config* cfg, int ef, gp_dp** out);
+GP_API int gp_dp_create_local(gp_ctx** ctxs, int nranks, uint64_t d, uint64_t r, const gp_pipeline_config* cfg,
+                              int ef, gp_dp** out);
+GP_API int gp_dp_step(gp_dp* dp, const float* d_grad, uint64_t seed, int step, float* d_mean, void* stream);
+GP_API const double* gp_dp_residual(const gp_dp* dp);
+GP_API int gp_dp_destroy(gp_dp* dp);
 
 #ifdef __cplusplus
 }  /* extern "C" */

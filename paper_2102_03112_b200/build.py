@@ -20,7 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
-SOURCES = ["capi.cu", "topr.cu", "container.cu", "indexcodec.cu", "values.cu", "bloom.cu", "p2.cu", "p1.cu", "rle.cu", "sort.cu", "values_fit.cu", "values_quant.cu", "huffman.cu", "inflate.cu", "dense.cu", "topr64.cu", "volume.cpp"]
+SOURCES = ["capi.cu", "topr.cu", "container.cu", "indexcodec.cu", "values.cu", "bloom.cu", "p2.cu", "p1.cu", "rle.cu", "sort.cu", "values_fit.cu", "values_quant.cu", "huffman.cu", "inflate.cu", "dense.cu", "topr64.cu", "volume.cpp", "dp_exchange.cpp"]
 
 
 def _run(cmd):
@@ -69,15 +69,20 @@ CLI_SRC = os.path.join(HERE, "..", "tests", "cpp", "gp_cli.cpp")
 CLI_OUT = os.path.join(HERE, "..", "tests", "cpp", "gp_cli")
 
 
+CPP_TESTS = ["gp_cli", "dp_test"]  # tests/cpp/<name>.cpp → tests/cpp/<name>
+
+
 def build_cli() -> str:
-    """The C++ host program over include/gradpack_b200.hpp (tests/test_gpu_cpp.py)."""
-    hdr = os.path.join(HERE, "..", "include", "gradpack_b200.hpp")
-    if (os.path.exists(CLI_OUT) and os.path.getmtime(CLI_OUT) > os.path.getmtime(CLI_SRC)
-            and os.path.getmtime(CLI_OUT) > os.path.getmtime(hdr) and os.path.getmtime(CLI_OUT) > os.path.getmtime(OUT)):
-        return CLI_OUT
-    _run(["g++", "-std=c++17", "-O2", "-I/usr/local/cuda/include", CLI_SRC, "-o", CLI_OUT, f"-L{HERE}",
-          "-lgradpack_b200", "-L/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{HERE}",
-          "-Wl,-rpath,/usr/local/cuda/lib64"])
+    """The C++ host programs over include/gradpack_b200.h(pp) (tests/test_gpu_cpp*.py)."""
+    hdrs = [os.path.join(HERE, "..", "include", h) for h in ("gradpack_b200.hpp", "gradpack_b200.h")]
+    for name in CPP_TESTS:
+        src = os.path.join(HERE, "..", "tests", "cpp", name + ".cpp")
+        out = os.path.join(HERE, "..", "tests", "cpp", name)
+        if (os.path.exists(out) and all(os.path.getmtime(out) > os.path.getmtime(p) for p in [src, OUT, *hdrs])):
+            continue
+        _run(["g++", "-std=c++17", "-O2", "-pthread", "-I/usr/local/cuda/include", src, "-o", out, f"-L{HERE}",
+              "-lgradpack_b200", "-L/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{HERE}",
+              "-Wl,-rpath,/usr/local/cuda/lib64"])
     return CLI_OUT
 
 
