@@ -20,7 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
-SOURCES = ["capi.cu", "topr.cu", "container.cu", "indexcodec.cu", "values.cu", "bloom.cu", "p2.cu", "p1.cu", "rle.cu", "sort.cu", "values_fit.cu", "values_quant.cu", "huffman.cu", "inflate.cu", "dense.cu", "topr64.cu", "volume.cpp", "dp_exchange.cpp"]
+SOURCES = ["capi.cu", "topr.cu", "container.cu", "indexcodec.cu", "values.cu", "bloom.cu", "p2.cu", "p1.cu", "rle.cu", "sort.cu", "values_fit.cu", "values_quant.cu", "huffman.cu", "inflate.cu", "dense.cu", "topr64.cu", "deflate.cu", "volume.cpp", "dp_exchange.cpp"]
 
 
 def _run(cmd):

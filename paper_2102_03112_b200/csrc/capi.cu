@@ -444,7 +444,7 @@ uint64_t gp_max_container_bytes(uint64_t d, uint64_t r, const gp_pipeline_config
       vl = 5 + 4 * ((n + bucket - 1) / bucket) + (n * bits + 7) / 8;
       break;
     }
-    case GP_VALUE_DEFLATE_SLOT: vl = 9 + 4 * n; break;
+    case GP_VALUE_DEFLATE_SLOT: vl = cfg->slot_codec == 1 ? deflate_slot_bound(n) : 9 + 4 * n; break;
     default: vl = 4 * n; break;
   }
   return 49 + il + vl + rl + 4;
@@ -484,10 +484,8 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
     if (cfg->quant_bits < 1 || cfg->quant_bits > 16) return set_error(ctx, GP_ERROR, "quantize: bits out of range [1, 16]");
     if (cfg->quant_bucket < 1) return set_error(ctx, GP_ERROR, "quantize: bucket must be >= 1");
   }
-  if (vm == GP_VALUE_DEFLATE_SLOT) {
-    if (cfg->slot_codec == 1) return set_error(ctx, GP_UNSUPPORTED, "the deflate byte codec is not on the device path");
-    if (cfg->slot_codec != 0) return set_error(ctx, GP_UNKNOWN_METHOD, "byte_compress: unknown codec id");
-  }
+  if (vm == GP_VALUE_DEFLATE_SLOT && cfg->slot_codec > 1)
+    return set_error(ctx, GP_UNKNOWN_METHOD, "byte_compress: unknown codec id");
   const uint64_t bound = gp_max_container_bytes(d, r, cfg);
   if (cap < bound) return set_error(ctx, GP_CAPACITY, "encode: output capacity below gp_max_container_bytes");
 
@@ -578,7 +576,12 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
       GP_STAGE(ctx, ST_VALUES, s,
                launch_values_quant(ctx, d_out, cfg->quant_bits, cfg->quant_bucket, n_bound, s));
       break;
-    case GP_VALUE_DEFLATE_SLOT: launch_values_slot(ctx, d_out, n_bound, s); break;
+    case GP_VALUE_DEFLATE_SLOT:
+      if (cfg->slot_codec == 1)
+        GP_STAGE(ctx, ST_VALUES, s, launch_values_deflate(ctx, d_out, n_bound, s));
+      else
+        launch_values_slot(ctx, d_out, n_bound, s);
+      break;
     default: break;
   }
   if (nz) {

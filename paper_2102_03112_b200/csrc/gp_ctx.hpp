@@ -275,6 +275,8 @@ void launch_values_quant(gp_ctx* ctx, uint8_t* out, int bits, uint32_t bucket, u
                          cudaStream_t s);                                                            // values_quant.cu
 void launch_decode_quant(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, cudaStream_t s);
 void launch_values_slot(gp_ctx* ctx, uint8_t* out, uint64_t n_bound, cudaStream_t s);
+void launch_values_deflate(gp_ctx* ctx, uint8_t* out, uint64_t n_bound, cudaStream_t s);  // deflate.cu
+uint64_t deflate_slot_bound(uint64_t n);
 void launch_decode_slot(gp_ctx* ctx, const uint8_t* in, cudaStream_t s);
 void launch_decode_inflate(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, cudaStream_t s);
 void launch_decode_scatter(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, float* dense, uint64_t dense_d,

@@ -100,11 +100,3 @@ def test_decode_error_classes_match_oracle(codec, oracle):
             assert got == want, (vm, kw, got, want)
             if want is not None:
                 assert float(dense.abs().sum()) == 0.0
-
-
-def test_deflate_slot_is_unsupported(codec):
-    from paper_2102_03112_b200 import PipelineConfig
-    from paper_2102_03112_b200.api import UnsupportedMethodError
-    g = torch.from_numpy(synthetic_gradient(1000, rank=1)).cuda()
-    with pytest.raises(UnsupportedMethodError):
-        codec.compress(g, 10, PipelineConfig(index_method=BITMAP, value_method=SLOT, slot_codec=1))
