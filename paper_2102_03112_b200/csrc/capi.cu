@@ -178,7 +178,7 @@ void carve(Workspace& w, uint8_t* base, uint64_t D) {
   w.scan_base = c.take<uint8_t>(128 + w.tiles_cap * 8);
   w.ticket = reinterpret_cast<uint32_t*>(w.scan_base);
   w.tiles = reinterpret_cast<uint64_t*>(w.scan_base ? w.scan_base + 128 : nullptr);
-  w.hist = c.take<uint32_t>(65536);
+  w.hist = c.take<uint32_t>(32768 + 256 + 65536 + 256);
   w.cand_idx = c.take<uint32_t>(D);
   w.cand_val = c.take<float>(D);
   w.support = c.take<uint32_t>(D);

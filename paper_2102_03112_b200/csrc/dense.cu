@@ -173,7 +173,10 @@ __global__ void __launch_bounds__(kNzBlock) nz_encode(const float* __restrict__ 
     const uint64_t b0 = static_cast<uint64_t>(tile) * (kNzTile / 8);
     const uint64_t nb = b0 + kNzTile / 8 <= bm_bytes ? kNzTile / 8 : bm_bytes - b0;
     block_store_bytes(bm_out + b0, words[b], nb);
-    block_store_bytes(val_out + 4 * tile_prefix, vals[b], 4ull * tile_total);
+    // the container holds r values: a tile past them (nnz > r, the speculation
+    // fails and the general path rewrites every byte) must not write beyond
+    const uint64_t keep = tile_prefix >= r ? 0 : (r - tile_prefix < tile_total ? r - tile_prefix : tile_total);
+    block_store_bytes(val_out + 4 * tile_prefix, vals[b], 4ull * keep);
     if (tile == ntiles - 1 && threadIdx.x == 0) {
       const uint64_t nnz = tile_prefix + tile_total;
       if (nnz == r) {

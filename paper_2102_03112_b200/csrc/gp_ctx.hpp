@@ -33,6 +33,8 @@ struct Plan {
   uint32_t thresh, tie_cut;     // exact threshold key; last kept index among ties
   uint64_t above, n_cand;       // keys in bins above bin_star; candidates emitted
   uint64_t thresh64;            // f64 input (topr64.cu): exact threshold key
+  uint64_t tie_q;               // keep the first tie_q keys == thresh (index order)
+  uint32_t tie_all, pad2;       // every key == thresh is kept
   // ---- bloom
   uint64_t m, seed_a, seed_b, minv;
   uint64_t seed;                // the pipeline seed of this encode
@@ -75,7 +77,7 @@ struct Workspace {
   uint32_t* ticket = nullptr;     // 32 tickets (first 128 B of scan_base)
   uint64_t* tiles = nullptr;      // scan tile descriptors
   size_t tiles_cap = 0;
-  uint32_t* hist = nullptr;       // 65536 bins
+  uint32_t* hist = nullptr;       // 32768 bins of key >> 16 + 65536 low-bit bins of the threshold bin
   uint32_t* cand_idx = nullptr;   // [D]
   float* cand_val = nullptr;      // [D]
   uint32_t* support = nullptr;    // [D]

@@ -183,6 +183,57 @@ __device__ __forceinline__ uint64_t lookback_warp(uint64_t* tiles, uint32_t tile
   return exclusive;
 }
 
+// The same with kW descriptors per lane per round (32 kW predecessors per L2
+// round trip), for passes whose tiles all run in one wave: every tile then
+// looks back at once and the nearest inclusive prefix trails by up to the
+// whole grid, so the walk length, not the work, sets the pass time.
+template <int kW>
+__device__ __forceinline__ uint64_t lookback_warp_wide(uint64_t* tiles, uint32_t tile, uint64_t aggregate) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) st_volatile(&tiles[0], kFlagInc | aggregate);
+    return 0;
+  }
+  if (lane == 0) st_volatile(&tiles[tile], kFlagAgg | aggregate);
+  uint64_t exclusive = 0;
+  int64_t base = static_cast<int64_t>(tile) - 1;
+  while (true) {
+    uint64_t s[kW];  // lane l, slot k: predecessor base - (kW l + k), nearest first
+#pragma unroll
+    for (int k = 0; k < kW; ++k) {
+      const int64_t idx = base - (kW * lane + k);
+      s[k] = idx >= 0 ? ld_volatile(&tiles[idx]) : kFlagInc;
+    }
+    bool pending = false;
+#pragma unroll
+    for (int k = 0; k < kW; ++k) pending |= (s[k] >> 62) == 0;
+    while (__any_sync(kFull, pending)) {
+      pending = false;
+#pragma unroll
+      for (int k = 0; k < kW; ++k)
+        if ((s[k] >> 62) == 0) {
+          s[k] = ld_volatile(&tiles[base - (kW * lane + k)]);
+          pending |= (s[k] >> 62) == 0;
+        }
+    }
+    int kin = kW;
+#pragma unroll
+    for (int k = kW - 1; k >= 0; --k)
+      if ((s[k] >> 62) == 2) kin = k;
+    const unsigned inc_mask = __ballot_sync(kFull, kin < kW);
+    const int first = inc_mask ? __ffs(inc_mask) - 1 : 32;
+    uint64_t v = 0;
+#pragma unroll
+    for (int k = 0; k < kW; ++k)
+      if (lane < first || (lane == first && k <= kin)) v += s[k] & kValMask;
+    exclusive += warp_sum(v);
+    if (inc_mask) break;
+    base -= 32 * kW;
+  }
+  if (lane == 0) st_volatile(&tiles[tile], kFlagInc | (exclusive + aggregate));
+  return exclusive;
+}
+
 // Claim the next tile (thread 0) and broadcast it through shared memory.
 __device__ __forceinline__ uint32_t claim_tile(uint32_t* ticket, uint32_t* smem_slot) {
   __syncthreads();
@@ -275,6 +326,30 @@ __device__ __forceinline__ void st_u32_unaligned(uint8_t* p, uint32_t v) {
 __device__ __forceinline__ void st_u64_unaligned(uint8_t* p, uint64_t v) {
   st_u32_unaligned(p, static_cast<uint32_t>(v));
   st_u32_unaligned(p + 4, static_cast<uint32_t>(v >> 32));
+}
+
+// 16-byte loads with an L2 eviction-priority hint: evict_last for data a later
+// pass of the same step reads again (kept in the 126 MB L2), evict_first for
+// its last use.
+__device__ __forceinline__ float4 ld_f4_keep(const float4* p) {
+  float4 v;
+  asm volatile(
+      "{\n\t.reg .b64 pol;\n\t"
+      "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+      "ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], pol;\n\t}"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float4 ld_f4_last(const float4* p) {
+  float4 v;
+  asm volatile(
+      "{\n\t.reg .b64 pol;\n\t"
+      "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+      "ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], pol;\n\t}"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "l"(p));
+  return v;
 }
 
 // The value sequence an encode hands to the value codec: f32 (top-r of an f32

@@ -81,13 +81,13 @@ def test_bucketed_step_is_bucketwise():
 
 
 def test_dp_step_with_error_feedback_matches_oracle(oracle):
-    """ef=True: three compensated steps at N = 1 against the oracle's worker loop."""
+    """ef="f32": three compensated steps at N = 1 against the oracle's f32 worker loop."""
     from oracle.ef import ef_step
     from paper_2102_03112_b200 import Codec
     from paper_2102_03112_b200.dp import SparseAllgather, pipeline_seed
     d, r = 250_000, 2_500
     codec = Codec(max_d=d)
-    ex = SparseAllgather(codec, d, r, _pcfg(P2, V_NONE, fpr=0.001), ef=True)
+    ex = SparseAllgather(codec, d, r, _pcfg(P2, V_NONE, fpr=0.001), ef="f32")
     e = np.zeros(d, np.float32)
     for step in range(3):
         g = synthetic_gradient(d, rank=step)
@@ -134,3 +134,24 @@ def test_concurrent_peer_decode_equals_sequential():
     for c in ex.dec:
         c.status()
     assert torch.equal(got, want)
+
+
+def test_dp_step_with_f64_error_feedback_matches_the_reference_loop(reference):
+    """ef=True (f64, the reference's precision): three compensated steps at N = 1
+    bit-identical to the reference build's own loop (harness.cpp:230-271)."""
+    from paper_2102_03112_b200 import Codec
+    from paper_2102_03112_b200.dp import SparseAllgather, pipeline_seed
+    d, r = 250_000, 2_500
+    codec = Codec(max_d=d)
+    ex = SparseAllgather(codec, d, r, _pcfg(P2, V_NONE, fpr=0.001), ef=True)
+    e = np.zeros(d, np.float64)
+    try:
+        for step in range(3):
+            g = synthetic_gradient(d, rank=step)
+            ex.step(torch.from_numpy(g).cuda(), step=step)
+            codec.status()
+            c = reference.ef_step64(g, e, r, GpConfig.make(P2, V_NONE, fpr=0.001, seed=pipeline_seed(1, 0, step)))
+            assert bytes(ex.out[: int(ex.length.item())].cpu().numpy()) == c
+            assert np.array_equal(ex.residual.cpu().numpy(), e)
+    finally:
+        codec.close()

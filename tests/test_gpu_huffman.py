@@ -94,7 +94,7 @@ def test_huffman_in_dp_graph_and_ef(oracle):
     from paper_2102_03112_b200.dp import SparseAllgather, pipeline_seed
     d, r = 120_000, 1_500
     codec = Codec(max_d=d)
-    ex = SparseAllgather(codec, d, r, PipelineConfig(index_method=3, value_method=0), ef=True, graph=True)
+    ex = SparseAllgather(codec, d, r, PipelineConfig(index_method=3, value_method=0), ef="f32", graph=True)
     g = torch.empty(d, dtype=torch.float32, device="cuda")
     e = np.zeros(d, np.float32)
     for step in range(3):
