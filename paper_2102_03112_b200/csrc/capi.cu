@@ -199,6 +199,7 @@ void carve(Workspace& w, uint8_t* base, uint64_t D) {
   w.p2_sets = c.take<uint32_t>(w.set_cap);
   w.p2_table = c.take<uint32_t>(256 * (w.set_cap / 4096 + 1) + 256);
   w.pairs = c.take<uint32_t>(w.pair_cap);
+  w.p2_rank = c.take<uint32_t>(w.pair_cap);
   w.p2_members = c.take<uint32_t>(w.pair_cap);
   w.first_touch = c.take<uint32_t>(D);
   w.u32a = c.take<uint32_t>(D);

@@ -102,6 +102,7 @@ struct Workspace {
   uint32_t* bucket = nullptr;     // per-bit counters [m_cap + 1]
   uint32_t* bucket_off = nullptr; // per-bit offsets [m_cap + 1]
   uint32_t* pairs = nullptr;      // conflict pairs [pair_cap]
+  uint32_t* p2_rank = nullptr;    // each pair's slot in its set [pair_cap]
   uint64_t pair_cap = 0;
   uint32_t* set_bit = nullptr;    // multi-member sets (bit) [m_cap]
   uint32_t* set_key = nullptr;    // sort keys [m_cap]

@@ -65,7 +65,7 @@ __global__ void p2_zero_counts(Plan* plan, uint32_t* count, uint64_t m_cap, cons
 template <int KM, bool kSmallM>
 __device__ __forceinline__ void pairs_body(const uint32_t* __restrict__ P, uint64_t n, uint32_t k, const FastMod& fm,
                                            uint64_t sa, uint64_t sb, uint32_t* __restrict__ pairs,
-                                           uint32_t* __restrict__ count) {
+                                           uint32_t* __restrict__ rank, uint32_t* __restrict__ count) {
   for (uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; p < n;
        p += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t x = P[p];
@@ -83,7 +83,7 @@ __device__ __forceinline__ void pairs_body(const uint32_t* __restrict__ P, uint6
         for (int i = 0; i < j; ++i) dup |= seen[i] == bit;
         seen[j] = bit;
         pairs[p * k + j] = dup ? 0xFFFFFFFFu : bit;
-        if (!dup) atomicAdd(&count[bit], 1u);
+        if (!dup) rank[p * k + j] = atomicAdd(&count[bit], 1u);  // the pair's slot in its set
       }
     }
   }
@@ -95,7 +95,7 @@ __device__ __forceinline__ void pairs_body(const uint32_t* __restrict__ P, uint6
 // group has the same bit.
 __device__ __forceinline__ void pairs_lanes(const uint32_t* __restrict__ P, uint64_t n, uint32_t k, const FastMod& fm,
                                             uint64_t sa, uint64_t sb, uint32_t* __restrict__ pairs,
-                                            uint32_t* __restrict__ count) {
+                                            uint32_t* __restrict__ rank, uint32_t* __restrict__ count) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t per = 32 / k;                 // positives per warp
   const uint32_t g = lane / k, j = lane - g * k;
@@ -117,7 +117,7 @@ __device__ __forceinline__ void pairs_lanes(const uint32_t* __restrict__ P, uint
     const bool dup = (peers & ((1u << lane) - 1u)) != 0u;
     if (ok) {
       pairs[p * k + j] = dup ? 0xFFFFFFFFu : bit;
-      if (!dup) atomicAdd(&count[bit], 1u);
+      if (!dup) rank[p * k + j] = atomicAdd(&count[bit], 1u);  // the pair's slot in its set
     }
   }
 }
@@ -126,7 +126,8 @@ __device__ __forceinline__ void pairs_lanes(const uint32_t* __restrict__ P, uint
 // form, each exits unless k is in its range (k is only known on the device).
 template <bool kWide>
 __global__ void p2_pairs(const uint32_t* __restrict__ P, Plan* plan, uint32_t* __restrict__ pairs,
-                         uint32_t* __restrict__ count, uint64_t pair_cap, uint64_t set_cap, uint32_t* status) {
+                         uint32_t* __restrict__ rank, uint32_t* __restrict__ count, uint64_t pair_cap,
+                         uint64_t set_cap, uint32_t* status) {
   if (failed(status) || !p2_active(plan) || (plan->k > 32) != kWide) return;
   const uint64_t n = plan->n_pos, m = plan->m;
   const uint32_t k = plan->k;
@@ -137,9 +138,9 @@ __global__ void p2_pairs(const uint32_t* __restrict__ P, Plan* plan, uint32_t* _
   const FastMod fm{m, plan->minv};
   const uint64_t sa = plan->seed_a + kGamma, sb = plan->seed_b + kGamma;
   if (kWide)
-    pairs_body<64, false>(P, n, k, fm, sa, sb, pairs, count);
+    pairs_body<64, false>(P, n, k, fm, sa, sb, pairs, rank, count);
   else
-    pairs_lanes(P, n, k, fm, sa, sb, pairs, count);
+    pairs_lanes(P, n, k, fm, sa, sb, pairs, rank, count);
   if (blockIdx.x == 0 && threadIdx.x == 0) plan->n_pairs = n * k;
 }
 
@@ -192,8 +193,8 @@ __global__ void __launch_bounds__(kTileBlock) p2_tiles(const uint32_t* __restric
     for (int q = 0; q < kTileItems; ++q) {
       if (c[q]) {
         const uint64_t b = tile * kTile + static_cast<uint64_t>(q) * kTileBlock + threadIdx.x;
+        slot[b] = o | (c[q] == 1 ? kSingleton : 0u);  // bucket start; a pair's rank places it
         o += c[q];
-        slot[b] = o | (c[q] == 1 ? kSingleton : 0u);  // end of the bucket; the scatter counts down
       }
     }
     table[threadIdx.x * ntiles + tile] = h[threadIdx.x];
@@ -201,12 +202,14 @@ __global__ void __launch_bounds__(kTileBlock) p2_tiles(const uint32_t* __restric
   }
 }
 
-// One thread per positive p and its k pairs: a size-1 set's member is
-// selected in stage A (every singleton is visited first, p2_select pass 1;
-// plain byte flags, idempotent) and recorded in single[]; multi-set members
-// go to their bucket (arbitrary order, sorted later).
-__global__ void p2_scatter(const uint32_t* __restrict__ pairs, const Plan* plan, uint32_t* slot,
-                           uint32_t* __restrict__ members, uint8_t* __restrict__ flags, const uint32_t* status) {
+// One thread per pair: a size-1 set's member is selected in stage A (every
+// singleton is visited first, p2_select pass 1; plain byte flags,
+// idempotent); every member goes to bucket start + its rank (the slot
+// p2_pairs' count atomic handed out) — no atomics here.  Buckets stay
+// unsorted: the engine ranks members by value.
+__global__ void p2_scatter(const uint32_t* __restrict__ pairs, const uint32_t* __restrict__ rank, const Plan* plan,
+                           const uint32_t* __restrict__ slot, uint32_t* __restrict__ members,
+                           uint8_t* __restrict__ flags, const uint32_t* status) {
   if (failed(status) || !p2_active(plan)) return;
   const uint64_t n = plan->n_pos;
   const uint32_t k = plan->k;
@@ -215,17 +218,21 @@ __global__ void p2_scatter(const uint32_t* __restrict__ pairs, const Plan* plan,
   // kU pairs per thread per step, strided by the grid: kU independent chains in flight
   constexpr int kU = 8;
   for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i0 < np; i0 += kU * stride) {
-    uint32_t bit[kU], v[kU];
+    uint32_t bit[kU], v[kU], rk[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) bit[u] = i0 + u * stride < np ? pairs[i0 + u * stride] : 0xFFFFFFFFu;
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t i = i0 + u * stride;
+      bit[u] = i < np ? pairs[i] : 0xFFFFFFFFu;
+      rk[u] = i < np ? rank[i] : 0u;
+    }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) v[u] = bit[u] != 0xFFFFFFFFu ? atomicSub(&slot[bit[u]], 1u) : 0u;
+    for (int u = 0; u < kU; ++u) v[u] = bit[u] != 0xFFFFFFFFu ? slot[bit[u]] : 0u;
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       if (bit[u] == 0xFFFFFFFFu) continue;
       const uint64_t i = i0 + u * stride;
       const uint32_t p = static_cast<uint32_t>(np < (1ull << 32) ? static_cast<uint32_t>(i) / k : i / k);
-      members[(v[u] & ~kSingleton) - 1u] = p;
+      members[(v[u] & ~kSingleton) + rk[u]] = p;
       if (v[u] & kSingleton) flags[p] = 1;  // flags were zeroed; every writer stores the same value
     }
   }
@@ -634,16 +641,16 @@ void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t 
   const uint64_t m_cap = std::min<uint64_t>(m_bound, w.set_cap);
   GP_LAUNCH(ctx, p2_zero_counts, ctx->sm_count * 4, 256, 0, s, w.plan, w.p2_count, m_cap, w.status);
   cudaMemsetAsync(w.p2_alloc, 0, sizeof(uint32_t), s);
-  GP_LAUNCH(ctx, p2_pairs<false>, grid_for(ctx, n_bound * 32, 256), 256, 0, s, w.pos, w.plan, w.pairs, w.p2_count, w.pair_cap,
-            w.set_cap, w.status);
-  GP_LAUNCH(ctx, p2_pairs<true>, grid_for(ctx, n_bound, 128), 128, 0, s, w.pos, w.plan, w.pairs, w.p2_count, w.pair_cap,
-            w.set_cap, w.status);
+  GP_LAUNCH(ctx, p2_pairs<false>, grid_for(ctx, n_bound * 32, 256), 256, 0, s, w.pos, w.plan, w.pairs, w.p2_rank,
+            w.p2_count, w.pair_cap, w.set_cap, w.status);
+  GP_LAUNCH(ctx, p2_pairs<true>, grid_for(ctx, n_bound, 128), 128, 0, s, w.pos, w.plan, w.pairs, w.p2_rank,
+            w.p2_count, w.pair_cap, w.set_cap, w.status);
   const uint64_t mtiles = (m_cap + kTile - 1) / kTile;
   const int tgrid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(mtiles, ctx->sm_count * 8ULL)));
   GP_LAUNCH(ctx, p2_tiles, tgrid, kTileBlock, 0, s, w.p2_count, w.plan, w.p2_off, w.p2_table, w.p2_alloc, w.status);
   cudaMemsetAsync(w.flags, 0, n_bound, s);
-  GP_LAUNCH(ctx, p2_scatter, grid_for(ctx, n_bound * k_bound, 256), 256, 0, s, w.pairs, w.plan, w.p2_off, w.p2_members,
-            w.flags, w.status);
+  GP_LAUNCH(ctx, p2_scatter, grid_for(ctx, n_bound * k_bound, 256), 256, 0, s, w.pairs, w.p2_rank, w.plan, w.p2_off,
+            w.p2_members, w.flags, w.status);
   launch_table_scan(ctx, w.p2_table, &w.plan->m, m_cap, 12, s);
   GP_LAUNCH(ctx, p2_count_sets, 1, 32, 0, s, w.plan, w.p2_table, w.status);
   GP_LAUNCH(ctx, p2_size_scatter, tgrid, kTileBlock, 0, s, w.plan, w.p2_count, w.p2_table, w.p2_sets, w.status);
