@@ -359,41 +359,44 @@ def native_main(args, cfg):
 
     # roofline of the dominant stage: algorithmic HBM bytes per launch / its event time
     per_launch = {k: (v[0] / v[1], v[1] / args.steps) for k, v in stage.items()}
-    algo_bytes = {  # minimum DRAM bytes a launch must move
-        "topr": 4.0 * d,                  # read the gradient once
+    # minimum DRAM bytes a launch must move (per unit x units per launch)
+    dense_bitmap = cfg["index"] == 1 and cfg["value"] == 0  # bitmap + raw f32: the fused dense paths (dense.cu)
+    nz_path = dense_bitmap and 4 * r_total >= d
+    algo_bytes = {
+        "topr": 4.0 * d + 8.0 * r_total,  # read the gradient once, write support + values
         "pack_crc": float(length),        # read the payloads once
         "dec_parse_crc": float(length),
-        "dec_scatter": 8.0 * r_total,     # read the support, write the values
+        # fused bitmap decode: bitmap + value run in, the whole dense slice out (overwrite mode);
+        # general scatter: support + values in, read-modify-write of the dense support
+        "dec_scatter": (d / 8.0 + 4.0 * r_total + 4.0 * d) if dense_bitmap else 16.0 * r_total,
         "gather": 8.0 * r_total,
         "bloom_scan": d / 8.0 + 8.0 * r_total,      # membership bitmap + positives
         "dec_bloom_scan": d / 8.0 + 8.0 * r_total,
     }
+    if nz_path:  # one pass: the gradient in, bitmap + nonzero values out
+        algo_bytes["index"] = 4.0 * d + d / 8.0 + 4.0 * r_total
     dom = max(stage.items(), key=lambda kv: kv[1][0])[0] if stage else None
     roof = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    traffic_tab, instr_tab = {}, {}
+    traffic_tab = {}
     if os.path.exists(tpath):
         with open(tpath) as f:
-            tt = json.load(f)
-        traffic_tab = tt.get(args.config, {})
-        instr_tab = tt.get(args.config + ":warp_instr", {})
+            traffic_tab = json.load(f).get(args.config, {})
     if dom is not None:
         ms_launch, _ = per_launch[dom]
         ab = algo_bytes.get(dom)
         achieved = (ab / (ms_launch * 1e-3) / 1e9) if ab else None
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 3) if achieved else None,
                 "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 6) if achieved else None,
-                "traffic": traffic_tab.get(dom), "ms_per_launch": round(ms_launch, 5), "peak_kind": peak_kind}
+                "traffic": traffic_tab.get(dom), "ms_per_launch": round(ms_launch, 5), "peak_kind": peak_kind,
+                "algo_bytes": ab}
         if dom in ("bloom_scan", "dec_bloom_scan"):
             roof["keys_per_s"] = round(d / (ms_launch * 1e-3), 1)
-            roof["note"] = ("full-range Bloom membership scan is integer-issue bound (SplitMix64 + 64x32 "
-                            "modulo per probe), not HBM bound: see DESIGN.md")
-            if instr_tab.get(dom):  # warp instructions per launch (ncu, profiles/) over this launch time
-                peak_wi = 148 * 4 * clocks.get("sm_mhz", 1965.0) * 1e6
-                ach = instr_tab[dom] / (ms_launch * 1e-3)
-                roof["issue"] = {"achieved_warp_instr_per_s": round(ach, 1), "peak": peak_wi,
-                                 "frac": round(ach / peak_wi, 4),
-                                 "source": "smsp__inst_executed.sum of the ncu full capture (profiles/r1)"}
+            # the schema's bound is hbm|tensor; this kernel's limiter is neither
+            roof["limiter"] = "integer issue (SplitMix64 + 64x32 modulo per probe)"
+            roof["note"] = ("full-range Bloom membership scan: its HBM fraction is tiny by design; the "
+                            "warp-instruction issue rate of the same kernel is measured by ncu in profiles/ "
+                            "(see DESIGN.md)")
     step_hbm_bytes = 8.0 * d + 2.0 * world * length
     step_roof = {"hbm_bytes": step_hbm_bytes, "t_roof_ms": step_hbm_bytes / (hbm * 1e9) * 1e3,
                  "frac": round(step_hbm_bytes / (hbm * 1e9) / (t_ms * 1e-3), 6)}

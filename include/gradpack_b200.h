@@ -259,6 +259,21 @@ GP_API int gp_volume(const uint8_t* h_container, uint64_t len, gp_volume_report*
 /* bloom_params (bloom.cpp:22-31).  Host arithmetic, returns GP_ERROR on bad args. */
 GP_API int gp_bloom_params(double epsilon, uint64_t r, uint64_t* m, uint32_t* k);
 
+/* Sharded decode index stage (the N > 1 exchange): positive_scan
+ * (bloom.cpp:123-128) of a serialized filter over the coordinate slice
+ * [lo, hi) only — the ascending positives there, global coordinates — so the
+ * N ranks of a step split the scans of all N filters by coordinate range
+ * instead of each scanning every filter over all of [0, d); and the
+ * selection (P0/Pd slice, P1, P2 replay, bloom.cpp:140-222) from a complete
+ * positive list assembled by the caller (d_count: |P| in device memory),
+ * finished by gp_decode_accumulate_own on the same context. */
+GP_API int gp_bloom_scan_range(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter_len, uint64_t d,
+                               uint64_t lo, uint64_t hi, uint32_t* d_positives, uint64_t cap,
+                               uint64_t* d_count, void* stream);
+GP_API int gp_decode_index_from_positions(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter_len, uint64_t d,
+                                          uint64_t r, int index_method, const uint32_t* d_positives,
+                                          const uint64_t* d_count, void* stream);
+
 /* ---------------------------------------------------------------- data-parallel step
  * Simulation::step's exchange between real workers (harness.cpp:219-293),
  * one process (or host thread) per GPU: encode own gradient (with

@@ -76,6 +76,8 @@ _SIGS = {
     "gp_crc32c": ([_vp, _vp, _u64, _vp, _vp], C.c_int),
     "gp_bloom_positive_scan": ([_vp, _vp, _u64, _u64, _vp, _u64, _vp, _vp], C.c_int),
     "gp_bloom_select": ([_vp, _vp, _u64, _u64, _u64, C.c_int, _vp, _vp], C.c_int),
+    "gp_bloom_scan_range": ([_vp, _vp, _u64, _u64, _u64, _u64, _vp, _u64, _vp, _vp], C.c_int),
+    "gp_decode_index_from_positions": ([_vp, _vp, _u64, _u64, _u64, C.c_int, _vp, _vp, _vp], C.c_int),
     "gp_volume": ([_vp, _u64, _P(GpVolume)], C.c_int),
     "gp_bloom_params": ([C.c_double, _u64, _P(_u64), _P(C.c_uint32)], C.c_int),
 }

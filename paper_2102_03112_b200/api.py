@@ -403,6 +403,21 @@ class Codec:
         self.status()
         return out[: int(count.item())]
 
+    def bloom_scan_range_into(self, filt: torch.Tensor, d: int, lo: int, hi: int, out: torch.Tensor,
+                              count: torch.Tensor, stream=None):
+        """Asynchronous positive_scan of a serialized filter over [lo, hi) only:
+        the ascending positives (global coordinates) to ``out`` (int32), their
+        number to ``count`` (int64, device)."""
+        self._raise(lib.gp_bloom_scan_range(self._ctx, _ptr(filt), filt.numel(), d, lo, hi, _ptr(out), out.numel(),
+                                            _ptr(count), _stream(stream)))
+
+    def decode_index_from_positions(self, filt: torch.Tensor, d: int, r: int, index_method: int,
+                                    positions: torch.Tensor, count: torch.Tensor, stream=None):
+        """The decode index stage (selection) from a complete positive list; finish
+        with decode_accumulate_own on this context."""
+        self._raise(lib.gp_decode_index_from_positions(self._ctx, _ptr(filt), filt.numel(), d, r, int(index_method),
+                                                       _ptr(positions), _ptr(count), _stream(stream)))
+
     def bloom_select(self, filt: torch.Tensor, d: int, r: int, index_method: int) -> torch.Tensor:
         """p1_select / p2_select (bloom.cpp:140-154, :175-222) over the positives
         of a serialized filter, seeded derive_selection_seed(seed_a, seed_b)."""

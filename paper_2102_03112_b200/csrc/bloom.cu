@@ -159,7 +159,10 @@ template <bool kSmallM, int kLaneKeys, int kLaneBatch, int kCap>
 __device__ __forceinline__ void members_body(const uint32_t* __restrict__ words, const Plan* plan,
                                              uint32_t* __restrict__ bitmap, uint8_t* dyn) {
   constexpr int kChunk = 32 * kLaneKeys, kBatch = 32 * kLaneBatch;
-  const uint32_t d = static_cast<uint32_t>(plan->d);
+  // keys [lo, lo + d): the whole range, or a slice (gp_bloom_scan_range); the
+  // stack holds global keys, the membership bitmap is slice-relative
+  const uint32_t lo = static_cast<uint32_t>(plan->scan_lo);
+  const uint32_t d = static_cast<uint32_t>(plan->scan_hi ? plan->scan_hi - plan->scan_lo : plan->d);
   const uint32_t k = plan->k;
   const FastMod fm{plan->m, plan->minv};
   const uint64_t sa = plan->seed_a + kGamma, sb = plan->seed_b + kGamma;
@@ -197,7 +200,7 @@ __device__ __forceinline__ void members_body(const uint32_t* __restrict__ words,
       for (int u = 0; u < kLaneBatch; ++u) {
         const bool ok = base + 32 * u + lane < top && ((wv[u] >> (pos[u] & 31)) & 1u);
         const bool member = ok && j[u] + 1u == k;
-        if (member) atomicOr(&bitmap[x[u] >> 5], 1u << (x[u] & 31));
+        if (member) atomicOr(&bitmap[(x[u] - lo) >> 5], 1u << ((x[u] - lo) & 31));
         const bool keep = ok && !member;
         const unsigned bal = __ballot_sync(kFull, keep);
         if (keep) {
@@ -218,7 +221,7 @@ __device__ __forceinline__ void members_body(const uint32_t* __restrict__ words,
       uint32_t pos[kLaneKeys], wv[kLaneKeys];
 #pragma unroll
       for (int q = 0; q < kLaneKeys; ++q) {
-        av[q] = mix64(static_cast<uint64_t>(x0 + q) ^ sa);
+        av[q] = mix64(static_cast<uint64_t>(lo + x0 + q) ^ sa);
         pos[q] = probe_pos<kSmallM>(av[q], fm);
       }
 #pragma unroll
@@ -240,7 +243,7 @@ __device__ __forceinline__ void members_body(const uint32_t* __restrict__ words,
 #pragma unroll
       for (int q = 0; q < kLaneKeys; ++q)
         if (pass >> q & 1u) {
-          qx[o] = x0 + q;
+          qx[o] = lo + x0 + q;
           qh[o] = av[q];
           ++o;
         }
@@ -296,7 +299,8 @@ __global__ void __launch_bounds__(kScanBlock) members_compact(const uint32_t* __
   if (failed(status)) return;
   const uint8_t im = plan->index_method;
   if (im < GP_INDEX_BLOOM_P0 || im > GP_INDEX_BLOOM_NAIVE) return;
-  const uint64_t nwd = (plan->d + 31) / 32;
+  const uint64_t lo = plan->scan_lo;
+  const uint64_t nwd = ((plan->scan_hi ? plan->scan_hi - lo : plan->d) + 31) / 32;
   constexpr int kW = 16;
   const uint64_t ntiles = (nwd + kScanBlock * kW - 1) / (kScanBlock * kW);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -322,7 +326,7 @@ __global__ void __launch_bounds__(kScanBlock) members_compact(const uint32_t* __
       const uint32_t incl = warp_inclusive_sum(n);
       uint64_t at = o + incl - n;
       for (uint32_t x = v[i]; x; x &= x - 1, ++at)
-        if (at < cap) pos_out[at] = static_cast<uint32_t>(32 * (wb + 32 * i + lane) + (__ffs(x) - 1));
+        if (at < cap) pos_out[at] = static_cast<uint32_t>(lo + 32 * (wb + 32 * i + lane) + (__ffs(x) - 1));
       o += __shfl_sync(kFull, incl, 31);
     }
     if (tile == ntiles - 1 && threadIdx.x == kScanBlock - 1) plan->n_pos = o;
@@ -423,6 +427,10 @@ void launch_bloom_scan(gp_ctx* ctx, uint64_t d_bound, uint64_t m_host, bool deco
   GP_LAUNCH(ctx, members_compact, static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, ctx->sm_count * 4ULL))),
             kScanBlock, 0, s, bitmap, w.plan, w.pos, ctx->max_d, w.tiles, w.ticket, w.status);
   GP_LAUNCH(ctx, bloom_after_scan, 1, 1, 0, s, w.plan, ctx->max_d, decoding ? 1 : 0, w.status);
+}
+
+void launch_bloom_after_scan(gp_ctx* ctx, bool decoding, cudaStream_t s) {
+  GP_LAUNCH(ctx, bloom_after_scan, 1, 1, 0, s, ctx->ws.plan, ctx->max_d, decoding ? 1 : 0, ctx->ws.status);
 }
 
 void launch_select_slice(gp_ctx* ctx, uint64_t n_bound, cudaStream_t s) {

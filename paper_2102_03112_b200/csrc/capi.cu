@@ -103,6 +103,8 @@ __global__ void init_plan(Plan* plan, PlanInit p) {
   plan->seed_a = hash64(0xA, seed);
   plan->seed_b = hash64(0xB, seed);
   plan->minv = p.minv;
+  plan->scan_lo = 0;  // full-range positive scans unless gp_bloom_scan_range narrows it
+  plan->scan_hi = 0;
 }
 
 // Simulation::pipeline_seed(seed, worker, *step) (harness.cpp:201-203, over
@@ -828,6 +830,83 @@ int gp_bloom_positive_scan(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter
   GP_LAUNCH(ctx, copy_positions, grid_for(ctx, d, 256), 256, 0, s, ctx->ws.pos, ctx->ws.plan, d_positives, cap,
             d_count, ctx->ws.status);
   return check_launch(ctx, "positive_scan");
+}
+
+__global__ void set_scan_range(Plan* plan, uint64_t lo, uint64_t hi) {
+  plan->scan_lo = lo;
+  plan->scan_hi = hi;
+}
+
+// caller positives -> ws.pos, |P| from a device word (the sharded decode)
+__global__ void take_positions(const uint32_t* __restrict__ src, const uint64_t* __restrict__ count, Plan* plan,
+                               uint32_t* __restrict__ pos, uint64_t cap, uint32_t* status) {
+  if (failed(status)) return;
+  const uint64_t n = *count;
+  if (n > cap) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) latch(status, GP_CAPACITY);
+    return;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) plan->n_pos = n;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    pos[i] = src[i];
+}
+
+int gp_bloom_scan_range(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter_len, uint64_t d, uint64_t lo,
+                        uint64_t hi, uint32_t* d_positives, uint64_t cap, uint64_t* d_count, void* stream) {
+  if (!ctx || !d_filter || !d_positives || !d_count) return set_error(ctx, GP_ERROR, "scan_range: null argument");
+  if (lo > hi || hi > d) return set_error(ctx, GP_ERROR, "scan_range: need lo <= hi <= d");
+  if (d < 1 || d > ctx->max_d) return set_error(ctx, GP_CAPACITY, "bloom: d exceeds the context's max_d");
+  auto s = static_cast<cudaStream_t>(stream);
+  PlanInit pi{};
+  pi.d = d;
+  pi.il = filter_len;
+  pi.index_method = GP_INDEX_BLOOM_P0;
+  pi.value_method = GP_VALUE_NONE;
+  GP_LAUNCH(ctx, init_plan, 1, 1, 0, s, ctx->ws.plan, pi);
+  GP_LAUNCH(ctx, component_offsets, 1, 1, 0, s, ctx->ws.plan);
+  launch_bloom_parse(ctx, d_filter, ctx->ws.m_cap, s);
+  if (hi == lo) {  // empty slice: |P| = 0 (the scan treats hi = 0 as "all of d")
+    GP_LAUNCH(ctx, set_scan_range, 1, 1, 0, s, ctx->ws.plan, 0, 0);
+    cudaMemsetAsync(d_count, 0, sizeof(uint64_t), s);
+    return check_launch(ctx, "scan_range");
+  }
+  GP_LAUNCH(ctx, set_scan_range, 1, 1, 0, s, ctx->ws.plan, lo, hi);
+  launch_bloom_scan(ctx, hi - lo, 0, false, s);
+  GP_LAUNCH(ctx, set_scan_range, 1, 1, 0, s, ctx->ws.plan, 0, 0);
+  GP_LAUNCH(ctx, copy_positions, grid_for(ctx, hi - lo, 256), 256, 0, s, ctx->ws.pos, ctx->ws.plan, d_positives,
+            cap, d_count, ctx->ws.status);
+  return check_launch(ctx, "scan_range");
+}
+
+int gp_decode_index_from_positions(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter_len, uint64_t d,
+                                   uint64_t r, int index_method, const uint32_t* d_positives,
+                                   const uint64_t* d_count, void* stream) {
+  if (!ctx || !d_filter || !d_positives || !d_count) return set_error(ctx, GP_ERROR, "index_from_positions: null");
+  if (index_method < GP_INDEX_BLOOM_P0 || index_method > GP_INDEX_BLOOM_PD)
+    return set_error(ctx, GP_ERROR, "index_from_positions: index_method must be Bloom P0, P1, P2 or Pd");
+  if (r < 1) return set_error(ctx, GP_ERROR, "index_from_positions: r must be >= 1");
+  if (d < 1 || d > ctx->max_d) return set_error(ctx, GP_CAPACITY, "bloom: d exceeds the context's max_d");
+  auto s = static_cast<cudaStream_t>(stream);
+  PlanInit pi{};
+  pi.d = d;
+  pi.r = r;
+  pi.il = filter_len;
+  pi.index_method = static_cast<uint8_t>(index_method);
+  pi.value_method = GP_VALUE_NONE;
+  GP_LAUNCH(ctx, init_plan, 1, 1, 0, s, ctx->ws.plan, pi);
+  GP_LAUNCH(ctx, component_offsets, 1, 1, 0, s, ctx->ws.plan);
+  launch_bloom_parse(ctx, d_filter, ctx->ws.m_cap, s);
+  GP_LAUNCH(ctx, take_positions, grid_for(ctx, d, 256), 256, 0, s, d_positives, d_count, ctx->ws.plan, ctx->ws.pos,
+            ctx->max_d, ctx->ws.status);
+  launch_bloom_after_scan(ctx, false, s);
+  if (index_method == GP_INDEX_BLOOM_P2)
+    launch_select_p2(ctx, d, ctx->ws.set_cap, 64, false, s);
+  else if (index_method == GP_INDEX_BLOOM_P1)
+    launch_select_p1(ctx, d, d, s);
+  else
+    launch_select_slice(ctx, d, s);
+  return check_launch(ctx, "index_from_positions");
 }
 
 int gp_decode_index_prepare(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter_len, uint64_t d, uint64_t r,

@@ -40,6 +40,7 @@ struct Plan {
   uint64_t seed;                // the pipeline seed of this encode
   uint32_t k, pad1;
   uint64_t n_pos;               // |P|
+  uint64_t scan_lo, scan_hi;    // positive scan over [scan_lo, scan_hi) only (0, 0: all of [0, d))
   uint64_t n_pairs, n_sets, n_multi, n_single_sel;
   uint64_t n_large;             // conflict sets of >= 255 members (ordered by a second pass)
   // ---- rle
@@ -256,6 +257,7 @@ void launch_bloom_build(gp_ctx* ctx, uint8_t* out, uint64_t m, uint64_t r, cudaS
 void launch_bloom_parse(gp_ctx* ctx, const uint8_t* in, uint64_t m_bound, cudaStream_t s);
 void launch_bloom_scan(gp_ctx* ctx, uint64_t d_bound, uint64_t m_host, bool decoding, cudaStream_t s);
 void launch_select_slice(gp_ctx* ctx, uint64_t n_bound, cudaStream_t s);
+void launch_bloom_after_scan(gp_ctx* ctx, bool decoding, cudaStream_t s);
 void launch_select_p1(gp_ctx* ctx, uint64_t n_bound, uint64_t r_bound, cudaStream_t s);
 void launch_flags_compact(gp_ctx* ctx, int method, uint64_t n_bound, cudaStream_t s);
 void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t k_bound, bool decoding,

@@ -63,7 +63,7 @@ class SparseAllgather:
     reference does (ef=True / "f64"), or in f32 (ef="f32")."""
 
     def __init__(self, codec, d: int, r: int, cfg, group=None, device=None, ef: bool = False,
-                 graph: bool = False, decode_codecs=None, early_codec=None):
+                 graph: bool = False, decode_codecs=None, early_codec=None, shard_scan: bool | None = None):
         self.codec = codec
         self.d, self.r, self.cfg = d, r, cfg
         self.group = group
@@ -98,6 +98,26 @@ class SparseAllgather:
             self.ev_index = torch.cuda.Event()
             self.ev_index.record()  # materialise the CUDA event handle
             self.ev_early = torch.cuda.Event()
+        # shard_scan (N > 1, Bloom P0/P1/P2/Pd): the positive scans of the N
+        # received filters are split by coordinate range — rank i scans every
+        # filter over [i d / N, (i + 1) d / N) and the slices are allgathered —
+        # so a rank scans d keys per step instead of N d; each container's
+        # selection then runs from its assembled positive list.
+        bloom_sel = 4 <= im <= 7
+        self.shard = bool(self.world > 1 and bloom_sel and (shard_scan if shard_scan is not None else True))
+        if self.shard:
+            from .api import bloom_params
+            m, _ = bloom_params(cfg.fpr, r)
+            self.filter_len = 26 + (m + 7) // 8 + (1 if im == 7 else 0)
+            n = self.world
+            self.lo, self.hi = self.rank * d // n, (self.rank + 1) * d // n
+            self.slice_cap = max(1, max((k + 1) * d // n - k * d // n for k in range(n)))
+            self.pslice = torch.empty((n, self.slice_cap), dtype=torch.int32, device=dev)
+            self.pcount = torch.zeros(n, dtype=torch.int64, device=dev)
+            self.pcount_all = torch.zeros(n * n, dtype=torch.int64, device=dev)
+            self.precv = None
+            self.pfull = torch.empty(d, dtype=torch.int32, device=dev)
+            self.pfull_n = torch.zeros(1, dtype=torch.int64, device=dev)
         self.dec_streams = ([torch.cuda.Stream(dev) for _ in self.dec]
                             if len(self.dec) > 1 and torch.device(dev).type == "cuda" else None)
         # graph=True (one rank, CUDA): the whole step — pipeline seed from a device
@@ -172,6 +192,9 @@ class SparseAllgather:
         sizes = self.sizes.tolist()
         mx = max(sizes)
         dist.all_gather_into_tensor(self.recv[: n * mx], self.out[:mx], group=self.group)
+        if self.shard:
+            self._decode_sharded(n, mx, sizes, out_dense, stream)
+            return out_dense
         if self.dec_streams is None:
             for j in range(n):  # fixed rank order, as the harness's worker order
                 self.codec.decode_accumulate(self.recv[j * mx: j * mx + sizes[j]], out_dense, scale=1.0 / n,
@@ -188,6 +211,43 @@ class SparseAllgather:
             self.codec.encode_ef_into(grad, self.residual, self.r, cfg, self.out, self.length, stream=stream)
         else:
             self.codec.encode_into(grad, self.r, cfg, self.out, self.length, stream=stream)
+
+    def _decode_sharded(self, n, mx, sizes, out_dense, stream):
+        """The decode of all N containers with the Bloom positive scans split by
+        coordinate range across the ranks (shard_scan)."""
+        if stream is not None:  # the buffer copies below must order with the codec calls
+            with torch.cuda.stream(stream):
+                return self._decode_sharded(n, mx, sizes, out_dense, None)
+        fl = self.filter_len
+        for j in range(n):  # this rank's slice of every container's positive set
+            filt = self.recv[j * mx + 49: j * mx + 49 + fl]
+            self.codec.bloom_scan_range_into(filt, self.d, self.lo, self.hi, self.pslice[j], self.pcount[j:j + 1],
+                                             stream=stream)
+        dist.all_gather_into_tensor(self.pcount_all, self.pcount, group=self.group)
+        cnt = self.pcount_all.tolist()  # cnt[i * n + j]: rank i's slice of container j (second host sync)
+        mxp = max(1, max(cnt))
+        if self.precv is None or self.precv.numel() < n * n * mxp:
+            self.precv = torch.empty(n * n * mxp, dtype=torch.int32, device=self.pslice.device)
+        send = self.pslice[:, :mxp].contiguous().view(-1)
+        dist.all_gather_into_tensor(self.precv[: n * n * mxp], send, group=self.group)
+        parts = self.precv[: n * n * mxp].view(n, n, mxp)  # [rank i][container j][:]
+        for j in range(n):  # rank order (harness.cpp:274-284)
+            total = 0
+            for i in range(n):  # slices in coordinate order: the ascending positive set
+                c = cnt[i * n + j]
+                if c:
+                    self.pfull[total: total + c].copy_(parts[i, j, :c])
+                total += c
+            self.pfull_n.fill_(total)
+            filt = self.recv[j * mx + 49: j * mx + 49 + fl]
+            self.codec.decode_index_from_positions(filt, self.d, self.r, int(self.cfg.index_method), self.pfull,
+                                                   self.pfull_n, stream=stream)
+            self.codec.set_decode_overwrite(j == 0)
+            try:
+                self.codec.decode_accumulate_own(self.recv[j * mx: (j + 1) * mx], out_dense,
+                                                 self.sizes[j:j + 1], self.cfg, scale=1.0 / n, stream=stream)
+            finally:
+                self.codec.set_decode_overwrite(False)
 
     def check(self, stream=None) -> None:
         """Synchronise and raise the first device error latched by any of this

@@ -54,6 +54,25 @@ class OracleCodec:
         out[: len(b)] = torch.frombuffer(bytearray(b), dtype=torch.uint8)
         length[0] = len(b)
 
+    # the sharded decode (shard_scan): range scans, then the selection from the
+    # assembled positive list — checked against the full scan here
+    def bloom_scan_range_into(self, filt, d, lo, hi, out, count, stream=None):
+        pos = oracle().positive_scan(filt.contiguous().numpy().tobytes(), d)
+        sl = pos[(pos >= lo) & (pos < hi)]
+        out[: sl.size] = torch.from_numpy(sl.astype(np.int32))
+        count[0] = sl.size
+
+    def decode_index_from_positions(self, filt, d, r, index_method, positions, count, stream=None):
+        got = positions[: int(count.item())].numpy().astype(np.uint32)
+        want = oracle().positive_scan(filt.contiguous().numpy().tobytes(), d)
+        assert np.array_equal(got, want), "assembled positive list differs from the full scan"
+
+    def set_decode_overwrite(self, on):
+        self._overwrite = bool(on)
+
+    def decode_accumulate_own(self, container, dense, length, hint, scale=1.0, stream=None):
+        self.decode_accumulate(container, dense, scale=scale, length=length, overwrite=getattr(self, "_overwrite", False))
+
     def status(self, stream=None):
         pass  # the oracle raises at the call that fails
 
