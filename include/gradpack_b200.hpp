@@ -86,7 +86,7 @@ struct SparseGradient {
   std::vector<double> values;     // values[i] belongs to support[i]
 };
 
-// RAII device buffer
+// RAII device buffer (fixed size)
 template <typename T>
 class DeviceBuffer {
  public:
@@ -106,6 +106,34 @@ class DeviceBuffer {
   size_t n_;
 };
 
+// A device buffer that only grows: the host-buffer calls below stage through
+// the Context's buffers, so repeated calls allocate nothing once warm.
+class GrowBuffer {
+ public:
+  GrowBuffer() = default;
+  ~GrowBuffer() {
+    if (p_) cudaFree(p_);
+  }
+  GrowBuffer(const GrowBuffer&) = delete;
+  GrowBuffer& operator=(const GrowBuffer&) = delete;
+  void* reserve(size_t bytes) {
+    if (bytes > cap_) {
+      if (p_) cudaFree(p_);
+      p_ = nullptr;
+      cap_ = 0;
+      const size_t want = bytes < 256 ? 256 : bytes + bytes / 4;  // headroom: fewer regrowths
+      if (cudaMalloc(&p_, want) != cudaSuccess) throw CudaError("cudaMalloc failed");
+      cap_ = want;
+    }
+    return p_;
+  }
+  size_t capacity() const { return cap_; }
+
+ private:
+  void* p_ = nullptr;
+  size_t cap_ = 0;
+};
+
 class Context {
  public:
   explicit Context(uint64_t max_d, int device = 0) {
@@ -118,6 +146,11 @@ class Context {
 
   gp_ctx* get() const { return ctx_; }
 
+  // staging slots of the host-buffer calls: 0 input vector, 1 support, 2 values,
+  // 3 container, 4 small scalars
+  template <typename T>
+  T* stage(int slot, size_t n) { return static_cast<T*>(staging_[slot].reserve(n * sizeof(T))); }
+
   // raise a launch-time status immediately
   void check(int rc) const {
     if (rc != GP_OK) throw_status(rc, gp_last_error(ctx_));
@@ -127,17 +160,18 @@ class Context {
 
  private:
   gp_ctx* ctx_ = nullptr;
+  GrowBuffer staging_[5];
 };
 
 namespace detail {
 inline void cuda_ok(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
 }
-inline std::vector<uint8_t> fetch(const DeviceBuffer<uint8_t>& out, const DeviceBuffer<uint64_t>& len) {
+inline std::vector<uint8_t> fetch(const uint8_t* out, const uint64_t* len) {
   uint64_t n = 0;
-  cuda_ok(cudaMemcpy(&n, len.get(), sizeof(n), cudaMemcpyDeviceToHost), "length");
+  cuda_ok(cudaMemcpy(&n, len, sizeof(n), cudaMemcpyDeviceToHost), "length");
   std::vector<uint8_t> bytes(n);
-  cuda_ok(cudaMemcpy(bytes.data(), out.get(), n, cudaMemcpyDeviceToHost), "container");
+  cuda_ok(cudaMemcpy(bytes.data(), out, n, cudaMemcpyDeviceToHost), "container");
   return bytes;
 }
 }  // namespace detail
@@ -145,11 +179,12 @@ inline std::vector<uint8_t> fetch(const DeviceBuffer<uint8_t>& out, const Device
 // top_r + compress_gradient(sg, cfg, &dense) + pack of a host gradient.
 inline std::vector<uint8_t> compress_dense(Context& ctx, const float* grad, uint64_t d, uint64_t r,
                                            const PipelineConfig& cfg) {
-  DeviceBuffer<float> g(d);
-  detail::cuda_ok(cudaMemcpy(g.get(), grad, d * sizeof(float), cudaMemcpyHostToDevice), "gradient");
-  DeviceBuffer<uint8_t> out(gp_max_container_bytes(d, r, &cfg));
-  DeviceBuffer<uint64_t> len(1);
-  ctx.check(gp_encode_topr(ctx.get(), g.get(), d, r, &cfg, out.get(), out.size(), len.get(), nullptr));
+  float* g = ctx.stage<float>(0, d);
+  detail::cuda_ok(cudaMemcpy(g, grad, d * sizeof(float), cudaMemcpyHostToDevice), "gradient");
+  const uint64_t cap = gp_max_container_bytes(d, r, &cfg);
+  uint8_t* out = ctx.stage<uint8_t>(3, cap);
+  uint64_t* len = ctx.stage<uint64_t>(4, 2);
+  ctx.check(gp_encode_topr(ctx.get(), g, d, r, &cfg, out, cap, len, nullptr));
   ctx.sync();
   return detail::fetch(out, len);
 }
@@ -157,36 +192,60 @@ inline std::vector<uint8_t> compress_dense(Context& ctx, const float* grad, uint
 // compress_gradient(sg, cfg, &dense) + pack for a caller-chosen support.
 inline std::vector<uint8_t> compress_gradient(Context& ctx, const float* dense, uint64_t d,
                                               const std::vector<uint32_t>& support, const PipelineConfig& cfg) {
-  DeviceBuffer<float> g(d);
-  DeviceBuffer<uint32_t> s(support.size());
-  detail::cuda_ok(cudaMemcpy(g.get(), dense, d * sizeof(float), cudaMemcpyHostToDevice), "dense");
-  detail::cuda_ok(cudaMemcpy(s.get(), support.data(), support.size() * 4, cudaMemcpyHostToDevice), "support");
-  DeviceBuffer<uint8_t> out(gp_max_container_bytes(d, support.size(), &cfg));
-  DeviceBuffer<uint64_t> len(1);
-  ctx.check(gp_encode_support(ctx.get(), g.get(), d, s.get(), support.size(), &cfg, out.get(), out.size(),
-                              len.get(), nullptr));
+  float* g = ctx.stage<float>(0, d);
+  uint32_t* s = ctx.stage<uint32_t>(1, support.size());
+  detail::cuda_ok(cudaMemcpy(g, dense, d * sizeof(float), cudaMemcpyHostToDevice), "dense");
+  detail::cuda_ok(cudaMemcpy(s, support.data(), support.size() * 4, cudaMemcpyHostToDevice), "support");
+  const uint64_t cap = gp_max_container_bytes(d, support.size(), &cfg);
+  uint8_t* out = ctx.stage<uint8_t>(3, cap);
+  uint64_t* len = ctx.stage<uint64_t>(4, 2);
+  ctx.check(gp_encode_support(ctx.get(), g, d, s, support.size(), &cfg, out, cap, len, nullptr));
+  ctx.sync();
+  return detail::fetch(out, len);
+}
+
+// compress_gradient(sg, cfg, dense) + pack with the reference's f64 values
+// (and optionally its f64 dense vector): bit-identical for any double.
+inline std::vector<uint8_t> compress_sparse(Context& ctx, const SparseGradient& sg, const PipelineConfig& cfg,
+                                            const double* dense = nullptr) {
+  const uint64_t d = sg.dim, r = sg.support.size();
+  if (sg.values.size() != r) throw Error("gradient: support/value length mismatch");
+  uint32_t* s = ctx.stage<uint32_t>(1, r);
+  double* v = ctx.stage<double>(2, r);
+  if (r) {
+    detail::cuda_ok(cudaMemcpy(s, sg.support.data(), r * 4, cudaMemcpyHostToDevice), "support");
+    detail::cuda_ok(cudaMemcpy(v, sg.values.data(), r * 8, cudaMemcpyHostToDevice), "values");
+  }
+  double* dn = nullptr;
+  if (dense) {
+    dn = ctx.stage<double>(0, d);
+    detail::cuda_ok(cudaMemcpy(dn, dense, d * 8, cudaMemcpyHostToDevice), "dense");
+  }
+  const uint64_t cap = gp_max_container_bytes(d, r ? r : 1, &cfg);
+  uint8_t* out = ctx.stage<uint8_t>(3, cap);
+  uint64_t* len = ctx.stage<uint64_t>(4, 2);
+  ctx.check(gp_encode_sparse(ctx.get(), d, r ? s : nullptr, r ? v : nullptr, r, dn, &cfg, out, cap, len, nullptr));
   ctx.sync();
   return detail::fetch(out, len);
 }
 
 // unpack + decompress_gradient.
 inline SparseGradient decompress_gradient(Context& ctx, const std::vector<uint8_t>& container, uint64_t cap) {
-  DeviceBuffer<uint8_t> in(container.size() ? container.size() : 1);
-  detail::cuda_ok(cudaMemcpy(in.get(), container.data(), container.size(), cudaMemcpyHostToDevice), "container");
-  DeviceBuffer<uint32_t> sup(cap);
-  DeviceBuffer<double> val(cap);
-  DeviceBuffer<uint64_t> meta(2);
-  ctx.check(gp_decode_sparse(ctx.get(), in.get(), container.size(), sup.get(), val.get(), cap, meta.get(),
-                             meta.get() + 1, nullptr));
+  uint8_t* in = ctx.stage<uint8_t>(3, container.size() ? container.size() : 1);
+  detail::cuda_ok(cudaMemcpy(in, container.data(), container.size(), cudaMemcpyHostToDevice), "container");
+  uint32_t* sup = ctx.stage<uint32_t>(1, cap);
+  double* val = ctx.stage<double>(2, cap);
+  uint64_t* meta = ctx.stage<uint64_t>(4, 2);
+  ctx.check(gp_decode_sparse(ctx.get(), in, container.size(), sup, val, cap, meta, meta + 1, nullptr));
   ctx.sync();
   uint64_t m[2];
-  detail::cuda_ok(cudaMemcpy(m, meta.get(), sizeof(m), cudaMemcpyDeviceToHost), "meta");
+  detail::cuda_ok(cudaMemcpy(m, meta, sizeof(m), cudaMemcpyDeviceToHost), "meta");
   SparseGradient sg;
   sg.dim = m[1];
   sg.support.resize(m[0]);
   sg.values.resize(m[0]);
-  detail::cuda_ok(cudaMemcpy(sg.support.data(), sup.get(), m[0] * 4, cudaMemcpyDeviceToHost), "support");
-  detail::cuda_ok(cudaMemcpy(sg.values.data(), val.get(), m[0] * 8, cudaMemcpyDeviceToHost), "values");
+  detail::cuda_ok(cudaMemcpy(sg.support.data(), sup, m[0] * 4, cudaMemcpyDeviceToHost), "support");
+  detail::cuda_ok(cudaMemcpy(sg.values.data(), val, m[0] * 8, cudaMemcpyDeviceToHost), "values");
   return sg;
 }
 

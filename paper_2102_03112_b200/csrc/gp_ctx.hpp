@@ -33,6 +33,8 @@ struct Plan {
   uint32_t thresh, tie_cut;     // exact threshold key; last kept index among ties
   uint64_t above, n_cand;       // keys in bins above bin_star; candidates emitted
   uint64_t thresh64;            // f64 input (topr64.cu): exact threshold key
+  uint64_t r64_prefix, r64_need;  // topr64 refine: 32-bit key prefix of T, rank under it
+  uint32_t r64_n, r64_pad;        // keys under that prefix
   uint64_t tie_q;               // keep the first tie_q keys == thresh (index order)
   uint32_t tie_all, pad2;       // every key == thresh is kept
   // ---- bloom

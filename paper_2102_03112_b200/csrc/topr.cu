@@ -313,6 +313,58 @@ __device__ __forceinline__ uint32_t stream_groups(const float* __restrict__ g, c
   return nc;
 }
 
+// Dense selections (r > d/16, e.g. natural sparsity with r = nnz): every
+// group is live, so the skip index and the live lists only cost; lane =
+// group, two 16-byte loads per lane per row of 32 groups, ranks by a warp
+// scan.  Same contract as stream_groups.
+template <typename EC, typename ET>
+__device__ __forceinline__ uint32_t stream_dense(const float* __restrict__ g, uint64_t glo, uint64_t ghi, uint64_t d,
+                                                 bool aligned, uint32_t klo, uint32_t khi, EC emit_c, ET tie) {
+  const int lane = threadIdx.x & 31;
+  uint32_t nc = 0;
+  for (uint64_t base = glo; base < ghi; base += 64) {
+    float v[2][kGroup];
+    uint64_t k0[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint64_t j = base + 32 * u + lane;
+      k0[u] = j < ghi ? j * kGroup : d;
+      if (k0[u] >= d) {
+#pragma unroll
+        for (int q = 0; q < kGroup; ++q) v[u][q] = 0.0f;
+      } else if (aligned && k0[u] + kGroup <= d) {
+        const float4 a = ld_f4_last(reinterpret_cast<const float4*>(g + k0[u]));
+        const float4 b = ld_f4_last(reinterpret_cast<const float4*>(g + k0[u]) + 1);
+        v[u][0] = a.x; v[u][1] = a.y; v[u][2] = a.z; v[u][3] = a.w;
+        v[u][4] = b.x; v[u][5] = b.y; v[u][6] = b.z; v[u][7] = b.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < kGroup; ++q) v[u][q] = k0[u] + q < d ? g[k0[u] + q] : 0.0f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      uint32_t mask = 0;
+#pragma unroll
+      for (int q = 0; q < kGroup; ++q) {
+        const uint32_t key = key_of(v[u][q]);
+        if (k0[u] + q < d && key >= klo) {
+          mask |= 1u << q;
+          if (key < khi) tie(key);
+        }
+      }
+      const uint32_t cnt = __popc(mask);
+      const uint32_t incl = warp_inclusive_sum(cnt);
+      uint32_t o = nc + incl - cnt;
+#pragma unroll
+      for (int q = 0; q < kGroup; ++q)
+        if (mask >> q & 1u) emit_c(o++, static_cast<uint32_t>(k0[u] + q), v[u][q]);
+      nc += __shfl_sync(kFull, incl, 31);
+    }
+  }
+  return nc;
+}
+
 // Ordered filter of the candidate list into the final support: one chunk of
 // the list per claimed ticket, one segment per warp, 128-entry rows ranked by
 // ballots.  Keys == T are kept while their rank among the list's T-ties is
@@ -409,8 +461,8 @@ __device__ void chunk_pairs(const uint32_t* __restrict__ cidx, const float* __re
 __global__ void __launch_bounds__(kCandBlock) topr_select(
     const float* __restrict__ g, const uint16_t* __restrict__ gmax, const uint32_t* __restrict__ ghist,
     const uint32_t* __restrict__ gcoarse, uint64_t d, uint64_t r, Plan* plan, uint32_t* cidx, float* cval,
-    uint32_t* sidx, float* sval, uint32_t* fine, uint32_t* fcoarse, uint64_t* cnt, uint64_t* pair, uint64_t chunk,
-    const uint32_t* status) {
+    uint32_t* sidx, float* sval, uint32_t* fine, uint32_t* fcoarse, uint64_t* cnt, uint64_t* pair, uint32_t* wcnt,
+    uint64_t chunk, bool dense, const uint32_t* status) {
   cg::grid_group grid = cg::this_grid();
   __shared__ uint32_t bidx[kCandWarps][kWarpCandCap];
   __shared__ float bval[kCandWarps][kWarpCandCap];
@@ -447,6 +499,19 @@ __global__ void __launch_bounds__(kCandBlock) topr_select(
     const uint64_t slot = c * chunk;
     const uint64_t lo = slot + warp * wseg < d ? slot + warp * wseg : d;
     const uint64_t hi = lo + wseg < d ? lo + wseg : d;
+    if (dense) {  // count now; the write pass follows (below, or straight to the support when b* is kept whole)
+      const uint32_t nd = stream_dense(g, lo / kGroup, (hi + kGroup - 1) / kGroup, d, aligned, klo, khi,
+                                       [](uint32_t, uint32_t, float) {}, tie);
+      if (lane == 0) wcnt[c * kCandWarps + warp] = nd;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint64_t tot = 0;
+        for (int w = 0; w < kCandWarps; ++w) tot += wcnt[c * kCandWarps + w];
+        cnt[c] = tot;
+      }
+      __syncthreads();
+      continue;
+    }
     const uint32_t nc = stream_groups(
         g, gmax, lo / kGroup, (hi + kGroup - 1) / kGroup, d, aligned, bstar, klo, khi, live_list[warp],
         [&](uint32_t o, uint32_t idx, float v) {
@@ -483,6 +548,41 @@ __global__ void __launch_bounds__(kCandBlock) topr_select(
     __syncthreads();
   }
   grid.sync();
+  if (dense) {  // the write pass of the dense selection (the re-read of g comes largely from L2)
+    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+      const uint64_t lo = c * chunk + warp * wseg < d ? c * chunk + warp * wseg : d;
+      const uint64_t hi = lo + wseg < d ? lo + wseg : d;
+      uint64_t at = c * chunk;  // the chunk's slot ...
+      if (full) {               // ... or, b* kept whole, its final place in the support
+        if (warp == 0) {
+          uint64_t v = 0;
+          for (uint64_t k = lane; k < c; k += 32) v += __ldcg(cnt + k);
+          v = warp_sum(v);
+          if (lane == 0) s_pre = v;
+        }
+        __syncthreads();
+        at = s_pre;
+      }
+      for (int w = 0; w < warp; ++w) at += __ldcg(wcnt + c * kCandWarps + w);
+      uint32_t* oi = full ? sidx : cidx;
+      float* ov = full ? sval : cval;
+      stream_dense(g, lo / kGroup, (hi + kGroup - 1) / kGroup, d, aligned, klo, khi,
+                   [&](uint32_t o, uint32_t idx, float v) {
+                     oi[at + o] = idx;
+                     ov[at + o] = v;
+                   },
+                   [](uint32_t) {});
+      __syncthreads();
+    }
+    if (full) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        plan->thresh = klo;
+        plan->tie_all = 1;
+      }
+      return;  // uniform: every block leaves before the next grid.sync
+    }
+    grid.sync();
+  }
   // ---- B: the exact threshold, in every block
   uint32_t T = klo, tall = 1;
   uint64_t q = 0;
@@ -562,6 +662,7 @@ void launch_top_r(gp_ctx* ctx, const float* grad, uint64_t d, uint64_t r, cudaSt
     const int grid = static_cast<int>(std::min<uint64_t>(std::max<uint64_t>(1, nchunks), blocks));
     uint64_t* cnt = w.tiles;
     uint64_t* pair = w.tiles + nchunks + 1;
+    uint32_t* wcnt = reinterpret_cast<uint32_t*>(w.tiles + 2 * (nchunks + 1));  // per-warp counts (dense)
     const float* gp = grad;
     const uint32_t* gh = w.hist;
     const uint32_t* gc = coarse;
@@ -571,7 +672,9 @@ void launch_top_r(gp_ctx* ctx, const float* grad, uint64_t d, uint64_t r, cudaSt
     uint32_t* si = w.support;
     float* sv = w.values;
     const uint32_t* st = w.status;
-    void* args[] = {&gp, &gmax, &gh, &gc, &d, &r, &plan, &ci, &cv, &si, &sv, &fine, &fcoarse, &cnt, &pair, &chunk, &st};
+    bool dense = r > d / 16;
+    void* args[] = {&gp, &gmax, &gh, &gc, &d, &r, &plan, &ci, &cv, &si, &sv, &fine, &fcoarse, &cnt, &pair, &wcnt, &chunk,
+                    &dense, &st};
     cudaLaunchCooperativeKernel(reinterpret_cast<void*>(topr_select), grid, kCandBlock, args, 0, s);
     ++ctx->launches;
   }
