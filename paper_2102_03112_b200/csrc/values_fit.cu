@@ -151,6 +151,7 @@ struct SegNode {
 };
 constexpr uint32_t kNoChild = 0xFFFFFFFFu;
 constexpr int kFewRanges = 8;  // rounds with <= 8 pending nodes reduce partials instead of atomics
+constexpr int kSmallBudget = 64;  // budgets up to this run the replicated piece list (no tree)
 
 // control words shared by the blocks of fit_segment_coop (global memory)
 struct SegState {
@@ -361,6 +362,8 @@ __global__ void __launch_bounds__(256) fit_segment_coop(Plan* plan, const double
   __shared__ double sres_dev[kFewRanges];
   __shared__ uint32_t sres_arg[kFewRanges];
   __shared__ uint64_t sh[40];
+  __shared__ SegNode small[kSmallBudget];
+  __shared__ int s_best;
   // uniform exit decisions only (every block must reach every grid.sync)
   if (failed(status) || !poly_active(plan)) return;
   const uint64_t n = plan->n_values;
@@ -421,6 +424,77 @@ __global__ void __launch_bounds__(256) fit_segment_coop(Plan* plan, const double
         seg_end[nseg + (split ? 1 : 0)] = e;
       }
       nseg += split ? 2 : 1;
+      continue;
+    }
+    if (budget <= kSmallBudget) {
+      // small budgets (C5's max_segments = 8): the reference's loop with the piece
+      // list replicated in every block — each split one sweep of its two
+      // children, decided identically everywhere; no tree, no leader, no extra
+      // grid barriers
+      int np = 1;
+      {
+        const uint32_t rb = 0, re = len;
+        seg_sweep_few(t + b, nullptr, nullptr, 1, &rb, &re, pdev + (sweep & 1) * kFewRanges * G,
+                      parg + (sweep & 1) * kFewRanges * G, sdev, sarg, sres_dev, sres_arg, grid);
+        ++sweep;
+        if (threadIdx.x == 0) {
+          small[0] = SegNode{0, len, sres_arg[0], 0u, sres_dev[0], kNoChild, 0u};
+          make_live(small[0], mp);
+        }
+      }
+      __syncthreads();
+      while (np < budget) {
+        if (threadIdx.x == 0) {
+          int best = -1;
+          for (int i = 0; i < np; ++i) {
+            if (!small[i].live) continue;
+            if (best < 0 || seg_before(small[i], small[best])) best = i;
+          }
+          s_best = best;
+        }
+        __syncthreads();
+        const int best = s_best;
+        if (best < 0) break;
+        const SegNode pp = small[best];
+        SegNode left{pp.begin, pp.arg, 0, 0u, 0.0, kNoChild, 0u}, right{pp.arg, pp.end, 0, 0u, 0.0, kNoChild, 0u};
+        if (np + 1 < budget) {  // another split may follow: evaluate both children
+          const uint32_t rb[2] = {pp.begin, pp.arg}, re[2] = {pp.arg, pp.end};
+          seg_sweep_few(t + b, nullptr, nullptr, 2, rb, re, pdev + (sweep & 1) * kFewRanges * G,
+                        parg + (sweep & 1) * kFewRanges * G, sdev, sarg, sres_dev, sres_arg, grid);
+          ++sweep;
+          left.arg = sres_arg[0];
+          left.dev = sres_dev[0];
+          right.arg = sres_arg[1];
+          right.dev = sres_dev[1];
+          make_live(left, mp);
+          make_live(right, mp);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          small[best] = left;
+          small[np] = right;
+        }
+        ++np;
+        __syncthreads();
+      }
+      if (nseg + np > seg_cap) {
+        overflow = true;
+        break;
+      }
+      if (leader) {
+        for (int i = 1; i < np; ++i) {  // by begin
+          const SegNode v = small[i];
+          int j = i;
+          while (j > 0 && small[j - 1].begin > v.begin) {
+            small[j] = small[j - 1];
+            --j;
+          }
+          small[j] = v;
+        }
+        for (int i = 0; i < np; ++i) seg_end[nseg + i] = b + small[i].end;
+      }
+      nseg += static_cast<uint32_t>(np);
+      __syncthreads();
       continue;
     }
     if (leader) {
