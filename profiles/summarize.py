@@ -25,7 +25,8 @@ STAGE_KERNELS = {
     "dec_bloom_scan": ["bloom_members", "members_compact"],
     "p2_sets": ["p2_pairs", "p2_scatter"],
     "dec_p2_sets": ["p2_pairs", "p2_scatter"],
-    "topr": ["topr_candidates"],
+    "topr": ["topr_hist", "topr_select"],
+    "index": ["nz_encode"],
     "p2_engine": ["p2_engine"],
     "dec_p2_engine": ["p2_engine"],
     "pack_crc": ["crc_chunks"],

@@ -95,6 +95,13 @@ def test_crc32c_bit_exact(codec, oracle):
         got = codec.crc32c(t[:n])
         assert got == oracle.crc32c(data[:n].tobytes()), n
     assert codec.crc32c(_dev(np.frombuffer(b"123456789", np.uint8))) == 0xE3069283
+    # misaligned starts and ends, ranges inside one 64-byte line, and ranges
+    # past one row of the fixed grid (148 x 1024 lanes x 64 B) — several rows
+    big = rng.integers(0, 256, 25_000_000 + 200, dtype=np.uint8)
+    t = _dev(big)
+    for off, n in [(1, 5), (3, 60), (63, 2), (17, 64), (5, 127), (13, 9_699_329), (0, 9_699_328), (7, 25_000_000),
+                   (64, 19_398_656 + 3), (33, 1_260_001)]:
+        assert codec.crc32c(t[off:off + n]) == oracle.crc32c(big[off:off + n].tobytes()), (off, n)
 
 
 @pytest.mark.parametrize("im,vm", [(NONE, V_NONE), (BITMAP, V_NONE), (BITMAP, V_F64), (NONE, V_F64)])
