@@ -195,8 +195,6 @@ void carve(Workspace& w, uint8_t* base, uint64_t D) {
   w.pair_cap = 4 * D;
   w.p2_count = c.take<uint32_t>(w.set_cap + 1);
   w.p2_off = c.take<uint32_t>(w.set_cap + 1);
-  w.p2_single = c.take<uint32_t>(w.set_cap);
-  w.p2_cursor = c.take<uint32_t>(w.set_cap);
   w.p2_alloc = c.take<uint32_t>(64);
   w.p2_sets = c.take<uint32_t>(w.set_cap);
   w.p2_table = c.take<uint32_t>(256 * (w.set_cap / 4096 + 1) + 256);

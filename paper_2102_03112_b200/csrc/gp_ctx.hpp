@@ -95,8 +95,6 @@ struct Workspace {
   uint64_t set_cap = 0;           // max filter width m for P2
   uint32_t* p2_count = nullptr;   // [set_cap + 1]
   uint32_t* p2_off = nullptr;     // [set_cap + 1]
-  uint32_t* p2_single = nullptr;  // member of size-1 sets [set_cap]
-  uint32_t* p2_cursor = nullptr;  // scatter cursors [set_cap]
   uint32_t* p2_alloc = nullptr;   // bucket-space allocator word
   uint32_t* p2_sets = nullptr;    // [set_cap]
   uint32_t* p2_table = nullptr;   // [256 * set_cap / 4096 + 256]

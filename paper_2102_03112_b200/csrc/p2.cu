@@ -5,7 +5,8 @@
 // positions; a bit's set is the ascending, de-duplicated list of positives
 // probing it; sets are ordered by (size, bit).  Device form:
 //   pairs    : one thread per positive, k positions de-duplicated in
-//              registers, per-bit distinct counts = set sizes (atomics)
+//              registers, per-bit distinct counts = set sizes, each pair's
+//              slot in its set from the count atomic
 //   tiles    : per 4096-bit tile: bucket space for multi sets from a global
 //              cursor, and the tile's histogram of set sizes
 //   scatter  : per pair: a singleton's member is recorded and selected
@@ -43,92 +44,86 @@ __device__ __forceinline__ bool p2_active(const Plan* plan) {
   return plan->index_method == GP_INDEX_BLOOM_P2;
 }
 
-// count[0, m] = 0 with m read on the device (decode only knows it there)
-__global__ void p2_zero_counts(Plan* plan, uint32_t* count, uint64_t m_cap, const uint32_t* status) {
+// count[0, m] = 0 with m read on the device (decode only knows it there),
+// the stage-A flags over P and the bucket-space cursor
+__global__ void p2_zero_counts(Plan* plan, uint32_t* count, uint64_t m_cap, uint8_t* flags, uint64_t n_cap,
+                               uint32_t* alloc, const uint32_t* status) {
   if (failed(status) || !p2_active(plan)) return;
   const uint64_t n = (plan->m < m_cap ? plan->m : m_cap) + 1;
-  if (blockIdx.x == 0 && threadIdx.x == 0) plan->n_large = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    plan->n_large = 0;
+    plan->n_single_sel = 0;  // counted by p2_size_scatter's stage-A pass
+    *alloc = 0;
+  }
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t t0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   const uint64_t n4 = n / 4;
   uint4* c4 = reinterpret_cast<uint4*>(count);
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n4;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    c4[i] = make_uint4(0, 0, 0, 0);
-  for (uint64_t i = 4 * n4 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    count[i] = 0;
+  for (uint64_t i = t0; i < n4; i += stride) c4[i] = make_uint4(0, 0, 0, 0);
+  for (uint64_t i = 4 * n4 + t0; i < n; i += stride) count[i] = 0;
+  const uint64_t np = plan->n_pos < n_cap ? plan->n_pos : n_cap;
+  for (uint64_t i = t0; i < (np + 15) / 16; i += stride) reinterpret_cast<uint4*>(flags)[i] = make_uint4(0, 0, 0, 0);
 }
 
-// One thread per positive p: its k probe positions, de-duplicated among
-// themselves (one positive joins a set once, the consecutive-duplicate rule of
-// bloom.cpp:159-164), so count[bit] ends as the set's size (fire-and-forget
-// atomics).
-template <int KM, bool kSmallM>
-__device__ __forceinline__ void pairs_body(const uint32_t* __restrict__ P, uint64_t n, uint32_t k, const FastMod& fm,
-                                           uint64_t sa, uint64_t sb, uint32_t* __restrict__ pairs,
-                                           uint32_t* __restrict__ rank, uint32_t* __restrict__ count) {
+// One thread per positive p: h_a, h_b once, then its k probe positions
+// mix64(h_a + j h_b) mod m (bloom.cpp:27-33), de-duplicated among themselves
+// (one positive joins a set once, the consecutive-duplicate rule of
+// bloom.cpp:159-164) — the first kReg in registers, beyond them (k > 16,
+// eps < 2^-16) an earlier position recomputed per comparison.  count[bit]
+// ends as the set's size; the count atomic hands each pair its slot in its
+// set (all of a positive's atomics issued before any result is used).  Pair
+// arrays are probe-major (j * n + p): each store instruction is coalesced.
+template <bool kSmallM>
+__device__ __forceinline__ void pairs_thread(const uint32_t* __restrict__ P, uint64_t n, uint32_t k,
+                                             const FastMod& fm, uint64_t sa, uint64_t sb,
+                                             uint32_t* __restrict__ pairs, uint32_t* __restrict__ rank,
+                                             uint32_t* __restrict__ count) {
+  constexpr int kReg = 16;
+  auto probe = [&](uint64_t h) {
+    return kSmallM ? fast_mod_small(mix64(h), fm.minv, static_cast<uint32_t>(fm.m))
+                   : static_cast<uint32_t>(fast_mod(mix64(h), fm));
+  };
   for (uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; p < n;
        p += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t x = P[p];
     const uint64_t a = mix64(x ^ sa), b = mix64(x ^ sb);
-    uint64_t h = a;
-    uint32_t seen[KM];  // registers for KM <= 16 (fully unrolled)
+    uint32_t bit[kReg], rk[kReg];
+    uint32_t keep = 0;  // bit j: probe j is the first occurrence of its position
 #pragma unroll
-    for (int j = 0; j < KM; ++j) {
+    for (int j = 0; j < kReg; ++j) {
+      bit[j] = j < static_cast<int>(k) ? probe(a + static_cast<uint64_t>(j) * b) : 0xFFFFFFFFu;
+      bool dup = false;
+#pragma unroll
+      for (int i = 0; i < j; ++i) dup |= bit[i] == bit[j];
+      if (j < static_cast<int>(k) && !dup) keep |= 1u << j;
+    }
+#pragma unroll
+    for (int j = 0; j < kReg; ++j)
+      if (keep >> j & 1u) rk[j] = atomicAdd(&count[bit[j]], 1u);
+#pragma unroll
+    for (int j = 0; j < kReg; ++j) {
       if (j < static_cast<int>(k)) {
-        const uint32_t bit = kSmallM ? fast_mod_small(mix64(h), fm.minv, static_cast<uint32_t>(fm.m))
-                                     : static_cast<uint32_t>(fast_mod(mix64(h), fm));
-        h += b;
-        bool dup = false;
-#pragma unroll
-        for (int i = 0; i < j; ++i) dup |= seen[i] == bit;
-        seen[j] = bit;
-        pairs[p * k + j] = dup ? 0xFFFFFFFFu : bit;
-        if (!dup) rank[p * k + j] = atomicAdd(&count[bit], 1u);  // the pair's slot in its set
+        pairs[j * n + p] = (keep >> j & 1u) ? bit[j] : 0xFFFFFFFFu;
+        if (keep >> j & 1u) rank[j * n + p] = rk[j];
       }
     }
-  }
-}
-
-// k <= 32: a warp holds floor(32/k) positives, one lane per probe (h_a, h_b
-// recomputed per lane); duplicates among a positive's probes are found with
-// match_any inside its lane group — a probe is dropped if a lower lane of the
-// group has the same bit.
-__device__ __forceinline__ void pairs_lanes(const uint32_t* __restrict__ P, uint64_t n, uint32_t k, const FastMod& fm,
-                                            uint64_t sa, uint64_t sb, uint32_t* __restrict__ pairs,
-                                            uint32_t* __restrict__ rank, uint32_t* __restrict__ count) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t per = 32 / k;                 // positives per warp
-  const uint32_t g = lane / k, j = lane - g * k;
-  const bool active = g < per;
-  const unsigned gmask = active ? (((k == 32) ? 0xFFFFFFFFu : ((1u << k) - 1u)) << (g * k)) : 0u;
-  const bool small = fm.m <= (1ull << 31);
-  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32);
-  for (uint64_t w = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) / 32; w * per < n; w += warps) {
-    const uint64_t p = w * per + g;
-    const bool ok = active && p < n;
-    uint32_t bit = 0xFFFFFFFFu;
-    if (ok) {
-      const uint64_t x = P[p];
-      const uint64_t h = mix64(x ^ sa) + static_cast<uint64_t>(j) * mix64(x ^ sb);
-      bit = small ? fast_mod_small(mix64(h), fm.minv, static_cast<uint32_t>(fm.m))
-                  : static_cast<uint32_t>(fast_mod(mix64(h), fm));
-    }
-    const unsigned peers = __match_any_sync(kFull, bit) & gmask;
-    const bool dup = (peers & ((1u << lane) - 1u)) != 0u;
-    if (ok) {
-      pairs[p * k + j] = dup ? 0xFFFFFFFFu : bit;
-      if (!dup) rank[p * k + j] = atomicAdd(&count[bit], 1u);  // the pair's slot in its set
+    for (uint32_t j = kReg; j < k; ++j) {
+      const uint32_t bj = probe(a + static_cast<uint64_t>(j) * b);
+      bool dup = false;
+#pragma unroll
+      for (int i = 0; i < kReg; ++i) dup |= bit[i] == bj;
+      for (uint32_t i = kReg; i < j && !dup; ++i) dup = probe(a + static_cast<uint64_t>(i) * b) == bj;
+      pairs[j * n + p] = dup ? 0xFFFFFFFFu : bj;
+      if (!dup) rank[j * n + p] = atomicAdd(&count[bj], 1u);
     }
   }
 }
 
-// kWide: the k > 32 form (one thread per positive); launched next to the lane
-// form, each exits unless k is in its range (k is only known on the device).
-template <bool kWide>
-__global__ void p2_pairs(const uint32_t* __restrict__ P, Plan* plan, uint32_t* __restrict__ pairs,
-                         uint32_t* __restrict__ rank, uint32_t* __restrict__ count, uint64_t pair_cap,
-                         uint64_t set_cap, uint32_t* status) {
-  if (failed(status) || !p2_active(plan) || (plan->k > 32) != kWide) return;
+__global__ void __launch_bounds__(256) p2_pairs(const uint32_t* __restrict__ P, Plan* plan,
+                                                uint32_t* __restrict__ pairs, uint32_t* __restrict__ rank,
+                                                uint32_t* __restrict__ count, uint64_t pair_cap, uint64_t set_cap,
+                                                uint32_t* status) {
+  if (failed(status) || !p2_active(plan)) return;
   const uint64_t n = plan->n_pos, m = plan->m;
   const uint32_t k = plan->k;
   if (n * k > pair_cap || n * k >= kSingleton || m > set_cap || k > 64) {
@@ -137,10 +132,10 @@ __global__ void p2_pairs(const uint32_t* __restrict__ P, Plan* plan, uint32_t* _
   }
   const FastMod fm{m, plan->minv};
   const uint64_t sa = plan->seed_a + kGamma, sb = plan->seed_b + kGamma;
-  if (kWide)
-    pairs_body<64, false>(P, n, k, fm, sa, sb, pairs, rank, count);
+  if (m <= (1ull << 31))
+    pairs_thread<true>(P, n, k, fm, sa, sb, pairs, rank, count);
   else
-    pairs_lanes(P, n, k, fm, sa, sb, pairs, rank, count);
+    pairs_thread<false>(P, n, k, fm, sa, sb, pairs, rank, count);
   if (blockIdx.x == 0 && threadIdx.x == 0) plan->n_pairs = n * k;
 }
 
@@ -231,37 +226,58 @@ __global__ void p2_scatter(const uint32_t* __restrict__ pairs, const uint32_t* _
     for (int u = 0; u < kU; ++u) {
       if (bit[u] == 0xFFFFFFFFu) continue;
       const uint64_t i = i0 + u * stride;
-      const uint32_t p = static_cast<uint32_t>(np < (1ull << 32) ? static_cast<uint32_t>(i) / k : i / k);
+      const uint32_t p = static_cast<uint32_t>(np < (1ull << 32) ? static_cast<uint32_t>(i) % static_cast<uint32_t>(n)
+                                                                 : i % n);  // probe-major: i = j * n + p
       members[(v[u] & ~kSingleton) + rk[u]] = p;
       if (v[u] & kSingleton) flags[p] = 1;  // flags were zeroed; every writer stores the same value
     }
   }
 }
 
-// n_sets = total over the digit table: the exclusive prefix at the first cell
-// of digit 255 counts every set below 255 members, p2_tiles counted the rest.
-__global__ void p2_count_sets(Plan* plan, const uint32_t* __restrict__ table, const uint32_t* status) {
-  if (failed(status) || !p2_active(plan) || threadIdx.x != 0) return;
-  const uint64_t ntiles = (plan->m + kTile - 1) / kTile;
-  plan->n_sets = table[kBigSet * ntiles] + plan->n_large;
-  const uint64_t n1 = table[2 * ntiles] - table[1 * ntiles];  // sets of size 1
-  plan->n_multi = plan->n_sets - n1;
-  plan->n_cand = n1;  // first multi set in the (size, bit) order
-  plan->n_single_sel = 0;  // counted by p2_stage_a
-}
-
 // Stable placement of the non-empty bits by size (counting sort over the
 // digit table): sets[table[size][tile] + rank] = bit, one tile per block.
 // Buckets stay unsorted: the engine ranks members by value instead.
-__global__ void __launch_bounds__(kTileBlock) p2_size_scatter(const Plan* plan, const uint32_t* __restrict__ size,
+//
+// The same launch finishes the set bookkeeping: n_sets = the exclusive prefix
+// at the first cell of digit 255 (every set below 255 members) + the large
+// sets p2_tiles counted; n_cand = the number of singletons (the first multi
+// set in the (size, bit) order); and stage A as a bitset over P (ballots of
+// the byte flags p2_scatter wrote) with its population count.
+__global__ void __launch_bounds__(kTileBlock) p2_size_scatter(Plan* plan, const uint32_t* __restrict__ size,
                                                               const uint32_t* __restrict__ table,
-                                                              uint32_t* __restrict__ sets, const uint32_t* status) {
+                                                              uint32_t* __restrict__ sets,
+                                                              const uint8_t* __restrict__ flags,
+                                                              uint32_t* __restrict__ selbits, const uint32_t* status) {
   constexpr int kW = kTileBlock / 32;
   __shared__ uint32_t wcnt[kW][256];
+  __shared__ uint32_t bsum;
   if (failed(status) || !p2_active(plan)) return;
   const uint64_t m = plan->m;
   const uint64_t ntiles = (m + kTile - 1) / kTile;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    plan->n_sets = table[kBigSet * ntiles] + plan->n_large;
+    const uint64_t n1 = table[2 * ntiles] - table[1 * ntiles];  // sets of size 1
+    plan->n_multi = plan->n_sets - n1;
+    plan->n_cand = n1;
+  }
+  {  // stage A
+    if (threadIdx.x == 0) bsum = 0;
+    __syncthreads();
+    const uint64_t n = plan->n_pos;
+    const uint64_t nw = (n + 31) / 32;
+    const uint64_t warps = static_cast<uint64_t>(gridDim.x) * kW;
+    uint32_t c = 0;
+    for (uint64_t w = blockIdx.x * static_cast<uint64_t>(kW) + warp; w < nw; w += warps) {
+      const uint64_t p = 32 * w + lane;
+      const unsigned bits = __ballot_sync(kFull, p < n && flags[p]);
+      if (lane == 0) selbits[w] = bits;
+      c += __popc(bits);
+    }
+    if (lane == 0 && c) atomicAdd(&bsum, c);
+    __syncthreads();  // one global atomic per block
+    if (threadIdx.x == 0 && bsum) atomicAdd(reinterpret_cast<unsigned long long*>(&plan->n_single_sel), bsum);
+  }
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     for (int w = 0; w < kW; ++w) wcnt[w][threadIdx.x] = 0;
     __syncthreads();
@@ -308,10 +324,9 @@ __global__ void __launch_bounds__(kTileBlock) p2_size_scatter(const Plan* plan, 
 // (bloom.cpp:166-172).  Nothing to do in practice (it takes 255 positives
 // probing one bit); when there is, one block merge-sorts the composite keys
 // size << 32 | bit (all distinct) with a binary-search merge per pass.
-__global__ void __launch_bounds__(1024) p2_sort_large(const Plan* plan, const uint32_t* __restrict__ size,
-                                                      uint32_t* sets, uint64_t* ka, uint64_t* kb,
-                                                      const uint32_t* status) {
-  if (failed(status) || !p2_active(plan)) return;
+// Run by the engine's block before its first round (one block of 1024).
+__device__ void p2_sort_large(const Plan* plan, const uint32_t* __restrict__ size, uint32_t* sets, uint64_t* ka,
+                              uint64_t* kb) {
   const uint64_t n = plan->n_large;
   if (n < 2) return;
   uint32_t* big = sets + (plan->n_sets - n);
@@ -341,24 +356,6 @@ __global__ void __launch_bounds__(1024) p2_sort_large(const Plan* plan, const ui
   for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) big[i] = static_cast<uint32_t>(src[i]);
 }
 
-// stage A as a bitset over P (ballot of the byte flags, one word per warp
-// iteration) and its population count
-__global__ void p2_stage_a(Plan* plan, const uint8_t* __restrict__ flags, uint32_t* __restrict__ selbits,
-                           const uint32_t* status) {
-  if (failed(status) || !p2_active(plan)) return;
-  const uint64_t n = plan->n_pos;
-  const uint64_t nw = (n + 31) / 32;
-  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x / 32);
-  uint32_t c = 0;
-  for (uint64_t w = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) / 32; w < nw; w += warps) {
-    const uint64_t p = 32 * w + (threadIdx.x & 31);
-    const unsigned bits = __ballot_sync(kFull, p < n && flags[p]);
-    if ((threadIdx.x & 31) == 0) selbits[w] = bits;
-    c += __popc(bits);
-  }
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(reinterpret_cast<unsigned long long*>(&plan->n_single_sel), c);
-}
-
 __device__ __forceinline__ bool bs_test(const uint32_t* bs, uint32_t p) { return (bs[p >> 5] >> (p & 31)) & 1u; }
 
 // Stage B, windowed: 1024 consecutive visits per round, one thread each.
@@ -373,27 +370,27 @@ __device__ __forceinline__ bool bs_test(const uint32_t* bs, uint32_t p) { return
 // visit, so every round commits >= 1 visit and the result equals the
 // sequential loop of bloom.cpp:198-219 bit for bit.
 template <bool kSmem>
-__device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __restrict__ sets,
+__device__ __forceinline__ void p2_engine_body(Plan* plan, uint32_t* sets,
                                                const uint32_t* __restrict__ off, const uint32_t* __restrict__ size,
                                                const uint32_t* __restrict__ members,
-                                               const uint32_t* __restrict__ single, uint32_t* selbits,
+                                               uint64_t* ka, uint64_t* kb, uint32_t* selbits,
                                                uint32_t* first_touch, uint32_t* status);
 
 template <bool kSmem>
-__global__ void __launch_bounds__(1024) p2_engine_win(Plan* plan, const uint32_t* __restrict__ sets,
+__global__ void __launch_bounds__(1024) p2_engine_win(Plan* plan, uint32_t* sets,
                                                       const uint32_t* __restrict__ off,
                                                       const uint32_t* __restrict__ size,
                                                       const uint32_t* __restrict__ members,
-                                                      const uint32_t* __restrict__ single, uint32_t* selbits,
+                                                      uint64_t* ka, uint64_t* kb, uint32_t* selbits,
                                                       uint32_t* first_touch, uint32_t* status) {
-  p2_engine_body<kSmem>(plan, sets, off, size, members, single, selbits, first_touch, status);
+  p2_engine_body<kSmem>(plan, sets, off, size, members, ka, kb, selbits, first_touch, status);
 }
 
 template <bool kSmem>
-__device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __restrict__ sets,
+__device__ __forceinline__ void p2_engine_body(Plan* plan, uint32_t* sets,
                                                const uint32_t* __restrict__ off, const uint32_t* __restrict__ size,
                                                const uint32_t* __restrict__ members,
-                                               const uint32_t* __restrict__ single, uint32_t* selbits,
+                                               uint64_t* ka, uint64_t* kb, uint32_t* selbits,
                                                uint32_t* first_touch, uint32_t* status) {
   extern __shared__ uint32_t sbits[];
   __shared__ uint64_t sh[40];
@@ -402,6 +399,8 @@ __device__ __forceinline__ void p2_engine_body(Plan* plan, const uint32_t* __res
   __shared__ uint32_t s_vstar, s_rejv, s_cut;
   __shared__ uint64_t s_cdraw, s_csel;
   if (failed(status) || !p2_active(plan)) return;
+  p2_sort_large(plan, size, sets, ka, kb);  // ends with a barrier when it runs
+  __syncthreads();
   constexpr uint32_t W = 1024;
   const uint32_t v = threadIdx.x;
   const uint64_t n = plan->n_pos, r = plan->r;
@@ -567,16 +566,16 @@ constexpr int kSmemBitsBytes = 160 * 1024;
 
 // |P| is only known on the device: run the shared-memory engine when the
 // selection bitset fits, the global-memory one otherwise.
-__global__ void __launch_bounds__(1024) p2_engine_dispatch(Plan* plan, const uint32_t* __restrict__ sets,
+__global__ void __launch_bounds__(1024) p2_engine_dispatch(Plan* plan, uint32_t* sets,
                                                            const uint32_t* __restrict__ off,
                                                            const uint32_t* __restrict__ size,
                                                            const uint32_t* __restrict__ members,
-                                                           const uint32_t* __restrict__ single, uint32_t* selbits,
+                                                           uint64_t* ka, uint64_t* kb, uint32_t* selbits,
                                                            uint32_t* first_touch, uint32_t* status) {
   if (((plan->n_pos + 31) / 32) * 4 <= static_cast<uint64_t>(kSmemBitsBytes))
-    p2_engine_body<true>(plan, sets, off, size, members, single, selbits, first_touch, status);
+    p2_engine_body<true>(plan, sets, off, size, members, ka, kb, selbits, first_touch, status);
   else
-    p2_engine_body<false>(plan, sets, off, size, members, single, selbits, first_touch, status);
+    p2_engine_body<false>(plan, sets, off, size, members, ka, kb, selbits, first_touch, status);
 }
 
 // sel = ascending P[p] for flagged p (bloom.cpp:221 sort), count must be r
@@ -639,32 +638,28 @@ void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t 
   Workspace& w = ctx->ws;
   stage_begin(ctx, decoding ? ST_DEC_P2_SETS : ST_P2_SETS, s);
   const uint64_t m_cap = std::min<uint64_t>(m_bound, w.set_cap);
-  GP_LAUNCH(ctx, p2_zero_counts, ctx->sm_count * 4, 256, 0, s, w.plan, w.p2_count, m_cap, w.status);
-  cudaMemsetAsync(w.p2_alloc, 0, sizeof(uint32_t), s);
-  GP_LAUNCH(ctx, p2_pairs<false>, grid_for(ctx, n_bound * 32, 256), 256, 0, s, w.pos, w.plan, w.pairs, w.p2_rank,
-            w.p2_count, w.pair_cap, w.set_cap, w.status);
-  GP_LAUNCH(ctx, p2_pairs<true>, grid_for(ctx, n_bound, 128), 128, 0, s, w.pos, w.plan, w.pairs, w.p2_rank,
-            w.p2_count, w.pair_cap, w.set_cap, w.status);
+  GP_LAUNCH(ctx, p2_zero_counts, ctx->sm_count * 4, 256, 0, s, w.plan, w.p2_count, m_cap, w.flags, n_bound, w.p2_alloc,
+            w.status);
+  GP_LAUNCH(ctx, p2_pairs, grid_for(ctx, n_bound, 256), 256, 0, s, w.pos, w.plan, w.pairs, w.p2_rank, w.p2_count,
+            w.pair_cap, w.set_cap, w.status);
   const uint64_t mtiles = (m_cap + kTile - 1) / kTile;
   const int tgrid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(mtiles, ctx->sm_count * 8ULL)));
   GP_LAUNCH(ctx, p2_tiles, tgrid, kTileBlock, 0, s, w.p2_count, w.plan, w.p2_off, w.p2_table, w.p2_alloc, w.status);
-  cudaMemsetAsync(w.flags, 0, n_bound, s);
   GP_LAUNCH(ctx, p2_scatter, grid_for(ctx, n_bound * k_bound, 256), 256, 0, s, w.pairs, w.p2_rank, w.plan, w.p2_off,
             w.p2_members, w.flags, w.status);
   launch_table_scan(ctx, w.p2_table, &w.plan->m, m_cap, 12, s);
-  GP_LAUNCH(ctx, p2_count_sets, 1, 32, 0, s, w.plan, w.p2_table, w.status);
-  GP_LAUNCH(ctx, p2_size_scatter, tgrid, kTileBlock, 0, s, w.plan, w.p2_count, w.p2_table, w.p2_sets, w.status);
-  GP_LAUNCH(ctx, p2_sort_large, 1, 1024, 0, s, w.plan, w.p2_count, w.p2_sets, reinterpret_cast<uint64_t*>(w.f64a),
-            reinterpret_cast<uint64_t*>(w.f64b), w.status);
-  GP_LAUNCH(ctx, p2_stage_a, grid_for(ctx, n_bound, 256), 256, 0, s, w.plan, w.flags, w.selbits, w.status);
+  GP_LAUNCH(ctx, p2_size_scatter, tgrid, kTileBlock, 0, s, w.plan, w.p2_count, w.p2_table, w.p2_sets, w.flags,
+            w.selbits, w.status);
   stage_end(ctx, s);
   stage_begin(ctx, decoding ? ST_DEC_P2_ENGINE : ST_P2_ENGINE, s);
   if (((n_bound + 31) / 32) * 4 <= static_cast<uint64_t>(kSmemBitsBytes)) {
     GP_LAUNCH(ctx, p2_engine_win<true>, 1, 1024, ((n_bound + 31) / 32) * 4, s, w.plan, w.p2_sets, w.p2_off,
-              w.p2_count, w.p2_members, w.p2_single, w.selbits, w.first_touch, w.status);
+              w.p2_count, w.p2_members, reinterpret_cast<uint64_t*>(w.f64a), reinterpret_cast<uint64_t*>(w.f64b), w.selbits,
+              w.first_touch, w.status);
   } else {
     GP_LAUNCH(ctx, p2_engine_dispatch, 1, 1024, kSmemBitsBytes, s, w.plan, w.p2_sets, w.p2_off, w.p2_count,
-              w.p2_members, w.p2_single, w.selbits, w.first_touch, w.status);
+              w.p2_members, reinterpret_cast<uint64_t*>(w.f64a), reinterpret_cast<uint64_t*>(w.f64b), w.selbits,
+              w.first_touch, w.status);
   }
   stage_end(ctx, s);
   launch_flags_compact(ctx, GP_INDEX_BLOOM_P2, n_bound, s);
