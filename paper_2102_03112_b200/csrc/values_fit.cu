@@ -123,7 +123,8 @@ __global__ void fit_prepare(const ValSrc values, const uint32_t* __restrict__ ma
     if (map[s] != s) ident = false;
     t[s] = s < l ? values[map[s]] : -values[map[n - 1 - (s - l)]];
   }
-  if (__any_sync(kFull, !ident) && (threadIdx.x & 31) == 0) atomicAnd(&plan->identity, 0u);
+  // one plain store per block at most (per-warp atomics on the flag serialised: ~10 us at C4)
+  if (__syncthreads_or(!ident) && threadIdx.x == 0) plan->identity = 0;
 }
 
 // ---------------------------------------------------------------- segmentation
@@ -717,11 +718,31 @@ __global__ void __launch_bounds__(256) fit_accumulate(const Plan* plan, const do
   }
 }
 
+// Legendre → t-monomial coefficients, P_{j+1} = ((2j+1) t P_j - j P_{j-1}) /
+// (j+1), evaluated at compile time with the same double operations the
+// solver used to run per segment (36 fp64 divisions off its serial path).
+struct LegendreTable {
+  double c[kCps][kCps];
+};
+constexpr LegendreTable make_legendre() {
+  LegendreTable T{};
+  for (int j = 0; j < kCps; ++j)
+    for (int p = 0; p < kCps; ++p) T.c[j][p] = 0.0;
+  T.c[0][0] = 1.0;
+  T.c[1][1] = 1.0;
+  for (int j = 1; j + 1 < kCps; ++j)
+    for (int p = 0; p <= j + 1; ++p)
+      T.c[j + 1][p] = ((2 * j + 1) * (p > 0 ? T.c[j][p - 1] : 0.0) - j * T.c[j - 1][p]) / (j + 1);
+  return T;
+}
+__constant__ LegendreTable kLegendre = make_legendre();
+
 // degree <= 7: one segment per block iteration; thread 0 solves (sizes <= 8x8)
 __global__ void fit_solve(Plan* plan, const double* __restrict__ t, const uint32_t* __restrict__ seg_end,
                           const uint64_t* __restrict__ chunk, const double* __restrict__ partial, float* coeffs,
                           const uint32_t* status) {
   __shared__ double sacc[kAcc];
+  __shared__ double spow[2][kCps];  // alpha^k, beta^k (curvefit.cpp:157-172's pow values), one lane each
   if (failed(status) || !poly_active(plan) || plan->degree > kMaxDeg) return;
   const uint32_t S = plan->nseg;
   const int deg = static_cast<int>(plan->degree);
@@ -729,6 +750,12 @@ __global__ void fit_solve(Plan* plan, const double* __restrict__ t, const uint32
   for (uint32_t seg = blockIdx.x; seg < S; seg += gridDim.x) {
     uint32_t b, e;
     seg_range(seg_end, seg, b, e);
+    if (e - b > 1 && threadIdx.x >= 32 && threadIdx.x < 32 + 2 * kCps) {
+      const uint32_t len = e - b, q = threadIdx.x - 32, k = q % kCps;
+      const double alpha = 2.0 / static_cast<double>(len - 1);
+      const double beta = -static_cast<double>(len + 1) / static_cast<double>(len - 1);
+      spow[q / kCps][k] = pow(q < kCps ? alpha : beta, static_cast<double>(k));
+    }
     {  // chunk partials of this segment, summed in chunk order, one accumulator per thread
       const uint64_t c0 = chunk[seg], ncs = chunk[seg + 1] - c0;
       if (threadIdx.x < kAcc) {
@@ -809,35 +836,20 @@ __global__ void fit_solve(Plan* plan, const double* __restrict__ t, const uint32
           for (int q = i + 1; q < kCps; ++q) v -= L[q][i] * aL[q];  // L[q][i] = 0 for q >= m
           aL[i] = (i < m && L[i][i] > 0.0) ? v / L[i][i] : 0.0;
         }
-        // Legendre → t-monomials: P_{j+1} = ((2j+1) t P_j - j P_{j-1}) / (j+1)
-        double Lc[kCps][kCps];
-#pragma unroll
-        for (int j = 0; j < kCps; ++j)
-#pragma unroll
-          for (int p = 0; p < kCps; ++p) Lc[j][p] = 0.0;
-        Lc[0][0] = 1.0;
-        Lc[1][1] = 1.0;
-#pragma unroll
-        for (int j = 1; j + 1 < kCps; ++j)
-#pragma unroll
-          for (int p = 0; p <= j + 1; ++p)
-            Lc[j + 1][p] = ((2 * j + 1) * (p > 0 ? Lc[j][p - 1] : 0.0) - j * Lc[j - 1][p]) / (j + 1);
         double ct[kCps];
 #pragma unroll
         for (int p = 0; p < kCps; ++p) {
           double v = 0.0;
 #pragma unroll
-          for (int j = p; j < kCps; ++j) v += aL[j] * Lc[j][p];  // aL[j] = 0 for j >= m
+          for (int j = p; j < kCps; ++j) v += aL[j] * kLegendre.c[j][p];  // aL[j] = 0 for j >= m
           ct[p] = v;
         }
         // t-monomials → x-monomials, curvefit.cpp:157-172 (the same pow() values)
-        const double alpha = 2.0 / static_cast<double>(len - 1);
-        const double beta = -static_cast<double>(len + 1) / static_cast<double>(len - 1);
         double pa[kCps], pb[kCps];
 #pragma unroll
         for (int k = 0; k < kCps; ++k) {
-          pa[k] = k < m ? pow(alpha, static_cast<double>(k)) : 0.0;
-          pb[k] = k < m ? pow(beta, static_cast<double>(k)) : 0.0;
+          pa[k] = k < m ? spow[0][k] : 0.0;
+          pb[k] = k < m ? spow[1][k] : 0.0;
         }
         constexpr double kBinom[kCps][kCps] = {{1, 0, 0, 0, 0, 0, 0, 0},       {1, 1, 0, 0, 0, 0, 0, 0},
                                                {1, 2, 1, 0, 0, 0, 0, 0},       {1, 3, 3, 1, 0, 0, 0, 0},
