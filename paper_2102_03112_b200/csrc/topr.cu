@@ -393,6 +393,79 @@ __device__ __forceinline__ uint64_t final_counts(const uint32_t* __restrict__ ci
 }
 
 // writes the warp's kept entries; A = kept output offset, B = T-ties before the segment
+// The dense selection's two passes over a warp segment of 8-key groups
+// [glo, ghi): kCount counts the keys >= klo (per-lane popcounts, one warp sum
+// at the end); otherwise the kept (index, value) pairs of each 512-key round
+// are staged in the warp's shared buffers at their in-round rank and copied
+// out by consecutive lanes to consecutive addresses (a per-lane run of
+// direct stores scattered 32 partial sectors per store instruction; at r =
+// 60% of d that was most of the select's time).
+template <bool kCount>
+__device__ __forceinline__ uint32_t dense_pass(const float* __restrict__ g, uint64_t glo, uint64_t ghi, uint64_t d,
+                                               bool aligned, uint32_t klo, uint32_t* sbi, float* sbv,
+                                               uint32_t* __restrict__ oi, float* __restrict__ ov, uint64_t at) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  uint32_t nc = 0;
+  for (uint64_t base = glo; base < ghi; base += 64) {
+    float v[2][kGroup];
+    uint64_t k0[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint64_t j = base + 32 * u + lane;
+      k0[u] = j < ghi ? j * kGroup : d;
+      if (k0[u] >= d) {
+#pragma unroll
+        for (int q = 0; q < kGroup; ++q) v[u][q] = 0.0f;
+      } else if (aligned && k0[u] + kGroup <= d) {
+        const float4 a = __ldcg(reinterpret_cast<const float4*>(g + k0[u]));
+        const float4 b = __ldcg(reinterpret_cast<const float4*>(g + k0[u]) + 1);
+        v[u][0] = a.x; v[u][1] = a.y; v[u][2] = a.z; v[u][3] = a.w;
+        v[u][4] = b.x; v[u][5] = b.y; v[u][6] = b.z; v[u][7] = b.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < kGroup; ++q) v[u][q] = k0[u] + q < d ? g[k0[u] + q] : 0.0f;
+      }
+    }
+    uint32_t mask[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      mask[u] = 0;
+#pragma unroll
+      for (int q = 0; q < kGroup; ++q)
+        if (k0[u] + q < d && key_of(v[u][q]) >= klo) mask[u] |= 1u << q;
+    }
+    if (kCount) {
+      nc += __popc(mask[0]) + __popc(mask[1]);
+      continue;
+    }
+    uint32_t o = 0;  // in-round rank: group (u, lane) order is index order
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint32_t c = __popc(mask[u]);
+      const uint32_t incl = warp_inclusive_sum(c);
+      uint32_t p = o + incl - c;
+#pragma unroll
+      for (int q = 0; q < kGroup; ++q)
+        if (mask[u] >> q & 1u) {
+          sbi[p] = static_cast<uint32_t>(k0[u] + q);
+          sbv[p] = v[u][q];
+          ++p;
+        }
+      o += __shfl_sync(kFull, incl, 31);
+    }
+    __syncwarp();
+    for (uint32_t k = lane; k < o; k += 32) {
+      oi[at + nc + k] = sbi[k];
+      ov[at + nc + k] = sbv[k];
+    }
+    __syncwarp();
+    nc += o;
+    (void)lt;
+  }
+  return kCount ? warp_sum(nc) : nc;
+}
+
 __device__ __forceinline__ void final_write(const uint32_t* __restrict__ cidx, const float* __restrict__ cval,
                                             uint64_t lo, uint64_t hi, uint32_t T, uint64_t q, uint64_t out,
                                             uint64_t ties, uint32_t* sidx, float* sval) {
@@ -500,8 +573,14 @@ __global__ void __launch_bounds__(kCandBlock) topr_select(
     const uint64_t lo = slot + warp * wseg < d ? slot + warp * wseg : d;
     const uint64_t hi = lo + wseg < d ? lo + wseg : d;
     if (dense) {  // count now; the write pass follows (below, or straight to the support when b* is kept whole)
-      const uint32_t nd = stream_dense(g, lo / kGroup, (hi + kGroup - 1) / kGroup, d, aligned, klo, khi,
-                                       [](uint32_t, uint32_t, float) {}, tie);
+      uint32_t nd;
+      if (full) {  // no tie histogram needed: count only
+        nd = dense_pass<true>(g, lo / kGroup, (hi + kGroup - 1) / kGroup, d, aligned, klo, nullptr, nullptr,
+                              nullptr, nullptr, 0);
+      } else {
+        nd = stream_dense(g, lo / kGroup, (hi + kGroup - 1) / kGroup, d, aligned, klo, khi,
+                          [](uint32_t, uint32_t, float) {}, tie);
+      }
       if (lane == 0) wcnt[c * kCandWarps + warp] = nd;
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -566,12 +645,8 @@ __global__ void __launch_bounds__(kCandBlock) topr_select(
       for (int w = 0; w < warp; ++w) at += __ldcg(wcnt + c * kCandWarps + w);
       uint32_t* oi = full ? sidx : cidx;
       float* ov = full ? sval : cval;
-      stream_dense(g, lo / kGroup, (hi + kGroup - 1) / kGroup, d, aligned, klo, khi,
-                   [&](uint32_t o, uint32_t idx, float v) {
-                     oi[at + o] = idx;
-                     ov[at + o] = v;
-                   },
-                   [](uint32_t) {});
+      dense_pass<false>(g, lo / kGroup, (hi + kGroup - 1) / kGroup, d, aligned, klo, bidx[warp], bval[warp], oi, ov,
+                        at);
       __syncthreads();
     }
     if (full) {
