@@ -176,6 +176,7 @@ void carve(Workspace& w, uint8_t* base, uint64_t D) {
   Carver c{base, 0};
   w.plan = c.take<Plan>(1);
   w.status = c.take<uint32_t>(64);
+  w.status_pre = c.take<uint32_t>(64);
   w.tiles_cap = 4 * (D / 1024) + 4096;
   w.scan_base = c.take<uint8_t>(128 + w.tiles_cap * 8);
   w.ticket = reinterpret_cast<uint32_t*>(w.scan_base);
@@ -294,8 +295,15 @@ int gp_ctx_create(int device, uint64_t max_d, gp_ctx** out) {
   if (e == cudaSuccess) e = cudaMemset(ctx->ws.plan, 0, sizeof(Plan));
   if (e == cudaSuccess) e = cudaMemset(ctx->ws.huff, 0, sizeof(HuffTable));  // empty Huffman table cache
   if (e == cudaSuccess) e = cudaMemset(ctx->ws.seg_state, 0, 8 * sizeof(uint32_t));  // fit segmentation control words
+  if (e == cudaSuccess) e = cudaMemset(ctx->ws.status_pre, 0, 64 * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess || crc_tables_init(ctx) != GP_OK) {
+    if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     cudaFree(base);
     delete ctx;
     return GP_CUDA;
@@ -307,6 +315,9 @@ int gp_ctx_create(int device, uint64_t max_d, gp_ctx** out) {
 void gp_ctx_destroy(gp_ctx* ctx) {
   if (!ctx) return;
   for (auto& e : ctx->prof.pool) cudaEventDestroy(e);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->ws.base) cudaFree(ctx->ws.base);
   delete ctx;
 }
@@ -634,61 +645,82 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const u
     h.index_method = hdr[6];
     h.value_method = hdr[7];
   }
-  // parse + CRC verdict always run first: the reference reports header and
-  // checksum errors before it looks at the method ids
-  GP_STAGE(ctx, ST_DEC_PARSE, s, launch_parse_container(ctx, d_in, len, d_len, hint ? &h : nullptr, s));
+  // parse, then the CRC verdict; the decode work that does not touch the
+  // caller's output (index and value decoders, into workspace buffers) runs
+  // on the context's side stream concurrently with the CRC, its errors held
+  // in a second status word and merged after the verdict in stream order
+  // (container.cu parse_container / merge_status), so error precedence is
+  // the reference's: header, checksum, post-CRC checks, method decoders
+  GP_STAGE(ctx, ST_DEC_PARSE, s, launch_parse_container(ctx, d_in, len, d_len, hint ? &h : nullptr, s);
+           cudaEventRecord(ctx->ev_fork, s); launch_verify_crc(ctx, d_in, s));
+  cudaStream_t ps = ctx->side;
+  cudaStreamWaitEvent(ps, ctx->ev_fork, 0);
+  auto join = [&]() {
+    cudaEventRecord(ctx->ev_join, ps);
+    cudaStreamWaitEvent(s, ctx->ev_join, 0);
+  };
   const int im = h.index_method, vm = h.value_method;
   const bool known = im <= GP_INDEX_BLOOM_NAIVE && vm <= GP_VALUE_RAW_F64;
   if (known && (!index_supported(im) || !value_supported(vm))) {
+    join();
     // surface header/CRC errors first, then report the unsupported method
     const int st = gp_ctx_status(ctx, stream);
     if (st != GP_OK) return st;
     return set_error(ctx, GP_UNSUPPORTED, "method not implemented on the device path");
   }
-  if (!known) return check_launch(ctx, "decode");  // the CRC verdict step latches UnknownMethod
+  if (!known) {  // the CRC verdict step latches UnknownMethod
+    join();
+    return check_launch(ctx, "decode");
+  }
   const uint64_t bound = ctx->max_d;
   // bitmap + raw values into a dense buffer (or a prepare for one): the fused
   // dense path (dense.cu) — per-tile counts and checks now, one scatter pass
   // reading bitmap words and value runs, no materialised support
   const bool fused = im == GP_INDEX_BITMAP && (vm == GP_VALUE_NONE || vm == GP_VALUE_RAW_F64) && !own &&
                      !d_support && !d_dense64 && (d_dense || !scatter);
+  Workspace& w = ctx->ws;
+  uint32_t* const main_status = w.status;
+  w.status = w.status_pre;  // every pre-verdict launch latches into the second word
   if (own && im != GP_INDEX_BLOOM_NAIVE) {
-    if (!is_bloom(im)) launch_own_support(ctx, bound, s);
+    if (!is_bloom(im)) launch_own_support(ctx, bound, ps);
   } else switch (im) {
-    case GP_INDEX_NONE: launch_decode_index_none(ctx, d_in, bound, s); break;
+    case GP_INDEX_NONE: launch_decode_index_none(ctx, d_in, bound, ps); break;
     case GP_INDEX_BITMAP:
       if (fused) {
-        GP_STAGE(ctx, ST_DEC_INDEX, s, launch_decode_bitmap_check(ctx, d_in, s); launch_bm_prepare(ctx, d_in, bound, s));
+        GP_STAGE(ctx, ST_DEC_INDEX, ps, launch_decode_bitmap_check(ctx, d_in, ps); launch_bm_prepare(ctx, d_in, bound, ps));
       } else {
-        launch_decode_index_bitmap(ctx, d_in, bound, s);
+        launch_decode_index_bitmap(ctx, d_in, bound, ps);
       }
       break;
-    case GP_INDEX_RLE: GP_STAGE(ctx, ST_DEC_INDEX, s, launch_decode_index_rle(ctx, d_in, len, bound, s)); break;
-    case GP_INDEX_HUFFMAN: GP_STAGE(ctx, ST_DEC_INDEX, s, launch_decode_index_huffman(ctx, d_in, len, s)); break;
+    case GP_INDEX_RLE: GP_STAGE(ctx, ST_DEC_INDEX, ps, launch_decode_index_rle(ctx, d_in, len, bound, ps)); break;
+    case GP_INDEX_HUFFMAN: GP_STAGE(ctx, ST_DEC_INDEX, ps, launch_decode_index_huffman(ctx, d_in, len, ps)); break;
     default: {
-      GP_STAGE(ctx, ST_DEC_BLOOM_SCAN, s, launch_bloom_parse(ctx, d_in, ctx->ws.m_cap, s);
-                                           launch_bloom_scan(ctx, bound, 0, true, s));
+      GP_STAGE(ctx, ST_DEC_BLOOM_SCAN, ps, launch_bloom_parse(ctx, d_in, ctx->ws.m_cap, ps);
+                                           launch_bloom_scan(ctx, bound, 0, true, ps));
       if (im == GP_INDEX_BLOOM_P2)
-        launch_select_p2(ctx, bound, ctx->ws.set_cap, 64, true, s);
+        launch_select_p2(ctx, bound, ctx->ws.set_cap, 64, true, ps);
       else if (im == GP_INDEX_BLOOM_P1)
-        GP_STAGE(ctx, ST_DEC_SELECT, s, launch_select_p1(ctx, bound, bound, s));
+        GP_STAGE(ctx, ST_DEC_SELECT, ps, launch_select_p1(ctx, bound, bound, ps));
       else
-        GP_STAGE(ctx, ST_DEC_SELECT, s, launch_select_slice(ctx, bound, s));
+        GP_STAGE(ctx, ST_DEC_SELECT, ps, launch_select_slice(ctx, bound, ps));
     }
   }
   switch (vm) {
     case GP_VALUE_NONE:
-    case GP_VALUE_RAW_F64: launch_values_raw_check(ctx, s); break;
+    case GP_VALUE_RAW_F64: launch_values_raw_check(ctx, ps); break;
     case GP_VALUE_FIT_POLY:
-    case GP_VALUE_FIT_DEXP: GP_STAGE(ctx, ST_DEC_VALUES, s, launch_decode_fit(ctx, d_in, bound, s)); break;
-    case GP_VALUE_QUANT: GP_STAGE(ctx, ST_DEC_VALUES, s, launch_decode_quant(ctx, d_in, bound, s)); break;
+    case GP_VALUE_FIT_DEXP: GP_STAGE(ctx, ST_DEC_VALUES, ps, launch_decode_fit(ctx, d_in, bound, ps)); break;
+    case GP_VALUE_QUANT: GP_STAGE(ctx, ST_DEC_VALUES, ps, launch_decode_quant(ctx, d_in, bound, ps)); break;
     case GP_VALUE_DEFLATE_SLOT:
-      launch_decode_slot(ctx, d_in, s);
-      GP_STAGE(ctx, ST_DEC_VALUES, s, launch_decode_inflate(ctx, d_in, bound, s));
+      launch_decode_slot(ctx, d_in, ps);
+      GP_STAGE(ctx, ST_DEC_VALUES, ps, launch_decode_inflate(ctx, d_in, bound, ps));
       break;
     default: break;
   }
-  if ((im == GP_INDEX_NONE || im == GP_INDEX_HUFFMAN) && !own) launch_validate_support(ctx, bound, s);
+  if ((im == GP_INDEX_NONE || im == GP_INDEX_HUFFMAN) && !own) launch_validate_support(ctx, bound, ps);
+  w.status = main_status;
+  join();
+  launch_merge_status(ctx, s);
   if (scatter && fused) {
     GP_STAGE(ctx, ST_DEC_SCATTER, s,
              launch_bm_scatter(ctx, d_in, bound, d_dense, dense_d, scale, ctx->decode_overwrite, s));

@@ -217,27 +217,39 @@ __global__ void __launch_bounds__(kCrcBlock) crc_chunks(const uint8_t* __restric
 }
 
 // unpack (container.cpp:84-127) up to, but not including, the CRC verdict.
+//
+// `pre` is the status word of the decode work that runs before the verdict,
+// concurrently with the CRC (capi.cu decode_common): it starts as a copy of
+// the main status, and every error found here — header errors and the
+// post-CRC checks — goes to it at once, so that work never runs on a plan
+// this kernel rejected; the main status gets the post-CRC checks only from
+// the CRC kernel, after its verdict.
 __global__ void parse_container(const uint8_t* __restrict__ in, uint64_t len_host, const uint64_t* len_dev,
                                 uint64_t max_d, Plan* plan, const gp_pipeline_config hint, int use_hint,
-                                uint32_t* status) {
+                                uint32_t* status, uint32_t* pre) {
+  *pre = *status;
   if (failed(status)) return;
+  auto fail = [&](uint32_t code) {
+    latch(status, code);
+    latch(pre, code);
+  };
   const uint64_t len = len_dev ? *len_dev : len_host;
-  if (len_dev && len > len_host) return latch(status, GP_CAPACITY);  // len_host is the buffer capacity
-  if (len < 4) return latch(status, GP_TRUNCATED);
-  if (in[0] != 'D' || in[1] != 'R' || in[2] != 'C' || in[3] != '1') return latch(status, GP_CORRUPT_PAYLOAD);
-  if (len < 6) return latch(status, GP_TRUNCATED);
+  if (len_dev && len > len_host) return fail(GP_CAPACITY);  // len_host is the buffer capacity
+  if (len < 4) return fail(GP_TRUNCATED);
+  if (in[0] != 'D' || in[1] != 'R' || in[2] != 'C' || in[3] != '1') return fail(GP_CORRUPT_PAYLOAD);
+  if (len < 6) return fail(GP_TRUNCATED);
   const uint32_t version = in[4] | (in[5] << 8);
-  if (version != 1) return latch(status, GP_DECODE);
-  if (len < 49) return latch(status, GP_TRUNCATED);
+  if (version != 1) return fail(GP_DECODE);
+  if (len < 49) return fail(GP_TRUNCATED);
   const uint8_t index_id = in[6], value_id = in[7], flags = in[8];
   const uint64_t d = ld_u64_unaligned(in + 9), r = ld_u64_unaligned(in + 17);
   const uint64_t il = ld_u64_unaligned(in + 25), vl = ld_u64_unaligned(in + 33), rl = ld_u64_unaligned(in + 41);
   const uint64_t body = il + vl + rl + 4;  // u64 wrap-around, as in the reference
   const uint64_t rem = len - 49;
-  if (rem < body) return latch(status, GP_TRUNCATED);
-  if (rem > body) return latch(status, GP_CORRUPT_PAYLOAD);
+  if (rem < body) return fail(GP_TRUNCATED);
+  if (rem > body) return fail(GP_CORRUPT_PAYLOAD);
   // bounds of the individual spans (guards against wrapped sums)
-  if (il > rem || vl > rem || rl > rem) return latch(status, GP_TRUNCATED);
+  if (il > rem || vl > rem || rl > rem) return fail(GP_TRUNCATED);
   plan->d = d;
   plan->r = r;
   plan->il = il;
@@ -262,6 +274,14 @@ __global__ void parse_container(const uint8_t* __restrict__ in, uint64_t len_hos
   else if (use_hint && (index_id != hint.index_method || value_id != hint.value_method)) post = GP_UNSUPPORTED;
   else if (d > max_d) post = GP_CAPACITY;
   plan->post_crc_error = post;
+  if (post) latch(pre, post);
+}
+
+// After the join of the pre-verdict work: its first error, if the verdict and
+// everything before it passed (the reference's order: header, CRC, post-CRC
+// checks, then the method decoders in stream order).
+__global__ void merge_status(uint32_t* status, const uint32_t* pre) {
+  if (!failed(status) && *pre) latch(status, *pre);
 }
 
 
@@ -348,12 +368,21 @@ void launch_parse_container(gp_ctx* ctx, const uint8_t* in, uint64_t len, const 
   Workspace& w = ctx->ws;
   gp_pipeline_config h{};
   if (hint) h = *hint;
-  GP_LAUNCH(ctx, parse_container, 1, 1, 0, s, in, len, len_dev, ctx->max_d, w.plan, h, hint ? 1 : 0, w.status);
+  GP_LAUNCH(ctx, parse_container, 1, 1, 0, s, in, len, len_dev, ctx->max_d, w.plan, h, hint ? 1 : 0, w.status,
+            w.status_pre);
+}
+
+void launch_verify_crc(gp_ctx* ctx, const uint8_t* in, cudaStream_t s) {
+  Workspace& w = ctx->ws;
   uint32_t* crc = reinterpret_cast<uint32_t*>(&w.plan->crc_calc);
   CrcEpilogue ep;
   ep.mode = 1;
   ep.plan = w.plan;
   crc_range(ctx, in, &w.plan->off_index, 0, &w.plan->il, &w.plan->vl, &w.plan->rl, 0, crc, s, ep);
+}
+
+void launch_merge_status(gp_ctx* ctx, cudaStream_t s) {
+  GP_LAUNCH(ctx, merge_status, 1, 1, 0, s, ctx->ws.status, ctx->ws.status_pre);
 }
 
 void launch_crc_host_range(gp_ctx* ctx, const uint8_t* data, uint64_t n, uint32_t* out, cudaStream_t s) {

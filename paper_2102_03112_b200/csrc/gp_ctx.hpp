@@ -76,6 +76,7 @@ struct Workspace {
   size_t bytes_total = 0;
   Plan* plan = nullptr;
   uint32_t* status = nullptr;
+  uint32_t* status_pre = nullptr;  // status of the decode work launched before the CRC verdict (container.cu)
   uint8_t* scan_base = nullptr;   // [128 B tickets | tile descriptors], zeroed per scan
   uint32_t* ticket = nullptr;     // 32 tickets (first 128 B of scan_base)
   uint64_t* tiles = nullptr;      // scan tile descriptors
@@ -172,7 +173,9 @@ struct gp_ctx {
   const uint64_t* seed_dev = nullptr;  // gp_ctx_set_seed_source: pipeline seed read on the device
   cudaEvent_t index_event = nullptr;   // gp_ctx_set_index_event: recorded once encode's index payload is final
   bool decode_overwrite = false;
-  const double* vals64 = nullptr;      // this encode's f64 value sequence (null: ws.values, f32)       // gp_ctx_set_decode_overwrite: dense = scale * decoded (zeros off the support)
+  const double* vals64 = nullptr;      // this encode's f64 value sequence (null: ws.values, f32)
+  cudaStream_t side = nullptr;         // decode work before the CRC verdict runs here, beside the CRC
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;       // gp_ctx_set_decode_overwrite: dense = scale * decoded (zeros off the support)
 };
 
 namespace gp {
@@ -239,6 +242,8 @@ void launch_finish_container(gp_ctx* ctx, uint8_t* out, uint64_t cap, uint64_t* 
                              cudaStream_t s);
 void launch_parse_container(gp_ctx* ctx, const uint8_t* in, uint64_t len, const uint64_t* len_dev,
                             const gp_pipeline_config* hint, cudaStream_t s);
+void launch_verify_crc(gp_ctx* ctx, const uint8_t* in, cudaStream_t s);
+void launch_merge_status(gp_ctx* ctx, cudaStream_t s);
 
 // indexcodec.cu
 void launch_index_none(gp_ctx* ctx, uint8_t* out, uint64_t r, cudaStream_t s);
