@@ -76,7 +76,10 @@ GP_API void gp_pipeline_config_default(gp_pipeline_config* cfg);
 typedef struct gp_ctx gp_ctx;
 
 /* One context per (device, stream user).  The workspace is sized once for
- * gradients of up to max_d elements; no allocation happens inside a step. */
+ * gradients of up to max_d elements; no allocation happens inside a step.
+ * The context also owns a second stream: a decode forks its index and value
+ * decoders onto it beside the CRC verdict (event fork/join, so the caller's
+ * stream — captured into a CUDA graph or not — sees one ordered call). */
 GP_API int gp_ctx_create(int device, uint64_t max_d, gp_ctx** out);
 GP_API void gp_ctx_destroy(gp_ctx* ctx);
 GP_API const char* gp_last_error(const gp_ctx* ctx);
