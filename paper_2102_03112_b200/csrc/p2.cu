@@ -629,7 +629,11 @@ void launch_flags_compact(gp_ctx* ctx, int method, uint64_t n_bound, cudaStream_
   Workspace& w = ctx->ws;
   const uint64_t ptiles = (n_bound + kTile - 1) / kTile;
   reset_scan(ctx, s, ptiles + 1);
-  GP_LAUNCH(ctx, flags_compact, grid_for(ctx, ptiles * kTileBlock, kTileBlock), kTileBlock, 0, s, w.pos, w.selbits,
+  // tiles are claimed in a loop: two blocks per SM cover any |P| (the host
+  // bound is d; at C4 |P| is ~1% of it and most of a d-sized grid would exit)
+  GP_LAUNCH(ctx, flags_compact,
+            static_cast<int>(std::min<uint64_t>(std::max<uint64_t>(ptiles, 1), 2ull * ctx->sm_count)), kTileBlock, 0, s,
+            w.pos, w.selbits,
             w.plan, method, w.sel, w.tiles, w.ticket, w.status);
 }
 

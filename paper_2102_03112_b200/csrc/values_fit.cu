@@ -1585,7 +1585,11 @@ void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, 
     ++ctx->launches;
   }
   const uint64_t seg_bound = std::min<uint64_t>(n_bound, w.seg_cap);
-  GP_LAUNCH(ctx, fit_accumulate, grid_for(ctx, (n_bound / kChunk + seg_bound + 1) * 256, 256), 256, 0, s, w.plan,
+  // 140 registers: one resident block per SM, so a grid beyond the SM count
+  // only adds waves of blocks that find no chunk (grid-stride over chunks)
+  GP_LAUNCH(ctx, fit_accumulate,
+            static_cast<int>(std::min<uint64_t>(n_bound / kChunk + seg_bound + 1, static_cast<uint64_t>(ctx->sm_count))),
+            256, 0, s, w.plan,
             w.f64b, w.seg_end, w.seg_chunk, w.partial, w.status);
   GP_LAUNCH(ctx, fit_solve, grid_for(ctx, seg_bound * 64, 64), 64, 0, s, w.plan, w.f64b, w.seg_end, w.seg_chunk,
             w.partial, w.coeffs, w.status);
