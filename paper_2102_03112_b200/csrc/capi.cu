@@ -105,6 +105,11 @@ __global__ void init_plan(Plan* plan, PlanInit p) {
   plan->minv = p.minv;
   plan->scan_lo = 0;  // full-range positive scans unless gp_bloom_scan_range narrows it
   plan->scan_hi = 0;
+  // the value codec's accumulators and flags (values_fit.cu)
+  plan->sign_split = 0;
+  plan->identity = 1;
+  plan->fit_kind = 0;
+  plan->dexp_fail = 0;
 }
 
 // Simulation::pipeline_seed(seed, worker, *step) (harness.cpp:201-203, over

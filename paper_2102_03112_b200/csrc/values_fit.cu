@@ -1532,20 +1532,13 @@ __global__ void dexp_decide(Plan* plan, const uint32_t* status) {
 void launch_radix_sort(gp_ctx* ctx, uint32_t* keys, uint32_t* vals, uint32_t* ktmp, uint32_t* vtmp,
                        const uint64_t* n_dev, uint64_t n_bound, int bits, cudaStream_t s);
 
-__global__ void fit_reset(Plan* plan) {
-  plan->sign_split = 0;
-  plan->identity = 1;
-  plan->fit_kind = 0;
-  plan->dexp_fail = 0;
-}
-
 static_assert(sizeof(SegNode) == 32, "workspace sizes SegNode at 32 bytes");
 static_assert(sizeof(SegState) == 32, "workspace sizes SegState at 32 bytes");
 
 void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, uint64_t n_bound, cudaStream_t s,
                        bool dexp) {
   Workspace& w = ctx->ws;
-  GP_LAUNCH(ctx, fit_reset, 1, 1, 0, s, w.plan);
+  // sign_split / identity / fit_kind / dexp_fail: reset by the encode's init_plan (capi.cu)
   const ValSrc vals{w.values, ctx->vals64};
   GP_LAUNCH(ctx, fit_keys, grid_for(ctx, n_bound, 256), 256, 0, s, vals, w.plan, w.u32a, w.u32b, w.status);
   launch_radix_sort(ctx, w.u32a, w.u32b, w.u32c, w.u32d, &w.plan->n_values, n_bound, 32, s);
