@@ -369,29 +369,16 @@ __device__ __forceinline__ bool bs_test(const uint32_t* bs, uint32_t p) { return
 // selection that reaches r.  The next window starts at the first uncommitted
 // visit, so every round commits >= 1 visit and the result equals the
 // sequential loop of bloom.cpp:198-219 bit for bit.
-template <bool kSmem>
+// kSmem: the selection bitset lives in shared memory; kFt: so does the
+// per-positive first-touch table (every visit's atomicMin and the dependency
+// reads become shared-memory operations instead of L2 round trips — two of
+// a round's dependent global chains; |P| up to ~48k, e.g. a C5 bucket)
+template <bool kSmem, bool kFt>
 __device__ __forceinline__ void p2_engine_body(Plan* plan, uint32_t* sets,
                                                const uint32_t* __restrict__ off, const uint32_t* __restrict__ size,
                                                const uint32_t* __restrict__ members,
                                                uint64_t* ka, uint64_t* kb, uint32_t* selbits,
-                                               uint32_t* first_touch, uint32_t* status);
-
-template <bool kSmem>
-__global__ void __launch_bounds__(1024) p2_engine_win(Plan* plan, uint32_t* sets,
-                                                      const uint32_t* __restrict__ off,
-                                                      const uint32_t* __restrict__ size,
-                                                      const uint32_t* __restrict__ members,
-                                                      uint64_t* ka, uint64_t* kb, uint32_t* selbits,
-                                                      uint32_t* first_touch, uint32_t* status) {
-  p2_engine_body<kSmem>(plan, sets, off, size, members, ka, kb, selbits, first_touch, status);
-}
-
-template <bool kSmem>
-__device__ __forceinline__ void p2_engine_body(Plan* plan, uint32_t* sets,
-                                               const uint32_t* __restrict__ off, const uint32_t* __restrict__ size,
-                                               const uint32_t* __restrict__ members,
-                                               uint64_t* ka, uint64_t* kb, uint32_t* selbits,
-                                               uint32_t* first_touch, uint32_t* status) {
+                                               uint32_t* first_touch_g, uint32_t* status) {
   extern __shared__ uint32_t sbits[];
   __shared__ uint64_t sh[40];
   // per-round block results: one barrier each (shared atomicMin / the single
@@ -406,6 +393,7 @@ __device__ __forceinline__ void p2_engine_body(Plan* plan, uint32_t* sets,
   const uint64_t n = plan->n_pos, r = plan->r;
   const uint64_t nwords = (n + 31) / 32;
   uint32_t* bits = kSmem ? sbits : selbits;
+  uint32_t* first_touch = kFt ? sbits + ((nwords + 3) & ~3ull) : first_touch_g;
   const bool fallback = plan->n_single_sel > r;
   if (kSmem || fallback)
     for (uint64_t w = v; w < nwords; w += W) bits[w] = fallback ? 0u : selbits[w];
@@ -562,20 +550,34 @@ __device__ __forceinline__ void p2_engine_body(Plan* plan, uint32_t* sets,
 }
 
 
-constexpr int kSmemBitsBytes = 160 * 1024;
+constexpr int kSmemFtBytes = 200 * 1024;    // bitset + first-touch table
+constexpr int kSmemBitsBytes = 160 * 1024;  // bitset alone (the rest stays L1 for the global chains)
 
-// |P| is only known on the device: run the shared-memory engine when the
-// selection bitset fits, the global-memory one otherwise.
+__device__ __forceinline__ bool ft_fits(uint64_t n) {
+  return (((n + 31) / 32 + 3) & ~3ull) * 4 + 4 * n <= static_cast<uint64_t>(kSmemFtBytes);
+}
+
+// |P| is only known on the device, so both engine launches are enqueued and
+// exactly one runs: kFt (bitset and first-touch table in shared memory, when
+// both fit) or the other (bitset in shared memory when it fits, else global).
+// Separate launches keep the smaller shared-memory carveout — and the larger
+// L1 for the global set / member chains — when the first-touch table does
+// not fit (c4s: requesting 200 KiB there cost 40% on the engine).
+template <bool kFt>
 __global__ void __launch_bounds__(1024) p2_engine_dispatch(Plan* plan, uint32_t* sets,
                                                            const uint32_t* __restrict__ off,
                                                            const uint32_t* __restrict__ size,
                                                            const uint32_t* __restrict__ members,
                                                            uint64_t* ka, uint64_t* kb, uint32_t* selbits,
                                                            uint32_t* first_touch, uint32_t* status) {
-  if (((plan->n_pos + 31) / 32) * 4 <= static_cast<uint64_t>(kSmemBitsBytes))
-    p2_engine_body<true>(plan, sets, off, size, members, ka, kb, selbits, first_touch, status);
+  const uint64_t n = plan->n_pos;
+  if (ft_fits(n) != kFt) return;
+  if (kFt)
+    p2_engine_body<true, true>(plan, sets, off, size, members, ka, kb, selbits, first_touch, status);
+  else if (((n + 31) / 32) * 4 <= static_cast<uint64_t>(kSmemBitsBytes))
+    p2_engine_body<true, false>(plan, sets, off, size, members, ka, kb, selbits, first_touch, status);
   else
-    p2_engine_body<false>(plan, sets, off, size, members, ka, kb, selbits, first_touch, status);
+    p2_engine_body<false, false>(plan, sets, off, size, members, ka, kb, selbits, first_touch, status);
 }
 
 // sel = ascending P[p] for flagged p (bloom.cpp:221 sort), count must be r
@@ -656,22 +658,23 @@ void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t 
             w.selbits, w.status);
   stage_end(ctx, s);
   stage_begin(ctx, decoding ? ST_DEC_P2_ENGINE : ST_P2_ENGINE, s);
-  if (((n_bound + 31) / 32) * 4 <= static_cast<uint64_t>(kSmemBitsBytes)) {
-    GP_LAUNCH(ctx, p2_engine_win<true>, 1, 1024, ((n_bound + 31) / 32) * 4, s, w.plan, w.p2_sets, w.p2_off,
-              w.p2_count, w.p2_members, reinterpret_cast<uint64_t*>(w.f64a), reinterpret_cast<uint64_t*>(w.f64b), w.selbits,
-              w.first_touch, w.status);
-  } else {
-    GP_LAUNCH(ctx, p2_engine_dispatch, 1, 1024, kSmemBitsBytes, s, w.plan, w.p2_sets, w.p2_off, w.p2_count,
-              w.p2_members, reinterpret_cast<uint64_t*>(w.f64a), reinterpret_cast<uint64_t*>(w.f64b), w.selbits,
-              w.first_touch, w.status);
+  {
+    const uint64_t bits_b = (((n_bound + 31) / 32 + 3) & ~3ull) * 4;  // for |P| <= n_bound
+    uint64_t* ka = reinterpret_cast<uint64_t*>(w.f64a);
+    uint64_t* kb = reinterpret_cast<uint64_t*>(w.f64b);
+    GP_LAUNCH(ctx, p2_engine_dispatch<true>, 1, 1024, std::min<uint64_t>(bits_b + 4 * n_bound, kSmemFtBytes), s,
+              w.plan, w.p2_sets, w.p2_off, w.p2_count, w.p2_members, ka, kb, w.selbits, w.first_touch, w.status);
+    if (bits_b + 4 * n_bound > static_cast<uint64_t>(kSmemFtBytes))  // else |P| <= n_bound always fits
+      GP_LAUNCH(ctx, p2_engine_dispatch<false>, 1, 1024, std::min<uint64_t>(bits_b, kSmemBitsBytes), s, w.plan,
+                w.p2_sets, w.p2_off, w.p2_count, w.p2_members, ka, kb, w.selbits, w.first_touch, w.status);
   }
   stage_end(ctx, s);
   launch_flags_compact(ctx, GP_INDEX_BLOOM_P2, n_bound, s);
 }
 
 void kernel_attrs_p2() {
-  cudaFuncSetAttribute(p2_engine_win<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBitsBytes);
-  cudaFuncSetAttribute(p2_engine_dispatch, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBitsBytes);
+  cudaFuncSetAttribute(p2_engine_dispatch<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemFtBytes);
+  cudaFuncSetAttribute(p2_engine_dispatch<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBitsBytes);
 }
 
 }  // namespace gp
