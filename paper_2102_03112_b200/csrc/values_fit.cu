@@ -738,15 +738,40 @@ constexpr LegendreTable make_legendre() {
 __constant__ LegendreTable kLegendre = make_legendre();
 
 // degree <= 7: one segment per block iteration; thread 0 solves (sizes <= 8x8)
+// emit_out != null: the model is also serialised here (fit_emit's layout,
+// curvefit.cpp:285-298): each segment's block writes its bound and
+// coefficients, block 0 the header fields — one launch fewer on the encode.
 __global__ void fit_solve(Plan* plan, const double* __restrict__ t, const uint32_t* __restrict__ seg_end,
                           const uint64_t* __restrict__ chunk, const double* __restrict__ partial, float* coeffs,
-                          const uint32_t* status) {
+                          uint8_t* emit_out, uint32_t* status) {
   __shared__ double sacc[kAcc];
   __shared__ double spow[2][kCps];  // alpha^k, beta^k (curvefit.cpp:157-172's pow values), one lane each
   if (failed(status) || !poly_active(plan) || plan->degree > kMaxDeg) return;
   const uint32_t S = plan->nseg;
   const int deg = static_cast<int>(plan->degree);
   const uint32_t cps = static_cast<uint32_t>(deg) + 1;
+  uint8_t* ep = nullptr;  // the value payload (emit_out + 49 + il) and its coefficient array
+  uint8_t* eq = nullptr;
+  if (emit_out) {
+    if (S > 0xffff) {  // curvefit.cpp:287
+      if (blockIdx.x == 0 && threadIdx.x == 0) latch(status, GP_ERROR);
+      return;
+    }
+    ep = emit_out + 49 + plan->il;
+    eq = ep + 3 + 4ull * S + 1;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      ep[0] = 0;  // piecewise polynomial
+      ep[1] = static_cast<uint8_t>(S);
+      ep[2] = static_cast<uint8_t>(S >> 8);
+      eq[-1] = static_cast<uint8_t>(deg);
+      const uint64_t nc = static_cast<uint64_t>(S) * cps;
+      st_u32_unaligned(eq + 4 * nc, plan->sign_split);
+      plan->vl = 1 + 2 + 4ull * S + 1 + 4ull * S * cps + 4;
+      uint32_t w = 0;
+      for (uint64_t x = plan->d - 1; x; x >>= 1) ++w;
+      plan->rl = plan->identity ? 0 : (plan->n_values * w + 7) / 8;
+    }
+  }
   for (uint32_t seg = blockIdx.x; seg < S; seg += gridDim.x) {
     uint32_t b, e;
     seg_range(seg_end, seg, b, e);
@@ -865,6 +890,11 @@ __global__ void fit_solve(Plan* plan, const double* __restrict__ t, const uint32
             out[k] = static_cast<float>(c);
           }
         }
+      }
+      if (ep) {
+        st_u32_unaligned(ep + 3 + 4ull * seg, e);
+        for (uint32_t j = 0; j < cps; ++j)
+          st_u32_unaligned(eq + 4 * (static_cast<uint64_t>(seg) * cps + j), __float_as_uint(out[j]));
       }
     }
     __syncthreads();
@@ -1584,12 +1614,13 @@ void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, 
             static_cast<int>(std::min<uint64_t>(n_bound / kChunk + seg_bound + 1, static_cast<uint64_t>(ctx->sm_count))),
             256, 0, s, w.plan,
             w.f64b, w.seg_end, w.seg_chunk, w.partial, w.status);
+  const bool fused_emit = !dexp && degree <= kMaxDeg;  // fit_solve serialises the model itself
   GP_LAUNCH(ctx, fit_solve, grid_for(ctx, seg_bound * 64, 64), 64, 0, s, w.plan, w.f64b, w.seg_end, w.seg_chunk,
-            w.partial, w.coeffs, w.status);
+            w.partial, w.coeffs, fused_emit ? out : nullptr, w.status);
   if (degree > kMaxDeg)
     GP_LAUNCH(ctx, fit_solve_wide, static_cast<int>(std::min<uint64_t>(seg_bound, kWideBlocks)), 256, 0, s, w.plan,
               w.f64b, w.seg_end, w.coeffs, w.fit_scratch, w.status);
-  GP_LAUNCH(ctx, fit_emit, 1, 256, 0, s, w.plan, out, degree, w.seg_end, w.coeffs, w.status);
+  if (!fused_emit) GP_LAUNCH(ctx, fit_emit, 1, 256, 0, s, w.plan, out, degree, w.seg_end, w.coeffs, w.status);
   GP_LAUNCH(ctx, reorder_pack, grid_for(ctx, n_bound * 4, 256), 256, 0, s, w.u32b, w.plan, out, w.status);
 }
 
