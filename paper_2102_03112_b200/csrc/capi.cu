@@ -567,7 +567,7 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
       if (im == GP_INDEX_BLOOM_NAIVE) break;  // values stay in support order (pipeline.cpp:196-199)
       GP_STAGE(ctx, ST_BLOOM_SCAN, s, launch_bloom_scan(ctx, d, pi.m, false, s));
       if (im == GP_INDEX_BLOOM_P2)
-        launch_select_p2(ctx, d, pi.m, pi.k, false, s);
+        launch_select_p2(ctx, d, pi.m, pi.k, false, s, r + static_cast<uint64_t>(cfg->fpr * static_cast<double>(d)));
       else if (im == GP_INDEX_BLOOM_P1)
         GP_STAGE(ctx, ST_SELECT, s, launch_select_p1(ctx, d, r, s));
       else

@@ -266,7 +266,7 @@ void launch_bloom_after_scan(gp_ctx* ctx, bool decoding, cudaStream_t s);
 void launch_select_p1(gp_ctx* ctx, uint64_t n_bound, uint64_t r_bound, cudaStream_t s);
 void launch_flags_compact(gp_ctx* ctx, int method, uint64_t n_bound, cudaStream_t s);
 void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t k_bound, bool decoding,
-                      cudaStream_t s);
+                      cudaStream_t s, uint64_t n_expect = 0);
 
 // sort.cu
 void launch_table_scan(gp_ctx* ctx, uint32_t* table, const uint64_t* n_dev, uint64_t n_bound, int tile_shift,

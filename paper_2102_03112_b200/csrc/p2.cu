@@ -569,9 +569,9 @@ __global__ void __launch_bounds__(1024) p2_engine_dispatch(Plan* plan, uint32_t*
                                                            const uint32_t* __restrict__ size,
                                                            const uint32_t* __restrict__ members,
                                                            uint64_t* ka, uint64_t* kb, uint32_t* selbits,
-                                                           uint32_t* first_touch, uint32_t* status) {
+                                                           uint32_t* first_touch, bool alone, uint32_t* status) {
   const uint64_t n = plan->n_pos;
-  if (ft_fits(n) != kFt) return;
+  if (!alone && ft_fits(n) != kFt) return;  // alone: the other kernel was not launched
   if (kFt)
     p2_engine_body<true, true>(plan, sets, off, size, members, ka, kb, selbits, first_touch, status);
   else if (((n + 31) / 32) * 4 <= static_cast<uint64_t>(kSmemBitsBytes))
@@ -640,7 +640,7 @@ void launch_flags_compact(gp_ctx* ctx, int method, uint64_t n_bound, cudaStream_
 }
 
 void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t k_bound, bool decoding,
-                      cudaStream_t s) {
+                      cudaStream_t s, uint64_t n_expect) {
   Workspace& w = ctx->ws;
   stage_begin(ctx, decoding ? ST_DEC_P2_SETS : ST_P2_SETS, s);
   const uint64_t m_cap = std::min<uint64_t>(m_bound, w.set_cap);
@@ -662,11 +662,20 @@ void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t 
     const uint64_t bits_b = (((n_bound + 31) / 32 + 3) & ~3ull) * 4;  // for |P| <= n_bound
     uint64_t* ka = reinterpret_cast<uint64_t*>(w.f64a);
     uint64_t* kb = reinterpret_cast<uint64_t*>(w.f64b);
-    GP_LAUNCH(ctx, p2_engine_dispatch<true>, 1, 1024, std::min<uint64_t>(bits_b + 4 * n_bound, kSmemFtBytes), s,
-              w.plan, w.p2_sets, w.p2_off, w.p2_count, w.p2_members, ka, kb, w.selbits, w.first_touch, w.status);
-    if (bits_b + 4 * n_bound > static_cast<uint64_t>(kSmemFtBytes))  // else |P| <= n_bound always fits
+    // n_expect (the encode's r + eps d, 0 when unknown): far above what the
+    // first-touch table holds, the shared-memory engine is not even launched
+    const bool ft_possible = n_expect == 0 || (((n_expect + 31) / 32 + 4) * 4 + 4 * n_expect) * 10 <=
+                                                  9ull * kSmemFtBytes;
+    if (ft_possible)
+      GP_LAUNCH(ctx, p2_engine_dispatch<true>, 1, 1024, std::min<uint64_t>(bits_b + 4 * n_bound, kSmemFtBytes), s,
+                w.plan, w.p2_sets, w.p2_off, w.p2_count, w.p2_members, ka, kb, w.selbits, w.first_touch, false,
+                w.status);
+    if (!ft_possible) {  // the other kernel must take every |P| (ft_fits is never consulted)
       GP_LAUNCH(ctx, p2_engine_dispatch<false>, 1, 1024, std::min<uint64_t>(bits_b, kSmemBitsBytes), s, w.plan,
-                w.p2_sets, w.p2_off, w.p2_count, w.p2_members, ka, kb, w.selbits, w.first_touch, w.status);
+                w.p2_sets, w.p2_off, w.p2_count, w.p2_members, ka, kb, w.selbits, w.first_touch, true, w.status);
+    } else if (bits_b + 4 * n_bound > static_cast<uint64_t>(kSmemFtBytes))  // else |P| <= n_bound always fits
+      GP_LAUNCH(ctx, p2_engine_dispatch<false>, 1, 1024, std::min<uint64_t>(bits_b, kSmemBitsBytes), s, w.plan,
+                w.p2_sets, w.p2_off, w.p2_count, w.p2_members, ka, kb, w.selbits, w.first_touch, false, w.status);
   }
   stage_end(ctx, s);
   launch_flags_compact(ctx, GP_INDEX_BLOOM_P2, n_bound, s);
