@@ -22,7 +22,6 @@ namespace gp {
 namespace {
 
 constexpr int kScanBlock = 256;
-constexpr int kTileKeyShift = 17;  // members_compact tile: 256 threads x 16 words x 32 keys
 constexpr uint64_t kSmemFilterMax = 150 * 1024;
 
 __global__ void bloom_insert(const uint32_t* __restrict__ keys, uint64_t r, const Plan* plan, uint32_t* words,
@@ -158,8 +157,7 @@ __device__ __forceinline__ uint32_t probe_pos(uint64_t h, const FastMod& fm) {
 
 template <bool kSmallM, int kLaneKeys, int kLaneBatch, int kCap>
 __device__ __forceinline__ void members_body(const uint32_t* __restrict__ words, const Plan* plan,
-                                             uint32_t* __restrict__ bitmap, uint32_t* __restrict__ tcnt,
-                                             uint8_t* dyn) {
+                                             uint32_t* __restrict__ bitmap, uint8_t* dyn) {
   constexpr int kChunk = 32 * kLaneKeys, kBatch = 32 * kLaneBatch;
   // keys [lo, lo + d): the whole range, or a slice (gp_bloom_scan_range); the
   // stack holds global keys, the membership bitmap is slice-relative
@@ -202,10 +200,7 @@ __device__ __forceinline__ void members_body(const uint32_t* __restrict__ words,
       for (int u = 0; u < kLaneBatch; ++u) {
         const bool ok = base + 32 * u + lane < top && ((wv[u] >> (pos[u] & 31)) & 1u);
         const bool member = ok && j[u] + 1u == k;
-        if (member) {
-          atomicOr(&bitmap[(x[u] - lo) >> 5], 1u << ((x[u] - lo) & 31));
-          atomicAdd(&tcnt[(x[u] - lo) >> kTileKeyShift], 1u);  // members per compaction tile
-        }
+        if (member) atomicOr(&bitmap[(x[u] - lo) >> 5], 1u << ((x[u] - lo) & 31));
         const bool keep = ok && !member;
         const unsigned bal = __ballot_sync(kFull, keep);
         if (keep) {
@@ -239,10 +234,7 @@ __device__ __forceinline__ void members_body(const uint32_t* __restrict__ words,
       c += nwarps;
       if (k == 1) {
         // kLaneKeys divides 32: a lane's keys share one bitmap word
-        if (pass) {
-          atomicOr(&bitmap[x0 >> 5], pass << (x0 & 31));
-          atomicAdd(&tcnt[x0 >> kTileKeyShift], __popc(pass));
-        }
+        if (pass) atomicOr(&bitmap[x0 >> 5], pass << (x0 & 31));
         continue;
       }
       const uint32_t cnt = __popc(pass);
@@ -274,7 +266,7 @@ __device__ __forceinline__ void members_body(const uint32_t* __restrict__ words,
 template <bool kSmem, int kLaneKeys, int kLaneBatch>
 __global__ void __launch_bounds__(kScanBlock) bloom_members(const uint32_t* __restrict__ gwords, Plan* plan,
                                                             uint32_t* __restrict__ bitmap,
-                                                            uint32_t* __restrict__ tcnt, const uint32_t* status) {
+                                                            const uint32_t* status) {
   using S = ScanShape<kSmem, kLaneKeys, kLaneBatch>;
   extern __shared__ __align__(16) uint8_t dyn[];
   if (failed(status)) return;
@@ -290,39 +282,32 @@ __global__ void __launch_bounds__(kScanBlock) bloom_members(const uint32_t* __re
     words = sw;
   }
   if (m <= (1ull << 31))
-    members_body<true, kLaneKeys, kLaneBatch, S::kCap>(words, plan, bitmap, tcnt, dyn);
+    members_body<true, kLaneKeys, kLaneBatch, S::kCap>(words, plan, bitmap, dyn);
   else
-    members_body<false, kLaneKeys, kLaneBatch, S::kCap>(words, plan, bitmap, tcnt, dyn);
+    members_body<false, kLaneKeys, kLaneBatch, S::kCap>(words, plan, bitmap, dyn);
 }
 
 // ordered compaction of the membership bitmap: 16 words per thread, in warp
 // rounds (lane l on word 32q + l of its warp's 512: coalesced loads); P is
-// ~1% of d, so each lane stores its own few bits at its rank.  A tile's
-// offset is the sum of the earlier tiles' member counts, which the scan
-// counted as it set the bits (tcnt) — one warp read, no look-back chain
-// (the decoupled look-back over ~200 tiles waited ~10 us on its spins)
+// ~1% of d, so each lane stores its own few bits at its rank
 __global__ void __launch_bounds__(kScanBlock) members_compact(const uint32_t* __restrict__ bitmap, Plan* plan,
                                                               uint32_t* __restrict__ pos_out, uint64_t cap,
-                                                              const uint32_t* __restrict__ tcnt,
+                                                              uint64_t* tiles, uint32_t* ticket,
                                                               const uint32_t* status) {
   __shared__ uint64_t sh[36];
+  __shared__ uint32_t slot;
   if (failed(status)) return;
   const uint8_t im = plan->index_method;
   if (im < GP_INDEX_BLOOM_P0 || im > GP_INDEX_BLOOM_NAIVE) return;
   const uint64_t lo = plan->scan_lo;
   const uint64_t nwd = ((plan->scan_hi ? plan->scan_hi - lo : plan->d) + 31) / 32;
   constexpr int kW = 16;
-  static_assert(kScanBlock * kW * 32 == (1 << kTileKeyShift), "a compaction tile covers 2^kTileKeyShift keys");
   const uint64_t ntiles = (nwd + kScanBlock * kW - 1) / (kScanBlock * kW);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    if (warp == 0) {
-      uint64_t v = 0;
-      for (uint64_t t = lane; t < tile; t += 32) v += __ldcg(tcnt + t);
-      v = warp_sum(v);
-      if (lane == 0) sh[34] = v;
-    }
-    const uint64_t wb = tile * kScanBlock * kW + static_cast<uint64_t>(warp) * (32 * kW);
+  while (true) {
+    const uint32_t tile = claim_tile(ticket, &slot);
+    if (tile >= ntiles) break;
+    const uint64_t wb = static_cast<uint64_t>(tile) * kScanBlock * kW + static_cast<uint64_t>(warp) * (32 * kW);
     uint32_t v[kW];
     uint32_t c = 0;
 #pragma unroll
@@ -333,8 +318,8 @@ __global__ void __launch_bounds__(kScanBlock) members_compact(const uint32_t* __
     }
     const uint32_t wc = __reduce_add_sync(kFull, c);
     uint64_t tot;
-    const uint64_t local = block_exclusive_sum<uint64_t, kScanBlock>(lane == 0 ? wc : 0, sh, tot);  // ends with a barrier
-    uint64_t o = __shfl_sync(kFull, sh[34] + local, 0);
+    uint64_t o = tile_exclusive_offset<kScanBlock>(lane == 0 ? wc : 0, tile, tiles, sh, tot);
+    o = __shfl_sync(kFull, o, 0);
 #pragma unroll
     for (int i = 0; i < kW; ++i) {
       const uint32_t n = __popc(v[i]);
@@ -345,7 +330,6 @@ __global__ void __launch_bounds__(kScanBlock) members_compact(const uint32_t* __
       o += __shfl_sync(kFull, incl, 31);
     }
     if (tile == ntiles - 1 && threadIdx.x == kScanBlock - 1) plan->n_pos = o;
-    __syncthreads();  // sh[34] is rewritten by the next tile
   }
 }
 
@@ -407,7 +391,7 @@ void launch_bloom_parse(gp_ctx* ctx, const uint8_t* in, uint64_t m_bound, cudaSt
 }
 
 template <int kLaneKeys, int kLaneBatch>
-void launch_members_global(gp_ctx* ctx, uint64_t d_bound, uint32_t* bitmap, uint32_t* tcnt, cudaStream_t s) {
+void launch_members_global(gp_ctx* ctx, uint64_t d_bound, uint32_t* bitmap, cudaStream_t s) {
   Workspace& w = ctx->ws;
   using S = ScanShape<false, kLaneKeys, kLaneBatch>;
   auto* kern = bloom_members<false, kLaneKeys, kLaneBatch>;
@@ -415,7 +399,7 @@ void launch_members_global(gp_ctx* ctx, uint64_t d_bound, uint32_t* bitmap, uint
   const uint64_t nchunks = (d_bound + S::kChunk - 1) / S::kChunk;
   const int grid = static_cast<int>(std::max<uint64_t>(
       1, std::min<uint64_t>((nchunks + kWarps - 1) / kWarps, static_cast<uint64_t>(ctx->sm_count) * per_sm)));
-  GP_LAUNCH(ctx, kern, grid, kScanBlock, S::kStackBytes, s, w.filter, w.plan, bitmap, tcnt, w.status);
+  GP_LAUNCH(ctx, kern, grid, kScanBlock, S::kStackBytes, s, w.filter, w.plan, bitmap, w.status);
 }
 
 // m_host: the filter width when the host knows it (encode), else 0 (decode:
@@ -423,11 +407,9 @@ void launch_members_global(gp_ctx* ctx, uint64_t d_bound, uint32_t* bitmap, uint
 void launch_bloom_scan(gp_ctx* ctx, uint64_t d_bound, uint64_t m_host, bool decoding, cudaStream_t s) {
   Workspace& w = ctx->ws;
   const uint64_t fbytes = ((m_host + 31) / 32) * 4;
-  uint32_t* bitmap = w.u32c;  // d-bit membership bitmap, then the per-tile member counts
+  uint32_t* bitmap = w.u32c;  // d-bit membership bitmap
   const uint64_t nwd = (d_bound + 31) / 32;
-  const uint64_t ntiles = (nwd + kScanBlock * 16 - 1) / (kScanBlock * 16);
-  uint32_t* tcnt = bitmap + (nwd + 31) / 32 * 32;
-  cudaMemsetAsync(bitmap, 0, ((nwd + 31) / 32 * 32 + ntiles) * 4, s);
+  cudaMemsetAsync(bitmap, 0, nwd * 4, s);
   if (m_host && fbytes <= kSmemFilterMax) {
     using S = ScanShape<true, 4, 2>;
     auto* kern = bloom_members<true, 4, 2>;
@@ -436,12 +418,14 @@ void launch_bloom_scan(gp_ctx* ctx, uint64_t d_bound, uint64_t m_host, bool deco
     const uint64_t nchunks = (d_bound + S::kChunk - 1) / S::kChunk;
     const int grid = static_cast<int>(std::max<uint64_t>(
         1, std::min<uint64_t>((nchunks + kWarps - 1) / kWarps, static_cast<uint64_t>(ctx->sm_count) * per_sm)));
-    GP_LAUNCH(ctx, kern, grid, kScanBlock, smem, s, w.filter, w.plan, bitmap, tcnt, w.status);
+    GP_LAUNCH(ctx, kern, grid, kScanBlock, smem, s, w.filter, w.plan, bitmap, w.status);
   } else {
-    launch_members_global<4, 4>(ctx, d_bound, bitmap, tcnt, s);  // 4 first probes / 4 batch probes per lane in flight
+    launch_members_global<4, 4>(ctx, d_bound, bitmap, s);  // 4 first probes / 4 batch probes per lane in flight
   }
+  const uint64_t ntiles = (nwd + kScanBlock * 16 - 1) / (kScanBlock * 16);
+  reset_scan(ctx, s, ntiles + 1);
   GP_LAUNCH(ctx, members_compact, static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, ctx->sm_count * 4ULL))),
-            kScanBlock, 0, s, bitmap, w.plan, w.pos, ctx->max_d, tcnt, w.status);
+            kScanBlock, 0, s, bitmap, w.plan, w.pos, ctx->max_d, w.tiles, w.ticket, w.status);
   GP_LAUNCH(ctx, bloom_after_scan, 1, 1, 0, s, w.plan, ctx->max_d, decoding ? 1 : 0, w.status);
 }
 
