@@ -14,10 +14,14 @@
 // words (r*k = 2.6M probes at C4).  Scan: ordered compaction over [0, d),
 // 4096 keys per tile; the filter is staged in shared memory when it fits
 // (<= 160 KiB: C1, C5 buckets), otherwise read through L1/L2 (C4: 459 KiB).
+#include <cooperative_groups.h>
+
 #include "gp_ctx.hpp"
 #include "gp_device.cuh"
 
 namespace gp {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -333,6 +337,62 @@ __global__ void __launch_bounds__(kScanBlock) members_compact(const uint32_t* __
   }
 }
 
+// The same compaction as one cooperative launch of one block per tile (when
+// the tiles fit one resident wave): every block keeps its 16 words per thread
+// in registers, publishes its tile's member count, and after one grid
+// barrier reads its offset — the sum of the earlier tiles' counts, one warp
+// read — instead of spinning on a decoupled look-back chain (~200 tiles at
+// C4: 19 us).
+__global__ void __launch_bounds__(kScanBlock) members_compact_coop(const uint32_t* __restrict__ bitmap, Plan* plan,
+                                                                   uint32_t* __restrict__ pos_out, uint64_t cap,
+                                                                   uint64_t* tcnt, const uint32_t* status) {
+  __shared__ uint64_t sh[36];
+  cg::grid_group grid = cg::this_grid();
+  if (failed(status)) return;  // uniform: nothing latches this word while the kernel runs
+  const uint8_t im = plan->index_method;
+  if (im < GP_INDEX_BLOOM_P0 || im > GP_INDEX_BLOOM_NAIVE) return;
+  const uint64_t lo = plan->scan_lo;
+  const uint64_t nwd = ((plan->scan_hi ? plan->scan_hi - lo : plan->d) + 31) / 32;
+  constexpr int kW = 16;
+  const uint64_t ntiles = (nwd + kScanBlock * kW - 1) / (kScanBlock * kW);
+  const uint64_t tile = blockIdx.x;
+  const bool live = tile < ntiles;  // blocks past the last tile only join the barrier
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t wb = tile * kScanBlock * kW + static_cast<uint64_t>(warp) * (32 * kW);
+  uint32_t v[kW];
+  uint32_t c = 0;
+#pragma unroll
+  for (int i = 0; i < kW; ++i) {
+    const uint64_t w = wb + 32 * i + lane;
+    v[i] = live && w < nwd ? bitmap[w] : 0u;
+    c += __popc(v[i]);
+  }
+  const uint32_t wc = __reduce_add_sync(kFull, c);
+  uint64_t tot;
+  const uint64_t local = block_exclusive_sum<uint64_t, kScanBlock>(lane == 0 ? wc : 0, sh, tot);
+  if (live && threadIdx.x == 0) tcnt[tile] = tot;
+  grid.sync();
+  if (!live) return;
+  if (warp == 0) {
+    uint64_t p = 0;
+    for (uint64_t t = lane; t < tile; t += 32) p += __ldcg(tcnt + t);
+    p = warp_sum(p);
+    if (lane == 0) sh[34] = p;
+  }
+  __syncthreads();
+  uint64_t o = __shfl_sync(kFull, sh[34] + local, 0);
+#pragma unroll
+  for (int i = 0; i < kW; ++i) {
+    const uint32_t n = __popc(v[i]);
+    const uint32_t incl = warp_inclusive_sum(n);
+    uint64_t at = o + incl - n;
+    for (uint32_t x = v[i]; x; x &= x - 1, ++at)
+      if (at < cap) pos_out[at] = static_cast<uint32_t>(lo + 32 * (wb + 32 * i + lane) + (__ffs(x) - 1));
+    o += __shfl_sync(kFull, incl, 31);
+  }
+  if (tile == ntiles - 1 && threadIdx.x == kScanBlock - 1) plan->n_pos = o;
+}
+
 // Post-scan bookkeeping: |P| >= r (pipeline.cpp:284-285), value counts, and
 // the P0 / Pd / naive selections which are slices of P.
 __global__ void bloom_after_scan(Plan* plan, uint64_t cap, int decoding, uint32_t* status) {
@@ -423,9 +483,25 @@ void launch_bloom_scan(gp_ctx* ctx, uint64_t d_bound, uint64_t m_host, bool deco
     launch_members_global<4, 4>(ctx, d_bound, bitmap, s);  // 4 first probes / 4 batch probes per lane in flight
   }
   const uint64_t ntiles = (nwd + kScanBlock * 16 - 1) / (kScanBlock * 16);
-  reset_scan(ctx, s, ntiles + 1);
-  GP_LAUNCH(ctx, members_compact, static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, ctx->sm_count * 4ULL))),
-            kScanBlock, 0, s, bitmap, w.plan, w.pos, ctx->max_d, w.tiles, w.ticket, w.status);
+  static int coop_per_sm = -1;
+  if (coop_per_sm < 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&coop_per_sm, members_compact_coop, kScanBlock, 0);
+  if (ntiles <= static_cast<uint64_t>(coop_per_sm) * ctx->sm_count && ntiles <= w.tiles_cap) {
+    int grid = static_cast<int>(std::max<uint64_t>(1, ntiles));
+    uint32_t* bm = bitmap;
+    Plan* plan = w.plan;
+    uint32_t* pos = w.pos;
+    uint64_t cap = ctx->max_d;
+    uint64_t* tc = w.tiles;
+    uint32_t* st = w.status;
+    void* args[] = {&bm, &plan, &pos, &cap, &tc, &st};
+    cudaLaunchCooperativeKernel(reinterpret_cast<void*>(members_compact_coop), grid, kScanBlock, args, 0, s);
+    ++ctx->launches;
+  } else {
+    reset_scan(ctx, s, ntiles + 1);
+    GP_LAUNCH(ctx, members_compact,
+              static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, ctx->sm_count * 4ULL))), kScanBlock, 0,
+              s, bitmap, w.plan, w.pos, ctx->max_d, w.tiles, w.ticket, w.status);
+  }
   GP_LAUNCH(ctx, bloom_after_scan, 1, 1, 0, s, w.plan, ctx->max_d, decoding ? 1 : 0, w.status);
 }
 
