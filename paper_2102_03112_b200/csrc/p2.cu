@@ -27,10 +27,14 @@
 // member count is 0 retires, 1 selects it, >= 2 draws below(cnt) from the
 // stream (rng.hpp:52-59, rejection exact) and selects that member.  Retired
 // sets need no flag: revisiting them changes nothing and draws nothing.
+#include <cooperative_groups.h>
+
 #include "gp_ctx.hpp"
 #include "gp_device.cuh"
 
 namespace gp {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -580,26 +584,27 @@ __global__ void __launch_bounds__(1024) p2_engine_dispatch(Plan* plan, uint32_t*
     p2_engine_body<false, false>(plan, sets, off, size, members, ka, kb, selbits, first_touch, status);
 }
 
-// sel = ascending P[p] for flagged p (bloom.cpp:221 sort), count must be r
+// sel = ascending P[p] for flagged p (bloom.cpp:221 sort), count must be r.
+// One cooperative launch: every block counts the selected positives of its
+// tiles (strided by the grid), publishes the counts, and after one grid
+// barrier writes each tile from the sum of the earlier tiles' counts (one
+// warp read) — no decoupled look-back chain, no ticket reset.
 __global__ void __launch_bounds__(kTileBlock) flags_compact(const uint32_t* __restrict__ P,
                                                             const uint32_t* __restrict__ selbits, Plan* plan,
-                                                            int method, uint32_t* __restrict__ sel, uint64_t* tiles,
-                                                            uint32_t* ticket, uint32_t* status) {
+                                                            int method, uint32_t* __restrict__ sel, uint64_t* tcnt,
+                                                            uint32_t* status) {
   __shared__ uint64_t sh[36];
-  __shared__ uint32_t slot;
-  if (failed(status) || plan->index_method != method) return;
+  cg::grid_group grid = cg::this_grid();
+  if (failed(status) || plan->index_method != method) return;  // uniform over the grid
   const uint64_t n = plan->n_pos;
   const uint64_t ntiles = (n + kTile - 1) / kTile;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
-  while (true) {
-    const uint32_t tile = claim_tile(ticket, &slot);
-    if (tile >= ntiles) break;
-    // warp rounds: round q of warp w covers positions wb + 32q + lane, one
-    // selection word (wb is a multiple of 32), so P loads and sel stores are
-    // coalesced (~90% of P is selected at C4)
-    const uint64_t wb = static_cast<uint64_t>(tile) * kTile + static_cast<uint64_t>(warp) * (32 * kTileItems);
-    uint32_t word[kTileItems];
+  // warp rounds: round q of warp w covers positions wb + 32q + lane, one
+  // selection word (wb is a multiple of 32), so P loads and sel stores are
+  // coalesced (~90% of P is selected at C4)
+  auto load = [&](uint64_t tile, uint32_t (&word)[kTileItems]) {
+    const uint64_t wb = tile * kTile + static_cast<uint64_t>(warp) * (32 * kTileItems);
     uint32_t c = 0;
 #pragma unroll
     for (int q = 0; q < kTileItems; ++q) {
@@ -609,10 +614,30 @@ __global__ void __launch_bounds__(kTileBlock) flags_compact(const uint32_t* __re
       word[q] = x;
       c += __popc(x);
     }
+    return c;
+  };
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    uint32_t word[kTileItems];
+    const uint32_t c = load(tile, word);  // every lane: the warp's count (one word per round)
     uint64_t tot;
-    uint64_t o = tile_exclusive_offset<kTileBlock>(lane == 0 ? c : 0, tile, tiles, sh, tot);
-    o = __shfl_sync(kFull, o, 0);
-    const uint64_t r = plan->r;
+    (void)block_exclusive_sum<uint64_t, kTileBlock>(lane == 0 ? c : 0, sh, tot);
+    if (threadIdx.x == 0) tcnt[tile] = tot;
+  }
+  grid.sync();
+  const uint64_t r = plan->r;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    if (warp == 0) {
+      uint64_t p = 0;
+      for (uint64_t t = lane; t < tile; t += 32) p += __ldcg(tcnt + t);
+      p = warp_sum(p);
+      if (lane == 0) sh[34] = p;
+    }
+    uint32_t word[kTileItems];
+    const uint32_t c = load(tile, word);  // every lane: the warp's count (one word per round)
+    uint64_t tot;
+    const uint64_t local = block_exclusive_sum<uint64_t, kTileBlock>(lane == 0 ? c : 0, sh, tot);  // barrier
+    uint64_t o = __shfl_sync(kFull, sh[34] + local, 0);
+    const uint64_t wb = tile * kTile + static_cast<uint64_t>(warp) * (32 * kTileItems);
 #pragma unroll
     for (int q = 0; q < kTileItems; ++q) {
       if (word[q] >> lane & 1u) {
@@ -622,6 +647,7 @@ __global__ void __launch_bounds__(kTileBlock) flags_compact(const uint32_t* __re
       o += __popc(word[q]);
     }
     if (tile == ntiles - 1 && threadIdx.x == kTileBlock - 1 && o != plan->r) latch(status, GP_ERROR);
+    __syncthreads();  // sh[34] is rewritten by the next tile
   }
 }
 
@@ -629,14 +655,18 @@ __global__ void __launch_bounds__(kTileBlock) flags_compact(const uint32_t* __re
 
 void launch_flags_compact(gp_ctx* ctx, int method, uint64_t n_bound, cudaStream_t s) {
   Workspace& w = ctx->ws;
+  // cooperative: every block resident (48 registers x 256 threads: 5 per SM)
   const uint64_t ptiles = (n_bound + kTile - 1) / kTile;
-  reset_scan(ctx, s, ptiles + 1);
-  // tiles are claimed in a loop: two blocks per SM cover any |P| (the host
-  // bound is d; at C4 |P| is ~1% of it and most of a d-sized grid would exit)
-  GP_LAUNCH(ctx, flags_compact,
-            static_cast<int>(std::min<uint64_t>(std::max<uint64_t>(ptiles, 1), 2ull * ctx->sm_count)), kTileBlock, 0, s,
-            w.pos, w.selbits,
-            w.plan, method, w.sel, w.tiles, w.ticket, w.status);
+  int grid = static_cast<int>(std::min<uint64_t>(std::max<uint64_t>(ptiles, 1), 2ull * ctx->sm_count));
+  const uint32_t* P = w.pos;
+  const uint32_t* sb = w.selbits;
+  Plan* plan = w.plan;
+  uint32_t* sel = w.sel;
+  uint64_t* tc = w.tiles;
+  uint32_t* st = w.status;
+  void* args[] = {&P, &sb, &plan, &method, &sel, &tc, &st};
+  cudaLaunchCooperativeKernel(reinterpret_cast<void*>(flags_compact), grid, kTileBlock, args, 0, s);
+  ++ctx->launches;
 }
 
 void launch_select_p2(gp_ctx* ctx, uint64_t n_bound, uint64_t m_bound, uint32_t k_bound, bool decoding,
