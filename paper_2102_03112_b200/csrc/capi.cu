@@ -232,7 +232,7 @@ void carve(Workspace& w, uint8_t* base, uint64_t D) {
   w.seg_chunk = c.take<uint64_t>(w.seg_cap + 1);
   w.fit_scratch = c.take<double>(static_cast<uint64_t>(kWideBlocks) * 3 * kFitMaxCps * kFitMaxCps);
   w.crc_cap = 2 * ((64 * D + (1 << 20)) / (64 * 256) + 64);
-  w.crc_digits = c.take<uint32_t>(9 * 256);  // 5 byte-digit shift tables + 4 lane-stride multiply tables
+  w.crc_digits = c.take<uint32_t>(13 * 256);  // 5 byte-digit shift tables + the full and small grids' lane-stride multiply tables
   w.crc_acc = c.take<uint32_t>(64);
   w.scratch = c.take<uint8_t>(2 * D);
   w.huff = c.take<HuffTable>(1);
@@ -657,7 +657,7 @@ static int decode_common(gp_ctx* ctx, const uint8_t* d_in, uint64_t len, const u
   // (container.cu parse_container / merge_status), so error precedence is
   // the reference's: header, checksum, post-CRC checks, method decoders
   GP_STAGE(ctx, ST_DEC_PARSE, s, launch_parse_container(ctx, d_in, len, d_len, hint ? &h : nullptr, s);
-           cudaEventRecord(ctx->ev_fork, s); launch_verify_crc(ctx, d_in, s));
+           cudaEventRecord(ctx->ev_fork, s); launch_verify_crc(ctx, d_in, len, s));
   cudaStream_t ps = ctx->side;
   cudaStreamWaitEvent(ps, ctx->ev_fork, 0);
   auto join = [&]() {

@@ -27,6 +27,7 @@ constexpr int kCrcBlocksPerSm = 1;  // the CRC grid is fixed: one 1024-lane bloc
 // byte-indexed lookups of a warp are conflict-free (a shared 256-entry table
 // serialises ~3.5-way on average).  128 KiB of dynamic shared memory.
 constexpr int kCrcLaneTableWords = 4 * 256 * 32;
+constexpr int kCrcSmallGrid = 24;  // blocks of the small-range CRC (1.5 MiB per row of 64-byte chunks)
 
 __device__ __forceinline__ uint32_t multmodp(uint32_t a, uint32_t b) {
   // a * b mod P in the reflected representation (bit 31 = x^0)
@@ -116,7 +117,8 @@ __device__ __forceinline__ uint32_t mul_const(const uint32_t (*M)[256], uint32_t
 __global__ void __launch_bounds__(kCrcBlock) crc_chunks(const uint8_t* __restrict__ base, const uint64_t* off_p,
                                                         uint64_t off_h, const uint64_t* len_a, const uint64_t* len_b,
                                                         const uint64_t* len_c, uint64_t len_h,
-                                                        const uint32_t* __restrict__ digits, uint32_t* acc,
+                                                        const uint32_t* __restrict__ digits,
+                                                        const uint32_t* __restrict__ mtab, uint32_t* acc,
                                                         uint32_t* done, uint32_t* out, const CrcEpilogue ep,
                                                         uint32_t* status) {
   extern __shared__ uint32_t TL[];  // [4][256][32] per-lane slice-by-4 tables
@@ -146,7 +148,7 @@ __global__ void __launch_bounds__(kCrcBlock) crc_chunks(const uint8_t* __restric
       T0[i] = c;
     }
     for (int i = threadIdx.x; i < 5 * 256; i += kCrcBlock) D[i / 256][i % 256] = digits[i];
-    for (int i = threadIdx.x; i < 4 * 256; i += kCrcBlock) M[i / 256][i % 256] = digits[5 * 256 + i];
+    for (int i = threadIdx.x; i < 4 * 256; i += kCrcBlock) M[i / 256][i % 256] = mtab[i];  // this grid's lane stride
     __syncthreads();
     // T_k[e] = T_{k-1}[e] advanced by one zero byte; replicate into every lane's column
     for (int i = threadIdx.x; i < 4 * 256; i += kCrcBlock) {
@@ -305,7 +307,7 @@ int crc_tables_init(gp_ctx* ctx) {
     }
     return p;
   };
-  uint32_t tab[9 * 256];
+  uint32_t tab[13 * 256];
   uint32_t unit = 1u << 23;  // x^8: one byte
   for (int i = 0; i < 5; ++i) {
     uint32_t p = 1u << 31;
@@ -315,13 +317,20 @@ int crc_tables_init(gp_ctx* ctx) {
     }
     unit = p;  // x^(8 * 256^(i+1))
   }
-  // M[j][b] = (b at byte j) * x^(8 * 64 * lanes) mod P: the lane stride of the fixed grid
-  uint64_t stride = 64ull * static_cast<uint64_t>(ctx->sm_count) * kCrcBlocksPerSm * kCrcBlock;
-  uint32_t S = 1u << 31;
-  for (int i = 0; stride; ++i, stride >>= 8)
-    if (stride & 0xFF) S = mult(tab[i * 256 + (stride & 0xFF)], S);
-  for (int j = 0; j < 4; ++j)
-    for (int b = 0; b < 256; ++b) tab[(5 + j) * 256 + b] = b ? mult(static_cast<uint32_t>(b) << (8 * j), S) : 0u;
+  // M[j][b] = (b at byte j) * x^(8 * 64 * lanes) mod P: the lane stride of a
+  // grid — the full one (one block per SM) and the small one (kCrcSmallGrid
+  // blocks, for ranges of at most one of its rows: the launch and the
+  // per-block table setup of ~120 idle blocks was most of a small CRC)
+  for (int g = 0; g < 2; ++g) {
+    uint64_t stride = 64ull * kCrcBlock *
+                      static_cast<uint64_t>(g == 0 ? ctx->sm_count * kCrcBlocksPerSm : kCrcSmallGrid);
+    uint32_t S = 1u << 31;
+    for (int i = 0; stride; ++i, stride >>= 8)
+      if (stride & 0xFF) S = mult(tab[i * 256 + (stride & 0xFF)], S);
+    for (int j = 0; j < 4; ++j)
+      for (int b = 0; b < 256; ++b)
+        tab[(5 + 4 * g + j) * 256 + b] = b ? mult(static_cast<uint32_t>(b) << (8 * j), S) : 0u;
+  }
   cudaError_t e = cudaFuncSetAttribute(crc_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kCrcLaneTableWords * static_cast<int>(sizeof(uint32_t)));
   if (e == cudaSuccess) e = cudaMemcpy(w.crc_digits, tab, sizeof(tab), cudaMemcpyHostToDevice);
@@ -332,21 +341,23 @@ int crc_tables_init(gp_ctx* ctx) {
 }
 
 namespace {
+// len_bound: an upper bound of the range's length (host side)
 void crc_range(gp_ctx* ctx, const uint8_t* base, const uint64_t* off_dev, uint64_t off_host, const uint64_t* la,
-               const uint64_t* lb, const uint64_t* lc, uint64_t len_host, uint32_t* out, cudaStream_t s,
-               const CrcEpilogue& ep) {
+               const uint64_t* lb, const uint64_t* lc, uint64_t len_host, uint64_t len_bound, uint32_t* out,
+               cudaStream_t s, const CrcEpilogue& ep) {
   Workspace& w = ctx->ws;
-  const int grid = ctx->sm_count * kCrcBlocksPerSm;
-  GP_LAUNCH(ctx, crc_chunks, grid, kCrcBlock, kCrcLaneTableWords * sizeof(uint32_t), s, base, off_dev, off_host, la, lb, lc, len_host, w.crc_digits,
-            w.crc_acc, w.crc_acc + 1, out, ep, w.status);
+  const bool small = len_bound + 128 <= 64ull * kCrcBlock * kCrcSmallGrid;
+  const int grid = small ? kCrcSmallGrid : ctx->sm_count * kCrcBlocksPerSm;
+  const uint32_t* mtab = w.crc_digits + (small ? 9 : 5) * 256;
+  GP_LAUNCH(ctx, crc_chunks, grid, kCrcBlock, kCrcLaneTableWords * sizeof(uint32_t), s, base, off_dev, off_host, la,
+            lb, lc, len_host, w.crc_digits, mtab, w.crc_acc, w.crc_acc + 1, out, ep, w.status);
 }
 }  // namespace
 
 void launch_crc_range(gp_ctx* ctx, const uint8_t* base, const uint64_t* off_dev, uint64_t off_host,
                       const uint64_t* la, const uint64_t* lb, const uint64_t* lc, uint64_t len_host,
                       uint64_t len_bound, uint32_t* out, cudaStream_t s) {
-  (void)len_bound;
-  crc_range(ctx, base, off_dev, off_host, la, lb, lc, len_host, out, s, CrcEpilogue{});
+  crc_range(ctx, base, off_dev, off_host, la, lb, lc, len_host, len_bound, out, s, CrcEpilogue{});
 }
 
 void launch_finish_container(gp_ctx* ctx, uint8_t* out, uint64_t cap, uint64_t* d_len, uint64_t len_bound,
@@ -359,8 +370,7 @@ void launch_finish_container(gp_ctx* ctx, uint8_t* out, uint64_t cap, uint64_t* 
   ep.out = out;
   ep.cap = cap;
   ep.d_len = d_len;
-  (void)len_bound;
-  crc_range(ctx, out, &w.plan->off_index, 0, &w.plan->il, &w.plan->vl, &w.plan->rl, 0, crc, s, ep);
+  crc_range(ctx, out, &w.plan->off_index, 0, &w.plan->il, &w.plan->vl, &w.plan->rl, 0, len_bound, crc, s, ep);
 }
 
 void launch_parse_container(gp_ctx* ctx, const uint8_t* in, uint64_t len, const uint64_t* len_dev,
@@ -372,13 +382,13 @@ void launch_parse_container(gp_ctx* ctx, const uint8_t* in, uint64_t len, const 
             w.status_pre);
 }
 
-void launch_verify_crc(gp_ctx* ctx, const uint8_t* in, cudaStream_t s) {
+void launch_verify_crc(gp_ctx* ctx, const uint8_t* in, uint64_t len_bound, cudaStream_t s) {
   Workspace& w = ctx->ws;
   uint32_t* crc = reinterpret_cast<uint32_t*>(&w.plan->crc_calc);
   CrcEpilogue ep;
   ep.mode = 1;
   ep.plan = w.plan;
-  crc_range(ctx, in, &w.plan->off_index, 0, &w.plan->il, &w.plan->vl, &w.plan->rl, 0, crc, s, ep);
+  crc_range(ctx, in, &w.plan->off_index, 0, &w.plan->il, &w.plan->vl, &w.plan->rl, 0, len_bound, crc, s, ep);
 }
 
 void launch_merge_status(gp_ctx* ctx, cudaStream_t s) {

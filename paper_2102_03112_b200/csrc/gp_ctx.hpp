@@ -242,7 +242,7 @@ void launch_finish_container(gp_ctx* ctx, uint8_t* out, uint64_t cap, uint64_t* 
                              cudaStream_t s);
 void launch_parse_container(gp_ctx* ctx, const uint8_t* in, uint64_t len, const uint64_t* len_dev,
                             const gp_pipeline_config* hint, cudaStream_t s);
-void launch_verify_crc(gp_ctx* ctx, const uint8_t* in, cudaStream_t s);
+void launch_verify_crc(gp_ctx* ctx, const uint8_t* in, uint64_t len_bound, cudaStream_t s);
 void launch_merge_status(gp_ctx* ctx, cudaStream_t s);
 
 // indexcodec.cu
