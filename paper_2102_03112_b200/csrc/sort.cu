@@ -242,16 +242,20 @@ void launch_table_scan(gp_ctx* ctx, uint32_t* table, const uint64_t* n_dev, uint
 
 // Sorts (keys, vals) of length *n_dev in place over `bits` low key bits
 // (multiple of 8, <= 32), ping-ponging through (ktmp, vtmp).  n_bound sizes grids.
+// hist_ready: the caller already accumulated the digit histograms of every
+// pass into sort_hist (the value codec's key kernel does).
 void launch_radix_sort(gp_ctx* ctx, uint32_t* keys, uint32_t* vals, uint32_t* ktmp, uint32_t* vtmp,
-                       const uint64_t* n_dev, uint64_t n_bound, int bits, cudaStream_t s) {
+                       const uint64_t* n_dev, uint64_t n_bound, int bits, cudaStream_t s, bool hist_ready) {
   Workspace& w = ctx->ws;
   const int npass = bits / 8;
   const uint64_t ntiles = (n_bound + kTile - 1) / kTile;
   cudaMemsetAsync(w.sort_flags, 0, (64 + ntiles) * sizeof(uint32_t), s);
-  cudaMemsetAsync(w.sort_hist, 0, 4 * 256 * sizeof(uint32_t), s);
-  const int hgrid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((n_bound + kBlock - 1) / kBlock,
-                                                                               ctx->sm_count * 2ULL)));
-  GP_LAUNCH(ctx, radix_hist, hgrid, kBlock, 0, s, keys, n_dev, npass, w.sort_hist, w.status);
+  if (!hist_ready) {
+    cudaMemsetAsync(w.sort_hist, 0, 4 * 256 * sizeof(uint32_t), s);
+    const int hgrid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((n_bound + kBlock - 1) / kBlock,
+                                                                                 ctx->sm_count * 2ULL)));
+    GP_LAUNCH(ctx, radix_hist, hgrid, kBlock, 0, s, keys, n_dev, npass, w.sort_hist, w.status);
+  }
   uint32_t *ki = keys, *vi = vals, *ko = ktmp, *vo = vtmp;
   uint32_t* agg = w.sort_table;
   uint32_t* inc = w.sort_table + 256 * (ntiles + 1);

@@ -71,34 +71,58 @@ __device__ __forceinline__ uint64_t desc_key64(double v) {
   return ~asc;
 }
 
+// ghist != null (f32 values): the radix sort's four digit histograms are
+// accumulated here too (shared bins, warp-aggregated), so the sort skips its
+// own histogram pass over the keys
 __global__ void fit_keys(const ValSrc values, Plan* plan, uint32_t* __restrict__ keys,
-                         uint32_t* __restrict__ idx, const uint32_t* status) {
+                         uint32_t* __restrict__ idx, uint32_t* __restrict__ ghist, const uint32_t* status) {
   __shared__ uint32_t cnt;
+  __shared__ uint32_t h[4][256];
   if (failed(status) || !fit_active(plan)) return;
   if (threadIdx.x == 0) cnt = 0;
+  if (ghist)
+    for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) h[i >> 8][i & 255] = 0;
   __syncthreads();
   const uint64_t n = plan->n_values;
+  const int lane = threadIdx.x & 31;
   uint32_t nonneg = 0;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    if (values.f64) {
-      const double v = values.f64[i];
-      keys[i] = static_cast<uint32_t>(desc_key64(v));
-      nonneg += v >= 0.0 ? 1u : 0u;
-    } else {
-      const float v = values.f32[i];
-      uint32_t b = __float_as_uint(v);
-      if (b == 0x80000000u) b = 0;  // -0.0 == +0.0 under operator>
-      const uint32_t asc = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-      keys[i] = ~asc;  // ascending key order == descending value order
-      nonneg += v >= 0.0f ? 1u : 0u;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x); i0 < n; i0 += stride) {  // warp-uniform
+    const uint64_t i = i0 + threadIdx.x;
+    const bool ok = i < n;
+    uint32_t key = 0;
+    if (ok) {
+      if (values.f64) {
+        const double v = values.f64[i];
+        key = static_cast<uint32_t>(desc_key64(v));
+        nonneg += v >= 0.0 ? 1u : 0u;
+      } else {
+        const float v = values.f32[i];
+        uint32_t b = __float_as_uint(v);
+        if (b == 0x80000000u) b = 0;  // -0.0 == +0.0 under operator>
+        const uint32_t asc = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+        key = ~asc;  // ascending key order == descending value order
+        nonneg += v >= 0.0f ? 1u : 0u;
+      }
+      keys[i] = key;
+      idx[i] = static_cast<uint32_t>(i);
     }
-    idx[i] = static_cast<uint32_t>(i);
+    if (ghist) {
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const uint32_t dig = ok ? (key >> (8 * p)) & 255u : 256u;
+        const unsigned peers = __match_any_sync(kFull, dig);
+        if (ok && (peers & ((1u << lane) - 1)) == 0) atomicAdd(&h[p][dig], __popc(peers));
+      }
+    }
   }
   nonneg = warp_sum(nonneg);
   if ((threadIdx.x & 31) == 0 && nonneg) atomicAdd(&cnt, nonneg);
   __syncthreads();
   if (threadIdx.x == 0 && cnt) atomicAdd(&plan->sign_split, cnt);
+  if (ghist)
+    for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x)
+      if (h[i >> 8][i & 255]) atomicAdd(&ghist[i], h[i >> 8][i & 255]);
 }
 
 // f64 pass 2 keys: the high words in pass 1's order
@@ -1560,7 +1584,7 @@ __global__ void dexp_decide(Plan* plan, const uint32_t* status) {
 }  // namespace
 
 void launch_radix_sort(gp_ctx* ctx, uint32_t* keys, uint32_t* vals, uint32_t* ktmp, uint32_t* vtmp,
-                       const uint64_t* n_dev, uint64_t n_bound, int bits, cudaStream_t s);
+                       const uint64_t* n_dev, uint64_t n_bound, int bits, cudaStream_t s, bool hist_ready = false);
 
 static_assert(sizeof(SegNode) == 32, "workspace sizes SegNode at 32 bytes");
 static_assert(sizeof(SegState) == 32, "workspace sizes SegState at 32 bytes");
@@ -1570,8 +1594,12 @@ void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, 
   Workspace& w = ctx->ws;
   // sign_split / identity / fit_kind / dexp_fail: reset by the encode's init_plan (capi.cu)
   const ValSrc vals{w.values, ctx->vals64};
-  GP_LAUNCH(ctx, fit_keys, grid_for(ctx, n_bound, 256), 256, 0, s, vals, w.plan, w.u32a, w.u32b, w.status);
-  launch_radix_sort(ctx, w.u32a, w.u32b, w.u32c, w.u32d, &w.plan->n_values, n_bound, 32, s);
+  // f32 values: the keys kernel also builds the sort's digit histograms
+  uint32_t* ghist = ctx->vals64 ? nullptr : w.sort_hist;
+  if (ghist) cudaMemsetAsync(ghist, 0, 4 * 256 * sizeof(uint32_t), s);
+  GP_LAUNCH(ctx, fit_keys, std::min(grid_for(ctx, n_bound, 256), 2 * ctx->sm_count), 256, 0, s, vals, w.plan, w.u32a,
+            w.u32b, ghist, w.status);
+  launch_radix_sort(ctx, w.u32a, w.u32b, w.u32c, w.u32d, &w.plan->n_values, n_bound, 32, s, ghist != nullptr);
   if (ctx->vals64) {  // the high words, stable on top of the low-word order
     GP_LAUNCH(ctx, fit_keys_hi, grid_for(ctx, n_bound, 256), 256, 0, s, ctx->vals64, w.plan, w.u32b, w.u32a, w.status);
     launch_radix_sort(ctx, w.u32a, w.u32b, w.u32c, w.u32d, &w.plan->n_values, n_bound, 32, s);
