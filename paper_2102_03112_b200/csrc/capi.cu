@@ -575,6 +575,8 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
       if (f64) {
         GP_STAGE(ctx, ST_GATHER, s, launch_gather_values64(ctx, dense64, d_support, d_values64, r, d, s));
         ctx->vals64 = ctx->ws.f64a;
+      } else if (vm == GP_VALUE_FIT_POLY || vm == GP_VALUE_FIT_DEXP) {
+        ctx->gather_dense = d_dense;  // the fit's key kernel gathers v[j] = dense[sel[j]] itself
       } else {
         GP_STAGE(ctx, ST_GATHER, s, launch_gather_values(ctx, d_dense, d, s));
       }
@@ -607,6 +609,7 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
   }
   GP_STAGE(ctx, ST_PACK, s, launch_finish_container(ctx, d_out, cap, d_len, bound, s));
   ctx->vals64 = nullptr;  // captured by the launches above
+  ctx->gather_dense = nullptr;
   return check_launch(ctx, "encode");
 }
 

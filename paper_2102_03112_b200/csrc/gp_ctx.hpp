@@ -174,6 +174,7 @@ struct gp_ctx {
   cudaEvent_t index_event = nullptr;   // gp_ctx_set_index_event: recorded once encode's index payload is final
   bool decode_overwrite = false;
   const double* vals64 = nullptr;      // this encode's f64 value sequence (null: ws.values, f32)
+  const float* gather_dense = nullptr;  // Bloom + fit encode: the key kernel gathers dense[sel[j]] (values_fit.cu)
   cudaStream_t side = nullptr;         // decode work before the CRC verdict runs here, beside the CRC
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;       // gp_ctx_set_decode_overwrite: dense = scale * decoded (zeros off the support)
 };

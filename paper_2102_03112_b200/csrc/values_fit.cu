@@ -74,8 +74,12 @@ __device__ __forceinline__ uint64_t desc_key64(double v) {
 // ghist != null (f32 values): the radix sort's four digit histograms are
 // accumulated here too (shared bins, warp-aggregated), so the sort skips its
 // own histogram pass over the keys
+//
+// gdense != null: the values are gathered here, v[j] = gdense[gsel[j]]
+// (gather_values, pipeline.cpp:38-54), and stored to vout for the later passes.
 __global__ void fit_keys(const ValSrc values, Plan* plan, uint32_t* __restrict__ keys,
-                         uint32_t* __restrict__ idx, uint32_t* __restrict__ ghist, const uint32_t* status) {
+                         uint32_t* __restrict__ idx, uint32_t* __restrict__ ghist, const float* __restrict__ gdense,
+                         const uint32_t* __restrict__ gsel, float* __restrict__ vout, const uint32_t* status) {
   __shared__ uint32_t cnt;
   __shared__ uint32_t h[4][256];
   if (failed(status) || !fit_active(plan)) return;
@@ -97,7 +101,13 @@ __global__ void fit_keys(const ValSrc values, Plan* plan, uint32_t* __restrict__
         key = static_cast<uint32_t>(desc_key64(v));
         nonneg += v >= 0.0 ? 1u : 0u;
       } else {
-        const float v = values.f32[i];
+        float v;
+        if (gdense) {
+          v = gdense[gsel[i]];
+          vout[i] = v;
+        } else {
+          v = values.f32[i];
+        }
         uint32_t b = __float_as_uint(v);
         if (b == 0x80000000u) b = 0;  // -0.0 == +0.0 under operator>
         const uint32_t asc = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
@@ -1597,8 +1607,9 @@ void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, 
   // f32 values: the keys kernel also builds the sort's digit histograms
   uint32_t* ghist = ctx->vals64 ? nullptr : w.sort_hist;
   if (ghist) cudaMemsetAsync(ghist, 0, 4 * 256 * sizeof(uint32_t), s);
+  const float* gdense = ctx->vals64 ? nullptr : ctx->gather_dense;
   GP_LAUNCH(ctx, fit_keys, std::min(grid_for(ctx, n_bound, 256), 2 * ctx->sm_count), 256, 0, s, vals, w.plan, w.u32a,
-            w.u32b, ghist, w.status);
+            w.u32b, ghist, gdense, w.sel, w.values, w.status);
   launch_radix_sort(ctx, w.u32a, w.u32b, w.u32c, w.u32d, &w.plan->n_values, n_bound, 32, s, ghist != nullptr);
   if (ctx->vals64) {  // the high words, stable on top of the low-word order
     GP_LAUNCH(ctx, fit_keys_hi, grid_for(ctx, n_bound, 256), 256, 0, s, ctx->vals64, w.plan, w.u32b, w.u32a, w.status);
