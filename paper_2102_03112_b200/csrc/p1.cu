@@ -113,7 +113,8 @@ __global__ void p1_bits(const Plan* plan, const uint8_t* __restrict__ flags, uin
 }  // namespace
 
 void launch_radix_sort(gp_ctx* ctx, uint32_t* keys, uint32_t* vals, uint32_t* ktmp, uint32_t* vtmp,
-                       const uint64_t* n_dev, uint64_t n_bound, int bits, cudaStream_t s, bool hist_ready = false);
+                       const uint64_t* n_dev, uint64_t n_bound, int bits, cudaStream_t s, bool hist_ready = false,
+                       const float* fit_v = nullptr, double* fit_t = nullptr);
 void launch_flags_compact(gp_ctx* ctx, int method, uint64_t n_bound, cudaStream_t s);
 
 void launch_select_p1(gp_ctx* ctx, uint64_t n_bound, uint64_t r_bound, cudaStream_t s) {

@@ -52,12 +52,22 @@ __global__ void __launch_bounds__(kBlock) radix_hist(const uint32_t* __restrict_
     if (h[i >> 8][i & 255]) atomicAdd(&ghist[i], h[i >> 8][i & 255]);
 }
 
+// FitOut (the value codec's last pass, f32 values): besides the sorted
+// (key, index) pairs, write the folded fp64 sequence t of fit_prepare —
+// t[s] = v[map[s]] below the sign split l, -v[map[n-1-(s-l)]] above it
+// (curvefit.cpp:26-39) — and clear the identity flag if any index moved.
+struct FitOut {
+  const float* v = nullptr;
+  double* t = nullptr;
+  Plan* plan = nullptr;
+};
+
 __global__ void __launch_bounds__(kBlock) radix_onesweep(const uint32_t* __restrict__ kin,
                                                          const uint32_t* __restrict__ vin, const uint64_t* n_dev,
                                                          int pass, const uint32_t* __restrict__ ghist,
                                                          uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                          uint32_t* flags, uint32_t* agg, uint32_t* inc,
-                                                         uint32_t* ticket, const uint32_t* status) {
+                                                         uint32_t* ticket, const FitOut fo, const uint32_t* status) {
   __shared__ uint32_t wcnt[kSortWarps][256];
   __shared__ uint32_t base[256];
   __shared__ __align__(16) uint32_t red_sh[kSortWarps][256];
@@ -176,6 +186,8 @@ __global__ void __launch_bounds__(kBlock) radix_onesweep(const uint32_t* __restr
   base[d] += prefix;
   __syncthreads();
   // ---- scatter
+  const uint64_t l = fo.t ? fo.plan->sign_split : 0;
+  bool moved = false;
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
     if (seg + 32 * j + lane < n) {
@@ -183,8 +195,15 @@ __global__ void __launch_bounds__(kBlock) radix_onesweep(const uint32_t* __restr
       const uint32_t dst = base[dig] + wcnt[warp][dig] + rank[j];
       kout[dst] = key[j];
       vout[dst] = val[j];
+      if (fo.t) {
+        const double x = static_cast<double>(fo.v[val[j]]);
+        if (dst < l) fo.t[dst] = x;
+        else fo.t[n - 1 - (dst - l)] = -x;
+        moved |= val[j] != dst;
+      }
     }
   }
+  if (fo.t && __syncthreads_or(moved) && threadIdx.x == 0) fo.plan->identity = 0;
 }
 
 // In-place exclusive scan of a u32 array whose length is n_mul * tiles(*n_dev)
@@ -245,7 +264,8 @@ void launch_table_scan(gp_ctx* ctx, uint32_t* table, const uint64_t* n_dev, uint
 // hist_ready: the caller already accumulated the digit histograms of every
 // pass into sort_hist (the value codec's key kernel does).
 void launch_radix_sort(gp_ctx* ctx, uint32_t* keys, uint32_t* vals, uint32_t* ktmp, uint32_t* vtmp,
-                       const uint64_t* n_dev, uint64_t n_bound, int bits, cudaStream_t s, bool hist_ready) {
+                       const uint64_t* n_dev, uint64_t n_bound, int bits, cudaStream_t s, bool hist_ready,
+                       const float* fit_v, double* fit_t) {
   Workspace& w = ctx->ws;
   const int npass = bits / 8;
   const uint64_t ntiles = (n_bound + kTile - 1) / kTile;
@@ -260,8 +280,14 @@ void launch_radix_sort(gp_ctx* ctx, uint32_t* keys, uint32_t* vals, uint32_t* kt
   uint32_t* agg = w.sort_table;
   uint32_t* inc = w.sort_table + 256 * (ntiles + 1);
   for (int p = 0; p < npass; ++p) {
+    FitOut fo;
+    if (fit_t && p == npass - 1) {
+      fo.v = fit_v;
+      fo.t = fit_t;
+      fo.plan = w.plan;
+    }
     GP_LAUNCH(ctx, radix_onesweep, static_cast<int>(std::max<uint64_t>(1, ntiles)), kBlock, 0, s, ki, vi, n_dev, p,
-              w.sort_hist, ko, vo, w.sort_flags + 64, agg, inc, w.sort_flags, w.status);
+              w.sort_hist, ko, vo, w.sort_flags + 64, agg, inc, w.sort_flags, fo, w.status);
     std::swap(ki, ko);
     std::swap(vi, vo);
   }

@@ -1594,7 +1594,8 @@ __global__ void dexp_decide(Plan* plan, const uint32_t* status) {
 }  // namespace
 
 void launch_radix_sort(gp_ctx* ctx, uint32_t* keys, uint32_t* vals, uint32_t* ktmp, uint32_t* vtmp,
-                       const uint64_t* n_dev, uint64_t n_bound, int bits, cudaStream_t s, bool hist_ready = false);
+                       const uint64_t* n_dev, uint64_t n_bound, int bits, cudaStream_t s, bool hist_ready = false,
+                       const float* fit_v = nullptr, double* fit_t = nullptr);
 
 static_assert(sizeof(SegNode) == 32, "workspace sizes SegNode at 32 bytes");
 static_assert(sizeof(SegState) == 32, "workspace sizes SegState at 32 bytes");
@@ -1610,12 +1611,14 @@ void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, 
   const float* gdense = ctx->vals64 ? nullptr : ctx->gather_dense;
   GP_LAUNCH(ctx, fit_keys, std::min(grid_for(ctx, n_bound, 256), 2 * ctx->sm_count), 256, 0, s, vals, w.plan, w.u32a,
             w.u32b, ghist, gdense, w.sel, w.values, w.status);
-  launch_radix_sort(ctx, w.u32a, w.u32b, w.u32c, w.u32d, &w.plan->n_values, n_bound, 32, s, ghist != nullptr);
+  // f32: the sort's last pass also writes fit_prepare's folded sequence t and the identity flag
+  launch_radix_sort(ctx, w.u32a, w.u32b, w.u32c, w.u32d, &w.plan->n_values, n_bound, 32, s, ghist != nullptr,
+                    ghist ? w.values : nullptr, ghist ? w.f64b : nullptr);
   if (ctx->vals64) {  // the high words, stable on top of the low-word order
     GP_LAUNCH(ctx, fit_keys_hi, grid_for(ctx, n_bound, 256), 256, 0, s, ctx->vals64, w.plan, w.u32b, w.u32a, w.status);
     launch_radix_sort(ctx, w.u32a, w.u32b, w.u32c, w.u32d, &w.plan->n_values, n_bound, 32, s);
   }
-  GP_LAUNCH(ctx, fit_prepare, grid_for(ctx, n_bound, 256), 256, 0, s, vals, w.u32b, w.plan, w.f64b, w.status);
+  if (!ghist) GP_LAUNCH(ctx, fit_prepare, grid_for(ctx, n_bound, 256), 256, 0, s, vals, w.u32b, w.plan, w.f64b, w.status);
   if (dexp) {
     GP_LAUNCH(ctx, dexp_fit, 2, kDexpBlock, 0, s, w.plan, w.f64b, w.seg_end, w.coeffs, w.status);
     GP_LAUNCH(ctx, dexp_decide, 1, 1, 0, s, w.plan, w.status);
