@@ -343,9 +343,14 @@ __global__ void __launch_bounds__(kScanBlock) members_compact(const uint32_t* __
 // barrier reads its offset — the sum of the earlier tiles' counts, one warp
 // read — instead of spinning on a decoupled look-back chain (~200 tiles at
 // C4: 19 us).
+__device__ __forceinline__ void after_scan_body(Plan* plan, uint64_t n, uint64_t cap, int decoding,
+                                                uint32_t* status);
+
+// (the last tile's last thread also runs the post-scan bookkeeping of
+// bloom_after_scan: one launch fewer per scan)
 __global__ void __launch_bounds__(kScanBlock) members_compact_coop(const uint32_t* __restrict__ bitmap, Plan* plan,
                                                                    uint32_t* __restrict__ pos_out, uint64_t cap,
-                                                                   uint64_t* tcnt, const uint32_t* status) {
+                                                                   uint64_t* tcnt, int decoding, uint32_t* status) {
   __shared__ uint64_t sh[36];
   cg::grid_group grid = cg::this_grid();
   if (failed(status)) return;  // uniform: nothing latches this word while the kernel runs
@@ -390,16 +395,18 @@ __global__ void __launch_bounds__(kScanBlock) members_compact_coop(const uint32_
       if (at < cap) pos_out[at] = static_cast<uint32_t>(lo + 32 * (wb + 32 * i + lane) + (__ffs(x) - 1));
     o += __shfl_sync(kFull, incl, 31);
   }
-  if (tile == ntiles - 1 && threadIdx.x == kScanBlock - 1) plan->n_pos = o;
+  if (tile == ntiles - 1 && threadIdx.x == kScanBlock - 1) {
+    plan->n_pos = o;
+    after_scan_body(plan, o, cap, decoding, status);
+  }
 }
 
 // Post-scan bookkeeping: |P| >= r (pipeline.cpp:284-285), value counts, and
 // the P0 / Pd / naive selections which are slices of P.
-__global__ void bloom_after_scan(Plan* plan, uint64_t cap, int decoding, uint32_t* status) {
-  if (failed(status)) return;
+__device__ __forceinline__ void after_scan_body(Plan* plan, uint64_t n, uint64_t cap, int decoding,
+                                                uint32_t* status) {
   const uint8_t im = plan->index_method;
-  if (im < GP_INDEX_BLOOM_P0 || im > GP_INDEX_BLOOM_NAIVE) return;
-  const uint64_t n = plan->n_pos, r = plan->r;
+  const uint64_t r = plan->r;
   if (n > cap) return latch(status, GP_CAPACITY);
   if (im == GP_INDEX_BLOOM_P0) {
     plan->n_sel = n;
@@ -412,6 +419,13 @@ __global__ void bloom_after_scan(Plan* plan, uint64_t cap, int decoding, uint32_
     plan->n_sel = r;
     plan->n_values = r;
   }
+}
+
+__global__ void bloom_after_scan(Plan* plan, uint64_t cap, int decoding, uint32_t* status) {
+  if (failed(status)) return;
+  const uint8_t im = plan->index_method;
+  if (im < GP_INDEX_BLOOM_P0 || im > GP_INDEX_BLOOM_NAIVE) return;
+  after_scan_body(plan, plan->n_pos, cap, decoding, status);
 }
 
 // sel <- P (P0, naive) or the Pd slice (bloom.cpp:224-236)
@@ -492,8 +506,9 @@ void launch_bloom_scan(gp_ctx* ctx, uint64_t d_bound, uint64_t m_host, bool deco
     uint32_t* pos = w.pos;
     uint64_t cap = ctx->max_d;
     uint64_t* tc = w.tiles;
+    int dec = decoding ? 1 : 0;
     uint32_t* st = w.status;
-    void* args[] = {&bm, &plan, &pos, &cap, &tc, &st};
+    void* args[] = {&bm, &plan, &pos, &cap, &tc, &dec, &st};
     cudaLaunchCooperativeKernel(reinterpret_cast<void*>(members_compact_coop), grid, kScanBlock, args, 0, s);
     ++ctx->launches;
   } else {
@@ -501,8 +516,8 @@ void launch_bloom_scan(gp_ctx* ctx, uint64_t d_bound, uint64_t m_host, bool deco
     GP_LAUNCH(ctx, members_compact,
               static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(ntiles, ctx->sm_count * 4ULL))), kScanBlock, 0,
               s, bitmap, w.plan, w.pos, ctx->max_d, w.tiles, w.ticket, w.status);
+    GP_LAUNCH(ctx, bloom_after_scan, 1, 1, 0, s, w.plan, ctx->max_d, decoding ? 1 : 0, w.status);
   }
-  GP_LAUNCH(ctx, bloom_after_scan, 1, 1, 0, s, w.plan, ctx->max_d, decoding ? 1 : 0, w.status);
 }
 
 void launch_bloom_after_scan(gp_ctx* ctx, bool decoding, cudaStream_t s) {
