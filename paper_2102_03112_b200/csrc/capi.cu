@@ -476,6 +476,8 @@ static int encode_common(gp_ctx* ctx, const float* d_dense, uint64_t d, const ui
   const bool f64 = d_values64 || ef_residual64;
   if (!ctx || !cfg || !d_out || (!d_dense && !f64) || (ef_residual64 && !d_dense))
     return set_error(ctx, GP_ERROR, "encode: null argument");
+  ctx->vals64 = nullptr;  // per-encode launch inputs (set below, cleared at the end): never stale
+  ctx->gather_dense = nullptr;
   auto s = static_cast<cudaStream_t>(stream);
   if (d < 1) return set_error(ctx, GP_ERROR, "sparsifier: dim must be >= 1");
   if (d > 0xFFFFFFFFULL) return set_error(ctx, GP_ERROR, "sparsifier: dim exceeds 32-bit index space");

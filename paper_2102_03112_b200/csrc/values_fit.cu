@@ -420,6 +420,55 @@ __global__ void __launch_bounds__(256) fit_segment_coop(Plan* plan, const double
   int sweep = 0;
   uint32_t nseg = 0;  // replicated in every block
   bool overflow = false;
+  // Automatic budgets (max_segments 0) depend only on each part's end points:
+  // when every part gets at most one split (the BASELINE configs), the parts'
+  // root sweeps share one grid sweep and one barrier, not one each
+  bool joint = max_segments <= 0 && nparts > 0;
+  long long jbudget[2] = {1, 1};
+  for (int pi = 0; pi < nparts && joint; ++pi) {
+    const uint32_t b = pb[pi], e = pe[pi], len = e - b;
+    if (len >= 4) {  // part_budget (curvefit.cpp:101-110, :424-428)
+      const double km = fabs(__dsub_rn(__dsub_rn(t[b], t[b + 1]), __dsub_rn(t[e - 2], t[e - 1])));
+      const double p = ceil(2.0 * sqrt(km > 0.0 ? km : 0.0));
+      const int kc = static_cast<int>(p) > 1 ? static_cast<int>(p) : 1;
+      jbudget[pi] = kc + 1 < 0xffff ? kc + 1 : 0xffff;
+    }
+    joint = jbudget[pi] <= 2;
+  }
+  if (joint) {
+    uint32_t rb[2], re[2];
+    int nr = 0, slot[2] = {-1, -1};
+    for (int pi = 0; pi < nparts; ++pi)
+      if (jbudget[pi] == 2) {
+        slot[pi] = nr;
+        rb[nr] = pb[pi];
+        re[nr++] = pe[pi];
+      }
+    if (nr > 0) {
+      seg_sweep_few(t, nullptr, nullptr, nr, rb, re, pdev, parg, sdev, sarg, sres_dev, sres_arg, grid);
+      ++sweep;
+    }
+    for (int pi = 0; pi < nparts; ++pi) {
+      const uint32_t b = pb[pi], e = pe[pi], len = e - b;
+      uint32_t split = 0;
+      if (slot[pi] >= 0) {
+        const double dv = sres_dev[slot[pi]];
+        SegNode root{0, len, dv > 0.0 ? sres_arg[slot[pi]] - b : 0u, 0u, dv, kNoChild, 0u};
+        make_live(root, mp);
+        if (root.live) split = root.arg;
+      }
+      if (nseg + 2 > seg_cap) {
+        overflow = true;
+        break;
+      }
+      if (leader) {
+        if (split) seg_end[nseg] = b + split;
+        seg_end[nseg + (split ? 1 : 0)] = e;
+      }
+      nseg += split ? 2 : 1;
+    }
+    nparts = 0;  // done: skip the general loop below
+  }
   for (int pi = 0; pi < nparts; ++pi) {
     const uint32_t b = pb[pi], e = pe[pi], len = e - b;
     long long budget;
