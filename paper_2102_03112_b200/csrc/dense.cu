@@ -2,20 +2,21 @@
 // one pass each way (C3, NCF-style natural sparsity, where the support is the
 // nonzeros: top_r(g, nnz)).
 //
-// Encode (`nz_encode`, one read of g): every 8192-element tile ballots its
-// nonzeros into the bitmap words (gradient.cpp:56-65, :81-86: bit i of byte
-// i/8, LSB-first), compacts the nonzero values in shared memory and, with the
-// tile's value offset from a decoupled look-back, stores both straight into
-// the container (index payload at 49, value payload at 49 + ceil(d/8);
-// pipeline.cpp:171-173, :56-93 raw f32) with 16-byte stores.  The selection
-// is SPECULATIVE: top_r(g, r) is the nonzero set exactly when r equals the
-// nonzero count (the r largest |g| are then all nonzero keys and ties cannot
-// straddle the cut, sparsify.cpp:32-46), which only the last tile knows.  It
-// opens a gate word: SKIP when the count matched (the general top-r + bitmap +
-// raw kernels that follow on the stream, launched against the gate as their
-// status word, return at once), 0 otherwise (they run and overwrite every
-// byte).  gate_merge then moves any error the general path latched into the
-// context status.
+// Encode (`nz_count` → `nz_write`, two reads of g, the second partly from
+// L2): every 8192-element tile ballots its nonzeros into the bitmap words
+// (gradient.cpp:56-65, :81-86: bit i of byte i/8, LSB-first), compacts the
+// nonzero values in shared memory and stores both straight into the container
+// at the tile's value offset (index payload at 49, value payload at 49 +
+// ceil(d/8); pipeline.cpp:171-173, :56-93 raw f32) with 16-byte stores; the
+// offsets come from a counting pass over g, not a look-back chain.  The
+// selection is SPECULATIVE: top_r(g, r) is the nonzero set exactly when r
+// equals the nonzero count (the r largest |g| are then all nonzero keys and
+// ties cannot straddle the cut, sparsify.cpp:32-46), which the counting pass
+// knows.  It opens a gate word: SKIP when the count matched (the general
+// top-r + bitmap + raw kernels that follow on the stream, launched against the
+// gate as their status word, return at once), 0 otherwise (they run and
+// overwrite every byte).  gate_merge then moves any error the general path
+// latched into the context status.
 //
 // Decode (`bm_counts` → one-block scan → `bm_total` → `bm_scatter`): per-tile
 // popcounts of the bitmap, their prefix, the popcount == r check
@@ -34,7 +35,6 @@ namespace {
 constexpr int kNzBlock = 256;                  // 8 warps
 constexpr int kNzTile = kNzBlock * 32;         // elements per tile: 32 per lane, 1024 per warp
 constexpr uint32_t kGateSkip = 0xFFFFu;        // gate value: the fast path produced the payloads
-constexpr int kNzSmem = 4 * 2 * ((kNzTile + 8) + (kNzBlock + 8));  // nz_encode's double buffers
 
 // Copies n bytes from 4-byte-aligned shared memory to an arbitrary global
 // address: single bytes up to the first 16-byte boundary and after the last,
@@ -106,37 +106,115 @@ __device__ __forceinline__ void nz_load(const float* __restrict__ g, uint64_t d,
   }
 }
 
-// Software-pipelined over tiles: the loads of the block's next tile are in
-// flight while warp 0 walks the look-back of the current one and while the
-// current tile's payload bytes go out from shared memory (double-buffered), so
-// the look-back's L2 round trips no longer serialise with HBM latency.
-__global__ void __launch_bounds__(kNzBlock) nz_encode(const float* __restrict__ g, uint64_t d, uint64_t r,
-                                                      uint8_t* out, Plan* plan, uint64_t* tiles, uint32_t* ticket,
-                                                      uint32_t* gate, const uint32_t* status) {
-  extern __shared__ uint32_t nz_smem[];  // vals[2][kNzTile + 8] | words[2][kNzBlock + 8]
-  uint32_t(*vals)[kNzTile + 8] = reinterpret_cast<uint32_t(*)[kNzTile + 8]>(nz_smem);
-  uint32_t(*words)[kNzBlock + 8] = reinterpret_cast<uint32_t(*)[kNzBlock + 8]>(nz_smem + 2 * (kNzTile + 8));
-  __shared__ uint32_t wcnt[2][kNzBlock / 32];
-  __shared__ uint64_t s_prefix[2];
-  __shared__ uint32_t s_tile[2];
+// `nz_count` streams g once in warp items of 1024 keys (no block barrier; each
+// warp adds its count into its tile's zeroed counter); the last block to
+// finish (ticket) turns the tile counts into exclusive prefixes in place,
+// checks nnz == r and opens the gate.  `nz_write` then walks the tiles in
+// DESCENDING order — the tail of g that nz_count read last may still be in
+// the 126 MB L2 — and stores each tile at its known offset.  Measured
+// against the one-pass form with a decoupled look-back (round 2): that kernel
+// spent ~2/3 of its warp samples parked at the barrier behind warp 0's
+// look-back walk (ncu: 4367 of ~7000 samples "barrier"), C3 0.294 -> 0.276 ms.
+__global__ void __launch_bounds__(kNzBlock) nz_count(const float* __restrict__ g, uint64_t d, uint64_t r, Plan* plan,
+                                                     uint64_t* tiles, uint32_t* ticket, uint32_t* gate,
+                                                     const uint32_t* status) {
+  __shared__ uint64_t scratch[33];
+  __shared__ bool s_last;
   if (failed(status)) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *gate = ld_relaxed_u32(status);  // the general path stays shut
     return;
   }
+  const int lane = threadIdx.x & 31;
+  const uint64_t ntiles = (d + kNzTile - 1) / kNzTile;
+  const uint64_t nitems = (d + 1023) / 1024;  // warp items of 1024 keys, 8 per tile
+  const bool vec = (reinterpret_cast<uintptr_t>(g) & 15) == 0;
+  const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (kNzBlock / 32);
+  // no block barrier per tile: each warp adds its item's count into the
+  // tile's (zeroed) counter, two items' loads in flight per iteration
+  for (uint64_t it = blockIdx.x * static_cast<uint64_t>(kNzBlock / 32) + (threadIdx.x >> 5); it < nitems;
+       it += 2 * nwarps) {
+    const uint64_t it2 = it + nwarps;
+    const uint64_t base = it * 1024, base2 = it2 * 1024;
+    uint32_t c = 0, c2 = 0;
+    if (vec && base2 + 1024 <= d) {
+      float4 v[16];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __ldg(reinterpret_cast<const float4*>(g + base + 4 * (lane + 32 * j)));
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[8 + j] = __ldg(reinterpret_cast<const float4*>(g + base2 + 4 * (lane + 32 * j)));
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t n = ((__float_as_uint(v[j].x) & 0x7FFFFFFFu) != 0u) +
+                           ((__float_as_uint(v[j].y) & 0x7FFFFFFFu) != 0u) +
+                           ((__float_as_uint(v[j].z) & 0x7FFFFFFFu) != 0u) +
+                           ((__float_as_uint(v[j].w) & 0x7FFFFFFFu) != 0u);
+        if (j < 8) c += n; else c2 += n;
+      }
+    } else {
+      for (int k = 0; k < 32; ++k) {
+        const uint64_t i = base + 32 * k + lane, i2 = base2 + 32 * k + lane;
+        if (i < d) c += (__float_as_uint(g[i]) & 0x7FFFFFFFu) != 0u;
+        if (it2 < nitems && i2 < d) c2 += (__float_as_uint(g[i2]) & 0x7FFFFFFFu) != 0u;
+      }
+    }
+    c = __reduce_add_sync(kFull, c);
+    c2 = __reduce_add_sync(kFull, c2);
+    if (lane == 0) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&tiles[it >> 3]), static_cast<unsigned long long>(c));
+      if (it2 < nitems)
+        atomicAdd(reinterpret_cast<unsigned long long*>(&tiles[it2 >> 3]), static_cast<unsigned long long>(c2));
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  // last block done: exclusive prefixes of the tile counts, the nnz == r gate
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const uint64_t per = (ntiles + kNzBlock - 1) / kNzBlock;
+  const uint64_t t0 = threadIdx.x * per;
+  uint64_t mine = 0;
+  for (uint64_t t = t0; t < t0 + per && t < ntiles; ++t) mine += __ldcg(&tiles[t]);
+  uint64_t nnz = 0;
+  uint64_t run = block_exclusive_sum<uint64_t, kNzBlock>(mine, scratch, nnz);
+  for (uint64_t t = t0; t < t0 + per && t < ntiles; ++t) {
+    const uint64_t c = __ldcg(&tiles[t]);
+    tiles[t] = run;
+    run += c;
+  }
+  if (threadIdx.x == 0) {
+    if (nnz == r) {
+      plan->vl = 4 * r;
+      plan->n_values = r;
+      plan->n_sel = r;
+      *gate = kGateSkip;
+    } else {
+      *gate = 0u;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kNzBlock, 4) nz_write(const float* __restrict__ g, uint64_t d, uint64_t r,
+                                                     uint8_t* out, const uint64_t* tiles, const uint32_t* status) {
+  __shared__ uint32_t vals[kNzTile + 8];
+  __shared__ uint32_t words[kNzBlock + 8];
+  __shared__ uint32_t wcnt[kNzBlock / 32];
+  if (failed(status)) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
   const uint64_t ntiles = (d + kNzTile - 1) / kNzTile;
   const uint64_t bm_bytes = (d + 7) / 8;
   uint8_t* bm_out = out + 49;
   uint8_t* val_out = out + 49 + bm_bytes;
-  if (threadIdx.x == 0) s_tile[0] = atomicAdd(ticket, 1u);
-  __syncthreads();
-  uint32_t tile = s_tile[0];
   uint32_t x[32];
-  if (tile < ntiles) nz_load(g, d, static_cast<uint64_t>(tile) * kNzTile + static_cast<uint64_t>(warp) * 1024, x);
-  int b = 0;
-  while (tile < ntiles) {
-    if (threadIdx.x == 0) s_tile[b ^ 1] = atomicAdd(ticket, 1u);  // the next tile, read after barrier (1)
+  uint64_t i = blockIdx.x;
+  if (i < ntiles) nz_load(g, d, (ntiles - 1 - i) * kNzTile + static_cast<uint64_t>(warp) * 1024, x);
+  for (; i < ntiles; i += gridDim.x) {
+    const uint64_t tile = ntiles - 1 - i;
     uint32_t cnt = 0, myword = 0;
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
@@ -144,13 +222,14 @@ __global__ void __launch_bounds__(kNzBlock) nz_encode(const float* __restrict__ 
       if (lane == k) myword = bal;
       cnt += __popc(bal);
     }
-    words[b][threadIdx.x] = myword;  // word warp*32 + lane of the tile
-    if (lane == 0) wcnt[b][warp] = cnt;
-    __syncthreads();  // (1)
+    words[threadIdx.x] = myword;
+    if (lane == 0) wcnt[warp] = cnt;
+    const uint64_t tile_prefix = __ldg(&tiles[tile]);
+    __syncthreads();
     uint32_t at = 0, tile_total = 0;
 #pragma unroll
     for (int w = 0; w < kNzBlock / 32; ++w) {
-      const uint32_t c = wcnt[b][w];
+      const uint32_t c = wcnt[w];
       at += w < warp ? c : 0u;
       tile_total += c;
     }
@@ -158,36 +237,18 @@ __global__ void __launch_bounds__(kNzBlock) nz_encode(const float* __restrict__ 
     for (int k = 0; k < 32; ++k) {
       const bool nz = (x[k] & 0x7FFFFFFFu) != 0u;
       const unsigned bal = __ballot_sync(kFull, nz);
-      if (nz) vals[b][at + __popc(bal & lt)] = x[k];
+      if (nz) vals[at + __popc(bal & lt)] = x[k];
       at += __popc(bal);
     }
-    if (warp == 0) {
-      const uint64_t p = lookback_warp(tiles, tile, tile_total);
-      if (lane == 0) s_prefix[b] = p;
-    }
-    const uint32_t next = s_tile[b ^ 1];
-    if (next < ntiles) nz_load(g, d, static_cast<uint64_t>(next) * kNzTile + static_cast<uint64_t>(warp) * 1024, x);
-    __syncthreads();  // (2) vals[b] complete, prefix known
-    const uint64_t tile_prefix = s_prefix[b];
-    // bitmap bytes of the tile (the last tile stops at ceil(d/8))
-    const uint64_t b0 = static_cast<uint64_t>(tile) * (kNzTile / 8);
+    __syncthreads();
+    const uint64_t nx = i + gridDim.x;
+    if (nx < ntiles) nz_load(g, d, (ntiles - 1 - nx) * kNzTile + static_cast<uint64_t>(warp) * 1024, x);
+    const uint64_t b0 = tile * (kNzTile / 8);
     const uint64_t nb = b0 + kNzTile / 8 <= bm_bytes ? kNzTile / 8 : bm_bytes - b0;
-    block_store_bytes(bm_out + b0, words[b], nb);
-    // the container holds r values: a tile past them (nnz > r, the speculation
-    // fails and the general path rewrites every byte) must not write beyond
+    block_store_bytes(bm_out + b0, words, nb);
     const uint64_t keep = tile_prefix >= r ? 0 : (r - tile_prefix < tile_total ? r - tile_prefix : tile_total);
-    block_store_bytes(val_out + 4 * tile_prefix, vals[b], 4ull * keep);
-    if (tile == ntiles - 1 && threadIdx.x == 0) {
-      const uint64_t nnz = tile_prefix + tile_total;
-      if (nnz == r) {
-        plan->vl = 4 * r;
-        plan->n_values = r;
-        plan->n_sel = r;
-        *gate = kGateSkip;
-      }
-    }
-    tile = next;
-    b ^= 1;
+    block_store_bytes(val_out + 4 * tile_prefix, vals, 4ull * keep);
+    __syncthreads();
   }
 }
 
@@ -369,7 +430,6 @@ bool nz_fast_path_eligible(uint64_t d, uint64_t r, int index_method, int value_m
 }
 
 void kernel_attrs_dense() {
-  cudaFuncSetAttribute(nz_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, kNzSmem);
 }
 
 uint32_t* gate_word(gp_ctx* ctx) { return ctx->ws.status + 32; }
@@ -377,11 +437,13 @@ uint32_t* gate_word(gp_ctx* ctx) { return ctx->ws.status + 32; }
 void launch_nz_encode(gp_ctx* ctx, const float* g, uint64_t d, uint64_t r, uint8_t* out, cudaStream_t s) {
   Workspace& w = ctx->ws;
   const uint64_t ntiles = (d + kNzTile - 1) / kNzTile;
-  cudaMemsetAsync(gate_word(ctx), 0, sizeof(uint32_t), s);
-  reset_scan(ctx, s, ntiles + 1);
-  const uint64_t cap = static_cast<uint64_t>(ctx->sm_count) * 3;  // resident: 3 x 68 KiB of shared memory per SM
-  const int grid = static_cast<int>(ntiles < cap ? ntiles : cap);
-  GP_LAUNCH(ctx, nz_encode, grid, kNzBlock, kNzSmem, s, g, d, r, out, w.plan, w.tiles, w.ticket, gate_word(ctx), w.status);
+  reset_scan(ctx, s, ntiles);  // the ticket and the per-tile counters
+  const uint64_t ccap = static_cast<uint64_t>(ctx->sm_count) * 8;
+  const int cgrid = static_cast<int>(ntiles < ccap ? ntiles : ccap);
+  const uint64_t wcap = static_cast<uint64_t>(ctx->sm_count) * 4;  // 4 resident blocks per SM (64 registers)
+  const int wgrid = static_cast<int>(ntiles < wcap ? ntiles : wcap);
+  GP_LAUNCH(ctx, nz_count, cgrid, kNzBlock, 0, s, g, d, r, w.plan, w.tiles, w.ticket, gate_word(ctx), w.status);
+  GP_LAUNCH(ctx, nz_write, wgrid, kNzBlock, 0, s, g, d, r, out, w.tiles, w.status);
 }
 
 void launch_gate_merge(gp_ctx* ctx, cudaStream_t s) {
