@@ -232,8 +232,8 @@ void carve(Workspace& w, uint8_t* base, uint64_t D) {
   w.seg_chunk = c.take<uint64_t>(w.seg_cap + 1);
   w.fit_scratch = c.take<double>(static_cast<uint64_t>(kWideBlocks) * 3 * kFitMaxCps * kFitMaxCps);
   w.crc_cap = 2 * ((64 * D + (1 << 20)) / (64 * 256) + 64);
-  w.crc_digits = c.take<uint32_t>(13 * 256);  // 5 byte-digit shift tables + the full and small grids' lane-stride multiply tables
-  w.crc_acc = c.take<uint32_t>(64);
+  w.crc_digits = c.take<uint32_t>(13 * 256 + kCrcSmallTabWords);  // 5 byte-digit shift tables + the full and small grids' lane-stride multiply tables + crc_tail's tables
+  w.crc_acc = c.take<uint32_t>(64 + 256);  // [0] XOR accumulator, [1] block counter, [2] crc_tail ticket, [64, 320) crc_tail partials
   w.scratch = c.take<uint8_t>(2 * D);
   w.huff = c.take<HuffTable>(1);
   w.huff_res = c.take<uint64_t>(16);

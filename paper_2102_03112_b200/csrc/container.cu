@@ -218,6 +218,154 @@ __global__ void __launch_bounds__(kCrcBlock) crc_chunks(const uint8_t* __restric
   }
 }
 
+// Small and medium ranges (container payloads up to a few MB: C1, C2, C4):
+// `crc_tail` cuts the range into 64-byte chunks aligned to its END — chunk q
+// = [E - 64(q+1), E - 64q), the first one front-padded with zeros, which a
+// raw (init 0) CRC ignores — so chunk q's contribution is its raw CRC times
+// x^(512 q) and no variable shift is ever needed: lane g of a G x 256 grid
+// folds chunks g, g + T, g + 2T ... by Horner with the constant x^(512 T),
+// then lanes combine in a tree (level j: v_L ^= x^(512 2^j) v_{L + 2^j}, in
+// the warp by shuffles, across warps and then across blocks — the last
+// block by ticket — through shared memory), every constant multiply one
+// 8-lookup nibble-table product.  The CRC's init 0xFFFFFFFF is folded in by
+// XORing the range's first four bytes with 0xFF (processing 4 zero bytes
+// from register I equals processing I's bytes from register 0); the final
+// XOR-out is one inversion.  Slice-by-4 tables are shared (not per lane): a
+// chunk is 64 lookups, bank conflicts cost little at these sizes, and a
+// block stages 12.5 KiB of tables instead of 138 KiB.
+constexpr int kTailBlock = 256;
+__device__ __forceinline__ uint32_t mul_nib(const uint32_t* t, uint32_t v) {
+  uint32_t r = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r ^= t[i * 16 + ((v >> (4 * i)) & 15u)];
+  return r;
+}
+
+__global__ void __launch_bounds__(kTailBlock) crc_tail(const uint8_t* __restrict__ base, const uint64_t* off_p,
+                                                       uint64_t off_h, const uint64_t* len_a, const uint64_t* len_b,
+                                                       const uint64_t* len_c, uint64_t len_h,
+                                                       const uint32_t* __restrict__ tabs, uint32_t* partials,
+                                                       uint32_t* ticket, uint32_t* out, const CrcEpilogue ep,
+                                                       uint32_t* status) {
+  __shared__ uint32_t T[4 * 256];
+  __shared__ uint32_t K[17 * 128];  // K[j] = x^(512 * 2^j) for j < 16, K[16] = x^(512 T)
+  __shared__ uint32_t red[kTailBlock / 32];
+  __shared__ bool last;
+  if (failed(status)) return;
+  const uint64_t off = off_p ? *off_p : off_h;
+  const uint64_t len = range_len(len_a, len_b, len_c, len_h);
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(base + off), E = a0 + len;
+  const uint64_t nchunks = (len + 63) / 64;
+  const uint64_t lanes = static_cast<uint64_t>(gridDim.x) * kTailBlock;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t v = 0;
+  if (static_cast<uint64_t>(blockIdx.x) * kTailBlock < nchunks && len >= 4) {
+    for (int i = threadIdx.x; i < 4 * 256 + 17 * 128; i += kTailBlock) {
+      const uint32_t x = __ldg(tabs + i);
+      if (i < 4 * 256) T[i] = x; else K[i - 4 * 256] = x;
+    }
+    __syncthreads();
+    const uint32_t sh = 8 * static_cast<uint32_t>(E & 3);
+    // the lane's chunks from the farthest (Horner: acc = x^(512 T) acc ^ crc(chunk))
+    const uint64_t g = blockIdx.x * static_cast<uint64_t>(kTailBlock) + threadIdx.x;
+    if (g < nchunks) {
+      uint64_t q = g + ((nchunks - 1 - g) / lanes) * lanes;
+      for (;;) {
+        const uintptr_t cs = E - 64 * (q + 1);  // may precede a0 (then by < 64 bytes): zeros
+        const uintptr_t wa = cs & ~static_cast<uintptr_t>(3);
+        uint32_t W[17];
+#pragma unroll
+        for (int k = 0; k < 17; ++k) {
+          const uintptr_t at = wa + 4 * k;
+          W[k] = (at < E && at + 4 > a0) ? __ldg(reinterpret_cast<const uint32_t*>(at)) : 0u;
+        }
+        uint32_t c = 0;
+        const bool head = cs < a0 + 4;  // the chunk holds the range's first bytes
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          uint32_t w = sh ? __funnelshift_r(W[k], W[k + 1], sh) : W[k];
+          if (head) {
+            const uintptr_t p0 = cs + 4 * k;  // bytes [p0, p0 + 4) of the range
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const uintptr_t p = p0 + b;
+              if (p < a0) w &= ~(0xFFu << (8 * b));              // before the range: zero
+              else if (p < a0 + 4) w ^= 0xFFu << (8 * b);      // the init term
+            }
+          }
+          c ^= w;
+          c = T[3 * 256 + (c & 0xFFu)] ^ T[2 * 256 + ((c >> 8) & 0xFFu)] ^ T[256 + ((c >> 16) & 0xFFu)] ^ T[c >> 24];
+        }
+        v ^= c;
+        if (q < lanes) break;
+        q -= lanes;
+        v = mul_nib(K + 16 * 128, v);
+      }
+    }
+    // tree over the block's lanes: lane L absorbs lane L + 2^j (farther from the end)
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const uint32_t o = __shfl_down_sync(kFull, v, 1u << j);
+      if ((lane & ((2u << j) - 1)) == 0) v ^= mul_nib(K + j * 128, o);
+    }
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+      v = lane < kTailBlock / 32 ? red[lane] : 0u;
+#pragma unroll
+      for (int j = 5; j < 8; ++j) {
+        const uint32_t o = __shfl_down_sync(kFull, v, 1u << (j - 5));
+        if ((lane & ((2u << (j - 5)) - 1)) == 0) v ^= mul_nib(K + j * 128, o);
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = v;  // block b's value, relative to chunk 256 b
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // the last block: blocks b (chunk 256 b) combined with x^(512 * 256 * 2^j)
+  uint32_t crc = 0;
+  if (len >= 4) {
+    const uint32_t nb = gridDim.x < 1024 ? gridDim.x : 1024;
+    uint32_t x = threadIdx.x < nb ? __ldcg(partials + threadIdx.x) : 0u;
+    for (int i = threadIdx.x; i < 8 * 128; i += kTailBlock) K[i] = __ldg(tabs + 4 * 256 + 8 * 128 + i);
+    __syncthreads();  // K[0..8) now holds x^(512 * 2^(j+8))
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const uint32_t o = __shfl_down_sync(kFull, x, 1u << j);
+      if ((lane & ((2u << j) - 1)) == 0) x ^= mul_nib(K + j * 128, o);
+    }
+    if (lane == 0) red[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      x = lane < kTailBlock / 32 ? red[lane] : 0u;
+#pragma unroll
+      for (int j = 5; j < 8; ++j) {
+        const uint32_t o = __shfl_down_sync(kFull, x, 1u << (j - 5));
+        if ((lane & ((2u << (j - 5)) - 1)) == 0) x ^= mul_nib(K + j * 128, o);
+      }
+    }
+    crc = x ^ 0xFFFFFFFFu;
+  } else if (threadIdx.x == 0) {  // 0-3 bytes: bytewise (table T0 = bit-serial here)
+    uint32_t c = 0xFFFFFFFFu;
+    for (uint64_t i = 0; i < len; ++i) {
+      c ^= reinterpret_cast<const uint8_t*>(a0)[i];
+      for (int k = 0; k < 8; ++k) c = (c >> 1) ^ ((c & 1u) ? kPoly : 0u);
+    }
+    crc = len ? (c ^ 0xFFFFFFFFu) : 0u;
+  }
+  if (threadIdx.x == 0) {
+    *out = crc;
+    if (ep.mode == 1) verify_body(ep.plan, crc, status);
+    if (ep.mode == 2) finish_body(ep.out, ep.cap, ep.d_len, ep.plan, crc, status);
+    *ticket = 0;  // ready for the next range
+  }
+}
+
 // unpack (container.cpp:84-127) up to, but not including, the CRC verdict.
 //
 // `pre` is the status word of the decode work that runs before the verdict,
@@ -307,7 +455,7 @@ int crc_tables_init(gp_ctx* ctx) {
     }
     return p;
   };
-  uint32_t tab[13 * 256];
+  std::vector<uint32_t> tab(13 * 256 + kCrcSmallTabWords);
   uint32_t unit = 1u << 23;  // x^8: one byte
   for (int i = 0; i < 5; ++i) {
     uint32_t p = 1u << 31;
@@ -331,10 +479,31 @@ int crc_tables_init(gp_ctx* ctx) {
       for (int b = 0; b < 256; ++b)
         tab[(5 + 4 * g + j) * 256 + b] = b ? mult(static_cast<uint32_t>(b) << (8 * j), S) : 0u;
   }
+  // crc_tail: slice-by-4 tables T_k (k zero bytes after the byte), nibble
+  // tables of x^(512 * 2^j), j < 16, and of x^(512 T) for its full grid
+  uint32_t* st = tab.data() + 13 * 256;
+  for (int e = 0; e < 256; ++e) {
+    uint32_t c = static_cast<uint32_t>(e);
+    for (int j = 0; j < 8; ++j) c = (c >> 1) ^ ((c & 1u) ? kPoly : 0u);
+    st[e] = c;
+  }
+  for (int k = 1; k < 4; ++k)
+    for (int e = 0; e < 256; ++e) st[k * 256 + e] = (st[(k - 1) * 256 + e] >> 8) ^ st[st[(k - 1) * 256 + e] & 0xFFu];
+  auto xpow = [&](uint64_t nbytes) {  // x^(8 nbytes) from the digit tables
+    uint32_t S = 1u << 31;
+    for (int i = 0; nbytes; ++i, nbytes >>= 8)
+      if (nbytes & 0xFF) S = mult(tab[i * 256 + (nbytes & 0xFF)], S);
+    return S;
+  };
+  for (int j = 0; j < 17; ++j) {
+    const uint32_t S = xpow(j < 16 ? (64ull << j) : 64ull * kTailBlock * static_cast<uint64_t>(ctx->sm_count));
+    for (int i = 0; i < 8; ++i)
+      for (int n = 0; n < 16; ++n) st[4 * 256 + j * 128 + i * 16 + n] = n ? mult(static_cast<uint32_t>(n) << (4 * i), S) : 0u;
+  }
   cudaError_t e = cudaFuncSetAttribute(crc_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kCrcLaneTableWords * static_cast<int>(sizeof(uint32_t)));
-  if (e == cudaSuccess) e = cudaMemcpy(w.crc_digits, tab, sizeof(tab), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemset(w.crc_acc, 0, 2 * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemcpy(w.crc_digits, tab.data(), tab.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(w.crc_acc, 0, (64 + 256) * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   w.crc_ready = e == cudaSuccess;
   return e == cudaSuccess ? GP_OK : GP_CUDA;
@@ -346,6 +515,17 @@ void crc_range(gp_ctx* ctx, const uint8_t* base, const uint64_t* off_dev, uint64
                const uint64_t* lb, const uint64_t* lc, uint64_t len_host, uint64_t len_bound, uint32_t* out,
                cudaStream_t s, const CrcEpilogue& ep) {
   Workspace& w = ctx->ws;
+  static const uint64_t tail_max = getenv("GP_CRC_TAIL_MAX") ? strtoull(getenv("GP_CRC_TAIL_MAX"), nullptr, 10)
+                                                              : (8ull << 20);
+  if (len_bound <= tail_max) {  // crc_tail: one lane per 64-byte chunk (Horner rows above one grid)
+    const uint64_t nch = (len_bound + 63) / 64;
+    const uint64_t need = (nch + kTailBlock - 1) / kTailBlock;
+    const int grid = static_cast<int>(need < static_cast<uint64_t>(ctx->sm_count) ? (need ? need : 1) : ctx->sm_count);
+    // a grid below the full one never takes a second row (x^(512 T) is the full grid's)
+    GP_LAUNCH(ctx, crc_tail, grid, kTailBlock, 0, s, base, off_dev, off_host, la, lb, lc, len_host,
+              w.crc_digits + 13 * 256, w.crc_acc + 64, w.crc_acc + 2, out, ep, w.status);
+    return;
+  }
   const bool small = len_bound + 128 <= 64ull * kCrcBlock * kCrcSmallGrid;
   const int grid = small ? kCrcSmallGrid : ctx->sm_count * kCrcBlocksPerSm;
   const uint32_t* mtab = w.crc_digits + (small ? 9 : 5) * 256;

@@ -228,6 +228,7 @@ void launch_top_r64(gp_ctx* ctx, const float* grad, double* residual, uint64_t d
 void launch_crc_range(gp_ctx* ctx, const uint8_t* base, const uint64_t* off_dev, uint64_t off_host,
                       const uint64_t* la, const uint64_t* lb, const uint64_t* lc, uint64_t len_host,
                       uint64_t len_bound, uint32_t* out, cudaStream_t s);
+constexpr int kCrcSmallTabWords = 4 * 256 + 17 * 128;  // crc_tail: slice-by-4 tables, 17 nibble-table constants
 int crc_tables_init(gp_ctx* ctx);  // container.cu (gp_ctx_create)
 bool nz_fast_path_eligible(uint64_t d, uint64_t r, int index_method, int value_method);  // dense.cu
 uint32_t* gate_word(gp_ctx* ctx);

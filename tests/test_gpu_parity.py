@@ -100,7 +100,11 @@ def test_crc32c_bit_exact(codec, oracle):
     big = rng.integers(0, 256, 25_000_000 + 200, dtype=np.uint8)
     t = _dev(big)
     for off, n in [(1, 5), (3, 60), (63, 2), (17, 64), (5, 127), (13, 9_699_329), (0, 9_699_328), (7, 25_000_000),
-                   (64, 19_398_656 + 3), (33, 1_260_001)]:
+                   (64, 19_398_656 + 3), (33, 1_260_001),
+                   # crc_tail (ranges up to 8 MiB): the init-term bytes across words and chunks,
+                   # one grid row exactly, one chunk past it, several Horner rows
+                   (2, 4), (1, 3), (61, 4), (62, 67), (60, 130), (9, 148 * 256 * 64), (11, 148 * 256 * 64 + 1),
+                   (6, 7_999_999), (4, 8 << 20)]:
         assert codec.crc32c(t[off:off + n]) == oracle.crc32c(big[off:off + n].tobytes()), (off, n)
 
 
