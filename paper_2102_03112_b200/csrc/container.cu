@@ -247,11 +247,20 @@ __global__ void __launch_bounds__(kTailBlock) crc_tail(const uint8_t* __restrict
                                                        const uint32_t* __restrict__ tabs, uint32_t* partials,
                                                        uint32_t* ticket, uint32_t* out, const CrcEpilogue ep,
                                                        uint32_t* status) {
+  constexpr int kTabWords = 4 * 256 + 17 * 128;  // T | K[0..17)
   __shared__ uint32_t T[4 * 256];
   __shared__ uint32_t K[17 * 128];  // K[j] = x^(512 * 2^j) for j < 16, K[16] = x^(512 T)
   __shared__ uint32_t red[kTailBlock / 32];
   __shared__ bool last;
-  if (failed(status)) return;
+  // every global read the block needs before its data — status, range, the
+  // tables — is issued at once (one round trip instead of a chain)
+  constexpr int kPer = (kTabWords + kTailBlock - 1) / kTailBlock;
+  uint32_t tr[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int i = threadIdx.x + k * kTailBlock;
+    tr[k] = i < 4 * 256 + 17 * 128 ? __ldg(tabs + i) : 0u;
+  }
   const uint64_t off = off_p ? *off_p : off_h;
   const uint64_t len = range_len(len_a, len_b, len_c, len_h);
   const uintptr_t a0 = reinterpret_cast<uintptr_t>(base + off), E = a0 + len;
@@ -259,12 +268,16 @@ __global__ void __launch_bounds__(kTailBlock) crc_tail(const uint8_t* __restrict
   const uint64_t lanes = static_cast<uint64_t>(gridDim.x) * kTailBlock;
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t v = 0;
-  if (static_cast<uint64_t>(blockIdx.x) * kTailBlock < nchunks && len >= 4) {
-    for (int i = threadIdx.x; i < 4 * 256 + 17 * 128; i += kTailBlock) {
-      const uint32_t x = __ldg(tabs + i);
-      if (i < 4 * 256) T[i] = x; else K[i - 4 * 256] = x;
-    }
-    __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int i = threadIdx.x + k * kTailBlock;
+    if (i < 4 * 256) T[i] = tr[k];
+    else if (i < 4 * 256 + 17 * 128) K[i - 4 * 256] = tr[k];
+  }
+  // a latched error skips the work but not the ticket (block-uniform, and the
+  // ticket always returns to 0)
+  const bool skip = __syncthreads_or(failed(status));
+  if (!skip && static_cast<uint64_t>(blockIdx.x) * kTailBlock < nchunks && len >= 4) {
     const uint32_t sh = 8 * static_cast<uint32_t>(E & 3);
     // the lane's chunks from the farthest (Horner: acc = x^(512 T) acc ^ crc(chunk))
     const uint64_t g = blockIdx.x * static_cast<uint64_t>(kTailBlock) + threadIdx.x;
@@ -329,15 +342,14 @@ __global__ void __launch_bounds__(kTailBlock) crc_tail(const uint8_t* __restrict
   __threadfence();
   // the last block: blocks b (chunk 256 b) combined with x^(512 * 256 * 2^j)
   uint32_t crc = 0;
-  if (len >= 4) {
+  if (skip) {
+  } else if (len >= 4) {
     const uint32_t nb = gridDim.x < 1024 ? gridDim.x : 1024;
     uint32_t x = threadIdx.x < nb ? __ldcg(partials + threadIdx.x) : 0u;
-    for (int i = threadIdx.x; i < 8 * 128; i += kTailBlock) K[i] = __ldg(tabs + 4 * 256 + 8 * 128 + i);
-    __syncthreads();  // K[0..8) now holds x^(512 * 2^(j+8))
 #pragma unroll
-    for (int j = 0; j < 5; ++j) {
+    for (int j = 0; j < 5; ++j) {  // blocks b, b + 2^j: x^(512 * 256 * 2^j) = K[j + 8]
       const uint32_t o = __shfl_down_sync(kFull, x, 1u << j);
-      if ((lane & ((2u << j) - 1)) == 0) x ^= mul_nib(K + j * 128, o);
+      if ((lane & ((2u << j) - 1)) == 0) x ^= mul_nib(K + (j + 8) * 128, o);
     }
     if (lane == 0) red[warp] = x;
     __syncthreads();
@@ -346,7 +358,7 @@ __global__ void __launch_bounds__(kTailBlock) crc_tail(const uint8_t* __restrict
 #pragma unroll
       for (int j = 5; j < 8; ++j) {
         const uint32_t o = __shfl_down_sync(kFull, x, 1u << (j - 5));
-        if ((lane & ((2u << (j - 5)) - 1)) == 0) x ^= mul_nib(K + j * 128, o);
+        if ((lane & ((2u << (j - 5)) - 1)) == 0) x ^= mul_nib(K + (j + 8) * 128, o);
       }
     }
     crc = x ^ 0xFFFFFFFFu;
@@ -359,9 +371,11 @@ __global__ void __launch_bounds__(kTailBlock) crc_tail(const uint8_t* __restrict
     crc = len ? (c ^ 0xFFFFFFFFu) : 0u;
   }
   if (threadIdx.x == 0) {
-    *out = crc;
-    if (ep.mode == 1) verify_body(ep.plan, crc, status);
-    if (ep.mode == 2) finish_body(ep.out, ep.cap, ep.d_len, ep.plan, crc, status);
+    if (!skip) {
+      *out = crc;
+      if (ep.mode == 1) verify_body(ep.plan, crc, status);
+      if (ep.mode == 2) finish_body(ep.out, ep.cap, ep.d_len, ep.plan, crc, status);
+    }
     *ticket = 0;  // ready for the next range
   }
 }
