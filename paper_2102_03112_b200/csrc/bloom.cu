@@ -30,6 +30,7 @@ constexpr uint64_t kSmemFilterMax = 150 * 1024;
 
 __global__ void bloom_insert(const uint32_t* __restrict__ keys, uint64_t r, const Plan* plan, uint32_t* words,
                              const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const FastMod fm{plan->m, plan->minv};
   const uint32_t k = plan->k;
@@ -49,6 +50,7 @@ __global__ void bloom_insert(const uint32_t* __restrict__ keys, uint64_t r, cons
 // filter payload: m u64, k u16, seed_a u64, seed_b u64, ceil(m/8) bytes (+ Pd variant)
 __global__ void bloom_emit(const uint32_t* __restrict__ words, const Plan* plan, uint8_t* out,
                            const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   uint8_t* p = out + 49;
   const uint64_t nb = (plan->m + 7) / 8;
@@ -68,6 +70,7 @@ __global__ void bloom_emit(const uint32_t* __restrict__ words, const Plan* plan,
 
 // BloomFilter::deserialize (bloom.cpp:96-112) + pipeline.cpp:261-273 trailing checks.
 __global__ void bloom_parse(const uint8_t* __restrict__ in, Plan* plan, uint64_t m_cap, uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const uint8_t im = plan->index_method;
   if (im < GP_INDEX_BLOOM_P0 || im > GP_INDEX_BLOOM_NAIVE) return;
@@ -109,6 +112,7 @@ __global__ void bloom_parse(const uint8_t* __restrict__ in, Plan* plan, uint64_t
 // aligned filter words from the payload bytes
 __global__ void bloom_load_words(const uint8_t* __restrict__ in, const Plan* plan, uint32_t* words,
                                  const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const uint8_t im = plan->index_method;
   if (im < GP_INDEX_BLOOM_P0 || im > GP_INDEX_BLOOM_NAIVE) return;
@@ -271,6 +275,7 @@ template <bool kSmem, int kLaneKeys, int kLaneBatch>
 __global__ void __launch_bounds__(kScanBlock) bloom_members(const uint32_t* __restrict__ gwords, Plan* plan,
                                                             uint32_t* __restrict__ bitmap,
                                                             const uint32_t* status) {
+  gp_pdl_wait();
   using S = ScanShape<kSmem, kLaneKeys, kLaneBatch>;
   extern __shared__ __align__(16) uint8_t dyn[];
   if (failed(status)) return;
@@ -298,6 +303,7 @@ __global__ void __launch_bounds__(kScanBlock) members_compact(const uint32_t* __
                                                               uint32_t* __restrict__ pos_out, uint64_t cap,
                                                               uint64_t* tiles, uint32_t* ticket,
                                                               const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint64_t sh[36];
   __shared__ uint32_t slot;
   if (failed(status)) return;
@@ -351,6 +357,7 @@ __device__ __forceinline__ void after_scan_body(Plan* plan, uint64_t n, uint64_t
 __global__ void __launch_bounds__(kScanBlock) members_compact_coop(const uint32_t* __restrict__ bitmap, Plan* plan,
                                                                    uint32_t* __restrict__ pos_out, uint64_t cap,
                                                                    uint64_t* tcnt, int decoding, uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint64_t sh[36];
   cg::grid_group grid = cg::this_grid();
   if (failed(status)) return;  // uniform: nothing latches this word while the kernel runs
@@ -422,6 +429,7 @@ __device__ __forceinline__ void after_scan_body(Plan* plan, uint64_t n, uint64_t
 }
 
 __global__ void bloom_after_scan(Plan* plan, uint64_t cap, int decoding, uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const uint8_t im = plan->index_method;
   if (im < GP_INDEX_BLOOM_P0 || im > GP_INDEX_BLOOM_NAIVE) return;
@@ -431,6 +439,7 @@ __global__ void bloom_after_scan(Plan* plan, uint64_t cap, int decoding, uint32_
 // sel <- P (P0, naive) or the Pd slice (bloom.cpp:224-236)
 __global__ void select_slice(const uint32_t* __restrict__ P, const Plan* plan, uint32_t* sel,
                              const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const uint8_t im = plan->index_method;
   uint64_t begin = 0, count = 0;

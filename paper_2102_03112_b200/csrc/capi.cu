@@ -46,6 +46,8 @@ void stage_end(gp_ctx* ctx, cudaStream_t s) {
   p.open_stage = -1;
 }
 
+bool g_pdl = !getenv("GP_PDL") || atoi(getenv("GP_PDL")) != 0;
+
 void reset_scan(gp_ctx* ctx, cudaStream_t s, uint64_t ntiles_bound) {
   Workspace& w = ctx->ws;
   const uint64_t n = ntiles_bound < w.tiles_cap ? ntiles_bound : w.tiles_cap;
@@ -80,6 +82,7 @@ struct PlanInit {
 };
 
 __global__ void init_plan(Plan* plan, PlanInit p) {
+  gp_pdl_wait();
   plan->d = p.d;
   plan->r = p.r;
   plan->index_method = p.index_method;
@@ -117,6 +120,7 @@ __global__ void init_plan(Plan* plan, PlanInit p) {
 // seed_out[b] = hash64(b, that seed) (the bucketed convention of dp.py).
 __global__ void pipeline_seed_kernel(uint64_t* seed_out, const uint64_t* step, uint64_t seed, uint32_t worker,
                                      uint32_t buckets) {
+  gp_pdl_wait();
   const uint64_t key = (static_cast<uint64_t>(worker) << 32) | (*step & 0xFFFFFFFFULL);
   const uint64_t ps = hash64(0xC0DEC, hash64(key, hash64(0xDA7A, seed)));
   if (buckets == 0) {
@@ -129,6 +133,7 @@ __global__ void pipeline_seed_kernel(uint64_t* seed_out, const uint64_t* step, u
 // compress_gradient's validate(sg) (gradient.cpp:19-30) + gather(dense, support)
 __global__ void take_support(const float* __restrict__ dense, const uint32_t* __restrict__ support, uint64_t r,
                              uint64_t d, uint32_t* ws_support, float* ws_values, uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < r;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -144,6 +149,7 @@ __global__ void take_support(const float* __restrict__ dense, const uint32_t* __
 
 // component calls: the filter payload starts at offset 0 of the caller's buffer
 __global__ void component_offsets(Plan* plan) {
+  gp_pdl_wait();
   plan->off_index = 0;
   plan->off_value = plan->il;
   plan->off_reorder = plan->il;
@@ -152,6 +158,7 @@ __global__ void component_offsets(Plan* plan) {
 // P (ascending positives) to the caller, |P| to *count; GP_CAPACITY past cap
 __global__ void copy_positions(const uint32_t* __restrict__ pos, const Plan* plan, uint32_t* __restrict__ out,
                                uint64_t cap, uint64_t* count, uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const uint64_t n = plan->n_pos;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -873,6 +880,7 @@ int gp_bloom_positive_scan(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter
 }
 
 __global__ void set_scan_range(Plan* plan, uint64_t lo, uint64_t hi) {
+  gp_pdl_wait();
   plan->scan_lo = lo;
   plan->scan_hi = hi;
 }
@@ -880,6 +888,7 @@ __global__ void set_scan_range(Plan* plan, uint64_t lo, uint64_t hi) {
 // caller positives -> ws.pos, |P| from a device word (the sharded decode)
 __global__ void take_positions(const uint32_t* __restrict__ src, const uint64_t* __restrict__ count, Plan* plan,
                                uint32_t* __restrict__ pos, uint64_t cap, uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const uint64_t n = *count;
   if (n > cap) {

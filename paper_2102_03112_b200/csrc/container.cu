@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(kCrcBlock) crc_chunks(const uint8_t* __restric
                                                         const uint32_t* __restrict__ mtab, uint32_t* acc,
                                                         uint32_t* done, uint32_t* out, const CrcEpilogue ep,
                                                         uint32_t* status) {
+  gp_pdl_wait();
   extern __shared__ uint32_t TL[];  // [4][256][32] per-lane slice-by-4 tables
   __shared__ uint32_t T0[256];
   __shared__ uint32_t D[5][256];
@@ -247,6 +248,7 @@ __global__ void __launch_bounds__(kTailBlock) crc_tail(const uint8_t* __restrict
                                                        const uint32_t* __restrict__ tabs, uint32_t* partials,
                                                        uint32_t* ticket, uint32_t* out, const CrcEpilogue ep,
                                                        uint32_t* status) {
+  gp_pdl_wait();
   constexpr int kTabWords = 4 * 256 + 17 * 128;  // T | K[0..17)
   __shared__ uint32_t T[4 * 256];
   __shared__ uint32_t K[17 * 128];  // K[j] = x^(512 * 2^j) for j < 16, K[16] = x^(512 T)
@@ -391,6 +393,7 @@ __global__ void __launch_bounds__(kTailBlock) crc_tail(const uint8_t* __restrict
 __global__ void parse_container(const uint8_t* __restrict__ in, uint64_t len_host, const uint64_t* len_dev,
                                 uint64_t max_d, Plan* plan, const gp_pipeline_config hint, int use_hint,
                                 uint32_t* status, uint32_t* pre) {
+  gp_pdl_wait();
   *pre = *status;
   if (failed(status)) return;
   auto fail = [&](uint32_t code) {
@@ -445,6 +448,7 @@ __global__ void parse_container(const uint8_t* __restrict__ in, uint64_t len_hos
 // everything before it passed (the reference's order: header, CRC, post-CRC
 // checks, then the method decoders in stream order).
 __global__ void merge_status(uint32_t* status, const uint32_t* pre) {
+  gp_pdl_wait();
   if (!failed(status) && *pre) latch(status, *pre);
 }
 

@@ -243,6 +243,7 @@ __device__ void chunk_code(const uint8_t* __restrict__ raw, uint64_t L, uint64_t
 // pass 1: per-chunk output sizes (sizes[c]) and Adler-32 partials
 __global__ void __launch_bounds__(kThreads) deflate_size(const float* __restrict__ v32, const Plan* plan,
                                                          uint64_t* sizes, uint64_t* adler, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ ChunkCode cc;
   __shared__ PmScratch pm;
   __shared__ uint64_t red[2][kThreads / 32];
@@ -285,6 +286,7 @@ __global__ void __launch_bounds__(kThreads) deflate_size(const float* __restrict
 // pass 2: every chunk's bytes at its offset (offs = exclusive scan of sizes)
 __global__ void __launch_bounds__(kThreads) deflate_emit(const float* __restrict__ v32, const Plan* plan,
                                                          const uint64_t* offs, uint8_t* out, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ ChunkCode cc;
   __shared__ uint32_t buf[kBufWords];
   __shared__ uint64_t sh[40];
@@ -362,6 +364,7 @@ __global__ void __launch_bounds__(kThreads) deflate_emit(const float* __restrict
 // framing, zlib header, the empty stream's block, Adler-32, vl
 __global__ void deflate_finish(Plan* plan, uint8_t* out, const uint64_t* offs, const uint64_t* sizes,
                                const uint64_t* adler, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || plan->value_method != GP_VALUE_DEFLATE_SLOT || threadIdx.x != 0) return;
   const uint64_t L = 4 * plan->n_values;
   const uint64_t nch = (L + kChunk - 1) / kChunk;
@@ -399,6 +402,7 @@ __global__ void deflate_finish(Plan* plan, uint8_t* out, const uint64_t* offs, c
 
 // f64 value sequences: their f32 bytes first (pipeline.cpp:77-80 put_f32)
 __global__ void deflate_raw32(const double* __restrict__ v64, const Plan* plan, float* raw, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || plan->value_method != GP_VALUE_DEFLATE_SLOT) return;
   const uint64_t n = plan->n_values;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;

@@ -118,6 +118,7 @@ __device__ __forceinline__ void nz_load(const float* __restrict__ g, uint64_t d,
 __global__ void __launch_bounds__(kNzBlock) nz_count(const float* __restrict__ g, uint64_t d, uint64_t r, Plan* plan,
                                                      uint64_t* tiles, uint32_t* ticket, uint32_t* gate,
                                                      const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint64_t scratch[33];
   __shared__ bool s_last;
   if (failed(status)) {
@@ -200,6 +201,7 @@ __global__ void __launch_bounds__(kNzBlock) nz_count(const float* __restrict__ g
 
 __global__ void __launch_bounds__(kNzBlock, 4) nz_write(const float* __restrict__ g, uint64_t d, uint64_t r,
                                                      uint8_t* out, const uint64_t* tiles, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint32_t vals[kNzTile + 8];
   __shared__ uint32_t words[kNzBlock + 8];
   __shared__ uint32_t wcnt[kNzBlock / 32];
@@ -253,6 +255,7 @@ __global__ void __launch_bounds__(kNzBlock, 4) nz_write(const float* __restrict_
 }
 
 __global__ void gate_merge(const uint32_t* gate, uint32_t* status) {
+  gp_pdl_wait();
   const uint32_t gv = *gate;
   if (gv != 0u && gv != kGateSkip) latch(status, gv);
 }
@@ -263,6 +266,7 @@ constexpr int kBmTileBytes = kNzTile / 8;  // 1 KiB of bitmap = 8192 coordinates
 // per-tile popcounts of the bitmap payload (tiles[t], u64)
 __global__ void bm_counts(const uint8_t* __restrict__ in, const Plan* plan, uint64_t* counts,
                           const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || plan->index_method != GP_INDEX_BITMAP) return;
   const uint64_t nbytes = plan->il;
   const uint8_t* p = in + plan->off_index;
@@ -289,6 +293,7 @@ __global__ void bm_counts(const uint8_t* __restrict__ in, const Plan* plan, uint
 
 // after the scan: total popcount, the decode's support size, the r check
 __global__ void bm_total(Plan* plan, const uint64_t* counts_excl, const uint64_t* counts, uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || plan->index_method != GP_INDEX_BITMAP) return;
   const uint64_t ntiles = (plan->il + kBmTileBytes - 1) / kBmTileBytes;
   const uint64_t n = ntiles ? counts_excl[ntiles - 1] + counts[ntiles - 1] : 0;
@@ -304,6 +309,7 @@ __global__ void bm_total(Plan* plan, const uint64_t* counts_excl, const uint64_t
 __global__ void __launch_bounds__(kNzBlock) bm_scatter(const uint8_t* __restrict__ in, const Plan* plan,
                                                        const uint64_t* offs, float* dense, uint64_t dense_d,
                                                        float scale, int overwrite, uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint32_t vals[kNzTile + 8];
   __shared__ uint32_t words[kNzBlock + 8];
   __shared__ uint32_t woff[kNzBlock / 32];
@@ -407,6 +413,7 @@ __global__ void __launch_bounds__(kNzBlock) bm_scatter(const uint8_t* __restrict
 // overwrite mode on the general scatter path: zero the dense buffer first
 // (skipped when the fused bitmap scatter writes every coordinate itself)
 __global__ void dense_zero(float* dense, uint64_t n, const Plan* plan, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || plan->fused_bitmap) return;
   float4* d4 = reinterpret_cast<float4*>(dense);
   const uint64_t n4 = (reinterpret_cast<uintptr_t>(dense) & 15) ? 0 : n / 4;

@@ -16,6 +16,12 @@
 
 #include "../../include/gradpack_b200.h"
 
+#ifdef __CUDACC__
+// first statement of every kernel: wait for the grid this launch depends on
+// (a no-op without programmatic dependent launch)
+__device__ __forceinline__ void gp_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#endif
+
 namespace gp {
 
 // Device-resident step descriptor, rewritten by each encode/decode call.
@@ -182,10 +188,31 @@ struct gp_ctx {
 namespace gp {
 
 // Every kernel launch goes through this macro so gp_ctx_launch_count() can
-// report how many native kernels a step enqueued.
+// report how many native kernels a step enqueued.  Launches carry the
+// programmatic-stream-serialization attribute (programmatic dependent launch,
+// also inside captured graphs): a kernel's launch and block scheduling
+// overlap the end of the kernel before it on the stream, and every kernel
+// begins with gp_pdl_wait() (griddepcontrol.wait: the preceding grid has
+// completed and its memory is visible) before it reads anything.  GP_PDL=0
+// launches without the attribute.
+extern bool g_pdl;
+template <typename... P, typename... A>
+inline void launch_k(void (*k)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... a) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, static_cast<A&&>(a)...);
+}
 #define GP_LAUNCH(ctx, kernel, grid, block, smem, stream, ...)                         \
   do {                                                                                \
-    kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                       \
+    ::gp::launch_k(kernel, (grid), (block), (smem), (stream), __VA_ARGS__);           \
     ++(ctx)->launches;                                                                \
   } while (0)
 

@@ -38,6 +38,7 @@ struct ChunkState {
 __device__ __forceinline__ bool huff_active(const Plan* plan) { return plan->index_method == GP_INDEX_HUFFMAN; }
 
 __global__ void huff_table(const Plan* plan, HuffTable* t, uint32_t* status) {
+  gp_pdl_wait();
   __shared__ HuffScratch x;
   if (failed(status) || !huff_active(plan)) return;
   if (t->d == plan->d && t->nsym && !t->error) return;  // built for this d already (the table is a function of d)
@@ -48,6 +49,7 @@ __global__ void huff_table(const Plan* plan, HuffTable* t, uint32_t* status) {
 __global__ void __launch_bounds__(kHBlock) huff_encode(const uint32_t* __restrict__ support, Plan* plan,
                                                        const HuffTable* __restrict__ gt, uint8_t* out,
                                                        uint64_t* tiles, uint32_t* ticket, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint64_t rcode[256];  // codes bit-reversed: emission order LSB-first
   __shared__ uint8_t len[256];
   __shared__ uint64_t sh[36];
@@ -217,6 +219,7 @@ __device__ __forceinline__ uint64_t nchunks_of(const Plan* plan) { return (8 * p
 
 __global__ void huff_spec(const uint8_t* __restrict__ in, const Plan* plan, const HuffTable* __restrict__ gt,
                           ChunkState* cs, uint64_t cap, uint32_t* status) {
+  gp_pdl_wait();
   __shared__ HuffSmem t;
   if (failed(status) || !huff_active(plan)) return;
   const uint64_t nch = nchunks_of(plan);
@@ -243,6 +246,7 @@ __global__ void huff_spec(const uint8_t* __restrict__ in, const Plan* plan, cons
 __global__ void huff_fix(const uint8_t* __restrict__ in, const Plan* plan, const HuffTable* __restrict__ gt,
                          const ChunkState* __restrict__ a, ChunkState* b, uint32_t* changed, int k,
                          uint32_t* status) {
+  gp_pdl_wait();
   __shared__ HuffSmem t;
   if (failed(status) || !huff_active(plan)) return;
   const uint64_t nch = nchunks_of(plan);
@@ -269,6 +273,7 @@ __global__ void huff_fix(const uint8_t* __restrict__ in, const Plan* plan, const
 // chunk that stopped on an error (by induction from chunk 0 its start is a
 // true codeword boundary, so that error is genuine and ends the stream).
 __global__ void huff_check(const Plan* plan, const ChunkState* __restrict__ cs, uint32_t* flag, uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || !huff_active(plan)) return;
   const uint64_t nch = nchunks_of(plan);
   for (uint64_t c = 1 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; c < nch;
@@ -282,6 +287,7 @@ __global__ void __launch_bounds__(kHBlock) huff_emit(const uint8_t* __restrict__
                                                      const HuffTable* __restrict__ gt, const ChunkState* cs,
                                                      uint8_t* sym, uint64_t* res, uint64_t* tiles, uint32_t* ticket,
                                                      const uint32_t* flag, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint64_t sh[36];
   __shared__ uint32_t slot;
   __shared__ HuffSmem t;
@@ -313,6 +319,7 @@ __global__ void __launch_bounds__(kHBlock) huff_emit(const uint8_t* __restrict__
 // the sequential decoder, for streams whose chunks did not settle
 __global__ void huff_serial(const uint8_t* __restrict__ in, const Plan* plan, const HuffTable* __restrict__ gt,
                             uint8_t* sym, uint64_t* res, const uint32_t* flag, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ HuffSmem t;
   if (failed(status) || !huff_active(plan) || !*flag) return;
   load_smem_table(gt, t);
@@ -324,6 +331,7 @@ __global__ void huff_serial(const uint8_t* __restrict__ in, const Plan* plan, co
 
 // decode(): first error, exhausted stream, trailing garbage (codecs.cpp:196-205)
 __global__ void huff_verdict(Plan* plan, const uint64_t* res, uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || !huff_active(plan)) return;
   const uint64_t need = 4 * plan->r;
   if (res[0] != ~0ull) return latch(status, static_cast<uint32_t>(res[0] & 15));
@@ -334,6 +342,7 @@ __global__ void huff_verdict(Plan* plan, const uint64_t* res, uint32_t* status) 
 // decode_indices range check (codecs.cpp:232-241); the keys are already the
 // LE words of the decoded bytes
 __global__ void huff_keys(Plan* plan, const uint32_t* __restrict__ sel, uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || !huff_active(plan)) return;
   const uint64_t r = plan->r, d = plan->d;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < r;
@@ -346,6 +355,7 @@ __global__ void huff_keys(Plan* plan, const uint32_t* __restrict__ sel, uint32_t
 }
 
 __global__ void huff_reset(uint64_t* res, uint32_t* flag, uint32_t* changed) {
+  gp_pdl_wait();
   res[0] = ~0ull;
   res[1] = 0;
   res[2] = 0;

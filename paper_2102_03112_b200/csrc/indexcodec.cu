@@ -16,6 +16,7 @@ constexpr int kTile = kTileBlock * kTileItems;
 
 __global__ void index_none_encode(const uint32_t* __restrict__ support, uint64_t r, uint8_t* out,
                                   const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   uint8_t* p = out + 49;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < r;
@@ -27,6 +28,7 @@ __global__ void index_none_encode(const uint32_t* __restrict__ support, uint64_t
 // distinct word per warp (consecutive keys usually share a word).
 __global__ void bitmap_scatter(const uint32_t* __restrict__ support, uint64_t r, uint32_t* words,
                                const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i - threadIdx.x % 32 < r;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -42,6 +44,7 @@ __global__ void bitmap_scatter(const uint32_t* __restrict__ support, uint64_t r,
 
 // copy ceil(d/8) bitmap bytes to the (unaligned) payload position
 __global__ void bitmap_emit(const uint32_t* __restrict__ words, uint64_t d, uint8_t* out, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const uint64_t nbytes = (d + 7) / 8;
   uint8_t* p = out + 49;
@@ -53,6 +56,7 @@ __global__ void bitmap_emit(const uint32_t* __restrict__ words, uint64_t d, uint
 
 // ------------------------------------------------------------ decode
 __global__ void index_none_decode(const uint8_t* __restrict__ in, Plan* plan, uint32_t* sel, uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || plan->index_method != GP_INDEX_NONE) return;
   const uint64_t r = plan->r;
   if (plan->il != 4 * r) {
@@ -71,6 +75,7 @@ __global__ void index_none_decode(const uint8_t* __restrict__ in, Plan* plan, ui
 
 // validate strictly increasing & < d (pipeline.cpp:299-305) — after the values
 __global__ void support_validate(const Plan* plan, const uint32_t* __restrict__ sel, uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || (plan->index_method != GP_INDEX_NONE && plan->index_method != GP_INDEX_HUFFMAN)) return;
   const uint64_t n = plan->n_sel, d = plan->d;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -81,6 +86,7 @@ __global__ void support_validate(const Plan* plan, const uint32_t* __restrict__ 
 
 // bitmap_from_bytes checks (gradient.cpp:88-97)
 __global__ void bitmap_check(const uint8_t* __restrict__ in, Plan* plan, uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || plan->index_method != GP_INDEX_BITMAP) return;
   const uint64_t d = plan->d;
   if (plan->il != (d + 7) / 8) return latch(status, GP_CORRUPT_PAYLOAD);
@@ -96,6 +102,7 @@ __global__ void bitmap_check(const uint8_t* __restrict__ in, Plan* plan, uint32_
 __global__ void __launch_bounds__(kTileBlock) bitmap_support(const uint8_t* __restrict__ in, Plan* plan,
                                                              uint32_t* sel, uint64_t* tiles, uint32_t* ticket,
                                                              uint64_t cap, uint32_t* status) {
+  gp_pdl_wait();
   constexpr int kRounds = kTileItems / 4;
   __shared__ uint64_t sh[36];
   __shared__ uint32_t slot;
@@ -167,6 +174,7 @@ __global__ void __launch_bounds__(kTileBlock) bitmap_support(const uint8_t* __re
 }
 
 __global__ void bitmap_popcount_check(Plan* plan, uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || plan->index_method != GP_INDEX_BITMAP) return;
   if (plan->il == 0) {
     plan->n_sel = 0;
@@ -216,6 +224,7 @@ void launch_decode_index_bitmap(gp_ctx* ctx, const uint8_t* in, uint64_t d_bound
 // container is the encoder's top-r support
 namespace {
 __global__ void own_support(Plan* plan, const uint32_t* __restrict__ support, uint32_t* sel, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const uint64_t r = plan->r;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < r;

@@ -175,6 +175,7 @@ struct Out {
 
 __global__ void slot_inflate(const uint8_t* __restrict__ in, const Plan* plan, uint8_t* __restrict__ out,
                              uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   if (plan->value_method != GP_VALUE_DEFLATE_SLOT || plan->slot_id != 1) return;
   __shared__ uint8_t lens[320];
@@ -301,6 +302,7 @@ __global__ void slot_inflate(const uint8_t* __restrict__ in, const Plan* plan, u
 // inflated little-endian f32 bytes -> the f64 value array decode_scatter reads
 __global__ void slot_widen(const uint8_t* __restrict__ raw, const Plan* plan, double* __restrict__ values,
                            const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   if (plan->value_method != GP_VALUE_DEFLATE_SLOT || plan->slot_id != 1) return;
   const uint64_t n = plan->n_values;

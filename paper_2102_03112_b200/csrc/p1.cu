@@ -26,6 +26,7 @@ __device__ __forceinline__ bool p1_active(const Plan* plan) { return plan->index
 
 __global__ void p1_draws(Plan* plan, uint32_t* __restrict__ jkey, uint32_t* __restrict__ step, uint32_t* reject,
                          const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || !p1_active(plan)) return;
   const uint64_t n = plan->n_pos, r = plan->r;
   const uint64_t seed = hash64(plan->seed_a, plan->seed_b);  // derive_selection_seed (pipeline.cpp:23-25)
@@ -42,6 +43,7 @@ __global__ void p1_draws(Plan* plan, uint32_t* __restrict__ jkey, uint32_t* __re
 // exact fallback: sequential stream with rejections (taken with probability ~r*n/2^64)
 __global__ void p1_draws_serial(Plan* plan, uint32_t* __restrict__ jkey, const uint32_t* reject,
                                 const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || !p1_active(plan) || !*reject || threadIdx.x != 0) return;
   const uint64_t n = plan->n_pos, r = plan->r;
   const uint64_t seed = hash64(plan->seed_a, plan->seed_b);
@@ -54,11 +56,13 @@ __global__ void p1_draws_serial(Plan* plan, uint32_t* __restrict__ jkey, const u
   }
 }
 
-__global__ void p1_reset(uint32_t* reject) { *reject = 0; }
+__global__ void p1_reset(uint32_t* reject) {
+  gp_pdl_wait(); *reject = 0; }
 
 // end (inclusive) of each target's group in the sorted pairs
 __global__ void p1_groups(const Plan* plan, const uint32_t* __restrict__ skey, uint32_t* __restrict__ gend,
                           const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || !p1_active(plan)) return;
   const uint64_t r = plan->r;
   for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < r;
@@ -82,6 +86,7 @@ __device__ __forceinline__ uint32_t latest_before(const uint32_t* skey, const ui
 __global__ void p1_resolve(const Plan* plan, const uint32_t* __restrict__ jkey, const uint32_t* __restrict__ skey,
                            const uint32_t* __restrict__ sstep, const uint32_t* __restrict__ gend,
                            uint8_t* __restrict__ flags, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || !p1_active(plan)) return;
   const uint64_t r = plan->r;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < r;
@@ -99,6 +104,7 @@ __global__ void p1_resolve(const Plan* plan, const uint32_t* __restrict__ jkey, 
 
 __global__ void p1_bits(const Plan* plan, const uint8_t* __restrict__ flags, uint32_t* __restrict__ selbits,
                         const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || !p1_active(plan)) return;
   const uint64_t n = plan->n_pos;
   const uint64_t nw = (n + 31) / 32;

@@ -52,6 +52,7 @@ __device__ __forceinline__ bool p2_active(const Plan* plan) {
 // the stage-A flags over P and the bucket-space cursor
 __global__ void p2_zero_counts(Plan* plan, uint32_t* count, uint64_t m_cap, uint8_t* flags, uint64_t n_cap,
                                uint32_t* alloc, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || !p2_active(plan)) return;
   const uint64_t n = (plan->m < m_cap ? plan->m : m_cap) + 1;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -127,6 +128,7 @@ __global__ void __launch_bounds__(256) p2_pairs(const uint32_t* __restrict__ P, 
                                                 uint32_t* __restrict__ pairs, uint32_t* __restrict__ rank,
                                                 uint32_t* __restrict__ count, uint64_t pair_cap, uint64_t set_cap,
                                                 uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || !p2_active(plan)) return;
   const uint64_t n = plan->n_pos, m = plan->m;
   const uint32_t k = plan->k;
@@ -150,6 +152,7 @@ __global__ void __launch_bounds__(256) p2_pairs(const uint32_t* __restrict__ P, 
 __global__ void __launch_bounds__(kTileBlock) p2_tiles(const uint32_t* __restrict__ count, Plan* plan,
                                                        uint32_t* __restrict__ slot, uint32_t* __restrict__ table,
                                                        uint32_t* alloc, uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint32_t h[256];
   __shared__ uint32_t sh32[33];
   __shared__ uint32_t s_base;
@@ -209,6 +212,7 @@ __global__ void __launch_bounds__(kTileBlock) p2_tiles(const uint32_t* __restric
 __global__ void p2_scatter(const uint32_t* __restrict__ pairs, const uint32_t* __restrict__ rank, const Plan* plan,
                            const uint32_t* __restrict__ slot, uint32_t* __restrict__ members,
                            uint8_t* __restrict__ flags, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || !p2_active(plan)) return;
   const uint64_t n = plan->n_pos;
   const uint32_t k = plan->k;
@@ -252,6 +256,7 @@ __global__ void __launch_bounds__(kTileBlock) p2_size_scatter(Plan* plan, const 
                                                               uint32_t* __restrict__ sets,
                                                               const uint8_t* __restrict__ flags,
                                                               uint32_t* __restrict__ selbits, const uint32_t* status) {
+  gp_pdl_wait();
   constexpr int kW = kTileBlock / 32;
   __shared__ uint32_t wcnt[kW][256];
   __shared__ uint32_t bsum;
@@ -574,6 +579,7 @@ __global__ void __launch_bounds__(1024) p2_engine_dispatch(Plan* plan, uint32_t*
                                                            const uint32_t* __restrict__ members,
                                                            uint64_t* ka, uint64_t* kb, uint32_t* selbits,
                                                            uint32_t* first_touch, bool alone, uint32_t* status) {
+  gp_pdl_wait();
   const uint64_t n = plan->n_pos;
   if (!alone && ft_fits(n) != kFt) return;  // alone: the other kernel was not launched
   if (kFt)
@@ -593,6 +599,7 @@ __global__ void __launch_bounds__(kTileBlock) flags_compact(const uint32_t* __re
                                                             const uint32_t* __restrict__ selbits, Plan* plan,
                                                             int method, uint32_t* __restrict__ sel, uint64_t* tcnt,
                                                             uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint64_t sh[36];
   cg::grid_group grid = cg::this_grid();
   if (failed(status) || plan->index_method != method) return;  // uniform over the grid

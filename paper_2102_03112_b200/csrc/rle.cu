@@ -66,6 +66,7 @@ __device__ __forceinline__ uint32_t start_ballot(const uint32_t* __restrict__ su
 // per-tile counts + one scan (scan_chunk_counts) place them.
 __global__ void __launch_bounds__(kBlock) rle_starts_count(const uint32_t* __restrict__ sup, uint64_t r,
                                                            uint64_t* counts, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint32_t wc[kBlock / 32];
   if (failed(status)) return;
   const uint64_t ntiles = (r + kTile - 1) / kTile;
@@ -90,6 +91,7 @@ __global__ void __launch_bounds__(kBlock) rle_starts_count(const uint32_t* __res
 __global__ void __launch_bounds__(kBlock) rle_starts(const uint32_t* __restrict__ sup, uint64_t r,
                                                      uint32_t* __restrict__ starts, Plan* plan,
                                                      const uint64_t* tile_offs, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint64_t sh[36];
   if (failed(status)) return;
   const uint64_t ntiles = (r + kTile - 1) / kTile;
@@ -121,6 +123,7 @@ __global__ void __launch_bounds__(kBlock) rle_sizes(const uint32_t* __restrict__
                                                     const uint32_t* __restrict__ starts, Plan* plan,
                                                     uint32_t* __restrict__ goff, uint64_t* tiles, uint32_t* ticket,
                                                     const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint64_t sh[36];
   __shared__ uint32_t slot;
   if (failed(status)) return;
@@ -168,6 +171,7 @@ __global__ void __launch_bounds__(kBlock) rle_sizes(const uint32_t* __restrict__
 __global__ void rle_groups(const uint32_t* __restrict__ sup, uint64_t r, uint64_t d,
                            const uint32_t* __restrict__ starts, const uint32_t* __restrict__ goff, const Plan* plan,
                            uint8_t* __restrict__ grp, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const uint64_t R = plan->n_runs;
   if (blockIdx.x == 0 && threadIdx.x == 0 && sup[0] > 0) put_varint(grp, sup[0]);
@@ -184,6 +188,7 @@ __global__ void rle_groups(const uint32_t* __restrict__ sup, uint64_t r, uint64_
 
 __global__ void rle_emit(const uint8_t* __restrict__ grp, const uint32_t* __restrict__ sup, const Plan* plan,
                          uint8_t* out, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const uint64_t G = plan->n_groups;
   const uint8_t pol = sup[0] == 0 ? 1 : 0;
@@ -205,6 +210,7 @@ __device__ __forceinline__ uint32_t group_at(const uint8_t* p, uint64_t t) {
 __global__ void __launch_bounds__(kBlock) rle_ends(const uint8_t* __restrict__ in, Plan* plan,
                                                    uint32_t* __restrict__ ends, uint64_t* tiles, uint32_t* ticket,
                                                    const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint64_t sh[36];
   __shared__ uint32_t slot;
   if (failed(status) || plan->index_method != GP_INDEX_RLE) return;
@@ -243,6 +249,7 @@ __global__ void __launch_bounds__(kBlock) rle_ends(const uint8_t* __restrict__ i
 // run length of varint v (a varint longer than 10 groups is flagged in rle_events)
 __global__ void rle_values(const uint8_t* __restrict__ in, const Plan* plan, const uint32_t* __restrict__ ends,
                            uint64_t* __restrict__ runs, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || plan->index_method != GP_INDEX_RLE) return;
   const uint8_t* p = in + plan->off_index;
   const uint64_t V = plan->n_runs;
@@ -261,6 +268,7 @@ __global__ void rle_values(const uint8_t* __restrict__ in, const Plan* plan, con
 __global__ void __launch_bounds__(kBlock) rle_scan(const Plan* plan, const uint64_t* __restrict__ runs,
                                                    uint64_t* __restrict__ cum, uint64_t* tiles, uint32_t* ticket,
                                                    const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint64_t sh[36];
   __shared__ uint32_t slot;
   if (failed(status) || plan->index_method != GP_INDEX_RLE) return;
@@ -298,6 +306,7 @@ __global__ void __launch_bounds__(kBlock) rle_scan(const Plan* plan, const uint6
 __global__ void rle_events(const uint8_t* __restrict__ in, const Plan* plan, const uint32_t* __restrict__ ends,
                            const uint64_t* __restrict__ runs, const uint64_t* __restrict__ cum,
                            unsigned long long* first, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || plan->index_method != GP_INDEX_RLE) return;
   const uint64_t V = plan->n_runs, d = plan->d;
   for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < V;
@@ -317,6 +326,7 @@ __global__ void rle_events(const uint8_t* __restrict__ in, const Plan* plan, con
 // decide: error class, or the number of runs and the slack check
 __global__ void rle_finish(const uint8_t* __restrict__ in, Plan* plan, const uint32_t* __restrict__ ends,
                            const unsigned long long* first, uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || plan->index_method != GP_INDEX_RLE) return;
   const uint8_t* p = in + plan->off_index;
   const uint64_t n = plan->il, V = plan->n_runs;
@@ -339,6 +349,7 @@ __global__ void rle_finish(const uint8_t* __restrict__ in, Plan* plan, const uin
 
 __global__ void rle_toggles(const Plan* plan, const uint64_t* __restrict__ cum, uint32_t* __restrict__ tog,
                             const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || plan->index_method != GP_INDEX_RLE) return;
   const uint64_t V = plan->n_runs, d = plan->d;
   for (uint64_t v = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; v < V;
@@ -351,6 +362,7 @@ __global__ void rle_toggles(const Plan* plan, const uint64_t* __restrict__ cum, 
 // bitmap = polarity XOR prefix-XOR(toggles); word parity carried by a scan
 __global__ void __launch_bounds__(kBlock) rle_bitmap(const Plan* plan, uint32_t* __restrict__ words, uint64_t* tiles,
                                                      uint32_t* ticket, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint64_t sh[36];
   __shared__ uint32_t slot;
   if (failed(status) || plan->index_method != GP_INDEX_RLE) return;
@@ -405,6 +417,7 @@ __global__ void __launch_bounds__(kBlock) rle_bitmap(const Plan* plan, uint32_t*
 __global__ void __launch_bounds__(kBlock) rle_support(const uint32_t* __restrict__ words, Plan* plan,
                                                       uint32_t* __restrict__ sel, uint64_t cap, uint64_t* tiles,
                                                       uint32_t* ticket, const uint32_t* status) {
+  gp_pdl_wait();
   constexpr int kRounds = kItems;
   __shared__ uint64_t sh[36];
   __shared__ uint32_t slot;
@@ -468,11 +481,13 @@ __global__ void __launch_bounds__(kBlock) rle_support(const uint32_t* __restrict
 }
 
 __global__ void rle_check(Plan* plan, uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || plan->index_method != GP_INDEX_RLE) return;
   if (plan->n_sel != plan->r) latch(status, GP_CORRUPT_PAYLOAD);  // pipeline.cpp:249-250
 }
 
-__global__ void rle_reset(unsigned long long* first) { *first = ~0ULL; }
+__global__ void rle_reset(unsigned long long* first) {
+  gp_pdl_wait(); *first = ~0ULL; }
 
 }  // namespace
 

@@ -30,6 +30,7 @@ constexpr int kSortWarps = kBlock / 32;
 __global__ void __launch_bounds__(kBlock) radix_hist(const uint32_t* __restrict__ keys, const uint64_t* n_dev,
                                                      int npass, uint32_t* __restrict__ ghist,
                                                      const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint32_t h[4][256];
   if (failed(status)) return;
   const uint64_t n = *n_dev;
@@ -68,6 +69,7 @@ __global__ void __launch_bounds__(kBlock) radix_onesweep(const uint32_t* __restr
                                                          uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                          uint32_t* flags, uint32_t* agg, uint32_t* inc,
                                                          uint32_t* ticket, const FitOut fo, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint32_t wcnt[kSortWarps][256];
   __shared__ uint32_t base[256];
   __shared__ __align__(16) uint32_t red_sh[kSortWarps][256];
@@ -211,6 +213,7 @@ __global__ void __launch_bounds__(kBlock) radix_onesweep(const uint32_t* __restr
 __global__ void __launch_bounds__(kBlock) scan_u32(uint32_t* data, const uint64_t* n_dev, uint64_t n_mul,
                                                    int tile_shift, uint64_t* tiles, uint32_t* ticket,
                                                    const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint64_t sh[36];
   __shared__ uint32_t slot;
   if (failed(status)) return;

@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(kHistBlock) topr_hist(const float* __restrict_
                                                         uint64_t d, uint32_t* __restrict__ ghist,
                                                         uint32_t* __restrict__ gcoarse, uint16_t* __restrict__ gmax,
                                                         const uint32_t* status) {
+  gp_pdl_wait();
   extern __shared__ uint32_t h[];  // kBins counters
   if (failed(status)) return;
   for (int i = threadIdx.x; i < kBins; i += kHistBlock) h[i] = 0;
@@ -156,6 +157,7 @@ __global__ void __launch_bounds__(kHistBlock) topr_hist(const float* __restrict_
 // summed here from the fine one
 __global__ void __launch_bounds__(1024) topr_pick_bin(const uint32_t* __restrict__ ghist, uint32_t* gcoarse,
                                                       uint64_t r, Plan* plan, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint64_t sh[40];
   if (failed(status)) return;
   if (threadIdx.x < kCoarse) {
@@ -536,6 +538,7 @@ __global__ void __launch_bounds__(kCandBlock) topr_select(
     const uint32_t* __restrict__ gcoarse, uint64_t d, uint64_t r, Plan* plan, uint32_t* cidx, float* cval,
     uint32_t* sidx, float* sval, uint32_t* fine, uint32_t* fcoarse, uint64_t* cnt, uint64_t* pair, uint32_t* wcnt,
     uint64_t chunk, bool dense, const uint32_t* status) {
+  gp_pdl_wait();
   cg::grid_group grid = cg::this_grid();
   __shared__ uint32_t bidx[kCandWarps][kWarpCandCap];
   __shared__ float bval[kCandWarps][kWarpCandCap];

@@ -41,6 +41,7 @@ __device__ __forceinline__ uint64_t key_of(double v) {
 __global__ void __launch_bounds__(kHistBlock) topr64_hist(const float* __restrict__ g, double* __restrict__ e,
                                                           uint64_t d, uint32_t* __restrict__ ghist,
                                                           const uint32_t* status) {
+  gp_pdl_wait();
   extern __shared__ uint32_t h[];
   if (failed(status)) return;
   for (int i = threadIdx.x; i < kBins; i += kHistBlock) h[i] = 0;
@@ -83,6 +84,7 @@ __device__ __forceinline__ void row_masks(const double* __restrict__ x, uint64_t
 __global__ void __launch_bounds__(kBlock) topr64_count(const double* __restrict__ x, uint64_t d,
                                                        const Plan* __restrict__ plan, uint64_t* cnt_c,
                                                        uint64_t* cnt_t, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint32_t wc[kBlock / 32], wt[kBlock / 32];
   if (failed(status)) return;
   const uint32_t bstar = plan->bin_star;
@@ -121,6 +123,7 @@ __global__ void __launch_bounds__(kBlock) topr64_write(const double* __restrict_
                                                        const uint64_t* off_t, uint32_t* __restrict__ cidx,
                                                        uint32_t* __restrict__ tidx, uint64_t* __restrict__ tkey,
                                                        uint32_t* fine, uint32_t* fcoarse, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint32_t wc[kBlock / 32], wt[kBlock / 32];
   __shared__ uint32_t sc[256];  // the coarse level: few distinct values, so counted per block first
   if (failed(status)) return;
@@ -183,6 +186,7 @@ constexpr int kFew = 4096;
 __global__ void __launch_bounds__(1024) topr64_refine_a(const uint32_t* ghist, const uint32_t* fine,
                                                         const uint32_t* fcoarse, uint64_t r, Plan* plan,
                                                         uint32_t* slow, uint32_t* nlist, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint64_t sh[40];
   __shared__ uint32_t s_c;
   __shared__ uint64_t s_before;
@@ -215,6 +219,7 @@ __global__ void __launch_bounds__(1024) topr64_refine_a(const uint32_t* ghist, c
 __global__ void topr64_collect(const uint64_t* __restrict__ tkey, const uint32_t* ghist, const Plan* plan,
                                const uint32_t* slow, uint32_t* lo32, uint32_t* lpos, uint32_t* nlist,
                                const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || *slow) return;
   const uint64_t nt = ghist[plan->bin_star];
   const uint64_t prefix = plan->r64_prefix;
@@ -241,6 +246,7 @@ __global__ void topr64_collect(const uint64_t* __restrict__ tkey, const uint32_t
 __global__ void __launch_bounds__(1024) topr64_refine_b(const uint32_t* __restrict__ tidx, const uint32_t* lo32g,
                                                         const uint32_t* lposg, Plan* plan, const uint32_t* slow,
                                                         const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint32_t lo32[kFew], lpos[kFew];
   __shared__ uint32_t h[256];
   __shared__ uint64_t sh[40];
@@ -321,6 +327,7 @@ __global__ void __launch_bounds__(1024) topr64_refine_b(const uint32_t* __restri
 __global__ void __launch_bounds__(1024) topr64_refine_slow(const double* __restrict__ x, const uint32_t* __restrict__ tidx,
                                                       const uint32_t* ghist, uint64_t r, Plan* plan,
                                                       const uint32_t* slow, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint32_t h[256];
   __shared__ uint64_t sh[40];
   __shared__ uint32_t s_digit, s_found;
@@ -403,6 +410,7 @@ __device__ __forceinline__ bool keep64(const double* __restrict__ x, const uint3
 __global__ void __launch_bounds__(kBlock) topr64_final_count(const double* __restrict__ x,
                                                              const uint32_t* __restrict__ cidx, const Plan* plan,
                                                              uint64_t* cnt, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint32_t wk[kBlock / 32];
   if (failed(status)) return;
   const uint64_t n = plan->n_cand, T = plan->thresh64;
@@ -428,6 +436,7 @@ __global__ void __launch_bounds__(kBlock) topr64_final_write(const double* __res
                                                              const uint32_t* __restrict__ cidx, Plan* plan,
                                                              const uint64_t* off, uint32_t* __restrict__ sidx,
                                                              double* __restrict__ sval, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint32_t wk[kBlock / 32];
   if (failed(status)) return;
   const uint64_t n = plan->n_cand, T = plan->thresh64;

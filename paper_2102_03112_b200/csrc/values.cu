@@ -14,6 +14,7 @@ namespace {
 
 __global__ void gather_values(const float* __restrict__ dense, const uint32_t* __restrict__ sel, const Plan* plan,
                               float* __restrict__ values, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const uint64_t n = plan->n_values;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -30,6 +31,7 @@ __global__ void gather_values(const float* __restrict__ dense, const uint32_t* _
 __global__ void gather_values64(const double* __restrict__ dense, const uint32_t* __restrict__ sup,
                                 const double* __restrict__ sval, uint64_t r, const uint32_t* __restrict__ sel,
                                 const Plan* plan, double* __restrict__ values, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const uint64_t n = plan->n_values;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -50,6 +52,7 @@ __global__ void gather_values64(const double* __restrict__ dense, const uint32_t
 
 __global__ void values_raw_encode(const ValSrc values, Plan* plan, uint8_t* out, int f64,
                                   const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const uint64_t n = plan->n_values;
   uint8_t* p = out + 49 + plan->il;
@@ -79,6 +82,7 @@ __global__ void values_raw_encode(const ValSrc values, Plan* plan, uint8_t* out,
 
 // decode_values length checks for the raw kinds (pipeline.cpp:98-99, :107-108)
 __global__ void values_raw_check(Plan* plan, uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const uint8_t vm = plan->value_method;
   const uint64_t n = plan->n_values;
@@ -98,6 +102,7 @@ __global__ void decode_scatter(const uint8_t* __restrict__ in, const Plan* plan,
                                const double* __restrict__ fitv, float* dense, uint64_t dense_d, float scale,
                                uint32_t* out_support, double* out_values, uint64_t cap, uint64_t* d_count,
                                uint64_t* d_dim, double* dense64, uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || plan->fused_bitmap) return;  // bitmap containers on the fused path: dense.cu bm_scatter
   // the container's d must equal the caller's dense length: to_dense builds a
   // d-vector (gradient.cpp:38-42) and the mean adds equal-length vectors

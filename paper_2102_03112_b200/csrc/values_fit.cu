@@ -80,6 +80,7 @@ __device__ __forceinline__ uint64_t desc_key64(double v) {
 __global__ void fit_keys(const ValSrc values, Plan* plan, uint32_t* __restrict__ keys,
                          uint32_t* __restrict__ idx, uint32_t* __restrict__ ghist, const float* __restrict__ gdense,
                          const uint32_t* __restrict__ gsel, float* __restrict__ vout, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint32_t cnt;
   __shared__ uint32_t h[4][256];
   if (failed(status) || !fit_active(plan)) return;
@@ -138,6 +139,7 @@ __global__ void fit_keys(const ValSrc values, Plan* plan, uint32_t* __restrict__
 // f64 pass 2 keys: the high words in pass 1's order
 __global__ void fit_keys_hi(const double* __restrict__ v64, const Plan* plan, const uint32_t* __restrict__ idx,
                             uint32_t* __restrict__ keys, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || !fit_active(plan)) return;
   const uint64_t n = plan->n_values;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -148,6 +150,7 @@ __global__ void fit_keys_hi(const double* __restrict__ v64, const Plan* plan, co
 // t[s] and the identity flag; map = sorted idx
 __global__ void fit_prepare(const ValSrc values, const uint32_t* __restrict__ map, Plan* plan,
                             double* __restrict__ t, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || !fit_active(plan)) return;
   const uint64_t n = plan->n_values;
   const uint64_t l = plan->sign_split;
@@ -391,6 +394,7 @@ __global__ void __launch_bounds__(256) fit_segment_coop(Plan* plan, const double
                                                         uint64_t* off, SegState* st, uint32_t* seg_end,
                                                         uint64_t* chunk, uint32_t node_cap, uint32_t seg_cap,
                                                         uint32_t* status) {
+  gp_pdl_wait();
   cg::grid_group grid = cg::this_grid();
   __shared__ double sdev[32];
   __shared__ uint32_t sarg[32];
@@ -746,6 +750,7 @@ __global__ void __launch_bounds__(256) fit_accumulate(const Plan* plan, const do
                                                       const uint32_t* __restrict__ seg_end,
                                                       const uint64_t* __restrict__ chunk,
                                                       double* __restrict__ partial, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ double red[8][kAcc];
   if (failed(status) || !poly_active(plan) || plan->degree > kMaxDeg) return;
   const uint32_t S = plan->nseg;
@@ -827,6 +832,7 @@ __constant__ LegendreTable kLegendre = make_legendre();
 __global__ void fit_solve(Plan* plan, const double* __restrict__ t, const uint32_t* __restrict__ seg_end,
                           const uint64_t* __restrict__ chunk, const double* __restrict__ partial, float* coeffs,
                           uint8_t* emit_out, uint32_t* status) {
+  gp_pdl_wait();
   __shared__ double sacc[kAcc];
   __shared__ double spow[2][kCps];  // alpha^k, beta^k (curvefit.cpp:157-172's pow values), one lane each
   if (failed(status) || !poly_active(plan) || plan->degree > kMaxDeg) return;
@@ -999,6 +1005,7 @@ constexpr int kWideScratch = 3 * kWideCps * kWideCps;                    // G | 
 __global__ void __launch_bounds__(256) fit_solve_wide(Plan* plan, const double* __restrict__ t,
                                                       const uint32_t* __restrict__ seg_end, float* coeffs,
                                                       double* scratch, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ double V[kWideBatch][kWideCps];
   __shared__ double Y[kWideBatch];
   __shared__ int16_t ej[kWideEntries], eq[kWideEntries];  // entry → (row, column); column -1 = rhs
@@ -1142,6 +1149,7 @@ __global__ void __launch_bounds__(256) fit_solve_wide(Plan* plan, const double* 
 // serialize_fit (curvefit.cpp:285-298) + reorder payload size; vl, rl, flags
 __global__ void fit_emit(Plan* plan, uint8_t* out, int cfg_degree, const uint32_t* __restrict__ seg_end,
                          const float* __restrict__ coeffs, uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || !fit_active(plan)) return;
   const uint32_t kind = plan->fit_kind;
   const uint32_t S = plan->nseg, deg = kind ? static_cast<uint32_t>(cfg_degree) : plan->degree;
@@ -1173,6 +1181,7 @@ __global__ void fit_emit(Plan* plan, uint8_t* out, int cfg_degree, const uint32_
 
 // reorder_encode (curvefit.cpp:332-340): entries of w bits, LSB-first
 __global__ void reorder_pack(const uint32_t* __restrict__ map, Plan* plan, uint8_t* out, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || !fit_active(plan) || plan->identity) return;
   const uint64_t rl = plan->rl, n = plan->n_values;
   uint32_t w = 0;
@@ -1203,6 +1212,7 @@ __global__ void reorder_pack(const uint32_t* __restrict__ map, Plan* plan, uint8
 // the sequential parse's first failure is the lowest failing bound index
 // (truncation before bound i, or bound i not increasing), found in parallel.
 __global__ void __launch_bounds__(256) fit_parse(const uint8_t* __restrict__ in, Plan* plan, uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint32_t s_first;
   __shared__ uint32_t s_found;
   __shared__ int s_err;
@@ -1312,6 +1322,7 @@ __global__ void __launch_bounds__(256) fit_parse(const uint8_t* __restrict__ in,
 // reorder entries (entry >= d → corrupt) + permutation check (curvefit.cpp:531-538)
 __global__ void reorder_unpack(const uint8_t* __restrict__ in, Plan* plan, uint32_t* __restrict__ map,
                                uint32_t* seen, uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || !fit_active(plan) || plan->rl == 0) return;
   const uint64_t n = plan->n_values, d = plan->d;
   uint32_t w = 0;
@@ -1341,6 +1352,7 @@ __global__ void reorder_unpack(const uint8_t* __restrict__ in, Plan* plan, uint3
 constexpr int kEvalSmemSeg = 64;
 __global__ void fit_eval(const uint8_t* __restrict__ in, const Plan* plan, const uint32_t* __restrict__ map,
                          double* __restrict__ out, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint32_t sb[kEvalSmemSeg];
   __shared__ float sc[kEvalSmemSeg * kCps];
   if (failed(status) || !fit_active(plan)) return;
@@ -1489,6 +1501,7 @@ __device__ void log_linear(const double* y, uint32_t begin, uint32_t len, double
 
 __global__ void __launch_bounds__(kDexpBlock) dexp_fit(Plan* plan, const double* __restrict__ t, uint32_t* seg_end,
                                                         float* coeffs, const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ double sh[(kDexpBlock / 32) * 14];
   __shared__ double sp[4], scand[4], sbest, slambda;
   __shared__ int sflag;  // bit0 accepted, bit1 converged, bit2 stop attempts
@@ -1633,6 +1646,7 @@ __global__ void __launch_bounds__(kDexpBlock) dexp_fit(Plan* plan, const double*
 
 // dexp model or the polynomial fallback (value_compress attempt 1)
 __global__ void dexp_decide(Plan* plan, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status) || plan->value_method != GP_VALUE_FIT_DEXP) return;
   if (plan->dexp_fail) return;  // fit_kind stays 0: the polynomial path runs
   const uint32_t n = static_cast<uint32_t>(plan->n_values), l = plan->sign_split;

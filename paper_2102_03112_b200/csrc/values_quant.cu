@@ -26,6 +26,7 @@ namespace {
 
 __global__ void quant_scales(const ValSrc values, Plan* plan, uint8_t* out, uint32_t bucket,
                              uint32_t* __restrict__ zlen, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const uint64_t n = plan->n_values;
   const uint64_t nb = (n + bucket - 1) / bucket;
@@ -49,6 +50,7 @@ __global__ void quant_scales(const ValSrc values, Plan* plan, uint8_t* out, uint
 // exclusive scan of zlen[0, nb) in place (one block of 1024)
 __global__ void __launch_bounds__(1024) quant_zscan(const Plan* plan, uint32_t bucket, uint32_t* zlen,
                                                     const uint32_t* status) {
+  gp_pdl_wait();
   __shared__ uint64_t sh[40];
   if (failed(status)) return;
   const uint64_t n = plan->n_values;
@@ -68,6 +70,7 @@ __global__ void __launch_bounds__(1024) quant_zscan(const Plan* plan, uint32_t b
 __global__ void quant_codes(const ValSrc values, const Plan* plan, const uint8_t* __restrict__ out,
                             uint32_t bits, uint32_t bucket, const uint32_t* __restrict__ zbefore,
                             uint32_t* __restrict__ codes, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const uint64_t n = plan->n_values;
   const uint8_t* sp = out + 49 + plan->il + 5;
@@ -96,6 +99,7 @@ __global__ void quant_codes(const ValSrc values, const Plan* plan, const uint8_t
 
 __global__ void quant_pack(const uint32_t* __restrict__ codes, Plan* plan, uint8_t* out, uint32_t bits,
                            uint32_t bucket, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const uint64_t n = plan->n_values;
   const uint64_t nb = (n + bucket - 1) / bucket;
@@ -126,6 +130,7 @@ __global__ void quant_pack(const uint32_t* __restrict__ codes, Plan* plan, uint8
 
 // parse_quant (codecs.cpp:335-351) + the trailing check (pipeline.cpp:127)
 __global__ void quant_parse(const uint8_t* __restrict__ in, Plan* plan, uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const uint64_t vl = plan->vl, count = plan->n_values;
   const uint8_t* p = in + plan->off_value;
@@ -146,6 +151,7 @@ __global__ void quant_parse(const uint8_t* __restrict__ in, Plan* plan, uint32_t
 
 __global__ void quant_values(const uint8_t* __restrict__ in, const Plan* plan, double* __restrict__ vals,
                              const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const uint64_t count = plan->n_values;
   const uint32_t bits = plan->q_bits, bucket = plan->q_bucket;
@@ -167,6 +173,7 @@ __global__ void quant_values(const uint8_t* __restrict__ in, const Plan* plan, d
 }
 
 __global__ void slot_encode(const ValSrc values, Plan* plan, uint8_t* out, const uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const uint64_t n = plan->n_values;
   uint8_t* p = out + 49 + plan->il;
@@ -183,6 +190,7 @@ __global__ void slot_encode(const ValSrc values, Plan* plan, uint8_t* out, const
 
 // byte_decompress (codecs.cpp:268-288) + pipeline.cpp:131-133
 __global__ void slot_parse(const uint8_t* __restrict__ in, Plan* plan, uint32_t* status) {
+  gp_pdl_wait();
   if (failed(status)) return;
   const uint64_t vl = plan->vl, count = plan->n_values;
   const uint8_t* p = in + plan->off_value;
