@@ -235,6 +235,8 @@ __global__ void __launch_bounds__(kCrcBlock) crc_chunks(const uint8_t* __restric
 // chunk is 64 lookups, bank conflicts cost little at these sizes, and a
 // block stages 12.5 KiB of tables instead of 138 KiB.
 constexpr int kTailBlock = 256;
+// crc_tail's largest grid (its partials buffer holds 256 blocks; x^(512 T) is built for it)
+inline int tail_grid_max(const gp_ctx* ctx) { return ctx->sm_count < 256 ? ctx->sm_count : 256; }
 __device__ __forceinline__ uint32_t mul_nib(const uint32_t* t, uint32_t v) {
   uint32_t r = 0;
 #pragma unroll
@@ -514,7 +516,7 @@ int crc_tables_init(gp_ctx* ctx) {
     return S;
   };
   for (int j = 0; j < 17; ++j) {
-    const uint32_t S = xpow(j < 16 ? (64ull << j) : 64ull * kTailBlock * static_cast<uint64_t>(ctx->sm_count));
+    const uint32_t S = xpow(j < 16 ? (64ull << j) : 64ull * kTailBlock * static_cast<uint64_t>(tail_grid_max(ctx)));
     for (int i = 0; i < 8; ++i)
       for (int n = 0; n < 16; ++n) st[4 * 256 + j * 128 + i * 16 + n] = n ? mult(static_cast<uint32_t>(n) << (4 * i), S) : 0u;
   }
@@ -538,7 +540,8 @@ void crc_range(gp_ctx* ctx, const uint8_t* base, const uint64_t* off_dev, uint64
   if (len_bound <= tail_max) {  // crc_tail: one lane per 64-byte chunk (Horner rows above one grid)
     const uint64_t nch = (len_bound + 63) / 64;
     const uint64_t need = (nch + kTailBlock - 1) / kTailBlock;
-    const int grid = static_cast<int>(need < static_cast<uint64_t>(ctx->sm_count) ? (need ? need : 1) : ctx->sm_count);
+    const int gmax = tail_grid_max(ctx);
+    const int grid = static_cast<int>(need < static_cast<uint64_t>(gmax) ? (need ? need : 1) : gmax);
     // a grid below the full one never takes a second row (x^(512 T) is the full grid's)
     GP_LAUNCH(ctx, crc_tail, grid, kTailBlock, 0, s, base, off_dev, off_host, la, lb, lc, len_host,
               w.crc_digits + 13 * 256, w.crc_acc + 64, w.crc_acc + 2, out, ep, w.status);

@@ -20,9 +20,9 @@
 //                  Coefficients agree with the reference within f32 rounding
 //                  (tolerance-checked).
 //   fit_emit / reorder_pack : serialize_fit + the bit-packed map
-// Decode: fit_parse (parse_fit + reorder checks), reorder_unpack (entries,
-// permutation check), fit_eval (fp64 Horner without FMA, sign unfold,
-// permutation scatter) — bit-exact for a given container.
+// Decode: fit_parse (parse_fit + reorder checks), fit_unpack_eval (reorder
+// entries + permutation check, fp64 Horner without FMA, sign unfold,
+// permutation scatter, one pass) — bit-exact for a given container.
 #include <cooperative_groups.h>
 
 #include "gp_ctx.hpp"
@@ -1309,7 +1309,7 @@ __global__ void __launch_bounds__(256) fit_parse(const uint8_t* __restrict__ in,
       return;
     }
   }
-  if (threadIdx.x == 0) {  // fit_eval reads bounds and coefficients from the payload itself
+  if (threadIdx.x == 0) {  // fit_unpack_eval reads bounds and coefficients from the payload itself
     plan->fit_bounds_at = plan->off_value + 3;
     plan->fit_coeffs_at = plan->off_value + coeff_at;
     plan->nseg = S;
@@ -1319,39 +1319,17 @@ __global__ void __launch_bounds__(256) fit_parse(const uint8_t* __restrict__ in,
   }
 }
 
-// reorder entries (entry >= d → corrupt) + permutation check (curvefit.cpp:531-538)
-__global__ void reorder_unpack(const uint8_t* __restrict__ in, Plan* plan, uint32_t* __restrict__ map,
-                               uint32_t* seen, uint32_t* status) {
-  gp_pdl_wait();
-  if (failed(status) || !fit_active(plan) || plan->rl == 0) return;
-  const uint64_t n = plan->n_values, d = plan->d;
-  uint32_t w = 0;
-  for (uint64_t x = d - 1; x; x >>= 1) ++w;
-  const uint8_t* p = in + plan->off_reorder;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    uint64_t v = 0;
-    const uint64_t bit0 = i * w;
-    for (uint32_t j = 0; j < w; ++j) {
-      const uint64_t bit = bit0 + j;
-      v |= static_cast<uint64_t>((p[bit >> 3] >> (bit & 7)) & 1u) << j;
-    }
-    if (v >= d || v >= n) {
-      latch(status, GP_CORRUPT_PAYLOAD);
-      continue;
-    }
-    map[i] = static_cast<uint32_t>(v);
-    if (atomicOr(&seen[v >> 5], 1u << (v & 31)) & (1u << (v & 31))) latch(status, GP_CORRUPT_PAYLOAD);
-  }
-}
-
-// value_decompress evaluate + unfold + scatter (curvefit.cpp:517-541).  Bounds
+// value_decompress (curvefit.cpp:517-541) in one pass: per value s, the
+// reorder entry (entry >= d or >= n → corrupt; permutation check by an
+// atomicOr bitset, :531-538), evaluate + unfold, store at the entry.  Bounds
 // and coefficients come straight from the payload (any degree byte and up to
 // 0xffff segments); models of <= 64 segments and <= 8 coefficients are staged
-// in shared memory, larger ones searched in place (binary search of the bounds).
+// in shared memory, larger ones searched in place (binary search of the
+// bounds).  Errors latch the pre-verdict status; nothing reaches the caller's
+// dense vector before the verdict (decode_common).
 constexpr int kEvalSmemSeg = 64;
-__global__ void fit_eval(const uint8_t* __restrict__ in, const Plan* plan, const uint32_t* __restrict__ map,
-                         double* __restrict__ out, const uint32_t* status) {
+__global__ void fit_unpack_eval(const uint8_t* __restrict__ in, const Plan* plan, uint32_t* __restrict__ map,
+                                uint32_t* seen, double* __restrict__ out, uint32_t* status) {
   gp_pdl_wait();
   __shared__ uint32_t sb[kEvalSmemSeg];
   __shared__ float sc[kEvalSmemSeg * kCps];
@@ -1366,11 +1344,30 @@ __global__ void fit_eval(const uint8_t* __restrict__ in, const Plan* plan, const
     for (uint32_t i = threadIdx.x; i < S * cps; i += blockDim.x) sc[i] = __uint_as_float(ld_u32_unaligned(cp + 4ull * i));
     __syncthreads();
   }
-  const uint64_t n = plan->n_values;
+  const uint64_t n = plan->n_values, d = plan->d;
   const uint64_t l = plan->sign_split;
   const bool reorder = plan->rl != 0;
+  uint32_t w = 0;
+  for (uint64_t x = d - 1; x; x >>= 1) ++w;
+  const uint8_t* rp = in + plan->off_reorder;
   for (uint64_t s = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; s < n;
        s += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint64_t dst = s;
+    if (reorder) {
+      uint64_t v = 0;
+      const uint64_t bit0 = s * w;
+      for (uint32_t j = 0; j < w; ++j) {
+        const uint64_t bit = bit0 + j;
+        v |= static_cast<uint64_t>((rp[bit >> 3] >> (bit & 7)) & 1u) << j;
+      }
+      if (v >= d || v >= n) {
+        latch(status, GP_CORRUPT_PAYLOAD);
+        continue;
+      }
+      map[s] = static_cast<uint32_t>(v);
+      if (atomicOr(&seen[v >> 5], 1u << (v & 31)) & (1u << (v & 31))) latch(status, GP_CORRUPT_PAYLOAD);
+      dst = v;
+    }
     const uint64_t j = s < l ? s : l + (n - 1 - s);  // position in the folded sequence
     uint32_t seg, begin;
     double acc = 0.0;
@@ -1404,8 +1401,7 @@ __global__ void fit_eval(const uint8_t* __restrict__ in, const Plan* plan, const
           acc = __dadd_rn(__dmul_rn(acc, x), static_cast<double>(__uint_as_float(ld_u32_unaligned(c + 4ull * q))));
       }
     }
-    const double v = s < l ? acc : -acc;
-    out[reorder ? map[s] : s] = v;
+    out[dst] = s < l ? acc : -acc;
   }
 }
 
@@ -1731,10 +1727,10 @@ void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, 
 
 void launch_decode_fit(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, cudaStream_t s) {
   Workspace& w = ctx->ws;
+  cudaMemsetAsync(w.u32c, 0, ((n_bound + 31) / 32) * 4, s);  // before fit_parse: the kernels chain by PDL
   GP_LAUNCH(ctx, fit_parse, 1, 256, 0, s, in, w.plan, w.status);
-  cudaMemsetAsync(w.u32c, 0, ((n_bound + 31) / 32) * 4, s);
-  GP_LAUNCH(ctx, reorder_unpack, grid_for(ctx, n_bound, 256), 256, 0, s, in, w.plan, w.u32b, w.u32c, w.status);
-  GP_LAUNCH(ctx, fit_eval, grid_for(ctx, n_bound, 256), 256, 0, s, in, w.plan, w.u32b, w.f64a, w.status);
+  GP_LAUNCH(ctx, fit_unpack_eval, grid_for(ctx, n_bound, 256), 256, 0, s, in, w.plan, w.u32b, w.u32c, w.f64a,
+            w.status);
 }
 
 }  // namespace gp

@@ -26,7 +26,7 @@ STAGE_KERNELS = {
     "p2_sets": ["p2_pairs", "p2_scatter"],
     "dec_p2_sets": ["p2_pairs", "p2_scatter"],
     "topr": ["topr_hist", "topr_select"],
-    "index": ["nz_encode"],
+    "index": ["nz_count", "nz_write"],
     "p2_engine": ["p2_engine"],
     "dec_p2_engine": ["p2_engine"],
     "pack_crc": ["crc_chunks"],
