@@ -137,36 +137,41 @@ __global__ void __launch_bounds__(kNzBlock) nz_count(const float* __restrict__ g
     const uint64_t it2 = it + nwarps;
     const uint64_t base = it * 1024, base2 = it2 * 1024;
     uint32_t c = 0, c2 = 0;
-    if (vec && base2 + 1024 <= d) {
-      float4 v[16];
+    // each item on the vector path unless it is the ragged last one (a second
+    // item past the end is simply absent: no scalar fallback for it)
+    const bool v1 = vec && base + 1024 <= d, v2 = vec && base2 + 1024 <= d;
+    float4 v[16];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = __ldg(reinterpret_cast<const float4*>(g + base + 4 * (lane + 32 * j)));
-#pragma unroll
-      for (int j = 0; j < 8; ++j) v[8 + j] = __ldg(reinterpret_cast<const float4*>(g + base2 + 4 * (lane + 32 * j)));
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const uint32_t n = ((__float_as_uint(v[j].x) & 0x7FFFFFFFu) != 0u) +
-                           ((__float_as_uint(v[j].y) & 0x7FFFFFFFu) != 0u) +
-                           ((__float_as_uint(v[j].z) & 0x7FFFFFFFu) != 0u) +
-                           ((__float_as_uint(v[j].w) & 0x7FFFFFFFu) != 0u);
-        if (j < 8) c += n; else c2 += n;
-      }
-    } else {
-      for (int k = 0; k < 32; ++k) {
-        const uint64_t i = base + 32 * k + lane, i2 = base2 + 32 * k + lane;
-        if (i < d) c += (__float_as_uint(g[i]) & 0x7FFFFFFFu) != 0u;
-        if (it2 < nitems && i2 < d) c2 += (__float_as_uint(g[i2]) & 0x7FFFFFFFu) != 0u;
-      }
+    for (int j = 0; j < 8; ++j) {
+      v[j] = v1 ? __ldg(reinterpret_cast<const float4*>(g + base + 4 * (lane + 32 * j))) : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[8 + j] = v2 ? __ldg(reinterpret_cast<const float4*>(g + base2 + 4 * (lane + 32 * j)))
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const uint32_t n = ((__float_as_uint(v[j].x) & 0x7FFFFFFFu) != 0u) + ((__float_as_uint(v[j].y) & 0x7FFFFFFFu) != 0u) +
+                         ((__float_as_uint(v[j].z) & 0x7FFFFFFFu) != 0u) + ((__float_as_uint(v[j].w) & 0x7FFFFFFFu) != 0u);
+      if (j < 8) c += n; else c2 += n;
+    }
+    if (!v1)
+      for (int k = 0; k < 32; ++k) {
+        const uint64_t i = base + 32 * k + lane;
+        if (i < d) c += (__float_as_uint(g[i]) & 0x7FFFFFFFu) != 0u;
+      }
+    if (!v2 && it2 < nitems)
+      for (int k = 0; k < 32; ++k) {
+        const uint64_t i = base2 + 32 * k + lane;
+        if (i < d) c2 += (__float_as_uint(g[i]) & 0x7FFFFFFFu) != 0u;
+      }
     c = __reduce_add_sync(kFull, c);
     c2 = __reduce_add_sync(kFull, c2);
     if (lane == 0) {
       atomicAdd(reinterpret_cast<unsigned long long*>(&tiles[it >> 3]), static_cast<unsigned long long>(c));
       if (it2 < nitems)
         atomicAdd(reinterpret_cast<unsigned long long*>(&tiles[it2 >> 3]), static_cast<unsigned long long>(c2));
-      __threadfence();
     }
   }
+  __threadfence();  // this thread's counter adds, before the block's ticket (one fence per thread, not per item)
   __syncthreads();
   // last block done: exclusive prefixes of the tile counts, the nnz == r gate
   if (threadIdx.x == 0) {
@@ -176,16 +181,33 @@ __global__ void __launch_bounds__(kNzBlock) nz_count(const float* __restrict__ g
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  // thread i owns tiles [i per, (i + 1) per): its counts are read once, all
+  // loads in flight together (16 per batch), summed, scanned, written back
   const uint64_t per = (ntiles + kNzBlock - 1) / kNzBlock;
   const uint64_t t0 = threadIdx.x * per;
+  const uint64_t t1 = t0 + per < ntiles ? t0 + per : ntiles;
+  constexpr int kBatch = 16;
+  uint64_t cnt[kBatch];
   uint64_t mine = 0;
-  for (uint64_t t = t0; t < t0 + per && t < ntiles; ++t) mine += __ldcg(&tiles[t]);
+  for (uint64_t b = t0; b < t1; b += kBatch) {
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k) cnt[k] = b + k < t1 ? __ldcg(&tiles[b + k]) : 0;
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k) mine += cnt[k];
+  }
   uint64_t nnz = 0;
   uint64_t run = block_exclusive_sum<uint64_t, kNzBlock>(mine, scratch, nnz);
-  for (uint64_t t = t0; t < t0 + per && t < ntiles; ++t) {
-    const uint64_t c = __ldcg(&tiles[t]);
-    tiles[t] = run;
-    run += c;
+  for (uint64_t b = t0; b < t1; b += kBatch) {
+    if (per > kBatch) {  // more than one batch: reload this one (the registers hold the last)
+#pragma unroll
+      for (int k = 0; k < kBatch; ++k) cnt[k] = b + k < t1 ? __ldcg(&tiles[b + k]) : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k)
+      if (b + k < t1) {
+        tiles[b + k] = run;
+        run += cnt[k];
+      }
   }
   if (threadIdx.x == 0) {
     if (nnz == r) {
