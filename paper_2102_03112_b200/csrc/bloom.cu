@@ -461,7 +461,7 @@ __global__ void select_slice(const uint32_t* __restrict__ P, const Plan* plan, u
 
 void launch_bloom_build(gp_ctx* ctx, uint8_t* out, uint64_t m, uint64_t r, cudaStream_t s) {
   Workspace& w = ctx->ws;
-  cudaMemsetAsync(w.filter, 0, ((m + 31) / 32) * 4, s);
+  fill_async(ctx, w.filter, 0, ((m + 31) / 32) * 4, s);
   GP_LAUNCH(ctx, bloom_insert, grid_for(ctx, r, 128), 128, 0, s, w.support, r, w.plan, w.filter, w.status);
   GP_LAUNCH(ctx, bloom_emit, grid_for(ctx, (m + 7) / 8, 256), 256, 0, s, w.filter, w.plan, out, w.status);
 }
@@ -492,7 +492,7 @@ void launch_bloom_scan(gp_ctx* ctx, uint64_t d_bound, uint64_t m_host, bool deco
   const uint64_t fbytes = ((m_host + 31) / 32) * 4;
   uint32_t* bitmap = w.u32c;  // d-bit membership bitmap
   const uint64_t nwd = (d_bound + 31) / 32;
-  cudaMemsetAsync(bitmap, 0, nwd * 4, s);
+  fill_async(ctx, bitmap, 0, nwd * 4, s);
   if (m_host && fbytes <= kSmemFilterMax) {
     using S = ScanShape<true, 4, 2>;
     auto* kern = bloom_members<true, 4, 2>;

@@ -48,10 +48,38 @@ void stage_end(gp_ctx* ctx, cudaStream_t s) {
 
 bool g_pdl = !getenv("GP_PDL") || atoi(getenv("GP_PDL")) != 0;
 
+namespace {
+__global__ void fill_bytes(uint8_t* p, uint32_t word, uint64_t bytes) {
+  gp_pdl_wait();
+  const uint64_t head = (16 - (reinterpret_cast<uintptr_t>(p) & 15)) & 15;
+  const uint64_t h = head < bytes ? head : bytes;
+  const uint64_t n16 = (bytes - h) / 16;
+  const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  uint4* q = reinterpret_cast<uint4*>(p + h);
+  for (uint64_t i = tid; i < n16; i += stride) q[i] = make_uint4(word, word, word, word);
+  if (tid < h) p[tid] = static_cast<uint8_t>(word);
+  const uint64_t tail = h + 16 * n16;
+  if (tid < bytes - tail) p[tail + tid] = static_cast<uint8_t>(word);
+}
+}  // namespace
+
+void fill_async(gp_ctx* ctx, void* p, int value, size_t bytes, cudaStream_t s) {
+  static const bool kern = !getenv("GP_FILL_KERNEL") || atoi(getenv("GP_FILL_KERNEL")) != 0;
+  if (!kern) {
+    cudaMemsetAsync(p, value, bytes, s);
+    return;
+  }
+  if (bytes == 0) return;
+  const uint32_t b = static_cast<uint32_t>(value) & 0xFFu;
+  GP_LAUNCH(ctx, fill_bytes, grid_for(ctx, (bytes + 15) / 16, 256), 256, 0, s, static_cast<uint8_t*>(p),
+            b * 0x01010101u, static_cast<uint64_t>(bytes));
+}
+
 void reset_scan(gp_ctx* ctx, cudaStream_t s, uint64_t ntiles_bound) {
   Workspace& w = ctx->ws;
   const uint64_t n = ntiles_bound < w.tiles_cap ? ntiles_bound : w.tiles_cap;
-  cudaMemsetAsync(w.scan_base, 0, 128 + n * 8, s);
+  fill_async(ctx, w.scan_base, 0, 128 + n * 8, s);
 }
 
 namespace {
@@ -371,7 +399,7 @@ int gp_ctx_status(gp_ctx* ctx, void* stream) {
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return set_error(ctx, GP_CUDA, std::string("status: ") + cudaGetErrorString(e));
   if (st != 0) {
-    cudaMemsetAsync(ctx->ws.status, 0, sizeof(uint32_t), s);
+    fill_async(ctx, ctx->ws.status, 0, sizeof(uint32_t), s);
     cudaStreamSynchronize(s);
     static const char* names[] = {"ok", "Error", "DecodeError", "TruncatedError", "ChecksumError",
                                   "UnknownMethodError", "CorruptPayloadError", "FitError", "CUDA",
@@ -917,7 +945,7 @@ int gp_bloom_scan_range(gp_ctx* ctx, const uint8_t* d_filter, uint64_t filter_le
   launch_bloom_parse(ctx, d_filter, ctx->ws.m_cap, s);
   if (hi == lo) {  // empty slice: |P| = 0 (the scan treats hi = 0 as "all of d")
     GP_LAUNCH(ctx, set_scan_range, 1, 1, 0, s, ctx->ws.plan, 0, 0);
-    cudaMemsetAsync(d_count, 0, sizeof(uint64_t), s);
+    fill_async(ctx, d_count, 0, sizeof(uint64_t), s);
     return check_launch(ctx, "scan_range");
   }
   GP_LAUNCH(ctx, set_scan_range, 1, 1, 0, s, ctx->ws.plan, lo, hi);

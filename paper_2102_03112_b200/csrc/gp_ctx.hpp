@@ -216,6 +216,10 @@ inline void launch_k(void (*k)(P...), dim3 grid, dim3 block, size_t smem, cudaSt
     ++(ctx)->launches;                                                                \
   } while (0)
 
+// cudaMemsetAsync as a PDL-chained kernel (a memset node between two kernels
+// breaks their programmatic launch overlap); GP_FILL_KERNEL=0 uses the memset
+void fill_async(gp_ctx* ctx, void* p, int value, size_t bytes, cudaStream_t s);
+
 // Grid for a grid-stride loop over n items: enough blocks to cover n, capped
 // at 8 resident blocks per SM.
 inline int grid_for(const gp_ctx* ctx, uint64_t n, int block) {

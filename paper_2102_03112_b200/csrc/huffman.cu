@@ -367,7 +367,7 @@ __global__ void huff_reset(uint64_t* res, uint32_t* flag, uint32_t* changed) {
 
 void launch_index_huffman(gp_ctx* ctx, uint8_t* out, uint64_t r, uint64_t il_bound, cudaStream_t s) {
   Workspace& w = ctx->ws;
-  cudaMemsetAsync(out + 49, 0, il_bound, s);
+  fill_async(ctx, out + 49, 0, il_bound, s);
   GP_LAUNCH(ctx, huff_table, 1, 1, 0, s, w.plan, w.huff, w.status);
   const uint64_t ntiles = (r + kHBlock * kHKeys - 1) / (kHBlock * kHKeys);
   reset_scan(ctx, s, ntiles + 1);

@@ -191,7 +191,7 @@ void launch_index_none(gp_ctx* ctx, uint8_t* out, uint64_t r, cudaStream_t s) {
 
 void launch_index_bitmap(gp_ctx* ctx, uint8_t* out, uint64_t d, uint64_t r, cudaStream_t s) {
   Workspace& w = ctx->ws;
-  cudaMemsetAsync(w.u32c, 0, ((d + 31) / 32) * 4, s);
+  fill_async(ctx, w.u32c, 0, ((d + 31) / 32) * 4, s);
   GP_LAUNCH(ctx, bitmap_scatter, grid_for(ctx, r, 256), 256, 0, s, w.support, r, w.u32c, w.status);
   GP_LAUNCH(ctx, bitmap_emit, grid_for(ctx, (d + 7) / 8, 256), 256, 0, s, w.u32c, d, out, w.status);
 }

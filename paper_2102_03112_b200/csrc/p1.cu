@@ -134,8 +134,8 @@ void launch_select_p1(gp_ctx* ctx, uint64_t n_bound, uint64_t r_bound, cudaStrea
   int bits = 8;
   while (bits < 32 && (1ull << bits) < n_bound) bits += 8;
   launch_radix_sort(ctx, w.u32a, w.u32b, w.u32c, w.u32d, &w.plan->r, r_bound, bits, s);
-  cudaMemsetAsync(w.first_touch, 0xFF, n_bound * sizeof(uint32_t), s);
-  cudaMemsetAsync(w.flags, 0, n_bound, s);
+  fill_async(ctx, w.first_touch, 0xFF, n_bound * sizeof(uint32_t), s);
+  fill_async(ctx, w.flags, 0, n_bound, s);
   GP_LAUNCH(ctx, p1_groups, grid_for(ctx, r_bound, 256), 256, 0, s, w.plan, w.u32a, w.first_touch, w.status);
   GP_LAUNCH(ctx, p1_resolve, grid_for(ctx, r_bound, 256), 256, 0, s, w.plan,
             reinterpret_cast<const uint32_t*>(w.f64a), w.u32a, w.u32b, w.first_touch, w.flags, w.status);

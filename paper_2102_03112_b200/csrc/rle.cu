@@ -525,7 +525,7 @@ void launch_decode_index_rle(gp_ctx* ctx, const uint8_t* in, uint64_t len_bound,
             w.status);
   GP_LAUNCH(ctx, rle_finish, 1, 1, 0, s, in, w.plan, w.u32a, first, w.status);
   const uint64_t nw = (d_bound + 31) / 32;
-  cudaMemsetAsync(w.u32c, 0, nw * 4, s);
+  fill_async(ctx, w.u32c, 0, nw * 4, s);
   GP_LAUNCH(ctx, rle_toggles, grid_for(ctx, len_bound, 256), 256, 0, s, w.plan, cum, w.u32c, w.status);
   const uint64_t wt = (nw + kTile - 1) / kTile;
   reset_scan(ctx, s, wt + 1);

@@ -272,9 +272,9 @@ void launch_radix_sort(gp_ctx* ctx, uint32_t* keys, uint32_t* vals, uint32_t* kt
   Workspace& w = ctx->ws;
   const int npass = bits / 8;
   const uint64_t ntiles = (n_bound + kTile - 1) / kTile;
-  cudaMemsetAsync(w.sort_flags, 0, (64 + ntiles) * sizeof(uint32_t), s);
+  fill_async(ctx, w.sort_flags, 0, (64 + ntiles) * sizeof(uint32_t), s);
   if (!hist_ready) {
-    cudaMemsetAsync(w.sort_hist, 0, 4 * 256 * sizeof(uint32_t), s);
+    fill_async(ctx, w.sort_hist, 0, 4 * 256 * sizeof(uint32_t), s);
     const int hgrid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((n_bound + kBlock - 1) / kBlock,
                                                                                  ctx->sm_count * 2ULL)));
     GP_LAUNCH(ctx, radix_hist, hgrid, kBlock, 0, s, keys, n_dev, npass, w.sort_hist, w.status);

@@ -715,7 +715,7 @@ void launch_top_r(gp_ctx* ctx, const float* grad, uint64_t d, uint64_t r, cudaSt
   uint32_t* coarse = w.hist + kBins;
   uint32_t* fine = coarse + kCoarse;
   uint32_t* fcoarse = fine + kFine;
-  cudaMemsetAsync(w.hist, 0, (kBins + kCoarse + kFine + 256) * sizeof(uint32_t), s);
+  fill_async(ctx, w.hist, 0, (kBins + kCoarse + kFine + 256) * sizeof(uint32_t), s);
   uint16_t* gmax = reinterpret_cast<uint16_t*>(w.u32d);  // skip index, d/8 entries
   const int hist_grid = static_cast<int>(std::min<uint64_t>((d / 4 + kHistBlock - 1) / kHistBlock + 1,
                                                             static_cast<uint64_t>(ctx->sm_count)));

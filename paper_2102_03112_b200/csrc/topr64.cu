@@ -475,7 +475,7 @@ void launch_topr_pick_bin(gp_ctx* ctx, uint64_t r, cudaStream_t s);  // topr.cu
 void launch_top_r64(gp_ctx* ctx, const float* grad, double* residual, uint64_t d, uint64_t r, cudaStream_t s) {
   Workspace& w = ctx->ws;
   const uint64_t nchunks = (d + kChunk - 1) / kChunk;
-  cudaMemsetAsync(w.hist, 0, (kBins + 256 + 65536 + 256) * sizeof(uint32_t), s);
+  fill_async(ctx, w.hist, 0, (kBins + 256 + 65536 + 256) * sizeof(uint32_t), s);
   const int hist_grid = static_cast<int>(std::min<uint64_t>((d + 4 * kHistBlock - 1) / (4 * kHistBlock),
                                                             static_cast<uint64_t>(ctx->sm_count)));
   GP_LAUNCH(ctx, topr64_hist, std::max(1, hist_grid), kHistBlock, kBins * 4, s, grad, residual, d, w.hist, w.status);
@@ -490,7 +490,7 @@ void launch_top_r64(gp_ctx* ctx, const float* grad, double* residual, uint64_t d
   uint32_t* fcoarse = fine + 65536;
   uint64_t* tkey = reinterpret_cast<uint64_t*>(w.f64b);  // compact tie keys (free during top-r)
   uint32_t* slow = w.ticket + 12;                        // zeroed below
-  cudaMemsetAsync(slow, 0, sizeof(uint32_t), s);
+  fill_async(ctx, slow, 0, sizeof(uint32_t), s);
   GP_LAUNCH(ctx, topr64_write, grid, kBlock, 0, s, residual, d, w.plan, off_c, off_t, w.cand_idx, w.u32a, tkey, fine,
             fcoarse, w.status);
   uint32_t* nlist = w.ticket + 13;

@@ -1666,7 +1666,7 @@ void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, 
   const ValSrc vals{w.values, ctx->vals64};
   // f32 values: the keys kernel also builds the sort's digit histograms
   uint32_t* ghist = ctx->vals64 ? nullptr : w.sort_hist;
-  if (ghist) cudaMemsetAsync(ghist, 0, 4 * 256 * sizeof(uint32_t), s);
+  if (ghist) fill_async(ctx, ghist, 0, 4 * 256 * sizeof(uint32_t), s);
   const float* gdense = ctx->vals64 ? nullptr : ctx->gather_dense;
   GP_LAUNCH(ctx, fit_keys, std::min(grid_for(ctx, n_bound, 256), 2 * ctx->sm_count), 256, 0, s, vals, w.plan, w.u32a,
             w.u32b, ghist, gdense, w.sel, w.values, w.status);
@@ -1727,7 +1727,7 @@ void launch_values_fit(gp_ctx* ctx, uint8_t* out, int degree, int max_segments, 
 
 void launch_decode_fit(gp_ctx* ctx, const uint8_t* in, uint64_t n_bound, cudaStream_t s) {
   Workspace& w = ctx->ws;
-  cudaMemsetAsync(w.u32c, 0, ((n_bound + 31) / 32) * 4, s);  // before fit_parse: the kernels chain by PDL
+  fill_async(ctx, w.u32c, 0, ((n_bound + 31) / 32) * 4, s);  // before fit_parse: the kernels chain by PDL
   GP_LAUNCH(ctx, fit_parse, 1, 256, 0, s, in, w.plan, w.status);
   GP_LAUNCH(ctx, fit_unpack_eval, grid_for(ctx, n_bound, 256), 256, 0, s, in, w.plan, w.u32b, w.u32c, w.f64a,
             w.status);
