@@ -21,3 +21,7 @@ ncu --set full --import-source on --clock-control none --cache-control none \
   -k regex:"nz_count|nz_write|crc_chunks|bm_scatter|bm_counts" -c 8 -o $o/full_c3 -f \
   python bench.py --config c3 --steps 1 --warmup 3 --no-cpu-baseline > $o/full_c3.log 2>&1
 tail -1 $o/full_c3.log
+for st in 12 16; do
+  timeout 300 python bench.py --config c5 --streams $st --steps 10 --warmup 3 --no-cpu-baseline > $o/c5_streams_$st.json 2>/dev/null
+  python -c "import json; d=json.load(open('$o/c5_streams_$st.json')); print('c5 streams $st', d['ms_per_step'])"
+done
