@@ -494,7 +494,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-early", action="store_true", help="N = 1: no early index decode on a second context")
     ap.add_argument("--no-graph", action="store_true", help="N = 1: launch the step eagerly instead of as a CUDA graph")
-    ap.add_argument("--streams", type=int, default=8, help="bucketed configs: codec contexts / CUDA streams")
+    ap.add_argument("--streams", type=int, default=16, help="bucketed configs: codec contexts / CUDA streams")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

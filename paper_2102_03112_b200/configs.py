@@ -32,7 +32,7 @@ CONFIGS = {
     "c2r": dict(workload="ResNet-20-sized 0.27M-element gradient, top-r 1%, RLE indices + raw f32 values",
                 d=269_722, ratio=0.01, index=2, value=0, fpr=0.01, degree=5, max_segments=0, sparse=False),
     "c5": dict(workload="BERT-large-sized 340M-element gradient, top-r 0.1%, bloom-filter P2 (eps=1e-3) + "
-                        "piecewise curve-fit (8 pieces), 16 independent 21.25M buckets pipelined on 8 streams",
+                        "piecewise curve-fit (8 pieces), 16 independent 21.25M buckets, one codec context and stream each",
                d=340_000_000, ratio=0.001, index=6, value=1, fpr=0.001, degree=5, max_segments=8, sparse=False,
                buckets=16),
 }
