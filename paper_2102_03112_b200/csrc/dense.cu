@@ -114,7 +114,8 @@ __device__ __forceinline__ void nz_load(const float* __restrict__ g, uint64_t d,
 // the 126 MB L2 — and stores each tile at its known offset.  Measured
 // against the one-pass form with a decoupled look-back (round 2): that kernel
 // spent ~2/3 of its warp samples parked at the barrier behind warp 0's
-// look-back walk (ncu: 4367 of ~7000 samples "barrier"), C3 0.294 -> 0.276 ms.
+// look-back walk (ncu: 4367 of ~7000 samples "barrier"); C3 index stage
+// 0.109 -> 0.077 ms, step 0.290 -> 0.251 ms (with the later PDL launches).
 __global__ void __launch_bounds__(kNzBlock) nz_count(const float* __restrict__ g, uint64_t d, uint64_t r, Plan* plan,
                                                      uint64_t* tiles, uint32_t* ticket, uint32_t* gate,
                                                      const uint32_t* status) {
